@@ -1,0 +1,181 @@
+"""CPU oracle for the signadd hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its
+``cpu_baseline`` leg and ``--impl reference``) may import this package, and
+only as the checker / CPU baseline -- never as the thing measured or shipped.
+The product package ``paper_1402_0532_b200`` does not import it.
+
+It wraps ``liboracle.so`` (``signadd_oracle.c``, a C restatement of the
+reference, op-for-op, file:line cited there) and restates the reference
+twiddle table (``transforms.py:108-146``) in numpy so that the oracle does not
+depend on the product package.
+
+Pinning: ``tests/test_oracle_golden.py`` checks every routine here against
+golden vectors produced by the unmodified reference (``tests/golden/
+make_golden.py``), value-for-value for fp64.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+__all__ = [
+    "build",
+    "twiddle_table",
+    "unit_tone",
+    "mf_complex",
+    "ndft",
+    "nfft",
+    "lag_product_mf",
+    "ambiguity_map",
+]
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with the committed Makefile (gcc only)."""
+    src = os.path.join(_HERE, "signadd_oracle.c")
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
+        subprocess.run(["make", "-s", "-C", _HERE, "liboracle.so"], check=True)
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    build()
+    lib = ctypes.CDLL(_LIB_PATH)
+    p = ctypes.c_void_p
+    i64 = ctypes.c_int64
+    ci = ctypes.c_int
+    for sfx in ("f64", "f32"):
+        getattr(lib, f"or_mf_complex_{sfx}").argtypes = [i64, p, p, p]
+        getattr(lib, f"or_ndft_{sfx}").argtypes = [i64, i64, p, p, p, ci]
+        getattr(lib, f"or_nfft_{sfx}").argtypes = [i64, i64, ci, p, p, p, ci]
+        getattr(lib, f"or_lag_product_mf_{sfx}").argtypes = [i64, p, p, i64, ci, p]
+        getattr(lib, f"or_ambiguity_map_{sfx}").argtypes = [
+            i64, p, p, i64, i64, i64, ctypes.c_double, ci, ci, p, p, ci]
+        for name in ("ndft", "nfft", "lag_product_mf", "ambiguity_map"):
+            getattr(lib, f"or_{name}_{sfx}").restype = ci
+    _lib = lib
+    return lib
+
+
+# --- twiddles: restates transforms.py:108-146 -------------------------------
+
+_QUADRANT = np.array([1.0 + 0.0j, 0.0 - 1.0j, -1.0 + 0.0j, 0.0 + 1.0j])
+_TW_CACHE: dict[int, np.ndarray] = {}
+
+
+def twiddle_table(n: int) -> np.ndarray:
+    """exp(-2j*pi*m/n), m=0..n-1, quadrant entries exact (transforms.py:122-133)."""
+    t = _TW_CACHE.get(n)
+    if t is None:
+        m = np.arange(n)
+        ang = (-2.0 * np.pi) * m / n
+        t = np.cos(ang) + 1j * np.sin(ang)
+        quad, rem = np.divmod(4 * m, n)
+        exact = rem == 0
+        t[exact] = _QUADRANT[quad[exact] % 4]
+        t.setflags(write=False)
+        _TW_CACHE[n] = t
+    return t
+
+
+def unit_tone(k0: int, n: int) -> np.ndarray:
+    """transforms.py:149-152."""
+    return np.conj(twiddle_table(n)[(k0 * np.arange(n)) % n])
+
+
+def _prep(x, dtype):
+    ct = np.complex128 if dtype == "f64" else np.complex64
+    return np.ascontiguousarray(np.asarray(x).astype(ct, copy=False))
+
+
+def _ptr(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _table(n, dtype):
+    t = twiddle_table(n)
+    return np.ascontiguousarray(t if dtype == "f64" else t.astype(np.complex64))
+
+
+def mf_complex(a, b, dtype: str = "f64") -> np.ndarray:
+    lib = _load()
+    a = _prep(a, dtype)
+    b = _prep(b, dtype)
+    a, b = np.broadcast_arrays(a, b)
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    out = np.empty_like(a)
+    getattr(lib, f"or_mf_complex_{dtype}")(a.size, _ptr(a), _ptr(b), _ptr(out))
+    return out
+
+
+def ndft(x, dtype: str = "f64", nthreads: int = 1) -> np.ndarray:
+    """Batched NDFT over the last axis (transforms.py:223-251)."""
+    lib = _load()
+    x = _prep(x, dtype)
+    n = x.shape[-1]
+    y = np.empty_like(x)
+    tw = _table(n, dtype)
+    rc = getattr(lib, f"or_ndft_{dtype}")(x.size // max(n, 1), n, _ptr(x), _ptr(tw), _ptr(y), nthreads)
+    if rc:
+        raise ValueError("oracle ndft: bad size")
+    return y
+
+
+def nfft(x, variant: str = "dit", dtype: str = "f64", nthreads: int = 1) -> np.ndarray:
+    """Batched NL-FFT over the last axis (DIT: transforms.py:254-298; DIF: DESIGN.md)."""
+    lib = _load()
+    x = _prep(x, dtype)
+    n = x.shape[-1]
+    y = np.empty_like(x)
+    tw = _table(n, dtype)
+    v = 1 if variant == "dif" else 0
+    rc = getattr(lib, f"or_nfft_{dtype}")(x.size // max(n, 1), n, v, _ptr(x), _ptr(tw), _ptr(y), nthreads)
+    if rc:
+        raise ValueError("oracle nfft: size must be a power of two >= 2")
+    return y
+
+
+def lag_product_mf(surv, ref, lag: int, n: int | None = None, conj: bool = True,
+                   dtype: str = "f64") -> np.ndarray:
+    """ambiguity.py:146-155 (guards are the caller's; see ambiguity.py:116-131)."""
+    lib = _load()
+    surv = _prep(surv, dtype)
+    ref = _prep(ref, dtype)
+    if n is None:
+        n = surv.size
+    assert surv.size >= n and ref.size >= n - lag and 0 <= lag
+    out = np.empty(n, dtype=surv.dtype)
+    getattr(lib, f"or_lag_product_mf_{dtype}")(n, _ptr(surv), _ptr(ref), lag, int(conj), _ptr(out))
+    return out
+
+
+def ambiguity_map(surv, ref, l0: int, l_count: int, m: int, gain: float = 1.0,
+                  conj: bool = True, doppler: str = "nfft", dtype: str = "f64",
+                  nthreads: int = 1) -> np.ndarray:
+    """Rows l0..l0+l_count-1 of the block-integrated eq12a map."""
+    lib = _load()
+    surv = _prep(surv, dtype)
+    ref = _prep(ref, dtype)
+    ns = surv.size
+    assert ref.size >= ns
+    out = np.empty((l_count, m), dtype=surv.dtype)
+    tw = _table(m, dtype)
+    d = 0 if doppler == "nfft" else 1
+    rc = getattr(lib, f"or_ambiguity_map_{dtype}")(
+        ns, _ptr(surv), _ptr(ref), l0, l_count, m, float(gain), int(conj), d,
+        _ptr(tw), _ptr(out), nthreads)
+    if rc:
+        raise ValueError("oracle ambiguity_map: bad sizes")
+    return out

@@ -1,0 +1,125 @@
+"""Pin the CPU oracle against golden vectors from the unmodified reference.
+
+The golden file is produced by ``tests/golden/make_golden.py`` (reference
+imported read-only); this module needs neither the reference nor a GPU.
+fp64 comparisons are value-exact (``==``; signed zeros may differ, see
+DESIGN.md "value identity").
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle
+
+
+def _eq(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    assert a.shape == b.shape
+    bad = np.flatnonzero(~(a == b))
+    assert bad.size == 0, f"{bad.size} mismatches, first at {bad[:5]}: {a.ravel()[bad[:3]]} vs {b.ravel()[bad[:3]]}"
+
+
+def test_twiddle_hash_pin(golden):
+    # transforms.py:108-146 restated in oracle.twiddle_table; hash-pinned
+    for n, h in zip(golden["tw_sizes"], golden["tw_sha"]):
+        t = oracle.twiddle_table(int(n))
+        assert hashlib.sha256(t.tobytes()).hexdigest() == str(h), n
+    _eq(oracle.twiddle_table(64), golden["tw_64"])
+
+
+def test_mf_complex_golden(golden):
+    _eq(oracle.mf_complex(golden["mf_a"], golden["mf_b"]), golden["mf_out"])
+
+
+def test_mf_complex_known_answers():
+    # test_operator.py:38-41, :162-168
+    out = oracle.mf_complex([1 + 2j, 5 - 4j, 1 + 0j], [3 - 1j, 0j, 1j])
+    _eq(out, [7 + 3j, 0j, 2j])
+    a, b, c = 1 + 0j, 1 + 1j, 1 - 1j
+    lhs = oracle.mf_complex(oracle.mf_complex(a, b), c)
+    rhs = oracle.mf_complex(a, oracle.mf_complex(b, c))
+    assert lhs == 6 + 0j and rhs == 5 + 0j
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 16, 64, 128, 256])
+def test_ndft_golden(golden, n):
+    _eq(oracle.ndft(golden[f"ndft_x_{n}"]), golden[f"ndft_y_{n}"])
+
+
+def test_ndft_tones_and_c1(golden):
+    tones = np.stack([oracle.unit_tone(k, 64) for k in range(64)])
+    _eq(oracle.ndft(tones), golden["ndft_tones_64"])
+    _eq(oracle.ndft(oracle.unit_tone(7, 64)), golden["ndft_tone7_64"])
+    assert int(np.argmax(np.abs(golden["ndft_tone7_64"]))) == 7
+    _eq(oracle.ndft(golden["c1_x"], nthreads=4), golden["c1_y"])
+    _eq(oracle.ndft([1 + 0j, 0j]), golden["ndft_two_point"])
+    _eq(oracle.ndft(golden["x_1024"]), golden["ndft_y_1024"])
+    _eq(oracle.ndft(golden["nfft_edge_x"][:64]), golden["ndft_edge_y"])
+
+
+@pytest.mark.parametrize("n", [2, 4, 8, 16, 32, 64, 128, 256, 512, 2048, 4096])
+def test_nfft_golden(golden, n):
+    _eq(oracle.nfft(golden[f"nfft_x_{n}"]), golden[f"nfft_y_{n}"])
+
+
+def test_nfft_tones_edges_large(golden):
+    tones = np.stack([oracle.unit_tone(k, 64) for k in range(64)])
+    _eq(oracle.nfft(tones), golden["nfft_tones_64"])
+    tones = np.stack([oracle.unit_tone(k, 512) for k in range(0, 512, 37)])
+    _eq(oracle.nfft(tones), golden["nfft_tones_512"])
+    _eq(oracle.nfft(golden["nfft_edge_x"]), golden["nfft_edge_y"])
+    _eq(oracle.nfft(golden["x_1024"]), golden["nfft_y_1024"])
+    r = np.random.default_rng(14020534)
+    x16 = r.standard_normal(65536) + 1j * r.standard_normal(65536)
+    y16 = oracle.nfft(x16)
+    _eq(y16[::257], golden["nfft_65536_sample"])
+    assert hashlib.sha256(y16.tobytes()).hexdigest() == str(golden["nfft_65536_sha"])
+
+
+def test_lag_products_golden(golden):
+    surv, ref = golden["lag_surv"], golden["lag_ref"]
+    for i, l in enumerate(golden["lag_lags"]):
+        _eq(oracle.lag_product_mf(surv, ref, int(l), 64), golden["lag_conj"][i])
+        _eq(oracle.lag_product_mf(surv, ref, int(l), 64, conj=False), golden["lag_noconj"][i])
+    _eq(oracle.lag_product_mf(surv, ref, 5, 40), golden["lag_short_n"])
+
+
+def test_eq12a_golden(golden):
+    surv, ref = golden["lag_surv"], golden["lag_ref"]
+    # T == 1 (m == ns): the block-integrated map IS ambiguity_eq12a
+    _eq(oracle.ambiguity_map(surv, ref, 0, 8, 64, gain=16.0), golden["eq12a_g16"])
+    _eq(oracle.ambiguity_map(surv, ref, 0, 8, 64), golden["eq12a_g1"])
+    _eq(oracle.ambiguity_map(surv, ref, 0, 4, 64, conj=False), golden["eq12a_noconj"])
+    _eq(oracle.ambiguity_map(golden["eq12a_512_surv"], golden["eq12a_512_ref"], 0, 16, 512, gain=4.0,
+                             nthreads=4), golden["eq12a_512"])
+
+
+def test_block_map_golden(golden):
+    rr, s = golden["map_surv"], golden["map_ref"]
+    _eq(oracle.ambiguity_map(rr, s, 0, 40, 64, nthreads=4), golden["map_ns4096_m64"])
+    _eq(oracle.ambiguity_map(rr, s, 100, 8, 64, gain=0.5, doppler="ndft"),
+        golden["map_ns4096_m64_ndft_l100_g05"])
+
+
+# --- DIF convention (no reference: parity unpinned; properties only) ---------
+
+def test_dif_properties():
+    g = np.random.default_rng(7)
+    for _ in range(20):
+        x = g.standard_normal(2) + 1j * g.standard_normal(2)
+        _eq(oracle.nfft(x, "dif"), oracle.ndft(x))  # N=2 equals NDFT
+    assert np.all(oracle.nfft(np.zeros((3, 16), complex), "dif") == 0)
+    viol = [k for k in range(64) if int(np.argmax(np.abs(oracle.nfft(oracle.unit_tone(k, 64), "dif")))) != k]
+    assert viol == []
+
+
+def test_fp32_restatement_close():
+    g = np.random.default_rng(3)
+    x = g.standard_normal((4, 512)) + 1j * g.standard_normal((4, 512))
+    y64 = oracle.nfft(x)
+    y32 = oracle.nfft(x.astype(np.complex64), dtype="f32")
+    err = np.max(np.abs(y32 - y64), axis=1) / np.sum(np.abs(y64), axis=1)
+    assert np.all(err < 1e-4)
