@@ -1,0 +1,511 @@
+"""bench.py -- driver contract benchmark for the B200 ⊙ hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload ndft|nlfft|map|map5]
+                    [--impl ours|reference] [--dtype c64|c128] [--no-extras]
+
+Headline (N=1): BASELINE.json configs[1] = C2, batched NDFT N=1024 x 65536
+vectors, complex64, fast (regrouped) mode.  One step = one pass of the NDFT over
+the whole batch (512 MiB in, 512 MiB out: larger than the 126 MB L2, so no flush
+is needed between steps).  value = complex ⊙-ops/s (reference count B*N^2,
+transforms.py:247) summed over ranks; ms_per_step is the max over ranks.
+
+Extras (N=1, rank 0): C3 NL-FFT 2^16 x 4096 (DIT and DIF) and C4 ⊙ map
+(1024 x 512 from 2^20) with their own rooflines, reported under "workloads".
+
+N>1 (torchrun, one process per GPU, NCCL): NDFT is weak-scaled (each rank its
+own C2 batch, no collective).  --workload map5 runs C5 (4096 x 2048 from 2^22)
+strong-scaled: delay bins sharded contiguously, map gathered to rank 0 with
+NCCL inside the timed region.
+
+--impl reference: the reference's CPU algorithm (oracle/ C port, all host
+threads) on the same workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "complex ⊙-ops/s (NDFT, NL-FFT); range-Doppler cells/s at 1/2/4/8 B200"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(prefix="clk", suffix=".csv")
+            os.close(fd)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "-i", str(self.dev),
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh,
+                stderr=subprocess.DEVNULL)
+            time.sleep(0.25)
+        except Exception as e:  # pragma: no cover
+            log("clock sampler unavailable:", e)
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["sampler_unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        rows = []
+        for line in open(self.path):
+            p = [s.strip() for s in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                rows.append((float(p[1]), float(p[2]), float(p[3]), p[5], p[6], p[7], p[8]))
+            except ValueError:
+                continue
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no_samples"]}
+        maxclk = max(r[1] for r in rows)
+        pmax = max(r[2] for r in rows)
+        load = [r for r in rows if r[2] >= 0.5 * pmax] or rows
+        reasons = set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in load:
+            for nm, v in zip(names, r[3:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(r[0] for r in load), "sm_max_mhz": maxclk,
+                "power_w_max": pmax, "samples": len(rows), "reasons": sorted(reasons)}
+
+
+# --------------------------------------------------------------------------- dist
+def dist_init():
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(ws, v: float) -> float:
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def timed(fn, steps, warmup, ws, sampler=None):
+    """W untimed steps, then K steps between barrier+sync; CUDA events on the
+    launching stream; returns (ms_per_step max over ranks, clocks)."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    barrier(ws)
+    if sampler:
+        sampler.start()
+    torch.cuda.synchronize()
+    barrier(ws)
+    s = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(steps):
+        fn()
+    e1.record(s)
+    torch.cuda.synchronize()
+    barrier(ws)
+    ms = e0.elapsed_time(e1) / steps
+    clocks = sampler.stop() if sampler else None
+    return max_over_ranks(ws, ms), clocks
+
+
+# --------------------------------------------------------------------------- peaks
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "MEASURED_PEAKS.json"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
+
+
+def fma_peak_tflops(dtype: str) -> float:
+    """Measured FMA-pipe peak (FFMA or DFMA) in TFLOP/s, live on this GPU."""
+    import ctypes
+    import torch
+    from paper_1402_0532_b200 import _native
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    blocks = sms * 8
+    sink = torch.zeros(1, dtype=torch.float64, device="cuda")
+    d = _native.SA_C64 if dtype == "c64" else _native.SA_C128
+    iters = 4096 if dtype == "c64" else 1024
+    best = 0.0
+    for _ in range(3):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _native.check(_native.lib().sa_fma_peak(d, iters, _native.ptr(sink), blocks, _native.stream_ptr()))
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) * 1e-3
+        fmas = blocks * 256 * iters * 16 * 8
+        best = max(best, 2 * fmas / t / 1e12)
+    return best
+
+
+# --------------------------------------------------------------------------- workloads
+def complex_dtype(name):
+    import torch
+    return torch.complex64 if name == "c64" else torch.complex128
+
+
+def wl_ndft(args, ws, rank):
+    """C2: batched NDFT N=1024 x 65536."""
+    import torch
+    import paper_1402_0532_b200 as sa
+    from paper_1402_0532_b200.workloads import c2_ndft
+    n, batch = 1024, 65536
+    cdt = complex_dtype(args.dtype)
+    t0 = time.time()
+    xh = torch.from_numpy(c2_ndft(n, batch)).to(cdt)
+    log(f"[rank {rank}] C2 input generated in {time.time() - t0:.1f}s")
+    xd = xh.cuda()
+    yd = torch.empty_like(xd)
+    ops = batch * n * n
+    step = lambda: sa.ndft_batch(xd, out=yd)  # noqa: E731
+    res = {"ops": ops, "step": step, "launches_per_step": 1,
+           "config": {"workload": "C2 batched NDFT (BASELINE.json configs[1])", "n": n,
+                      "batch": batch, "mode": "fast (sign-split regrouped accumulation)",
+                      "dtype": "complex64" if args.dtype == "c64" else "complex128",
+                      "l2_policy": "inputs (512 MiB c64) larger than L2; no flush",
+                      "parallelism": f"dp{ws} (independent vectors, weak scaling)"}}
+    if not args.no_e2e:
+        hin = xh.pin_memory()
+        hout = torch.empty_like(hin).pin_memory()
+        res["e2e_step"] = lambda: sa.ndft_batch(hin, out=hout)
+        res["h2d"] = hin.numel() * hin.element_size()
+        res["d2h"] = hout.numel() * hout.element_size()
+    res["roofline"] = lambda ms: roof_alu(args.dtype, ops * 16 / (ms * 1e-3) / 1e12, args)
+    res["cpu"] = lambda P: cpu_ndft(xh.numpy(), P)
+    res["dtype"] = "f32" if args.dtype == "c64" else "f64"
+    return res
+
+
+def roof_alu(dtype, achieved_tflops, args):
+    peak = fma_peak_tflops(dtype)
+    return {"bound": "fp32_alu" if dtype == "c64" else "fp64_alu", "achieved": round(achieved_tflops, 3),
+            "peak": round(peak, 3), "unit": "TFLOP/s", "frac": round(achieved_tflops / peak, 4),
+            "traffic": None,
+            "peak_source": "measured live: sa_fma_peak FFMA/DFMA microbenchmark (MEASURED_PEAKS.json "
+                           "has no CUDA-core figure)",
+            "algorithmic": "8 FMA (16 flop) per complex ⊙ (sign-split identity)"}
+
+
+def roof_hbm(bytes_per_step, ms):
+    peaks, src = measured_peaks()
+    ach = bytes_per_step / (ms * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None, "peak_source": src}
+
+
+def cpu_ndft(x, P):
+    import oracle
+    rows = min(x.shape[0], max(64, 8 * P))
+    sample = np.ascontiguousarray(x[:rows])
+    t = time.perf_counter()
+    oracle.ndft(sample, dtype="f32" if sample.dtype == np.complex64 else "f64", nthreads=P)
+    dt = time.perf_counter() - t
+    n = x.shape[1]
+    return {"value": rows * n * n / dt, "unit": "⊙/s", "cores": P, "kind": "port",
+            "sample": f"first {rows} of the C2 vectors (N={n}), oracle/signadd_oracle.c or_ndft "
+                      f"(sequential, op-for-op restatement of transforms.py:223-251), {P} threads, "
+                      f"{dt:.2f}s wall"}
+
+
+def wl_nlfft(args, ws, rank, variant="dit", batch=4096, n=1 << 16):
+    """C3: NL-FFT 2^16 x 4096 (inputs synthesised on the GPU, same model as workloads.c3)."""
+    import torch
+    import paper_1402_0532_b200 as sa
+    cdt = complex_dtype(args.dtype)
+    g = torch.Generator(device="cuda").manual_seed(14020534 + rank)
+    re = torch.randn(batch, n, device="cuda", dtype=torch.float64, generator=g)
+    im = torch.randn(batch, n, device="cuda", dtype=torch.float64, generator=g)
+    xd = torch.complex(re, im) * math.sqrt(0.5)
+    del re, im
+    t = torch.arange(n, device="cuda", dtype=torch.float64)
+    k = torch.randint(1, 5, (batch,), device="cuda", generator=g)
+    for j in range(4):
+        a = torch.rand(batch, 1, device="cuda", dtype=torch.float64, generator=g) * 0.9 + 0.1
+        f = torch.rand(batch, 1, device="cuda", dtype=torch.float64, generator=g) * n
+        ph = torch.rand(batch, 1, device="cuda", dtype=torch.float64, generator=g) * 2 * math.pi
+        on = (k > j).to(torch.float64)[:, None]
+        xd += on * a * torch.exp(1j * (2 * math.pi * f * t[None] / n + ph))
+    xd = xd.to(cdt)
+    xd = xd.contiguous()
+    yd = torch.empty_like(xd)
+    ops = batch * n * (int(math.log2(n)) + 1) if variant == "dit" else batch * sa.nfft_dif_complex_ops(n)
+    step = lambda: sa.nfft_batch(xd, out=yd, variant=variant)  # noqa: E731
+    bytes_step = 2 * xd.numel() * xd.element_size()
+    res = {"ops": ops, "step": step, "launches_per_step": 2, "bytes": bytes_step,
+           "config": {"workload": f"C3 NL-FFT {variant.upper()} (BASELINE.json configs[2])", "n": n,
+                      "batch": batch, "dtype": str(cdt).replace("torch.", "")}}
+    res["roofline"] = lambda ms: roof_hbm(bytes_step, ms)
+    return res
+
+
+def wl_map(args, ws, rank, c5=False):
+    """C4 (1 GPU) / C5 (sharded) ⊙ range-Doppler map."""
+    import torch
+    import paper_1402_0532_b200 as sa
+    from paper_1402_0532_b200.workloads import c4_scene, c5_scene
+    sc = c5_scene() if c5 else c4_scene()
+    L, M = (4096, 2048) if c5 else (1024, 512)
+    cdt = complex_dtype(args.dtype)
+    surv = torch.from_numpy(sc.surv).to(cdt).cuda()
+    ref = torch.from_numpy(sc.ref).to(cdt).cuda()
+    ns = surv.numel()
+    rows = L // ws
+    l0 = rank * rows
+    out = torch.empty((rows, M), dtype=cdt, device="cuda")
+    ws_buf = torch.empty(rows * M * out.element_size(), dtype=torch.uint8, device="cuda")
+    full = torch.empty((L, M), dtype=cdt, device="cuda") if (ws > 1 and rank == 0) else None
+
+    def step():
+        sa.ambiguity_map(surv, ref, rows, M, l0=l0, out=out, workspace=ws_buf)
+        if ws > 1:
+            import torch.distributed as dist
+            dist.gather(out, [full[i * rows:(i + 1) * rows] for i in range(ws)] if rank == 0 else None, dst=0)
+
+    z = torch.empty((rows, M), dtype=cdt, device="cuda")
+    from paper_1402_0532_b200 import _native
+
+    def lag_only():
+        _native.check(_native.lib().sa_ambiguity_integrate(
+            _native.SA_C64 if args.dtype == "c64" else _native.SA_C128, _native.ptr(surv), _native.ptr(ref),
+            ns, ns, l0, rows, M, 1, _native.SA_NDFT_FAST, _native.ptr(z), _native.stream_ptr()))
+
+    ops = sa.map_complex_ops(L, ns, M)
+    res = {"ops": ops, "cells": L * M, "step": step, "lag_only": lag_only, "launches_per_step": 2,
+           "config": {"workload": ("C5" if c5 else "C4") + " ⊙ range-Doppler map (BASELINE.json configs["
+                      + ("4" if c5 else "3") + "])", "ns": ns, "delay_bins": L, "doppler_bins": M,
+                      "block_T": ns // M, "doppler": "NL-FFT DIT", "dtype": str(cdt).replace("torch.", ""),
+                      "parallelism": f"delay-bin shards x{ws}" + (", NCCL gather to rank 0" if ws > 1 else "")}}
+    return res
+
+
+# --------------------------------------------------------------------------- main
+def run_ours(args):
+    import torch
+    ws, rank, local = dist_init()
+    import paper_1402_0532_b200 as sa
+    sa.require_native()
+    w = args.workload
+    if w == "ndft":
+        res = wl_ndft(args, ws, rank)
+    elif w == "nlfft":
+        res = wl_nlfft(args, ws, rank)
+    elif w in ("map", "map5"):
+        res = wl_map(args, ws, rank, c5=(w == "map5"))
+    else:
+        raise SystemExit(f"unknown workload {w}")
+    sampler = ClockSampler(local) if rank == 0 else None
+    ms, clocks = timed(res["step"], args.steps, args.warmup, ws, sampler)
+    if w in ("map", "map5"):
+        value = res["cells"] / (ms * 1e-3)
+        unit = "cells/s"
+    else:
+        value = res["ops"] * ws / (ms * 1e-3)
+        unit = "⊙/s"
+    line = {"metric": METRIC, "value": value, "unit": unit, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak" if w in ("ndft", "nlfft") else "strong", "vs_baseline": None,
+            "dtype": res.get("dtype", "f32" if args.dtype == "c64" else "f64"), "data": "synthetic (seeded, SURVEY §8d model)",
+            "config": res["config"], "clocks": clocks,
+            "gpu_launches": res["launches_per_step"] * args.steps}
+    if w in ("map", "map5"):
+        line["ops_per_s"] = res["ops"] / (ms * 1e-3)
+    if rank == 0 and "roofline" in res:
+        line["roofline"] = res["roofline"](ms)
+    if w in ("map", "map5") and rank == 0:
+        lms, _ = timed(res["lag_only"], args.steps, 1, 1)
+        peak = fma_peak_tflops(args.dtype)
+        ach = 16 * res["config"]["ns"] * (res["config"]["delay_bins"] // ws) / (lms * 1e-3) / 1e12
+        line["roofline"] = {"bound": "fp32_alu" if args.dtype == "c64" else "fp64_alu",
+                            "achieved": round(ach, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
+                            "frac": round(ach / peak, 4), "traffic": None, "kernel": "k_lag_integrate_fast",
+                            "kernel_ms": lms, "share_of_step": round(lms / ms, 4) if ws == 1 else None,
+                            "peak_source": "measured live sa_fma_peak"}
+    # e2e through the public API with host buffers
+    if "e2e_step" in res:
+        ems, _ = timed(res["e2e_step"], max(2, args.steps // 2), 1, ws)
+        line["e2e"] = {"value": res["ops"] * ws / (ems * 1e-3), "unit": unit, "ms_per_step": ems,
+                       "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"],
+                       "api": "paper_1402_0532_b200.ndft_batch(pinned host tensor, out=pinned host tensor)"}
+        line["gpu_launches"] += max(2, args.steps // 2)
+    # CPU baseline: rank 0, N=1 only
+    if rank == 0 and ws == 1 and "cpu" in res and not args.no_cpu:
+        P = len(os.sched_getaffinity(0))
+        line["cpu_baseline"] = res["cpu"](P)
+    # extras (N=1)
+    if rank == 0 and ws == 1 and not args.no_extras and w == "ndft":
+        extras = {}
+        for name, fn in (("C3_nlfft_dit", lambda: wl_nlfft(args, ws, rank, "dit")),
+                         ("C3_nlfft_dif", lambda: wl_nlfft(args, ws, rank, "dif")),
+                         ("C4_map", lambda: wl_map(args, ws, rank))):
+            try:
+                r = fn()
+                ems, _ = timed(r["step"], max(3, args.steps // 2), 2, 1)
+                e = {"ms_per_step": ems, "config": r["config"], "ops_per_s": r["ops"] / (ems * 1e-3)}
+                if "cells" in r:
+                    e["cells_per_s"] = r["cells"] / (ems * 1e-3)
+                    lms, _ = timed(r["lag_only"], 5, 1, 1)
+                    peak = fma_peak_tflops(args.dtype)
+                    ach = 16 * r["config"]["ns"] * r["config"]["delay_bins"] / (lms * 1e-3) / 1e12
+                    e["roofline"] = {"bound": "fp32_alu", "achieved": round(ach, 3), "peak": round(peak, 3),
+                                     "unit": "TFLOP/s", "frac": round(ach / peak, 4), "kernel": "k_lag_integrate_fast",
+                                     "kernel_ms": lms, "hbm_gbs_of_step": round(
+                                         (2 * r["config"]["ns"] * 8 + r["cells"] * 8) / (ems * 1e-3) / 1e9, 1)}
+                else:
+                    e["roofline"] = r["roofline"](ems)
+                extras[name] = e
+                del r
+                torch.cuda.empty_cache()
+            except Exception as ex:  # keep the headline line even if an extra fails
+                extras[name] = {"error": repr(ex)}
+        line["workloads"] = extras
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """Reference CPU algorithm (oracle C port, all host threads) on the same workload."""
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    P = len(os.sched_getaffinity(0))
+    w = args.workload
+    if w == "ndft":
+        from paper_1402_0532_b200.workloads import c2_ndft
+        n, rows = 1024, max(64, 4 * P)
+        g = np.random.default_rng(14020532 + 1)
+        x = (g.standard_normal((rows, n)) + 1j * g.standard_normal((rows, n))) / np.sqrt(2)
+        x = x.astype(np.complex64 if args.dtype == "c64" else np.complex128)
+        dts = "f32" if args.dtype == "c64" else "f64"
+        fn = lambda: oracle.ndft(x, dtype=dts, nthreads=P)  # noqa: E731
+        ops = rows * n * n
+        unit = "⊙/s"
+        cfg = {"workload": "C2 batched NDFT (BASELINE.json configs[1])", "n": n, "batch": 65536,
+               "sample_rows_per_step": rows}
+        sample = f"{rows} CN(0,1) vectors of N={n} per step (bounded sample of C2)"
+    elif w == "nlfft":
+        n, rows = 1 << 16, max(8, P)
+        g = np.random.default_rng(1)
+        x = (g.standard_normal((rows, n)) + 1j * g.standard_normal((rows, n))).astype(
+            np.complex64 if args.dtype == "c64" else np.complex128)
+        dts = "f32" if args.dtype == "c64" else "f64"
+        fn = lambda: oracle.nfft(x, "dit", dtype=dts, nthreads=P)  # noqa: E731
+        ops = rows * n * 17
+        unit = "⊙/s"
+        cfg = {"workload": "C3 NL-FFT DIT", "n": n, "batch": 4096, "sample_rows_per_step": rows}
+        sample = f"{rows} vectors of 2^16 per step"
+    else:
+        from paper_1402_0532_b200.workloads import c4_scene, c5_scene
+        sc = c5_scene() if w == "map5" else c4_scene()
+        L, M = (4096, 2048) if w == "map5" else (1024, 512)
+        rows = max(4, P)
+        dts = "f32" if args.dtype == "c64" else "f64"
+        s = sc.surv.astype(np.complex64 if dts == "f32" else np.complex128)
+        r = sc.ref.astype(s.dtype)
+        fn = lambda: oracle.ambiguity_map(s, r, 0, rows, M, dtype=dts, nthreads=P)  # noqa: E731
+        ops = rows * M
+        unit = "cells/s"
+        cfg = {"workload": ("C5" if w == "map5" else "C4") + " ⊙ range-Doppler map", "delay_bins": L,
+               "doppler_bins": M, "sample_rows_per_step": rows}
+        sample = f"{rows} delay rows per step"
+    for _ in range(args.warmup):
+        fn()
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        fn()
+    dt = (time.perf_counter() - t) / args.steps
+    v = ops / dt
+    line = {"metric": METRIC, "impl": "reference", "value": v, "unit": unit, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": dts, "data": "synthetic (seeded)",
+            "config": cfg,
+            "cpu_baseline": {"value": v, "unit": unit, "cores": P, "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="ndft", choices=["ndft", "nlfft", "map", "map5"])
+    ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warning: contract requires >= 3 warm-up steps")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

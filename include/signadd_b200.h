@@ -1,0 +1,129 @@
+/*
+ * signadd_b200.h -- C ABI of the B200 (sm_100a) sign-additive hot path.
+ *
+ * Drop-in boundary for the reference package signadd 0.1.0 (pure Python/numpy;
+ * it has no FFI of its own -- its boundary is its Python call surface, which
+ * paper_1402_0532_b200/ mirrors on top of this ABI via ctypes).  Each entry
+ * point names the reference interface it replaces.
+ *
+ * Conventions
+ *   - extern "C", plain pointers and sizes, no C++ or torch types.
+ *   - Complex data is interleaved {re, im}: dtype SA_C64 = float2 (complex64),
+ *     SA_C128 = double2 (complex128), matching numpy/torch layouts.
+ *   - All data pointers are DEVICE pointers on the current CUDA device, owned
+ *     by the caller.  The library owns only twiddle sets (create/destroy).
+ *   - `stream` is a cudaStream_t passed as void*; every call is stream-ordered,
+ *     performs no host synchronisation and is re-entrant per stream.
+ *   - Return 0 on success, a negative SA_ERR_* on failure; sa_last_error()
+ *     gives a thread-local message.  No exceptions cross the ABI.
+ */
+#ifndef SIGNADD_B200_H
+#define SIGNADD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SA_ABI_VERSION 1
+
+enum sa_dtype { SA_C64 = 0, SA_C128 = 1 };
+
+enum sa_status {
+  SA_OK = 0,
+  SA_ERR_ARG = -1,         /* null pointer / bad enum / negative size        */
+  SA_ERR_CONTRACT = -2,    /* reference ContractError: size, power of two, lag */
+  SA_ERR_DOMAIN = -3,      /* reference DomainError: NaN / Inf operand       */
+  SA_ERR_CUDA = -4,        /* CUDA runtime error                             */
+  SA_ERR_UNSUPPORTED = -5  /* valid request this build does not implement    */
+};
+
+enum sa_ndft_mode {
+  SA_NDFT_FAST = 0,  /* sign-split regrouped accumulation (8 FMA per ⊙)        */
+  SA_NDFT_EXACT = 1  /* per-⊙ rounding, sequential accumulation: value-identical
+                        to transforms.py:223-251                               */
+};
+
+enum sa_nlfft_variant { SA_DIT = 0, SA_DIF = 1 };
+
+enum sa_doppler { SA_DOPPLER_NLFFT = 0, SA_DOPPLER_NDFT = 1 };
+
+/* ABI version (SA_ABI_VERSION). */
+int sa_version(void);
+
+/* Thread-local description of the last failure. */
+const char *sa_last_error(void);
+
+/* Build a device twiddle set from the HOST reference table.
+ * Replaces: TwiddleTable / twiddle_table (transforms.py:108-146); the table
+ * itself (cos/sin of (-2pi)m/n with exact quadrant entries) is computed by the
+ * caller exactly as the reference does and passed in as n interleaved
+ * complex128 values.  For SA_C64 the entries are rounded to nearest float. */
+int sa_twiddle_create(int device, int dtype, int64_t n, const double *host_table, void *stream,
+                      void **handle);
+int sa_twiddle_destroy(void *handle);
+
+/* out[i] = a[i] ⊙ b[i] (complex sign-additive product).
+ * Replaces: mf_complex / _mf_complex_raw (operator.py:128-131,159-176). */
+int sa_mf_complex(int dtype, const void *a, const void *b, void *out, int64_t count, void *stream);
+
+/* Sets *d_flag (device int) to 1 if any component of x is NaN/Inf.
+ * Replaces: _require_finite / _as_samples checks (operator.py:112-115,
+ * transforms.py:161-162) for device-resident inputs. */
+int sa_check_finite(int dtype, const void *x, int64_t count, int *d_flag, void *stream);
+
+/* Batched N-point nonlinear DFT: y[b,k] = sum_m W^(km mod n) ⊙ (gain*x[b,m]).
+ * Replaces: ndft (transforms.py:223-251), batched over `batch` contiguous rows.
+ * gain == 1.0 skips the scaling (as ambiguity.py:176-177).  tw: twiddle set
+ * for n.  x and y must not overlap. */
+int sa_ndft(int dtype, const void *x, void *y, int64_t batch, int64_t n, const void *tw, int mode,
+            double gain, void *stream);
+
+/* Batched N-point nonlinear FFT, n a power of two >= 2.
+ * SA_DIT replaces nfft (transforms.py:254-298), value-identical.
+ * SA_DIF is the decimation-in-frequency convention of DESIGN.md (no reference).
+ * Input scaled by gain first (gain == 1.0: untouched).  x == y is allowed. */
+int sa_nlfft(int dtype, int variant, const void *x, void *y, int64_t batch, int64_t n,
+             const void *tw, double gain, void *stream);
+
+/* One ⊙ lag-product row: out[i] = surv[i] ⊙ conj?(ref[i-lag]), ref[<0] = 0.
+ * Replaces: lag_product_mf (ambiguity.py:146-155) incl. its guards
+ * (ambiguity.py:121-128 -> SA_ERR_CONTRACT). */
+int sa_lag_product_mf(int dtype, const void *surv, const void *ref, int64_t n, int64_t ref_len,
+                      int64_t lag, int conj, void *out, void *stream);
+
+/* Workspace needed by sa_ambiguity_map (may be 0). */
+int sa_ambiguity_workspace_bytes(int dtype, int64_t l_count, int64_t m, int64_t *bytes);
+
+/* Range-Doppler map rows l0..l0+l_count-1 (row-major l_count x m):
+ *   y_l[i] = surv[i] ⊙ conj?(ref[i-l])               (lag_product_mf, n = ns)
+ *   z_l[q] = sum_{t<T} y_l[qT+t],  T = ns/m            (block integration)
+ *   row_l  = NLFFT_m(gain*z_l) or NDFT_m(gain*z_l)      (_surface row, :174-178)
+ * With m == ns (T == 1) this is ambiguity_eq12a (ambiguity.py:197-202) for the
+ * rows requested, value-identical for the NL-FFT Doppler transform.
+ * mode: SA_NDFT_FAST uses the regrouped 8-FMA lag accumulation for T > 1;
+ * SA_NDFT_EXACT rounds every ⊙ (always used when T == 1).
+ * tw: twiddle set for m.  Rows are independent (ambiguity.py:27-28): any row
+ * range may be computed on any device (delay-bin sharding). */
+int sa_ambiguity_map(int dtype, const void *surv, const void *ref, int64_t ns, int64_t ref_len,
+                     int64_t l0, int64_t l_count, int64_t m, double gain, int conj, int doppler,
+                     int mode, const void *tw, void *out, void *workspace, int64_t ws_bytes,
+                     void *stream);
+
+/* Stage 1 of sa_ambiguity_map alone: z (l_count x m) = block sums of the ⊙
+ * lag products (no gain, no Doppler transform).  Same guards and modes. */
+int sa_ambiguity_integrate(int dtype, const void *surv, const void *ref, int64_t ns,
+                           int64_t ref_len, int64_t l0, int64_t l_count, int64_t m, int conj,
+                           int mode, void *z, void *stream);
+
+/* FMA-pipe peak microbenchmark (roofline denominator): `blocks` CTAs x 256
+ * threads each run `iters` iterations of 8 independent FMA chains; writes a
+ * sink value to d_sink (8 bytes).  dtype selects FFMA or DFMA. */
+int sa_fma_peak(int dtype, int64_t iters, void *d_sink, int blocks, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SIGNADD_B200_H */

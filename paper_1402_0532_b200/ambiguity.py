@@ -1,0 +1,248 @@
+"""⊙ range-Doppler maps on the B200 (mirrors ambiguity.py of signadd 0.1.0).
+
+Drop-ins (reference file:line):
+  * ``lag_product_mf``  (ambiguity.py:146-155, guards :116-131)
+  * ``ambiguity_eq12a`` (ambiguity.py:197-202 via _surface :158-187)
+  * ``compute_ambiguity`` for variant "eq12a" (ambiguity.py:224-239)
+  * ``AmbiguitySurface``, ``AmbiguityVariant``, ``SPEED_OF_LIGHT``
+
+Extension: ``ambiguity_map`` -- the block-integrated map of SURVEY §8(d)
+(y_l = lag_product_mf(surv, ref, l, Ns); z_l[q] = Σ_{t<T} y_l[qT+t];
+row_l = NLFFT_M(gain·z_l) or NDFT_M(gain·z_l), T = Ns/M) over any row range,
+device-resident, one stream-ordered call.  With M == Ns it is eq12a.
+
+The exact-arithmetic variants eq11/eq12b/eq12c are not on the north-star path
+("next" row (f)); ``compute_ambiguity`` raises NotImplementedError
+for them rather than computing them on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from enum import Enum
+
+import numpy as np
+
+from . import _native
+from ._device import is_device_tensor, require_cuda, sa_dtype_of, to_device, torch
+from .errors import ContractError, OpCounter, OpCountReport
+from .transforms import ComplexSignal, nfft_complex_ops, ndft_complex_ops
+from .twiddle import device_twiddles
+
+__all__ = ["SPEED_OF_LIGHT", "AmbiguityVariant", "AmbiguitySurface", "lag_product_mf",
+           "ambiguity_eq12a", "compute_ambiguity", "ambiguity_map"]
+
+SPEED_OF_LIGHT = 299_792_458.0
+
+
+class AmbiguityVariant(str, Enum):
+    EQ11 = "eq11"
+    EQ12A = "eq12a"
+    EQ12B = "eq12b"
+    EQ12C = "eq12c"
+
+
+@dataclass(frozen=True)
+class AmbiguitySurface:
+    """L x N complex surface over (range bin l, Doppler bin p) (ambiguity.py:64-113)."""
+
+    values: np.ndarray
+    range_bin_m: float
+    doppler_bin_hz: float
+    variant: AmbiguityVariant
+    sample_rate_hz: float
+    lag_op_counts: OpCountReport = field(default_factory=OpCountReport)
+    transform_op_counts: OpCountReport = field(default_factory=OpCountReport)
+
+    @property
+    def op_counts(self) -> OpCountReport:
+        return self.lag_op_counts + self.transform_op_counts
+
+    @property
+    def l_bins(self) -> int:
+        return self.values.shape[0]
+
+    @property
+    def n(self) -> int:
+        return self.values.shape[1]
+
+    def magnitude(self) -> np.ndarray:
+        return np.abs(self.values)
+
+    def magnitude_db(self, floor_db: float = -300.0) -> np.ndarray:
+        mag = self.magnitude()
+        peak = mag.max()
+        if peak <= 0.0:
+            return np.full(mag.shape, floor_db)
+        with np.errstate(divide="ignore"):
+            db = 20.0 * np.log10(mag / peak)
+        return np.maximum(db, floor_db)
+
+    def range_cut(self, floor_db: float = -300.0):
+        db = self.magnitude_db(floor_db).max(axis=1)
+        ls = np.arange(self.l_bins)
+        return ls, ls * self.range_bin_m / 1000.0, db
+
+    def doppler_cut(self, floor_db: float = -300.0):
+        db = self.magnitude_db(floor_db).max(axis=0)
+        n = self.n
+        p = np.arange(n)
+        freq = np.where(p <= n // 2, p, p - n) * self.doppler_bin_hz
+        order = np.argsort(freq, kind="stable")
+        return freq[order], db[order]
+
+
+def _samples(sig):
+    if isinstance(sig, ComplexSignal):
+        return sig.samples
+    if is_device_tensor(sig):
+        return sig
+    return np.asarray(sig, dtype=complex)
+
+
+def _lag_guards(surv_len: int, ref_len: int, l: int, n: int) -> None:
+    # ambiguity.py:121-128 (+ l > n, where the reference's slice assignment
+    # raises a numpy ValueError; ContractError is a ValueError subclass)
+    if l < 0:
+        raise ContractError(f"lag must be non-negative, got {l}")
+    if l >= ref_len:
+        raise ContractError(f"lag {l} is not below the reference length {ref_len}")
+    if surv_len < n:
+        raise ContractError(f"surveillance signal shorter than n={n}")
+    if ref_len < n - l:
+        raise ContractError(f"reference signal too short for n={n}, lag={l}")
+    if l > n:
+        raise ContractError(f"lag {l} exceeds n={n} (reference slice assignment fails)")
+
+
+def _dev(x, dtype):
+    T = torch()
+    if is_device_tensor(x):
+        t = x.reshape(-1)
+        return (t if t.dtype == dtype else t.to(dtype)).contiguous()
+    return to_device(np.ascontiguousarray(np.asarray(x).reshape(-1)), dtype)
+
+
+def lag_product_mf(s_surv, s_ref, l: int, n: int | None = None, conjugate_ref: bool = True,
+                   counter: OpCounter | None = None):
+    """y[i] = s_surv[i] ⊙ conj(s_ref[i-l]), zero reference for i < l (ambiguity.py:146-155)."""
+    surv = _samples(s_surv)
+    ref = _samples(s_ref)
+    device_io = is_device_tensor(surv) or is_device_tensor(ref)
+    if n is None:
+        n = int(surv.shape[0])
+    _lag_guards(int(surv.shape[0]), int(ref.shape[0]), l, n)
+    require_cuda()
+    T = torch()
+    dt = T.complex128
+    if device_io:
+        dt = T.promote_types(surv.dtype if is_device_tensor(surv) else T.complex128,
+                             ref.dtype if is_device_tensor(ref) else T.complex128)
+    ds = _dev(surv, dt)[:n]
+    dr = _dev(ref, dt)
+    out = T.empty(n, dtype=dt, device="cuda")
+    _native.check(_native.lib().sa_lag_product_mf(
+        sa_dtype_of(out), _native.ptr(ds), _native.ptr(dr), n, dr.numel(), l, int(conjugate_ref),
+        _native.ptr(out), _native.stream_ptr()))
+    if counter is not None:
+        counter.count_complex(n)
+    return out if device_io else out.cpu().numpy()
+
+
+def ambiguity_map(s_surv, s_ref, l_bins: int, m: int, *, l0: int = 0, gain: float = 1.0,
+                  conjugate_ref: bool = True, doppler: str = "nfft", mode: str = "fast",
+                  out=None, workspace=None, dtype=None):
+    """Rows l0..l0+l_bins-1 of the block-integrated ⊙ range-Doppler map.
+
+    Inputs: CUDA tensors (stay on device, no sync) or host arrays (result
+    returned on the host).  Ns = len(s_surv); T = Ns / m must be an integer.
+    """
+    T = torch()
+    surv = _samples(s_surv)
+    ref = _samples(s_ref)
+    device_io = is_device_tensor(surv) or is_device_tensor(ref)
+    if dtype is None:
+        dtype = surv.dtype if is_device_tensor(surv) else T.complex128
+    require_cuda()
+    ds = _dev(surv, dtype)
+    dr = _dev(ref, dtype)
+    ns = ds.numel()
+    if l_bins < 1:
+        raise ContractError("l_bins must be >= 1")
+    if m < 1 or ns % m != 0:
+        raise ContractError(f"map: Ns={ns} must be a positive multiple of m={m}")
+    for l in (l0, l0 + l_bins - 1):
+        _lag_guards(ns, dr.numel(), l, ns)
+    d = sa_dtype_of(ds)
+    if out is None:
+        out = T.empty((l_bins, m), dtype=ds.dtype, device=ds.device)
+    need = ctypes.c_int64()
+    _native.check(_native.lib().sa_ambiguity_workspace_bytes(d, l_bins, m, ctypes.byref(need)))
+    if workspace is None or workspace.numel() * workspace.element_size() < need.value:
+        workspace = T.empty(max(1, need.value), dtype=T.uint8, device=ds.device)
+    dop = {"nfft": _native.SA_DOPPLER_NLFFT, "ndft": _native.SA_DOPPLER_NDFT}[doppler]
+    md = {"fast": _native.SA_NDFT_FAST, "exact": _native.SA_NDFT_EXACT}[mode]
+    tw = device_twiddles(m, d, ds.device.index)
+    _native.check(_native.lib().sa_ambiguity_map(
+        d, _native.ptr(ds), _native.ptr(dr), ns, dr.numel(), l0, l_bins, m, float(gain),
+        int(conjugate_ref), dop, md, ctypes.c_void_p(tw), _native.ptr(out), _native.ptr(workspace),
+        workspace.numel() * workspace.element_size(), _native.stream_ptr()))
+    return out if device_io else out.cpu().numpy()
+
+
+def _surface_rate(s_surv, s_ref) -> float:
+    # ambiguity.py:163-170
+    fs = None
+    for sig in (s_surv, s_ref):
+        if isinstance(sig, ComplexSignal):
+            if fs is not None and sig.sample_rate_hz != fs:
+                raise ContractError("surveillance and reference sample rates differ")
+            fs = sig.sample_rate_hz
+    if fs is None:
+        raise ContractError("at least one input must be a ComplexSignal carrying a sample rate")
+    return fs
+
+
+def ambiguity_eq12a(s_surv, s_ref, l_bins: int, n: int, transform_input_gain: float = 1.0,
+                    conjugate_ref: bool = True) -> AmbiguitySurface:
+    """Fully sign-additive surface: ⊙ lag product into the NL-FFT (ambiguity.py:197-202).
+
+    All l_bins rows in one device call; value-identical to the reference.
+    """
+    if l_bins < 1:
+        raise ContractError("l_bins must be >= 1")
+    fs = _surface_rate(s_surv, s_ref)
+    surv = np.asarray(_samples(s_surv), dtype=complex)
+    ref = np.asarray(_samples(s_ref), dtype=complex)
+    for l in (0, l_bins - 1):
+        _lag_guards(surv.size, ref.size, l, n)
+    if n < 2 or (n & (n - 1)) != 0:
+        raise ContractError(f"nfft: size must be a power of two >= 2, got {n}")
+    vals = ambiguity_map(surv[:n], ref, l_bins, n, gain=transform_input_gain,
+                         conjugate_ref=conjugate_ref, doppler="nfft", mode="exact")
+    lag_c = OpCounter()
+    lag_c.count_complex(l_bins * n)
+    tr_c = OpCounter()
+    tr_c.count_complex(l_bins * nfft_complex_ops(n))
+    return AmbiguitySurface(values=vals, range_bin_m=SPEED_OF_LIGHT / fs, doppler_bin_hz=fs / n,
+                            variant=AmbiguityVariant.EQ12A, sample_rate_hz=fs,
+                            lag_op_counts=lag_c.report(), transform_op_counts=tr_c.report())
+
+
+def compute_ambiguity(variant, s_surv, s_ref, l_bins: int, n: int,
+                      transform_input_gain: float = 1.0,
+                      conjugate_ref: bool = True) -> AmbiguitySurface:
+    """Dispatch on variant (ambiguity.py:224-239); eq12a is the B200 path."""
+    variant = AmbiguityVariant(variant)
+    if variant is AmbiguityVariant.EQ12A:
+        return ambiguity_eq12a(s_surv, s_ref, l_bins, n, transform_input_gain, conjugate_ref)
+    raise NotImplementedError(
+        f"variant {variant.value} uses exact multiplication (out of the ⊙ hot path; "
+        "see DESIGN.md 'out of scope')")
+
+
+def map_complex_ops(l_bins: int, ns: int, m: int, doppler: str = "nfft") -> int:
+    """Reference ⊙ count of a map: L·Ns lag ⊙ + L·(M(log2M+1) or M²) transform ⊙."""
+    tr = nfft_complex_ops(m) if doppler == "nfft" else ndft_complex_ops(m)
+    return l_bins * ns + l_bins * tr

@@ -1,0 +1,218 @@
+// sa_abi.cu -- the extern "C" boundary (include/signadd_b200.h).
+//
+// Argument validation mirrors the reference contracts so the Python shim can
+// map status codes to the reference exception classes:
+//   SA_ERR_CONTRACT <-> ContractError (transforms.py:166-169; ambiguity.py:121-128)
+//   SA_ERR_DOMAIN   <-> DomainError   (operator.py:112-115; transforms.py:161-162)
+#include <cstdarg>
+#include <cstdio>
+#include <mutex>
+
+#include "sa_common.cuh"
+#include "sa_internal.h"
+
+static thread_local char g_err[512] = "";
+
+void sa_set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+#define SA_REQUIRE(cond, code, ...) \
+  do {                              \
+    if (!(cond)) {                  \
+      sa_set_error(__VA_ARGS__);    \
+      return code;                  \
+    }                               \
+  } while (0)
+
+static bool dtype_ok(int d) { return d == SA_C64 || d == SA_C128; }
+static bool pow2(int64_t n) { return n >= 2 && (n & (n - 1)) == 0; }
+
+static int check_tw(const void *tw, int dtype, int64_t n, bool need_stage) {
+  const SaTwiddles *t = (const SaTwiddles *)tw;
+  SA_REQUIRE(t != nullptr, SA_ERR_ARG, "twiddle handle is null");
+  SA_REQUIRE(t->dtype == dtype, SA_ERR_ARG, "twiddle dtype %d != %d", t->dtype, dtype);
+  SA_REQUIRE(t->n == n, SA_ERR_ARG, "twiddle set is for n=%lld, call needs n=%lld",
+             (long long)t->n, (long long)n);
+  SA_REQUIRE(!need_stage || t->stage != nullptr, SA_ERR_ARG, "twiddle set has no stage table");
+  int dev = -1;
+  cudaGetDevice(&dev);
+  SA_REQUIRE(dev == t->device, SA_ERR_ARG, "twiddle set lives on device %d, current is %d",
+             t->device, dev);
+  return SA_OK;
+}
+
+extern "C" {
+
+int sa_version(void) { return SA_ABI_VERSION; }
+
+const char *sa_last_error(void) { return g_err; }
+
+int sa_twiddle_create(int device, int dtype, int64_t n, const double *host_table, void *stream,
+                      void **handle) {
+  SA_REQUIRE(dtype_ok(dtype), SA_ERR_ARG, "bad dtype %d", dtype);
+  SA_REQUIRE(n >= 1, SA_ERR_CONTRACT, "TwiddleTable: size must be >= 1");
+  SA_REQUIRE(host_table && handle, SA_ERR_ARG, "null pointer");
+  int prev = 0;
+  SA_CUDA_TRY(cudaGetDevice(&prev));
+  SA_CUDA_TRY(cudaSetDevice(device));
+  SaTwiddles *tw = new SaTwiddles{dtype, n, device, nullptr, nullptr, nullptr};
+  int rc = sa_twiddles_build(tw, host_table, (cudaStream_t)stream);
+  cudaSetDevice(prev);
+  if (rc != SA_OK) {
+    cudaFree(tw->raw);
+    cudaFree(tw->quad);
+    cudaFree(tw->stage);
+    delete tw;
+    return rc;
+  }
+  *handle = tw;
+  return SA_OK;
+}
+
+int sa_twiddle_destroy(void *handle) {
+  SaTwiddles *tw = (SaTwiddles *)handle;
+  if (!tw) return SA_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(tw->device);
+  cudaFree(tw->raw);
+  cudaFree(tw->quad);
+  cudaFree(tw->stage);
+  cudaSetDevice(prev);
+  delete tw;
+  return SA_OK;
+}
+
+int sa_mf_complex(int dtype, const void *a, const void *b, void *out, int64_t count,
+                  void *stream) {
+  SA_REQUIRE(dtype_ok(dtype), SA_ERR_ARG, "bad dtype %d", dtype);
+  SA_REQUIRE(count >= 0, SA_ERR_ARG, "negative count");
+  SA_REQUIRE(count == 0 || (a && b && out), SA_ERR_ARG, "null pointer");
+  return sa_launch_mf_complex(dtype, a, b, out, count, (cudaStream_t)stream);
+}
+
+int sa_check_finite(int dtype, const void *x, int64_t count, int *d_flag, void *stream) {
+  SA_REQUIRE(dtype_ok(dtype), SA_ERR_ARG, "bad dtype %d", dtype);
+  SA_REQUIRE(count >= 0 && d_flag, SA_ERR_ARG, "bad arguments");
+  SA_REQUIRE(count == 0 || x, SA_ERR_ARG, "null pointer");
+  return sa_launch_check_finite(dtype, x, count, d_flag, (cudaStream_t)stream);
+}
+
+int sa_ndft(int dtype, const void *x, void *y, int64_t batch, int64_t n, const void *tw, int mode,
+            double gain, void *stream) {
+  SA_REQUIRE(dtype_ok(dtype), SA_ERR_ARG, "bad dtype %d", dtype);
+  SA_REQUIRE(n >= 1, SA_ERR_CONTRACT, "transform input must be a 1-d sequence of length >= 1");
+  SA_REQUIRE(batch >= 0, SA_ERR_ARG, "negative batch");
+  SA_REQUIRE(mode == SA_NDFT_FAST || mode == SA_NDFT_EXACT, SA_ERR_ARG, "bad mode %d", mode);
+  SA_REQUIRE(batch == 0 || (x && y), SA_ERR_ARG, "null pointer");
+  SA_REQUIRE(x != y || batch == 0, SA_ERR_ARG, "sa_ndft: x and y must not overlap");
+  int rc = check_tw(tw, dtype, n, false);
+  if (rc) return rc;
+  return sa_launch_ndft(dtype, x, y, batch, n, (const SaTwiddles *)tw, mode, gain,
+                        (cudaStream_t)stream);
+}
+
+int sa_nlfft(int dtype, int variant, const void *x, void *y, int64_t batch, int64_t n,
+             const void *tw, double gain, void *stream) {
+  SA_REQUIRE(dtype_ok(dtype), SA_ERR_ARG, "bad dtype %d", dtype);
+  SA_REQUIRE(variant == SA_DIT || variant == SA_DIF, SA_ERR_ARG, "bad variant %d", variant);
+  SA_REQUIRE(pow2(n), SA_ERR_CONTRACT, "nfft: size must be a power of two >= 2, got %lld",
+             (long long)n);
+  SA_REQUIRE(batch >= 0, SA_ERR_ARG, "negative batch");
+  SA_REQUIRE(batch == 0 || (x && y), SA_ERR_ARG, "null pointer");
+  int rc = check_tw(tw, dtype, n, true);
+  if (rc) return rc;
+  return sa_launch_nlfft(dtype, variant, x, y, batch, n, (const SaTwiddles *)tw, gain,
+                         (cudaStream_t)stream);
+}
+
+// ambiguity.py:116-131 guards
+static int lag_guards(int64_t n, int64_t surv_len, int64_t ref_len, int64_t lag) {
+  SA_REQUIRE(lag >= 0, SA_ERR_CONTRACT, "lag must be non-negative, got %lld", (long long)lag);
+  SA_REQUIRE(lag < ref_len, SA_ERR_CONTRACT, "lag %lld is not below the reference length %lld",
+             (long long)lag, (long long)ref_len);
+  SA_REQUIRE(surv_len >= n, SA_ERR_CONTRACT, "surveillance signal shorter than n=%lld",
+             (long long)n);
+  SA_REQUIRE(ref_len >= n - lag, SA_ERR_CONTRACT, "reference signal too short for n=%lld, lag=%lld",
+             (long long)n, (long long)lag);
+  return SA_OK;
+}
+
+int sa_lag_product_mf(int dtype, const void *surv, const void *ref, int64_t n, int64_t ref_len,
+                      int64_t lag, int conj, void *out, void *stream) {
+  SA_REQUIRE(dtype_ok(dtype), SA_ERR_ARG, "bad dtype %d", dtype);
+  SA_REQUIRE(n >= 0, SA_ERR_ARG, "negative n");
+  int rc = lag_guards(n, n, ref_len, lag);
+  if (rc) return rc;
+  SA_REQUIRE(n == 0 || (surv && ref && out), SA_ERR_ARG, "null pointer");
+  return sa_launch_lag_product(dtype, surv, ref, n, ref_len, lag, conj, out, (cudaStream_t)stream);
+}
+
+int sa_ambiguity_workspace_bytes(int dtype, int64_t l_count, int64_t m, int64_t *bytes) {
+  SA_REQUIRE(dtype_ok(dtype) && bytes && l_count >= 0 && m >= 1, SA_ERR_ARG, "bad arguments");
+  *bytes = sa_ambiguity_ws_bytes(dtype, l_count, m);
+  return SA_OK;
+}
+
+int sa_ambiguity_map(int dtype, const void *surv, const void *ref, int64_t ns, int64_t ref_len,
+                     int64_t l0, int64_t l_count, int64_t m, double gain, int conj, int doppler,
+                     int mode, const void *tw, void *out, void *workspace, int64_t ws_bytes,
+                     void *stream) {
+  SA_REQUIRE(dtype_ok(dtype), SA_ERR_ARG, "bad dtype %d", dtype);
+  SA_REQUIRE(l_count >= 1, SA_ERR_CONTRACT, "l_bins must be >= 1");
+  SA_REQUIRE(m >= 1 && ns >= m && ns % m == 0, SA_ERR_CONTRACT,
+             "map: ns=%lld must be a positive multiple of m=%lld", (long long)ns, (long long)m);
+  SA_REQUIRE(doppler == SA_DOPPLER_NLFFT || doppler == SA_DOPPLER_NDFT, SA_ERR_ARG,
+             "bad doppler %d", doppler);
+  SA_REQUIRE(doppler == SA_DOPPLER_NDFT || pow2(m), SA_ERR_CONTRACT,
+             "nfft: size must be a power of two >= 2, got %lld", (long long)m);
+  SA_REQUIRE(mode == SA_NDFT_FAST || mode == SA_NDFT_EXACT, SA_ERR_ARG, "bad mode %d", mode);
+  // the largest lag must satisfy the lag_product_mf guards for n = ns
+  int rc = lag_guards(ns, ns, ref_len, l0 + l_count - 1);
+  if (rc) return rc;
+  rc = lag_guards(ns, ns, ref_len, l0);
+  if (rc) return rc;
+  SA_REQUIRE(surv && ref && out, SA_ERR_ARG, "null pointer");
+  int64_t need = sa_ambiguity_ws_bytes(dtype, l_count, m);
+  SA_REQUIRE(workspace && ws_bytes >= need, SA_ERR_ARG, "workspace too small: %lld < %lld bytes",
+             (long long)ws_bytes, (long long)need);
+  rc = check_tw(tw, dtype, m, doppler == SA_DOPPLER_NLFFT);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  rc = sa_launch_lag_integrate(dtype, surv, ref, ns, ref_len, l0, l_count, m, conj, mode,
+                               workspace, s);
+  if (rc) return rc;
+  if (doppler == SA_DOPPLER_NLFFT)
+    return sa_launch_nlfft(dtype, SA_DIT, workspace, out, l_count, m, (const SaTwiddles *)tw, gain,
+                           s);
+  return sa_launch_ndft(dtype, workspace, out, l_count, m, (const SaTwiddles *)tw,
+                        ns == m ? SA_NDFT_EXACT : mode, gain, s);
+}
+
+int sa_ambiguity_integrate(int dtype, const void *surv, const void *ref, int64_t ns,
+                           int64_t ref_len, int64_t l0, int64_t l_count, int64_t m, int conj,
+                           int mode, void *z, void *stream) {
+  SA_REQUIRE(dtype_ok(dtype), SA_ERR_ARG, "bad dtype %d", dtype);
+  SA_REQUIRE(l_count >= 1, SA_ERR_CONTRACT, "l_bins must be >= 1");
+  SA_REQUIRE(m >= 1 && ns >= m && ns % m == 0, SA_ERR_CONTRACT,
+             "map: ns=%lld must be a positive multiple of m=%lld", (long long)ns, (long long)m);
+  SA_REQUIRE(mode == SA_NDFT_FAST || mode == SA_NDFT_EXACT, SA_ERR_ARG, "bad mode %d", mode);
+  int rc = lag_guards(ns, ns, ref_len, l0 + l_count - 1);
+  if (rc) return rc;
+  rc = lag_guards(ns, ns, ref_len, l0);
+  if (rc) return rc;
+  SA_REQUIRE(surv && ref && z, SA_ERR_ARG, "null pointer");
+  return sa_launch_lag_integrate(dtype, surv, ref, ns, ref_len, l0, l_count, m, conj, mode, z,
+                                 (cudaStream_t)stream);
+}
+
+int sa_fma_peak(int dtype, int64_t iters, void *d_sink, int blocks, void *stream) {
+  SA_REQUIRE(dtype_ok(dtype) && d_sink && iters > 0 && blocks > 0, SA_ERR_ARG, "bad arguments");
+  return sa_launch_fma_peak(dtype, iters, d_sink, blocks, (cudaStream_t)stream);
+}
+
+}  // extern "C"

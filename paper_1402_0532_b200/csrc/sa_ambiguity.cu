@@ -1,0 +1,232 @@
+// sa_ambiguity.cu -- ⊙ lag products and their block integration for the
+// range-Doppler map (ambiguity.py:116-187; SURVEY §8(d) map composition).
+//
+//   y_l[i] = surv[i] ⊙ conj(ref[i-l])   (ref[<0] = 0, ambiguity.py:129-131,151)
+//   z_l[q] = Σ_{t<T} y_l[qT + t]         (T = ns/m; T == 1 is ambiguity_eq12a)
+//
+// The Doppler transform of gain*z_l is sa_nlfft / sa_ndft (sa_abi.cu).
+//
+// FAST lag kernel (T % 8 == 0): ALU-bound correlation tiling (SURVEY §7 hard
+// part 5).  One CTA = one integration block q x 64 lags (8 warps x 8 lags).
+// The block's T surveillance samples and the T+63 reference samples it can see
+// are staged once in smem as {re, im, sgn re, sgn im} (conjugation folded in).
+// Each lane walks sub-blocks of 8 samples and holds 8 samples x 8 lags in
+// registers: 8 + 15 smem loads feed 64 ⊙ = 512 FMAs (regrouped identity
+// a⊗b = sgn(b)a + sgn(a)b, 8 FMA per ⊙).  Samples with i < l read zeros, which
+// contribute exactly 0, so the causal edge needs no branch.  Per-lag partial
+// sums are reduced across the warp with shuffles.
+#include <algorithm>
+
+#include "sa_common.cuh"
+#include "sa_internal.h"
+
+namespace {
+
+template <typename T> using C2 = typename SaVec<T>::c2;
+template <typename T> using C4 = typename SaVec<T>::c4;
+
+constexpr int LAG_WARPS = 8;
+constexpr int LAGS_PER_WARP = 8;
+constexpr int LAGS_PER_CTA = LAG_WARPS * LAGS_PER_WARP;  // 64
+
+__host__ __device__ __forceinline__ int pad8(int s) { return s + (s >> 3); }  // one 16B/32B pad per 8 entries
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_lag_product(const C2<T> *__restrict__ surv,
+                                                     const C2<T> *__restrict__ ref, int64_t n,
+                                                     int64_t lag, bool conj,
+                                                     C2<T> *__restrict__ out) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    C2<T> a = surv[i];
+    T cr = T(0), ci = T(0);
+    if (i >= lag) {
+      C2<T> r = ref[i - lag];
+      cr = r.x;
+      ci = conj ? -r.y : r.y;
+    }
+    C2<T> o;
+    sa_mfc_literal<T>(a.x, a.y, cr, ci, o.x, o.y);  // operand order (surv, ref): :152
+    out[i] = o;
+  }
+}
+
+// Exact / generic: one thread per (lag, q); every ⊙ rounded, sequential sum
+// over t from +0 (identical to the oracle's composition; T == 1 -> eq12a rows).
+template <typename T>
+__global__ void __launch_bounds__(256) k_lag_integrate_exact(
+    const C2<T> *__restrict__ surv, const C2<T> *__restrict__ ref, int64_t ref_len, int64_t l0,
+    int64_t l_count, int64_t m, int64_t tb, bool conj, C2<T> *__restrict__ z) {
+  int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= l_count * m) return;
+  int64_t l = l0 + id / m, q = id % m;
+  T sr = T(0), si = T(0);
+  for (int64_t t = 0; t < tb; ++t) {
+    int64_t i = q * tb + t;
+    C2<T> a = surv[i];
+    T cr = T(0), ci = T(0);
+    int64_t j = i - l;
+    if (j >= 0 && j < ref_len) {
+      C2<T> r = ref[j];
+      cr = r.x;
+      ci = conj ? -r.y : r.y;
+    } else if (conj) {
+      ci = -T(0);
+    }
+    T rr, ri;
+    sa_mfc_literal<T>(a.x, a.y, cr, ci, rr, ri);
+    sr = sa_add(sr, rr);
+    si = sa_add(si, ri);
+  }
+  z[id] = {sr, si};
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_lag_integrate_fast(
+    const C2<T> *__restrict__ surv, const C2<T> *__restrict__ ref, int64_t ref_len, int64_t l0,
+    int64_t l_count, int64_t m, int tb, bool conj, C2<T> *__restrict__ z) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int win = tb + LAGS_PER_CTA - 1;
+  C4<T> *ss = reinterpret_cast<C4<T> *>(smem_raw);  // surveillance block, padded
+  C4<T> *rs = ss + pad8(tb) + 1;                     // reference window, padded
+
+  const int64_t q = blockIdx.x;
+  const int64_t lt = l0 + (int64_t)blockIdx.y * LAGS_PER_CTA;  // first lag of the CTA
+  const int64_t i0 = q * tb;
+  const int64_t ws = i0 - lt - (LAGS_PER_CTA - 1);  // global ref index of window slot 0
+
+  for (int s = threadIdx.x; s < tb; s += blockDim.x) {
+    C2<T> a = surv[i0 + s];
+    ss[pad8(s)] = {a.x, a.y, sa_sgn(a.x), sa_sgn(a.y)};
+  }
+  for (int s = threadIdx.x; s < win; s += blockDim.x) {
+    int64_t j = ws + s;
+    T cr = T(0), ci = T(0);
+    if (j >= 0 && j < ref_len) {
+      C2<T> r = ref[j];
+      cr = r.x;
+      ci = conj ? -r.y : r.y;
+    }
+    rs[pad8(s)] = {cr, ci, sa_sgn(cr), sa_sgn(ci)};
+  }
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t lw = lt + warp * LAGS_PER_WARP;  // first lag of this warp
+  if (lw - l0 >= l_count) return;                // whole warp past the last row
+
+  T accr[LAGS_PER_WARP], acci[LAGS_PER_WARP];
+#pragma unroll
+  for (int j = 0; j < LAGS_PER_WARP; ++j) accr[j] = acci[j] = T(0);
+
+  const int nsb = tb >> 3;
+  for (int sb = lane; sb < nsb; sb += 32) {
+    const int t0 = sb * 8;
+    C4<T> a[8], c[15];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = ss[pad8(t0 + i)];
+    // window index of (sample t0+i, lag lw+j) = t0 + 63 - 8*warp - j + i
+    const int base = t0 + (LAGS_PER_CTA - 1) - LAGS_PER_WARP * warp - (LAGS_PER_WARP - 1);
+#pragma unroll
+    for (int u = 0; u < 15; ++u) c[u] = rs[pad8(base + u)];
+#pragma unroll
+    for (int j = 0; j < LAGS_PER_WARP; ++j) {
+      T ar = accr[j], ai = acci[j];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const C4<T> &s = a[i];      // {sr, si, sgn sr, sgn si}
+        const C4<T> &r = c[i - j + 7];  // {cr, ci, sgn cr, sgn ci}
+        ar = sa_fma(r.z, s.x, ar);
+        ar = sa_fma(s.z, r.x, ar);
+        ar = sa_fma(-r.w, s.y, ar);
+        ar = sa_fma(-s.w, r.y, ar);
+        ai = sa_fma(r.z, s.y, ai);
+        ai = sa_fma(s.w, r.x, ai);
+        ai = sa_fma(s.z, r.y, ai);
+        ai = sa_fma(r.w, s.x, ai);
+      }
+      accr[j] = ar;
+      acci[j] = ai;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < LAGS_PER_WARP; ++j) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      accr[j] = sa_add(accr[j], __shfl_xor_sync(0xffffffffu, accr[j], o));
+      acci[j] = sa_add(acci[j], __shfl_xor_sync(0xffffffffu, acci[j], o));
+    }
+  }
+  if (lane < LAGS_PER_WARP) {
+    T vr = accr[0], vi = acci[0];
+#pragma unroll
+    for (int j = 1; j < LAGS_PER_WARP; ++j)
+      if (lane == j) {
+        vr = accr[j];
+        vi = acci[j];
+      }
+    int64_t row = lw + lane - l0;
+    if (row < l_count) z[row * m + q] = {vr, vi};
+  }
+}
+
+template <typename T>
+int launch_integrate(const void *survv, const void *refv, int64_t ns, int64_t ref_len, int64_t l0,
+                     int64_t l_count, int64_t m, int conj, int mode, void *zv, cudaStream_t s) {
+  const C2<T> *surv = (const C2<T> *)survv;
+  const C2<T> *ref = (const C2<T> *)refv;
+  C2<T> *z = (C2<T> *)zv;
+  const int64_t tb = ns / m;
+  if (l_count == 0 || m == 0) return SA_OK;
+  const bool fast = mode == SA_NDFT_FAST && tb % 8 == 0 && tb <= 8192 && m <= 0x7fffffff;
+  if (!fast) {
+    int64_t tot = l_count * m;
+    k_lag_integrate_exact<T><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(
+        surv, ref, ref_len, l0, l_count, m, tb, conj != 0, z);
+    SA_LAUNCH_CHECK();
+    return SA_OK;
+  }
+  const int win = (int)tb + LAGS_PER_CTA - 1;
+  size_t bytes = sizeof(C4<T>) * ((size_t)pad8((int)tb) + 1 + pad8(win) + 1);
+  auto kern = k_lag_integrate_fast<T>;
+  SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  int64_t ltiles = (l_count + LAGS_PER_CTA - 1) / LAGS_PER_CTA;
+  for (int64_t t0 = 0; t0 < ltiles; t0 += 65535) {
+    int64_t nt = std::min<int64_t>(65535, ltiles - t0);
+    dim3 grid((unsigned)m, (unsigned)nt);
+    kern<<<grid, 256, bytes, s>>>(surv, ref, ref_len, l0 + t0 * LAGS_PER_CTA,
+                                  l_count - t0 * LAGS_PER_CTA, m, (int)tb, conj != 0,
+                                  z + t0 * LAGS_PER_CTA * m);
+  }
+  SA_LAUNCH_CHECK();
+  return SA_OK;
+}
+
+}  // namespace
+
+int64_t sa_ambiguity_ws_bytes(int dtype, int64_t l_count, int64_t m) {
+  return l_count * m * (dtype == SA_C64 ? (int64_t)sizeof(float2) : (int64_t)sizeof(double2));
+}
+
+int sa_launch_lag_product(int dtype, const void *surv, const void *ref, int64_t n, int64_t ref_len,
+                          int64_t lag, int conj, void *out, cudaStream_t s) {
+  (void)ref_len;
+  if (n == 0) return SA_OK;
+  int g = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  if (dtype == SA_C64)
+    k_lag_product<float><<<g, 256, 0, s>>>((const float2 *)surv, (const float2 *)ref, n, lag,
+                                           conj != 0, (float2 *)out);
+  else
+    k_lag_product<double><<<g, 256, 0, s>>>((const double2 *)surv, (const double2 *)ref, n, lag,
+                                            conj != 0, (double2 *)out);
+  SA_LAUNCH_CHECK();
+  return SA_OK;
+}
+
+int sa_launch_lag_integrate(int dtype, const void *surv, const void *ref, int64_t ns,
+                            int64_t ref_len, int64_t l0, int64_t l_count, int64_t m, int conj,
+                            int mode, void *z, cudaStream_t s) {
+  if (dtype == SA_C64)
+    return launch_integrate<float>(surv, ref, ns, ref_len, l0, l_count, m, conj, mode, z, s);
+  return launch_integrate<double>(surv, ref, ns, ref_len, l0, l_count, m, conj, mode, z, s);
+}

@@ -1,0 +1,66 @@
+// sa_internal.h -- internal launchers shared by the kernel translation units and
+// the C ABI (sa_abi.cu).  Not part of the public interface (see include/).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/signadd_b200.h"
+
+// Device-resident twiddle set for one (device, n, dtype).  Built from the HOST
+// reference table (transforms.py:122-133) -- never from device sincos.
+struct SaTwiddles {
+  int dtype;
+  int64_t n;
+  int device;
+  void *raw;    // n complex entries (c64: round-to-nearest cast of the fp64 table)
+  void *quad;   // n x {wr, wi, sgn wr, sgn wi}                      (NDFT)
+  void *stage;  // (n-1) x {|wr|, |wi|, sgn wr, sgn wi}, stage-packed:
+                //   stage s (1..log2 n) at offset 2^(s-1)-1, entry j = table[j*n/2^s]
+};
+
+void sa_set_error(const char *fmt, ...);
+
+#define SA_CUDA_TRY(expr)                                                       \
+  do {                                                                          \
+    cudaError_t _e = (expr);                                                    \
+    if (_e != cudaSuccess) {                                                    \
+      sa_set_error("%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e),       \
+                   __FILE__, __LINE__);                                         \
+      return SA_ERR_CUDA;                                                       \
+    }                                                                           \
+  } while (0)
+
+#define SA_LAUNCH_CHECK()                                                       \
+  do {                                                                          \
+    cudaError_t _e = cudaGetLastError();                                        \
+    if (_e != cudaSuccess) {                                                    \
+      sa_set_error("kernel launch failed: %s (%s:%d)", cudaGetErrorString(_e),  \
+                   __FILE__, __LINE__);                                         \
+      return SA_ERR_CUDA;                                                       \
+    }                                                                           \
+  } while (0)
+
+// sa_twiddles.cu
+int sa_twiddles_build(SaTwiddles *tw, const double *host_table, cudaStream_t s);
+
+// sa_mf.cu
+int sa_launch_mf_complex(int dtype, const void *a, const void *b, void *out, int64_t count,
+                         cudaStream_t s);
+int sa_launch_check_finite(int dtype, const void *x, int64_t count, int *d_flag, cudaStream_t s);
+int sa_launch_fma_peak(int dtype, int64_t iters, void *d_sink, int blocks, cudaStream_t s);
+
+// sa_ndft.cu
+int sa_launch_ndft(int dtype, const void *x, void *y, int64_t batch, int64_t n,
+                   const SaTwiddles *tw, int mode, double gain, cudaStream_t s);
+
+// sa_nlfft.cu
+int sa_launch_nlfft(int dtype, int variant, const void *x, void *y, int64_t batch, int64_t n,
+                    const SaTwiddles *tw, double gain, cudaStream_t s);
+
+// sa_ambiguity.cu
+int64_t sa_ambiguity_ws_bytes(int dtype, int64_t l_count, int64_t m);
+int sa_launch_lag_product(int dtype, const void *surv, const void *ref, int64_t n, int64_t ref_len,
+                          int64_t lag, int conj, void *out, cudaStream_t s);
+int sa_launch_lag_integrate(int dtype, const void *surv, const void *ref, int64_t ns,
+                            int64_t ref_len, int64_t l0, int64_t l_count, int64_t m, int conj,
+                            int mode, void *z, cudaStream_t s);

@@ -1,0 +1,275 @@
+// sa_ndft.cu -- batched N-point nonlinear DFT (transforms.py:223-251).
+//
+// X[k] = sum_m W^(km mod N) ⊙ x[m].
+//
+// EXACT mode: every ⊙ rounded as operator.py:124-131 and accumulated column by
+// column from +0 in index order (transforms.py:244-246): value-identical to the
+// reference.
+//
+// FAST mode (the batched hot path): with the identity a⊗b = sgn(b)a + sgn(a)b,
+//   Re X[k] = Σ_m  sgn(xr)Wr + sgn(Wr)xr − sgn(xi)Wi − sgn(Wi)xi
+//   Im X[k] = Σ_m  sgn(xr)Wi + sgn(Wi)xr + sgn(xi)Wr + sgn(Wr)xi
+// i.e. 8 FP32/FP64 FMAs per ⊙ into two accumulators (SURVEY §7 hard part 6).
+// Only the rounding of the sum changes (fp64: ~1e-16 relative).
+//
+// FAST kernel layout (CUDA cores; the north star excludes tensor cores):
+//   CTA = 8 warps.  All warps share one tile of BV = 32*TB vectors; warp w owns
+//   TK consecutive bins.  Lane l owns vectors l + 32*i (i < TB).  The twiddle
+//   table {Wr, Wi, sWr, sWi} lives in smem and is read as a warp-wide
+//   broadcast (every lane needs the same W^(km)); vector data {xr, xi, sxr, sxi}
+//   is staged per chunk of NC samples into smem [m][v] (XOR-swizzled, so both
+//   the transposing stores and the inner-loop loads are conflict-free) with a
+//   register prefetch of the next chunk overlapping the FMA loop.
+#include <algorithm>
+
+#include "sa_common.cuh"
+#include "sa_internal.h"
+
+namespace {
+
+template <typename T> using C2 = typename SaVec<T>::c2;
+template <typename T> using C4 = typename SaVec<T>::c4;
+
+constexpr int NDFT_THREADS = 256;
+constexpr int NDFT_WARPS = NDFT_THREADS / 32;
+constexpr int NC = 16;  // samples per staged chunk
+
+template <typename T> struct NdftCfg;
+template <> struct NdftCfg<float> {
+  static constexpr int TB = 4;  // vectors per lane
+  static constexpr int TK = 8;  // bins per thread
+};
+template <> struct NdftCfg<double> {
+  static constexpr int TB = 2;
+  static constexpr int TK = 8;
+};
+
+SA_HD int swz(int mm, int vv) { return vv ^ ((mm >> 1) & 7); }
+
+template <typename T, bool POW2, bool TW_SMEM>
+__global__ void __launch_bounds__(NDFT_THREADS)
+    k_ndft_fast(const C2<T> *__restrict__ x, C2<T> *__restrict__ y, int64_t batch, int n,
+                const C4<T> *__restrict__ quad, T gain, bool use_gain) {
+  constexpr int TB = NdftCfg<T>::TB, TK = NdftCfg<T>::TK;
+  constexpr int BV = 32 * TB;               // vectors per CTA
+  constexpr int BK = NDFT_WARPS * TK;       // bins per CTA
+  constexpr int CHUNK = BV * NC;            // complex samples per chunk
+  constexpr int PER_T = CHUNK / 2 / NDFT_THREADS;  // 2-sample loads per thread
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C4<T> *xs = reinterpret_cast<C4<T> *>(smem_raw);  // [2][NC][BV]
+  C4<T> *tws = xs + 2 * NC * BV;                    // [n] (TW_SMEM)
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t v0 = (int64_t)blockIdx.y * BV;
+  const int kbase = blockIdx.x * BK + warp * TK;
+
+  if (TW_SMEM)
+    for (int i = threadIdx.x; i < n; i += NDFT_THREADS) tws[i] = quad[i];
+
+  // staging map: thread handles sample pairs (mm, mm+1) of vector vv; 8 lanes
+  // cover one vector's NC=16 samples (128 B for c64, coalesced).
+  auto ld_chunk = [&](int m0, C2<T> (&r)[PER_T][2]) {
+#pragma unroll
+    for (int q = 0; q < PER_T; ++q) {
+      int e = threadIdx.x + q * NDFT_THREADS;
+      int vv = e >> 3, mm = (e & 7) * 2;
+      int64_t v = v0 + vv;
+      int m = m0 + mm;
+      C2<T> a = {T(0), T(0)}, b = {T(0), T(0)};
+      if (v < batch) {
+        const C2<T> *row = x + v * n;
+        if (m < n) a = sa_ldg(row + m);
+        if (m + 1 < n) b = sa_ldg(row + m + 1);
+      }
+      r[q][0] = a;
+      r[q][1] = b;
+    }
+  };
+  auto st_chunk = [&](int buf, C2<T> (&r)[PER_T][2]) {
+    C4<T> *dst = xs + buf * NC * BV;
+#pragma unroll
+    for (int q = 0; q < PER_T; ++q) {
+      int e = threadIdx.x + q * NDFT_THREADS;
+      int vv = e >> 3, mm = (e & 7) * 2;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        C2<T> a = r[q][h];
+        if (use_gain) {
+          a.x = sa_mul(gain, a.x);
+          a.y = sa_mul(gain, a.y);
+        }
+        dst[(mm + h) * BV + swz(mm + h, vv)] = {a.x, a.y, sa_sgn(a.x), sa_sgn(a.y)};
+      }
+    }
+  };
+
+  T accr[TK][TB], acci[TK][TB];
+#pragma unroll
+  for (int kk = 0; kk < TK; ++kk)
+#pragma unroll
+    for (int i = 0; i < TB; ++i) accr[kk][i] = acci[kk][i] = T(0);
+
+  int idx[TK];  // (k*m) mod n for the current m
+  int kst[TK];  // k mod n (bins past n are computed but never stored)
+#pragma unroll
+  for (int kk = 0; kk < TK; ++kk) {
+    idx[kk] = 0;
+    kst[kk] = (kbase + kk) % n;
+  }
+
+  const int nchunks = (n + NC - 1) / NC;
+  C2<T> pre[PER_T][2];
+  ld_chunk(0, pre);
+  st_chunk(0, pre);
+  __syncthreads();
+
+  for (int c = 0; c < nchunks; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < nchunks) ld_chunk((c + 1) * NC, pre);
+    const C4<T> *cur = xs + buf * NC * BV;
+    const int mlim = min(NC, n - c * NC);
+#pragma unroll 4
+    for (int mm = 0; mm < mlim; ++mm) {
+      C4<T> d[TB];
+#pragma unroll
+      for (int i = 0; i < TB; ++i) d[i] = cur[mm * BV + swz(mm, lane + 32 * i)];
+#pragma unroll
+      for (int kk = 0; kk < TK; ++kk) {
+        C4<T> w = TW_SMEM ? tws[idx[kk]] : sa_ldg(&quad[idx[kk]]);
+        int nx = idx[kk] + kst[kk];
+        if (POW2) {
+          nx &= n - 1;
+        } else {
+          nx = nx >= n ? nx - n : nx;
+        }
+        idx[kk] = nx;
+#pragma unroll
+        for (int i = 0; i < TB; ++i) {
+          // d = {xr, xi, sgn xr, sgn xi} ; w = {Wr, Wi, sgn Wr, sgn Wi}
+          T ar = accr[kk][i], ai = acci[kk][i];
+          ar = sa_fma(d[i].z, w.x, ar);
+          ar = sa_fma(w.z, d[i].x, ar);
+          ar = sa_fma(-d[i].w, w.y, ar);
+          ar = sa_fma(-w.w, d[i].y, ar);
+          ai = sa_fma(d[i].z, w.y, ai);
+          ai = sa_fma(w.w, d[i].x, ai);
+          ai = sa_fma(d[i].w, w.x, ai);
+          ai = sa_fma(w.z, d[i].y, ai);
+          accr[kk][i] = ar;
+          acci[kk][i] = ai;
+        }
+      }
+    }
+    if (c + 1 < nchunks) st_chunk(buf ^ 1, pre);
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int i = 0; i < TB; ++i) {
+    int64_t v = v0 + lane + 32 * i;
+    if (v >= batch) continue;
+    C2<T> *row = y + v * n;
+#pragma unroll
+    for (int kk = 0; kk < TK; ++kk) {
+      int k = kbase + kk;
+      if (k < n) row[k] = {accr[kk][i], acci[kk][i]};
+    }
+  }
+}
+
+// Exact sequential NDFT: one thread per (vector, bin); x[m] is a warp broadcast.
+template <typename T>
+__global__ void __launch_bounds__(256) k_ndft_exact(const C2<T> *__restrict__ x,
+                                                    C2<T> *__restrict__ y, int n,
+                                                    const C2<T> *__restrict__ raw, T gain,
+                                                    bool use_gain) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t v = blockIdx.y;
+  const C2<T> *row = x + v * n;
+  T accr = T(0), acci = T(0);
+  int idx = 0;
+  const int kk = k < n ? k : 0;
+  for (int m = 0; m < n; ++m) {
+    C2<T> xv = sa_ldg(row + m);
+    if (use_gain) {
+      xv.x = sa_mul(gain, xv.x);
+      xv.y = sa_mul(gain, xv.y);
+    }
+    C2<T> w = sa_ldg(raw + idx);
+    T rr, ri;
+    sa_mfc_literal<T>(w.x, w.y, xv.x, xv.y, rr, ri);  // operand order (W, x): transforms.py:243
+    accr = sa_add(accr, rr);
+    acci = sa_add(acci, ri);
+    idx += kk;
+    if (idx >= n) idx -= n;
+  }
+  if (k < n) y[v * n + k] = {accr, acci};
+}
+
+template <typename T>
+int launch(const void *xv, void *yv, int64_t batch, int64_t n64, const SaTwiddles *tw, int mode,
+           double gain, cudaStream_t s) {
+  const C2<T> *x = (const C2<T> *)xv;
+  C2<T> *y = (C2<T> *)yv;
+  const bool use_gain = gain != 1.0;
+  const T g = (T)gain;
+  if (batch == 0) return SA_OK;
+  if (n64 > (1 << 24)) {
+    sa_set_error("sa_ndft: n=%lld too large", (long long)n64);
+    return SA_ERR_UNSUPPORTED;
+  }
+  const int n = (int)n64;
+  if (mode == SA_NDFT_EXACT) {
+    if (batch > 65535) {
+      // grid.y limit: split into slices
+      for (int64_t b = 0; b < batch; b += 65535) {
+        int64_t nb = std::min<int64_t>(65535, batch - b);
+        dim3 grid((n + 255) / 256, (unsigned)nb);
+        k_ndft_exact<T><<<grid, 256, 0, s>>>(x + b * n, y + b * n, n, (const C2<T> *)tw->raw, g,
+                                             use_gain);
+      }
+    } else {
+      dim3 grid((n + 255) / 256, (unsigned)batch);
+      k_ndft_exact<T><<<grid, 256, 0, s>>>(x, y, n, (const C2<T> *)tw->raw, g, use_gain);
+    }
+    SA_LAUNCH_CHECK();
+    return SA_OK;
+  }
+  constexpr int BV = 32 * NdftCfg<T>::TB;
+  constexpr int BK = NDFT_WARPS * NdftCfg<T>::TK;
+  const bool pow2 = (n & (n - 1)) == 0;
+  const bool tw_smem = (size_t)n * sizeof(C4<T>) <= 64 * 1024;
+  size_t bytes = sizeof(C4<T>) * (2 * NC * BV + (tw_smem ? n : 0));
+  const C4<T> *quad = (const C4<T> *)tw->quad;
+  int64_t vblocks = (batch + BV - 1) / BV;
+  unsigned kblocks = (unsigned)((n + BK - 1) / BK);
+  for (int64_t vb = 0; vb < vblocks; vb += 65535) {
+    int64_t nvb = std::min<int64_t>(65535, vblocks - vb);
+    dim3 grid(kblocks, (unsigned)nvb);
+    const C2<T> *xs = x + vb * BV * n;
+    C2<T> *ys = y + vb * BV * n;
+    int64_t bleft = batch - vb * BV;
+#define SA_NDFT_GO(P2, TS)                                                                  \
+  do {                                                                                      \
+    auto kern = k_ndft_fast<T, P2, TS>;                                                     \
+    SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                     (int)bytes));                                          \
+    kern<<<grid, NDFT_THREADS, bytes, s>>>(xs, ys, bleft, n, quad, g, use_gain);           \
+  } while (0)
+    if (pow2 && tw_smem) SA_NDFT_GO(true, true);
+    else if (pow2) SA_NDFT_GO(true, false);
+    else if (tw_smem) SA_NDFT_GO(false, true);
+    else SA_NDFT_GO(false, false);
+#undef SA_NDFT_GO
+  }
+  SA_LAUNCH_CHECK();
+  return SA_OK;
+}
+
+}  // namespace
+
+int sa_launch_ndft(int dtype, const void *x, void *y, int64_t batch, int64_t n,
+                   const SaTwiddles *tw, int mode, double gain, cudaStream_t s) {
+  if (dtype == SA_C64) return launch<float>(x, y, batch, n, tw, mode, gain, s);
+  return launch<double>(x, y, batch, n, tw, mode, gain, s);
+}

@@ -1,0 +1,86 @@
+"""Multi-GPU ⊙ range-Doppler map: delay-bin sharding + NCCL gather.
+
+One process per GPU (torch.distributed).  Rows are independent
+(ambiguity.py:27-28; test_ambiguity.py:208-217), so rank r computes the
+contiguous delay rows [r*L/G, (r+1)*L/G) with no exchange, and the map's only
+collective is the gather of the row blocks to the root -- a rank's block lands
+at offset r*rows, which is exactly the row-major map.
+
+The host logic (partition, gather layout) is backend-agnostic and covered with
+gloo on CPU (tests/test_sharding_gloo.py); on B200s the backend is NCCL over
+NVLink/NVSwitch.
+"""
+
+from __future__ import annotations
+
+
+def shard_rows(l_bins: int, world: int, rank: int) -> tuple[int, int]:
+    """(first row, row count) of rank's contiguous delay-bin shard.
+
+    Uneven L is allowed: the first L % G ranks get one extra row."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of {world}")
+    base, extra = divmod(l_bins, world)
+    count = base + (1 if rank < extra else 0)
+    first = rank * base + min(rank, extra)
+    return first, count
+
+
+def gather_rows(local, full, l_bins: int, group=None, dst: int = 0):
+    """Gather every rank's row block into ``full`` (L x M) on ``dst``.
+
+    Uses ``dist.gather`` when all shards have equal size (one collective),
+    else point-to-point sends/recvs of the uneven blocks."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    sizes = [shard_rows(l_bins, world, r)[1] for r in range(world)]
+    if len(set(sizes)) == 1:
+        if rank == dst:
+            parts = [full[shard_rows(l_bins, world, r)[0]:][: sizes[r]] for r in range(world)]
+            dist.gather(local, parts, dst=dst, group=group)
+        else:
+            dist.gather(local, None, dst=dst, group=group)
+        return full if rank == dst else None
+    if rank == dst:
+        for r in range(world):
+            f, c = shard_rows(l_bins, world, r)
+            if r == dst:
+                full[f:f + c].copy_(local)
+            elif c:
+                dist.recv(full[f:f + c], src=r, group=group)
+        return full
+    if local.shape[0]:
+        dist.send(local, dst=dst, group=group)
+    return None
+
+
+def ambiguity_map_sharded(surv, ref, l_bins: int, m: int, *, gain: float = 1.0,
+                          conjugate_ref: bool = True, doppler: str = "nfft", mode: str = "fast",
+                          group=None, dst: int = 0, out_full=None, out_local=None, workspace=None):
+    """Compute this rank's delay rows on its GPU and gather the map to ``dst``.
+
+    surv/ref: full CUDA tensors on every rank (broadcast beforehand if needed).
+    Returns the (L x M) map on ``dst``, None elsewhere."""
+    import torch
+    import torch.distributed as dist
+    from .ambiguity import ambiguity_map
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    first, count = shard_rows(l_bins, world, rank)
+    if out_local is None:
+        out_local = torch.empty((count, m), dtype=surv.dtype, device=surv.device)
+    if count:
+        ambiguity_map(surv, ref, count, m, l0=first, gain=gain, conjugate_ref=conjugate_ref,
+                      doppler=doppler, mode=mode, out=out_local, workspace=workspace)
+    if rank == dst and out_full is None:
+        out_full = torch.empty((l_bins, m), dtype=surv.dtype, device=surv.device)
+    return gather_rows(out_local, out_full, l_bins, group=group, dst=dst)
+
+
+def broadcast_inputs(surv, ref, src: int = 0, group=None):
+    """ncclBroadcast of the two input streams from ``src``."""
+    import torch.distributed as dist
+    dist.broadcast(surv, src=src, group=group)
+    dist.broadcast(ref, src=src, group=group)
+    return surv, ref

@@ -1,0 +1,303 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle and the
+reference golden vectors.  Mirrors the reference's hot-path tests
+(test_operator.py, test_transforms.py, test_ambiguity.py) plus the batched
+configs of BASELINE.json at oracle-sized subsets and full-size properties.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle
+from parity import TOL_F32, TOL_F64, assert_literal, assert_value_equal, literal, strict
+
+pytestmark = pytest.mark.gpu
+
+
+def T():
+    import torch
+    return torch
+
+
+def dev(a, dt=None):
+    t = T().from_numpy(np.ascontiguousarray(a))
+    if dt is not None:
+        t = t.to(dt)
+    return t.cuda()
+
+
+# --- operator (test_operator.py) ----------------------------------------------
+
+def test_mf_complex_golden_bitwise(sa, golden):
+    out = sa.mf_complex(golden["mf_a"], golden["mf_b"])
+    assert out.tobytes() == golden["mf_out"].tobytes()  # incl. signed zeros
+
+
+def test_mf_complex_examples_and_errors(sa):
+    assert sa.mf_complex(1 + 2j, 3 - 1j) == 7 + 3j
+    assert sa.mf_complex(5 - 4j, 0j) == 0j
+    assert sa.mf_complex(1 + 0j, 1j) == 2j
+    assert sa.mf_real(3, 2) == 5.0 and sa.mf_real(-1.5, 2) == -3.5 and sa.mf_real(7, 0) == 0.0
+    assert sa.mf_sign(-3, 2) == -1 and sa.mf_sign(0, 5) == 0
+    assert sa.vector_product([1, -2, 3], [1, -2, 3]) == 12.0
+    assert np.array_equal(sa.scalar_vector(2, [1, -1]), [3.0, -3.0])
+    for bad in (float("nan"), float("inf")):
+        with pytest.raises(sa.DomainError):
+            sa.mf_complex(complex(bad, 0), 1 + 1j)
+    a, b, c = 1 + 0j, 1 + 1j, 1 - 1j
+    assert sa.mf_complex(sa.mf_complex(a, b), c) == 6 and sa.mf_complex(a, sa.mf_complex(b, c)) == 5
+
+
+def test_mf_complex_fp32_device(sa):
+    g = np.random.default_rng(1)
+    a = (g.standard_normal(100001) + 1j * g.standard_normal(100001)).astype(np.complex64)
+    b = (g.standard_normal(100001) + 1j * g.standard_normal(100001)).astype(np.complex64)
+    a[::97] = 0
+    b[5::89] = -0.0
+    out = sa.mf_complex(dev(a), dev(b)).cpu().numpy()
+    assert_value_equal(out, oracle.mf_complex(a, b, dtype="f32"))
+
+
+def test_mf_complex_negation_and_commutativity(sa):
+    g = np.random.default_rng(20240817)
+    a = g.uniform(-10, 10, 1000) + 1j * g.uniform(-10, 10, 1000)
+    b = g.uniform(-10, 10, 1000) + 1j * g.uniform(-10, 10, 1000)
+    assert np.array_equal(sa.mf_complex(-a, b), -sa.mf_complex(a, b))  # test_operator.py:225-229
+    assert np.array_equal(sa.mf_complex(a, b), sa.mf_complex(b, a))
+
+
+# --- NDFT (test_transforms.py) -------------------------------------------------
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 16, 64, 128, 256])
+def test_ndft_dropin_golden(sa, golden, n):
+    s = sa.ndft(golden[f"ndft_x_{n}"])
+    assert_value_equal(s.bins, golden[f"ndft_y_{n}"])
+    assert s.op_counts.complex_mf_ops == n * n and s.transform_kind.value == "ndft"
+
+
+def test_ndft_dropin_known_answers(sa, golden):
+    assert np.array_equal(sa.ndft([1 + 0j, 0j]).bins, [2 + 0j, 2 + 0j])
+    assert np.array_equal(sa.ndft(np.zeros(16, complex)).bins, np.zeros(16))
+    tones = [sa.peak_index(sa.ndft(sa.unit_tone(k, 64))) for k in range(64)]
+    assert tones == list(range(64))
+    assert_value_equal(sa.ndft(golden["x_1024"]).bins, golden["ndft_y_1024"])
+    assert_value_equal(sa.ndft(golden["nfft_edge_x"][:64]).bins, golden["ndft_edge_y"])
+    with pytest.raises(sa.ContractError):
+        sa.ndft(np.ones((2, 2), complex))
+    with pytest.raises(sa.DomainError):
+        sa.ndft([np.nan, 1.0])
+
+
+def test_ndft_batch_c1(sa, golden):
+    from paper_1402_0532_b200.workloads import c1_ndft64
+    x = c1_ndft64(4096)
+    ref = oracle.ndft(x, nthreads=8)
+    # fp64 exact mode: value-identical to the oracle (and hence the reference)
+    assert_value_equal(sa.ndft_batch(dev(x), mode="exact").cpu().numpy(), ref)
+    # fp64 fast mode (regrouped accumulation)
+    y = sa.ndft_batch(dev(x), mode="fast").cpu().numpy()
+    assert_literal(y, ref, TOL_F64)
+    assert int(np.argmax(np.abs(y[0]))) == 7
+    assert abs(y[0, 7] - (162.8437409998975 + 0j)) < 1e-9 * 283.13656515590407
+    # fp32 (complex64 input, compared against the fp64 oracle of the same values)
+    x32 = x.astype(np.complex64)
+    ref32 = oracle.ndft(x32.astype(np.complex128), nthreads=8)
+    y32 = sa.ndft_batch(dev(x32), mode="fast").cpu().numpy()
+    assert_literal(y32, ref32, TOL_F32)
+    assert int(np.argmax(np.abs(y32[0]))) == 7
+    # golden C1 rows
+    assert_literal(sa.ndft_batch(dev(golden["c1_x"])).cpu().numpy(), golden["c1_y"], TOL_F64)
+
+
+@pytest.mark.parametrize("n", [7, 100, 1000, 1024, 2048])
+def test_ndft_batch_sizes(sa, n):
+    g = np.random.default_rng(n)
+    x = g.standard_normal((33, n)) + 1j * g.standard_normal((33, n))
+    x[3] = 0
+    x[4, ::3] = 0
+    ref = oracle.ndft(x, nthreads=8)
+    assert_literal(sa.ndft_batch(dev(x)).cpu().numpy(), ref, TOL_F64)
+    assert_value_equal(sa.ndft_batch(dev(x), mode="exact").cpu().numpy(), ref)
+    y32 = sa.ndft_batch(dev(x.astype(np.complex64))).cpu().numpy()
+    assert_literal(y32, oracle.ndft(x.astype(np.complex64).astype(np.complex128), nthreads=8), TOL_F32)
+
+
+def test_ndft_c2_subset(sa):
+    """C2 (N=1024, 65536 vectors, 10% tones) on the GPU; oracle on every 256th row."""
+    from paper_1402_0532_b200.workloads import c2_ndft
+    x = c2_ndft()
+    rows = np.arange(0, x.shape[0], 256)
+    for dt, cdt, tol in ((T().complex128, np.complex128, TOL_F64), (T().complex64, np.complex64, TOL_F32)):
+        xd = dev(x.astype(cdt))
+        y = sa.ndft_batch(xd)
+        ys = y[T().from_numpy(rows).cuda()].cpu().numpy()
+        ref = oracle.ndft(x[rows].astype(cdt).astype(np.complex128), nthreads=8)
+        e = assert_literal(ys, ref, tol)
+        print(f"C2 {cdt.__name__}: literal max {e.max():.2e}, strict max {strict(ys, ref).max():.2e}")
+        del xd, y
+
+
+def test_ndft_gain(sa):
+    g = np.random.default_rng(5)
+    x = g.standard_normal((4, 64)) + 1j * g.standard_normal((4, 64))
+    ref = oracle.ndft(16.0 * x)
+    assert_value_equal(sa.ndft_batch(dev(x), mode="exact", gain=16.0).cpu().numpy(), ref)
+
+
+# --- NL-FFT (test_transforms.py) ------------------------------------------------
+
+@pytest.mark.parametrize("n", [2, 4, 8, 16, 32, 64, 128, 256, 512, 2048, 4096])
+def test_nfft_dropin_golden(sa, golden, n):
+    s = sa.nfft(golden[f"nfft_x_{n}"])
+    assert_value_equal(s.bins, golden[f"nfft_y_{n}"])
+    assert s.op_counts.complex_mf_ops == n * (int(np.log2(n)) + 1)
+
+
+def test_nfft_dropin_properties(sa, golden):
+    assert np.array_equal(sa.nfft([1 + 0j, 0j]).bins, [2 + 0j, 2 + 0j])
+    assert np.array_equal(sa.nfft(np.zeros(16, complex)).bins, np.zeros(16))
+    assert [sa.peak_index(sa.nfft(sa.unit_tone(k, 64))) for k in range(64)] == list(range(64))
+    tones = np.stack([sa.unit_tone(k, 64) for k in range(64)])
+    assert_value_equal(sa.nfft_batch(dev(tones)).cpu().numpy(), golden["nfft_tones_64"])
+    tones = np.stack([sa.unit_tone(k, 512) for k in range(0, 512, 37)])
+    assert_value_equal(sa.nfft_batch(dev(tones)).cpu().numpy(), golden["nfft_tones_512"])
+    assert_value_equal(sa.nfft(golden["nfft_edge_x"]).bins, golden["nfft_edge_y"])
+    for n in (1, 3, 12, 100):
+        with pytest.raises(sa.ContractError):
+            sa.nfft(np.ones(n, complex))
+    g = np.random.default_rng(61)
+    for _ in range(20):
+        x = g.standard_normal(2) + 1j * g.standard_normal(2)
+        assert np.array_equal(sa.nfft(x).bins, sa.ndft(x).bins)
+
+
+def test_nfft_65536_reference_hash(sa, golden):
+    r = np.random.default_rng(14020534)
+    x = r.standard_normal(65536) + 1j * r.standard_normal(65536)
+    y = sa.nfft(x).bins
+    assert_value_equal(y[::257], golden["nfft_65536_sample"])
+    assert hashlib.sha256(y.tobytes()).hexdigest() == str(golden["nfft_65536_sha"])
+
+
+@pytest.mark.parametrize("variant", ["dit", "dif"])
+@pytest.mark.parametrize("logn", list(range(1, 19)))
+def test_nfft_batch_vs_oracle(sa, variant, logn):
+    n = 1 << logn
+    batch = max(1, min(64, (1 << 18) // n))
+    g = np.random.default_rng(logn)
+    x = g.standard_normal((batch, n)) + 1j * g.standard_normal((batch, n))
+    x[0, ::5] = 0
+    if batch > 1:
+        x[1] = 0
+    # fp64: value-identical to the oracle (= reference for DIT)
+    y = sa.nfft_batch(dev(x), variant=variant).cpu().numpy()
+    assert_value_equal(y, oracle.nfft(x, variant, nthreads=8))
+    # fp32: value-identical to the fp32 restatement, and within 1e-4 of fp64
+    x32 = x.astype(np.complex64)
+    y32 = sa.nfft_batch(dev(x32), variant=variant).cpu().numpy()
+    assert_value_equal(y32, oracle.nfft(x32, variant, dtype="f32", nthreads=8))
+    assert_literal(y32, oracle.nfft(x32.astype(np.complex128), variant, nthreads=8), TOL_F32)
+
+
+def test_nfft_c3_subset(sa):
+    """C3 rows (CN + 1-4 off-grid tones), N=2^16: GPU vs oracle, both variants."""
+    from paper_1402_0532_b200.workloads import c3_nlfft_rows
+    x = c3_nlfft_rows(1 << 16, np.arange(0, 4096, 512))
+    for variant in ("dit", "dif"):
+        y = sa.nfft_batch(dev(x), variant=variant).cpu().numpy()
+        assert_value_equal(y, oracle.nfft(x, variant, nthreads=8))
+        y32 = sa.nfft_batch(dev(x.astype(np.complex64)), variant=variant).cpu().numpy()
+        ref = oracle.nfft(x.astype(np.complex64).astype(np.complex128), variant, nthreads=8)
+        e = assert_literal(y32, ref, TOL_F32)
+        print(f"C3 {variant} fp32: literal max {e.max():.2e}; strict p50 "
+              f"{np.median(strict(y32, ref)):.2e} max {strict(y32, ref).max():.2e}")
+
+
+def test_nfft_gain_and_inplace(sa):
+    g = np.random.default_rng(9)
+    x = g.standard_normal((8, 256)) + 1j * g.standard_normal((8, 256))
+    assert_value_equal(sa.nfft_batch(dev(x), gain=16.0).cpu().numpy(), oracle.nfft(16.0 * x))
+    xd = dev(x)
+    sa.nfft_batch(xd, out=xd)
+    assert_value_equal(xd.cpu().numpy(), oracle.nfft(x))
+
+
+# --- lag products and maps (test_ambiguity.py) -------------------------------------
+
+def test_lag_product_golden(sa, golden):
+    surv, ref = golden["lag_surv"], golden["lag_ref"]
+    for i, l in enumerate(golden["lag_lags"]):
+        assert_value_equal(sa.lag_product_mf(surv, ref, int(l), 64), golden["lag_conj"][i])
+        assert_value_equal(sa.lag_product_mf(surv, ref, int(l), 64, conjugate_ref=False),
+                           golden["lag_noconj"][i])
+    assert_value_equal(sa.lag_product_mf(surv, ref, 5, 40), golden["lag_short_n"])
+    assert np.array_equal(sa.lag_product_mf(np.full(4, 1 + 2j), np.full(4, 3 + 1j), 0), np.full(4, 7 + 3j))
+    with pytest.raises(sa.ContractError):
+        sa.lag_product_mf(np.ones(8, complex), np.ones(8, complex), 8)
+    with pytest.raises(sa.ContractError):
+        sa.lag_product_mf(np.ones(8, complex), np.ones(8, complex), -1)
+    with pytest.raises(sa.ContractError):
+        sa.lag_product_mf(np.ones(4, complex), np.ones(8, complex), 0, n=8)
+
+
+def test_eq12a_golden(sa, golden):
+    fs = 200_000.0
+    S = sa.ComplexSignal
+    surv, ref = S(golden["lag_surv"], fs), S(golden["lag_ref"], fs)
+    a = sa.ambiguity_eq12a(surv, ref, 8, 64, transform_input_gain=16.0)
+    assert_value_equal(a.values, golden["eq12a_g16"])
+    assert a.lag_op_counts.complex_mf_ops == 8 * 64 and a.transform_op_counts.complex_mul_ops == 0
+    assert_value_equal(sa.ambiguity_eq12a(surv, ref, 8, 64).values, golden["eq12a_g1"])
+    assert_value_equal(sa.ambiguity_eq12a(surv, ref, 4, 64, conjugate_ref=False).values,
+                       golden["eq12a_noconj"])
+    s5 = sa.compute_ambiguity("eq12a", S(golden["eq12a_512_surv"], fs), S(golden["eq12a_512_ref"], fs),
+                              16, 512, transform_input_gain=4.0)
+    assert_value_equal(s5.values, golden["eq12a_512"])
+    assert s5.doppler_bin_hz == fs / 512
+    z = sa.ambiguity_eq12a(S(np.zeros(16), fs), S(np.ones(16), fs), 4, 16)
+    assert np.array_equal(z.values, np.zeros((4, 16)))
+
+
+def test_rows_independent_of_order(sa):
+    # test_ambiguity.py:208-217: any row range gives bit-identical rows
+    g = np.random.default_rng(988)
+    surv = g.standard_normal(64) + 1j * g.standard_normal(64)
+    ref = np.exp(2j * np.pi * g.random(64))
+    full = sa.ambiguity_map(surv, ref, 8, 64, gain=16.0, mode="exact")
+    for l in reversed(range(8)):
+        row = sa.ambiguity_map(surv, ref, 1, 64, l0=l, gain=16.0, mode="exact")
+        assert full[l].tobytes() == row[0].tobytes()
+        y = sa.lag_product_mf(surv, ref, l, 64)
+        assert_value_equal(row[0], sa.nfft(16.0 * y).bins)
+
+
+def test_block_map_golden(sa, golden):
+    rr, s = golden["map_surv"], golden["map_ref"]
+    ex = sa.ambiguity_map(rr, s, 40, 64, mode="exact")
+    assert_value_equal(ex, golden["map_ns4096_m64"])  # sequential sums: value-identical
+    fa = sa.ambiguity_map(rr, s, 40, 64, mode="fast")
+    assert_literal(fa, golden["map_ns4096_m64"], TOL_F64)
+    nd = sa.ambiguity_map(rr, s, 8, 64, l0=100, gain=0.5, doppler="ndft", mode="exact")
+    assert_literal(nd, golden["map_ns4096_m64_ndft_l100_g05"], TOL_F64)
+    f32 = sa.ambiguity_map(dev(rr.astype(np.complex64)), dev(s.astype(np.complex64)), 40, 64).cpu().numpy()
+    ref32 = oracle.ambiguity_map(rr.astype(np.complex64), s.astype(np.complex64), 0, 40, 64)
+    assert_literal(f32, ref32, TOL_F32)
+
+
+def test_map_c4_sampled_rows(sa):
+    """C4: 2^20 samples, 1024 delay bins x 512 Doppler bins, c64 on the GPU; the fp64
+    oracle (of the same complex64 inputs) on 16 sampled rows incl. the target rows."""
+    from paper_1402_0532_b200.workloads import c4_scene
+    sc = c4_scene()
+    surv = sc.surv.astype(np.complex64)
+    ref = sc.ref.astype(np.complex64)
+    y = sa.ambiguity_map(dev(surv), dev(ref), 1024, 512).cpu().numpy()
+    rows = sorted(set([0, 1, 511, 1023] + [int(t) for t in sc.delays] + list(range(100, 1000, 97))))
+    for l in rows:
+        ref_row = oracle.ambiguity_map(surv.astype(np.complex128), ref.astype(np.complex128), l, 1, 512)
+        assert_literal(y[l:l + 1], ref_row, TOL_F32)
+    # fp64 path on a few rows
+    y64 = sa.ambiguity_map(dev(sc.surv), dev(sc.ref), 64, 512, l0=sc.delays[0] - 10).cpu().numpy()
+    ref64 = oracle.ambiguity_map(sc.surv, sc.ref, int(sc.delays[0]) - 10, 64, 512, nthreads=8)
+    assert_literal(y64, ref64, TOL_F64)
