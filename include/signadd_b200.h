@@ -118,6 +118,7 @@ int sa_ambiguity_integrate(int dtype, const void *surv, const void *ref, int64_t
                            int mode, void *z, void *stream);
 
 /* FMA-pipe peak microbenchmark (roofline denominator): `blocks` CTAs x 256
+ * (dtype 2 = packed fp32x2 FFMA2)
  * threads each run `iters` iterations of 8 independent FMA chains; writes a
  * sink value to d_sink (8 bytes).  dtype selects FFMA or DFMA. */
 int sa_fma_peak(int dtype, int64_t iters, void *d_sink, int blocks, void *stream);

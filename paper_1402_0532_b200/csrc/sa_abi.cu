@@ -211,7 +211,8 @@ int sa_ambiguity_integrate(int dtype, const void *surv, const void *ref, int64_t
 }
 
 int sa_fma_peak(int dtype, int64_t iters, void *d_sink, int blocks, void *stream) {
-  SA_REQUIRE(dtype_ok(dtype) && d_sink && iters > 0 && blocks > 0, SA_ERR_ARG, "bad arguments");
+  SA_REQUIRE((dtype_ok(dtype) || dtype == 2) && d_sink && iters > 0 && blocks > 0, SA_ERR_ARG,
+             "bad arguments");
   return sa_launch_fma_peak(dtype, iters, d_sink, blocks, (cudaStream_t)stream);
 }
 

@@ -46,7 +46,9 @@ __global__ void __launch_bounds__(256) k_lag_product(const C2<T> *__restrict__ s
       ci = conj ? -r.y : r.y;
     }
     C2<T> o;
-    sa_mfc_literal<T>(a.x, a.y, cr, ci, o.x, o.y);  // operand order (surv, ref): :152
+    T rr, ri;
+    sa_mfc_literal<T>(a.x, a.y, cr, ci, rr, ri);  // operand order (surv, ref): :152
+    sa_np_complex<T>(rr, ri, o.x, o.y);          // rr + 1j*ri (:155)
     out[i] = o;
   }
 }

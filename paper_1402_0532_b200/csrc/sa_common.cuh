@@ -70,6 +70,14 @@ template <typename T> SA_HD void sa_mfc_literal(T ar, T ai, T br, T bi, T &rr, T
   ri = sa_add(sa_mfr_literal(ai, br), sa_mfr_literal(bi, ar));
 }
 
+// numpy assembles results as `rr + 1j * ri` (operator.py:173, ambiguity.py:155):
+// imag = +0 + ri (so -0 becomes +0), real = rr + (0*ri - 0).  Emulated so the
+// elementwise drop-ins are byte-identical, signed zeros included.
+template <typename T> SA_HD void sa_np_complex(T rr, T ri, T &re, T &im) {
+  re = sa_add(rr, sa_sub(sa_mul(T(0), ri), T(0)));
+  im = sa_add(ri, T(0));
+}
+
 // Same value, identity form with precomputed signs (sa = sgn(a) etc.)
 template <typename T> SA_HD T sa_mfr_id(T a, T sa, T b, T sb) { return sa_fma(sa, b, sa_mul(sb, a)); }
 

@@ -57,6 +57,10 @@ int sa_launch_ndft(int dtype, const void *x, void *y, int64_t batch, int64_t n,
 int sa_launch_nlfft(int dtype, int variant, const void *x, void *y, int64_t batch, int64_t n,
                     const SaTwiddles *tw, double gain, cudaStream_t s);
 
+// sa_nlfft64k.cu (fused single-pass N = 2^16; SA_ERR_UNSUPPORTED -> use the generic path)
+int sa_launch_nlfft64k(int dtype, int variant, const void *x, void *y, int64_t batch, int64_t n,
+                       const SaTwiddles *tw, double gain, cudaStream_t s);
+
 // sa_ambiguity.cu
 int64_t sa_ambiguity_ws_bytes(int dtype, int64_t l_count, int64_t m);
 int sa_launch_lag_product(int dtype, const void *surv, const void *ref, int64_t n, int64_t ref_len,

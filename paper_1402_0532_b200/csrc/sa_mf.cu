@@ -14,7 +14,9 @@ __global__ void __launch_bounds__(256) k_mf_complex(const typename SaVec<T>::c2 
     auto x = __ldcs(&a[i]);
     auto y = __ldcs(&b[i]);
     typename SaVec<T>::c2 r;
-    sa_mfc_literal<T>(x.x, x.y, y.x, y.y, r.x, r.y);
+    T rr, ri;
+    sa_mfc_literal<T>(x.x, x.y, y.x, y.y, rr, ri);
+    sa_np_complex<T>(rr, ri, r.x, r.y);
     __stcs(&out[i], r);
   }
 }
@@ -52,6 +54,33 @@ __global__ void __launch_bounds__(256) k_fma_peak(int64_t iters, T mul, T *sink)
   }
   T r = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
   if (r == T(-1.2345)) sink[0] = r;  // never true; keeps the chains live
+}
+
+// packed fp32x2 FMA (sm_100 FFMA2): 8 chains of 2 lanes each
+__global__ void __launch_bounds__(256) k_fma2_peak(int64_t iters, float mul, float *sink) {
+  unsigned long long a[8];
+  float2 m2 = {mul, mul}, c2 = {1e-7f, 1e-7f};
+  unsigned long long mr = *reinterpret_cast<unsigned long long *>(&m2);
+  unsigned long long cr = *reinterpret_cast<unsigned long long *>(&c2);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    float2 v = {float(threadIdx.x + j), float(threadIdx.x + 2 * j)};
+    a[j] = *reinterpret_cast<unsigned long long *>(&v);
+  }
+#pragma unroll 1
+  for (int64_t i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(a[j]) : "l"(mr), "l"(cr));
+  }
+  float r = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    float2 v = *reinterpret_cast<float2 *>(&a[j]);
+    r += v.x + v.y;
+  }
+  if (r == -1.2345f) sink[0] = r;
 }
 
 static int grid_for(int64_t count) {
@@ -92,6 +121,8 @@ int sa_launch_check_finite(int dtype, const void *x, int64_t count, int *d_flag,
 int sa_launch_fma_peak(int dtype, int64_t iters, void *d_sink, int blocks, cudaStream_t s) {
   if (dtype == SA_C64)
     k_fma_peak<float><<<blocks, 256, 0, s>>>(iters, 0.999999f, (float *)d_sink);
+  else if (dtype == 2)
+    k_fma2_peak<<<blocks, 256, 0, s>>>(iters, 0.999999f, (float *)d_sink);
   else
     k_fma_peak<double><<<blocks, 256, 0, s>>>(iters, 0.999999, (double *)d_sink);
   SA_LAUNCH_CHECK();

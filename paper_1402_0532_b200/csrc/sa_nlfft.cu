@@ -272,6 +272,11 @@ int launch(int variant, const void *xv, void *yv, int64_t batch, int64_t n, cons
     SA_LAUNCH_CHECK();
     return SA_OK;
   }
+  {
+    int rc = sa_launch_nlfft64k(sizeof(T) == 4 ? SA_C64 : SA_C128, variant, xv, yv, batch, n, tw,
+                                gain, s);
+    if (rc != SA_ERR_UNSUPPORTED) return rc;
+  }
   if (x == y) {
     sa_set_error("sa_nlfft: n=%lld needs two passes; in-place (x == y) is not supported",
                  (long long)n);

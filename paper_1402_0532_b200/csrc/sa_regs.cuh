@@ -1,0 +1,178 @@
+// sa_regs.cuh -- register-level complex ⊙ arithmetic for the NL-FFT butterflies,
+// and TMA / mbarrier helpers.
+//
+// fp32 values live as packed {re, im} pairs in 64-bit registers and use the
+// sm_100 packed instructions (fma/mul/add.rn.f32x2 -> FFMA2/FMUL2/FADD2).  ptxas
+// folds the scalar broadcasts {w,w}, the pair swap {hi,lo} and the partial
+// negation {t,-t} into operand modifiers, so a full DIT butterfly
+//   t = w ⊙ b ; a' = a + t ; b' = a − t
+// is 6 packed FP instructions + 2 two-instruction signs.  Every lane result is
+// rounded exactly as sa_tw_mul (sa_common.cuh) -- value-identical to the
+// reference (operator.py:124-131, transforms.py:282-295).
+#pragma once
+#include <cuda.h>
+
+#include "sa_common.cuh"
+
+typedef unsigned long long sa_u64;
+
+template <typename T> struct Ar;
+
+template <> struct Ar<float> {
+  using V = sa_u64;
+  using C2 = float2;
+  using C4 = float4;
+  static SA_HD V pack(float lo, float hi) {
+    V r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+  }
+  static SA_HD void unpack(V v, float &lo, float &hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  }
+  static SA_HD V from(C2 c) { return pack(c.x, c.y); }
+  static SA_HD C2 to(V v) {
+    C2 c;
+    unpack(v, c.x, c.y);
+    return c;
+  }
+  static SA_HD V add(V a, V b) {
+    V d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+  }
+  static SA_HD V sub(V a, V b) {
+    V d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+  }
+  static SA_HD V mul(V a, V b) {
+    V d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+  }
+  static SA_HD V fma(V a, V b, V c) {
+    V d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+  }
+  static SA_HD V sgn(V b) {
+    float lo, hi;
+    unpack(b, lo, hi);
+    return pack(sa_sgn(lo), sa_sgn(hi));
+  }
+  static SA_HD V scale(V a, float g) { return mul(pack(g, g), a); }
+  // w ⊙ b with w = {|wr|, |wi|, sgn wr, sgn wi}
+  static SA_HD V twmul(const C4 &w, V b) {
+    V sb = sgn(b);
+    V q1 = fma(sb, pack(w.x, w.x), b);  // {P1, P4}
+    V q2 = fma(sb, pack(w.y, w.y), b);  // {P3, P2}
+    V tq = mul(pack(w.w, -w.w), q2);    // {t·P3, −t·P2}
+    float lo, hi;
+    unpack(tq, lo, hi);
+    return fma(pack(w.z, w.z), q1, pack(hi, lo));  // {sP1 − tP2, sP4 + tP3}
+  }
+  static SA_HD V one_mul(V b) { return add(sgn(b), b); }  // 1 ⊙ b
+  static SA_HD V mj_mul(V b) {                            // (−j) ⊙ b
+    float lo, hi;
+    unpack(add(sgn(b), b), lo, hi);
+    return pack(hi, -lo);
+  }
+};
+
+template <> struct Ar<double> {
+  using V = double2;
+  using C2 = double2;
+  using C4 = double4;
+  static SA_HD V from(C2 c) { return c; }
+  static SA_HD C2 to(V v) { return v; }
+  static SA_HD V add(V a, V b) { return {sa_add(a.x, b.x), sa_add(a.y, b.y)}; }
+  static SA_HD V sub(V a, V b) { return {sa_sub(a.x, b.x), sa_sub(a.y, b.y)}; }
+  static SA_HD V scale(V a, double g) { return {sa_mul(g, a.x), sa_mul(g, a.y)}; }
+  static SA_HD V twmul(const C4 &w, V b) {
+    V r;
+    sa_tw_mul<double>(w.x, w.y, w.z, w.w, b.x, b.y, r.x, r.y);
+    return r;
+  }
+  static SA_HD V one_mul(V b) { return {sa_fma(sa_sgn(b.x), 1.0, b.x), sa_fma(sa_sgn(b.y), 1.0, b.y)}; }
+  static SA_HD V mj_mul(V b) {
+    V u = one_mul(b);
+    return {u.y, -u.x};
+  }
+};
+
+// DIT butterflies on registers
+template <typename T> SA_HD void r_dit(typename Ar<T>::V &a, typename Ar<T>::V &b,
+                                       const typename Ar<T>::C4 &w) {
+  auto t = Ar<T>::twmul(w, b);
+  b = Ar<T>::sub(a, t);
+  a = Ar<T>::add(a, t);
+}
+template <typename T> SA_HD void r_dit_one(typename Ar<T>::V &a, typename Ar<T>::V &b) {
+  auto t = Ar<T>::one_mul(b);
+  b = Ar<T>::sub(a, t);
+  a = Ar<T>::add(a, t);
+}
+template <typename T> SA_HD void r_dit_mj(typename Ar<T>::V &a, typename Ar<T>::V &b) {
+  auto t = Ar<T>::mj_mul(b);
+  b = Ar<T>::sub(a, t);
+  a = Ar<T>::add(a, t);
+}
+// bottom stage: full 2-point NDFT (transforms.py:270-280)
+template <typename T> SA_HD void r_two_point(typename Ar<T>::V &a, typename Ar<T>::V &b) {
+  auto u = Ar<T>::one_mul(a);
+  auto t = Ar<T>::one_mul(b);
+  a = Ar<T>::add(u, t);
+  b = Ar<T>::sub(u, t);
+}
+// DIF butterfly: a' = a + b ; b' = w ⊙ (a − b)
+template <typename T> SA_HD void r_dif(typename Ar<T>::V &a, typename Ar<T>::V &b,
+                                       const typename Ar<T>::C4 &w) {
+  auto d = Ar<T>::sub(a, b);
+  a = Ar<T>::add(a, b);
+  b = Ar<T>::twmul(w, d);
+}
+template <typename T> SA_HD void r_dif_one(typename Ar<T>::V &a, typename Ar<T>::V &b) {
+  auto d = Ar<T>::sub(a, b);
+  a = Ar<T>::add(a, b);
+  b = Ar<T>::one_mul(d);
+}
+template <typename T> SA_HD void r_dif_mj(typename Ar<T>::V &a, typename Ar<T>::V &b) {
+  auto d = Ar<T>::sub(a, b);
+  a = Ar<T>::add(a, b);
+  b = Ar<T>::mj_mul(d);
+}
+
+// ---------------------------------------------------------------------------
+// shared-memory addresses, mbarriers, TMA
+// ---------------------------------------------------------------------------
+SA_HD uint32_t sa_smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+SA_HD void sa_mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa_smem_u32(bar)), "r"(count));
+}
+SA_HD void sa_mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa_smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+SA_HD void sa_mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "SA_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra SA_WAIT_%=;\n}\n" ::"r"(sa_smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+SA_HD void sa_fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+SA_HD void sa_fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// 2-D TMA tile load global -> this CTA's smem, completion on an mbarrier
+SA_HD void sa_tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(sa_smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(sa_smem_u32(bar))
+      : "memory");
+}

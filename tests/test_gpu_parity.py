@@ -301,3 +301,25 @@ def test_map_c4_sampled_rows(sa):
     y64 = sa.ambiguity_map(dev(sc.surv), dev(sc.ref), 64, 512, l0=sc.delays[0] - 10).cpu().numpy()
     ref64 = oracle.ambiguity_map(sc.surv, sc.ref, int(sc.delays[0]) - 10, 64, 512, nthreads=8)
     assert_literal(y64, ref64, TOL_F64)
+
+
+@pytest.mark.parametrize("dt", ["c64", "c128"])
+def test_nfft64k_persistent_loop(sa, dt):
+    """Fused single-pass 2^16 kernel with more signals than resident clusters
+    (exercises the persistent loop, TMA double buffering and the cluster
+    barriers), with gain and in place."""
+    g = np.random.default_rng(164)
+    b = 80
+    x = g.standard_normal((b, 1 << 16)) + 1j * g.standard_normal((b, 1 << 16))
+    x[7] = 0
+    x[9, ::3] = 0
+    cdt = np.complex64 if dt == "c64" else np.complex128
+    xs = x.astype(cdt)
+    od = "f32" if dt == "c64" else "f64"
+    ref = oracle.nfft(2.5 * xs.astype(np.complex128) if dt == "c128" else (np.float32(2.5) * xs), "dit",
+                      dtype=od, nthreads=8)
+    y = sa.nfft_batch(dev(xs), gain=2.5).cpu().numpy()
+    assert_value_equal(y, ref)
+    xd = dev(xs)
+    sa.nfft_batch(xd, out=xd)
+    assert_value_equal(xd.cpu().numpy(), oracle.nfft(xs, "dit", dtype=od, nthreads=8))
