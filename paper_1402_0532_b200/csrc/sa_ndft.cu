@@ -24,6 +24,7 @@
 
 #include "sa_common.cuh"
 #include "sa_internal.h"
+#include "sa_regs.cuh"
 
 namespace {
 
@@ -177,6 +178,148 @@ __global__ void __launch_bounds__(NDFT_THREADS)
   }
 }
 
+
+// fp32 FAST kernel with packed FFMA2: two vectors per 64-bit accumulator pair.
+// Per sample m and bin k a lane issues 8 FFMA2 for its 2 vector pairs (= 16
+// ⊙-accumulate lane-ops of the scalar kernel's 32 FFMA), halving issue slots so
+// the FMA pipe, not instruction issue/dispatch, is the limit.  smem chunk layout
+// per (m, pair p): D0 = {xr_a, xr_b, xi_a, xi_b}, D1 = {sxr_a, sxr_b, sxi_a, sxi_b}.
+template <bool POW2, bool TW_SMEM>
+__global__ void __launch_bounds__(NDFT_THREADS)
+    k_ndft_fast_f32x2(const float2 *__restrict__ x, float2 *__restrict__ y, int64_t batch, int n,
+                      const float4 *__restrict__ quad, float gain, bool use_gain) {
+  using A = Ar<float>;
+  using V = A::V;
+  constexpr int TP = 2;                 // vector pairs per lane
+  constexpr int TK = 8;                 // bins per thread
+  constexpr int BP = 32 * TP;           // pairs per CTA
+  constexpr int BV = 2 * BP;            // vectors per CTA (128)
+  constexpr int BK = NDFT_WARPS * TK;   // bins per CTA (64)
+  constexpr int PER_T = BP * NC / NDFT_THREADS;  // (pair, m) loads per thread per chunk
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float4 *d0 = reinterpret_cast<float4 *>(smem_raw);  // [2][NC][BP]
+  float4 *d1 = d0 + 2 * NC * BP;                       // [2][NC][BP]
+  float4 *tws = d1 + 2 * NC * BP;                      // [n] (TW_SMEM)
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t v0 = (int64_t)blockIdx.y * BV;
+  const int kbase = blockIdx.x * BK + warp * TK;
+  if (TW_SMEM)
+    for (int i = threadIdx.x; i < n; i += NDFT_THREADS) tws[i] = quad[i];
+
+  auto ld_chunk = [&](int m0, float2 (&r)[PER_T][2]) {
+#pragma unroll
+    for (int q = 0; q < PER_T; ++q) {
+      int e = threadIdx.x + q * NDFT_THREADS;
+      int p = e % BP, mm = e / BP;
+      int m = m0 + mm;
+      float2 a = {0.f, 0.f}, b = {0.f, 0.f};
+      int64_t va = v0 + 2 * p;
+      if (m < n) {
+        if (va < batch) a = __ldg(x + va * n + m);
+        if (va + 1 < batch) b = __ldg(x + (va + 1) * n + m);
+      }
+      r[q][0] = a;
+      r[q][1] = b;
+    }
+  };
+  auto st_chunk = [&](int buf, float2 (&r)[PER_T][2]) {
+#pragma unroll
+    for (int q = 0; q < PER_T; ++q) {
+      int e = threadIdx.x + q * NDFT_THREADS;
+      int p = e % BP, mm = e / BP;
+      float2 a = r[q][0], b = r[q][1];
+      if (use_gain) {
+        a = {sa_mul(gain, a.x), sa_mul(gain, a.y)};
+        b = {sa_mul(gain, b.x), sa_mul(gain, b.y)};
+      }
+      d0[(buf * NC + mm) * BP + p] = {a.x, b.x, a.y, b.y};
+      d1[(buf * NC + mm) * BP + p] = {sa_sgn(a.x), sa_sgn(b.x), sa_sgn(a.y), sa_sgn(b.y)};
+    }
+  };
+
+  V accr[TK][TP], acci[TK][TP];
+#pragma unroll
+  for (int kk = 0; kk < TK; ++kk)
+#pragma unroll
+    for (int i = 0; i < TP; ++i) accr[kk][i] = acci[kk][i] = 0ull;
+  int idx[TK], kst[TK];
+#pragma unroll
+  for (int kk = 0; kk < TK; ++kk) {
+    idx[kk] = 0;
+    kst[kk] = (kbase + kk) % n;
+  }
+  const int nchunks = (n + NC - 1) / NC;
+  float2 pre[PER_T][2];
+  ld_chunk(0, pre);
+  st_chunk(0, pre);
+  __syncthreads();
+  for (int c = 0; c < nchunks; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < nchunks) ld_chunk((c + 1) * NC, pre);
+    const float4 *c0 = d0 + buf * NC * BP;
+    const float4 *c1 = d1 + buf * NC * BP;
+    const int mlim = min(NC, n - c * NC);
+#pragma unroll 2
+    for (int mm = 0; mm < mlim; ++mm) {
+      V xr[TP], xi[TP], sr[TP], si[TP];
+#pragma unroll
+      for (int i = 0; i < TP; ++i) {
+        float4 a = c0[mm * BP + lane + 32 * i];
+        float4 b = c1[mm * BP + lane + 32 * i];
+        xr[i] = A::pack(a.x, a.y);
+        xi[i] = A::pack(a.z, a.w);
+        sr[i] = A::pack(b.x, b.y);
+        si[i] = A::pack(b.z, b.w);
+      }
+#pragma unroll
+      for (int kk = 0; kk < TK; ++kk) {
+        float4 w = TW_SMEM ? tws[idx[kk]] : __ldg(&quad[idx[kk]]);
+        int nx = idx[kk] + kst[kk];
+        if (POW2) nx &= n - 1;
+        else nx = nx >= n ? nx - n : nx;
+        idx[kk] = nx;
+        const V wr = A::pack(w.x, w.x), wi = A::pack(w.y, w.y), swr = A::pack(w.z, w.z),
+                swi = A::pack(w.w, w.w), nwi = A::pack(-w.y, -w.y), nswi = A::pack(-w.w, -w.w);
+#pragma unroll
+        for (int i = 0; i < TP; ++i) {
+          // Re += sxr*Wr + sWr*xr - sxi*Wi - sWi*xi ; Im += sxr*Wi + sWi*xr + sxi*Wr + sWr*xi
+          V ar = accr[kk][i], ai = acci[kk][i];
+          ar = A::fma(sr[i], wr, ar);
+          ar = A::fma(swr, xr[i], ar);
+          ar = A::fma(si[i], nwi, ar);
+          ar = A::fma(nswi, xi[i], ar);
+          ai = A::fma(sr[i], wi, ai);
+          ai = A::fma(swi, xr[i], ai);
+          ai = A::fma(si[i], wr, ai);
+          ai = A::fma(swr, xi[i], ai);
+          accr[kk][i] = ar;
+          acci[kk][i] = ai;
+        }
+      }
+    }
+    if (c + 1 < nchunks) st_chunk(buf ^ 1, pre);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < TP; ++i) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      int64_t v = v0 + 2 * (lane + 32 * i) + h;
+      if (v >= batch) continue;
+      float2 *row = y + v * n;
+#pragma unroll
+      for (int kk = 0; kk < TK; ++kk) {
+        int k = kbase + kk;
+        float r0, r1, i0, i1;
+        A::unpack(accr[kk][i], r0, r1);
+        A::unpack(acci[kk][i], i0, i1);
+        if (k < n) row[k] = h ? make_float2(r1, i1) : make_float2(r0, i0);
+      }
+    }
+  }
+}
+
 // Exact sequential NDFT: one thread per (vector, bin); x[m] is a warp broadcast.
 template <typename T>
 __global__ void __launch_bounds__(256) k_ndft_exact(const C2<T> *__restrict__ x,
@@ -240,6 +383,8 @@ int launch(const void *xv, void *yv, int64_t batch, int64_t n64, const SaTwiddle
   const bool pow2 = (n & (n - 1)) == 0;
   const bool tw_smem = (size_t)n * sizeof(C4<T>) <= 64 * 1024;
   size_t bytes = sizeof(C4<T>) * (2 * NC * BV + (tw_smem ? n : 0));
+  // fp32: packed FFMA2 kernel (same tile: 128 vectors x 64 bins, same smem bytes)
+  constexpr bool F32X2 = sizeof(T) == 4;
   const C4<T> *quad = (const C4<T> *)tw->quad;
   int64_t vblocks = (batch + BV - 1) / BV;
   unsigned kblocks = (unsigned)((n + BK - 1) / BK);
@@ -251,10 +396,18 @@ int launch(const void *xv, void *yv, int64_t batch, int64_t n64, const SaTwiddle
     int64_t bleft = batch - vb * BV;
 #define SA_NDFT_GO(P2, TS)                                                                  \
   do {                                                                                      \
-    auto kern = k_ndft_fast<T, P2, TS>;                                                     \
-    SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                                     (int)bytes));                                          \
-    kern<<<grid, NDFT_THREADS, bytes, s>>>(xs, ys, bleft, n, quad, g, use_gain);           \
+    if constexpr (F32X2) {                                                                  \
+      auto kern = k_ndft_fast_f32x2<P2, TS>;                                                \
+      SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                       (int)bytes));                                        \
+      kern<<<grid, NDFT_THREADS, bytes, s>>>((const float2 *)xs, (float2 *)ys, bleft, n,    \
+                                             (const float4 *)quad, (float)g, use_gain);     \
+    } else {                                                                                \
+      auto kern = k_ndft_fast<T, P2, TS>;                                                   \
+      SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                       (int)bytes));                                        \
+      kern<<<grid, NDFT_THREADS, bytes, s>>>(xs, ys, bleft, n, quad, g, use_gain);         \
+    }                                                                                       \
   } while (0)
     if (pow2 && tw_smem) SA_NDFT_GO(true, true);
     else if (pow2) SA_NDFT_GO(true, false);

@@ -50,7 +50,7 @@ template <typename T> struct L64 {
   static constexpr size_t INTER = sizeof(C2) * 256 * COLS;
   static constexpr size_t WORK = sizeof(C2) * 256 * TC;
   static constexpr size_t TWA = sizeof(C4) * 255;
-  static constexpr size_t SMEM = INTER + 2 * WORK + TWA + 16;
+  static constexpr size_t SMEM = INTER + 2 * WORK + TWA + 32;
   static constexpr int EW = sizeof(C2) / 8;  // 8-byte TMA elements per complex
 };
 
@@ -89,14 +89,20 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
   if (tid == 0) {
     sa_mbar_init(&mbar[0], 1);
     sa_mbar_init(&mbar[1], 1);
+    sa_mbar_init(&mbar[2], 1);  // "node storage full": expect_tx(INTER) per signal
     sa_fence_mbar_init();
   }
   __syncthreads();
   cluster.sync();
 
-  C2 *inter_rank[P::CL];
+  // cluster-window addresses of every peer's node storage and "full" mbarrier
+  uint32_t inter_rank[P::CL], full_rank[P::CL];
 #pragma unroll
-  for (int r = 0; r < P::CL; ++r) inter_rank[r] = cluster.map_shared_rank(inter, r);
+  for (int r = 0; r < P::CL; ++r) {
+    inter_rank[r] = sa_mapa(sa_smem_u32(inter), r);
+    full_rank[r] = sa_mapa(sa_smem_u32(&mbar[2]), r);
+  }
+  uint32_t sig_iter = 0;
 
   auto issue = [&](int64_t sig, int tt, int buf) {
     if (tid == 0) {
@@ -109,8 +115,10 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
 
   int64_t it = 0;  // global tile counter (buffer / parity)
   if (cid < batch) issue(cid, 0, 0);
+  sa_cluster_arrive_relaxed();  // "node storage free" for the first signal
 
-  for (int64_t sig = cid; sig < batch; sig += ncl) {
+  for (int64_t sig = cid; sig < batch; sig += ncl, ++sig_iter) {
+    if (tid == 0) sa_mbar_expect_tx(&mbar[2], (uint32_t)P::INTER);
     // ------------------------------------------------------------- phase A
     for (int tt = 0; tt < TILES; ++tt, ++it) {
       const int buf = (int)(it & 1);
@@ -166,58 +174,277 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
         for (int k = 0; k < 16; ++k)
           if (!(k & hr)) r_dit<T>(v[k], v[k + hr], twA[(h - 1) + m2_g + 16 * (k & (hr - 1))]);
       }
-      // scatter node row R = rev8(c) over the cluster: column q lives in CTA q / COLS
+      // scatter node row R = rev8(c) over the cluster: column q lives in CTA q / COLS.
+      // Before the first scatter of a signal, every CTA must be done reading its
+      // node storage for the previous signal (arrived after its last phase-B read).
+      if (tt == 0) sa_cluster_wait();
       {
         const int c = rank * COLS + tt * TC + m2_cc;
         const int R = rev8(c);
         constexpr int KPC = COLS / 16;  // registers per owner CTA
 #pragma unroll
         for (int k = 0; k < 16; ++k)
-          inter_rank[k / KPC][R * COLS + m2_g + 16 * (k % KPC)] = A::to(v[k]);
+          sa_st_async(inter_rank[k / KPC] + (uint32_t)(sizeof(C2) * (R * COLS + m2_g + 16 * (k % KPC))),
+                      A::to(v[k]), full_rank[k / KPC]);
       }
       __syncthreads();  // work[buf] fully consumed before it is re-armed
     }
-    cluster.sync();
     // ------------------------------------------------------------- phase B
     C2 *ysig = y + sig * NN;
+    // twiddles: round 1 (stages 9..12) w1[h-1+a] = stage[off(t) + a*256 + q];
+    //           round 2 (stages 13..16) w2[hr-1+a] = stage[off(t) + (g+16a)*256 + q].
+    // Software-pipelined: w2 of tile tt and w1 of tile tt+1 are in flight while
+    // the other round computes, so L2 latency is hidden.
+    C4 w1[15], w2[15];
+    auto load_w1 = [&](int q) {
+#pragma unroll
+      for (int t = 1; t <= 4; ++t)
+#pragma unroll
+        for (int a = 0; a < (1 << (t - 1)); ++a)
+          w1[(1 << (t - 1)) - 1 + a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + a * 256 + q]);
+    };
+    auto load_w2 = [&](int q) {
+#pragma unroll
+      for (int t = 5; t <= 8; ++t)
+#pragma unroll
+        for (int a = 0; a < (1 << (t - 5)); ++a)
+          w2[(1 << (t - 5)) - 1 + a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + (m1_g + 16 * a) * 256 + q]);
+    };
+    // fp64 keeps one twiddle set in flight (register budget); fp32 pipelines both.
+    constexpr bool PREF = sizeof(T) == 4;
+    load_w1(rank * COLS + m1_cc);
+    sa_mbar_wait_cluster(&mbar[2], sig_iter & 1);  // all INTER bytes of this signal landed
     for (int tt = 0; tt < TILES; ++tt) {
       const int lq = tt * TC + m1_cc;
       const int q = rank * COLS + lq;
+      if (PREF) load_w2(q);
+      else if (tt > 0) load_w1(q);
       V v[16];
 #pragma unroll
       for (int k = 0; k < 16; ++k) v[k] = A::from(inter[(m1_g * 16 + k) * COLS + lq]);
 #pragma unroll
       for (int t = 1; t <= 4; ++t) {  // global stage s = 8 + t, pairs along R bits 0..3
         const int h = 1 << (t - 1);
-        const int off = (1 << (7 + t)) - 1;
-        C4 w[8];
-#pragma unroll
-        for (int a = 0; a < h; ++a) w[a] = sa_ldg(&stage[off + a * 256 + q]);
 #pragma unroll
         for (int k = 0; k < 16; ++k)
-          if (!(k & h)) r_dit<T>(v[k], v[k + h], w[k & (h - 1)]);
+          if (!(k & h)) r_dit<T>(v[k], v[k + h], w1[h - 1 + (k & (h - 1))]);
       }
 #pragma unroll
       for (int k = 0; k < 16; ++k) inter[(m1_g * 16 + k) * COLS + lq] = A::to(v[k]);
       __syncthreads();
+      if (PREF && tt + 1 < TILES) load_w1(q + TC);
+      if (!PREF) load_w2(q);
 #pragma unroll
       for (int k = 0; k < 16; ++k) v[k] = A::from(inter[(m1_g + 16 * k) * COLS + lq]);
 #pragma unroll
       for (int t = 5; t <= 8; ++t) {  // global stage s = 8 + t, pairs along R bits 4..7
         const int hr = 1 << (t - 5);
-        const int off = (1 << (7 + t)) - 1;
-        C4 w[8];
-#pragma unroll
-        for (int a = 0; a < hr; ++a) w[a] = sa_ldg(&stage[off + (m1_g + 16 * a) * 256 + q]);
 #pragma unroll
         for (int k = 0; k < 16; ++k)
-          if (!(k & hr)) r_dit<T>(v[k], v[k + hr], w[k & (hr - 1)]);
+          if (!(k & hr)) r_dit<T>(v[k], v[k + hr], w2[hr - 1 + (k & (hr - 1))]);
       }
 #pragma unroll
       for (int k = 0; k < 16; ++k) __stcs(&ysig[(m1_g + 16 * k) * 256 + q], A::to(v[k]));
     }
-    cluster.sync();
+    // Every value this CTA loaded from its node storage has been consumed by the
+    // stores above (in-order issue), so a relaxed arrive is enough to let the
+    // other CTAs start scattering the next signal into it.
+    sa_cluster_arrive_relaxed();
   }
+  sa_cluster_wait();  // pairs the last arrive; no CTA leaves while others may still read
+}
+
+// DIF (DESIGN.md convention): stages s = 16..2 with top = a + b, bot = W ⊙ (a − b),
+// final 2-point NDFT, bit-reversed output.  Mirror image of the DIT kernel:
+//   phase 1: CTA r takes node columns q in [r*COLS, (r+1)*COLS) of x[256 R + q]
+//     (TMA tiles), runs stages 16..9 along R (j = (R mod 2^(t-1))*256 + q), and
+//     sends row R to the CTA owning c = rev8(R) (DSMEM), stored q-swizzled;
+//   phase 2: CTA r' runs stages 8..2 + the 2-point stage along q for its rows
+//     and writes out[rev8(q)*256 + c] (coalesced over c).
+template <typename T>
+__global__ void __launch_bounds__(L64<T>::THREADS, 1)
+    k_nlfft64k_dif(const __grid_constant__ CUtensorMap tmx, typename Ar<T>::C2 *__restrict__ y,
+                   int64_t batch, const typename Ar<T>::C4 *__restrict__ stage, T gain,
+                   int use_gain) {
+  using P = L64<T>;
+  using A = Ar<T>;
+  using V = typename A::V;
+  using C2 = typename P::C2;
+  using C4 = typename P::C4;
+  constexpr int TC = P::TC, COLS = P::COLS, TILES = P::TILES;
+  constexpr bool PREF = sizeof(T) == 4;
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  C2 *inter = reinterpret_cast<C2 *>(smem_raw);  // [COLS local rows][256 q], q ^ (lr & 15)
+  C2 *work = reinterpret_cast<C2 *>(smem_raw + P::INTER);
+  C4 *twA = reinterpret_cast<C4 *>(smem_raw + P::INTER + 2 * P::WORK);
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem_raw + P::INTER + 2 * P::WORK + P::TWA);
+
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int64_t cid = blockIdx.x / P::CL;
+  const int64_t ncl = gridDim.x / P::CL;
+  const int tid = threadIdx.x;
+  const int m1_cc = tid % TC, m1_g = tid / TC;
+  const int m2_g = tid & 15, m2_cc = tid >> 4;
+
+  for (int e = tid; e < 255; e += P::THREADS) twA[e] = stage[e];
+  if (tid == 0) {
+    sa_mbar_init(&mbar[0], 1);
+    sa_mbar_init(&mbar[1], 1);
+    sa_mbar_init(&mbar[2], 1);
+    sa_fence_mbar_init();
+  }
+  __syncthreads();
+  cluster.sync();
+
+  uint32_t inter_rank[P::CL], full_rank[P::CL];
+#pragma unroll
+  for (int r = 0; r < P::CL; ++r) {
+    inter_rank[r] = sa_mapa(sa_smem_u32(inter), r);
+    full_rank[r] = sa_mapa(sa_smem_u32(&mbar[2]), r);
+  }
+
+  auto issue = [&](int64_t sig, int tt, int buf) {
+    if (tid == 0) {
+      sa_fence_proxy_async();
+      sa_mbar_expect_tx(&mbar[buf], (uint32_t)P::WORK);
+      sa_tma_load_2d(work + buf * 256 * TC, &tmx, (rank * COLS + tt * TC) * P::EW, (int)(sig * 256),
+                     &mbar[buf]);
+    }
+  };
+  // phase-1 twiddles: wa (stages 16..13, R bits 7..4): stage[off(t) + (g+16a)*256 + q], t=5..8
+  //                   wb (stages 12..9,  R bits 3..0): stage[off(t) + a*256 + q],      t=1..4
+  C4 wa[15], wb[15];
+  auto load_wa = [&](int q) {
+#pragma unroll
+    for (int t = 5; t <= 8; ++t)
+#pragma unroll
+      for (int a = 0; a < (1 << (t - 5)); ++a)
+        wa[(1 << (t - 5)) - 1 + a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + (m1_g + 16 * a) * 256 + q]);
+  };
+  auto load_wb = [&](int q) {
+#pragma unroll
+    for (int t = 1; t <= 4; ++t)
+#pragma unroll
+      for (int a = 0; a < (1 << (t - 1)); ++a)
+        wb[(1 << (t - 1)) - 1 + a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + a * 256 + q]);
+  };
+
+  int64_t it = 0;
+  uint32_t sig_iter = 0;
+  if (cid < batch) issue(cid, 0, 0);
+  sa_cluster_arrive_relaxed();  // node storage free for the first signal
+  const int rg1 = rev4(m1_g);
+
+  for (int64_t sig = cid; sig < batch; sig += ncl, ++sig_iter) {
+    if (tid == 0) sa_mbar_expect_tx(&mbar[2], (uint32_t)P::INTER);
+    // ------------------------------------------------------------- phase 1
+    for (int tt = 0; tt < TILES; ++tt, ++it) {
+      const int buf = (int)(it & 1);
+      const int q = rank * COLS + tt * TC + m1_cc;
+      load_wa(q);
+      if (PREF) load_wb(q);
+      if (tt + 1 < TILES) issue(sig, tt + 1, buf ^ 1);
+      else if (sig + ncl < batch) issue(sig + ncl, 0, buf ^ 1);
+      sa_mbar_wait(&mbar[buf], (uint32_t)((it >> 1) & 1));
+      C2 *wk = work + buf * 256 * TC;
+      V v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {  // R = g + 16k
+        V x = A::from(wk[(m1_g + 16 * k) * TC + m1_cc]);
+        v[k] = use_gain ? A::scale(x, gain) : x;
+      }
+#pragma unroll
+      for (int t = 8; t >= 5; --t) {  // global stage s = 8 + t, R bits 7..4
+        const int hr = 1 << (t - 5);
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if (!(k & hr)) r_dif<T>(v[k], v[k + hr], wa[hr - 1 + (k & (hr - 1))]);
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) wk[(m1_g + 16 * k) * TC + m1_cc] = A::to(v[k]);
+      __syncthreads();
+      if (!PREF) load_wb(q);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = A::from(wk[(m1_g * 16 + k) * TC + m1_cc]);  // R = 16g + k
+#pragma unroll
+      for (int t = 4; t >= 1; --t) {  // R bits 3..0
+        const int h = 1 << (t - 1);
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if (!(k & h)) r_dif<T>(v[k], v[k + h], wb[h - 1 + (k & (h - 1))]);
+      }
+      // row R = 16g + k goes to the CTA owning c = rev8(R): local row lr = c mod COLS
+      if (tt == 0) sa_cluster_wait();  // peers are done reading their node storage
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int c = crev4(k) * 16 + rg1;
+        const int lr = c % COLS;
+        sa_st_async(inter_rank[c / COLS] + (uint32_t)(sizeof(C2) * (lr * 256 + (q ^ (lr & 15)))),
+                    A::to(v[k]), full_rank[c / COLS]);
+      }
+      __syncthreads();  // work[buf] consumed before it is re-armed
+    }
+    sa_mbar_wait_cluster(&mbar[2], sig_iter & 1);
+    // ------------------------------------------------------------- phase 2
+    C2 *ysig = y + sig * NN;
+    for (int tt = 0; tt < TILES; ++tt) {
+      V v[16];
+      {  // round 1 (M2: g fastest): q = g + 16k ; stages 8..5
+        const int lr = tt * TC + m2_cc;
+        C2 *row = inter + lr * 256;
+        const int sw = lr & 15;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = A::from(row[(m2_g + 16 * k) ^ sw]);
+#pragma unroll
+        for (int s = 8; s >= 5; --s) {
+          const int hr = 1 << (s - 5), h = 1 << (s - 1);
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            if (!(k & hr)) r_dif<T>(v[k], v[k + hr], twA[(h - 1) + m2_g + 16 * (k & (hr - 1))]);
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) row[(m2_g + 16 * k) ^ sw] = A::to(v[k]);
+      }
+      __syncthreads();
+      {  // round 2 (M1: cc fastest): q = 16g + k ; stages 4..2 + 2-point ; bit-reversed store
+        const int lr = tt * TC + m1_cc;
+        const C2 *row = inter + lr * 256;
+        const int sw = lr & 15;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = A::from(row[(m1_g * 16 + k) ^ sw]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {  // s = 4: j = k
+          if (k == 0) r_dif_one<T>(v[k], v[k + 8]);
+          else if (k == 4) r_dif_mj<T>(v[k], v[k + 8]);
+          else r_dif<T>(v[k], v[k + 8], twA[7 + k]);
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k)  // s = 3: j = k & 3
+          if (!(k & 4)) {
+            const int j = k & 3;
+            if (j == 0) r_dif_one<T>(v[k], v[k + 4]);
+            else if (j == 2) r_dif_mj<T>(v[k], v[k + 4]);
+            else r_dif<T>(v[k], v[k + 4], twA[3 + j]);
+          }
+#pragma unroll
+        for (int k = 0; k < 16; ++k)  // s = 2: j = k & 1
+          if (!(k & 2)) {
+            if (k & 1) r_dif_mj<T>(v[k], v[k + 2]);
+            else r_dif_one<T>(v[k], v[k + 2]);
+          }
+#pragma unroll
+        for (int k = 0; k < 16; k += 2) r_two_point<T>(v[k], v[k + 1]);
+        const int c = rank * COLS + lr;
+        const int rg = rev4(m1_g);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) __stcs(&ysig[(crev4(k) * 16 + rg) * 256 + c], A::to(v[k]));
+      }
+    }
+    sa_cluster_arrive_relaxed();  // all node-storage reads consumed (stores issued)
+  }
+  sa_cluster_wait();
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -233,7 +460,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 template <typename T>
-int launch64k(const void *x, void *y, int64_t batch, const SaTwiddles *tw, double gain,
+int launch64k(int variant, const void *x, void *y, int64_t batch, const SaTwiddles *tw, double gain,
               cudaStream_t s) {
   using P = L64<T>;
   auto enc = encode_fn();
@@ -253,7 +480,7 @@ int launch64k(const void *x, void *y, int64_t batch, const SaTwiddles *tw, doubl
     sa_set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
     return SA_ERR_CUDA;
   }
-  auto kern = k_nlfft64k_dit<T>;
+  auto kern = variant == SA_DIT ? k_nlfft64k_dit<T> : k_nlfft64k_dif<T>;
   SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM));
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -285,8 +512,8 @@ int launch64k(const void *x, void *y, int64_t batch, const SaTwiddles *tw, doubl
 // Returns SA_ERR_UNSUPPORTED when the fused path does not apply (caller falls back).
 int sa_launch_nlfft64k(int dtype, int variant, const void *x, void *y, int64_t batch, int64_t n,
                        const SaTwiddles *tw, double gain, cudaStream_t s) {
-  if (n != NN || variant != SA_DIT || batch < 1) return SA_ERR_UNSUPPORTED;
+  if (n != NN || batch < 1) return SA_ERR_UNSUPPORTED;
   if (((uintptr_t)x & 15) != 0) return SA_ERR_UNSUPPORTED;
-  if (dtype == SA_C64) return launch64k<float>(x, y, batch, tw, gain, s);
-  return launch64k<double>(x, y, batch, tw, gain, s);
+  if (dtype == SA_C64) return launch64k<float>(variant, x, y, batch, tw, gain, s);
+  return launch64k<double>(variant, x, y, batch, tw, gain, s);
 }

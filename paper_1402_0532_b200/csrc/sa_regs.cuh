@@ -176,3 +176,38 @@ SA_HD void sa_tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uin
       "l"(map), "r"(c0), "r"(c1), "r"(sa_smem_u32(bar))
       : "memory");
 }
+
+// split cluster barrier: arrive early, wait late.  release only where DSMEM
+// writes must be published; relaxed where only execution order matters (a CTA's
+// own smem reads completed -- their values were consumed -- before it arrives).
+SA_HD void sa_cluster_arrive_release() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+SA_HD void sa_cluster_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory"); }
+SA_HD void sa_cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
+
+// DSMEM producer -> consumer hand-off without fences: st.async writes into a
+// cluster peer's smem and credits the bytes to the peer's mbarrier
+// (complete_tx); the peer waits on its own mbarrier with cluster-scope acquire.
+SA_HD uint32_t sa_mapa(uint32_t local_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
+  return r;
+}
+SA_HD void sa_st_async(uint32_t addr, float2 v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(addr),
+               "f"(v.x), "f"(v.y), "r"(mbar)
+               : "memory");
+}
+SA_HD void sa_st_async(uint32_t addr, double2 v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(addr),
+               "d"(v.x), "d"(v.y), "r"(mbar)
+               : "memory");
+}
+SA_HD void sa_mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "SA_WAITC_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra SA_WAITC_%=;\n}\n" ::"r"(sa_smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
