@@ -8,14 +8,17 @@
 //     bit-reversed blocks, SURVEY §7 hard part 4), in TMA-loaded tiles of TC
 //     columns x 256 rows, runs global stages 1..8 in two register radix-16
 //     rounds (stage 1 = the 2-point NDFT bottom), and scatters node row
-//     R = rev8(c) over the cluster through DSMEM: q-columns [r*COLS, (r+1)*COLS)
-//     of every row live in CTA r.
-//   cluster barrier
-//   phase B: CTA r runs global stages 9..16 along R for its COLS columns
-//     (twiddle j = (R mod 2^(t-1))*256 + q) and writes y[256 R + q] (coalesced).
-//   cluster barrier (node storage reusable), next signal.
-// HBM traffic = one read + one write of the signal.  The next tile's TMA load
-// is issued before the current tile is processed (double buffer, mbarriers).
+//     R = rev8(c) over the cluster with st.async into the owner's smem,
+//     crediting the owner's "full" mbarrier (no fence, no cluster barrier):
+//     q-columns [r*COLS, (r+1)*COLS) of every row live in CTA r.
+//   phase B: CTA r waits for its 128 KiB, runs global stages 9..16 along R for
+//     its columns (twiddle j = (R mod 2^(t-1))*256 + q), writes y[256 R + q].
+//   A relaxed cluster arrive (after the last read of the node storage) / wait
+//     (before the next signal's first scatter) guards the storage reuse.
+// Each CTA runs NG independent thread groups (named barriers, own TMA buffer
+// and mbarrier), each owning every NG-th tile, so one group's barrier / TMA /
+// L2 latency is covered by the others' arithmetic (16 warps/SM for c64).
+// HBM traffic = one read + one write of the signal.
 #include <algorithm>
 #include <cooperative_groups.h>
 #include <cudaTypedefs.h>
@@ -34,29 +37,91 @@ template <typename T> struct K64;
 template <> struct K64<float> {
   static constexpr int TC = 16;  // columns per tile
   static constexpr int CL = 4;   // cluster size
+  static constexpr int NG = 2;   // thread groups per CTA
 };
 template <> struct K64<double> {
   static constexpr int TC = 8;
   static constexpr int CL = 8;
+  static constexpr int NG = 2;
 };
 
 template <typename T> struct L64 {
-  static constexpr int TC = K64<T>::TC, CL = K64<T>::CL;
-  static constexpr int THREADS = 16 * TC;
-  static constexpr int COLS = 256 / CL;  // node columns owned per CTA
-  static constexpr int TILES = COLS / TC;
+  static constexpr int TC = K64<T>::TC, CL = K64<T>::CL, NG = K64<T>::NG;
+  static constexpr int GT = 16 * TC;          // threads per group
+  static constexpr int THREADS = NG * GT;
+  static constexpr int COLS = 256 / CL;       // node columns owned per CTA
+  static constexpr int TILES = COLS / TC;     // tiles per CTA per phase
+  static constexpr int TPG = TILES / NG;      // tiles per group per phase
   using C2 = typename Ar<T>::C2;
   using C4 = typename Ar<T>::C4;
   static constexpr size_t INTER = sizeof(C2) * 256 * COLS;
-  static constexpr size_t WORK = sizeof(C2) * 256 * TC;
+  static constexpr size_t WORK = sizeof(C2) * 256 * TC;  // one tile
   static constexpr size_t TWA = sizeof(C4) * 255;
-  static constexpr size_t SMEM = INTER + 2 * WORK + TWA + 32;
+  static constexpr size_t MBAR_OFF = INTER + NG * WORK + TWA;
+  static constexpr size_t SMEM = MBAR_OFF + 8 * (NG + 1);
   static constexpr int EW = sizeof(C2) / 8;  // 8-byte TMA elements per complex
+  static_assert(TILES % NG == 0, "tiles must split evenly over groups");
 };
 
 SA_HD int rev4(int v) { return (int)(__brev((unsigned)v) >> 28); }
 SA_HD int rev8(int v) { return (int)(__brev((unsigned)v) >> 24); }
 constexpr int crev4(int v) { return ((v & 1) << 3) | ((v & 2) << 1) | ((v & 4) >> 1) | ((v & 8) >> 3); }
+
+SA_HD void group_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// per-CTA setup shared by DIT and DIF
+template <typename T> struct Ctx {
+  using P = L64<T>;
+  typename P::C2 *inter, *work;
+  typename P::C4 *twA;
+  uint64_t *tma_bar, *full_bar;
+  uint32_t inter_rank[P::CL], full_rank[P::CL];
+  int rank, gi, gt;
+  int64_t cid, ncl;
+};
+
+template <typename T>
+SA_HD void ctx_init(Ctx<T> &c, unsigned char *smem_raw, const typename L64<T>::C4 *stage) {
+  using P = L64<T>;
+  cg::cluster_group cluster = cg::this_cluster();
+  c.inter = reinterpret_cast<typename P::C2 *>(smem_raw);
+  c.work = reinterpret_cast<typename P::C2 *>(smem_raw + P::INTER);
+  c.twA = reinterpret_cast<typename P::C4 *>(smem_raw + P::INTER + P::NG * P::WORK);
+  c.tma_bar = reinterpret_cast<uint64_t *>(smem_raw + P::MBAR_OFF);
+  c.full_bar = c.tma_bar + P::NG;
+  c.rank = (int)cluster.block_rank();
+  c.cid = blockIdx.x / P::CL;
+  c.ncl = gridDim.x / P::CL;
+  c.gi = threadIdx.x / P::GT;
+  c.gt = threadIdx.x % P::GT;
+  for (int e = threadIdx.x; e < 255; e += P::THREADS) c.twA[e] = stage[e];  // global stages 1..8
+  if (threadIdx.x == 0) {
+    for (int g = 0; g < P::NG; ++g) sa_mbar_init(&c.tma_bar[g], 1);
+    sa_mbar_init(c.full_bar, 1);  // expect_tx(INTER) once per signal
+    sa_fence_mbar_init();
+  }
+  __syncthreads();
+  cluster.sync();
+#pragma unroll
+  for (int r = 0; r < P::CL; ++r) {
+    c.inter_rank[r] = sa_mapa(sa_smem_u32(c.inter), r);
+    c.full_rank[r] = sa_mapa(sa_smem_u32(c.full_bar), r);
+  }
+}
+
+// group-leader TMA of tile tt (TC columns x 256 rows) of signal sig into the group buffer
+template <typename T>
+SA_HD void tma_tile(const Ctx<T> &c, const CUtensorMap *tmx, int64_t sig, int tt) {
+  using P = L64<T>;
+  if (c.gt == 0) {
+    sa_fence_proxy_async();
+    sa_mbar_expect_tx(&c.tma_bar[c.gi], (uint32_t)P::WORK);
+    sa_tma_load_2d(c.work + c.gi * 256 * P::TC, tmx, (c.rank * P::COLS + tt * P::TC) * P::EW,
+                   (int)(sig * 256), &c.tma_bar[c.gi]);
+  }
+}
 
 template <typename T>
 __global__ void __launch_bounds__(L64<T>::THREADS, 1)
@@ -68,67 +133,29 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
   using V = typename A::V;
   using C2 = typename P::C2;
   using C4 = typename P::C4;
-  constexpr int TC = P::TC, COLS = P::COLS, TILES = P::TILES;
-
+  constexpr int TC = P::TC, COLS = P::COLS, NG = P::NG, GT = P::GT, TPG = P::TPG;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  C2 *inter = reinterpret_cast<C2 *>(smem_raw);
-  C2 *work = reinterpret_cast<C2 *>(smem_raw + P::INTER);
-  C4 *twA = reinterpret_cast<C4 *>(smem_raw + P::INTER + 2 * P::WORK);
-  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem_raw + P::INTER + 2 * P::WORK + P::TWA);
+  Ctx<T> c;
+  ctx_init<T>(c, smem_raw, stage);
+  const int gbar = 1 + c.gi;
+  const int m1_cc = c.gt % TC, m1_g = c.gt / TC;
+  const int m2_g = c.gt & 15, m2_cc = c.gt >> 4;
+  C2 *wk = c.work + c.gi * 256 * TC;
+  C4 *twA = c.twA;
 
-  cg::cluster_group cluster = cg::this_cluster();
-  const int rank = (int)cluster.block_rank();
-  const int64_t cid = blockIdx.x / P::CL;
-  const int64_t ncl = gridDim.x / P::CL;
-  const int tid = threadIdx.x;
-  // mapping M1: cc fastest ; mapping M2: g fastest
-  const int m1_cc = tid % TC, m1_g = tid / TC;
-  const int m2_g = tid & 15, m2_cc = tid >> 4;
+  uint32_t tile_it = 0;  // this group's TMA uses (parity)
+  uint32_t sig_it = 0;
+  if (c.cid < batch) tma_tile<T>(c, &tmx, c.cid, c.gi);
+  sa_cluster_arrive_relaxed();  // node storage free for the first signal
 
-  for (int e = tid; e < 255; e += P::THREADS) twA[e] = stage[e];  // global stages 1..8
-  if (tid == 0) {
-    sa_mbar_init(&mbar[0], 1);
-    sa_mbar_init(&mbar[1], 1);
-    sa_mbar_init(&mbar[2], 1);  // "node storage full": expect_tx(INTER) per signal
-    sa_fence_mbar_init();
-  }
-  __syncthreads();
-  cluster.sync();
-
-  // cluster-window addresses of every peer's node storage and "full" mbarrier
-  uint32_t inter_rank[P::CL], full_rank[P::CL];
-#pragma unroll
-  for (int r = 0; r < P::CL; ++r) {
-    inter_rank[r] = sa_mapa(sa_smem_u32(inter), r);
-    full_rank[r] = sa_mapa(sa_smem_u32(&mbar[2]), r);
-  }
-  uint32_t sig_iter = 0;
-
-  auto issue = [&](int64_t sig, int tt, int buf) {
-    if (tid == 0) {
-      sa_fence_proxy_async();
-      sa_mbar_expect_tx(&mbar[buf], (uint32_t)P::WORK);
-      sa_tma_load_2d(work + buf * 256 * TC, &tmx, (rank * COLS + tt * TC) * P::EW, (int)(sig * 256),
-                     &mbar[buf]);
-    }
-  };
-
-  int64_t it = 0;  // global tile counter (buffer / parity)
-  if (cid < batch) issue(cid, 0, 0);
-  sa_cluster_arrive_relaxed();  // "node storage free" for the first signal
-
-  for (int64_t sig = cid; sig < batch; sig += ncl, ++sig_iter) {
-    if (tid == 0) sa_mbar_expect_tx(&mbar[2], (uint32_t)P::INTER);
+  for (int64_t sig = c.cid; sig < batch; sig += c.ncl, ++sig_it) {
+    if (threadIdx.x == 0) sa_mbar_expect_tx(c.full_bar, (uint32_t)P::INTER);
     // ------------------------------------------------------------- phase A
-    for (int tt = 0; tt < TILES; ++tt, ++it) {
-      const int buf = (int)(it & 1);
-      if (tt + 1 < TILES) issue(sig, tt + 1, buf ^ 1);
-      else if (sig + ncl < batch) issue(sig + ncl, 0, buf ^ 1);
-      sa_mbar_wait(&mbar[buf], (uint32_t)((it >> 1) & 1));
-      C2 *wk = work + buf * 256 * TC;
+    for (int u = 0; u < TPG; ++u, ++tile_it) {
+      const int tt = c.gi + NG * u;
+      sa_mbar_wait(&c.tma_bar[c.gi], tile_it & 1);
       V v[16];
-      // round 1 (M1): v[k] = node 16g+k of sub-transform cc = X[rev8(16g+k)][cc]
-      {
+      {  // round 1 (M1): v[k] = node 16g+k of sub-transform cc = X[rev8(16g+k)][cc]
         const int rg = rev4(m1_g);
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
@@ -158,15 +185,17 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
           else r_dit<T>(v[k], v[k + 8], twA[7 + k]);
         }
       }
-      __syncthreads();
+      group_sync(gbar, GT);
 #pragma unroll
       for (int k = 0; k < 16; ++k)  // exchange: node q = 16g+k, column swizzled by q & (TC-1)
         wk[(m1_g * 16 + k) * TC + (m1_cc ^ (k & (TC - 1)))] = A::to(v[k]);
-      __syncthreads();
-      // round 2 (M2): v[k] = node g + 16k of sub-transform cc ; global stages 5..8
+      group_sync(gbar, GT);
 #pragma unroll
-      for (int k = 0; k < 16; ++k)
+      for (int k = 0; k < 16; ++k)  // round 2 (M2): node g + 16k of sub-transform cc
         v[k] = A::from(wk[(m2_g + 16 * k) * TC + (m2_cc ^ (m2_g & (TC - 1)))]);
+      group_sync(gbar, GT);  // tile buffer consumed: re-arm it
+      if (u + 1 < TPG) tma_tile<T>(c, &tmx, sig, tt + NG);
+      else if (sig + c.ncl < batch) tma_tile<T>(c, &tmx, sig + c.ncl, c.gi);
 #pragma unroll
       for (int t = 5; t <= 8; ++t) {
         const int hr = 1 << (t - 5), h = 1 << (t - 1);
@@ -174,91 +203,72 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
         for (int k = 0; k < 16; ++k)
           if (!(k & hr)) r_dit<T>(v[k], v[k + hr], twA[(h - 1) + m2_g + 16 * (k & (hr - 1))]);
       }
-      // scatter node row R = rev8(c) over the cluster: column q lives in CTA q / COLS.
-      // Before the first scatter of a signal, every CTA must be done reading its
-      // node storage for the previous signal (arrived after its last phase-B read).
-      if (tt == 0) sa_cluster_wait();
+      // scatter node row R = rev8(c): column q lives in CTA q / COLS (st.async credits its mbarrier)
+      if (u == 0) sa_cluster_wait();  // peers finished reading their storage (previous signal)
       {
-        const int c = rank * COLS + tt * TC + m2_cc;
-        const int R = rev8(c);
+        const int cc = c.rank * COLS + tt * TC + m2_cc;
+        const int R = rev8(cc);
         constexpr int KPC = COLS / 16;  // registers per owner CTA
 #pragma unroll
         for (int k = 0; k < 16; ++k)
-          sa_st_async(inter_rank[k / KPC] + (uint32_t)(sizeof(C2) * (R * COLS + m2_g + 16 * (k % KPC))),
-                      A::to(v[k]), full_rank[k / KPC]);
+          sa_st_async(c.inter_rank[k / KPC] + (uint32_t)(sizeof(C2) * (R * COLS + m2_g + 16 * (k % KPC))),
+                      A::to(v[k]), c.full_rank[k / KPC]);
       }
-      __syncthreads();  // work[buf] fully consumed before it is re-armed
     }
     // ------------------------------------------------------------- phase B
     C2 *ysig = y + sig * NN;
-    // twiddles: round 1 (stages 9..12) w1[h-1+a] = stage[off(t) + a*256 + q];
-    //           round 2 (stages 13..16) w2[hr-1+a] = stage[off(t) + (g+16a)*256 + q].
-    // Software-pipelined: w2 of tile tt and w1 of tile tt+1 are in flight while
-    // the other round computes, so L2 latency is hidden.
-    C4 w1[15], w2[15];
-    auto load_w1 = [&](int q) {
+    C4 w[15];
+    sa_mbar_wait_cluster(c.full_bar, sig_it & 1);  // all INTER bytes of this signal landed
+    for (int u = 0; u < TPG; ++u) {
+      const int tt = c.gi + NG * u;
+      const int lq = tt * TC + m1_cc;
+      const int q = c.rank * COLS + lq;
 #pragma unroll
-      for (int t = 1; t <= 4; ++t)
+      for (int t = 1; t <= 4; ++t)  // stages 9..12: w[h-1+a] = stage[off + a*256 + q]
 #pragma unroll
         for (int a = 0; a < (1 << (t - 1)); ++a)
-          w1[(1 << (t - 1)) - 1 + a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + a * 256 + q]);
-    };
-    auto load_w2 = [&](int q) {
-#pragma unroll
-      for (int t = 5; t <= 8; ++t)
-#pragma unroll
-        for (int a = 0; a < (1 << (t - 5)); ++a)
-          w2[(1 << (t - 5)) - 1 + a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + (m1_g + 16 * a) * 256 + q]);
-    };
-    // fp64 keeps one twiddle set in flight (register budget); fp32 pipelines both.
-    constexpr bool PREF = sizeof(T) == 4;
-    load_w1(rank * COLS + m1_cc);
-    sa_mbar_wait_cluster(&mbar[2], sig_iter & 1);  // all INTER bytes of this signal landed
-    for (int tt = 0; tt < TILES; ++tt) {
-      const int lq = tt * TC + m1_cc;
-      const int q = rank * COLS + lq;
-      if (PREF) load_w2(q);
-      else if (tt > 0) load_w1(q);
+          w[(1 << (t - 1)) - 1 + a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + a * 256 + q]);
       V v[16];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = A::from(inter[(m1_g * 16 + k) * COLS + lq]);
+      for (int k = 0; k < 16; ++k) v[k] = A::from(c.inter[(m1_g * 16 + k) * COLS + lq]);
 #pragma unroll
-      for (int t = 1; t <= 4; ++t) {  // global stage s = 8 + t, pairs along R bits 0..3
+      for (int t = 1; t <= 4; ++t) {  // R bits 0..3
         const int h = 1 << (t - 1);
 #pragma unroll
         for (int k = 0; k < 16; ++k)
-          if (!(k & h)) r_dit<T>(v[k], v[k + h], w1[h - 1 + (k & (h - 1))]);
+          if (!(k & h)) r_dit<T>(v[k], v[k + h], w[h - 1 + (k & (h - 1))]);
       }
 #pragma unroll
-      for (int k = 0; k < 16; ++k) inter[(m1_g * 16 + k) * COLS + lq] = A::to(v[k]);
-      __syncthreads();
-      if (PREF && tt + 1 < TILES) load_w1(q + TC);
-      if (!PREF) load_w2(q);
+      for (int t = 5; t <= 8; ++t)  // stages 13..16: w[hr-1+a] = stage[off + (g+16a)*256 + q]
 #pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = A::from(inter[(m1_g + 16 * k) * COLS + lq]);
+        for (int a = 0; a < (1 << (t - 5)); ++a)
+          w[(1 << (t - 5)) - 1 + a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + (m1_g + 16 * a) * 256 + q]);
 #pragma unroll
-      for (int t = 5; t <= 8; ++t) {  // global stage s = 8 + t, pairs along R bits 4..7
+      for (int k = 0; k < 16; ++k) c.inter[(m1_g * 16 + k) * COLS + lq] = A::to(v[k]);
+      group_sync(gbar, GT);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = A::from(c.inter[(m1_g + 16 * k) * COLS + lq]);
+#pragma unroll
+      for (int t = 5; t <= 8; ++t) {  // R bits 4..7
         const int hr = 1 << (t - 5);
 #pragma unroll
         for (int k = 0; k < 16; ++k)
-          if (!(k & hr)) r_dit<T>(v[k], v[k + hr], w2[hr - 1 + (k & (hr - 1))]);
+          if (!(k & hr)) r_dit<T>(v[k], v[k + hr], w[hr - 1 + (k & (hr - 1))]);
       }
 #pragma unroll
       for (int k = 0; k < 16; ++k) __stcs(&ysig[(m1_g + 16 * k) * 256 + q], A::to(v[k]));
     }
-    // Every value this CTA loaded from its node storage has been consumed by the
-    // stores above (in-order issue), so a relaxed arrive is enough to let the
-    // other CTAs start scattering the next signal into it.
+    // every node-storage value this thread loaded was consumed by the stores above
     sa_cluster_arrive_relaxed();
   }
-  sa_cluster_wait();  // pairs the last arrive; no CTA leaves while others may still read
+  sa_cluster_wait();  // pairs the last arrive
 }
 
 // DIF (DESIGN.md convention): stages s = 16..2 with top = a + b, bot = W ⊙ (a − b),
 // final 2-point NDFT, bit-reversed output.  Mirror image of the DIT kernel:
 //   phase 1: CTA r takes node columns q in [r*COLS, (r+1)*COLS) of x[256 R + q]
 //     (TMA tiles), runs stages 16..9 along R (j = (R mod 2^(t-1))*256 + q), and
-//     sends row R to the CTA owning c = rev8(R) (DSMEM), stored q-swizzled;
+//     sends row R to the CTA owning c = rev8(R) (st.async), stored q-swizzled;
 //   phase 2: CTA r' runs stages 8..2 + the 2-point stage along q for its rows
 //     and writes out[rev8(q)*256 + c] (coalesced over c).
 template <typename T>
@@ -271,84 +281,34 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
   using V = typename A::V;
   using C2 = typename P::C2;
   using C4 = typename P::C4;
-  constexpr int TC = P::TC, COLS = P::COLS, TILES = P::TILES;
-  constexpr bool PREF = sizeof(T) == 4;
-
+  constexpr int TC = P::TC, COLS = P::COLS, NG = P::NG, GT = P::GT, TPG = P::TPG;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  C2 *inter = reinterpret_cast<C2 *>(smem_raw);  // [COLS local rows][256 q], q ^ (lr & 15)
-  C2 *work = reinterpret_cast<C2 *>(smem_raw + P::INTER);
-  C4 *twA = reinterpret_cast<C4 *>(smem_raw + P::INTER + 2 * P::WORK);
-  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem_raw + P::INTER + 2 * P::WORK + P::TWA);
-
-  cg::cluster_group cluster = cg::this_cluster();
-  const int rank = (int)cluster.block_rank();
-  const int64_t cid = blockIdx.x / P::CL;
-  const int64_t ncl = gridDim.x / P::CL;
-  const int tid = threadIdx.x;
-  const int m1_cc = tid % TC, m1_g = tid / TC;
-  const int m2_g = tid & 15, m2_cc = tid >> 4;
-
-  for (int e = tid; e < 255; e += P::THREADS) twA[e] = stage[e];
-  if (tid == 0) {
-    sa_mbar_init(&mbar[0], 1);
-    sa_mbar_init(&mbar[1], 1);
-    sa_mbar_init(&mbar[2], 1);
-    sa_fence_mbar_init();
-  }
-  __syncthreads();
-  cluster.sync();
-
-  uint32_t inter_rank[P::CL], full_rank[P::CL];
-#pragma unroll
-  for (int r = 0; r < P::CL; ++r) {
-    inter_rank[r] = sa_mapa(sa_smem_u32(inter), r);
-    full_rank[r] = sa_mapa(sa_smem_u32(&mbar[2]), r);
-  }
-
-  auto issue = [&](int64_t sig, int tt, int buf) {
-    if (tid == 0) {
-      sa_fence_proxy_async();
-      sa_mbar_expect_tx(&mbar[buf], (uint32_t)P::WORK);
-      sa_tma_load_2d(work + buf * 256 * TC, &tmx, (rank * COLS + tt * TC) * P::EW, (int)(sig * 256),
-                     &mbar[buf]);
-    }
-  };
-  // phase-1 twiddles: wa (stages 16..13, R bits 7..4): stage[off(t) + (g+16a)*256 + q], t=5..8
-  //                   wb (stages 12..9,  R bits 3..0): stage[off(t) + a*256 + q],      t=1..4
-  C4 wa[15], wb[15];
-  auto load_wa = [&](int q) {
-#pragma unroll
-    for (int t = 5; t <= 8; ++t)
-#pragma unroll
-      for (int a = 0; a < (1 << (t - 5)); ++a)
-        wa[(1 << (t - 5)) - 1 + a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + (m1_g + 16 * a) * 256 + q]);
-  };
-  auto load_wb = [&](int q) {
-#pragma unroll
-    for (int t = 1; t <= 4; ++t)
-#pragma unroll
-      for (int a = 0; a < (1 << (t - 1)); ++a)
-        wb[(1 << (t - 1)) - 1 + a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + a * 256 + q]);
-  };
-
-  int64_t it = 0;
-  uint32_t sig_iter = 0;
-  if (cid < batch) issue(cid, 0, 0);
-  sa_cluster_arrive_relaxed();  // node storage free for the first signal
+  Ctx<T> c;
+  ctx_init<T>(c, smem_raw, stage);
+  const int gbar = 1 + c.gi;
+  const int m1_cc = c.gt % TC, m1_g = c.gt / TC;
+  const int m2_g = c.gt & 15, m2_cc = c.gt >> 4;
+  C2 *wk = c.work + c.gi * 256 * TC;
+  C4 *twA = c.twA;
   const int rg1 = rev4(m1_g);
 
-  for (int64_t sig = cid; sig < batch; sig += ncl, ++sig_iter) {
-    if (tid == 0) sa_mbar_expect_tx(&mbar[2], (uint32_t)P::INTER);
+  uint32_t tile_it = 0, sig_it = 0;
+  if (c.cid < batch) tma_tile<T>(c, &tmx, c.cid, c.gi);
+  sa_cluster_arrive_relaxed();
+
+  for (int64_t sig = c.cid; sig < batch; sig += c.ncl, ++sig_it) {
+    if (threadIdx.x == 0) sa_mbar_expect_tx(c.full_bar, (uint32_t)P::INTER);
     // ------------------------------------------------------------- phase 1
-    for (int tt = 0; tt < TILES; ++tt, ++it) {
-      const int buf = (int)(it & 1);
-      const int q = rank * COLS + tt * TC + m1_cc;
-      load_wa(q);
-      if (PREF) load_wb(q);
-      if (tt + 1 < TILES) issue(sig, tt + 1, buf ^ 1);
-      else if (sig + ncl < batch) issue(sig + ncl, 0, buf ^ 1);
-      sa_mbar_wait(&mbar[buf], (uint32_t)((it >> 1) & 1));
-      C2 *wk = work + buf * 256 * TC;
+    for (int u = 0; u < TPG; ++u, ++tile_it) {
+      const int tt = c.gi + NG * u;
+      const int q = c.rank * COLS + tt * TC + m1_cc;
+      C4 w[15];
+#pragma unroll
+      for (int t = 5; t <= 8; ++t)  // stages 16..13: w[hr-1+a] = stage[off + (g+16a)*256 + q]
+#pragma unroll
+        for (int a = 0; a < (1 << (t - 5)); ++a)
+          w[(1 << (t - 5)) - 1 + a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + (m1_g + 16 * a) * 256 + q]);
+      sa_mbar_wait(&c.tma_bar[c.gi], tile_it & 1);
       V v[16];
 #pragma unroll
       for (int k = 0; k < 16; ++k) {  // R = g + 16k
@@ -356,44 +316,50 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
         v[k] = use_gain ? A::scale(x, gain) : x;
       }
 #pragma unroll
-      for (int t = 8; t >= 5; --t) {  // global stage s = 8 + t, R bits 7..4
+      for (int t = 8; t >= 5; --t) {  // R bits 7..4
         const int hr = 1 << (t - 5);
 #pragma unroll
         for (int k = 0; k < 16; ++k)
-          if (!(k & hr)) r_dif<T>(v[k], v[k + hr], wa[hr - 1 + (k & (hr - 1))]);
+          if (!(k & hr)) r_dif<T>(v[k], v[k + hr], w[hr - 1 + (k & (hr - 1))]);
       }
 #pragma unroll
+      for (int t = 1; t <= 4; ++t)  // stages 12..9: w[h-1+a] = stage[off + a*256 + q]
+#pragma unroll
+        for (int a = 0; a < (1 << (t - 1)); ++a)
+          w[(1 << (t - 1)) - 1 + a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + a * 256 + q]);
+#pragma unroll
       for (int k = 0; k < 16; ++k) wk[(m1_g + 16 * k) * TC + m1_cc] = A::to(v[k]);
-      __syncthreads();
-      if (!PREF) load_wb(q);
+      group_sync(gbar, GT);
 #pragma unroll
       for (int k = 0; k < 16; ++k) v[k] = A::from(wk[(m1_g * 16 + k) * TC + m1_cc]);  // R = 16g + k
+      group_sync(gbar, GT);  // tile buffer consumed: re-arm it
+      if (u + 1 < TPG) tma_tile<T>(c, &tmx, sig, tt + NG);
+      else if (sig + c.ncl < batch) tma_tile<T>(c, &tmx, sig + c.ncl, c.gi);
 #pragma unroll
       for (int t = 4; t >= 1; --t) {  // R bits 3..0
         const int h = 1 << (t - 1);
 #pragma unroll
         for (int k = 0; k < 16; ++k)
-          if (!(k & h)) r_dif<T>(v[k], v[k + h], wb[h - 1 + (k & (h - 1))]);
+          if (!(k & h)) r_dif<T>(v[k], v[k + h], w[h - 1 + (k & (h - 1))]);
       }
-      // row R = 16g + k goes to the CTA owning c = rev8(R): local row lr = c mod COLS
-      if (tt == 0) sa_cluster_wait();  // peers are done reading their node storage
+      if (u == 0) sa_cluster_wait();
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const int c = crev4(k) * 16 + rg1;
-        const int lr = c % COLS;
-        sa_st_async(inter_rank[c / COLS] + (uint32_t)(sizeof(C2) * (lr * 256 + (q ^ (lr & 15)))),
-                    A::to(v[k]), full_rank[c / COLS]);
+      for (int k = 0; k < 16; ++k) {  // row R = 16g + k -> CTA owning cr = rev8(R), local row cr mod COLS
+        const int cr = crev4(k) * 16 + rg1;
+        const int lr = cr % COLS;
+        sa_st_async(c.inter_rank[cr / COLS] + (uint32_t)(sizeof(C2) * (lr * 256 + (q ^ (lr & 15)))),
+                    A::to(v[k]), c.full_rank[cr / COLS]);
       }
-      __syncthreads();  // work[buf] consumed before it is re-armed
     }
-    sa_mbar_wait_cluster(&mbar[2], sig_iter & 1);
+    sa_mbar_wait_cluster(c.full_bar, sig_it & 1);
     // ------------------------------------------------------------- phase 2
     C2 *ysig = y + sig * NN;
-    for (int tt = 0; tt < TILES; ++tt) {
+    for (int u = 0; u < TPG; ++u) {
+      const int tt = c.gi + NG * u;
       V v[16];
       {  // round 1 (M2: g fastest): q = g + 16k ; stages 8..5
         const int lr = tt * TC + m2_cc;
-        C2 *row = inter + lr * 256;
+        C2 *row = c.inter + lr * 256;
         const int sw = lr & 15;
 #pragma unroll
         for (int k = 0; k < 16; ++k) v[k] = A::from(row[(m2_g + 16 * k) ^ sw]);
@@ -407,10 +373,10 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
 #pragma unroll
         for (int k = 0; k < 16; ++k) row[(m2_g + 16 * k) ^ sw] = A::to(v[k]);
       }
-      __syncthreads();
+      group_sync(gbar, GT);
       {  // round 2 (M1: cc fastest): q = 16g + k ; stages 4..2 + 2-point ; bit-reversed store
         const int lr = tt * TC + m1_cc;
-        const C2 *row = inter + lr * 256;
+        const C2 *row = c.inter + lr * 256;
         const int sw = lr & 15;
 #pragma unroll
         for (int k = 0; k < 16; ++k) v[k] = A::from(row[(m1_g * 16 + k) ^ sw]);
@@ -436,13 +402,13 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
           }
 #pragma unroll
         for (int k = 0; k < 16; k += 2) r_two_point<T>(v[k], v[k + 1]);
-        const int c = rank * COLS + lr;
+        const int cr = c.rank * COLS + lr;
         const int rg = rev4(m1_g);
 #pragma unroll
-        for (int k = 0; k < 16; ++k) __stcs(&ysig[(crev4(k) * 16 + rg) * 256 + c], A::to(v[k]));
+        for (int k = 0; k < 16; ++k) __stcs(&ysig[(crev4(k) * 16 + rg) * 256 + cr], A::to(v[k]));
       }
     }
-    sa_cluster_arrive_relaxed();  // all node-storage reads consumed (stores issued)
+    sa_cluster_arrive_relaxed();
   }
   sa_cluster_wait();
 }

@@ -62,21 +62,29 @@ template <> struct Ar<float> {
     return pack(sa_sgn(lo), sa_sgn(hi));
   }
   static SA_HD V scale(V a, float g) { return mul(pack(g, g), a); }
-  // w ⊙ b with w = {|wr|, |wi|, sgn wr, sgn wi}
+  static SA_HD V swap(V v) {
+    float lo, hi;
+    unpack(v, lo, hi);
+    return pack(hi, lo);
+  }
+  static SA_HD V neg_hi(V v) {
+    float lo, hi;
+    unpack(v, lo, hi);
+    return pack(lo, -hi);
+  }
+  // w ⊙ b with w = {|wr|, |wi|, sgn wr, sgn wi}.  Written so that every pair
+  // shuffle is an operand modifier (LO_HI swap, scalar broadcast, negated
+  // broadcast, high-half negation): 4 packed instructions, no MOVs.
   static SA_HD V twmul(const C4 &w, V b) {
     V sb = sgn(b);
-    V q1 = fma(sb, pack(w.x, w.x), b);  // {P1, P4}
-    V q2 = fma(sb, pack(w.y, w.y), b);  // {P3, P2}
-    V tq = mul(pack(w.w, -w.w), q2);    // {t·P3, −t·P2}
-    float lo, hi;
-    unpack(tq, lo, hi);
-    return fma(pack(w.z, w.z), q1, pack(hi, lo));  // {sP1 − tP2, sP4 + tP3}
+    V q1 = fma(sb, pack(w.x, w.x), b);                   // {P1, P4}
+    V q2 = fma(swap(sb), pack(w.y, w.y), swap(b));       // {P2, P3}
+    V tq = mul(pack(-w.w, -w.w), q2);                    // {−tP2, −tP3}
+    return fma(pack(w.z, w.z), q1, neg_hi(tq));          // {sP1 − tP2, sP4 + tP3}
   }
   static SA_HD V one_mul(V b) { return add(sgn(b), b); }  // 1 ⊙ b
-  static SA_HD V mj_mul(V b) {                            // (−j) ⊙ b
-    float lo, hi;
-    unpack(add(sgn(b), b), lo, hi);
-    return pack(hi, -lo);
+  static SA_HD V mj_mul(V b) {                            // (−j) ⊙ b = {u.hi, −u.lo}
+    return neg_hi(swap(add(sgn(b), b)));
   }
 };
 
