@@ -59,13 +59,14 @@ int sa_twiddle_create(int device, int dtype, int64_t n, const double *host_table
   int prev = 0;
   SA_CUDA_TRY(cudaGetDevice(&prev));
   SA_CUDA_TRY(cudaSetDevice(device));
-  SaTwiddles *tw = new SaTwiddles{dtype, n, device, nullptr, nullptr, nullptr};
+  SaTwiddles *tw = new SaTwiddles{dtype, n, device, nullptr, nullptr, nullptr, nullptr};
   int rc = sa_twiddles_build(tw, host_table, (cudaStream_t)stream);
   cudaSetDevice(prev);
   if (rc != SA_OK) {
     cudaFree(tw->raw);
     cudaFree(tw->quad);
     cudaFree(tw->stage);
+    cudaFree(tw->stage2);
     delete tw;
     return rc;
   }
@@ -82,6 +83,7 @@ int sa_twiddle_destroy(void *handle) {
   cudaFree(tw->raw);
   cudaFree(tw->quad);
   cudaFree(tw->stage);
+  cudaFree(tw->stage2);
   cudaSetDevice(prev);
   delete tw;
   return SA_OK;

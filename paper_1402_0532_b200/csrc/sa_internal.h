@@ -16,6 +16,7 @@ struct SaTwiddles {
   void *quad;   // n x {wr, wi, sgn wr, sgn wi}                      (NDFT)
   void *stage;  // (n-1) x {|wr|, |wi|, sgn wr, sgn wi}, stage-packed:
                 //   stage s (1..log2 n) at offset 2^(s-1)-1, entry j = table[j*n/2^s]
+  void *stage2; // (n-1) x {wr, wi}, same stage-packed order (8/16-byte entries)
 };
 
 void sa_set_error(const char *fmt, ...);

@@ -20,6 +20,7 @@
 // L2 latency is covered by the others' arithmetic (16 warps/SM for c64).
 // HBM traffic = one read + one write of the signal.
 #include <algorithm>
+#include <cstdlib>
 #include <cooperative_groups.h>
 #include <cudaTypedefs.h>
 
@@ -58,7 +59,7 @@ template <typename T> struct L64 {
   static constexpr size_t WORK = sizeof(C2) * 256 * TC;  // one tile
   static constexpr size_t TWA = sizeof(C4) * 255;
   static constexpr size_t MBAR_OFF = INTER + NG * WORK + TWA;
-  static constexpr size_t SMEM = MBAR_OFF + 8 * (NG + 1);
+  static constexpr size_t SMEM = MBAR_OFF + 8 * (NG + 2);
   static constexpr int EW = sizeof(C2) / 8;  // 8-byte TMA elements per complex
   static_assert(TILES % NG == 0, "tiles must split evenly over groups");
 };
@@ -76,8 +77,8 @@ template <typename T> struct Ctx {
   using P = L64<T>;
   typename P::C2 *inter, *work;
   typename P::C4 *twA;
-  uint64_t *tma_bar, *full_bar;
-  uint32_t inter_rank[P::CL], full_rank[P::CL];
+  uint64_t *tma_bar, *full_bar, *empty_bar;
+  uint32_t inter_rank[P::CL], full_rank[P::CL], empty_rank[P::CL];
   int rank, gi, gt;
   int64_t cid, ncl;
 };
@@ -91,6 +92,7 @@ SA_HD void ctx_init(Ctx<T> &c, unsigned char *smem_raw, const typename L64<T>::C
   c.twA = reinterpret_cast<typename P::C4 *>(smem_raw + P::INTER + P::NG * P::WORK);
   c.tma_bar = reinterpret_cast<uint64_t *>(smem_raw + P::MBAR_OFF);
   c.full_bar = c.tma_bar + P::NG;
+  c.empty_bar = c.full_bar + 1;
   c.rank = (int)cluster.block_rank();
   c.cid = blockIdx.x / P::CL;
   c.ncl = gridDim.x / P::CL;
@@ -99,7 +101,8 @@ SA_HD void ctx_init(Ctx<T> &c, unsigned char *smem_raw, const typename L64<T>::C
   for (int e = threadIdx.x; e < 255; e += P::THREADS) c.twA[e] = stage[e];  // global stages 1..8
   if (threadIdx.x == 0) {
     for (int g = 0; g < P::NG; ++g) sa_mbar_init(&c.tma_bar[g], 1);
-    sa_mbar_init(c.full_bar, 1);  // expect_tx(INTER) once per signal
+    sa_mbar_init(c.full_bar, 1);        // expect_tx(INTER) once per signal
+    sa_mbar_init(c.empty_bar, P::CL);   // one remote arrive per peer per signal
     sa_fence_mbar_init();
   }
   __syncthreads();
@@ -108,7 +111,18 @@ SA_HD void ctx_init(Ctx<T> &c, unsigned char *smem_raw, const typename L64<T>::C
   for (int r = 0; r < P::CL; ++r) {
     c.inter_rank[r] = sa_mapa(sa_smem_u32(c.inter), r);
     c.full_rank[r] = sa_mapa(sa_smem_u32(c.full_bar), r);
+    c.empty_rank[r] = sa_mapa(sa_smem_u32(c.empty_bar), r);
   }
+}
+
+// "my node storage may be overwritten": all threads of the CTA finished reading
+// it (bar.sync 0), then one thread arrives on every peer's empty barrier.
+template <typename T> SA_HD void release_storage(const Ctx<T> &c) {
+  using P = L64<T>;
+  __syncthreads();
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int r = 0; r < P::CL; ++r) sa_mbar_arrive_remote(c.empty_rank[r]);
 }
 
 // group-leader TMA of tile tt (TC columns x 256 rows) of signal sig into the group buffer
@@ -123,11 +137,32 @@ SA_HD void tma_tile(const Ctx<T> &c, const CUtensorMap *tmx, int64_t sig, int tt
   }
 }
 
+// Twiddles of the 8 cross-row stages (global 9..16) for node column q, as raw
+// (wr, wi): wf[h-1+a] = table_s[a*256 + q] (stages 9..12, t = 1..4) and
+// wf[15 + hr-1+a] = table_s[(g+16a)*256 + q] (stages 13..16, t = 5..8).  Every
+// one has wr != 0 and wi < 0 unless q is 0 or 128 (j == 0 or j == h/2), so warps
+// away from those two columns use the FMUL-free product (sa_regs.cuh).
+template <typename T>
+SA_HD void load_wf(typename Ar<T>::C2 (&wf)[30], const typename Ar<T>::C2 *__restrict__ stage2,
+                   int q, int g) {
+#pragma unroll
+  for (int t = 1; t <= 4; ++t)
+#pragma unroll
+    for (int a = 0; a < (1 << (t - 1)); ++a)
+      wf[(1 << (t - 1)) - 1 + a] = sa_ldg(&stage2[(1 << (7 + t)) - 1 + a * 256 + q]);
+#pragma unroll
+  for (int t = 5; t <= 8; ++t)
+#pragma unroll
+    for (int a = 0; a < (1 << (t - 5)); ++a)
+      wf[15 + (1 << (t - 5)) - 1 + a] = sa_ldg(&stage2[(1 << (7 + t)) - 1 + (g + 16 * a) * 256 + q]);
+}
+SA_HD bool special_column(int q) { return __any_sync(0xffffffffu, q == 0 || q == 128); }
+
 template <typename T>
 __global__ void __launch_bounds__(L64<T>::THREADS, 1)
     k_nlfft64k_dit(const __grid_constant__ CUtensorMap tmx, typename Ar<T>::C2 *__restrict__ y,
-                   int64_t batch, const typename Ar<T>::C4 *__restrict__ stage, T gain,
-                   int use_gain) {
+                   int64_t batch, const typename Ar<T>::C4 *__restrict__ stage,
+                   const typename Ar<T>::C2 *__restrict__ stage2, T gain, int use_gain, int probe) {
   using P = L64<T>;
   using A = Ar<T>;
   using V = typename A::V;
@@ -146,7 +181,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
   uint32_t tile_it = 0;  // this group's TMA uses (parity)
   uint32_t sig_it = 0;
   if (c.cid < batch) tma_tile<T>(c, &tmx, c.cid, c.gi);
-  sa_cluster_arrive_relaxed();  // node storage free for the first signal
+  release_storage<T>(c);  // node storage free for the first signal
 
   for (int64_t sig = c.cid; sig < batch; sig += c.ncl, ++sig_it) {
     if (threadIdx.x == 0) sa_mbar_expect_tx(c.full_bar, (uint32_t)P::INTER);
@@ -162,6 +197,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
           V x = A::from(wk[(crev4(k) * 16 + rg) * TC + m1_cc]);
           v[k] = use_gain ? A::scale(x, gain) : x;
         }
+        if (!(probe & 1)) {
 #pragma unroll
         for (int k = 0; k < 16; k += 2) r_two_point<T>(v[k], v[k + 1]);  // stage 1
 #pragma unroll
@@ -184,6 +220,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
           else if (k == 4) r_dit_mj<T>(v[k], v[k + 8]);
           else r_dit<T>(v[k], v[k + 8], twA[7 + k]);
         }
+        }
       }
       group_sync(gbar, GT);
 #pragma unroll
@@ -196,6 +233,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
       group_sync(gbar, GT);  // tile buffer consumed: re-arm it
       if (u + 1 < TPG) tma_tile<T>(c, &tmx, sig, tt + NG);
       else if (sig + c.ncl < batch) tma_tile<T>(c, &tmx, sig + c.ncl, c.gi);
+      if (!(probe & 1)) {
 #pragma unroll
       for (int t = 5; t <= 8; ++t) {
         const int hr = 1 << (t - 5), h = 1 << (t - 1);
@@ -203,65 +241,87 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
         for (int k = 0; k < 16; ++k)
           if (!(k & hr)) r_dit<T>(v[k], v[k + hr], twA[(h - 1) + m2_g + 16 * (k & (hr - 1))]);
       }
+      }
       // scatter node row R = rev8(c): column q lives in CTA q / COLS (st.async credits its mbarrier)
-      if (u == 0) sa_cluster_wait();  // peers finished reading their storage (previous signal)
+      if (u == 0) sa_mbar_wait(c.empty_bar, sig_it & 1);  // peers finished reading (previous signal)
       {
         const int cc = c.rank * COLS + tt * TC + m2_cc;
         const int R = rev8(cc);
         constexpr int KPC = COLS / 16;  // registers per owner CTA
 #pragma unroll
         for (int k = 0; k < 16; ++k)
-          sa_st_async(c.inter_rank[k / KPC] + (uint32_t)(sizeof(C2) * (R * COLS + m2_g + 16 * (k % KPC))),
-                      A::to(v[k]), c.full_rank[k / KPC]);
+          sa_st_async(c.inter_rank[(probe & 4) ? c.rank : k / KPC] + (uint32_t)(sizeof(C2) * (R * COLS + m2_g + 16 * (k % KPC))),
+                      A::to(v[k]), c.full_rank[(probe & 4) ? c.rank : k / KPC]);
       }
     }
     // ------------------------------------------------------------- phase B
     C2 *ysig = y + sig * NN;
-    C4 w[15];
-    sa_mbar_wait_cluster(c.full_bar, sig_it & 1);  // all INTER bytes of this signal landed
+    C2 wf[30];
+    {
+      const int q0 = c.rank * COLS + c.gi * TC + m1_cc;  // independent of the node storage
+      if (!special_column(q0)) load_wf<T>(wf, stage2, q0, m1_g);
+    }
+    sa_mbar_wait(c.full_bar, sig_it & 1);  // all INTER bytes of this signal landed
     for (int u = 0; u < TPG; ++u) {
       const int tt = c.gi + NG * u;
       const int lq = tt * TC + m1_cc;
       const int q = c.rank * COLS + lq;
-#pragma unroll
-      for (int t = 1; t <= 4; ++t)  // stages 9..12: w[h-1+a] = stage[off + a*256 + q]
-#pragma unroll
-        for (int a = 0; a < (1 << (t - 1)); ++a)
-          w[(1 << (t - 1)) - 1 + a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + a * 256 + q]);
+      const bool gen = special_column(q);
+      if (u > 0 && !gen) load_wf<T>(wf, stage2, q, m1_g);
       V v[16];
 #pragma unroll
       for (int k = 0; k < 16; ++k) v[k] = A::from(c.inter[(m1_g * 16 + k) * COLS + lq]);
+      if (gen) {  // columns 0 / 128: general twiddles (zero components), loaded per stage
 #pragma unroll
-      for (int t = 1; t <= 4; ++t) {  // R bits 0..3
-        const int h = 1 << (t - 1);
+        for (int t = 1; t <= 4; ++t) {  // R bits 0..3
+          const int h = 1 << (t - 1);
+          C4 w[8];
 #pragma unroll
-        for (int k = 0; k < 16; ++k)
-          if (!(k & h)) r_dit<T>(v[k], v[k + h], w[h - 1 + (k & (h - 1))]);
+          for (int a = 0; a < h; ++a) w[a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + a * 256 + q]);
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            if (!(k & h)) r_dit<T>(v[k], v[k + h], w[k & (h - 1)]);
+        }
+      } else if (!(probe & 2)) {
+#pragma unroll
+        for (int t = 1; t <= 4; ++t) {
+          const int h = 1 << (t - 1);
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            if (!(k & h)) r_dit_fast<T>(v[k], v[k + h], wf[h - 1 + (k & (h - 1))]);
+        }
       }
-#pragma unroll
-      for (int t = 5; t <= 8; ++t)  // stages 13..16: w[hr-1+a] = stage[off + (g+16a)*256 + q]
-#pragma unroll
-        for (int a = 0; a < (1 << (t - 5)); ++a)
-          w[(1 << (t - 5)) - 1 + a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + (m1_g + 16 * a) * 256 + q]);
 #pragma unroll
       for (int k = 0; k < 16; ++k) c.inter[(m1_g * 16 + k) * COLS + lq] = A::to(v[k]);
       group_sync(gbar, GT);
 #pragma unroll
       for (int k = 0; k < 16; ++k) v[k] = A::from(c.inter[(m1_g + 16 * k) * COLS + lq]);
+      if (gen) {
 #pragma unroll
-      for (int t = 5; t <= 8; ++t) {  // R bits 4..7
-        const int hr = 1 << (t - 5);
+        for (int t = 5; t <= 8; ++t) {  // R bits 4..7
+          const int hr = 1 << (t - 5);
+          C4 w[8];
 #pragma unroll
-        for (int k = 0; k < 16; ++k)
-          if (!(k & hr)) r_dit<T>(v[k], v[k + hr], w[hr - 1 + (k & (hr - 1))]);
+          for (int a = 0; a < hr; ++a)
+            w[a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + (m1_g + 16 * a) * 256 + q]);
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            if (!(k & hr)) r_dit<T>(v[k], v[k + hr], w[k & (hr - 1)]);
+        }
+      } else if (!(probe & 2)) {
+#pragma unroll
+        for (int t = 5; t <= 8; ++t) {
+          const int hr = 1 << (t - 5);
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            if (!(k & hr)) r_dit_fast<T>(v[k], v[k + hr], wf[15 + hr - 1 + (k & (hr - 1))]);
+        }
       }
 #pragma unroll
       for (int k = 0; k < 16; ++k) __stcs(&ysig[(m1_g + 16 * k) * 256 + q], A::to(v[k]));
     }
-    // every node-storage value this thread loaded was consumed by the stores above
-    sa_cluster_arrive_relaxed();
+    if (sig + c.ncl < batch) release_storage<T>(c);
   }
-  sa_cluster_wait();  // pairs the last arrive
 }
 
 // DIF (DESIGN.md convention): stages s = 16..2 with top = a + b, bot = W ⊙ (a − b),
@@ -274,8 +334,8 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
 template <typename T>
 __global__ void __launch_bounds__(L64<T>::THREADS, 1)
     k_nlfft64k_dif(const __grid_constant__ CUtensorMap tmx, typename Ar<T>::C2 *__restrict__ y,
-                   int64_t batch, const typename Ar<T>::C4 *__restrict__ stage, T gain,
-                   int use_gain) {
+                   int64_t batch, const typename Ar<T>::C4 *__restrict__ stage,
+                   const typename Ar<T>::C2 *__restrict__ stage2, T gain, int use_gain, int probe) {
   using P = L64<T>;
   using A = Ar<T>;
   using V = typename A::V;
@@ -294,7 +354,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
 
   uint32_t tile_it = 0, sig_it = 0;
   if (c.cid < batch) tma_tile<T>(c, &tmx, c.cid, c.gi);
-  sa_cluster_arrive_relaxed();
+  release_storage<T>(c);
 
   for (int64_t sig = c.cid; sig < batch; sig += c.ncl, ++sig_it) {
     if (threadIdx.x == 0) sa_mbar_expect_tx(c.full_bar, (uint32_t)P::INTER);
@@ -302,12 +362,9 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
     for (int u = 0; u < TPG; ++u, ++tile_it) {
       const int tt = c.gi + NG * u;
       const int q = c.rank * COLS + tt * TC + m1_cc;
-      C4 w[15];
-#pragma unroll
-      for (int t = 5; t <= 8; ++t)  // stages 16..13: w[hr-1+a] = stage[off + (g+16a)*256 + q]
-#pragma unroll
-        for (int a = 0; a < (1 << (t - 5)); ++a)
-          w[(1 << (t - 5)) - 1 + a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + (m1_g + 16 * a) * 256 + q]);
+      const bool gen = special_column(q);
+      C2 wf[30];
+      if (!gen) load_wf<T>(wf, stage2, q, m1_g);
       sa_mbar_wait(&c.tma_bar[c.gi], tile_it & 1);
       V v[16];
 #pragma unroll
@@ -315,18 +372,27 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
         V x = A::from(wk[(m1_g + 16 * k) * TC + m1_cc]);
         v[k] = use_gain ? A::scale(x, gain) : x;
       }
+      if (gen) {  // columns 0 / 128: general twiddles, loaded per stage
 #pragma unroll
-      for (int t = 8; t >= 5; --t) {  // R bits 7..4
-        const int hr = 1 << (t - 5);
+        for (int t = 8; t >= 5; --t) {  // R bits 7..4
+          const int hr = 1 << (t - 5);
+          C4 w[8];
 #pragma unroll
-        for (int k = 0; k < 16; ++k)
-          if (!(k & hr)) r_dif<T>(v[k], v[k + hr], w[hr - 1 + (k & (hr - 1))]);
+          for (int a = 0; a < hr; ++a)
+            w[a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + (m1_g + 16 * a) * 256 + q]);
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            if (!(k & hr)) r_dif<T>(v[k], v[k + hr], w[k & (hr - 1)]);
+        }
+      } else {
+#pragma unroll
+        for (int t = 8; t >= 5; --t) {
+          const int hr = 1 << (t - 5);
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            if (!(k & hr)) r_dif_fast<T>(v[k], v[k + hr], wf[15 + hr - 1 + (k & (hr - 1))]);
+        }
       }
-#pragma unroll
-      for (int t = 1; t <= 4; ++t)  // stages 12..9: w[h-1+a] = stage[off + a*256 + q]
-#pragma unroll
-        for (int a = 0; a < (1 << (t - 1)); ++a)
-          w[(1 << (t - 1)) - 1 + a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + a * 256 + q]);
 #pragma unroll
       for (int k = 0; k < 16; ++k) wk[(m1_g + 16 * k) * TC + m1_cc] = A::to(v[k]);
       group_sync(gbar, GT);
@@ -335,14 +401,27 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
       group_sync(gbar, GT);  // tile buffer consumed: re-arm it
       if (u + 1 < TPG) tma_tile<T>(c, &tmx, sig, tt + NG);
       else if (sig + c.ncl < batch) tma_tile<T>(c, &tmx, sig + c.ncl, c.gi);
+      if (gen) {
 #pragma unroll
-      for (int t = 4; t >= 1; --t) {  // R bits 3..0
-        const int h = 1 << (t - 1);
+        for (int t = 4; t >= 1; --t) {  // R bits 3..0
+          const int h = 1 << (t - 1);
+          C4 w[8];
 #pragma unroll
-        for (int k = 0; k < 16; ++k)
-          if (!(k & h)) r_dif<T>(v[k], v[k + h], w[h - 1 + (k & (h - 1))]);
+          for (int a = 0; a < h; ++a) w[a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + a * 256 + q]);
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            if (!(k & h)) r_dif<T>(v[k], v[k + h], w[k & (h - 1)]);
+        }
+      } else {
+#pragma unroll
+        for (int t = 4; t >= 1; --t) {
+          const int h = 1 << (t - 1);
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            if (!(k & h)) r_dif_fast<T>(v[k], v[k + h], wf[h - 1 + (k & (h - 1))]);
+        }
       }
-      if (u == 0) sa_cluster_wait();
+      if (u == 0) sa_mbar_wait(c.empty_bar, sig_it & 1);
 #pragma unroll
       for (int k = 0; k < 16; ++k) {  // row R = 16g + k -> CTA owning cr = rev8(R), local row cr mod COLS
         const int cr = crev4(k) * 16 + rg1;
@@ -351,7 +430,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
                     A::to(v[k]), c.full_rank[cr / COLS]);
       }
     }
-    sa_mbar_wait_cluster(c.full_bar, sig_it & 1);
+    sa_mbar_wait(c.full_bar, sig_it & 1);
     // ------------------------------------------------------------- phase 2
     C2 *ysig = y + sig * NN;
     for (int u = 0; u < TPG; ++u) {
@@ -408,9 +487,8 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
         for (int k = 0; k < 16; ++k) __stcs(&ysig[(crev4(k) * 16 + rg) * 256 + cr], A::to(v[k]));
       }
     }
-    sa_cluster_arrive_relaxed();
+    if (sig + c.ncl < batch) release_storage<T>(c);
   }
-  sa_cluster_wait();
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -423,6 +501,17 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
       fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
   }
   return fn;
+}
+
+// experiment hook (not part of the ABI): SA_NLFFT64K_PROBE bitmask skips work
+// to time the kernel skeleton; 0 (default) = normal operation.
+int probe_flags() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("SA_NLFFT64K_PROBE");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
 }
 
 template <typename T>
@@ -469,7 +558,9 @@ int launch64k(int variant, const void *x, void *y, int64_t batch, const SaTwiddl
   int64_t ncl = std::min<int64_t>(batch, max_clusters);
   cfg.gridDim = dim3((unsigned)(ncl * P::CL));
   SA_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, map, (typename P::C2 *)y, batch,
-                                 (const typename P::C4 *)tw->stage, (T)gain, (int)(gain != 1.0)));
+                                 (const typename P::C4 *)tw->stage,
+                                 (const typename P::C2 *)tw->stage2, (T)gain, (int)(gain != 1.0),
+                                 probe_flags()));
   return SA_OK;
 }
 

@@ -82,6 +82,17 @@ template <> struct Ar<float> {
     V tq = mul(pack(-w.w, -w.w), q2);                    // {−tP2, −tP3}
     return fma(pack(w.z, w.z), q1, neg_hi(tq));          // {sP1 − tP2, sP4 + tP3}
   }
+  // w ⊙ b for a twiddle with wr != 0 and wi < 0 (every stage j except 0 and
+  // h/2): sgn wi = −1 and sgn wr = ±1 come from the raw value, no FMUL2.
+  //   rr = σP1 + P2 ; ri = σP4 − P3
+  static SA_HD V twmul_fast(const C2 &w, V b) {
+    V sb = sgn(b);
+    const float A = fabsf(w.x), B = fabsf(w.y);
+    const float s = __int_as_float((__float_as_int(w.x) & 0x80000000) | 0x3f800000);
+    V q1 = fma(sb, pack(A, A), b);              // {P1, P4}
+    V q2 = fma(swap(sb), pack(B, B), swap(b));  // {P2, P3}
+    return fma(pack(s, s), q1, neg_hi(q2));     // {σP1 + P2, σP4 − P3}
+  }
   static SA_HD V one_mul(V b) { return add(sgn(b), b); }  // 1 ⊙ b
   static SA_HD V mj_mul(V b) {                            // (−j) ⊙ b = {u.hi, −u.lo}
     return neg_hi(swap(add(sgn(b), b)));
@@ -102,6 +113,13 @@ template <> struct Ar<double> {
     sa_tw_mul<double>(w.x, w.y, w.z, w.w, b.x, b.y, r.x, r.y);
     return r;
   }
+  static SA_HD V twmul_fast(const C2 &w, V b) {  // wr != 0, wi < 0
+    const double sbr = sa_sgn(b.x), sbi = sa_sgn(b.y);
+    const double A = fabs(w.x), B = fabs(w.y), s = w.x < 0.0 ? -1.0 : 1.0;
+    const double p1 = sa_fma(sbr, A, b.x), p4 = sa_fma(sbi, A, b.y);
+    const double p2 = sa_fma(sbi, B, b.y), p3 = sa_fma(sbr, B, b.x);
+    return {sa_fma(s, p1, p2), sa_fma(s, p4, -p3)};
+  }
   static SA_HD V one_mul(V b) { return {sa_fma(sa_sgn(b.x), 1.0, b.x), sa_fma(sa_sgn(b.y), 1.0, b.y)}; }
   static SA_HD V mj_mul(V b) {
     V u = one_mul(b);
@@ -115,6 +133,18 @@ template <typename T> SA_HD void r_dit(typename Ar<T>::V &a, typename Ar<T>::V &
   auto t = Ar<T>::twmul(w, b);
   b = Ar<T>::sub(a, t);
   a = Ar<T>::add(a, t);
+}
+template <typename T> SA_HD void r_dit_fast(typename Ar<T>::V &a, typename Ar<T>::V &b,
+                                            const typename Ar<T>::C2 &w) {
+  auto t = Ar<T>::twmul_fast(w, b);
+  b = Ar<T>::sub(a, t);
+  a = Ar<T>::add(a, t);
+}
+template <typename T> SA_HD void r_dif_fast(typename Ar<T>::V &a, typename Ar<T>::V &b,
+                                            const typename Ar<T>::C2 &w) {
+  auto d = Ar<T>::sub(a, b);
+  a = Ar<T>::add(a, b);
+  b = Ar<T>::twmul_fast(w, d);
 }
 template <typename T> SA_HD void r_dit_one(typename Ar<T>::V &a, typename Ar<T>::V &b) {
   auto t = Ar<T>::one_mul(b);
@@ -218,4 +248,11 @@ SA_HD void sa_mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
       " @!p bra SA_WAITC_%=;\n}\n" ::"r"(sa_smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+// remote arrive on a peer CTA's mbarrier (address from sa_mapa).  Relaxed:
+// used only to say "my reads of the storage you write into are complete".
+SA_HD void sa_mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
 }

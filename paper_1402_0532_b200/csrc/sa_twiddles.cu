@@ -19,13 +19,14 @@ __global__ void k_tw_raw_quad(const double2 *__restrict__ host_tab, int64_t n,
 // value table[j * n / 2^s]  (transforms.py:295: entries[arange(h) * (n // m)])
 template <typename T>
 __global__ void k_tw_stage(const typename SaVec<T>::c2 *__restrict__ raw, int64_t n,
-                           typename SaVec<T>::c4 *stage) {
+                           typename SaVec<T>::c4 *stage, typename SaVec<T>::c2 *stage2) {
   int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n - 1) return;
   int s = 63 - __clzll(e + 1) + 1;
   int64_t j = e + 1 - (1LL << (s - 1));
   auto w = raw[j * (n >> s)];
   stage[e] = {fabs(w.x), fabs(w.y), sa_sgn_np(w.x), sa_sgn_np(w.y)};
+  stage2[e] = w;
 }
 
 int sa_twiddles_build(SaTwiddles *tw, const double *host_table, cudaStream_t s) {
@@ -39,15 +40,19 @@ int sa_twiddles_build(SaTwiddles *tw, const double *host_table, cudaStream_t s) 
   SA_CUDA_TRY(cudaMalloc(&tw->raw, c2 * n));
   SA_CUDA_TRY(cudaMalloc(&tw->quad, c4 * n));
   tw->stage = nullptr;
+  tw->stage2 = nullptr;
   if (pow2) SA_CUDA_TRY(cudaMalloc(&tw->stage, c4 * (n - 1)));
+  if (pow2) SA_CUDA_TRY(cudaMalloc(&tw->stage2, c2 * (n - 1)));
   int g = (int)((n + 255) / 256);
   if (tw->dtype == SA_C64) {
     k_tw_raw_quad<float><<<g, 256, 0, s>>>(d_host, n, (float2 *)tw->raw, (float4 *)tw->quad);
-    if (pow2) k_tw_stage<float><<<g, 256, 0, s>>>((const float2 *)tw->raw, n, (float4 *)tw->stage);
+    if (pow2) k_tw_stage<float><<<g, 256, 0, s>>>((const float2 *)tw->raw, n, (float4 *)tw->stage,
+                                                  (float2 *)tw->stage2);
   } else {
     k_tw_raw_quad<double><<<g, 256, 0, s>>>(d_host, n, (double2 *)tw->raw, (double4 *)tw->quad);
     if (pow2)
-      k_tw_stage<double><<<g, 256, 0, s>>>((const double2 *)tw->raw, n, (double4 *)tw->stage);
+      k_tw_stage<double><<<g, 256, 0, s>>>((const double2 *)tw->raw, n, (double4 *)tw->stage,
+                                                   (double2 *)tw->stage2);
   }
   SA_LAUNCH_CHECK();
   SA_CUDA_TRY(cudaFreeAsync(d_host, s));
