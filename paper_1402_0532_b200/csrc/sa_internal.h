@@ -62,6 +62,10 @@ int sa_launch_nlfft(int dtype, int variant, const void *x, void *y, int64_t batc
 int sa_launch_nlfft64k(int dtype, int variant, const void *x, void *y, int64_t batch, int64_t n,
                        const SaTwiddles *tw, double gain, cudaStream_t s);
 
+// sa_nlfft2p.cu (persistent work-queue two-pass N = 2^16, DIT, out of place)
+int sa_launch_nlfft2p(int dtype, int variant, const void *x, void *y, int64_t batch, int64_t n,
+                      const SaTwiddles *tw, double gain, cudaStream_t s);
+
 // sa_ambiguity.cu
 int64_t sa_ambiguity_ws_bytes(int dtype, int64_t l_count, int64_t m);
 int sa_launch_lag_product(int dtype, const void *surv, const void *ref, int64_t n, int64_t ref_len,

@@ -17,6 +17,7 @@
 //               each column q, twiddle j = (R mod 2^(t-1))*N2 + q.
 // DIF runs the mirror image (cols first, then rows + bit-reversed store).
 #include <algorithm>
+#include <cstdlib>
 
 #include "sa_common.cuh"
 #include "sa_internal.h"
@@ -273,8 +274,18 @@ int launch(int variant, const void *xv, void *yv, int64_t batch, int64_t n, cons
     return SA_OK;
   }
   {
-    int rc = sa_launch_nlfft64k(sizeof(T) == 4 ? SA_C64 : SA_C128, variant, xv, yv, batch, n, tw,
-                                gain, s);
+    // N = 2^16: persistent work-queue kernel (out of place) or the cluster kernel
+    // default: cluster kernel (measured faster); SA_NLFFT_IMPL=2p selects the
+    // persistent work-queue kernel (out of place, DIT) for comparison.
+    static int impl = -1;
+    if (impl < 0) {
+      const char *e = getenv("SA_NLFFT_IMPL");
+      impl = (e && e[0] == '2') ? 0 : 1;
+    }
+    const int d = sizeof(T) == 4 ? SA_C64 : SA_C128;
+    int rc = SA_ERR_UNSUPPORTED;
+    if (impl == 0) rc = sa_launch_nlfft2p(d, variant, xv, yv, batch, n, tw, gain, s);
+    if (rc == SA_ERR_UNSUPPORTED) rc = sa_launch_nlfft64k(d, variant, xv, yv, batch, n, tw, gain, s);
     if (rc != SA_ERR_UNSUPPORTED) return rc;
   }
   if (x == y) {

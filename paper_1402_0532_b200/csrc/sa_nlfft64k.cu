@@ -20,7 +20,6 @@
 // L2 latency is covered by the others' arithmetic (16 warps/SM for c64).
 // HBM traffic = one read + one write of the signal.
 #include <algorithm>
-#include <cstdlib>
 #include <cooperative_groups.h>
 #include <cudaTypedefs.h>
 
@@ -35,33 +34,41 @@ constexpr int LOGN = 16;
 constexpr int NN = 1 << LOGN;
 
 template <typename T> struct K64;
+// SPLIT = true : the NG groups share one signal's tiles (one node storage);
+// SPLIT = false: each group owns its own signal stream and node storage, so one
+//                group's phase A overlaps the other's phase B.
 template <> struct K64<float> {
   static constexpr int TC = 16;  // columns per tile
   static constexpr int CL = 4;   // cluster size
   static constexpr int NG = 2;   // thread groups per CTA
+  static constexpr bool SPLIT = true;
 };
 template <> struct K64<double> {
   static constexpr int TC = 8;
   static constexpr int CL = 8;
   static constexpr int NG = 2;
+  static constexpr bool SPLIT = true;
 };
 
 template <typename T> struct L64 {
   static constexpr int TC = K64<T>::TC, CL = K64<T>::CL, NG = K64<T>::NG;
+  static constexpr bool SPLIT = K64<T>::SPLIT;
+  static constexpr int NS = SPLIT ? 1 : NG;   // node storages per CTA
   static constexpr int GT = 16 * TC;          // threads per group
   static constexpr int THREADS = NG * GT;
   static constexpr int COLS = 256 / CL;       // node columns owned per CTA
   static constexpr int TILES = COLS / TC;     // tiles per CTA per phase
-  static constexpr int TPG = TILES / NG;      // tiles per group per phase
+  static constexpr int TPG = SPLIT ? TILES / NG : TILES;  // tiles per group per phase
   using C2 = typename Ar<T>::C2;
   using C4 = typename Ar<T>::C4;
-  static constexpr size_t INTER = sizeof(C2) * 256 * COLS;
+  static constexpr size_t INTER1 = sizeof(C2) * 256 * COLS;  // one signal's share
+  static constexpr size_t INTER = NS * INTER1;
   static constexpr size_t WORK = sizeof(C2) * 256 * TC;  // one tile
   static constexpr size_t TWA = sizeof(C4) * 255;
   static constexpr size_t MBAR_OFF = INTER + NG * WORK + TWA;
-  static constexpr size_t SMEM = MBAR_OFF + 8 * (NG + 2);
+  static constexpr size_t SMEM = MBAR_OFF + 8 * (NG + 2 * NS);
   static constexpr int EW = sizeof(C2) / 8;  // 8-byte TMA elements per complex
-  static_assert(TILES % NG == 0, "tiles must split evenly over groups");
+  static_assert(!SPLIT || TILES % NG == 0, "tiles must split evenly over groups");
 };
 
 SA_HD int rev4(int v) { return (int)(__brev((unsigned)v) >> 28); }
@@ -87,22 +94,26 @@ template <typename T>
 SA_HD void ctx_init(Ctx<T> &c, unsigned char *smem_raw, const typename L64<T>::C4 *stage) {
   using P = L64<T>;
   cg::cluster_group cluster = cg::this_cluster();
-  c.inter = reinterpret_cast<typename P::C2 *>(smem_raw);
+  c.gi = threadIdx.x / P::GT;
+  const int st = P::SPLIT ? 0 : c.gi;  // this group's node storage
+  c.inter = reinterpret_cast<typename P::C2 *>(smem_raw + st * P::INTER1);
   c.work = reinterpret_cast<typename P::C2 *>(smem_raw + P::INTER);
   c.twA = reinterpret_cast<typename P::C4 *>(smem_raw + P::INTER + P::NG * P::WORK);
   c.tma_bar = reinterpret_cast<uint64_t *>(smem_raw + P::MBAR_OFF);
-  c.full_bar = c.tma_bar + P::NG;
-  c.empty_bar = c.full_bar + 1;
+  uint64_t *full0 = c.tma_bar + P::NG, *empty0 = full0 + P::NS;
+  c.full_bar = full0 + st;
+  c.empty_bar = empty0 + st;
   c.rank = (int)cluster.block_rank();
   c.cid = blockIdx.x / P::CL;
   c.ncl = gridDim.x / P::CL;
-  c.gi = threadIdx.x / P::GT;
   c.gt = threadIdx.x % P::GT;
   for (int e = threadIdx.x; e < 255; e += P::THREADS) c.twA[e] = stage[e];  // global stages 1..8
   if (threadIdx.x == 0) {
     for (int g = 0; g < P::NG; ++g) sa_mbar_init(&c.tma_bar[g], 1);
-    sa_mbar_init(c.full_bar, 1);        // expect_tx(INTER) once per signal
-    sa_mbar_init(c.empty_bar, P::CL);   // one remote arrive per peer per signal
+    for (int g = 0; g < P::NS; ++g) {
+      sa_mbar_init(&full0[g], 1);       // expect_tx(INTER1) once per signal
+      sa_mbar_init(&empty0[g], P::CL);  // one remote arrive per peer per signal
+    }
     sa_fence_mbar_init();
   }
   __syncthreads();
@@ -119,10 +130,14 @@ SA_HD void ctx_init(Ctx<T> &c, unsigned char *smem_raw, const typename L64<T>::C
 // it (bar.sync 0), then one thread arrives on every peer's empty barrier.
 template <typename T> SA_HD void release_storage(const Ctx<T> &c) {
   using P = L64<T>;
-  __syncthreads();
-  if (threadIdx.x == 0)
+  if (P::SPLIT) __syncthreads();
+  else group_sync(1 + c.gi, P::GT);
+  if (P::SPLIT ? threadIdx.x == 0 : c.gt == 0)
 #pragma unroll
     for (int r = 0; r < P::CL; ++r) sa_mbar_arrive_remote(c.empty_rank[r]);
+}
+template <typename T> SA_HD bool storage_leader(const Ctx<T> &c) {
+  return L64<T>::SPLIT ? threadIdx.x == 0 : c.gt == 0;
 }
 
 // group-leader TMA of tile tt (TC columns x 256 rows) of signal sig into the group buffer
@@ -162,7 +177,7 @@ template <typename T>
 __global__ void __launch_bounds__(L64<T>::THREADS, 1)
     k_nlfft64k_dit(const __grid_constant__ CUtensorMap tmx, typename Ar<T>::C2 *__restrict__ y,
                    int64_t batch, const typename Ar<T>::C4 *__restrict__ stage,
-                   const typename Ar<T>::C2 *__restrict__ stage2, T gain, int use_gain, int probe) {
+                   const typename Ar<T>::C2 *__restrict__ stage2, T gain, int use_gain) {
   using P = L64<T>;
   using A = Ar<T>;
   using V = typename A::V;
@@ -180,14 +195,17 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
 
   uint32_t tile_it = 0;  // this group's TMA uses (parity)
   uint32_t sig_it = 0;
-  if (c.cid < batch) tma_tile<T>(c, &tmx, c.cid, c.gi);
+  if ((P::SPLIT ? c.cid : c.cid * NG + c.gi) < batch)
+    tma_tile<T>(c, &tmx, P::SPLIT ? c.cid : c.cid * NG + c.gi, P::SPLIT ? c.gi : 0);
   release_storage<T>(c);  // node storage free for the first signal
 
-  for (int64_t sig = c.cid; sig < batch; sig += c.ncl, ++sig_it) {
-    if (threadIdx.x == 0) sa_mbar_expect_tx(c.full_bar, (uint32_t)P::INTER);
+  const int64_t sig0 = P::SPLIT ? c.cid : c.cid * NG + c.gi;
+  const int64_t step = P::SPLIT ? c.ncl : c.ncl * NG;
+  for (int64_t sig = sig0; sig < batch; sig += step, ++sig_it) {
+    if (storage_leader<T>(c)) sa_mbar_expect_tx(c.full_bar, (uint32_t)P::INTER1);
     // ------------------------------------------------------------- phase A
     for (int u = 0; u < TPG; ++u, ++tile_it) {
-      const int tt = c.gi + NG * u;
+      const int tt = P::SPLIT ? c.gi + NG * u : u;
       sa_mbar_wait(&c.tma_bar[c.gi], tile_it & 1);
       V v[16];
       {  // round 1 (M1): v[k] = node 16g+k of sub-transform cc = X[rev8(16g+k)][cc]
@@ -197,7 +215,6 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
           V x = A::from(wk[(crev4(k) * 16 + rg) * TC + m1_cc]);
           v[k] = use_gain ? A::scale(x, gain) : x;
         }
-        if (!(probe & 1)) {
 #pragma unroll
         for (int k = 0; k < 16; k += 2) r_two_point<T>(v[k], v[k + 1]);  // stage 1
 #pragma unroll
@@ -220,7 +237,6 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
           else if (k == 4) r_dit_mj<T>(v[k], v[k + 8]);
           else r_dit<T>(v[k], v[k + 8], twA[7 + k]);
         }
-        }
       }
       group_sync(gbar, GT);
 #pragma unroll
@@ -231,16 +247,14 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
       for (int k = 0; k < 16; ++k)  // round 2 (M2): node g + 16k of sub-transform cc
         v[k] = A::from(wk[(m2_g + 16 * k) * TC + (m2_cc ^ (m2_g & (TC - 1)))]);
       group_sync(gbar, GT);  // tile buffer consumed: re-arm it
-      if (u + 1 < TPG) tma_tile<T>(c, &tmx, sig, tt + NG);
-      else if (sig + c.ncl < batch) tma_tile<T>(c, &tmx, sig + c.ncl, c.gi);
-      if (!(probe & 1)) {
+      if (u + 1 < TPG) tma_tile<T>(c, &tmx, sig, P::SPLIT ? tt + NG : tt + 1);
+      else if (sig + step < batch) tma_tile<T>(c, &tmx, sig + step, P::SPLIT ? c.gi : 0);
 #pragma unroll
       for (int t = 5; t <= 8; ++t) {
         const int hr = 1 << (t - 5), h = 1 << (t - 1);
 #pragma unroll
         for (int k = 0; k < 16; ++k)
           if (!(k & hr)) r_dit<T>(v[k], v[k + hr], twA[(h - 1) + m2_g + 16 * (k & (hr - 1))]);
-      }
       }
       // scatter node row R = rev8(c): column q lives in CTA q / COLS (st.async credits its mbarrier)
       if (u == 0) sa_mbar_wait(c.empty_bar, sig_it & 1);  // peers finished reading (previous signal)
@@ -250,20 +264,20 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
         constexpr int KPC = COLS / 16;  // registers per owner CTA
 #pragma unroll
         for (int k = 0; k < 16; ++k)
-          sa_st_async(c.inter_rank[(probe & 4) ? c.rank : k / KPC] + (uint32_t)(sizeof(C2) * (R * COLS + m2_g + 16 * (k % KPC))),
-                      A::to(v[k]), c.full_rank[(probe & 4) ? c.rank : k / KPC]);
+          sa_st_async(c.inter_rank[k / KPC] + (uint32_t)(sizeof(C2) * (R * COLS + m2_g + 16 * (k % KPC))),
+                      A::to(v[k]), c.full_rank[k / KPC]);
       }
     }
     // ------------------------------------------------------------- phase B
     C2 *ysig = y + sig * NN;
     C2 wf[30];
     {
-      const int q0 = c.rank * COLS + c.gi * TC + m1_cc;  // independent of the node storage
+      const int q0 = c.rank * COLS + (P::SPLIT ? c.gi : 0) * TC + m1_cc;  // independent of the node storage
       if (!special_column(q0)) load_wf<T>(wf, stage2, q0, m1_g);
     }
     sa_mbar_wait(c.full_bar, sig_it & 1);  // all INTER bytes of this signal landed
     for (int u = 0; u < TPG; ++u) {
-      const int tt = c.gi + NG * u;
+      const int tt = P::SPLIT ? c.gi + NG * u : u;
       const int lq = tt * TC + m1_cc;
       const int q = c.rank * COLS + lq;
       const bool gen = special_column(q);
@@ -282,7 +296,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
           for (int k = 0; k < 16; ++k)
             if (!(k & h)) r_dit<T>(v[k], v[k + h], w[k & (h - 1)]);
         }
-      } else if (!(probe & 2)) {
+      } else {
 #pragma unroll
         for (int t = 1; t <= 4; ++t) {
           const int h = 1 << (t - 1);
@@ -308,7 +322,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
           for (int k = 0; k < 16; ++k)
             if (!(k & hr)) r_dit<T>(v[k], v[k + hr], w[k & (hr - 1)]);
         }
-      } else if (!(probe & 2)) {
+      } else {
 #pragma unroll
         for (int t = 5; t <= 8; ++t) {
           const int hr = 1 << (t - 5);
@@ -320,7 +334,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
 #pragma unroll
       for (int k = 0; k < 16; ++k) __stcs(&ysig[(m1_g + 16 * k) * 256 + q], A::to(v[k]));
     }
-    if (sig + c.ncl < batch) release_storage<T>(c);
+    if (sig + step < batch) release_storage<T>(c);
   }
 }
 
@@ -335,7 +349,7 @@ template <typename T>
 __global__ void __launch_bounds__(L64<T>::THREADS, 1)
     k_nlfft64k_dif(const __grid_constant__ CUtensorMap tmx, typename Ar<T>::C2 *__restrict__ y,
                    int64_t batch, const typename Ar<T>::C4 *__restrict__ stage,
-                   const typename Ar<T>::C2 *__restrict__ stage2, T gain, int use_gain, int probe) {
+                   const typename Ar<T>::C2 *__restrict__ stage2, T gain, int use_gain) {
   using P = L64<T>;
   using A = Ar<T>;
   using V = typename A::V;
@@ -353,14 +367,17 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
   const int rg1 = rev4(m1_g);
 
   uint32_t tile_it = 0, sig_it = 0;
-  if (c.cid < batch) tma_tile<T>(c, &tmx, c.cid, c.gi);
+  if ((P::SPLIT ? c.cid : c.cid * NG + c.gi) < batch)
+    tma_tile<T>(c, &tmx, P::SPLIT ? c.cid : c.cid * NG + c.gi, P::SPLIT ? c.gi : 0);
   release_storage<T>(c);
 
-  for (int64_t sig = c.cid; sig < batch; sig += c.ncl, ++sig_it) {
-    if (threadIdx.x == 0) sa_mbar_expect_tx(c.full_bar, (uint32_t)P::INTER);
+  const int64_t sig0 = P::SPLIT ? c.cid : c.cid * NG + c.gi;
+  const int64_t step = P::SPLIT ? c.ncl : c.ncl * NG;
+  for (int64_t sig = sig0; sig < batch; sig += step, ++sig_it) {
+    if (storage_leader<T>(c)) sa_mbar_expect_tx(c.full_bar, (uint32_t)P::INTER1);
     // ------------------------------------------------------------- phase 1
     for (int u = 0; u < TPG; ++u, ++tile_it) {
-      const int tt = c.gi + NG * u;
+      const int tt = P::SPLIT ? c.gi + NG * u : u;
       const int q = c.rank * COLS + tt * TC + m1_cc;
       const bool gen = special_column(q);
       C2 wf[30];
@@ -399,8 +416,8 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
 #pragma unroll
       for (int k = 0; k < 16; ++k) v[k] = A::from(wk[(m1_g * 16 + k) * TC + m1_cc]);  // R = 16g + k
       group_sync(gbar, GT);  // tile buffer consumed: re-arm it
-      if (u + 1 < TPG) tma_tile<T>(c, &tmx, sig, tt + NG);
-      else if (sig + c.ncl < batch) tma_tile<T>(c, &tmx, sig + c.ncl, c.gi);
+      if (u + 1 < TPG) tma_tile<T>(c, &tmx, sig, P::SPLIT ? tt + NG : tt + 1);
+      else if (sig + step < batch) tma_tile<T>(c, &tmx, sig + step, P::SPLIT ? c.gi : 0);
       if (gen) {
 #pragma unroll
         for (int t = 4; t >= 1; --t) {  // R bits 3..0
@@ -434,7 +451,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
     // ------------------------------------------------------------- phase 2
     C2 *ysig = y + sig * NN;
     for (int u = 0; u < TPG; ++u) {
-      const int tt = c.gi + NG * u;
+      const int tt = P::SPLIT ? c.gi + NG * u : u;
       V v[16];
       {  // round 1 (M2: g fastest): q = g + 16k ; stages 8..5
         const int lr = tt * TC + m2_cc;
@@ -487,7 +504,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
         for (int k = 0; k < 16; ++k) __stcs(&ysig[(crev4(k) * 16 + rg) * 256 + cr], A::to(v[k]));
       }
     }
-    if (sig + c.ncl < batch) release_storage<T>(c);
+    if (sig + step < batch) release_storage<T>(c);
   }
 }
 
@@ -501,17 +518,6 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
       fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
   }
   return fn;
-}
-
-// experiment hook (not part of the ABI): SA_NLFFT64K_PROBE bitmask skips work
-// to time the kernel skeleton; 0 (default) = normal operation.
-int probe_flags() {
-  static int v = -1;
-  if (v < 0) {
-    const char *e = getenv("SA_NLFFT64K_PROBE");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
 }
 
 template <typename T>
@@ -559,8 +565,7 @@ int launch64k(int variant, const void *x, void *y, int64_t batch, const SaTwiddl
   cfg.gridDim = dim3((unsigned)(ncl * P::CL));
   SA_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, map, (typename P::C2 *)y, batch,
                                  (const typename P::C4 *)tw->stage,
-                                 (const typename P::C2 *)tw->stage2, (T)gain, (int)(gain != 1.0),
-                                 probe_flags()));
+                                 (const typename P::C2 *)tw->stage2, (T)gain, (int)(gain != 1.0)));
   return SA_OK;
 }
 
