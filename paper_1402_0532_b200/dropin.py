@@ -1,0 +1,138 @@
+"""Install the B200 hot path into an imported reference ``signadd`` package.
+
+    import signadd
+    from paper_1402_0532_b200 import dropin
+    dropin.install(signadd)          # patches every name binding of the path
+
+Names patched: ``signadd.{ndft, nfft, lag_product_mf,
+ambiguity_eq12a, compute_ambiguity}``, ``signadd.transforms.{ndft, nfft}``,
+``signadd.ambiguity.{nfft, lag_product_mf, ambiguity_eq12a, compute_ambiguity}``
+(module globals looked up at call time, ambiguity.py:39,201-202),
+``signadd.detection.compute_ambiguity`` (detection.py:24,187),
+``signadd.cli.{ndft, nfft}`` and ``cli._TRANSFORMS`` (captured at import,
+cli.py:51-71).  ``mf_complex`` is optional (``mf_complex=True``): the reference
+test oracles (tests/oracles.py:10) call it and are meant to stay on the CPU.
+
+The wrappers return the reference's own types (``Spectrum``,
+``AmbiguitySurface``, ``OpCountReport``) and raise the reference's own
+exception classes, so callers cannot tell the difference except by speed.
+Variants other than eq12a keep the reference implementation (exact multiply is
+off the ⊙ path).
+"""
+
+from __future__ import annotations
+
+import functools
+
+from . import ambiguity as _amb
+from . import operator as _op
+from . import transforms as _tr
+from .errors import ContractError, DomainError
+
+_ORIG: dict = {}
+
+
+def _translate(ref):
+    """Decorator factory: map our exceptions to the reference's classes."""
+    def deco(fn):
+        @functools.wraps(fn)
+        def wrapper(*a, **kw):
+            try:
+                return fn(*a, **kw)
+            except ContractError as e:
+                raise ref.ContractError(str(e)) from None
+            except DomainError as e:
+                raise ref.DomainError(str(e)) from None
+        return wrapper
+    return deco
+
+
+def _to_ref_counts(ref, r):
+    return ref.OpCountReport(r.sign_ops, r.abs_ops, r.add_ops, r.complex_mf_ops, r.complex_mul_ops)
+
+
+def _unwrap_signal(ref, x):
+    return x.samples if isinstance(x, ref.ComplexSignal) else x
+
+
+def install(ref, *, mf_complex: bool = False) -> None:
+    """Patch the reference module ``ref`` (the imported ``signadd`` package)."""
+    import importlib
+    tmod = importlib.import_module(ref.__name__ + ".transforms")
+    amod = importlib.import_module(ref.__name__ + ".ambiguity")
+    dmod = importlib.import_module(ref.__name__ + ".detection")
+    cmod = importlib.import_module(ref.__name__ + ".cli")
+    tr = _translate(ref)
+
+    @tr
+    def ndft(x, counter=None):
+        s = _tr.ndft(_unwrap_signal(ref, x), counter)
+        return ref.Spectrum(s.bins, ref.TransformKind.NDFT, _to_ref_counts(ref, s.op_counts))
+
+    @tr
+    def nfft(x, counter=None):
+        s = _tr.nfft(_unwrap_signal(ref, x), counter)
+        return ref.Spectrum(s.bins, ref.TransformKind.NFFT, _to_ref_counts(ref, s.op_counts))
+
+    @tr
+    def lag_product_mf(s_surv, s_ref, l, n=None, conjugate_ref=True, counter=None):
+        return _amb.lag_product_mf(_unwrap_signal(ref, s_surv), _unwrap_signal(ref, s_ref), l, n,
+                                   conjugate_ref, counter)
+
+    orig_compute = amod.compute_ambiguity
+
+    @tr
+    def ambiguity_eq12a(s_surv, s_ref, l_bins, n, transform_input_gain=1.0, conjugate_ref=True):
+        # ambiguity.py:158-170 checks (sample rates) on the reference's own types
+        if l_bins < 1:
+            raise ContractError("l_bins must be >= 1")
+        fs = None
+        for sig in (s_surv, s_ref):
+            if isinstance(sig, ref.ComplexSignal):
+                if fs is not None and sig.sample_rate_hz != fs:
+                    raise ContractError("surveillance and reference sample rates differ")
+                fs = sig.sample_rate_hz
+        if fs is None:
+            raise ContractError("at least one input must be a ComplexSignal carrying a sample rate")
+        ours = _amb.ambiguity_eq12a(_tr.ComplexSignal(_unwrap_signal(ref, s_surv), fs),
+                                    _tr.ComplexSignal(_unwrap_signal(ref, s_ref), fs),
+                                    l_bins, n, transform_input_gain, conjugate_ref)
+        return ref.AmbiguitySurface(values=ours.values, range_bin_m=ours.range_bin_m,
+                                    doppler_bin_hz=ours.doppler_bin_hz,
+                                    variant=ref.AmbiguityVariant.EQ12A, sample_rate_hz=fs,
+                                    lag_op_counts=_to_ref_counts(ref, ours.lag_op_counts),
+                                    transform_op_counts=_to_ref_counts(ref, ours.transform_op_counts))
+
+    def compute_ambiguity(variant, s_surv, s_ref, l_bins, n, transform_input_gain=1.0,
+                          conjugate_ref=True):
+        if ref.AmbiguityVariant(variant) is ref.AmbiguityVariant.EQ12A:
+            return ambiguity_eq12a(s_surv, s_ref, l_bins, n, transform_input_gain, conjugate_ref)
+        return orig_compute(variant, s_surv, s_ref, l_bins, n, transform_input_gain, conjugate_ref)
+
+    patches = [
+        (ref, "ndft", ndft), (ref, "nfft", nfft), (ref, "lag_product_mf", lag_product_mf),
+        (ref, "ambiguity_eq12a", ambiguity_eq12a), (ref, "compute_ambiguity", compute_ambiguity),
+        (tmod, "ndft", ndft), (tmod, "nfft", nfft),
+        (amod, "nfft", nfft), (amod, "lag_product_mf", lag_product_mf),
+        (amod, "ambiguity_eq12a", ambiguity_eq12a), (amod, "compute_ambiguity", compute_ambiguity),
+        (dmod, "compute_ambiguity", compute_ambiguity),
+        (cmod, "ndft", ndft), (cmod, "nfft", nfft),
+    ]
+    if mf_complex:
+        patches.append((ref, "mf_complex", tr(_op.mf_complex)))
+    for mod, name, fn in patches:
+        _ORIG.setdefault((mod.__name__, name), getattr(mod, name))
+        setattr(mod, name, fn)
+    cmod._TRANSFORMS["ndft"] = ndft
+    cmod._TRANSFORMS["nfft"] = nfft
+
+
+def uninstall(ref) -> None:
+    """Restore the reference bindings saved by install()."""
+    import importlib
+    for (modname, name), fn in _ORIG.items():
+        setattr(importlib.import_module(modname), name, fn)
+    cmod = importlib.import_module(ref.__name__ + ".cli")
+    cmod._TRANSFORMS["ndft"] = _ORIG.get((cmod.__name__, "ndft"), cmod._TRANSFORMS["ndft"])
+    cmod._TRANSFORMS["nfft"] = _ORIG.get((cmod.__name__, "nfft"), cmod._TRANSFORMS["nfft"])
+    _ORIG.clear()
