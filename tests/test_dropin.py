@@ -108,7 +108,7 @@ def test_reference_pipeline_eq12a_matches_cpu(ref, sa):
     """Scene synthesis (reference, CPU) -> eq12a surface: drop-in vs reference CPU."""
     from paper_1402_0532_b200 import dropin
     import signadd.detection as dmod
-    scn = ref.two_targets_one_clutter(seed=3, n=1024, l_bins=32)
+    scn = ref.two_targets_one_clutter(seed=3)  # reference defaults: n=4096, 64 delay bins
     cpu = dmod.surface_for_scenario(scn, "eq12a")
     dropin.install(ref)
     try:
