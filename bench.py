@@ -235,26 +235,51 @@ def wl_ndft(args, ws, rank):
     return res
 
 
+def ncu_traffic(kernel_prefix):
+    """DRAM bytes (read + write) per launch of a kernel, from the committed ncu
+    --set full summary (profiles/*_kernels.json, tools/ncu_summary.py), or None."""
+    import glob
+    best = None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_kernels.json"))):
+        try:
+            d = json.load(open(f))
+        except Exception:
+            continue
+        for name, k in d.items():
+            if name.startswith(kernel_prefix) and "dram_read_bytes" in k:
+                best = {"bytes_per_launch": k["dram_read_bytes"] + k.get("dram_write_bytes", 0),
+                        "source": os.path.relpath(f, ROOT)}
+    return best
+
+
 def roof_alu(dtype, achieved_tflops, args):
     peak = fma_peak_tflops(dtype)
+    kern = "k_ndft_fast_f32x2" if dtype == "c64" else "k_ndft_fast<double"
+    tr = ncu_traffic(kern)
     return {"bound": "fp32_alu" if dtype == "c64" else "fp64_alu", "achieved": round(achieved_tflops, 3),
             "peak": round(peak, 3), "unit": "TFLOP/s", "frac": round(achieved_tflops / peak, 4),
-            "traffic": None,
+            "traffic": tr["bytes_per_launch"] if tr else None, "traffic_unit": "bytes/launch",
+            "traffic_source": tr["source"] if tr else None,
+            "algorithmic_bytes": 2 * 65536 * 1024 * (8 if dtype == "c64" else 16),
+            "kernel": kern,
             "peak_source": "measured live: sa_fma_peak FFMA/DFMA microbenchmark (MEASURED_PEAKS.json "
                            "has no CUDA-core figure)",
             "algorithmic": "8 FMA (16 flop) per complex ⊙ (sign-split identity)"}
 
 
-def roof_hbm(bytes_per_step, ms):
+def roof_hbm(bytes_per_step, ms, kernel=None):
     peaks, src = measured_peaks()
     ach = bytes_per_step / (ms * 1e-3) / 1e9
+    tr = ncu_traffic(kernel) if kernel else None
     return {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None, "peak_source": src}
+            "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": tr["bytes_per_launch"] if tr else None,
+            "traffic_unit": "bytes/launch", "algorithmic_bytes": bytes_per_step, "kernel": kernel,
+            "peak_source": src}
 
 
 def cpu_ndft(x, P):
     import oracle
-    rows = min(x.shape[0], max(64, 8 * P))
+    rows = min(x.shape[0], 4096, max(256, 40 * P))  # ~10-30 s of CPU work at ~30 ms/vector/core
     sample = np.ascontiguousarray(x[:rows])
     t = time.perf_counter()
     oracle.ndft(sample, dtype="f32" if sample.dtype == np.complex64 else "f64", nthreads=P)
@@ -293,7 +318,9 @@ def wl_nlfft(args, ws, rank, variant="dit", batch=4096, n=1 << 16):
     res = {"ops": ops, "step": step, "launches_per_step": 2, "bytes": bytes_step,
            "config": {"workload": f"C3 NL-FFT {variant.upper()} (BASELINE.json configs[2])", "n": n,
                       "batch": batch, "dtype": str(cdt).replace("torch.", "")}}
-    res["roofline"] = lambda ms: roof_hbm(bytes_step, ms)
+    kname = ("k_nlfft64k_dit" if variant == "dit" else "k_nlfft64k_dif") + (
+        "<float" if args.dtype == "c64" else "<double")
+    res["roofline"] = lambda ms: roof_hbm(bytes_step, ms, kname)
     return res
 
 
