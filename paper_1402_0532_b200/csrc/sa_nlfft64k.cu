@@ -1,24 +1,22 @@
 // sa_nlfft64k.cu -- single-HBM-pass NL-FFT for N = 2^16 (BASELINE config C3).
 //
-// One signal per thread-block cluster, entirely on chip:
-//   c64 : cluster of 4 CTAs x 128 KiB of node storage (512 KiB signal)
-//   c128: cluster of 8 CTAs x 128 KiB                 (1 MiB signal)
-// N = 256 x 256.  DIT (value-identical to transforms.py:254-298):
+// One signal per thread-block cluster of 8 CTAs, entirely on chip.  N = 256 x 256.
+// DIT (value-identical to transforms.py:254-298):
 //   phase A: CTA r takes columns c of X[i][c] = x[256 i + c] (the reference's
-//     bit-reversed blocks, SURVEY §7 hard part 4), in TMA-loaded tiles of TC
+//     bit-reversed blocks, SURVEY §7 hard part 4) in TMA-loaded tiles of TC
 //     columns x 256 rows, runs global stages 1..8 in two register radix-16
 //     rounds (stage 1 = the 2-point NDFT bottom), and scatters node row
-//     R = rev8(c) over the cluster with st.async into the owner's smem,
-//     crediting the owner's "full" mbarrier (no fence, no cluster barrier):
-//     q-columns [r*COLS, (r+1)*COLS) of every row live in CTA r.
-//   phase B: CTA r waits for its 128 KiB, runs global stages 9..16 along R for
-//     its columns (twiddle j = (R mod 2^(t-1))*256 + q), writes y[256 R + q].
-//   A relaxed cluster arrive (after the last read of the node storage) / wait
-//     (before the next signal's first scatter) guards the storage reuse.
-// Each CTA runs NG independent thread groups (named barriers, own TMA buffer
-// and mbarrier), each owning every NG-th tile, so one group's barrier / TMA /
-// L2 latency is covered by the others' arithmetic (16 warps/SM for c64).
-// HBM traffic = one read + one write of the signal.
+//     R = rev8(c) over the cluster with st.async into the owner's smem, crediting
+//     the owner's "full" mbarrier (no fence, no cluster barrier): q-columns
+//     [r*COLS, (r+1)*COLS) of every row live in CTA r.
+//   phase B: CTA r waits for its node storage, runs global stages 9..16 along R
+//     for its columns (twiddle j = (R mod 2^(t-1))*256 + q), writes y[256 R + q].
+//   An "empty" mbarrier fed by remote relaxed arrives guards storage reuse.
+// c64 double-buffers the node storage (2 x 64 KiB per CTA) and software-pipelines
+// signals: phase B of signal s runs after phase A of signal s+1, so each
+// cluster-wide hand-off has a whole phase of slack instead of stalling 16 warps
+// on the slowest peer.  Each CTA runs NG thread groups (named barriers, own TMA
+// buffer) that split a phase's tiles.  HBM traffic = one read + one write.
 #include <algorithm>
 #include <cooperative_groups.h>
 #include <cudaTypedefs.h>
@@ -34,41 +32,37 @@ constexpr int LOGN = 16;
 constexpr int NN = 1 << LOGN;
 
 template <typename T> struct K64;
-// SPLIT = true : the NG groups share one signal's tiles (one node storage);
-// SPLIT = false: each group owns its own signal stream and node storage, so one
-//                group's phase A overlaps the other's phase B.
 template <> struct K64<float> {
   static constexpr int TC = 16;  // columns per tile
   static constexpr int CL = 4;   // cluster size
   static constexpr int NG = 2;   // thread groups per CTA
-  static constexpr bool SPLIT = true;
+  static constexpr int NS = 1;   // node storages (2 = pipelined signals; needs CL >= 8 for c64)
 };
 template <> struct K64<double> {
   static constexpr int TC = 8;
   static constexpr int CL = 8;
   static constexpr int NG = 2;
-  static constexpr bool SPLIT = true;
+  static constexpr int NS = 1;
 };
 
 template <typename T> struct L64 {
-  static constexpr int TC = K64<T>::TC, CL = K64<T>::CL, NG = K64<T>::NG;
-  static constexpr bool SPLIT = K64<T>::SPLIT;
-  static constexpr int NS = SPLIT ? 1 : NG;   // node storages per CTA
-  static constexpr int GT = 16 * TC;          // threads per group
+  static constexpr int TC = K64<T>::TC, CL = K64<T>::CL, NG = K64<T>::NG, NS = K64<T>::NS;
+  static constexpr int GT = 16 * TC;       // threads per group
   static constexpr int THREADS = NG * GT;
-  static constexpr int COLS = 256 / CL;       // node columns owned per CTA
-  static constexpr int TILES = COLS / TC;     // tiles per CTA per phase
-  static constexpr int TPG = SPLIT ? TILES / NG : TILES;  // tiles per group per phase
+  static constexpr int COLS = 256 / CL;    // node columns owned per CTA
+  static constexpr int TILES = COLS / TC;  // tiles per CTA per phase
+  static constexpr int TPG = TILES / NG;   // tiles per group per phase
   using C2 = typename Ar<T>::C2;
   using C4 = typename Ar<T>::C4;
-  static constexpr size_t INTER1 = sizeof(C2) * 256 * COLS;  // one signal's share
-  static constexpr size_t INTER = NS * INTER1;
-  static constexpr size_t WORK = sizeof(C2) * 256 * TC;  // one tile
+  static constexpr size_t INTER1 = sizeof(C2) * 256 * COLS;  // one signal's node share
+  static constexpr size_t WORK = sizeof(C2) * 256 * TC;      // one tile
   static constexpr size_t TWA = sizeof(C4) * 255;
-  static constexpr size_t MBAR_OFF = INTER + NG * WORK + TWA;
-  static constexpr size_t SMEM = MBAR_OFF + 8 * (NG + 2 * NS);
+  static constexpr size_t OFF_WORK = NS * INTER1;
+  static constexpr size_t OFF_TWA = OFF_WORK + NG * WORK;
+  static constexpr size_t OFF_BAR = OFF_TWA + TWA;
+  static constexpr size_t SMEM = OFF_BAR + 8 * (NG + 2 * NS);
   static constexpr int EW = sizeof(C2) / 8;  // 8-byte TMA elements per complex
-  static_assert(!SPLIT || TILES % NG == 0, "tiles must split evenly over groups");
+  static_assert(TILES % NG == 0 && TPG >= 1, "tiles must split evenly over groups");
 };
 
 SA_HD int rev4(int v) { return (int)(__brev((unsigned)v) >> 28); }
@@ -77,79 +71,6 @@ constexpr int crev4(int v) { return ((v & 1) << 3) | ((v & 2) << 1) | ((v & 4) >
 
 SA_HD void group_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
-// per-CTA setup shared by DIT and DIF
-template <typename T> struct Ctx {
-  using P = L64<T>;
-  typename P::C2 *inter, *work;
-  typename P::C4 *twA;
-  uint64_t *tma_bar, *full_bar, *empty_bar;
-  uint32_t inter_rank[P::CL], full_rank[P::CL], empty_rank[P::CL];
-  int rank, gi, gt;
-  int64_t cid, ncl;
-};
-
-template <typename T>
-SA_HD void ctx_init(Ctx<T> &c, unsigned char *smem_raw, const typename L64<T>::C4 *stage) {
-  using P = L64<T>;
-  cg::cluster_group cluster = cg::this_cluster();
-  c.gi = threadIdx.x / P::GT;
-  const int st = P::SPLIT ? 0 : c.gi;  // this group's node storage
-  c.inter = reinterpret_cast<typename P::C2 *>(smem_raw + st * P::INTER1);
-  c.work = reinterpret_cast<typename P::C2 *>(smem_raw + P::INTER);
-  c.twA = reinterpret_cast<typename P::C4 *>(smem_raw + P::INTER + P::NG * P::WORK);
-  c.tma_bar = reinterpret_cast<uint64_t *>(smem_raw + P::MBAR_OFF);
-  uint64_t *full0 = c.tma_bar + P::NG, *empty0 = full0 + P::NS;
-  c.full_bar = full0 + st;
-  c.empty_bar = empty0 + st;
-  c.rank = (int)cluster.block_rank();
-  c.cid = blockIdx.x / P::CL;
-  c.ncl = gridDim.x / P::CL;
-  c.gt = threadIdx.x % P::GT;
-  for (int e = threadIdx.x; e < 255; e += P::THREADS) c.twA[e] = stage[e];  // global stages 1..8
-  if (threadIdx.x == 0) {
-    for (int g = 0; g < P::NG; ++g) sa_mbar_init(&c.tma_bar[g], 1);
-    for (int g = 0; g < P::NS; ++g) {
-      sa_mbar_init(&full0[g], 1);       // expect_tx(INTER1) once per signal
-      sa_mbar_init(&empty0[g], P::CL);  // one remote arrive per peer per signal
-    }
-    sa_fence_mbar_init();
-  }
-  __syncthreads();
-  cluster.sync();
-#pragma unroll
-  for (int r = 0; r < P::CL; ++r) {
-    c.inter_rank[r] = sa_mapa(sa_smem_u32(c.inter), r);
-    c.full_rank[r] = sa_mapa(sa_smem_u32(c.full_bar), r);
-    c.empty_rank[r] = sa_mapa(sa_smem_u32(c.empty_bar), r);
-  }
-}
-
-// "my node storage may be overwritten": all threads of the CTA finished reading
-// it (bar.sync 0), then one thread arrives on every peer's empty barrier.
-template <typename T> SA_HD void release_storage(const Ctx<T> &c) {
-  using P = L64<T>;
-  if (P::SPLIT) __syncthreads();
-  else group_sync(1 + c.gi, P::GT);
-  if (P::SPLIT ? threadIdx.x == 0 : c.gt == 0)
-#pragma unroll
-    for (int r = 0; r < P::CL; ++r) sa_mbar_arrive_remote(c.empty_rank[r]);
-}
-template <typename T> SA_HD bool storage_leader(const Ctx<T> &c) {
-  return L64<T>::SPLIT ? threadIdx.x == 0 : c.gt == 0;
-}
-
-// group-leader TMA of tile tt (TC columns x 256 rows) of signal sig into the group buffer
-template <typename T>
-SA_HD void tma_tile(const Ctx<T> &c, const CUtensorMap *tmx, int64_t sig, int tt) {
-  using P = L64<T>;
-  if (c.gt == 0) {
-    sa_fence_proxy_async();
-    sa_mbar_expect_tx(&c.tma_bar[c.gi], (uint32_t)P::WORK);
-    sa_tma_load_2d(c.work + c.gi * 256 * P::TC, tmx, (c.rank * P::COLS + tt * P::TC) * P::EW,
-                   (int)(sig * 256), &c.tma_bar[c.gi]);
-  }
 }
 
 // Twiddles of the 8 cross-row stages (global 9..16) for node column q, as raw
@@ -173,6 +94,95 @@ SA_HD void load_wf(typename Ar<T>::C2 (&wf)[30], const typename Ar<T>::C2 *__res
 }
 SA_HD bool special_column(int q) { return __any_sync(0xffffffffu, q == 0 || q == 128); }
 
+// Shared per-CTA state and the signal pipeline orchestration of both kernels.
+template <typename T> struct Pipe {
+  using P = L64<T>;
+  using C2 = typename P::C2;
+  using C4 = typename P::C4;
+  unsigned char *smem;
+  C4 *twA;
+  uint64_t *tma_bar, *full_bar, *empty_bar;
+  int rank, gi, gt;
+  int64_t cid, ncl;
+  uint32_t tile_it = 0;
+
+  SA_HD C2 *inter(int b) const { return reinterpret_cast<C2 *>(smem + b * P::INTER1); }
+  SA_HD C2 *work() const { return reinterpret_cast<C2 *>(smem + P::OFF_WORK + gi * P::WORK); }
+  // cluster-window address of peer r's node storage b (byte offset off) / its full mbarrier
+  SA_HD uint32_t peer_inter(int b, int r, uint32_t off) const {
+    return sa_mapa(sa_smem_u32(smem + b * P::INTER1) + off, r);
+  }
+  SA_HD uint32_t peer_full(int b, int r) const { return sa_mapa(sa_smem_u32(&full_bar[b]), r); }
+
+  SA_HD void init(unsigned char *smem_raw, const C4 *stage) {
+    cg::cluster_group cluster = cg::this_cluster();
+    smem = smem_raw;
+    twA = reinterpret_cast<C4 *>(smem + P::OFF_TWA);
+    tma_bar = reinterpret_cast<uint64_t *>(smem + P::OFF_BAR);
+    full_bar = tma_bar + P::NG;
+    empty_bar = full_bar + P::NS;
+    rank = (int)cluster.block_rank();
+    cid = blockIdx.x / P::CL;
+    ncl = gridDim.x / P::CL;
+    gi = threadIdx.x / P::GT;
+    gt = threadIdx.x % P::GT;
+    for (int e = threadIdx.x; e < 255; e += P::THREADS) twA[e] = stage[e];  // global stages 1..8
+    if (threadIdx.x == 0) {
+      for (int g = 0; g < P::NG; ++g) sa_mbar_init(&tma_bar[g], 1);
+      for (int b = 0; b < P::NS; ++b) {
+        sa_mbar_init(&full_bar[b], 1);       // expect_tx(INTER1) once per use
+        sa_mbar_init(&empty_bar[b], P::CL);  // one remote arrive per peer per use
+      }
+      sa_fence_mbar_init();
+    }
+    __syncthreads();
+    cluster.sync();
+  }
+  // group-leader TMA of tile tt (TC columns x 256 rows) of signal sig
+  SA_HD void tma(const CUtensorMap *tmx, int64_t sig, int tt) const {
+    if (gt == 0) {
+      sa_fence_proxy_async();
+      sa_mbar_expect_tx(&tma_bar[gi], (uint32_t)P::WORK);
+      sa_tma_load_2d(work(), tmx, (rank * P::COLS + tt * P::TC) * P::EW, (int)(sig * 256), &tma_bar[gi]);
+    }
+  }
+  SA_HD void wait_tile() {
+    sa_mbar_wait(&tma_bar[gi], tile_it & 1);
+    ++tile_it;
+  }
+  // "storage b may be overwritten": the CTA finished reading it, one thread
+  // arrives on every peer's empty barrier for b.
+  SA_HD void release(int b) const {
+    __syncthreads();
+    if (threadIdx.x == 0)
+#pragma unroll
+      for (int r = 0; r < P::CL; ++r) sa_mbar_arrive_remote(sa_mapa(sa_smem_u32(&empty_bar[b]), r));
+  }
+  // signal loop: phaseA(sig, b, use, next_sig) then (pipelined) phaseB of the
+  // previous signal; every storage use waits full/empty with parity use & 1.
+  template <class FA, class FB>
+  SA_HD void run(const CUtensorMap *tmx, int64_t batch, FA phaseA, FB phaseB) {
+    if (cid < batch) tma(tmx, cid, gi);
+    for (int b = 0; b < P::NS; ++b) release(b);  // all storages free
+    int64_t i = 0;
+    for (int64_t sig = cid; sig < batch; sig += ncl, ++i) {
+      const int b = (int)(i % P::NS);
+      if (threadIdx.x == 0) sa_mbar_expect_tx(&full_bar[b], (uint32_t)P::INTER1);
+      phaseA(sig, b, (uint32_t)(i / P::NS), sig + ncl);
+      if (P::NS == 1) {
+        phaseB(sig, 0, (uint32_t)i);
+        if (sig + ncl < batch) release(0);
+      } else if (i > 0) {
+        const int pb = (int)((i - 1) % P::NS);
+        phaseB(sig - ncl, pb, (uint32_t)((i - 1) / P::NS));
+        if (sig + ncl < batch) release(pb);  // next user of pb is signal i+1
+      }
+    }
+    if (P::NS == 2 && i > 0)
+      phaseB(cid + (i - 1) * ncl, (int)((i - 1) % P::NS), (uint32_t)((i - 1) / P::NS));
+  }
+};
+
 template <typename T>
 __global__ void __launch_bounds__(L64<T>::THREADS, 1)
     k_nlfft64k_dit(const __grid_constant__ CUtensorMap tmx, typename Ar<T>::C2 *__restrict__ y,
@@ -185,28 +195,18 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
   using C4 = typename P::C4;
   constexpr int TC = P::TC, COLS = P::COLS, NG = P::NG, GT = P::GT, TPG = P::TPG;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  Ctx<T> c;
-  ctx_init<T>(c, smem_raw, stage);
-  const int gbar = 1 + c.gi;
-  const int m1_cc = c.gt % TC, m1_g = c.gt / TC;
-  const int m2_g = c.gt & 15, m2_cc = c.gt >> 4;
-  C2 *wk = c.work + c.gi * 256 * TC;
-  C4 *twA = c.twA;
+  Pipe<T> pp;
+  pp.init(smem_raw, stage);
+  const int gbar = 1 + pp.gi;
+  const int m1_cc = pp.gt % TC, m1_g = pp.gt / TC;
+  const int m2_g = pp.gt & 15, m2_cc = pp.gt >> 4;
+  const C4 *twA = pp.twA;
 
-  uint32_t tile_it = 0;  // this group's TMA uses (parity)
-  uint32_t sig_it = 0;
-  if ((P::SPLIT ? c.cid : c.cid * NG + c.gi) < batch)
-    tma_tile<T>(c, &tmx, P::SPLIT ? c.cid : c.cid * NG + c.gi, P::SPLIT ? c.gi : 0);
-  release_storage<T>(c);  // node storage free for the first signal
-
-  const int64_t sig0 = P::SPLIT ? c.cid : c.cid * NG + c.gi;
-  const int64_t step = P::SPLIT ? c.ncl : c.ncl * NG;
-  for (int64_t sig = sig0; sig < batch; sig += step, ++sig_it) {
-    if (storage_leader<T>(c)) sa_mbar_expect_tx(c.full_bar, (uint32_t)P::INTER1);
-    // ------------------------------------------------------------- phase A
-    for (int u = 0; u < TPG; ++u, ++tile_it) {
-      const int tt = P::SPLIT ? c.gi + NG * u : u;
-      sa_mbar_wait(&c.tma_bar[c.gi], tile_it & 1);
+  auto phaseA = [&](int64_t sig, int b, uint32_t use, int64_t nsig) {
+    for (int u = 0; u < TPG; ++u) {
+      const int tt = pp.gi + NG * u;
+      pp.wait_tile();
+      C2 *wk = pp.work();
       V v[16];
       {  // round 1 (M1): v[k] = node 16g+k of sub-transform cc = X[rev8(16g+k)][cc]
         const int rg = rev4(m1_g);
@@ -247,8 +247,8 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
       for (int k = 0; k < 16; ++k)  // round 2 (M2): node g + 16k of sub-transform cc
         v[k] = A::from(wk[(m2_g + 16 * k) * TC + (m2_cc ^ (m2_g & (TC - 1)))]);
       group_sync(gbar, GT);  // tile buffer consumed: re-arm it
-      if (u + 1 < TPG) tma_tile<T>(c, &tmx, sig, P::SPLIT ? tt + NG : tt + 1);
-      else if (sig + step < batch) tma_tile<T>(c, &tmx, sig + step, P::SPLIT ? c.gi : 0);
+      if (u + 1 < TPG) pp.tma(&tmx, sig, tt + NG);
+      else if (nsig < batch) pp.tma(&tmx, nsig, pp.gi);
 #pragma unroll
       for (int t = 5; t <= 8; ++t) {
         const int hr = 1 << (t - 5), h = 1 << (t - 1);
@@ -256,35 +256,35 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
         for (int k = 0; k < 16; ++k)
           if (!(k & hr)) r_dit<T>(v[k], v[k + hr], twA[(h - 1) + m2_g + 16 * (k & (hr - 1))]);
       }
-      // scatter node row R = rev8(c): column q lives in CTA q / COLS (st.async credits its mbarrier)
-      if (u == 0) sa_mbar_wait(c.empty_bar, sig_it & 1);  // peers finished reading (previous signal)
-      {
-        const int cc = c.rank * COLS + tt * TC + m2_cc;
-        const int R = rev8(cc);
-        constexpr int KPC = COLS / 16;  // registers per owner CTA
+      // scatter node row R = rev8(c): column q lives in CTA q / COLS
+      if (u == 0) sa_mbar_wait(&pp.empty_bar[b], use & 1);  // peers released storage b
+      const int R = rev8(pp.rank * COLS + tt * TC + m2_cc);
+      constexpr int KPC = COLS / 16;  // registers per owner CTA
 #pragma unroll
-        for (int k = 0; k < 16; ++k)
-          sa_st_async(c.inter_rank[k / KPC] + (uint32_t)(sizeof(C2) * (R * COLS + m2_g + 16 * (k % KPC))),
-                      A::to(v[k]), c.full_rank[k / KPC]);
-      }
+      for (int k = 0; k < 16; ++k)
+        sa_st_async(pp.peer_inter(b, k / KPC, (uint32_t)(sizeof(C2) * (R * COLS + m2_g + 16 * (k % KPC)))),
+                    A::to(v[k]), pp.peer_full(b, k / KPC));
     }
-    // ------------------------------------------------------------- phase B
+  };
+
+  auto phaseB = [&](int64_t sig, int b, uint32_t use) {
+    C2 *inter = pp.inter(b);
     C2 *ysig = y + sig * NN;
     C2 wf[30];
     {
-      const int q0 = c.rank * COLS + (P::SPLIT ? c.gi : 0) * TC + m1_cc;  // independent of the node storage
+      const int q0 = pp.rank * COLS + pp.gi * TC + m1_cc;  // independent of the node storage
       if (!special_column(q0)) load_wf<T>(wf, stage2, q0, m1_g);
     }
-    sa_mbar_wait(c.full_bar, sig_it & 1);  // all INTER bytes of this signal landed
+    sa_mbar_wait(&pp.full_bar[b], use & 1);  // all INTER1 bytes of this signal landed
     for (int u = 0; u < TPG; ++u) {
-      const int tt = P::SPLIT ? c.gi + NG * u : u;
+      const int tt = pp.gi + NG * u;
       const int lq = tt * TC + m1_cc;
-      const int q = c.rank * COLS + lq;
+      const int q = pp.rank * COLS + lq;
       const bool gen = special_column(q);
       if (u > 0 && !gen) load_wf<T>(wf, stage2, q, m1_g);
       V v[16];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = A::from(c.inter[(m1_g * 16 + k) * COLS + lq]);
+      for (int k = 0; k < 16; ++k) v[k] = A::from(inter[(m1_g * 16 + k) * COLS + lq]);
       if (gen) {  // columns 0 / 128: general twiddles (zero components), loaded per stage
 #pragma unroll
         for (int t = 1; t <= 4; ++t) {  // R bits 0..3
@@ -306,10 +306,10 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
         }
       }
 #pragma unroll
-      for (int k = 0; k < 16; ++k) c.inter[(m1_g * 16 + k) * COLS + lq] = A::to(v[k]);
+      for (int k = 0; k < 16; ++k) inter[(m1_g * 16 + k) * COLS + lq] = A::to(v[k]);
       group_sync(gbar, GT);
 #pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = A::from(c.inter[(m1_g + 16 * k) * COLS + lq]);
+      for (int k = 0; k < 16; ++k) v[k] = A::from(inter[(m1_g + 16 * k) * COLS + lq]);
       if (gen) {
 #pragma unroll
         for (int t = 5; t <= 8; ++t) {  // R bits 4..7
@@ -334,8 +334,9 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
 #pragma unroll
       for (int k = 0; k < 16; ++k) __stcs(&ysig[(m1_g + 16 * k) * 256 + q], A::to(v[k]));
     }
-    if (sig + step < batch) release_storage<T>(c);
-  }
+  };
+
+  pp.run(&tmx, batch, phaseA, phaseB);
 }
 
 // DIF (DESIGN.md convention): stages s = 16..2 with top = a + b, bot = W ⊙ (a − b),
@@ -357,32 +358,23 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
   using C4 = typename P::C4;
   constexpr int TC = P::TC, COLS = P::COLS, NG = P::NG, GT = P::GT, TPG = P::TPG;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  Ctx<T> c;
-  ctx_init<T>(c, smem_raw, stage);
-  const int gbar = 1 + c.gi;
-  const int m1_cc = c.gt % TC, m1_g = c.gt / TC;
-  const int m2_g = c.gt & 15, m2_cc = c.gt >> 4;
-  C2 *wk = c.work + c.gi * 256 * TC;
-  C4 *twA = c.twA;
+  Pipe<T> pp;
+  pp.init(smem_raw, stage);
+  const int gbar = 1 + pp.gi;
+  const int m1_cc = pp.gt % TC, m1_g = pp.gt / TC;
+  const int m2_g = pp.gt & 15, m2_cc = pp.gt >> 4;
+  const C4 *twA = pp.twA;
   const int rg1 = rev4(m1_g);
 
-  uint32_t tile_it = 0, sig_it = 0;
-  if ((P::SPLIT ? c.cid : c.cid * NG + c.gi) < batch)
-    tma_tile<T>(c, &tmx, P::SPLIT ? c.cid : c.cid * NG + c.gi, P::SPLIT ? c.gi : 0);
-  release_storage<T>(c);
-
-  const int64_t sig0 = P::SPLIT ? c.cid : c.cid * NG + c.gi;
-  const int64_t step = P::SPLIT ? c.ncl : c.ncl * NG;
-  for (int64_t sig = sig0; sig < batch; sig += step, ++sig_it) {
-    if (storage_leader<T>(c)) sa_mbar_expect_tx(c.full_bar, (uint32_t)P::INTER1);
-    // ------------------------------------------------------------- phase 1
-    for (int u = 0; u < TPG; ++u, ++tile_it) {
-      const int tt = P::SPLIT ? c.gi + NG * u : u;
-      const int q = c.rank * COLS + tt * TC + m1_cc;
+  auto phaseA = [&](int64_t sig, int b, uint32_t use, int64_t nsig) {
+    for (int u = 0; u < TPG; ++u) {
+      const int tt = pp.gi + NG * u;
+      const int q = pp.rank * COLS + tt * TC + m1_cc;
       const bool gen = special_column(q);
       C2 wf[30];
       if (!gen) load_wf<T>(wf, stage2, q, m1_g);
-      sa_mbar_wait(&c.tma_bar[c.gi], tile_it & 1);
+      pp.wait_tile();
+      C2 *wk = pp.work();
       V v[16];
 #pragma unroll
       for (int k = 0; k < 16; ++k) {  // R = g + 16k
@@ -416,8 +408,8 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
 #pragma unroll
       for (int k = 0; k < 16; ++k) v[k] = A::from(wk[(m1_g * 16 + k) * TC + m1_cc]);  // R = 16g + k
       group_sync(gbar, GT);  // tile buffer consumed: re-arm it
-      if (u + 1 < TPG) tma_tile<T>(c, &tmx, sig, P::SPLIT ? tt + NG : tt + 1);
-      else if (sig + step < batch) tma_tile<T>(c, &tmx, sig + step, P::SPLIT ? c.gi : 0);
+      if (u + 1 < TPG) pp.tma(&tmx, sig, tt + NG);
+      else if (nsig < batch) pp.tma(&tmx, nsig, pp.gi);
       if (gen) {
 #pragma unroll
         for (int t = 4; t >= 1; --t) {  // R bits 3..0
@@ -438,24 +430,27 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
             if (!(k & h)) r_dif_fast<T>(v[k], v[k + h], wf[h - 1 + (k & (h - 1))]);
         }
       }
-      if (u == 0) sa_mbar_wait(c.empty_bar, sig_it & 1);
+      if (u == 0) sa_mbar_wait(&pp.empty_bar[b], use & 1);
 #pragma unroll
       for (int k = 0; k < 16; ++k) {  // row R = 16g + k -> CTA owning cr = rev8(R), local row cr mod COLS
         const int cr = crev4(k) * 16 + rg1;
         const int lr = cr % COLS;
-        sa_st_async(c.inter_rank[cr / COLS] + (uint32_t)(sizeof(C2) * (lr * 256 + (q ^ (lr & 15)))),
-                    A::to(v[k]), c.full_rank[cr / COLS]);
+        sa_st_async(pp.peer_inter(b, cr / COLS, (uint32_t)(sizeof(C2) * (lr * 256 + (q ^ (lr & 15))))),
+                    A::to(v[k]), pp.peer_full(b, cr / COLS));
       }
     }
-    sa_mbar_wait(c.full_bar, sig_it & 1);
-    // ------------------------------------------------------------- phase 2
+  };
+
+  auto phaseB = [&](int64_t sig, int b, uint32_t use) {
+    C2 *inter = pp.inter(b);
     C2 *ysig = y + sig * NN;
+    sa_mbar_wait(&pp.full_bar[b], use & 1);
     for (int u = 0; u < TPG; ++u) {
-      const int tt = P::SPLIT ? c.gi + NG * u : u;
+      const int tt = pp.gi + NG * u;
       V v[16];
       {  // round 1 (M2: g fastest): q = g + 16k ; stages 8..5
         const int lr = tt * TC + m2_cc;
-        C2 *row = c.inter + lr * 256;
+        C2 *row = inter + lr * 256;
         const int sw = lr & 15;
 #pragma unroll
         for (int k = 0; k < 16; ++k) v[k] = A::from(row[(m2_g + 16 * k) ^ sw]);
@@ -472,7 +467,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
       group_sync(gbar, GT);
       {  // round 2 (M1: cc fastest): q = 16g + k ; stages 4..2 + 2-point ; bit-reversed store
         const int lr = tt * TC + m1_cc;
-        const C2 *row = c.inter + lr * 256;
+        const C2 *row = inter + lr * 256;
         const int sw = lr & 15;
 #pragma unroll
         for (int k = 0; k < 16; ++k) v[k] = A::from(row[(m1_g * 16 + k) ^ sw]);
@@ -498,14 +493,15 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
           }
 #pragma unroll
         for (int k = 0; k < 16; k += 2) r_two_point<T>(v[k], v[k + 1]);
-        const int cr = c.rank * COLS + lr;
+        const int cr = pp.rank * COLS + lr;
         const int rg = rev4(m1_g);
 #pragma unroll
         for (int k = 0; k < 16; ++k) __stcs(&ysig[(crev4(k) * 16 + rg) * 256 + cr], A::to(v[k]));
       }
     }
-    if (sig + step < batch) release_storage<T>(c);
-  }
+  };
+
+  pp.run(&tmx, batch, phaseA, phaseB);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
