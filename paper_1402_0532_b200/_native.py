@@ -14,6 +14,8 @@ from .errors import ContractError, DomainError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsignadd_b200.so")
+if os.environ.get("SA_LIB_PATH"):  # development: time an alternative build of the library
+    LIB_PATH = os.environ["SA_LIB_PATH"]
 
 SA_C64, SA_C128 = 0, 1
 SA_NDFT_FAST, SA_NDFT_EXACT = 0, 1

@@ -131,24 +131,32 @@ __global__ void __launch_bounds__(256) k_lag_integrate_fast(
     const int base = t0 + (LAGS_PER_CTA - 1) - LAGS_PER_WARP * warp - (LAGS_PER_WARP - 1);
 #pragma unroll
     for (int u = 0; u < 15; ++u) c[u] = rs[pad8(base + u)];
+    // Consecutive FMAs share the surveillance operand (register-reuse cache)
+    // and walk the 8 lags; per lag the terms add in the order
+    //   Re: scr*sr, ssr*cr, -sci*si, -ssi*ci ;  Im: scr*si, ssi*cr, ssr*ci, sci*sr.
 #pragma unroll
-    for (int j = 0; j < LAGS_PER_WARP; ++j) {
-      T ar = accr[j], ai = acci[j];
+    for (int i = 0; i < 8; ++i) {
+      const C4<T> &s = a[i];  // {sr, si, sgn sr, sgn si}; reference c[i-j+7] = {cr, ci, sgn cr, sgn ci}
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const C4<T> &s = a[i];      // {sr, si, sgn sr, sgn si}
-        const C4<T> &r = c[i - j + 7];  // {cr, ci, sgn cr, sgn ci}
-        ar = sa_fma(r.z, s.x, ar);
-        ar = sa_fma(s.z, r.x, ar);
-        ar = sa_fma(-r.w, s.y, ar);
-        ar = sa_fma(-s.w, r.y, ar);
-        ai = sa_fma(r.z, s.y, ai);
-        ai = sa_fma(s.w, r.x, ai);
-        ai = sa_fma(s.z, r.y, ai);
-        ai = sa_fma(r.w, s.x, ai);
+      for (int j = 0; j < LAGS_PER_WARP; ++j) {
+        accr[j] = sa_fma(s.x, c[i - j + 7].z, accr[j]);
+        acci[j] = sa_fma(s.y, c[i - j + 7].z, acci[j]);
       }
-      accr[j] = ar;
-      acci[j] = ai;
+#pragma unroll
+      for (int j = 0; j < LAGS_PER_WARP; ++j) {
+        accr[j] = sa_fma(s.z, c[i - j + 7].x, accr[j]);
+        acci[j] = sa_fma(s.w, c[i - j + 7].x, acci[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < LAGS_PER_WARP; ++j) {
+        accr[j] = sa_fma(s.y, -c[i - j + 7].w, accr[j]);
+        acci[j] = sa_fma(s.z, c[i - j + 7].y, acci[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < LAGS_PER_WARP; ++j) {
+        accr[j] = sa_fma(s.w, -c[i - j + 7].y, accr[j]);
+        acci[j] = sa_fma(s.x, c[i - j + 7].w, acci[j]);
+      }
     }
   }
 #pragma unroll

@@ -134,9 +134,10 @@ __global__ void __launch_bounds__(NDFT_THREADS)
       C4<T> d[TB];
 #pragma unroll
       for (int i = 0; i < TB; ++i) d[i] = cur[mm * BV + swz(mm, lane + 32 * i)];
+      C4<T> w[TK];
 #pragma unroll
       for (int kk = 0; kk < TK; ++kk) {
-        C4<T> w = TW_SMEM ? tws[idx[kk]] : sa_ldg(&quad[idx[kk]]);
+        w[kk] = TW_SMEM ? tws[idx[kk]] : sa_ldg(&quad[idx[kk]]);
         int nx = idx[kk] + kst[kk];
         if (POW2) {
           nx &= n - 1;
@@ -144,20 +145,31 @@ __global__ void __launch_bounds__(NDFT_THREADS)
           nx = nx >= n ? nx - n : nx;
         }
         idx[kk] = nx;
+      }
+      // d = {xr, xi, sgn xr, sgn xi} ; w = {Wr, Wi, sgn Wr, sgn Wi}.  Consecutive
+      // FMAs share the data operand (register-reuse cache, see the f32x2 kernel);
+      // per accumulator the terms add in the same order as before.
 #pragma unroll
-        for (int i = 0; i < TB; ++i) {
-          // d = {xr, xi, sgn xr, sgn xi} ; w = {Wr, Wi, sgn Wr, sgn Wi}
-          T ar = accr[kk][i], ai = acci[kk][i];
-          ar = sa_fma(d[i].z, w.x, ar);
-          ar = sa_fma(w.z, d[i].x, ar);
-          ar = sa_fma(-d[i].w, w.y, ar);
-          ar = sa_fma(-w.w, d[i].y, ar);
-          ai = sa_fma(d[i].z, w.y, ai);
-          ai = sa_fma(w.w, d[i].x, ai);
-          ai = sa_fma(d[i].w, w.x, ai);
-          ai = sa_fma(w.z, d[i].y, ai);
-          accr[kk][i] = ar;
-          acci[kk][i] = ai;
+      for (int i = 0; i < TB; ++i) {
+#pragma unroll
+        for (int kk = 0; kk < TK; ++kk) {
+          accr[kk][i] = sa_fma(d[i].z, w[kk].x, accr[kk][i]);
+          acci[kk][i] = sa_fma(d[i].z, w[kk].y, acci[kk][i]);
+        }
+#pragma unroll
+        for (int kk = 0; kk < TK; ++kk) {
+          accr[kk][i] = sa_fma(d[i].x, w[kk].z, accr[kk][i]);
+          acci[kk][i] = sa_fma(d[i].x, w[kk].w, acci[kk][i]);
+        }
+#pragma unroll
+        for (int kk = 0; kk < TK; ++kk) {
+          accr[kk][i] = sa_fma(d[i].w, -w[kk].y, accr[kk][i]);
+          acci[kk][i] = sa_fma(d[i].w, w[kk].x, acci[kk][i]);
+        }
+#pragma unroll
+        for (int kk = 0; kk < TK; ++kk) {
+          accr[kk][i] = sa_fma(d[i].y, -w[kk].w, accr[kk][i]);
+          acci[kk][i] = sa_fma(d[i].y, w[kk].z, acci[kk][i]);
         }
       }
     }
@@ -184,22 +196,35 @@ __global__ void __launch_bounds__(NDFT_THREADS)
 // ⊙-accumulate lane-ops of the scalar kernel's 32 FFMA), halving issue slots so
 // the FMA pipe, not instruction issue/dispatch, is the limit.  smem chunk layout
 // per (m, pair p): D0 = {xr_a, xr_b, xi_a, xi_b}, D1 = {sxr_a, sxr_b, sxi_a, sxi_b}.
+template <int TP_, int TK_, int NC_> struct F2Cfg {
+  static constexpr int TP = TP_;  // vector pairs per lane
+  static constexpr int TK = TK_;  // bins per thread
+  static constexpr int NCH = NC_; // samples per staged chunk
+  static constexpr int BP = 32 * TP;            // pairs per CTA
+  static constexpr int BV = 2 * BP;             // vectors per CTA
+  static constexpr int BK = NDFT_WARPS * TK;    // bins per CTA
+  static constexpr size_t STAGE_BYTES = 2 * 2 * NCH * BP * sizeof(float4);
+};
+#ifndef SA_F2_TP  // tile shape (vector pairs per lane, bins per thread, chunk); -D for sweeps
+#define SA_F2_TP 2
+#define SA_F2_TK 8
+#define SA_F2_NC 16
+#endif
+using F2 = F2Cfg<SA_F2_TP, SA_F2_TK, SA_F2_NC>;  // default: 128 vectors x 64 bins per CTA
+
 template <bool POW2, bool TW_SMEM>
 __global__ void __launch_bounds__(NDFT_THREADS)
     k_ndft_fast_f32x2(const float2 *__restrict__ x, float2 *__restrict__ y, int64_t batch, int n,
                       const float4 *__restrict__ quad, float gain, bool use_gain) {
   using A = Ar<float>;
   using V = A::V;
-  constexpr int TP = 2;                 // vector pairs per lane
-  constexpr int TK = 8;                 // bins per thread
-  constexpr int BP = 32 * TP;           // pairs per CTA
-  constexpr int BV = 2 * BP;            // vectors per CTA (128)
-  constexpr int BK = NDFT_WARPS * TK;   // bins per CTA (64)
-  constexpr int PER_T = BP * NC / NDFT_THREADS;  // (pair, m) loads per thread per chunk
+  constexpr int TP = F2::TP, TK = F2::TK, NCH = F2::NCH, BP = F2::BP, BV = F2::BV, BK = F2::BK;
+  constexpr int PER_T = BP * NCH / NDFT_THREADS;  // (pair, m) loads per thread per chunk
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  float4 *d0 = reinterpret_cast<float4 *>(smem_raw);  // [2][NC][BP]
-  float4 *d1 = d0 + 2 * NC * BP;                       // [2][NC][BP]
-  float4 *tws = d1 + 2 * NC * BP;                      // [n] (TW_SMEM)
+  float4 *d0 = reinterpret_cast<float4 *>(smem_raw);  // [2][NCH][BP] {xr_a, xr_b, xi_a, xi_b}
+  float4 *d1 = d0 + 2 * NCH * BP;                      // [2][NCH][BP] signs
+  float4 *tws = d1 + 2 * NCH * BP;                     // [n] (TW_SMEM)
+  const unsigned char *twb = reinterpret_cast<const unsigned char *>(tws);
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t v0 = (int64_t)blockIdx.y * BV;
@@ -233,8 +258,8 @@ __global__ void __launch_bounds__(NDFT_THREADS)
         a = {sa_mul(gain, a.x), sa_mul(gain, a.y)};
         b = {sa_mul(gain, b.x), sa_mul(gain, b.y)};
       }
-      d0[(buf * NC + mm) * BP + p] = {a.x, b.x, a.y, b.y};
-      d1[(buf * NC + mm) * BP + p] = {sa_sgn(a.x), sa_sgn(b.x), sa_sgn(a.y), sa_sgn(b.y)};
+      d0[(buf * NCH + mm) * BP + p] = {a.x, b.x, a.y, b.y};
+      d1[(buf * NCH + mm) * BP + p] = {sa_sgn(a.x), sa_sgn(b.x), sa_sgn(a.y), sa_sgn(b.y)};
     }
   };
 
@@ -243,23 +268,25 @@ __global__ void __launch_bounds__(NDFT_THREADS)
   for (int kk = 0; kk < TK; ++kk)
 #pragma unroll
     for (int i = 0; i < TP; ++i) accr[kk][i] = acci[kk][i] = 0ull;
-  int idx[TK], kst[TK];
+  // twiddle byte offsets (k*m mod n) * 16 for the current m, stepped by k*16
+  int off[TK], kst[TK];
 #pragma unroll
   for (int kk = 0; kk < TK; ++kk) {
-    idx[kk] = 0;
-    kst[kk] = (kbase + kk) % n;
+    off[kk] = 0;
+    kst[kk] = ((kbase + kk) % n) * (int)sizeof(float4);
   }
-  const int nchunks = (n + NC - 1) / NC;
+  const int nb = n * (int)sizeof(float4);
+  const int nchunks = (n + NCH - 1) / NCH;
   float2 pre[PER_T][2];
   ld_chunk(0, pre);
   st_chunk(0, pre);
   __syncthreads();
   for (int c = 0; c < nchunks; ++c) {
     const int buf = c & 1;
-    if (c + 1 < nchunks) ld_chunk((c + 1) * NC, pre);
-    const float4 *c0 = d0 + buf * NC * BP;
-    const float4 *c1 = d1 + buf * NC * BP;
-    const int mlim = min(NC, n - c * NC);
+    if (c + 1 < nchunks) ld_chunk((c + 1) * NCH, pre);
+    const float4 *c0 = d0 + buf * NCH * BP;
+    const float4 *c1 = d1 + buf * NCH * BP;
+    const int mlim = min(NCH, n - c * NCH);
 #pragma unroll 2
     for (int mm = 0; mm < mlim; ++mm) {
       V xr[TP], xi[TP], sr[TP], si[TP];
@@ -272,29 +299,43 @@ __global__ void __launch_bounds__(NDFT_THREADS)
         sr[i] = A::pack(b.x, b.y);
         si[i] = A::pack(b.z, b.w);
       }
+      float4 w[TK];
 #pragma unroll
       for (int kk = 0; kk < TK; ++kk) {
-        float4 w = TW_SMEM ? tws[idx[kk]] : __ldg(&quad[idx[kk]]);
-        int nx = idx[kk] + kst[kk];
-        if (POW2) nx &= n - 1;
-        else nx = nx >= n ? nx - n : nx;
-        idx[kk] = nx;
-        const V wr = A::pack(w.x, w.x), wi = A::pack(w.y, w.y), swr = A::pack(w.z, w.z),
-                swi = A::pack(w.w, w.w), nwi = A::pack(-w.y, -w.y), nswi = A::pack(-w.w, -w.w);
+        w[kk] = TW_SMEM ? *reinterpret_cast<const float4 *>(twb + off[kk])
+                        : __ldg(reinterpret_cast<const float4 *>(
+                              reinterpret_cast<const unsigned char *>(quad) + off[kk]));
+        int nx = off[kk] + kst[kk];
+        if (POW2) nx &= nb - 1;
+        else nx = nx >= nb ? nx - nb : nx;
+        off[kk] = nx;
+      }
+      // Operand order for the register-reuse cache: consecutive FFMA2 share the
+      // data pair (slot a) and differ in twiddle scalar and accumulator, so each
+      // reads one 64-bit and one 32-bit register -- within the 2-cycle pipe slot.
+      // Per accumulator the terms still add in the order
+      //   Re: sxr*Wr, xr*sWr, -sxi*Wi, -xi*sWi ;  Im: sxr*Wi, xr*sWi, sxi*Wr, xi*sWr.
 #pragma unroll
-        for (int i = 0; i < TP; ++i) {
-          // Re += sxr*Wr + sWr*xr - sxi*Wi - sWi*xi ; Im += sxr*Wi + sWi*xr + sxi*Wr + sWr*xi
-          V ar = accr[kk][i], ai = acci[kk][i];
-          ar = A::fma(sr[i], wr, ar);
-          ar = A::fma(swr, xr[i], ar);
-          ar = A::fma(si[i], nwi, ar);
-          ar = A::fma(nswi, xi[i], ar);
-          ai = A::fma(sr[i], wi, ai);
-          ai = A::fma(swi, xr[i], ai);
-          ai = A::fma(si[i], wr, ai);
-          ai = A::fma(swr, xi[i], ai);
-          accr[kk][i] = ar;
-          acci[kk][i] = ai;
+      for (int i = 0; i < TP; ++i) {
+#pragma unroll
+        for (int kk = 0; kk < TK; ++kk) {
+          accr[kk][i] = A::fma(sr[i], A::pack(w[kk].x, w[kk].x), accr[kk][i]);
+          acci[kk][i] = A::fma(sr[i], A::pack(w[kk].y, w[kk].y), acci[kk][i]);
+        }
+#pragma unroll
+        for (int kk = 0; kk < TK; ++kk) {
+          accr[kk][i] = A::fma(xr[i], A::pack(w[kk].z, w[kk].z), accr[kk][i]);
+          acci[kk][i] = A::fma(xr[i], A::pack(w[kk].w, w[kk].w), acci[kk][i]);
+        }
+#pragma unroll
+        for (int kk = 0; kk < TK; ++kk) {
+          accr[kk][i] = A::fma(si[i], A::pack(-w[kk].y, -w[kk].y), accr[kk][i]);
+          acci[kk][i] = A::fma(si[i], A::pack(w[kk].x, w[kk].x), acci[kk][i]);
+        }
+#pragma unroll
+        for (int kk = 0; kk < TK; ++kk) {
+          accr[kk][i] = A::fma(xi[i], A::pack(-w[kk].w, -w[kk].w), accr[kk][i]);
+          acci[kk][i] = A::fma(xi[i], A::pack(w[kk].z, w[kk].z), acci[kk][i]);
         }
       }
     }
@@ -378,13 +419,14 @@ int launch(const void *xv, void *yv, int64_t batch, int64_t n64, const SaTwiddle
     SA_LAUNCH_CHECK();
     return SA_OK;
   }
-  constexpr int BV = 32 * NdftCfg<T>::TB;
-  constexpr int BK = NDFT_WARPS * NdftCfg<T>::TK;
+  // fp32: packed FFMA2 kernel (F2 tile); fp64: scalar DFMA kernel (NdftCfg tile)
+  constexpr bool F32X2 = sizeof(T) == 4;
+  constexpr int BV = F32X2 ? F2::BV : 32 * NdftCfg<T>::TB;
+  constexpr int BK = F32X2 ? F2::BK : NDFT_WARPS * NdftCfg<T>::TK;
   const bool pow2 = (n & (n - 1)) == 0;
   const bool tw_smem = (size_t)n * sizeof(C4<T>) <= 64 * 1024;
-  size_t bytes = sizeof(C4<T>) * (2 * NC * BV + (tw_smem ? n : 0));
-  // fp32: packed FFMA2 kernel (same tile: 128 vectors x 64 bins, same smem bytes)
-  constexpr bool F32X2 = sizeof(T) == 4;
+  size_t bytes = (F32X2 ? F2::STAGE_BYTES : sizeof(C4<T>) * 2 * NC * BV) +
+                 sizeof(C4<T>) * (tw_smem ? n : 0);
   const C4<T> *quad = (const C4<T> *)tw->quad;
   int64_t vblocks = (batch + BV - 1) / BV;
   unsigned kblocks = (unsigned)((n + BK - 1) / BK);
