@@ -208,12 +208,15 @@ template <int TP_, int TK_, int NC_> struct F2Cfg {
 #ifndef SA_F2_TP  // tile shape (vector pairs per lane, bins per thread, chunk); -D for sweeps
 #define SA_F2_TP 2
 #define SA_F2_TK 8
-#define SA_F2_NC 16
+#define SA_F2_NC 8
 #endif
 using F2 = F2Cfg<SA_F2_TP, SA_F2_TK, SA_F2_NC>;  // default: 128 vectors x 64 bins per CTA
 
+#ifndef SA_F2_MINB
+#define SA_F2_MINB 2
+#endif
 template <bool POW2, bool TW_SMEM>
-__global__ void __launch_bounds__(NDFT_THREADS)
+__global__ void __launch_bounds__(NDFT_THREADS, SA_F2_MINB)
     k_ndft_fast_f32x2(const float2 *__restrict__ x, float2 *__restrict__ y, int64_t batch, int n,
                       const float4 *__restrict__ quad, float gain, bool use_gain) {
   using A = Ar<float>;
