@@ -350,10 +350,11 @@ def wl_map(args, ws, rank, c5=False):
     full = torch.empty((L, M), dtype=cdt, device="cuda") if (ws > 1 and rank == 0) else None
 
     def step():
-        sa.ambiguity_map(surv, ref, rows, M, l0=l0, out=out, workspace=ws_buf)
-        if ws > 1:
-            import torch.distributed as dist
-            dist.gather(out, [full[i * rows:(i + 1) * rows] for i in range(ws)] if rank == 0 else None, dst=0)
+        if ws > 1:  # delay-bin shard + NCCL gather of the row blocks to rank 0
+            from paper_1402_0532_b200.sharded import ambiguity_map_sharded
+            ambiguity_map_sharded(surv, ref, L, M, out_full=full, out_local=out, workspace=ws_buf)
+        else:
+            sa.ambiguity_map(surv, ref, rows, M, l0=l0, out=out, workspace=ws_buf)
 
     z = torch.empty((rows, M), dtype=cdt, device="cuda")
     from paper_1402_0532_b200 import _native

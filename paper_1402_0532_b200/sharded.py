@@ -26,6 +26,12 @@ def shard_rows(l_bins: int, world: int, rank: int) -> tuple[int, int]:
     return first, count
 
 
+def _wire(t):
+    """NCCL has no complex types: collectives move the interleaved (re, im) view."""
+    import torch
+    return torch.view_as_real(t) if t is not None and t.is_complex() else t
+
+
 def gather_rows(local, full, l_bins: int, group=None, dst: int = 0):
     """Gather every rank's row block into ``full`` (L x M) on ``dst``.
 
@@ -37,10 +43,10 @@ def gather_rows(local, full, l_bins: int, group=None, dst: int = 0):
     sizes = [shard_rows(l_bins, world, r)[1] for r in range(world)]
     if len(set(sizes)) == 1:
         if rank == dst:
-            parts = [full[shard_rows(l_bins, world, r)[0]:][: sizes[r]] for r in range(world)]
-            dist.gather(local, parts, dst=dst, group=group)
+            parts = [_wire(full[shard_rows(l_bins, world, r)[0]:][: sizes[r]]) for r in range(world)]
+            dist.gather(_wire(local), parts, dst=dst, group=group)
         else:
-            dist.gather(local, None, dst=dst, group=group)
+            dist.gather(_wire(local), None, dst=dst, group=group)
         return full if rank == dst else None
     if rank == dst:
         for r in range(world):
@@ -48,10 +54,10 @@ def gather_rows(local, full, l_bins: int, group=None, dst: int = 0):
             if r == dst:
                 full[f:f + c].copy_(local)
             elif c:
-                dist.recv(full[f:f + c], src=r, group=group)
+                dist.recv(_wire(full[f:f + c]), src=r, group=group)
         return full
     if local.shape[0]:
-        dist.send(local, dst=dst, group=group)
+        dist.send(_wire(local), dst=dst, group=group)
     return None
 
 
@@ -81,6 +87,6 @@ def ambiguity_map_sharded(surv, ref, l_bins: int, m: int, *, gain: float = 1.0,
 def broadcast_inputs(surv, ref, src: int = 0, group=None):
     """ncclBroadcast of the two input streams from ``src``."""
     import torch.distributed as dist
-    dist.broadcast(surv, src=src, group=group)
-    dist.broadcast(ref, src=src, group=group)
+    dist.broadcast(_wire(surv), src=src, group=group)
+    dist.broadcast(_wire(ref), src=src, group=group)
     return surv, ref

@@ -323,3 +323,65 @@ def test_nfft64k_persistent_loop(sa, dt):
     xd = dev(xs)
     sa.nfft_batch(xd, out=xd)
     assert_value_equal(xd.cpu().numpy(), oracle.nfft(xs, "dit", dtype=od, nthreads=8))
+
+
+def test_map_c5_sampled_rows(sa):
+    """C5 (2^22 samples, 8 targets), 4096 delay bins x 2048 Doppler bins, c64 on
+    the GPU; the fp64 oracle of the same complex64 inputs on the target rows and
+    the edge rows; a row range computed alone equals the same rows of the full map
+    bit for bit (the delay-bin sharding invariant)."""
+    from paper_1402_0532_b200.workloads import c5_scene
+    sc = c5_scene()
+    surv = sc.surv.astype(np.complex64)
+    ref = sc.ref.astype(np.complex64)
+    ds, dr = dev(surv), dev(ref)
+    full = sa.ambiguity_map(ds, dr, 4096, 2048)
+    assert full.shape == (4096, 2048)
+    rows = sorted(set([0, 4095] + [int(t) for t in sc.delays[:3]]))
+    y = full[T().tensor(rows, device=full.device)].cpu().numpy()
+    s128, r128 = surv.astype(np.complex128), ref.astype(np.complex128)
+    for i, l in enumerate(rows):
+        assert_literal(y[i:i + 1], oracle.ambiguity_map(s128, r128, l, 1, 2048, nthreads=8), TOL_F32)
+    part = sa.ambiguity_map(ds, dr, 512, 2048, l0=1536)
+    assert T().equal(part, full[1536:2048])
+
+
+def _sharded_worker(port, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        import paper_1402_0532_b200 as sa
+        from paper_1402_0532_b200.sharded import ambiguity_map_sharded, broadcast_inputs
+        from paper_1402_0532_b200.workloads import radar_scene
+        sc = radar_scene(1 << 16, 2, 4242)
+        ds = torch.from_numpy(sc.surv.astype(np.complex64)).cuda()
+        dr = torch.from_numpy(sc.ref.astype(np.complex64)).cuda()
+        broadcast_inputs(ds, dr)
+        full = ambiguity_map_sharded(ds, dr, 96, 128)
+        direct = sa.ambiguity_map(ds, dr, 96, 128)
+        q.put(bool(torch.equal(full, direct)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_map_nccl_single_rank(sa):
+    """The multi-GPU map path (NCCL broadcast, delay-bin shard, NCCL gather) on
+    one GPU in a world of 1: the gathered map equals the single-call map."""
+    import socket
+    import torch.multiprocessing as mp
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_sharded_worker, args=(port, q))
+    p.start()
+    p.join(300)
+    assert p.exitcode == 0
+    assert q.get(timeout=10) is True
