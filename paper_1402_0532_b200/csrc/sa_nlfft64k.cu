@@ -31,18 +31,33 @@ namespace {
 constexpr int LOGN = 16;
 constexpr int NN = 1 << LOGN;
 
+#ifndef SA_GREL
+#define SA_GREL 1
+#endif
+#ifndef SA_LOCALQ
+#define SA_LOCALQ 1  // the CTA's own share of the scatter: st.shared + warp arrivals
+#endif
+#ifndef SA_K64F_TC
+#define SA_K64F_TC 16
+#define SA_K64F_CL 4
+#define SA_K64F_NG 2
+#define SA_K64F_MINB 1
+#endif
+
 template <typename T> struct K64;
 template <> struct K64<float> {
-  static constexpr int TC = 16;  // columns per tile
-  static constexpr int CL = 4;   // cluster size
-  static constexpr int NG = 2;   // thread groups per CTA
-  static constexpr int NS = 1;   // node storages (2 = pipelined signals; needs CL >= 8 for c64)
+  static constexpr int TC = SA_K64F_TC;  // columns per tile
+  static constexpr int CL = SA_K64F_CL;  // cluster size
+  static constexpr int NG = SA_K64F_NG;  // thread groups per CTA
+  static constexpr int NS = 1;           // node storages (2 = pipelined signals; needs CL >= 8 for c64)
+  static constexpr int MINB = SA_K64F_MINB;  // resident CTAs per SM
 };
 template <> struct K64<double> {
   static constexpr int TC = 8;
   static constexpr int CL = 8;
   static constexpr int NG = 2;
   static constexpr int NS = 1;
+  static constexpr int MINB = 1;
 };
 
 template <typename T> struct L64 {
@@ -92,6 +107,10 @@ SA_HD void load_wf(typename Ar<T>::C2 (&wf)[30], const typename Ar<T>::C2 *__res
     for (int a = 0; a < (1 << (t - 5)); ++a)
       wf[15 + (1 << (t - 5)) - 1 + a] = sa_ldg(&stage2[(1 << (7 + t)) - 1 + (g + 16 * a) * 256 + q]);
 }
+// general form {|wr|, |wi|, sgn wr, sgn wi} (as the stage table) of a raw twiddle
+template <typename T> SA_HD typename Ar<T>::C4 c4of(const typename Ar<T>::C2 &w) {
+  return {fabs(w.x), fabs(w.y), sa_sgn(w.x), sa_sgn(w.y)};
+}
 SA_HD bool special_column(int q) { return __any_sync(0xffffffffu, q == 0 || q == 128); }
 
 // Shared per-CTA state and the signal pipeline orchestration of both kernels.
@@ -107,6 +126,13 @@ template <typename T> struct Pipe {
   uint32_t tile_it = 0;
 
   SA_HD C2 *inter(int b) const { return reinterpret_cast<C2 *>(smem + b * P::INTER1); }
+  // after a thread's last local scatter store of a signal: its warp's arrive on full[b]
+  SA_HD void local_done(int b) const {
+    if (SA_LOCALQ) {
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) sa_mbar_arrive_local(&full_bar[b]);
+    }
+  }
   SA_HD C2 *work() const { return reinterpret_cast<C2 *>(smem + P::OFF_WORK + gi * P::WORK); }
   // cluster-window address of peer r's node storage b (byte offset off) / its full mbarrier
   SA_HD uint32_t peer_inter(int b, int r, uint32_t off) const {
@@ -130,8 +156,9 @@ template <typename T> struct Pipe {
     if (threadIdx.x == 0) {
       for (int g = 0; g < P::NG; ++g) sa_mbar_init(&tma_bar[g], 1);
       for (int b = 0; b < P::NS; ++b) {
-        sa_mbar_init(&full_bar[b], 1);       // expect_tx(INTER1) once per use
-        sa_mbar_init(&empty_bar[b], P::CL);  // one remote arrive per peer per use
+        // expect_tx(remote bytes) once per use (+ one arrive per warp for the local share)
+        sa_mbar_init(&full_bar[b], 1 + (SA_LOCALQ ? P::THREADS / 32 : 0));
+        sa_mbar_init(&empty_bar[b], SA_GREL ? P::CL * P::NG : P::CL);  // remote arrives per use
       }
       sa_fence_mbar_init();
     }
@@ -150,11 +177,16 @@ template <typename T> struct Pipe {
     sa_mbar_wait(&tma_bar[gi], tile_it & 1);
     ++tile_it;
   }
-  // "storage b may be overwritten": the CTA finished reading it, one thread
-  // arrives on every peer's empty barrier for b.
+  // "storage b may be overwritten": the CTA (SA_GREL: this thread group)
+  // finished reading it; one thread arrives on every peer's empty barrier for b.
   SA_HD void release(int b) const {
+#if SA_GREL
+    group_sync(1 + gi, P::GT);
+    if (gt == 0)
+#else
     __syncthreads();
     if (threadIdx.x == 0)
+#endif
 #pragma unroll
       for (int r = 0; r < P::CL; ++r) sa_mbar_arrive_remote(sa_mapa(sa_smem_u32(&empty_bar[b]), r));
   }
@@ -167,7 +199,8 @@ template <typename T> struct Pipe {
     int64_t i = 0;
     for (int64_t sig = cid; sig < batch; sig += ncl, ++i) {
       const int b = (int)(i % P::NS);
-      if (threadIdx.x == 0) sa_mbar_expect_tx(&full_bar[b], (uint32_t)P::INTER1);
+      if (threadIdx.x == 0)
+        sa_mbar_expect_tx(&full_bar[b], (uint32_t)(SA_LOCALQ ? P::INTER1 - P::INTER1 / P::CL : P::INTER1));
       phaseA(sig, b, (uint32_t)(i / P::NS), sig + ncl);
       if (P::NS == 1) {
         phaseB(sig, 0, (uint32_t)i);
@@ -184,7 +217,7 @@ template <typename T> struct Pipe {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(L64<T>::THREADS, 1)
+__global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
     k_nlfft64k_dit(const __grid_constant__ CUtensorMap tmx, typename Ar<T>::C2 *__restrict__ y,
                    int64_t batch, const typename Ar<T>::C4 *__restrict__ stage,
                    const typename Ar<T>::C2 *__restrict__ stage2, T gain, int use_gain) {
@@ -261,10 +294,13 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
       const int R = rev8(pp.rank * COLS + tt * TC + m2_cc);
       constexpr int KPC = COLS / 16;  // registers per owner CTA
 #pragma unroll
-      for (int k = 0; k < 16; ++k)
-        sa_st_async(pp.peer_inter(b, k / KPC, (uint32_t)(sizeof(C2) * (R * COLS + m2_g + 16 * (k % KPC)))),
-                    A::to(v[k]), pp.peer_full(b, k / KPC));
+      for (int k = 0; k < 16; ++k) {
+        const int e = R * COLS + m2_g + 16 * (k % KPC);
+        if (SA_LOCALQ && k / KPC == pp.rank) pp.inter(b)[e] = A::to(v[k]);
+        else sa_st_async(pp.peer_inter(b, k / KPC, (uint32_t)(sizeof(C2) * e)), A::to(v[k]), pp.peer_full(b, k / KPC));
+      }
     }
+    pp.local_done(b);
   };
 
   auto phaseB = [&](int64_t sig, int b, uint32_t use) {
@@ -273,7 +309,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
     C2 wf[30];
     {
       const int q0 = pp.rank * COLS + pp.gi * TC + m1_cc;  // independent of the node storage
-      if (!special_column(q0)) load_wf<T>(wf, stage2, q0, m1_g);
+      load_wf<T>(wf, stage2, q0, m1_g);
     }
     sa_mbar_wait(&pp.full_bar[b], use & 1);  // all INTER1 bytes of this signal landed
     for (int u = 0; u < TPG; ++u) {
@@ -281,20 +317,17 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
       const int lq = tt * TC + m1_cc;
       const int q = pp.rank * COLS + lq;
       const bool gen = special_column(q);
-      if (u > 0 && !gen) load_wf<T>(wf, stage2, q, m1_g);
+      if (u > 0) load_wf<T>(wf, stage2, q, m1_g);
       V v[16];
 #pragma unroll
       for (int k = 0; k < 16; ++k) v[k] = A::from(inter[(m1_g * 16 + k) * COLS + lq]);
-      if (gen) {  // columns 0 / 128: general twiddles (zero components), loaded per stage
+      if (gen) {  // warps with column 0 / 128: general product (twiddles with zero components)
 #pragma unroll
         for (int t = 1; t <= 4; ++t) {  // R bits 0..3
           const int h = 1 << (t - 1);
-          C4 w[8];
-#pragma unroll
-          for (int a = 0; a < h; ++a) w[a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + a * 256 + q]);
 #pragma unroll
           for (int k = 0; k < 16; ++k)
-            if (!(k & h)) r_dit<T>(v[k], v[k + h], w[k & (h - 1)]);
+            if (!(k & h)) r_dit<T>(v[k], v[k + h], c4of<T>(wf[h - 1 + (k & (h - 1))]));
         }
       } else {
 #pragma unroll
@@ -314,13 +347,9 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
 #pragma unroll
         for (int t = 5; t <= 8; ++t) {  // R bits 4..7
           const int hr = 1 << (t - 5);
-          C4 w[8];
-#pragma unroll
-          for (int a = 0; a < hr; ++a)
-            w[a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + (m1_g + 16 * a) * 256 + q]);
 #pragma unroll
           for (int k = 0; k < 16; ++k)
-            if (!(k & hr)) r_dit<T>(v[k], v[k + hr], w[k & (hr - 1)]);
+            if (!(k & hr)) r_dit<T>(v[k], v[k + hr], c4of<T>(wf[15 + hr - 1 + (k & (hr - 1))]));
         }
       } else {
 #pragma unroll
@@ -347,7 +376,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
 //   phase 2: CTA r' runs stages 8..2 + the 2-point stage along q for its rows
 //     and writes out[rev8(q)*256 + c] (coalesced over c).
 template <typename T>
-__global__ void __launch_bounds__(L64<T>::THREADS, 1)
+__global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
     k_nlfft64k_dif(const __grid_constant__ CUtensorMap tmx, typename Ar<T>::C2 *__restrict__ y,
                    int64_t batch, const typename Ar<T>::C4 *__restrict__ stage,
                    const typename Ar<T>::C2 *__restrict__ stage2, T gain, int use_gain) {
@@ -372,7 +401,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
       const int q = pp.rank * COLS + tt * TC + m1_cc;
       const bool gen = special_column(q);
       C2 wf[30];
-      if (!gen) load_wf<T>(wf, stage2, q, m1_g);
+      load_wf<T>(wf, stage2, q, m1_g);
       pp.wait_tile();
       C2 *wk = pp.work();
       V v[16];
@@ -381,17 +410,13 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
         V x = A::from(wk[(m1_g + 16 * k) * TC + m1_cc]);
         v[k] = use_gain ? A::scale(x, gain) : x;
       }
-      if (gen) {  // columns 0 / 128: general twiddles, loaded per stage
+      if (gen) {  // warps with column 0 / 128: general product
 #pragma unroll
         for (int t = 8; t >= 5; --t) {  // R bits 7..4
           const int hr = 1 << (t - 5);
-          C4 w[8];
-#pragma unroll
-          for (int a = 0; a < hr; ++a)
-            w[a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + (m1_g + 16 * a) * 256 + q]);
 #pragma unroll
           for (int k = 0; k < 16; ++k)
-            if (!(k & hr)) r_dif<T>(v[k], v[k + hr], w[k & (hr - 1)]);
+            if (!(k & hr)) r_dif<T>(v[k], v[k + hr], c4of<T>(wf[15 + hr - 1 + (k & (hr - 1))]));
         }
       } else {
 #pragma unroll
@@ -414,12 +439,9 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
 #pragma unroll
         for (int t = 4; t >= 1; --t) {  // R bits 3..0
           const int h = 1 << (t - 1);
-          C4 w[8];
-#pragma unroll
-          for (int a = 0; a < h; ++a) w[a] = sa_ldg(&stage[(1 << (7 + t)) - 1 + a * 256 + q]);
 #pragma unroll
           for (int k = 0; k < 16; ++k)
-            if (!(k & h)) r_dif<T>(v[k], v[k + h], w[k & (h - 1)]);
+            if (!(k & h)) r_dif<T>(v[k], v[k + h], c4of<T>(wf[h - 1 + (k & (h - 1))]));
         }
       } else {
 #pragma unroll
@@ -435,10 +457,12 @@ __global__ void __launch_bounds__(L64<T>::THREADS, 1)
       for (int k = 0; k < 16; ++k) {  // row R = 16g + k -> CTA owning cr = rev8(R), local row cr mod COLS
         const int cr = crev4(k) * 16 + rg1;
         const int lr = cr % COLS;
-        sa_st_async(pp.peer_inter(b, cr / COLS, (uint32_t)(sizeof(C2) * (lr * 256 + (q ^ (lr & 15))))),
-                    A::to(v[k]), pp.peer_full(b, cr / COLS));
+        const int e = lr * 256 + (q ^ (lr & 15));
+        if (SA_LOCALQ && cr / COLS == pp.rank) pp.inter(b)[e] = A::to(v[k]);  // owner is warp-uniform
+        else sa_st_async(pp.peer_inter(b, cr / COLS, (uint32_t)(sizeof(C2) * e)), A::to(v[k]), pp.peer_full(b, cr / COLS));
       }
     }
+    pp.local_done(b);
   };
 
   auto phaseB = [&](int64_t sig, int b, uint32_t use) {
@@ -539,6 +563,7 @@ int launch64k(int variant, const void *x, void *y, int64_t batch, const SaTwiddl
   }
   auto kern = variant == SA_DIT ? k_nlfft64k_dit<T> : k_nlfft64k_dif<T>;
   SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM));
+  if (P::CL > 8) SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

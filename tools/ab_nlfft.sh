@@ -1,0 +1,26 @@
+#!/bin/bash
+# Interleaved A/B timing of the 2^16 NL-FFT cluster kernel across library builds:
+#   tools/ab_nlfft.sh [-d "complex64:dit complex128:dit"] [-r ROUNDS] lib1.so lib2.so ...
+# Each (round, lib) runs in a fresh process: 3 warm-up + 30 timed launches, CUDA events.
+cd "$(dirname "$0")/.."
+cases="complex64:dit"; rounds=3
+while getopts "d:r:" o; do case $o in d) cases=$OPTARG;; r) rounds=$OPTARG;; esac; done
+shift $((OPTIND - 1))
+for r in $(seq $rounds); do
+  for l in "$@"; do
+    SA_NLFFT_IMPL=cluster SA_LIB_PATH=$PWD/$l timeout 300 python - $cases <<'PY' | sed "s|^|$l |"
+import sys, torch
+import paper_1402_0532_b200 as sa
+for c in sys.argv[1:]:
+    dt, var = c.split(":")
+    x = torch.randn(4096, 65536, dtype=getattr(torch, dt), device="cuda"); y = torch.empty_like(x)
+    for _ in range(3): sa.nfft_batch(x, out=y, variant=var)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(); e0.record()
+    for _ in range(30): sa.nfft_batch(x, out=y, variant=var)
+    e1.record(); torch.cuda.synchronize()
+    print(f"{dt} {var} {e0.elapsed_time(e1) / 30:.3f} ms")
+    del x, y
+PY
+  done
+done | sort | awk '{k=$1" "$2" "$3; v=$4; if(!(k in m)||v<m[k])m[k]=v; a[k]=a[k]" "v} END{for(k in m)print k, "min", m[k], "all", a[k]}' | sort

@@ -18,7 +18,8 @@ for dt in (torch.complex64, torch.complex128):
         print(f"{str(dt)[6:]} {var} {ms:.3f} ms  {gb/ms*1e3:.0f} GB/s")
         del x, y
 '''
-for impl in ["2p", "cluster"]:
+impls = [sys.argv[sys.argv.index("--impl") + 1]] if "--impl" in sys.argv else ["2p", "cluster"]
+for impl in impls:
     env = dict(os.environ, SA_NLFFT_IMPL=impl)
     out = subprocess.run(["timeout", "300", sys.executable, "-c", code], env=env, capture_output=True, text=True)
     print("impl", impl, "rc", out.returncode); print(out.stdout.strip(), out.stderr.strip()[-300:])
