@@ -19,6 +19,7 @@
 
 #include "sa_common.cuh"
 #include "sa_internal.h"
+#include "sa_regs.cuh"
 
 namespace {
 
@@ -97,19 +98,33 @@ __global__ void __launch_bounds__(256) k_lag_integrate_fast(
   const int64_t i0 = q * tb;
   const int64_t ws = i0 - lt - (LAGS_PER_CTA - 1);  // global ref index of window slot 0
 
-  for (int s = threadIdx.x; s < tb; s += blockDim.x) {
-    C2<T> a = surv[i0 + s];
-    ss[pad8(s)] = {a.x, a.y, sa_sgn(a.x), sa_sgn(a.y)};
-  }
-  for (int s = threadIdx.x; s < win; s += blockDim.x) {
-    int64_t j = ws + s;
-    T cr = T(0), ci = T(0);
-    if (j >= 0 && j < ref_len) {
-      C2<T> r = ref[j];
-      cr = r.x;
-      ci = conj ? -r.y : r.y;
+  // Prologue: PF loads in flight per thread (all issued before the first use).
+  constexpr int PF = 8;
+  for (int s0 = threadIdx.x; s0 < tb; s0 += PF * blockDim.x) {
+    C2<T> a[PF];
+#pragma unroll
+    for (int u = 0; u < PF; ++u)
+      if (s0 + u * (int)blockDim.x < tb) a[u] = sa_ldg(&surv[i0 + s0 + u * blockDim.x]);
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const int s = s0 + u * blockDim.x;
+      if (s < tb) ss[pad8(s)] = {a[u].x, a[u].y, sa_sgn(a[u].x), sa_sgn(a[u].y)};
     }
-    rs[pad8(s)] = {cr, ci, sa_sgn(cr), sa_sgn(ci)};
+  }
+  for (int s0 = threadIdx.x; s0 < win; s0 += PF * blockDim.x) {
+    C2<T> r[PF];
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const int64_t j = ws + s0 + u * blockDim.x;
+      r[u] = {T(0), T(0)};
+      if (s0 + u * (int)blockDim.x < win && j >= 0 && j < ref_len) r[u] = sa_ldg(&ref[j]);
+    }
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const int s = s0 + u * blockDim.x;
+      const T cr = r[u].x, ci = conj ? -r[u].y : r[u].y;
+      if (s < win) rs[pad8(s)] = {cr, ci, sa_sgn(cr), sa_sgn(ci)};
+    }
   }
   __syncthreads();
 
@@ -180,6 +195,142 @@ __global__ void __launch_bounds__(256) k_lag_integrate_fast(
   }
 }
 
+// complex64, T % 16 == 0: entry e of S holds samples e and e + T/2, entry u of
+// C window slots u and u + T/2, each as {x, x'}, {y, y'} (S0/C0) and the signs
+// {sx, sx'}, {sy, sy'} (S1/C1), in pad8-strided float4 arrays.
+__global__ void __launch_bounds__(256, 2) k_lag_integrate_f32x2(
+    const float2 *__restrict__ surv, const float2 *__restrict__ ref, int64_t ref_len, int64_t l0,
+    int64_t l_count, int64_t m, int tb, bool conj, float2 *__restrict__ z) {
+  using A = Ar<float>;
+  using V = A::V;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int h = tb >> 1;
+  const int hw = h + LAGS_PER_CTA - 1;  // window pair entries
+  float4 *S0 = reinterpret_cast<float4 *>(smem_raw);
+  float4 *S1 = S0 + pad8(h) + 1;
+  float4 *C0 = S1 + pad8(h) + 1;
+  float4 *C1 = C0 + pad8(hw) + 1;
+
+  const int64_t q = blockIdx.x;
+  const int64_t lt = l0 + (int64_t)blockIdx.y * LAGS_PER_CTA;
+  const int64_t i0 = q * tb;
+  const int64_t ws = i0 - lt - (LAGS_PER_CTA - 1);
+
+  constexpr int PF = 4;
+  for (int e0 = threadIdx.x; e0 < h; e0 += PF * blockDim.x) {
+    float2 a[PF], b[PF];
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < h) {
+        a[u] = __ldg(&surv[i0 + e]);
+        b[u] = __ldg(&surv[i0 + e + h]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < h) {
+        S0[pad8(e)] = {a[u].x, b[u].x, a[u].y, b[u].y};
+        S1[pad8(e)] = {sa_sgn(a[u].x), sa_sgn(b[u].x), sa_sgn(a[u].y), sa_sgn(b[u].y)};
+      }
+    }
+  }
+  for (int e0 = threadIdx.x; e0 < hw; e0 += PF * blockDim.x) {
+    float2 a[PF], b[PF];
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const int e = e0 + u * blockDim.x;
+      const int64_t j = ws + e, k = j + h;
+      a[u] = b[u] = {0.f, 0.f};
+      if (e < hw && j >= 0 && j < ref_len) a[u] = __ldg(&ref[j]);
+      if (e < hw && k >= 0 && k < ref_len) b[u] = __ldg(&ref[k]);
+    }
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const int e = e0 + u * blockDim.x;
+      const float ai = conj ? -a[u].y : a[u].y, bi = conj ? -b[u].y : b[u].y;
+      if (e < hw) {
+        C0[pad8(e)] = {a[u].x, b[u].x, ai, bi};
+        C1[pad8(e)] = {sa_sgn(a[u].x), sa_sgn(b[u].x), sa_sgn(ai), sa_sgn(bi)};
+      }
+    }
+  }
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t lw = lt + warp * LAGS_PER_WARP;
+  if (lw - l0 >= l_count) return;
+
+  V accr[LAGS_PER_WARP], acci[LAGS_PER_WARP];
+#pragma unroll
+  for (int j = 0; j < LAGS_PER_WARP; ++j) accr[j] = acci[j] = 0ull;
+
+  const int nsb = h >> 3;
+  for (int sb = lane; sb < nsb; sb += 32) {
+    const int t0 = sb * 8;
+    const int base = t0 + (LAGS_PER_CTA - 1) - LAGS_PER_WARP * warp - (LAGS_PER_WARP - 1);
+    V cx[15], cy[15], cz[15], cw[15];  // window pairs {re}, {im}, {sgn re}, {sgn im}
+#pragma unroll
+    for (int u = 0; u < 15; ++u) {
+      const float4 c0 = C0[pad8(base + u)], c1 = C1[pad8(base + u)];
+      cx[u] = A::pack(c0.x, c0.y);
+      cy[u] = A::pack(c0.z, c0.w);
+      cz[u] = A::pack(c1.x, c1.y);
+      cw[u] = A::pack(c1.z, c1.w);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float4 s0 = S0[pad8(t0 + i)], s1 = S1[pad8(t0 + i)];
+      const V sx = A::pack(s0.x, s0.y), sy = A::pack(s0.z, s0.w);
+      const V sz = A::pack(s1.x, s1.y), sw = A::pack(s1.z, s1.w);
+      // consecutive FFMA2 share the surveillance pair; per lag the terms add as
+      //   Re: sx*cz, sz*cx, -sy*cw, -sw*cy ;  Im: sy*cz, sw*cx, sz*cy, sx*cw
+#pragma unroll
+      for (int j = 0; j < LAGS_PER_WARP; ++j) accr[j] = A::fma(sx, cz[i - j + 7], accr[j]);
+#pragma unroll
+      for (int j = 0; j < LAGS_PER_WARP; ++j) acci[j] = A::fma(sy, cz[i - j + 7], acci[j]);
+#pragma unroll
+      for (int j = 0; j < LAGS_PER_WARP; ++j) accr[j] = A::fma(sz, cx[i - j + 7], accr[j]);
+#pragma unroll
+      for (int j = 0; j < LAGS_PER_WARP; ++j) acci[j] = A::fma(sw, cx[i - j + 7], acci[j]);
+#pragma unroll
+      for (int j = 0; j < LAGS_PER_WARP; ++j) accr[j] = A::fma(A::neg(sy), cw[i - j + 7], accr[j]);
+#pragma unroll
+      for (int j = 0; j < LAGS_PER_WARP; ++j) acci[j] = A::fma(sz, cy[i - j + 7], acci[j]);
+#pragma unroll
+      for (int j = 0; j < LAGS_PER_WARP; ++j) accr[j] = A::fma(A::neg(sw), cy[i - j + 7], accr[j]);
+#pragma unroll
+      for (int j = 0; j < LAGS_PER_WARP; ++j) acci[j] = A::fma(sx, cw[i - j + 7], acci[j]);
+    }
+  }
+  float vr[LAGS_PER_WARP], vi[LAGS_PER_WARP];
+#pragma unroll
+  for (int j = 0; j < LAGS_PER_WARP; ++j) {
+    float a, b;
+    A::unpack(accr[j], a, b);
+    vr[j] = sa_add(a, b);
+    A::unpack(acci[j], a, b);
+    vi[j] = sa_add(a, b);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      vr[j] = sa_add(vr[j], __shfl_xor_sync(0xffffffffu, vr[j], o));
+      vi[j] = sa_add(vi[j], __shfl_xor_sync(0xffffffffu, vi[j], o));
+    }
+  }
+  if (lane < LAGS_PER_WARP) {
+    float r = vr[0], i = vi[0];
+#pragma unroll
+    for (int j = 1; j < LAGS_PER_WARP; ++j)
+      if (lane == j) {
+        r = vr[j];
+        i = vi[j];
+      }
+    const int64_t row = lw + lane - l0;
+    if (row < l_count) z[row * m + q] = {r, i};
+  }
+}
+
 template <typename T>
 int launch_integrate(const void *survv, const void *refv, int64_t ns, int64_t ref_len, int64_t l0,
                      int64_t l_count, int64_t m, int conj, int mode, void *zv, cudaStream_t s) {
@@ -196,11 +347,26 @@ int launch_integrate(const void *survv, const void *refv, int64_t ns, int64_t re
     SA_LAUNCH_CHECK();
     return SA_OK;
   }
+  int64_t ltiles = (l_count + LAGS_PER_CTA - 1) / LAGS_PER_CTA;
+  if (sizeof(T) == 4 && tb % 16 == 0) {
+    const int h = (int)tb / 2, hw = h + LAGS_PER_CTA - 1;
+    size_t bytes = 2 * sizeof(float4) * ((size_t)pad8(h) + 1 + pad8(hw) + 1);
+    SA_CUDA_TRY(cudaFuncSetAttribute(k_lag_integrate_f32x2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)bytes));
+    for (int64_t t0 = 0; t0 < ltiles; t0 += 65535) {
+      int64_t nt = std::min<int64_t>(65535, ltiles - t0);
+      dim3 grid((unsigned)m, (unsigned)nt);
+      k_lag_integrate_f32x2<<<grid, 256, bytes, s>>>(
+          (const float2 *)surv, (const float2 *)ref, ref_len, l0 + t0 * LAGS_PER_CTA,
+          l_count - t0 * LAGS_PER_CTA, m, (int)tb, conj != 0, (float2 *)(z + t0 * LAGS_PER_CTA * m));
+    }
+    SA_LAUNCH_CHECK();
+    return SA_OK;
+  }
   const int win = (int)tb + LAGS_PER_CTA - 1;
   size_t bytes = sizeof(C4<T>) * ((size_t)pad8((int)tb) + 1 + pad8(win) + 1);
   auto kern = k_lag_integrate_fast<T>;
   SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  int64_t ltiles = (l_count + LAGS_PER_CTA - 1) / LAGS_PER_CTA;
   for (int64_t t0 = 0; t0 < ltiles; t0 += 65535) {
     int64_t nt = std::min<int64_t>(65535, ltiles - t0);
     dim3 grid((unsigned)m, (unsigned)nt);

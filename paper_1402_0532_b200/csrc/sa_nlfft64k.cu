@@ -42,6 +42,7 @@ constexpr int NN = 1 << LOGN;
 #define SA_K64F_CL 4
 #define SA_K64F_NG 2
 #define SA_K64F_MINB 1
+#define SA_K64F_NS 1
 #endif
 
 template <typename T> struct K64;
@@ -49,7 +50,7 @@ template <> struct K64<float> {
   static constexpr int TC = SA_K64F_TC;  // columns per tile
   static constexpr int CL = SA_K64F_CL;  // cluster size
   static constexpr int NG = SA_K64F_NG;  // thread groups per CTA
-  static constexpr int NS = 1;           // node storages (2 = pipelined signals; needs CL >= 8 for c64)
+  static constexpr int NS = SA_K64F_NS;  // node storages (2 = pipelined signals; needs CL >= 8 for c64)
   static constexpr int MINB = SA_K64F_MINB;  // resident CTAs per SM
 };
 template <> struct K64<double> {

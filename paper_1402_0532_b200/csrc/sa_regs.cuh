@@ -67,6 +67,11 @@ template <> struct Ar<float> {
     unpack(v, lo, hi);
     return pack(hi, lo);
   }
+  static SA_HD V neg(V v) {  // folds into the consuming FFMA2/FADD2 operand (-R.F32x2)
+    float lo, hi;
+    unpack(v, lo, hi);
+    return pack(-lo, -hi);
+  }
   static SA_HD V neg_hi(V v) {
     float lo, hi;
     unpack(v, lo, hi);
