@@ -385,3 +385,24 @@ def test_sharded_map_nccl_single_rank(sa):
     p.join(300)
     assert p.exitcode == 0
     assert q.get(timeout=10) is True
+
+
+@pytest.mark.parametrize("tb", [8, 16, 24, 48, 2048])
+def test_map_c64_block_lengths(sa, tb):
+    """complex64 fast lag integration for every kernel the block length T selects
+    (T % 16 == 0: packed FFMA2 pairs i / i+T/2; T % 8 == 0: scalar tiles), with
+    ragged lag counts (not a multiple of the 64-lag tile) and a nonzero l0, vs the
+    oracle of the same complex64 inputs; exact mode is value-equal to the f32 oracle."""
+    g = np.random.default_rng(500 + tb)
+    m = 32
+    ns = tb * m
+    surv = (g.standard_normal(ns) + 1j * g.standard_normal(ns)).astype(np.complex64)
+    ref = np.exp(2j * np.pi * g.random(ns)).astype(np.complex64)
+    surv[5] = 0
+    ref[9] = 0
+    l0, L = 3, 70
+    y = sa.ambiguity_map(dev(surv), dev(ref), L, m, l0=l0).cpu().numpy()
+    assert_literal(y, oracle.ambiguity_map(surv.astype(np.complex128), ref.astype(np.complex128), l0, L, m,
+                                           nthreads=8), TOL_F32)
+    ye = sa.ambiguity_map(dev(surv), dev(ref), L, m, l0=l0, mode="exact").cpu().numpy()
+    assert_value_equal(ye, oracle.ambiguity_map(surv, ref, l0, L, m, dtype="f32", nthreads=8))
