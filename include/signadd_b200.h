@@ -117,6 +117,30 @@ int sa_ambiguity_integrate(int dtype, const void *surv, const void *ref, int64_t
                            int64_t ref_len, int64_t l0, int64_t l_count, int64_t m, int conj,
                            int mode, void *z, void *stream);
 
+/* Workspace bytes for sa_map_peaks. */
+int sa_peaks_workspace_bytes(int64_t rows, int64_t cols, int k, int64_t *bytes);
+
+/* The k strongest strict local maxima of |map| (rows x cols, device).
+ * Replaces: detection.find_peaks (detection.py:85-108).  A cell qualifies when
+ * strictly greater than its 8 neighbours (cells beyond the edge never block);
+ * |v| is numpy's complex absolute value, max*sqrt(fma(r, r, 1)) with
+ * r = min/max of |re|, |im| (bit-exact to np.abs on the reference host).
+ * Peaks come strongest first, equal magnitudes in row-major order.
+ * Outputs (device): idx[k] = row-major cell index (-1 past the last peak),
+ * mag[k] = magnitude as double, *count = number of peaks found (<= k).
+ * 1 <= k <= 1024 (SA_ERR_UNSUPPORTED above). */
+int sa_map_peaks(int dtype, const void *map, int64_t rows, int64_t cols, int k, int64_t *idx,
+                 double *mag, int32_t *count, void *workspace, int64_t ws_bytes, void *stream);
+
+/* The two maxima behind detection.sidelobe_floor_db (detection.py:148-171):
+ * out (device, 3 x uint64) = {bit pattern of max |map|, bit pattern of max
+ * |map| outside every guard box, number of outside cells}.  Box b covers rows
+ * |l - centers[2b]| <= g0 and Doppler bins at circular distance <= g1 from
+ * centers[2b+1] (device int32 centers[2 * ncent]), as _guard_mask
+ * (detection.py:137-145).  The dB arithmetic stays with the caller. */
+int sa_map_floor(int dtype, const void *map, int64_t rows, int64_t cols, const int32_t *centers,
+                 int ncent, int g0, int g1, uint64_t *out, void *stream);
+
 /* FMA-pipe peak microbenchmark (roofline denominator): `blocks` CTAs x 256
  * (dtype 2 = packed fp32x2 FFMA2)
  * threads each run `iters` iterations of 8 independent FMA chains; writes a

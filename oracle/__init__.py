@@ -35,6 +35,9 @@ __all__ = [
     "nfft",
     "lag_product_mf",
     "ambiguity_map",
+    "abs_np",
+    "find_peaks",
+    "map_floor",
 ]
 
 
@@ -64,6 +67,10 @@ def _load():
             i64, p, p, i64, i64, i64, ctypes.c_double, ci, ci, p, p, ci]
         for name in ("ndft", "nfft", "lag_product_mf", "ambiguity_map"):
             getattr(lib, f"or_{name}_{sfx}").restype = ci
+        getattr(lib, f"or_abs_np_{sfx}").argtypes = [i64, p, p]
+        getattr(lib, f"or_find_peaks_{sfx}").argtypes = [i64, i64, p, i64, p, p]
+        getattr(lib, f"or_find_peaks_{sfx}").restype = i64
+        getattr(lib, f"or_map_floor_{sfx}").argtypes = [i64, i64, p, p, ci, ci, ci, p]
     _lib = lib
     return lib
 
@@ -179,3 +186,46 @@ def ambiguity_map(surv, ref, l0: int, l_count: int, m: int, gain: float = 1.0,
     if rc:
         raise ValueError("oracle ambiguity_map: bad sizes")
     return out
+
+
+# --- detection: restates detection.py:85-171 ----------------
+
+def _prep2d(values, dtype: str) -> np.ndarray:
+    v = np.asarray(values)
+    if v.ndim != 2:
+        raise ValueError("surface values must be 2-D")
+    return np.ascontiguousarray(v, dtype=np.complex128 if dtype == "f64" else np.complex64)
+
+
+def abs_np(z, dtype: str = "f64") -> np.ndarray:
+    """numpy's complex magnitude as the reference host computes it (C restatement)."""
+    zz = np.ascontiguousarray(np.asarray(z).ravel(), dtype=np.complex128 if dtype == "f64" else np.complex64)
+    out = np.empty(zz.size, dtype=np.float64 if dtype == "f64" else np.float32)
+    getattr(_load(), f"or_abs_np_{dtype}")(
+        zz.size, zz.ctypes.data, out.ctypes.data)
+    return out
+
+
+def find_peaks(values, k: int, dtype: str = "f64") -> np.ndarray:
+    """detection.find_peaks (detection.py:85-108): rows (l, p, magnitude), strongest first."""
+    v = _prep2d(values, dtype)
+    idx = np.empty(max(k, 1), dtype=np.int64)
+    mag = np.empty(max(k, 1), dtype=np.float64)
+    n = getattr(_load(), f"or_find_peaks_{dtype}")(v.shape[0], v.shape[1], v.ctypes.data, k,
+                                                    idx.ctypes.data, mag.ctypes.data)
+    if n < 0:
+        raise ValueError("find_peaks: bad arguments")
+    out = np.empty((n, 3))
+    out[:, 0], out[:, 1], out[:, 2] = idx[:n] // v.shape[1], idx[:n] % v.shape[1], mag[:n]
+    return out
+
+
+def map_floor(values, centers, guard, dtype: str = "f64") -> tuple[float, float, int]:
+    """(max |v|, max |v| outside every guard box, outside cells) -- the inputs of
+    detection.sidelobe_floor_db (detection.py:148-171; boxes as _guard_mask :137-145)."""
+    v = _prep2d(values, dtype)
+    c = np.ascontiguousarray(np.asarray(centers, dtype=np.int32).reshape(-1, 2))
+    out = np.empty(3)
+    getattr(_load(), f"or_map_floor_{dtype}")(v.shape[0], v.shape[1], v.ctypes.data, c.ctypes.data,
+                                               c.shape[0], int(guard[0]), int(guard[1]), out.ctypes.data)
+    return float(out[0]), float(out[1]), int(out[2])

@@ -310,4 +310,103 @@ static int64_t or_bitrev(int64_t i, int64_t bits) {
 OR_DEFINE(double, f64, fabs)
 OR_DEFINE(float, f32, fabsf)
 
+/* ---- detection (detection.py:85-171), SURVEY §8(f)-1 ------------------------
+ * Magnitude: numpy's complex absolute value, as its SIMD loop computes it on the
+ * reference host (L = max, S = min of |re|, |im|; r = S/L, 0 when L == 0;
+ * |v| = sqrt(fma(r, r, 1)) * L), pinned against np.abs by the golden vectors.
+ * find_peaks: strict 8-neighbour maxima (detection.py:96-104; cells beyond the
+ * edge never block), ordered as the stable argsort of -|v| over the row-major
+ * candidates (detection.py:106): magnitude descending, then row-major index.
+ * Floor inputs: max |v| and max |v| outside every guard box (_guard_mask,
+ * detection.py:137-145) plus the outside-cell count. */
+typedef struct {
+    double mag;
+    int64_t idx;
+} or_cand;
+
+static int or_cand_cmp(const void *a, const void *b) {
+    const or_cand *x = (const or_cand *)a, *y = (const or_cand *)b;
+    if (x->mag != y->mag) return x->mag > y->mag ? -1 : 1;
+    return x->idx < y->idx ? -1 : (x->idx > y->idx);
+}
+
+#define OR_DETECT(T, SFX, FABS, FMA, SQRT)                                         \
+    T or_cabs_np_##SFX(T re, T im) {                                               \
+        re = FABS(re);                                                             \
+        im = FABS(im);                                                             \
+        if (isinf(re) || isinf(im)) return (T)INFINITY;                            \
+        if (isnan(re) || isnan(im)) return (T)NAN;                                 \
+        T L = re > im ? re : im, S = re > im ? im : re;                            \
+        T r = (L == (T)0) ? (T)0 : S / L;                                          \
+        return SQRT(FMA(r, r, (T)1)) * L;                                          \
+    }                                                                              \
+    void or_abs_np_##SFX(int64_t n, const T *z, T *out) {                          \
+        for (int64_t i = 0; i < n; ++i) out[i] = or_cabs_np_##SFX(z[2 * i], z[2 * i + 1]); \
+    }                                                                              \
+    /* returns the number of peaks written (<= k), -1 on bad arguments */         \
+    int64_t or_find_peaks_##SFX(int64_t rows, int64_t cols, const T *v, int64_t k, \
+                                int64_t *out_idx, double *out_mag) {               \
+        if (rows < 1 || cols < 1 || k < 1) return -1;                              \
+        T *mag = (T *)malloc(sizeof(T) * rows * cols);                             \
+        or_cand *c = (or_cand *)malloc(sizeof(or_cand) * rows * cols);             \
+        int64_t nc = 0;                                                            \
+        for (int64_t i = 0; i < rows * cols; ++i)                                  \
+            mag[i] = or_cabs_np_##SFX(v[2 * i], v[2 * i + 1]);                     \
+        for (int64_t l = 0; l < rows; ++l)                                         \
+            for (int64_t p = 0; p < cols; ++p) {                                   \
+                T m = mag[l * cols + p];                                           \
+                int strict = 1;                                                    \
+                for (int dl = -1; dl <= 1; ++dl)                                   \
+                    for (int dp = -1; dp <= 1; ++dp) {                             \
+                        if (!dl && !dp) continue;                                  \
+                        int64_t ll = l + dl, pp = p + dp;                          \
+                        if (ll < 0 || ll >= rows || pp < 0 || pp >= cols) continue; \
+                        if (!(m > mag[ll * cols + pp])) strict = 0;                \
+                    }                                                              \
+                if (strict) {                                                      \
+                    c[nc].mag = (double)m;                                         \
+                    c[nc].idx = l * cols + p;                                      \
+                    ++nc;                                                          \
+                }                                                                  \
+            }                                                                      \
+        qsort(c, (size_t)nc, sizeof(or_cand), or_cand_cmp);                        \
+        int64_t n = nc < k ? nc : k;                                               \
+        for (int64_t i = 0; i < n; ++i) {                                          \
+            out_idx[i] = c[i].idx;                                                 \
+            out_mag[i] = c[i].mag;                                                 \
+        }                                                                          \
+        free(mag);                                                                 \
+        free(c);                                                                   \
+        return n;                                                                  \
+    }                                                                              \
+    void or_map_floor_##SFX(int64_t rows, int64_t cols, const T *v,                \
+                            const int32_t *centers, int ncent, int g0, int g1,     \
+                            double *out3) {                                        \
+        double all = 0.0, outside = 0.0, n_out = 0.0;                              \
+        for (int64_t l = 0; l < rows; ++l)                                         \
+            for (int64_t p = 0; p < cols; ++p) {                                   \
+                double m = (double)or_cabs_np_##SFX(v[2 * (l * cols + p)],         \
+                                                    v[2 * (l * cols + p) + 1]);    \
+                int in = 0;                                                        \
+                for (int b = 0; b < ncent && !in; ++b) {                           \
+                    int64_t dl = l - centers[2 * b];                               \
+                    int64_t d = (p - centers[2 * b + 1]) % cols;                   \
+                    if (d < 0) d += cols;                                          \
+                    int64_t dp = d < cols - d ? d : cols - d;                      \
+                    in = dl <= g0 && dl >= -g0 && dp <= g1;                        \
+                }                                                                  \
+                if (m > all) all = m;                                              \
+                if (!in) {                                                         \
+                    if (m > outside) outside = m;                                  \
+                    n_out += 1.0;                                                  \
+                }                                                                  \
+            }                                                                      \
+        out3[0] = all;                                                             \
+        out3[1] = outside;                                                         \
+        out3[2] = n_out;                                                           \
+    }
+
+OR_DETECT(double, f64, fabs, fma, sqrt)
+OR_DETECT(float, f32, fabsf, fmaf, sqrtf)
+
 int or_version(void) { return 1; }

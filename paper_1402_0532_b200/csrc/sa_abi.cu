@@ -212,6 +212,34 @@ int sa_ambiguity_integrate(int dtype, const void *surv, const void *ref, int64_t
                                  (cudaStream_t)stream);
 }
 
+int sa_peaks_workspace_bytes(int64_t rows, int64_t cols, int k, int64_t *bytes) {
+  SA_REQUIRE(bytes && rows >= 1 && cols >= 1 && k >= 1, SA_ERR_ARG, "bad arguments");
+  *bytes = sa_peaks_ws_bytes(rows, cols, k);
+  return SA_OK;
+}
+
+int sa_map_peaks(int dtype, const void *map, int64_t rows, int64_t cols, int k, int64_t *idx,
+                 double *mag, int32_t *count, void *workspace, int64_t ws_bytes, void *stream) {
+  SA_REQUIRE(dtype_ok(dtype), SA_ERR_ARG, "bad dtype %d", dtype);
+  SA_REQUIRE(k >= 1, SA_ERR_CONTRACT, "find_peaks: k must be >= 1");
+  SA_REQUIRE(k <= 1024, SA_ERR_UNSUPPORTED, "find_peaks: k = %d > 1024", k);
+  SA_REQUIRE(rows >= 1 && cols >= 1, SA_ERR_ARG, "empty map");
+  SA_REQUIRE(map && idx && mag && count && workspace, SA_ERR_ARG, "null pointer");
+  SA_REQUIRE(ws_bytes >= sa_peaks_ws_bytes(rows, cols, k), SA_ERR_ARG, "workspace too small");
+  return sa_launch_map_peaks(dtype, map, rows, cols, k, (long long *)idx, mag, count, workspace,
+                             (cudaStream_t)stream);
+}
+
+int sa_map_floor(int dtype, const void *map, int64_t rows, int64_t cols, const int32_t *centers,
+                 int ncent, int g0, int g1, uint64_t *out, void *stream) {
+  SA_REQUIRE(dtype_ok(dtype), SA_ERR_ARG, "bad dtype %d", dtype);
+  SA_REQUIRE(g0 >= 0 && g1 >= 0 && ncent >= 0, SA_ERR_ARG, "bad guard");
+  SA_REQUIRE(rows >= 1 && cols >= 1, SA_ERR_ARG, "empty map");
+  SA_REQUIRE(map && out && (centers || ncent == 0), SA_ERR_ARG, "null pointer");
+  return sa_launch_map_floor(dtype, map, rows, cols, centers, ncent, g0, g1, (unsigned long long *)out,
+                             (cudaStream_t)stream);
+}
+
 int sa_fma_peak(int dtype, int64_t iters, void *d_sink, int blocks, void *stream) {
   SA_REQUIRE((dtype_ok(dtype) || dtype == 2) && d_sink && iters > 0 && blocks > 0, SA_ERR_ARG,
              "bad arguments");

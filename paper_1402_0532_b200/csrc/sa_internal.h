@@ -68,6 +68,11 @@ int sa_launch_nlfft2p(int dtype, int variant, const void *x, void *y, int64_t ba
 
 // sa_ambiguity.cu
 int64_t sa_ambiguity_ws_bytes(int dtype, int64_t l_count, int64_t m);
+int64_t sa_peaks_ws_bytes(int64_t rows, int64_t cols, int k);
+int sa_launch_map_peaks(int dtype, const void *map, int64_t rows, int64_t cols, int k, long long *idx, double *mag,
+                        int *count, void *ws, cudaStream_t s);
+int sa_launch_map_floor(int dtype, const void *map, int64_t rows, int64_t cols, const int *centers, int ncent,
+                        int g0, int g1, unsigned long long *out, cudaStream_t s);
 int sa_launch_lag_product(int dtype, const void *surv, const void *ref, int64_t n, int64_t ref_len,
                           int64_t lag, int conj, void *out, cudaStream_t s);
 int sa_launch_lag_integrate(int dtype, const void *surv, const void *ref, int64_t ns,

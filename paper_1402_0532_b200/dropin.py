@@ -8,7 +8,8 @@ Names patched: ``signadd.{ndft, nfft, lag_product_mf,
 ambiguity_eq12a, compute_ambiguity}``, ``signadd.transforms.{ndft, nfft}``,
 ``signadd.ambiguity.{nfft, lag_product_mf, ambiguity_eq12a, compute_ambiguity}``
 (module globals looked up at call time, ambiguity.py:39,201-202),
-``signadd.detection.compute_ambiguity`` (detection.py:24,187),
+``signadd.detection.{compute_ambiguity, find_peaks, sidelobe_floor_db}``
+(detection.py:24,85,148,187; ``classify`` looks both up at call time),
 ``signadd.cli.{ndft, nfft}`` and ``cli._TRANSFORMS`` (captured at import,
 cli.py:51-71).  ``mf_complex`` is optional (``mf_complex=True``): the reference
 test oracles (tests/oracles.py:10) call it and are meant to stay on the CPU.
@@ -109,6 +110,17 @@ def install(ref, *, mf_complex: bool = False) -> None:
             return ambiguity_eq12a(s_surv, s_ref, l_bins, n, transform_input_gain, conjugate_ref)
         return orig_compute(variant, s_surv, s_ref, l_bins, n, transform_input_gain, conjugate_ref)
 
+    from . import detection as _det
+    rmod = importlib.import_module(ref.__name__ + ".radar")
+
+    @tr
+    def find_peaks(surface, k):
+        return [dmod.Peak(pk.l, pk.p, pk.magnitude) for pk in _det.find_peaks(surface, k)]
+
+    @tr
+    def sidelobe_floor_db(surface, scenario, guard=_det.DEFAULT_GUARD):
+        return _det.sidelobe_floor_db(surface, rmod.true_bins(scenario), guard)
+
     patches = [
         (ref, "ndft", ndft), (ref, "nfft", nfft), (ref, "lag_product_mf", lag_product_mf),
         (ref, "ambiguity_eq12a", ambiguity_eq12a), (ref, "compute_ambiguity", compute_ambiguity),
@@ -116,6 +128,7 @@ def install(ref, *, mf_complex: bool = False) -> None:
         (amod, "nfft", nfft), (amod, "lag_product_mf", lag_product_mf),
         (amod, "ambiguity_eq12a", ambiguity_eq12a), (amod, "compute_ambiguity", compute_ambiguity),
         (dmod, "compute_ambiguity", compute_ambiguity),
+        (dmod, "find_peaks", find_peaks), (dmod, "sidelobe_floor_db", sidelobe_floor_db),
         (cmod, "ndft", ndft), (cmod, "nfft", nfft),
     ]
     if mf_complex:

@@ -152,6 +152,52 @@ def main() -> None:
         rows.append(sa.ndft(0.5 * zz).bins)
     g["map_ns4096_m64_ndft_l100_g05"] = np.stack(rows)
 
+    # --- detection: magnitudes, find_peaks, classify, floor -----
+    import signadd.detection as det
+    r = np.random.default_rng(14020536)
+    z = r.standard_normal(4096) * 10.0 ** r.integers(-6, 7, 4096) + 1j * (
+        r.standard_normal(4096) * 10.0 ** r.integers(-6, 7, 4096))
+    z[:4] = [0, 3.0, -4j, 1e-300 + 1e-300j]
+    g["abs_z"] = z
+    g["abs_m"] = np.abs(z)
+    g["abs_z32"] = z.astype(np.complex64)
+    g["abs_m32"] = np.abs(z.astype(np.complex64))
+
+    def surf(values):
+        return sa.AmbiguitySurface(values=np.asarray(values, dtype=complex), range_bin_m=1.0,
+                                   doppler_bin_hz=1.0, variant=sa.AmbiguityVariant.EQ12A,
+                                   sample_rate_hz=1.0)
+
+    def peaks(values, k):
+        return np.array([(pk.l, pk.p, pk.magnitude) for pk in det.find_peaks(surf(values), k)],
+                        dtype=float).reshape(-1, 3)
+
+    ph = lambda shape: np.exp(2j * np.pi * r.random(shape))
+    cases = {
+        "rnd_7x9": r.standard_normal((7, 9)) + 1j * r.standard_normal((7, 9)),
+        "ties_16x24": r.integers(0, 4, (16, 24)) * ph((16, 24)),
+        "flat_5x5": np.full((5, 5), 2.0 + 1j),
+        "one_1x1": np.array([[0.5 - 0.25j]]),
+        "row_1x17": r.standard_normal((1, 17)) + 0j,
+        "col_17x1": r.standard_normal((17, 1)) * 1j,
+        "big_40x70": (r.standard_normal((40, 70)) + 1j * r.standard_normal((40, 70))) * 1e3,
+    }
+    cases["ties_16x24"][3, 5] = 7 * ph(())  # an isolated strict maximum among plateaus
+    for name, v in cases.items():
+        g[f"det_{name}"] = np.asarray(v, dtype=complex)
+        for k in (1, 3, 1000):
+            g[f"det_{name}_k{k}"] = peaks(v, k)
+    scn = sa.two_targets_one_clutter(seed=3, n=512, l_bins=64)
+    sf = det.surface_for_scenario(scn, "eq12a")
+    g["det_scn_values"] = sf.values
+    g["det_scn_true_bins"] = np.array(sa.true_bins(scn) if hasattr(sa, "true_bins")
+                                      else __import__("signadd.radar").radar.true_bins(scn))
+    g["det_scn_peaks"] = peaks(sf.values, len(scn.obstacles))
+    rep = det.classify(sf, scn)
+    g["det_scn_statuses"] = np.array([s_ == "detected" for s_ in rep.statuses])
+    for gd in ((1, 1), (2, 2), (3, 5)):
+        g[f"det_scn_floor_{gd[0]}_{gd[1]}"] = np.array(det.sidelobe_floor_db(sf, scn, gd))
+
     np.savez_compressed(OUT, **g)
     print("wrote", OUT, os.path.getsize(OUT), "bytes,", len(g), "arrays")
 

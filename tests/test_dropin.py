@@ -118,3 +118,23 @@ def test_reference_pipeline_eq12a_matches_cpu(ref, sa):
     assert gpu.values.shape == cpu.values.shape
     assert np.array_equal(gpu.values, cpu.values)  # value-identical (fp64, T == 1)
     assert gpu.op_counts == cpu.op_counts
+
+
+@pytest.mark.gpu
+def test_reference_classify_through_dropin(ref, sa):
+    """detection.classify (reference) with find_peaks / sidelobe_floor_db on the GPU."""
+    from paper_1402_0532_b200 import dropin
+    import signadd.detection as dmod
+    scn = ref.two_targets_one_clutter(seed=5, n=512, l_bins=64)
+    sf = dmod.surface_for_scenario(scn, "eq12a")
+    cpu = dmod.classify(sf, scn)
+    cpu_floor = dmod.sidelobe_floor_db(sf, scn, (3, 4))
+    dropin.install(ref)
+    try:
+        assert dmod.find_peaks.__module__ == "paper_1402_0532_b200.dropin"
+        gpu = dmod.classify(sf, scn)
+        gpu_floor = dmod.sidelobe_floor_db(sf, scn, (3, 4))
+    finally:
+        dropin.uninstall(ref)
+    assert gpu == cpu  # statuses, overall, floor, peaks (reference Peak objects)
+    assert gpu_floor == cpu_floor

@@ -123,3 +123,36 @@ def test_fp32_restatement_close():
     y32 = oracle.nfft(x.astype(np.complex64), dtype="f32")
     err = np.max(np.abs(y32 - y64), axis=1) / np.sum(np.abs(y64), axis=1)
     assert np.all(err < 1e-4)
+
+
+# --- detection (detection.py:85-171) ----------------------------
+
+def test_abs_matches_numpy_simd_formula(golden):
+    """The magnitude restatement equals np.abs as the reference host computed it."""
+    assert np.array_equal(oracle.abs_np(golden["abs_z"]), golden["abs_m"])
+    assert np.array_equal(oracle.abs_np(golden["abs_z32"], "f32"), golden["abs_m32"])
+
+
+DET_CASES = ["rnd_7x9", "ties_16x24", "flat_5x5", "one_1x1", "row_1x17", "col_17x1", "big_40x70"]
+
+
+@pytest.mark.parametrize("name", DET_CASES)
+@pytest.mark.parametrize("k", [1, 3, 1000])
+def test_find_peaks_golden(golden, name, k):
+    got = oracle.find_peaks(golden[f"det_{name}"], k)
+    assert np.array_equal(got, golden[f"det_{name}_k{k}"])
+
+
+def test_scenario_detection_golden(golden):
+    """Scene -> eq12a surface -> find_peaks / classify / sidelobe_floor_db (reference)."""
+    v, tb = golden["det_scn_values"], golden["det_scn_true_bins"]
+    pk = oracle.find_peaks(v, len(tb))
+    assert np.array_equal(pk, golden["det_scn_peaks"])
+    hits = [any(abs(l - l0) <= 2 and min(abs(p - p0) % v.shape[1], v.shape[1] - abs(p - p0) % v.shape[1]) <= 2
+                for l, p, _ in pk) for l0, p0 in tb]
+    assert hits == list(golden["det_scn_statuses"])
+    for g0, g1 in ((1, 1), (2, 2), (3, 5)):
+        gmax, out, n_out = oracle.map_floor(v, tb, (g0, g1))
+        assert n_out > 0
+        db = max(20.0 * np.log10(out / gmax), -300.0)
+        assert db == float(golden[f"det_scn_floor_{g0}_{g1}"])

@@ -8,7 +8,7 @@ import sys
 
 rows = list(csv.reader(open(sys.argv[1])))
 h = rows[1]
-data = [dict(zip(h, r)) for r in rows[2:] if len(r) == len(h)]
+data = [dict(zip(h, r)) for r in rows[2:] if len(r) == len(h) and r[0] != h[0]]
 S = lambda d: int(d["Warp Stall Sampling (All Samples)"] or 0)
 reasons = [k for k in h if k.startswith("stall_") and "Not Issued" not in k]
 tot = sum(S(d) for d in data)
