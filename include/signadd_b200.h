@@ -45,9 +45,19 @@ enum sa_ndft_mode {
                         to transforms.py:223-251                               */
 };
 
-enum sa_nlfft_variant { SA_DIT = 0, SA_DIF = 1 };
+enum sa_nlfft_variant {
+  SA_DIT = 0,       /* nonlinear FFT, nfft (transforms.py:254-298)                  */
+  SA_DIF = 1,       /* nonlinear FFT, decimation in frequency      */
+  SA_FFT_EXACT = 2  /* exact radix-2 DIT FFT, fft_exact (transforms.py:200-220):
+                       numpy's complex multiply of the twiddle, bit-exact           */
+};
 
-enum sa_doppler { SA_DOPPLER_NLFFT = 0, SA_DOPPLER_NDFT = 1 };
+enum sa_doppler { SA_DOPPLER_NLFFT = 0, SA_DOPPLER_NDFT = 1, SA_DOPPLER_FFT_EXACT = 2 };
+
+enum sa_lag_kind {
+  SA_LAG_MF = 0,    /* sign-additive lag product, lag_product_mf (eq12a / eq12b)   */
+  SA_LAG_EXACT = 1  /* exact multiply, lag_product_exact (eq11 / eq12c)            */
+};
 
 /* ABI version (SA_ABI_VERSION). */
 int sa_version(void);
@@ -83,6 +93,7 @@ int sa_ndft(int dtype, const void *x, void *y, int64_t batch, int64_t n, const v
 /* Batched N-point nonlinear FFT, n a power of two >= 2.
  * SA_DIT replaces nfft (transforms.py:254-298), value-identical.
  * SA_DIF is the decimation-in-frequency convention of DESIGN.md (no reference).
+ * SA_FFT_EXACT replaces fft_exact (transforms.py:200-220), bit-exact.
  * Input scaled by gain first (gain == 1.0: untouched).  x == y is allowed. */
 int sa_nlfft(int dtype, int variant, const void *x, void *y, int64_t batch, int64_t n,
              const void *tw, double gain, void *stream);
@@ -92,6 +103,12 @@ int sa_nlfft(int dtype, int variant, const void *x, void *y, int64_t batch, int6
  * (ambiguity.py:121-128 -> SA_ERR_CONTRACT). */
 int sa_lag_product_mf(int dtype, const void *surv, const void *ref, int64_t n, int64_t ref_len,
                       int64_t lag, int conj, void *out, void *stream);
+
+/* One exact lag-product row: out[i] = surv[i] * conj?(ref[i-lag]) with numpy's
+ * complex multiply, ref[<0] = 0.  Replaces: lag_product_exact
+ * (ambiguity.py:134-143), same guards as sa_lag_product_mf. */
+int sa_lag_product_exact(int dtype, const void *surv, const void *ref, int64_t n, int64_t ref_len,
+                         int64_t lag, int conj, void *out, void *stream);
 
 /* Workspace needed by sa_ambiguity_map (may be 0). */
 int sa_ambiguity_workspace_bytes(int dtype, int64_t l_count, int64_t m, int64_t *bytes);
@@ -116,6 +133,21 @@ int sa_ambiguity_map(int dtype, const void *surv, const void *ref, int64_t ns, i
 int sa_ambiguity_integrate(int dtype, const void *surv, const void *ref, int64_t ns,
                            int64_t ref_len, int64_t l0, int64_t l_count, int64_t m, int conj,
                            int mode, void *z, void *stream);
+
+/* sa_ambiguity_map for every variant of ambiguity.py:5-14: lag_kind
+ * SA_LAG_MF / SA_LAG_EXACT and doppler SA_DOPPLER_NLFFT / _NDFT / _FFT_EXACT.
+ * With m == ns: eq11 = (EXACT, FFT_EXACT), eq12a = (MF, NLFFT),
+ * eq12b = (MF, FFT_EXACT), eq12c = (EXACT, NLFFT) (ambiguity.py:190-221), all
+ * value-identical.  The exact lag product is always summed sequentially. */
+int sa_ambiguity_map_v(int dtype, int lag_kind, const void *surv, const void *ref, int64_t ns,
+                       int64_t ref_len, int64_t l0, int64_t l_count, int64_t m, double gain, int conj,
+                       int doppler, int mode, const void *tw, void *out, void *workspace,
+                       int64_t ws_bytes, void *stream);
+
+/* sa_ambiguity_integrate with a lag kind. */
+int sa_ambiguity_integrate_v(int dtype, int lag_kind, const void *surv, const void *ref, int64_t ns,
+                             int64_t ref_len, int64_t l0, int64_t l_count, int64_t m, int conj,
+                             int mode, void *z, void *stream);
 
 /* Workspace bytes for sa_map_peaks. */
 int sa_peaks_workspace_bytes(int64_t rows, int64_t cols, int k, int64_t *bytes);

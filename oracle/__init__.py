@@ -35,6 +35,8 @@ __all__ = [
     "nfft",
     "lag_product_mf",
     "ambiguity_map",
+    "fft_exact",
+    "lag_product_exact",
     "abs_np",
     "find_peaks",
     "map_floor",
@@ -65,6 +67,12 @@ def _load():
         getattr(lib, f"or_lag_product_mf_{sfx}").argtypes = [i64, p, p, i64, ci, p]
         getattr(lib, f"or_ambiguity_map_{sfx}").argtypes = [
             i64, p, p, i64, i64, i64, ctypes.c_double, ci, ci, p, p, ci]
+        getattr(lib, f"or_ambiguity_map_v_{sfx}").argtypes = [
+            i64, p, p, i64, i64, i64, ctypes.c_double, ci, ci, ci, p, p, ci]
+        getattr(lib, f"or_ambiguity_map_v_{sfx}").restype = ci
+        getattr(lib, f"or_fft_exact_{sfx}").argtypes = [i64, i64, p, p, p, ci]
+        getattr(lib, f"or_fft_exact_{sfx}").restype = ci
+        getattr(lib, f"or_lag_product_exact_{sfx}").argtypes = [i64, p, p, i64, ci, p]
         for name in ("ndft", "nfft", "lag_product_mf", "ambiguity_map"):
             getattr(lib, f"or_{name}_{sfx}").restype = ci
         getattr(lib, f"or_abs_np_{sfx}").argtypes = [i64, p, p]
@@ -168,10 +176,42 @@ def lag_product_mf(surv, ref, lag: int, n: int | None = None, conj: bool = True,
     return out
 
 
+def fft_exact(x, dtype: str = "f64", nthreads: int = 1) -> np.ndarray:
+    """Batched exact radix-2 DIT FFT over the last axis (transforms.py:200-220)."""
+    lib = _load()
+    x = _prep(x, dtype)
+    n = x.shape[-1]
+    y = np.empty_like(x)
+    tw = _table(n, dtype)
+    rc = getattr(lib, f"or_fft_exact_{dtype}")(x.size // max(n, 1), n, _ptr(x), _ptr(tw), _ptr(y), nthreads)
+    if rc:
+        raise ValueError("oracle fft_exact: size must be a power of two")
+    return y
+
+
+def lag_product_exact(surv, ref, lag: int, n: int | None = None, conj: bool = True,
+                      dtype: str = "f64") -> np.ndarray:
+    """ambiguity.py:134-143 (numpy complex multiply, guards are the caller's)."""
+    lib = _load()
+    surv = _prep(surv, dtype)
+    ref = _prep(ref, dtype)
+    if n is None:
+        n = surv.size
+    assert surv.size >= n and ref.size >= n - lag and 0 <= lag
+    out = np.empty(n, dtype=surv.dtype)
+    getattr(lib, f"or_lag_product_exact_{dtype}")(n, _ptr(surv), _ptr(ref), lag, int(conj), _ptr(out))
+    return out
+
+
+_DOPPLER = {"nfft": 0, "ndft": 1, "fft": 2}
+
+
 def ambiguity_map(surv, ref, l0: int, l_count: int, m: int, gain: float = 1.0,
                   conj: bool = True, doppler: str = "nfft", dtype: str = "f64",
-                  nthreads: int = 1) -> np.ndarray:
-    """Rows l0..l0+l_count-1 of the block-integrated eq12a map."""
+                  nthreads: int = 1, lag: str = "mf") -> np.ndarray:
+    """Rows l0..l0+l_count-1 of the block-integrated map: lag "mf"
+    (eq12a/eq12b) or "exact" (eq11/eq12c); doppler "nfft", "ndft" or "fft"
+    (fft_exact).  With m == len(surv) (T = 1) these are the reference variants."""
     lib = _load()
     surv = _prep(surv, dtype)
     ref = _prep(ref, dtype)
@@ -179,10 +219,9 @@ def ambiguity_map(surv, ref, l0: int, l_count: int, m: int, gain: float = 1.0,
     assert ref.size >= ns
     out = np.empty((l_count, m), dtype=surv.dtype)
     tw = _table(m, dtype)
-    d = 0 if doppler == "nfft" else 1
-    rc = getattr(lib, f"or_ambiguity_map_{dtype}")(
-        ns, _ptr(surv), _ptr(ref), l0, l_count, m, float(gain), int(conj), d,
-        _ptr(tw), _ptr(out), nthreads)
+    rc = getattr(lib, f"or_ambiguity_map_v_{dtype}")(
+        ns, _ptr(surv), _ptr(ref), l0, l_count, m, float(gain), int(conj), 0 if lag == "mf" else 1,
+        _DOPPLER[doppler], _ptr(tw), _ptr(out), nthreads)
     if rc:
         raise ValueError("oracle ambiguity_map: bad sizes")
     return out

@@ -91,7 +91,7 @@ static int64_t or_bitrev(int64_t i, int64_t bits) {
 /* ------------------------------------------------------------------------ */
 /* Templated body: instantiated for double (f64) and float (f32)            */
 /* ------------------------------------------------------------------------ */
-#define OR_DEFINE(T, SFX, FABS)                                                    \
+#define OR_DEFINE(T, SFX, FABS, FMA)                                               \
     /* np.sign: +1 / -1 / +0 (np.sign(-0.0) == +0.0) -- operator.py:121 */         \
     static inline T or_sgn_##SFX(T v) { return v > (T)0 ? (T)1 : (v < (T)0 ? (T)-1 : (T)0); } \
     /* operator.py:124-125: sign(a)*sign(b)*(|a|+|b|), one rounding (the sum) */   \
@@ -102,6 +102,15 @@ static int64_t or_bitrev(int64_t i, int64_t bits) {
     static inline void or_mfc_##SFX(T ar, T ai, T br, T bi, T *rr, T *ri) {         \
         *rr = or_mfr_##SFX(ar, br) - or_mfr_##SFX(ai, bi);                         \
         *ri = or_mfr_##SFX(ai, br) + or_mfr_##SFX(bi, ar);                         \
+    }                                                                              \
+    /* numpy complex multiply a*b as the reference host computes it (SIMD loop, \
+     * verified bit-exact): re = fma(ar, br, -(ai*bi)), im = fma(ar, bi, ai*br). \
+     * Used by fft_exact (transforms.py:212) and lag_product_exact            \
+     * (ambiguity.py:134-143). */                                               \
+    static inline void or_npmul_##SFX(T ar, T ai, T br, T bi, T *rr, T *ri) {      \
+        T p = ai * bi, q = ai * br;                                                \
+        *rr = FMA(ar, br, -p);                                                     \
+        *ri = FMA(ar, bi, q);                                                      \
     }                                                                              \
     void or_mf_complex_##SFX(int64_t count, const T *a, const T *b, T *out) {      \
         for (int64_t i = 0; i < count; ++i)                                        \
@@ -205,12 +214,38 @@ static int64_t or_bitrev(int64_t i, int64_t bits) {
             y[2 * r + 1] = tmp[2 * i + 1];                                         \
         }                                                                          \
     }                                                                              \
+    /* transforms.py:200-220 fft_exact: bit-reversed input, stages m = 2..N,   \
+     * t = w_j * b (numpy complex multiply, w_j = entries[j*N/m]),             \
+     * y = [a + t, a - t] per block. */                                           \
+    static void or_fft_exact_one_##SFX(int64_t n, const T *x, const T *tw, T *y) { \
+        int64_t bits = or_log2_pow2(n);                                            \
+        for (int64_t i = 0; i < n; ++i) {                                          \
+            int64_t r = or_bitrev(i, bits);                                        \
+            y[2 * i] = x[2 * r];                                                   \
+            y[2 * i + 1] = x[2 * r + 1];                                           \
+        }                                                                          \
+        for (int64_t m = 2; m <= n; m <<= 1) {                                     \
+            int64_t h = m / 2;                                                     \
+            for (int64_t b0 = 0; b0 < n; b0 += m)                                  \
+                for (int64_t j = 0; j < h; ++j) {                                  \
+                    int64_t w = j * (n / m);                                       \
+                    T *a = y + 2 * (b0 + j), *b = y + 2 * (b0 + j + h);            \
+                    T tr, ti;                                                      \
+                    or_npmul_##SFX(tw[2 * w], tw[2 * w + 1], b[0], b[1], &tr, &ti); \
+                    T ar = a[0], ai = a[1];                                        \
+                    a[0] = ar + tr;                                                \
+                    a[1] = ai + ti;                                                \
+                    b[0] = ar - tr;                                                \
+                    b[1] = ai - ti;                                                \
+                }                                                                  \
+        }                                                                          \
+    }                                                                              \
     typedef struct {                                                               \
         int64_t n;                                                                 \
         const T *x;                                                                \
         const T *tw;                                                               \
         T *y;                                                                      \
-        int kind; /* 0 ndft, 1 dit, 2 dif */                                       \
+        int kind; /* 0 ndft, 1 dit, 2 dif, 3 fft_exact */                          \
     } or_tctx_##SFX;                                                               \
     static void or_tbody_##SFX(void *p, int64_t lo, int64_t hi) {                  \
         or_tctx_##SFX *c = (or_tctx_##SFX *)p;                                     \
@@ -220,7 +255,8 @@ static int64_t or_bitrev(int64_t i, int64_t bits) {
             T *yb = c->y + 2 * c->n * b;                                           \
             if (c->kind == 0) or_ndft_one_##SFX(c->n, xb, c->tw, yb);              \
             else if (c->kind == 1) or_nfft_dit_one_##SFX(c->n, xb, c->tw, yb, tmp); \
-            else or_nfft_dif_one_##SFX(c->n, xb, c->tw, yb, tmp);                  \
+            else if (c->kind == 2) or_nfft_dif_one_##SFX(c->n, xb, c->tw, yb, tmp); \
+            else or_fft_exact_one_##SFX(c->n, xb, c->tw, yb);                      \
         }                                                                          \
         free(tmp);                                                                 \
     }                                                                              \
@@ -236,6 +272,30 @@ static int64_t or_bitrev(int64_t i, int64_t bits) {
         if (or_log2_pow2(n) < 0 || batch < 0) return -1;                           \
         or_tctx_##SFX c = {n, x, tw, y, variant == 1 ? 2 : 1};                     \
         or_parallel_for(batch, nthreads, or_tbody_##SFX, &c);                      \
+        return 0;                                                                  \
+    }                                                                              \
+    int or_fft_exact_##SFX(int64_t batch, int64_t n, const T *x, const T *tw, T *y, \
+                           int nthreads) {                                         \
+        if (or_log2_pow2(n) < 0 || batch < 0) return -1;                           \
+        or_tctx_##SFX c = {n, x, tw, y, 3};                                        \
+        or_parallel_for(batch, nthreads, or_tbody_##SFX, &c);                      \
+        return 0;                                                                  \
+    }                                                                              \
+    /* ambiguity.py:134-143 lag_product_exact: y = surv * conj(shifted), where  \
+     * shifted[i] = ref[i-l] (0 for i < l) and np.conj negates the imaginary    \
+     * part (0 -> -0); numpy complex multiply. */                                 \
+    int or_lag_product_exact_##SFX(int64_t n, const T *surv, const T *ref,         \
+                                   int64_t lag, int conj, T *out) {                \
+        for (int64_t i = 0; i < n; ++i) {                                          \
+            T cr = (T)0, ci = (T)0;                                                \
+            if (i >= lag) {                                                        \
+                cr = ref[2 * (i - lag)];                                           \
+                ci = ref[2 * (i - lag) + 1];                                       \
+            }                                                                      \
+            if (conj) ci = -ci;                                                    \
+            or_npmul_##SFX(surv[2 * i], surv[2 * i + 1], cr, ci, &out[2 * i],      \
+                           &out[2 * i + 1]);                                       \
+        }                                                                          \
         return 0;                                                                  \
     }                                                                              \
     /* ambiguity.py:116-131,146-155: y[i] = surv[i] (x) conj(ref[i-l]), ref      \
@@ -260,7 +320,7 @@ static int64_t or_bitrev(int64_t i, int64_t bits) {
         int64_t ns, m, l0;                                                         \
         const T *surv, *ref, *tw;                                                  \
         double gain;                                                               \
-        int conj, doppler;                                                         \
+        int conj, doppler, lag_kind;                                               \
         T *out;                                                                    \
     } or_actx_##SFX;                                                               \
     static void or_abody_##SFX(void *p, int64_t lo, int64_t hi) {                  \
@@ -270,7 +330,10 @@ static int64_t or_bitrev(int64_t i, int64_t bits) {
         T *tmp = (T *)malloc(sizeof(T) * 2 * c->m);                                \
         int64_t tb = c->ns / c->m;                                                 \
         for (int64_t r = lo; r < hi; ++r) {                                        \
-            or_lag_product_mf_##SFX(c->ns, c->surv, c->ref, c->l0 + r, c->conj, y); \
+            if (c->lag_kind == 0)                                                  \
+                or_lag_product_mf_##SFX(c->ns, c->surv, c->ref, c->l0 + r, c->conj, y); \
+            else                                                                   \
+                or_lag_product_exact_##SFX(c->ns, c->surv, c->ref, c->l0 + r, c->conj, y); \
             for (int64_t q = 0; q < c->m; ++q) {                                   \
                 T sr = (T)0, si = (T)0;                                            \
                 for (int64_t t = 0; t < tb; ++t) {                                 \
@@ -286,7 +349,8 @@ static int64_t or_bitrev(int64_t i, int64_t bits) {
             }                                                                      \
             T *row = c->out + 2 * c->m * r;                                        \
             if (c->doppler == 0) or_nfft_dit_one_##SFX(c->m, z, c->tw, row, tmp);  \
-            else or_ndft_one_##SFX(c->m, z, c->tw, row);                           \
+            else if (c->doppler == 1) or_ndft_one_##SFX(c->m, z, c->tw, row);      \
+            else or_fft_exact_one_##SFX(c->m, z, c->tw, row);                      \
         }                                                                          \
         free(y);                                                                   \
         free(z);                                                                   \
@@ -296,19 +360,28 @@ static int64_t or_bitrev(int64_t i, int64_t bits) {
      * T = ns/m consecutive products (sequential, from +0), times gain, then     \
      * the M-point NL-FFT (doppler 0) or NDFT (doppler 1).  T == 1 is exactly    \
      * ambiguity_eq12a (ambiguity.py:197-202). */                                 \
+    /* lag_kind 0: sign-additive lag product (eq12a/b), 1: exact multiply      \
+     * (eq11/eq12c); doppler 0: nfft, 1: ndft, 2: fft_exact. */                   \
+    int or_ambiguity_map_v_##SFX(int64_t ns, const T *surv, const T *ref,          \
+                                 int64_t l0, int64_t l_count, int64_t m,           \
+                                 double gain, int conj, int lag_kind, int doppler, \
+                                 const T *tw, T *out, int nthreads) {              \
+        if (m < 1 || ns % m != 0 || l0 < 0 || l_count < 0) return -1;              \
+        if (doppler != 1 && or_log2_pow2(m) < 0) return -1;                        \
+        or_actx_##SFX c = {ns, m, l0, surv, ref, tw, gain, conj, doppler, lag_kind, out}; \
+        or_parallel_for(l_count, nthreads, or_abody_##SFX, &c);                    \
+        return 0;                                                                  \
+    }                                                                              \
     int or_ambiguity_map_##SFX(int64_t ns, const T *surv, const T *ref,            \
                                int64_t l0, int64_t l_count, int64_t m,             \
                                double gain, int conj, int doppler, const T *tw,    \
                                T *out, int nthreads) {                             \
-        if (m < 1 || ns % m != 0 || l0 < 0 || l_count < 0) return -1;              \
-        if (doppler == 0 && or_log2_pow2(m) < 0) return -1;                        \
-        or_actx_##SFX c = {ns, m, l0, surv, ref, tw, gain, conj, doppler, out};    \
-        or_parallel_for(l_count, nthreads, or_abody_##SFX, &c);                    \
-        return 0;                                                                  \
+        return or_ambiguity_map_v_##SFX(ns, surv, ref, l0, l_count, m, gain, conj, 0, \
+                                        doppler, tw, out, nthreads);               \
     }
 
-OR_DEFINE(double, f64, fabs)
-OR_DEFINE(float, f32, fabsf)
+OR_DEFINE(double, f64, fabs, fma)
+OR_DEFINE(float, f32, fabsf, fmaf)
 
 /* ---- detection (detection.py:85-171), SURVEY §8(f)-1 ------------------------
  * Magnitude: numpy's complex absolute value, as its SIMD loop computes it on the

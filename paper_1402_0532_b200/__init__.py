@@ -19,6 +19,8 @@ from .transforms import (
     ComplexSignal,
     Spectrum,
     TransformKind,
+    fft_exact,
+    fft_exact_complex_muls,
     ndft,
     ndft_batch,
     ndft_complex_ops,
@@ -34,9 +36,13 @@ from .ambiguity import (
     SPEED_OF_LIGHT,
     AmbiguitySurface,
     AmbiguityVariant,
+    ambiguity_eq11,
     ambiguity_eq12a,
+    ambiguity_eq12b,
+    ambiguity_eq12c,
     ambiguity_map,
     compute_ambiguity,
+    lag_product_exact,
     lag_product_mf,
     map_complex_ops,
 )

@@ -19,8 +19,9 @@ if os.environ.get("SA_LIB_PATH"):  # development: time an alternative build of t
 
 SA_C64, SA_C128 = 0, 1
 SA_NDFT_FAST, SA_NDFT_EXACT = 0, 1
-SA_DIT, SA_DIF = 0, 1
-SA_DOPPLER_NLFFT, SA_DOPPLER_NDFT = 0, 1
+SA_DIT, SA_DIF, SA_FFT_EXACT = 0, 1, 2
+SA_LAG_MF, SA_LAG_EXACT = 0, 1
+SA_DOPPLER_NLFFT, SA_DOPPLER_NDFT, SA_DOPPLER_FFT_EXACT = 0, 1, 2
 
 SA_OK, SA_ERR_ARG, SA_ERR_CONTRACT, SA_ERR_DOMAIN, SA_ERR_CUDA, SA_ERR_UNSUPPORTED = 0, -1, -2, -3, -4, -5
 
@@ -40,6 +41,10 @@ SIGNATURES = {
     "sa_ambiguity_map": (_I, [_I, _P, _P, _I64, _I64, _I64, _I64, _I64, _D, _I, _I, _I, _P, _P,
                              _P, _I64, _P]),
     "sa_ambiguity_integrate": (_I, [_I, _P, _P, _I64, _I64, _I64, _I64, _I64, _I, _I, _P, _P]),
+    "sa_lag_product_exact": (_I, [_I, _P, _P, _I64, _I64, _I64, _I, _P, _P]),
+    "sa_ambiguity_map_v": (_I, [_I, _I, _P, _P, _I64, _I64, _I64, _I64, _I64, ctypes.c_double, _I, _I, _I, _P,
+                                _P, _P, _I64, _P]),
+    "sa_ambiguity_integrate_v": (_I, [_I, _I, _P, _P, _I64, _I64, _I64, _I64, _I64, _I, _I, _P, _P]),
     "sa_peaks_workspace_bytes": (_I, [_I64, _I64, _I, ctypes.POINTER(_I64)]),
     "sa_map_peaks": (_I, [_I, _P, _I64, _I64, _I, _P, _P, _P, _P, _I64, _P]),
     "sa_map_floor": (_I, [_I, _P, _I64, _I64, _P, _I, _I, _I, _P, _P]),

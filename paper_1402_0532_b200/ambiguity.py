@@ -2,8 +2,10 @@
 
 Drop-ins (reference file:line):
   * ``lag_product_mf``  (ambiguity.py:146-155, guards :116-131)
+  * ``lag_product_exact`` (ambiguity.py:134-143)
   * ``ambiguity_eq12a`` (ambiguity.py:197-202 via _surface :158-187)
-  * ``compute_ambiguity`` for variant "eq12a" (ambiguity.py:224-239)
+  * ``ambiguity_eq11`` / ``ambiguity_eq12b`` / ``ambiguity_eq12c`` (ambiguity.py:190-221)
+  * ``compute_ambiguity`` for every variant (ambiguity.py:224-239)
   * ``AmbiguitySurface``, ``AmbiguityVariant``, ``SPEED_OF_LIGHT``
 
 Extension: ``ambiguity_map`` -- the block-integrated map of SURVEY §8(d)
@@ -11,9 +13,10 @@ Extension: ``ambiguity_map`` -- the block-integrated map of SURVEY §8(d)
 row_l = NLFFT_M(gain·z_l) or NDFT_M(gain·z_l), T = Ns/M) over any row range,
 device-resident, one stream-ordered call.  With M == Ns it is eq12a.
 
-The exact-arithmetic variants eq11/eq12b/eq12c are not on the north-star path
-("next" row (f)); ``compute_ambiguity`` raises NotImplementedError
-for them rather than computing them on the CPU.
+The exact-arithmetic variants use numpy's complex multiply,
+reproduced bit-for-bit on the device (``sa_npmul``): eq11 / eq12b / eq12c are
+value-identical to the reference, eq12c included (its exact lag residues feed
+the sign decisions of the NL-FFT).
 """
 
 from __future__ import annotations
@@ -27,11 +30,12 @@ import numpy as np
 from . import _native
 from ._device import is_device_tensor, require_cuda, sa_dtype_of, to_device, torch
 from .errors import ContractError, OpCounter, OpCountReport
-from .transforms import ComplexSignal, nfft_complex_ops, ndft_complex_ops
+from .transforms import ComplexSignal, fft_exact_complex_muls, nfft_complex_ops, ndft_complex_ops
 from .twiddle import device_twiddles
 
 __all__ = ["SPEED_OF_LIGHT", "AmbiguityVariant", "AmbiguitySurface", "lag_product_mf",
-           "ambiguity_eq12a", "compute_ambiguity", "ambiguity_map"]
+           "lag_product_exact", "ambiguity_eq11", "ambiguity_eq12a", "ambiguity_eq12b",
+           "ambiguity_eq12c", "compute_ambiguity", "ambiguity_map"]
 
 SPEED_OF_LIGHT = 299_792_458.0
 
@@ -127,6 +131,22 @@ def _dev(x, dtype):
 def lag_product_mf(s_surv, s_ref, l: int, n: int | None = None, conjugate_ref: bool = True,
                    counter: OpCounter | None = None):
     """y[i] = s_surv[i] ⊙ conj(s_ref[i-l]), zero reference for i < l (ambiguity.py:146-155)."""
+    out = _lag_product(s_surv, s_ref, l, n, conjugate_ref, "sa_lag_product_mf")
+    if counter is not None:
+        counter.count_complex(out.shape[0])
+    return out
+
+
+def lag_product_exact(s_surv, s_ref, l: int, n: int | None = None, conjugate_ref: bool = True,
+                      counter: OpCounter | None = None):
+    """y[i] = s_surv[i] * conj(s_ref[i-l]) with numpy's complex multiply (ambiguity.py:134-143)."""
+    out = _lag_product(s_surv, s_ref, l, n, conjugate_ref, "sa_lag_product_exact")
+    if counter is not None:
+        counter.count_complex_mul(out.shape[0])
+    return out
+
+
+def _lag_product(s_surv, s_ref, l, n, conjugate_ref, entry):
     surv = _samples(s_surv)
     ref = _samples(s_ref)
     device_io = is_device_tensor(surv) or is_device_tensor(ref)
@@ -142,21 +162,21 @@ def lag_product_mf(s_surv, s_ref, l: int, n: int | None = None, conjugate_ref: b
     ds = _dev(surv, dt)[:n]
     dr = _dev(ref, dt)
     out = T.empty(n, dtype=dt, device="cuda")
-    _native.check(_native.lib().sa_lag_product_mf(
+    _native.check(getattr(_native.lib(), entry)(
         sa_dtype_of(out), _native.ptr(ds), _native.ptr(dr), n, dr.numel(), l, int(conjugate_ref),
         _native.ptr(out), _native.stream_ptr()))
-    if counter is not None:
-        counter.count_complex(n)
     return out if device_io else out.cpu().numpy()
 
 
 def ambiguity_map(s_surv, s_ref, l_bins: int, m: int, *, l0: int = 0, gain: float = 1.0,
                   conjugate_ref: bool = True, doppler: str = "nfft", mode: str = "fast",
-                  out=None, workspace=None, dtype=None):
-    """Rows l0..l0+l_bins-1 of the block-integrated ⊙ range-Doppler map.
+                  lag: str = "mf", out=None, workspace=None, dtype=None):
+    """Rows l0..l0+l_bins-1 of the block-integrated range-Doppler map.
 
     Inputs: CUDA tensors (stay on device, no sync) or host arrays (result
     returned on the host).  Ns = len(s_surv); T = Ns / m must be an integer.
+    lag: "mf" (⊙, eq12a/eq12b) or "exact" (numpy multiply, eq11/eq12c);
+    doppler: "nfft", "ndft" or "fft" (fft_exact).
     """
     T = torch()
     surv = _samples(s_surv)
@@ -181,11 +201,16 @@ def ambiguity_map(s_surv, s_ref, l_bins: int, m: int, *, l0: int = 0, gain: floa
     _native.check(_native.lib().sa_ambiguity_workspace_bytes(d, l_bins, m, ctypes.byref(need)))
     if workspace is None or workspace.numel() * workspace.element_size() < need.value:
         workspace = T.empty(max(1, need.value), dtype=T.uint8, device=ds.device)
-    dop = {"nfft": _native.SA_DOPPLER_NLFFT, "ndft": _native.SA_DOPPLER_NDFT}[doppler]
+    dop = {"nfft": _native.SA_DOPPLER_NLFFT, "ndft": _native.SA_DOPPLER_NDFT,
+           "fft": _native.SA_DOPPLER_FFT_EXACT}[doppler]
     md = {"fast": _native.SA_NDFT_FAST, "exact": _native.SA_NDFT_EXACT}[mode]
+    lk = {"mf": _native.SA_LAG_MF, "exact": _native.SA_LAG_EXACT}[lag]
+    if doppler != "ndft" and (m < 2 or (m & (m - 1)) != 0):
+        raise ContractError(f"{'nfft' if doppler == 'nfft' else 'fft_exact'}: size must be a power of two >= 2, "
+                            f"got {m}")
     tw = device_twiddles(m, d, ds.device.index)
-    _native.check(_native.lib().sa_ambiguity_map(
-        d, _native.ptr(ds), _native.ptr(dr), ns, dr.numel(), l0, l_bins, m, float(gain),
+    _native.check(_native.lib().sa_ambiguity_map_v(
+        d, lk, _native.ptr(ds), _native.ptr(dr), ns, dr.numel(), l0, l_bins, m, float(gain),
         int(conjugate_ref), dop, md, ctypes.c_void_p(tw), _native.ptr(out), _native.ptr(workspace),
         workspace.numel() * workspace.element_size(), _native.stream_ptr()))
     return out if device_io else out.cpu().numpy()
@@ -204,12 +229,19 @@ def _surface_rate(s_surv, s_ref) -> float:
     return fs
 
 
-def ambiguity_eq12a(s_surv, s_ref, l_bins: int, n: int, transform_input_gain: float = 1.0,
-                    conjugate_ref: bool = True) -> AmbiguitySurface:
-    """Fully sign-additive surface: ⊙ lag product into the NL-FFT (ambiguity.py:197-202).
+# variant -> (lag product, Doppler transform) (ambiguity.py:5-14)
+_VARIANTS = {
+    AmbiguityVariant.EQ11: ("exact", "fft"),
+    AmbiguityVariant.EQ12A: ("mf", "nfft"),
+    AmbiguityVariant.EQ12B: ("mf", "fft"),
+    AmbiguityVariant.EQ12C: ("exact", "nfft"),
+}
 
-    All l_bins rows in one device call; value-identical to the reference.
-    """
+
+def _surface(variant: AmbiguityVariant, s_surv, s_ref, l_bins: int, n: int, gain: float,
+             conjugate_ref: bool) -> AmbiguitySurface:
+    """_surface (ambiguity.py:158-187) for one variant: all l_bins rows in one
+    device call, value-identical to the reference row loop."""
     if l_bins < 1:
         raise ContractError("l_bins must be >= 1")
     fs = _surface_rate(s_surv, s_ref)
@@ -217,29 +249,62 @@ def ambiguity_eq12a(s_surv, s_ref, l_bins: int, n: int, transform_input_gain: fl
     ref = np.asarray(_samples(s_ref), dtype=complex)
     for l in (0, l_bins - 1):
         _lag_guards(surv.size, ref.size, l, n)
+    lag, doppler = _VARIANTS[variant]
     if n < 2 or (n & (n - 1)) != 0:
-        raise ContractError(f"nfft: size must be a power of two >= 2, got {n}")
-    vals = ambiguity_map(surv[:n], ref, l_bins, n, gain=transform_input_gain,
-                         conjugate_ref=conjugate_ref, doppler="nfft", mode="exact")
+        raise ContractError(f"{'nfft' if doppler == 'nfft' else 'fft_exact'}: size must be a power of two >= 2, "
+                            f"got {n}")
+    vals = ambiguity_map(surv[:n], ref, l_bins, n, gain=gain, conjugate_ref=conjugate_ref,
+                         doppler=doppler, mode="exact", lag=lag)
     lag_c = OpCounter()
-    lag_c.count_complex(l_bins * n)
+    if lag == "mf":
+        lag_c.count_complex(l_bins * n)
+    else:
+        lag_c.count_complex_mul(l_bins * n)
     tr_c = OpCounter()
-    tr_c.count_complex(l_bins * nfft_complex_ops(n))
+    if doppler == "nfft":
+        tr_c.count_complex(l_bins * nfft_complex_ops(n))
+    else:
+        tr_c.count_complex_mul(l_bins * fft_exact_complex_muls(n))
     return AmbiguitySurface(values=vals, range_bin_m=SPEED_OF_LIGHT / fs, doppler_bin_hz=fs / n,
-                            variant=AmbiguityVariant.EQ12A, sample_rate_hz=fs,
+                            variant=variant, sample_rate_hz=fs,
                             lag_op_counts=lag_c.report(), transform_op_counts=tr_c.report())
+
+
+def ambiguity_eq11(s_surv, s_ref, l_bins: int, n: int, conjugate_ref: bool = True) -> AmbiguitySurface:
+    """Classic cross-ambiguity: exact lag product, exact FFT (ambiguity.py:190-194)."""
+    return _surface(AmbiguityVariant.EQ11, s_surv, s_ref, l_bins, n, 1.0, conjugate_ref)
+
+
+def ambiguity_eq12a(s_surv, s_ref, l_bins: int, n: int, transform_input_gain: float = 1.0,
+                    conjugate_ref: bool = True) -> AmbiguitySurface:
+    """Fully sign-additive surface: ⊙ lag product into the NL-FFT (ambiguity.py:197-202)."""
+    return _surface(AmbiguityVariant.EQ12A, s_surv, s_ref, l_bins, n, transform_input_gain, conjugate_ref)
+
+
+def ambiguity_eq12b(s_surv, s_ref, l_bins: int, n: int, conjugate_ref: bool = True) -> AmbiguitySurface:
+    """⊙ lag product, exact FFT (ambiguity.py:205-209)."""
+    return _surface(AmbiguityVariant.EQ12B, s_surv, s_ref, l_bins, n, 1.0, conjugate_ref)
+
+
+def ambiguity_eq12c(s_surv, s_ref, l_bins: int, n: int, transform_input_gain: float = 1.0,
+                    conjugate_ref: bool = True) -> AmbiguitySurface:
+    """Exact lag product into the NL-FFT (ambiguity.py:212-221)."""
+    return _surface(AmbiguityVariant.EQ12C, s_surv, s_ref, l_bins, n, transform_input_gain, conjugate_ref)
 
 
 def compute_ambiguity(variant, s_surv, s_ref, l_bins: int, n: int,
                       transform_input_gain: float = 1.0,
                       conjugate_ref: bool = True) -> AmbiguitySurface:
-    """Dispatch on variant (ambiguity.py:224-239); eq12a is the B200 path."""
+    """Dispatch on variant (ambiguity.py:224-239); the gain reaches only the
+    nonlinear-FFT variants."""
     variant = AmbiguityVariant(variant)
+    if variant is AmbiguityVariant.EQ11:
+        return ambiguity_eq11(s_surv, s_ref, l_bins, n, conjugate_ref)
     if variant is AmbiguityVariant.EQ12A:
         return ambiguity_eq12a(s_surv, s_ref, l_bins, n, transform_input_gain, conjugate_ref)
-    raise NotImplementedError(
-        f"variant {variant.value} uses exact multiplication (out of the ⊙ hot path; "
-        "see DESIGN.md 'out of scope')")
+    if variant is AmbiguityVariant.EQ12B:
+        return ambiguity_eq12b(s_surv, s_ref, l_bins, n, conjugate_ref)
+    return ambiguity_eq12c(s_surv, s_ref, l_bins, n, transform_input_gain, conjugate_ref)
 
 
 def map_complex_ops(l_bins: int, ns: int, m: int, doppler: str = "nfft") -> int:

@@ -121,7 +121,8 @@ int sa_ndft(int dtype, const void *x, void *y, int64_t batch, int64_t n, const v
 int sa_nlfft(int dtype, int variant, const void *x, void *y, int64_t batch, int64_t n,
              const void *tw, double gain, void *stream) {
   SA_REQUIRE(dtype_ok(dtype), SA_ERR_ARG, "bad dtype %d", dtype);
-  SA_REQUIRE(variant == SA_DIT || variant == SA_DIF, SA_ERR_ARG, "bad variant %d", variant);
+  SA_REQUIRE(variant == SA_DIT || variant == SA_DIF || variant == SA_FFT_EXACT, SA_ERR_ARG, "bad variant %d",
+             variant);
   SA_REQUIRE(pow2(n), SA_ERR_CONTRACT, "nfft: size must be a power of two >= 2, got %lld",
              (long long)n);
   SA_REQUIRE(batch >= 0, SA_ERR_ARG, "negative batch");
@@ -151,7 +152,18 @@ int sa_lag_product_mf(int dtype, const void *surv, const void *ref, int64_t n, i
   int rc = lag_guards(n, n, ref_len, lag);
   if (rc) return rc;
   SA_REQUIRE(n == 0 || (surv && ref && out), SA_ERR_ARG, "null pointer");
-  return sa_launch_lag_product(dtype, surv, ref, n, ref_len, lag, conj, out, (cudaStream_t)stream);
+  return sa_launch_lag_product(dtype, SA_LAG_MF, surv, ref, n, ref_len, lag, conj, out, (cudaStream_t)stream);
+}
+
+int sa_lag_product_exact(int dtype, const void *surv, const void *ref, int64_t n, int64_t ref_len,
+                         int64_t lag, int conj, void *out, void *stream) {
+  SA_REQUIRE(dtype_ok(dtype), SA_ERR_ARG, "bad dtype %d", dtype);
+  SA_REQUIRE(n >= 0, SA_ERR_ARG, "negative n");
+  int rc = lag_guards(n, n, ref_len, lag);
+  if (rc) return rc;
+  SA_REQUIRE(n == 0 || (surv && ref && out), SA_ERR_ARG, "null pointer");
+  return sa_launch_lag_product(dtype, SA_LAG_EXACT, surv, ref, n, ref_len, lag, conj, out,
+                               (cudaStream_t)stream);
 }
 
 int sa_ambiguity_workspace_bytes(int dtype, int64_t l_count, int64_t m, int64_t *bytes) {
@@ -164,12 +176,21 @@ int sa_ambiguity_map(int dtype, const void *surv, const void *ref, int64_t ns, i
                      int64_t l0, int64_t l_count, int64_t m, double gain, int conj, int doppler,
                      int mode, const void *tw, void *out, void *workspace, int64_t ws_bytes,
                      void *stream) {
+  return sa_ambiguity_map_v(dtype, SA_LAG_MF, surv, ref, ns, ref_len, l0, l_count, m, gain, conj, doppler,
+                            mode, tw, out, workspace, ws_bytes, stream);
+}
+
+int sa_ambiguity_map_v(int dtype, int lag_kind, const void *surv, const void *ref, int64_t ns,
+                       int64_t ref_len, int64_t l0, int64_t l_count, int64_t m, double gain, int conj,
+                       int doppler, int mode, const void *tw, void *out, void *workspace,
+                       int64_t ws_bytes, void *stream) {
   SA_REQUIRE(dtype_ok(dtype), SA_ERR_ARG, "bad dtype %d", dtype);
+  SA_REQUIRE(lag_kind == SA_LAG_MF || lag_kind == SA_LAG_EXACT, SA_ERR_ARG, "bad lag kind %d", lag_kind);
   SA_REQUIRE(l_count >= 1, SA_ERR_CONTRACT, "l_bins must be >= 1");
   SA_REQUIRE(m >= 1 && ns >= m && ns % m == 0, SA_ERR_CONTRACT,
              "map: ns=%lld must be a positive multiple of m=%lld", (long long)ns, (long long)m);
-  SA_REQUIRE(doppler == SA_DOPPLER_NLFFT || doppler == SA_DOPPLER_NDFT, SA_ERR_ARG,
-             "bad doppler %d", doppler);
+  SA_REQUIRE(doppler == SA_DOPPLER_NLFFT || doppler == SA_DOPPLER_NDFT || doppler == SA_DOPPLER_FFT_EXACT,
+             SA_ERR_ARG, "bad doppler %d", doppler);
   SA_REQUIRE(doppler == SA_DOPPLER_NDFT || pow2(m), SA_ERR_CONTRACT,
              "nfft: size must be a power of two >= 2, got %lld", (long long)m);
   SA_REQUIRE(mode == SA_NDFT_FAST || mode == SA_NDFT_EXACT, SA_ERR_ARG, "bad mode %d", mode);
@@ -182,15 +203,15 @@ int sa_ambiguity_map(int dtype, const void *surv, const void *ref, int64_t ns, i
   int64_t need = sa_ambiguity_ws_bytes(dtype, l_count, m);
   SA_REQUIRE(workspace && ws_bytes >= need, SA_ERR_ARG, "workspace too small: %lld < %lld bytes",
              (long long)ws_bytes, (long long)need);
-  rc = check_tw(tw, dtype, m, doppler == SA_DOPPLER_NLFFT);
+  rc = check_tw(tw, dtype, m, doppler != SA_DOPPLER_NDFT);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
-  rc = sa_launch_lag_integrate(dtype, surv, ref, ns, ref_len, l0, l_count, m, conj, mode,
+  rc = sa_launch_lag_integrate(dtype, lag_kind, surv, ref, ns, ref_len, l0, l_count, m, conj, mode,
                                workspace, s);
   if (rc) return rc;
-  if (doppler == SA_DOPPLER_NLFFT)
-    return sa_launch_nlfft(dtype, SA_DIT, workspace, out, l_count, m, (const SaTwiddles *)tw, gain,
-                           s);
+  if (doppler != SA_DOPPLER_NDFT)
+    return sa_launch_nlfft(dtype, doppler == SA_DOPPLER_NLFFT ? SA_DIT : SA_FFT_EXACT, workspace, out, l_count,
+                           m, (const SaTwiddles *)tw, gain, s);
   return sa_launch_ndft(dtype, workspace, out, l_count, m, (const SaTwiddles *)tw,
                         ns == m ? SA_NDFT_EXACT : mode, gain, s);
 }
@@ -198,7 +219,15 @@ int sa_ambiguity_map(int dtype, const void *surv, const void *ref, int64_t ns, i
 int sa_ambiguity_integrate(int dtype, const void *surv, const void *ref, int64_t ns,
                            int64_t ref_len, int64_t l0, int64_t l_count, int64_t m, int conj,
                            int mode, void *z, void *stream) {
+  return sa_ambiguity_integrate_v(dtype, SA_LAG_MF, surv, ref, ns, ref_len, l0, l_count, m, conj, mode, z,
+                                  stream);
+}
+
+int sa_ambiguity_integrate_v(int dtype, int lag_kind, const void *surv, const void *ref, int64_t ns,
+                             int64_t ref_len, int64_t l0, int64_t l_count, int64_t m, int conj,
+                             int mode, void *z, void *stream) {
   SA_REQUIRE(dtype_ok(dtype), SA_ERR_ARG, "bad dtype %d", dtype);
+  SA_REQUIRE(lag_kind == SA_LAG_MF || lag_kind == SA_LAG_EXACT, SA_ERR_ARG, "bad lag kind %d", lag_kind);
   SA_REQUIRE(l_count >= 1, SA_ERR_CONTRACT, "l_bins must be >= 1");
   SA_REQUIRE(m >= 1 && ns >= m && ns % m == 0, SA_ERR_CONTRACT,
              "map: ns=%lld must be a positive multiple of m=%lld", (long long)ns, (long long)m);
@@ -208,7 +237,7 @@ int sa_ambiguity_integrate(int dtype, const void *surv, const void *ref, int64_t
   rc = lag_guards(ns, ns, ref_len, l0);
   if (rc) return rc;
   SA_REQUIRE(surv && ref && z, SA_ERR_ARG, "null pointer");
-  return sa_launch_lag_integrate(dtype, surv, ref, ns, ref_len, l0, l_count, m, conj, mode, z,
+  return sa_launch_lag_integrate(dtype, lag_kind, surv, ref, ns, ref_len, l0, l_count, m, conj, mode, z,
                                  (cudaStream_t)stream);
 }
 

@@ -32,7 +32,10 @@ constexpr int LAGS_PER_CTA = LAG_WARPS * LAGS_PER_WARP;  // 64
 
 __host__ __device__ __forceinline__ int pad8(int s) { return s + (s >> 3); }  // one 16B/32B pad per 8 entries
 
-template <typename T>
+// EXACT = false: lag_product_mf (ambiguity.py:146-155); EXACT = true:
+// lag_product_exact (ambiguity.py:134-143), surv * np.conj(shifted) with
+// numpy's complex multiply (np.conj of the zero prefix gives imag -0).
+template <typename T, bool EXACT>
 __global__ void __launch_bounds__(256) k_lag_product(const C2<T> *__restrict__ surv,
                                                      const C2<T> *__restrict__ ref, int64_t n,
                                                      int64_t lag, bool conj,
@@ -45,18 +48,25 @@ __global__ void __launch_bounds__(256) k_lag_product(const C2<T> *__restrict__ s
       C2<T> r = ref[i - lag];
       cr = r.x;
       ci = conj ? -r.y : r.y;
+    } else if (EXACT && conj) {
+      ci = -T(0);
     }
     C2<T> o;
-    T rr, ri;
-    sa_mfc_literal<T>(a.x, a.y, cr, ci, rr, ri);  // operand order (surv, ref): :152
-    sa_np_complex<T>(rr, ri, o.x, o.y);          // rr + 1j*ri (:155)
+    if (EXACT) {
+      sa_npmul<T>(a.x, a.y, cr, ci, o.x, o.y);
+    } else {
+      T rr, ri;
+      sa_mfc_literal<T>(a.x, a.y, cr, ci, rr, ri);  // operand order (surv, ref): :152
+      sa_np_complex<T>(rr, ri, o.x, o.y);          // rr + 1j*ri (:155)
+    }
     out[i] = o;
   }
 }
 
-// Exact / generic: one thread per (lag, q); every ⊙ rounded, sequential sum
-// over t from +0 (identical to the oracle's composition; T == 1 -> eq12a rows).
-template <typename T>
+// Exact / generic: one thread per (lag, q); every product rounded, sequential
+// sum over t from +0 (identical to the oracle's composition; T == 1 -> the
+// reference rows).  EXACT selects the exact-multiply lag product (eq11/eq12c).
+template <typename T, bool EXACT>
 __global__ void __launch_bounds__(256) k_lag_integrate_exact(
     const C2<T> *__restrict__ surv, const C2<T> *__restrict__ ref, int64_t ref_len, int64_t l0,
     int64_t l_count, int64_t m, int64_t tb, bool conj, C2<T> *__restrict__ z) {
@@ -77,7 +87,8 @@ __global__ void __launch_bounds__(256) k_lag_integrate_exact(
       ci = -T(0);
     }
     T rr, ri;
-    sa_mfc_literal<T>(a.x, a.y, cr, ci, rr, ri);
+    if (EXACT) sa_npmul<T>(a.x, a.y, cr, ci, rr, ri);
+    else sa_mfc_literal<T>(a.x, a.y, cr, ci, rr, ri);
     sr = sa_add(sr, rr);
     si = sa_add(si, ri);
   }
@@ -332,18 +343,20 @@ __global__ void __launch_bounds__(256, 2) k_lag_integrate_f32x2(
 }
 
 template <typename T>
-int launch_integrate(const void *survv, const void *refv, int64_t ns, int64_t ref_len, int64_t l0,
-                     int64_t l_count, int64_t m, int conj, int mode, void *zv, cudaStream_t s) {
+int launch_integrate(int lag_kind, const void *survv, const void *refv, int64_t ns, int64_t ref_len,
+                     int64_t l0, int64_t l_count, int64_t m, int conj, int mode, void *zv, cudaStream_t s) {
   const C2<T> *surv = (const C2<T> *)survv;
   const C2<T> *ref = (const C2<T> *)refv;
   C2<T> *z = (C2<T> *)zv;
   const int64_t tb = ns / m;
   if (l_count == 0 || m == 0) return SA_OK;
-  const bool fast = mode == SA_NDFT_FAST && tb % 8 == 0 && tb <= 8192 && m <= 0x7fffffff;
+  // the exact-multiply lag product always takes the sequential kernel
+  const bool fast = lag_kind == SA_LAG_MF && mode == SA_NDFT_FAST && tb % 8 == 0 && tb <= 8192 &&
+                    m <= 0x7fffffff;
   if (!fast) {
     int64_t tot = l_count * m;
-    k_lag_integrate_exact<T><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(
-        surv, ref, ref_len, l0, l_count, m, tb, conj != 0, z);
+    auto kern = lag_kind == SA_LAG_EXACT ? k_lag_integrate_exact<T, true> : k_lag_integrate_exact<T, false>;
+    kern<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(surv, ref, ref_len, l0, l_count, m, tb, conj != 0, z);
     SA_LAUNCH_CHECK();
     return SA_OK;
   }
@@ -384,25 +397,28 @@ int64_t sa_ambiguity_ws_bytes(int dtype, int64_t l_count, int64_t m) {
   return l_count * m * (dtype == SA_C64 ? (int64_t)sizeof(float2) : (int64_t)sizeof(double2));
 }
 
-int sa_launch_lag_product(int dtype, const void *surv, const void *ref, int64_t n, int64_t ref_len,
-                          int64_t lag, int conj, void *out, cudaStream_t s) {
+template <typename T>
+void launch_lag_product(int lag_kind, const void *surv, const void *ref, int64_t n, int64_t lag, int conj,
+                        void *out, cudaStream_t s) {
+  const int g = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  auto kern = lag_kind == SA_LAG_EXACT ? k_lag_product<T, true> : k_lag_product<T, false>;
+  kern<<<g, 256, 0, s>>>((const C2<T> *)surv, (const C2<T> *)ref, n, lag, conj != 0, (C2<T> *)out);
+}
+
+int sa_launch_lag_product(int dtype, int lag_kind, const void *surv, const void *ref, int64_t n,
+                          int64_t ref_len, int64_t lag, int conj, void *out, cudaStream_t s) {
   (void)ref_len;
   if (n == 0) return SA_OK;
-  int g = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
-  if (dtype == SA_C64)
-    k_lag_product<float><<<g, 256, 0, s>>>((const float2 *)surv, (const float2 *)ref, n, lag,
-                                           conj != 0, (float2 *)out);
-  else
-    k_lag_product<double><<<g, 256, 0, s>>>((const double2 *)surv, (const double2 *)ref, n, lag,
-                                            conj != 0, (double2 *)out);
+  if (dtype == SA_C64) launch_lag_product<float>(lag_kind, surv, ref, n, lag, conj, out, s);
+  else launch_lag_product<double>(lag_kind, surv, ref, n, lag, conj, out, s);
   SA_LAUNCH_CHECK();
   return SA_OK;
 }
 
-int sa_launch_lag_integrate(int dtype, const void *surv, const void *ref, int64_t ns,
+int sa_launch_lag_integrate(int dtype, int lag_kind, const void *surv, const void *ref, int64_t ns,
                             int64_t ref_len, int64_t l0, int64_t l_count, int64_t m, int conj,
                             int mode, void *z, cudaStream_t s) {
   if (dtype == SA_C64)
-    return launch_integrate<float>(surv, ref, ns, ref_len, l0, l_count, m, conj, mode, z, s);
-  return launch_integrate<double>(surv, ref, ns, ref_len, l0, l_count, m, conj, mode, z, s);
+    return launch_integrate<float>(lag_kind, surv, ref, ns, ref_len, l0, l_count, m, conj, mode, z, s);
+  return launch_integrate<double>(lag_kind, surv, ref, ns, ref_len, l0, l_count, m, conj, mode, z, s);
 }

@@ -78,6 +78,17 @@ template <typename T> SA_HD void sa_np_complex(T rr, T ri, T &re, T &im) {
   im = sa_add(ri, T(0));
 }
 
+// numpy complex multiply a*b as the reference host's SIMD loop computes it
+// (verified bit-exact, oracle/signadd_oracle.c or_npmul):
+//   re = fma(ar, br, -(ai*bi)),  im = fma(ar, bi, ai*br)
+// Used by the exact-multiply variants: fft_exact (transforms.py:212) and
+// lag_product_exact (ambiguity.py:134-143).
+template <typename T> SA_HD void sa_npmul(T ar, T ai, T br, T bi, T &rr, T &ri) {
+  const T p = sa_mul(ai, bi), q = sa_mul(ai, br);
+  rr = sa_fma(ar, br, -p);
+  ri = sa_fma(ar, bi, q);
+}
+
 // Same value, identity form with precomputed signs (sa = sgn(a) etc.)
 template <typename T> SA_HD T sa_mfr_id(T a, T sa, T b, T sb) { return sa_fma(sa, b, sa_mul(sb, a)); }
 

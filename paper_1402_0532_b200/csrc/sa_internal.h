@@ -73,8 +73,8 @@ int sa_launch_map_peaks(int dtype, const void *map, int64_t rows, int64_t cols, 
                         int *count, void *ws, cudaStream_t s);
 int sa_launch_map_floor(int dtype, const void *map, int64_t rows, int64_t cols, const int *centers, int ncent,
                         int g0, int g1, unsigned long long *out, cudaStream_t s);
-int sa_launch_lag_product(int dtype, const void *surv, const void *ref, int64_t n, int64_t ref_len,
+int sa_launch_lag_product(int dtype, int lag_kind, const void *surv, const void *ref, int64_t n, int64_t ref_len,
                           int64_t lag, int conj, void *out, cudaStream_t s);
-int sa_launch_lag_integrate(int dtype, const void *surv, const void *ref, int64_t ns,
+int sa_launch_lag_integrate(int dtype, int lag_kind, const void *surv, const void *ref, int64_t ns,
                             int64_t ref_len, int64_t l0, int64_t l_count, int64_t m, int conj,
                             int mode, void *z, cudaStream_t s);

@@ -5,6 +5,8 @@
 // w_j = entries[j*N/m] to the odd branch, top = a + w⊗b and bot = a + (−w)⊗b,
 // evaluated as a − (w⊗b) which is exactly equal (test_operator.py:225-229).
 // DIF follows the DESIGN.md convention (no reference; "parity unpinned").
+// The same kernels run fft_exact (transforms.py:200-220, variant SA_FFT_EXACT):
+// every stage an exact butterfly with numpy's complex multiply of the raw twiddle.
 //
 // Node layout is free (SURVEY §7 hard part 4): the reference's bit-reversed
 // array is never materialised in HBM; bit reversal is folded into smem
@@ -54,6 +56,17 @@ template <typename T> SA_HD void bfly_two_point(C2<T> &a, C2<T> &b) {
   b = {sa_sub(ur, tr), sa_sub(ui, ti)};
 }
 
+// Exact DIT butterfly of fft_exact (transforms.py:210-214): t = w * b with
+// numpy's complex multiply, a <- a + t, b <- a − t.  Raw twiddle (wr, wi).
+template <typename T> SA_HD void bfly_exact(C2<T> &a, C2<T> &b, const C2<T> &w) {
+  T tr, ti;
+  sa_npmul<T>(w.x, w.y, b.x, b.y, tr, ti);
+  C2<T> top = {sa_add(a.x, tr), sa_add(a.y, ti)};
+  C2<T> bot = {sa_sub(a.x, tr), sa_sub(a.y, ti)};
+  a = top;
+  b = bot;
+}
+
 // DIF butterfly: a <- a + b ; b <- w ⊗ (a − b)
 template <typename T> SA_HD void bfly_dif(C2<T> &a, C2<T> &b, const C4<T> &w) {
   T dr = sa_sub(a.x, b.x), di = sa_sub(a.y, b.y);
@@ -76,12 +89,14 @@ __device__ void tile_stage(C2<T> *sm, int TC, int L, int t, const TwF &twf) {
     int p = ((k >> (t - 1)) << t) | (k & (h - 1));
     C2<T> x = sm[p * TC + col];
     C2<T> y = sm[(p + h) * TC + col];
-    if (KIND == 0) {
+    if constexpr (KIND == 0) {
       bfly_two_point<T>(x, y);
-    } else if (KIND == 1) {
+    } else if constexpr (KIND == 1) {
       bfly_dit<T>(x, y, twf(h, p, col));
-    } else {
+    } else if constexpr (KIND == 2) {
       bfly_dif<T>(x, y, twf(h, p, col));
+    } else {
+      bfly_exact<T>(x, y, twf(h, p, col));
     }
     sm[p * TC + col] = x;
     sm[(p + h) * TC + col] = y;
@@ -107,14 +122,31 @@ template <typename T> struct TwCols {
   }
 };
 
+// Raw-twiddle functors for the exact FFT (stage-packed raw table, same indexing)
+template <typename T> struct TwLocalRaw {
+  const C2<T> *stage2;
+  SA_HD C2<T> operator()(int h, int p, int) const { return sa_ldg(&stage2[(h - 1) + (p & (h - 1))]); }
+};
+template <typename T> struct TwColsRaw {
+  const C2<T> *stage2;
+  int n2, q0;
+  SA_HD C2<T> operator()(int h, int R, int col) const {
+    int64_t hg = (int64_t)h * n2;
+    return sa_ldg(&stage2[(hg - 1) + (int64_t)(R & (h - 1)) * n2 + q0 + col]);
+  }
+};
+
+// V: 0 = DIT nfft, 1 = DIF, 2 = exact radix-2 DIT FFT (fft_exact).
 // ---------------------------------------------------------------------------
 // Single pass: SPB whole transforms per CTA, all log2 N stages on chip.
 // ---------------------------------------------------------------------------
-template <typename T, bool DIF>
+template <typename T, int V>
 __global__ void __launch_bounds__(256) k_nlfft_single(const C2<T> *__restrict__ x, C2<T> *y,
                                                       int64_t batch, int logn, int spb,
-                                                      const C4<T> *__restrict__ stage, T gain,
+                                                      const C4<T> *__restrict__ stage,
+                                                      const C2<T> *__restrict__ stage2, T gain,
                                                       bool use_gain) {
+  constexpr bool DIF = V == 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C2<T> *sm = reinterpret_cast<C2<T> *>(smem_raw);
   const int n = 1 << logn;
@@ -134,7 +166,10 @@ __global__ void __launch_bounds__(256) k_nlfft_single(const C2<T> *__restrict__ 
   }
   __syncthreads();
   TwLocal<T> twf{stage};
-  if (!DIF) {
+  if constexpr (V == 2) {
+    TwLocalRaw<T> twr{stage2};
+    for (int t = 1; t <= logn; ++t) tile_stage<T, 3>(sm, spb, n, t, twr);
+  } else if constexpr (!DIF) {
     tile_stage<T, 0>(sm, spb, n, 1, twf);
     for (int t = 2; t <= logn; ++t) tile_stage<T, 1>(sm, spb, n, t, twf);
   } else {
@@ -155,11 +190,13 @@ __global__ void __launch_bounds__(256) k_nlfft_single(const C2<T> *__restrict__ 
 //   DIF (pass 2): sub-transform for row R = rev_N1(c) reads buf[R*N2 + q], DIF
 //                 stages log N2..2 + final 2-point, writes out[rev_N2(q)*N1 + c].
 // ---------------------------------------------------------------------------
-template <typename T, bool DIF>
+template <typename T, int V>
 __global__ void __launch_bounds__(256) k_nlfft_rows(const C2<T> *__restrict__ in, C2<T> *out,
                                                     int logn1, int logn2, int tc,
-                                                    const C4<T> *__restrict__ stage, T gain,
+                                                    const C4<T> *__restrict__ stage,
+                                                    const C2<T> *__restrict__ stage2, T gain,
                                                     bool use_gain) {
+  constexpr bool DIF = V == 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C2<T> *sm = reinterpret_cast<C2<T> *>(smem_raw);
   const int n1 = 1 << logn1, n2 = 1 << logn2;
@@ -183,8 +220,13 @@ __global__ void __launch_bounds__(256) k_nlfft_rows(const C2<T> *__restrict__ in
   __syncthreads();
   TwLocal<T> twf{stage};
   if (!DIF) {
-    tile_stage<T, 0>(sm, tc, n2, 1, twf);
-    for (int t = 2; t <= logn2; ++t) tile_stage<T, 1>(sm, tc, n2, t, twf);
+    if constexpr (V == 2) {
+      TwLocalRaw<T> twr{stage2};
+      for (int t = 1; t <= logn2; ++t) tile_stage<T, 3>(sm, tc, n2, t, twr);
+    } else {
+      tile_stage<T, 0>(sm, tc, n2, 1, twf);
+      for (int t = 2; t <= logn2; ++t) tile_stage<T, 1>(sm, tc, n2, t, twf);
+    }
     for (int e = threadIdx.x; e < tot; e += blockDim.x) {
       int q = e % n2, cc = e / n2;  // each sub-transform row contiguous in HBM
       int R = sa_brev(c0 + cc, logn1);
@@ -205,11 +247,13 @@ __global__ void __launch_bounds__(256) k_nlfft_rows(const C2<T> *__restrict__ in
 // transform along R.  DIT pass B (stages log N2+1..log N) or DIF pass 1
 // (stages log N..log N2+1).  In place is safe (tile read fully before write).
 // ---------------------------------------------------------------------------
-template <typename T, bool DIF>
+template <typename T, int V>
 __global__ void __launch_bounds__(256) k_nlfft_cols(const C2<T> *in, C2<T> *out, int logn1,
                                                     int logn2, int tc,
-                                                    const C4<T> *__restrict__ stage, T gain,
+                                                    const C4<T> *__restrict__ stage,
+                                                    const C2<T> *__restrict__ stage2, T gain,
                                                     bool use_gain) {
+  constexpr bool DIF = V == 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C2<T> *sm = reinterpret_cast<C2<T> *>(smem_raw);
   const int n1 = 1 << logn1, n2 = 1 << logn2;
@@ -226,7 +270,10 @@ __global__ void __launch_bounds__(256) k_nlfft_cols(const C2<T> *in, C2<T> *out,
   }
   __syncthreads();
   TwCols<T> twf{stage, n2, q0};
-  if (!DIF) {
+  if constexpr (V == 2) {
+    TwColsRaw<T> twr{stage2, n2, q0};
+    for (int t = 1; t <= logn1; ++t) tile_stage<T, 3>(sm, tc, n1, t, twr);
+  } else if constexpr (!DIF) {
     for (int t = 1; t <= logn1; ++t) tile_stage<T, 1>(sm, tc, n1, t, twf);
   } else {
     for (int t = logn1; t >= 1; --t) tile_stage<T, 2>(sm, tc, n1, t, twf);
@@ -251,6 +298,7 @@ int launch(int variant, const void *xv, void *yv, int64_t batch, int64_t n, cons
   const C2<T> *x = (const C2<T> *)xv;
   C2<T> *y = (C2<T> *)yv;
   const C4<T> *stage = (const C4<T> *)tw->stage;
+  const C2<T> *stage2 = (const C2<T> *)tw->stage2;
   const bool use_gain = gain != 1.0;
   const T g = (T)gain;
   const int logn = sa_ilog2_host(n);
@@ -261,19 +309,14 @@ int launch(int variant, const void *xv, void *yv, int64_t batch, int64_t n, cons
     spb = (int)std::min<int64_t>(spb, batch);
     size_t bytes = sizeof(C2<T>) * (size_t)spb * n;
     int64_t blocks = (batch + spb - 1) / spb;
-    if (variant == SA_DIT) {
-      if (set_smem(k_nlfft_single<T, false>, bytes)) return SA_ERR_CUDA;
-      k_nlfft_single<T, false><<<(unsigned)blocks, 256, bytes, s>>>(x, y, batch, logn, spb, stage,
-                                                                    g, use_gain);
-    } else {
-      if (set_smem(k_nlfft_single<T, true>, bytes)) return SA_ERR_CUDA;
-      k_nlfft_single<T, true><<<(unsigned)blocks, 256, bytes, s>>>(x, y, batch, logn, spb, stage,
-                                                                   g, use_gain);
-    }
+    auto kern = variant == SA_DIT ? k_nlfft_single<T, 0>
+                : variant == SA_DIF ? k_nlfft_single<T, 1> : k_nlfft_single<T, 2>;
+    if (set_smem(kern, bytes)) return SA_ERR_CUDA;
+    kern<<<(unsigned)blocks, 256, bytes, s>>>(x, y, batch, logn, spb, stage, stage2, g, use_gain);
     SA_LAUNCH_CHECK();
     return SA_OK;
   }
-  {
+  if (variant != SA_FFT_EXACT) {
     // N = 2^16: persistent work-queue kernel (out of place) or the cluster kernel
     // default: cluster kernel (measured faster); SA_NLFFT_IMPL=2p selects the
     // persistent work-queue kernel (out of place, DIT) for comparison.
@@ -305,24 +348,24 @@ int launch(int variant, const void *xv, void *yv, int64_t batch, int64_t n, cons
   size_t bytes_cols = sizeof(C2<T>) * (size_t)tc * n1;
   int64_t grid_rows = batch * (n1 / tc);
   int64_t grid_cols = batch * (n2 / tc);
-  if (variant == SA_DIT) {
-    if (set_smem(k_nlfft_rows<T, false>, bytes_rows)) return SA_ERR_CUDA;
-    if (set_smem(k_nlfft_cols<T, false>, bytes_cols)) return SA_ERR_CUDA;
-    k_nlfft_rows<T, false><<<(unsigned)grid_rows, 256, bytes_rows, s>>>(x, y, logn1, logn2, tc,
-                                                                        stage, g, use_gain);
-    k_nlfft_cols<T, false><<<(unsigned)grid_cols, 256, bytes_cols, s>>>(y, y, logn1, logn2, tc,
-                                                                        stage, g, false);
+  if (variant != SA_DIF) {
+    auto rows = variant == SA_DIT ? k_nlfft_rows<T, 0> : k_nlfft_rows<T, 2>;
+    auto cols = variant == SA_DIT ? k_nlfft_cols<T, 0> : k_nlfft_cols<T, 2>;
+    if (set_smem(rows, bytes_rows)) return SA_ERR_CUDA;
+    if (set_smem(cols, bytes_cols)) return SA_ERR_CUDA;
+    rows<<<(unsigned)grid_rows, 256, bytes_rows, s>>>(x, y, logn1, logn2, tc, stage, stage2, g, use_gain);
+    cols<<<(unsigned)grid_cols, 256, bytes_cols, s>>>(y, y, logn1, logn2, tc, stage, stage2, g, false);
   } else {
-    if (set_smem(k_nlfft_rows<T, true>, bytes_rows)) return SA_ERR_CUDA;
-    if (set_smem(k_nlfft_cols<T, true>, bytes_cols)) return SA_ERR_CUDA;
+    if (set_smem(k_nlfft_rows<T, 1>, bytes_rows)) return SA_ERR_CUDA;
+    if (set_smem(k_nlfft_cols<T, 1>, bytes_cols)) return SA_ERR_CUDA;
     // pass 2 scatters rows to bit-reversed output columns, so it cannot run in
     // place: pass 1 writes a stream-ordered scratch, pass 2 reads it.
     C2<T> *scratch = nullptr;
     SA_CUDA_TRY(cudaMallocAsync((void **)&scratch, sizeof(C2<T>) * (size_t)(batch * n), s));
-    k_nlfft_cols<T, true><<<(unsigned)grid_cols, 256, bytes_cols, s>>>(x, scratch, logn1, logn2,
-                                                                       tc, stage, g, use_gain);
-    k_nlfft_rows<T, true><<<(unsigned)grid_rows, 256, bytes_rows, s>>>(scratch, y, logn1, logn2,
-                                                                       tc, stage, g, false);
+    k_nlfft_cols<T, 1><<<(unsigned)grid_cols, 256, bytes_cols, s>>>(x, scratch, logn1, logn2, tc, stage,
+                                                                    stage2, g, use_gain);
+    k_nlfft_rows<T, 1><<<(unsigned)grid_rows, 256, bytes_rows, s>>>(scratch, y, logn1, logn2, tc, stage,
+                                                                    stage2, g, false);
     SA_CUDA_TRY(cudaFreeAsync(scratch, s));
   }
   SA_LAUNCH_CHECK();

@@ -32,8 +32,8 @@ from .twiddle import TwiddleTable, device_twiddles, twiddle_table
 
 __all__ = [
     "ComplexSignal", "TransformKind", "Spectrum", "TwiddleTable", "twiddle_table", "unit_tone",
-    "ndft", "nfft", "ndft_batch", "nfft_batch", "peak_index", "ndft_complex_ops",
-    "nfft_complex_ops", "nfft_butterflies", "nfft_dif_complex_ops",
+    "ndft", "nfft", "fft_exact", "ndft_batch", "nfft_batch", "peak_index", "ndft_complex_ops",
+    "nfft_complex_ops", "nfft_butterflies", "nfft_dif_complex_ops", "fft_exact_complex_muls",
 ]
 
 
@@ -158,6 +158,24 @@ def nfft(x, counter: OpCounter | None = None) -> Spectrum:
     return Spectrum(bins, TransformKind.NFFT, local.report())
 
 
+def fft_exact(x, counter: OpCounter | None = None) -> Spectrum:
+    """Exact radix-2 DIT FFT, bit-identical to transforms.py:200-220 (numpy's
+    complex multiply of every twiddle product reproduced on the device)."""
+    v = _as_samples(x)
+    n = v.size
+    logn = _require_pow2(n, "fft_exact")
+    require_cuda()
+    d = to_device(v, torch().complex128).view(1, n)
+    y = torch().empty_like(d)
+    _launch_nlfft(d, y, _native.SA_FFT_EXACT, 1.0)
+    local = OpCounter()
+    local.count_complex_mul((n // 2) * logn)
+    bins = y.view(n).cpu().numpy()
+    if counter is not None:
+        counter.merge(local)
+    return Spectrum(bins, TransformKind.FFT_EXACT, local.report())
+
+
 # --- batched extension -------------------------------------------------------------
 
 def _batched(x, out, check_finite: bool, dtype):
@@ -231,8 +249,9 @@ def ndft_batch(x, *, mode: str = "fast", gain: float = 1.0, out=None, check_fini
 
 def nfft_batch(x, *, variant: str = "dit", gain: float = 1.0, out=None, check_finite: bool = False,
                dtype=None):
-    """Batched NL-FFT (DIT = reference nfft; DIF = DESIGN.md convention)."""
-    v = {"dit": _native.SA_DIT, "dif": _native.SA_DIF}[variant]
+    """Batched NL-FFT (DIT = reference nfft; DIF = DESIGN.md convention);
+    variant "exact" is the exact-multiply fft_exact (transforms.py:200-220)."""
+    v = {"dit": _native.SA_DIT, "dif": _native.SA_DIF, "exact": _native.SA_FFT_EXACT}[variant]
     xd, yd, host = _batched(x, out, check_finite, dtype)
     _require_pow2(xd.shape[1], "nfft")
     _launch_nlfft(xd, yd, v, gain)
@@ -258,6 +277,11 @@ def nfft_complex_ops(n: int) -> int:
 
 def nfft_butterflies(n: int) -> int:
     return (n // 2) * _require_pow2(n, "nfft_butterflies")
+
+
+def fft_exact_complex_muls(n: int) -> int:
+    """(N/2)*log2(N) twiddle products (transforms.py:213)."""
+    return (n // 2) * _require_pow2(n, "fft_exact_complex_muls")
 
 
 def nfft_dif_complex_ops(n: int) -> int:

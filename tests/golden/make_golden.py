@@ -152,6 +152,33 @@ def main() -> None:
         rows.append(sa.ndft(0.5 * zz).bins)
     g["map_ns4096_m64_ndft_l100_g05"] = np.stack(rows)
 
+    # --- exact-multiply variants: fft_exact, lag_product_exact,
+    #     eq11 / eq12b / eq12c surfaces ----------------------------------------
+    r = np.random.default_rng(14020537)
+    for n in (2, 4, 8, 64, 512, 4096):
+        x = r.standard_normal(n) + 1j * r.standard_normal(n)
+        g[f"fftx_x_{n}"] = x
+        g[f"fftx_y_{n}"] = sa.fft_exact(x).bins
+    xz = np.zeros(16, complex)
+    xz[3] = -0.0 - 0.0j
+    g["fftx_zero16"] = sa.fft_exact(xz).bins
+    sv = r.standard_normal(256) + 1j * r.standard_normal(256)
+    rf = np.exp(2j * np.pi * r.random(256))
+    g["vx_surv"], g["vx_ref"] = sv, rf
+    for l in (0, 1, 37, 255):
+        g[f"lagx_{l}"] = sa.lag_product_exact(sv, rf, l, 256)
+    g["lagx_noconj_5"] = sa.lag_product_exact(sv, rf, 5, 256, conjugate_ref=False)
+    S, R = sa.ComplexSignal(sv, fs), sa.ComplexSignal(rf, fs)
+    for var in ("eq11", "eq12b", "eq12c"):
+        sf = sa.compute_ambiguity(var, S, R, 12, 256, transform_input_gain=4.0)
+        g[f"amb_{var}"] = sf.values
+        g[f"amb_{var}_counts"] = np.array([
+            sf.lag_op_counts.sign_ops, sf.lag_op_counts.abs_ops, sf.lag_op_counts.add_ops,
+            sf.lag_op_counts.complex_mf_ops, sf.lag_op_counts.complex_mul_ops,
+            sf.transform_op_counts.sign_ops, sf.transform_op_counts.abs_ops, sf.transform_op_counts.add_ops,
+            sf.transform_op_counts.complex_mf_ops, sf.transform_op_counts.complex_mul_ops])
+    g["amb_eq12c_noconj_g1"] = sa.compute_ambiguity("eq12c", S, R, 6, 256, conjugate_ref=False).values
+
     # --- detection: magnitudes, find_peaks, classify, floor -----
     import signadd.detection as det
     r = np.random.default_rng(14020536)

@@ -72,8 +72,16 @@ def test_contracts_raise_before_device():
         sa.ambiguity_eq12a(S(np.ones(8), 1.0), S(np.ones(8), 2.0), 2, 8)
     with pytest.raises(sa.ContractError):
         sa.ambiguity_eq12a(S(np.ones(8), 1.0), S(np.ones(8), 1.0), 0, 8)
-    with pytest.raises(NotImplementedError):
-        sa.compute_ambiguity("eq11", S(np.ones(8), 1.0), S(np.ones(8), 1.0), 2, 8)
+    for var in ("eq11", "eq12b", "eq12c"):  # exact-multiply variants: same contracts
+        with pytest.raises(sa.ContractError, match="power of two"):
+            sa.compute_ambiguity(var, S(np.ones(12), 1.0), S(np.ones(12), 1.0), 2, 12)
+        with pytest.raises(sa.ContractError):
+            sa.compute_ambiguity(var, S(np.ones(8), 1.0), S(np.ones(8), 1.0), 9, 8)
+    for n in (1, 3, 12):
+        with pytest.raises(sa.ContractError, match="fft_exact"):
+            sa.fft_exact(np.ones(n, complex))
+    with pytest.raises(sa.ContractError):
+        sa.lag_product_exact(np.ones(8, complex), np.ones(8, complex), 8)
 
 
 def test_no_cpu_fallback_without_gpu():

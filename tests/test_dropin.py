@@ -138,3 +138,29 @@ def test_reference_classify_through_dropin(ref, sa):
         dropin.uninstall(ref)
     assert gpu == cpu  # statuses, overall, floor, peaks (reference Peak objects)
     assert gpu_floor == cpu_floor
+
+
+@pytest.mark.gpu
+def test_reference_exact_variants_through_dropin(ref, sa, golden):
+    """compute_ambiguity for eq11 / eq12b / eq12c (and fft_exact, the CLI's
+    'fft' transform) through the drop-in equal the reference's own CPU results."""
+    from paper_1402_0532_b200 import dropin
+    import signadd.cli as cmod
+    fs = 200_000.0
+    S, R = ref.ComplexSignal(golden["vx_surv"], fs), ref.ComplexSignal(golden["vx_ref"], fs)
+    cpu = {v: ref.compute_ambiguity(v, S, R, 5, 256, transform_input_gain=2.0) for v in ("eq11", "eq12b", "eq12c")}
+    x = golden["fftx_x_512"]
+    cpu_fft = ref.fft_exact(x)
+    dropin.install(ref)
+    try:
+        assert cmod._TRANSFORMS["fft"].__module__ == "paper_1402_0532_b200.dropin"
+        for v, c in cpu.items():
+            g = ref.compute_ambiguity(v, S, R, 5, 256, transform_input_gain=2.0)
+            assert isinstance(g, ref.AmbiguitySurface) and g.variant is c.variant
+            assert np.array_equal(g.values, c.values)
+            assert g.op_counts == c.op_counts
+        f = ref.fft_exact(x)
+        assert np.array_equal(f.bins, cpu_fft.bins) and f.op_counts == cpu_fft.op_counts
+        assert f.transform_kind is ref.TransformKind.FFT_EXACT
+    finally:
+        dropin.uninstall(ref)

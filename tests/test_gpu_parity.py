@@ -406,3 +406,69 @@ def test_map_c64_block_lengths(sa, tb):
                                            nthreads=8), TOL_F32)
     ye = sa.ambiguity_map(dev(surv), dev(ref), L, m, l0=l0, mode="exact").cpu().numpy()
     assert_value_equal(ye, oracle.ambiguity_map(surv, ref, l0, L, m, dtype="f32", nthreads=8))
+
+
+# --- exact-multiply variants --------------------------------------
+
+@pytest.mark.parametrize("n", [2, 4, 8, 64, 512, 4096])
+def test_fft_exact_dropin_golden(sa, golden, n):
+    s = sa.fft_exact(golden[f"fftx_x_{n}"])
+    assert s.transform_kind is sa.TransformKind.FFT_EXACT
+    assert s.bins.tobytes() == golden[f"fftx_y_{n}"].tobytes()  # bitwise, signed zeros included
+    assert s.op_counts.complex_mul_ops == (n // 2) * int(np.log2(n))
+
+
+def test_fft_exact_signed_zero_golden(sa, golden):
+    x = np.zeros(16, complex)
+    x[3] = -0.0 - 0.0j
+    assert sa.fft_exact(x).bins.tobytes() == golden["fftx_zero16"].tobytes()
+
+
+@pytest.mark.parametrize("logn", [1, 5, 12, 13, 14, 16, 18])
+@pytest.mark.parametrize("dt", ["c64", "c128"])
+def test_fft_exact_batch_vs_oracle(sa, logn, dt):
+    """Single-pass (n <= 2^13 / 2^12) and two-pass kernels, 2^16 included (the
+    fused ⊙ kernel is not used for the exact FFT)."""
+    n = 1 << logn
+    b = max(1, min(64, (1 << 19) // n))
+    g = np.random.default_rng(300 + logn)
+    x = (g.standard_normal((b, n)) + 1j * g.standard_normal((b, n))).astype(np.complex64 if dt == "c64" else complex)
+    y = sa.nfft_batch(dev(x), variant="exact").cpu().numpy()
+    assert_value_equal(y, oracle.fft_exact(x, dtype="f32" if dt == "c64" else "f64", nthreads=8))
+
+
+def test_lag_product_exact_golden(sa, golden):
+    sv, rf = golden["vx_surv"], golden["vx_ref"]
+    for l in (0, 1, 37, 255):
+        assert sa.lag_product_exact(sv, rf, l, 256).tobytes() == golden[f"lagx_{l}"].tobytes()
+    assert sa.lag_product_exact(sv, rf, 5, 256, conjugate_ref=False).tobytes() == golden["lagx_noconj_5"].tobytes()
+
+
+@pytest.mark.parametrize("var", ["eq11", "eq12b", "eq12c"])
+def test_exact_variant_surfaces_golden(sa, golden, var):
+    S = sa.ComplexSignal
+    sv, rf = golden["vx_surv"], golden["vx_ref"]
+    sf = sa.compute_ambiguity(var, S(sv, 200_000.0), S(rf, 200_000.0), 12, 256, transform_input_gain=4.0)
+    assert sf.variant.value == var
+    assert_value_equal(sf.values, golden[f"amb_{var}"])
+    c = golden[f"amb_{var}_counts"]
+    got = [sf.lag_op_counts.sign_ops, sf.lag_op_counts.abs_ops, sf.lag_op_counts.add_ops,
+           sf.lag_op_counts.complex_mf_ops, sf.lag_op_counts.complex_mul_ops,
+           sf.transform_op_counts.sign_ops, sf.transform_op_counts.abs_ops, sf.transform_op_counts.add_ops,
+           sf.transform_op_counts.complex_mf_ops, sf.transform_op_counts.complex_mul_ops]
+    assert got == list(c)
+    if var == "eq12c":
+        v = sa.compute_ambiguity("eq12c", S(sv, 1.0), S(rf, 1.0), 6, 256, conjugate_ref=False).values
+        assert_value_equal(v, golden["amb_eq12c_noconj_g1"])
+
+
+@pytest.mark.parametrize("lag,doppler", [("exact", "fft"), ("mf", "fft"), ("exact", "nfft"), ("exact", "ndft")])
+def test_block_map_exact_variants_vs_oracle(sa, golden, lag, doppler):
+    """Block-integrated maps (T = 64) with every lag / Doppler combination:
+    complex128 value-identical to the oracle composition, complex64 vs the f32 oracle."""
+    rr, s = golden["map_surv"], golden["map_ref"]
+    got = sa.ambiguity_map(rr, s, 20, 64, l0=30, gain=2.0, lag=lag, doppler=doppler, mode="exact")
+    assert_value_equal(got, oracle.ambiguity_map(rr, s, 30, 20, 64, gain=2.0, lag=lag, doppler=doppler))
+    r32, s32 = rr.astype(np.complex64), s.astype(np.complex64)
+    got = sa.ambiguity_map(dev(r32), dev(s32), 20, 64, l0=30, lag=lag, doppler=doppler, mode="exact").cpu().numpy()
+    assert_value_equal(got, oracle.ambiguity_map(r32, s32, 30, 20, 64, lag=lag, doppler=doppler, dtype="f32"))

@@ -156,3 +156,37 @@ def test_scenario_detection_golden(golden):
         assert n_out > 0
         db = max(20.0 * np.log10(out / gmax), -300.0)
         assert db == float(golden[f"det_scn_floor_{g0}_{g1}"])
+
+
+# --- exact-multiply variants ------------------------------------
+
+@pytest.mark.parametrize("n", [2, 4, 8, 64, 512, 4096])
+def test_fft_exact_golden(golden, n):
+    _eq(oracle.fft_exact(golden[f"fftx_x_{n}"]), golden[f"fftx_y_{n}"])
+
+
+def test_fft_exact_zero_golden(golden):
+    x = np.zeros(16, complex)
+    x[3] = -0.0 - 0.0j
+    assert oracle.fft_exact(x).tobytes() == golden["fftx_zero16"].tobytes()  # signed zeros too
+
+
+def test_lag_product_exact_golden(golden):
+    sv, rf = golden["vx_surv"], golden["vx_ref"]
+    for l in (0, 1, 37, 255):
+        assert oracle.lag_product_exact(sv, rf, l, 256).tobytes() == golden[f"lagx_{l}"].tobytes()
+    assert oracle.lag_product_exact(sv, rf, 5, 256, conj=False).tobytes() == golden["lagx_noconj_5"].tobytes()
+
+
+@pytest.mark.parametrize("var", ["eq11", "eq12b", "eq12c"])
+def test_exact_variant_surfaces_golden(golden, var):
+    """T = 1 maps with the variant's lag product and Doppler transform equal the
+    reference surfaces (gain 4 reaches only eq12c, ambiguity.py:224-239)."""
+    sv, rf = golden["vx_surv"], golden["vx_ref"]
+    lag = "exact" if var in ("eq11", "eq12c") else "mf"
+    dop = "nfft" if var == "eq12c" else "fft"
+    got = oracle.ambiguity_map(sv, rf, 0, 12, 256, gain=4.0 if var == "eq12c" else 1.0, lag=lag, doppler=dop)
+    _eq(got, golden[f"amb_{var}"])
+    got = oracle.ambiguity_map(sv, rf, 0, 6, 256, conj=False, lag="exact", doppler="nfft") if var == "eq12c" else None
+    if got is not None:
+        _eq(got, golden["amb_eq12c_noconj_g1"])
