@@ -385,12 +385,16 @@ def wl_map(args, ws, rank, c5=False):
     l0 = rank * rows
     out = torch.empty((rows, M), dtype=cdt, device="cuda")
     ws_buf = torch.empty(rows * M * out.element_size(), dtype=torch.uint8, device="cuda")
-    full = torch.empty((L, M), dtype=cdt, device="cuda") if (ws > 1 and rank == 0) else None
+
+    pm = None
+    if ws > 1:  # rank 0's map, IPC-shared once: every rank's kernels store their rows into it
+        from paper_1402_0532_b200.sharded import PeerMap
+        pm = PeerMap(L, M, cdt)
 
     def step():
-        if ws > 1:  # delay-bin shard + NCCL gather of the row blocks to rank 0
+        if ws > 1:  # delay-bin shard, rows stored straight into rank 0's map (NVLink), one barrier
             from paper_1402_0532_b200.sharded import ambiguity_map_sharded
-            ambiguity_map_sharded(surv, ref, L, M, out_full=full, out_local=out, workspace=ws_buf)
+            ambiguity_map_sharded(surv, ref, L, M, peer_map=pm, workspace=ws_buf)
         else:
             sa.ambiguity_map(surv, ref, rows, M, l0=l0, out=out, workspace=ws_buf)
 
@@ -407,7 +411,9 @@ def wl_map(args, ws, rank, c5=False):
            "config": {"workload": ("C5" if c5 else "C4") + " ⊙ range-Doppler map (BASELINE.json configs["
                       + ("4" if c5 else "3") + "])", "ns": ns, "delay_bins": L, "doppler_bins": M,
                       "block_T": ns // M, "doppler": "NL-FFT DIT", "dtype": str(cdt).replace("torch.", ""),
-                      "parallelism": f"delay-bin shards x{ws}" + (", NCCL gather to rank 0" if ws > 1 else "")}}
+                      "parallelism": f"delay-bin shards x{ws}" + (
+                          ", rows stored by the transform kernels into rank 0's IPC-shared map over NVLink, "
+                          "one barrier" if ws > 1 else "")}}
     return res
 
 

@@ -173,6 +173,12 @@ int sa_map_peaks(int dtype, const void *map, int64_t rows, int64_t cols, int k, 
 int sa_map_floor(int dtype, const void *map, int64_t rows, int64_t cols, const int32_t *centers,
                  int ncent, int g0, int g1, uint64_t *out, void *stream);
 
+/* Multi-GPU plumbing: enable direct loads/stores from the current device to
+ * `peer_device` memory (NVLink / NVSwitch).  Idempotent.  Used by the sharded
+ * map, whose Doppler-transform kernels write their rows straight into the
+ * root's map (an IPC mapping of it) instead of gathering afterwards. */
+int sa_enable_peer_access(int peer_device);
+
 /* FMA-pipe peak microbenchmark (roofline denominator): `blocks` CTAs x 256
  * (dtype 2 = packed fp32x2 FFMA2)
  * threads each run `iters` iterations of 8 independent FMA chains; writes a

@@ -269,6 +269,23 @@ int sa_map_floor(int dtype, const void *map, int64_t rows, int64_t cols, const i
                              (cudaStream_t)stream);
 }
 
+int sa_enable_peer_access(int peer_device) {
+  int dev = 0, n = 0, ok = 0;
+  SA_CUDA_TRY(cudaGetDevice(&dev));
+  SA_CUDA_TRY(cudaGetDeviceCount(&n));
+  SA_REQUIRE(peer_device >= 0 && peer_device < n, SA_ERR_ARG, "bad peer device %d", peer_device);
+  if (peer_device == dev) return SA_OK;
+  SA_CUDA_TRY(cudaDeviceCanAccessPeer(&ok, dev, peer_device));
+  SA_REQUIRE(ok, SA_ERR_UNSUPPORTED, "device %d cannot access peer %d", dev, peer_device);
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return SA_OK;
+  }
+  SA_CUDA_TRY(e);
+  return SA_OK;
+}
+
 int sa_fma_peak(int dtype, int64_t iters, void *d_sink, int blocks, void *stream) {
   SA_REQUIRE((dtype_ok(dtype) || dtype == 2) && d_sink && iters > 0 && blocks > 0, SA_ERR_ARG,
              "bad arguments");

@@ -472,3 +472,49 @@ def test_block_map_exact_variants_vs_oracle(sa, golden, lag, doppler):
     r32, s32 = rr.astype(np.complex64), s.astype(np.complex64)
     got = sa.ambiguity_map(dev(r32), dev(s32), 20, 64, l0=30, lag=lag, doppler=doppler, mode="exact").cpu().numpy()
     assert_value_equal(got, oracle.ambiguity_map(r32, s32, 30, 20, 64, lag=lag, doppler=doppler, dtype="f32"))
+
+
+def _p2p_worker(rank, port, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        import paper_1402_0532_b200 as sa
+        from paper_1402_0532_b200.sharded import PeerMap, ambiguity_map_sharded
+        from paper_1402_0532_b200.workloads import radar_scene
+        sc = radar_scene(1 << 16, 2, 4343)
+        ds = torch.from_numpy(sc.surv.astype(np.complex64)).cuda()
+        dr = torch.from_numpy(sc.ref.astype(np.complex64)).cuda()
+        pm = PeerMap(101, 128, ds.dtype)  # odd row count: uneven shards
+        for _ in range(2):  # the shared map is reused across calls
+            full = ambiguity_map_sharded(ds, dr, 101, 128, peer_map=pm)
+        if rank == 0:
+            q.put(bool(torch.equal(full, sa.ambiguity_map(ds, dr, 101, 128))))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_map_p2p_two_ranks_one_gpu(sa):
+    """Fused compute + delivery: two ranks (two processes sharing the GPU, gloo
+    for the host handshake) store their Doppler rows straight into rank 0's
+    IPC-shared map; the result equals the single-call map bit for bit."""
+    import socket
+    import torch.multiprocessing as mp
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_p2p_worker, args=(r, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(300)
+    assert [p.exitcode for p in ps] == [0, 0]
+    assert q.get(timeout=10) is True
