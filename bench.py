@@ -464,8 +464,10 @@ def run_ours(args):
         ems, _ = timed(res["e2e_step"], max(2, args.steps // 2), 1, ws)
         line["e2e"] = {"value": res["ops"] * ws / (ems * 1e-3), "unit": unit, "ms_per_step": ems,
                        "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"],
-                       "api": "paper_1402_0532_b200.ndft_batch(pinned host tensor, out=pinned host tensor)"}
-        line["gpu_launches"] += max(2, args.steps // 2)
+                       "api": "paper_1402_0532_b200.ndft_batch(pinned host tensor, out=pinned host tensor)",
+                       "pipeline": "H2D / transform / D2H overlapped over 16 MiB row chunks"}
+        from paper_1402_0532_b200.transforms import pipeline_chunks
+        line["gpu_launches"] += max(2, args.steps // 2) * pipeline_chunks(res["h2d"])
     # CPU baseline: rank 0, N=1 only
     if rank == 0 and ws == 1 and "cpu" in res and not args.no_cpu:
         P = len(os.sched_getaffinity(0))

@@ -34,6 +34,7 @@ __all__ = [
     "ComplexSignal", "TransformKind", "Spectrum", "TwiddleTable", "twiddle_table", "unit_tone",
     "ndft", "nfft", "fft_exact", "ndft_batch", "nfft_batch", "peak_index", "ndft_complex_ops",
     "nfft_complex_ops", "nfft_butterflies", "nfft_dif_complex_ops", "fft_exact_complex_muls",
+    "pipeline_chunks",
 ]
 
 
@@ -233,6 +234,76 @@ def _finish(yd, host_result, out, x):
     return r.reshape(-1) if np.asarray(x).ndim == 1 else r
 
 
+_SIDE_STREAMS: dict = {}
+
+
+def _pinned_host(t) -> bool:
+    T = torch()
+    return isinstance(t, T.Tensor) and not t.is_cuda and t.is_pinned()
+
+
+def pipeline_chunks(nbytes: int) -> int:
+    """Row chunks of a pinned-host batched call: 16 MiB each, at most 64 --
+    measured best on C2 (512 MiB each way): 22.6 ms end to end vs 21.8 ms for
+    the device-resident transform.  One transform launch per chunk."""
+    return int(max(1, min(64, nbytes // (16 << 20))))
+
+
+def _host_pipelined(x, out, launch_rows, row_align: int, dtype):
+    """Pinned host (B, N) in -> pinned host out, with H2D / compute / D2H
+    overlapped over row chunks: chunk i uploads on one side stream, runs once
+    uploaded (alternating between the current stream and a second compute
+    stream, so consecutive chunks' waves overlap), downloads on another side
+    stream once computed.  PCIe is full duplex, so the transform of chunk i
+    overlaps the copies of chunks i+-1.  Returns the host output (synchronised)."""
+    T = torch()
+    xh = x if x.dim() == 2 else x.reshape(1, -1)
+    if dtype is not None and xh.dtype != dtype:
+        return None  # would need a host-side conversion: take the simple path
+    sa_dtype_of(xh)
+    if out is None:
+        out = T.empty(xh.shape, dtype=xh.dtype, pin_memory=True)
+    oh = out if out.dim() == 2 else out.view(xh.shape)
+    rows, n = xh.shape
+    total = xh.numel() * xh.element_size()
+    chunks = pipeline_chunks(total)
+    step = -(-rows // chunks)
+    step = -(-step // row_align) * row_align
+    dev = T.cuda.current_device()
+    if dev not in _SIDE_STREAMS:
+        _SIDE_STREAMS[dev] = (T.cuda.Stream(), T.cuda.Stream(), T.cuda.Stream())
+    up, down, alt = _SIDE_STREAMS[dev]
+    cur = T.cuda.current_stream()
+    alt.wait_stream(cur)
+    xd = T.empty(xh.shape, dtype=xh.dtype, device="cuda")
+    yd = T.empty_like(xd)
+    up.wait_stream(cur)  # device buffers are fresh allocations on `cur`
+    for r0 in range(0, rows, step):
+        r1 = min(rows, r0 + step)
+        with T.cuda.stream(up):
+            xd[r0:r1].copy_(xh[r0:r1], non_blocking=True)
+            ev_in = T.cuda.Event()
+            ev_in.record(up)
+        # consecutive chunks alternate between two compute streams, so one
+        # chunk's last wave overlaps the next chunk's first
+        ks = alt if (r0 // step) % 2 else cur
+        ks.wait_event(ev_in)
+        with T.cuda.stream(ks):
+            launch_rows(xd[r0:r1], yd[r0:r1])
+        ev_k = T.cuda.Event()
+        ev_k.record(ks)
+        down.wait_event(ev_k)
+        with T.cuda.stream(down):
+            oh[r0:r1].copy_(yd[r0:r1], non_blocking=True)
+    cur.wait_stream(down)
+    xd.record_stream(up)
+    yd.record_stream(down)
+    xd.record_stream(alt)
+    yd.record_stream(alt)
+    cur.synchronize()
+    return out.view(x.shape) if x.dim() == 1 else out
+
+
 def ndft_batch(x, *, mode: str = "fast", gain: float = 1.0, out=None, check_finite: bool = False,
                dtype=None):
     """Batched NDFT over the last axis of a (B, N) complex64/complex128 input.
@@ -242,6 +313,10 @@ def ndft_batch(x, *, mode: str = "fast", gain: float = 1.0, out=None, check_fini
     (as ``transform_gain * y`` in ambiguity.py:176-177).
     """
     m = {"fast": _native.SA_NDFT_FAST, "exact": _native.SA_NDFT_EXACT}[mode]
+    if _pinned_host(x) and (out is None or _pinned_host(out)) and not check_finite:
+        r = _host_pipelined(x, out, lambda a, b: _launch_ndft(a, b, m, gain), 128, dtype)
+        if r is not None:
+            return r
     xd, yd, host = _batched(x, out, check_finite, dtype)
     _launch_ndft(xd, yd, m, gain)
     return _finish(yd, host, out, x)
@@ -252,6 +327,11 @@ def nfft_batch(x, *, variant: str = "dit", gain: float = 1.0, out=None, check_fi
     """Batched NL-FFT (DIT = reference nfft; DIF = DESIGN.md convention);
     variant "exact" is the exact-multiply fft_exact (transforms.py:200-220)."""
     v = {"dit": _native.SA_DIT, "dif": _native.SA_DIF, "exact": _native.SA_FFT_EXACT}[variant]
+    if _pinned_host(x) and (out is None or _pinned_host(out)) and not check_finite:
+        _require_pow2(x.shape[-1], "nfft")
+        r = _host_pipelined(x, out, lambda a, b: _launch_nlfft(a, b, v, gain), 1, dtype)
+        if r is not None:
+            return r
     xd, yd, host = _batched(x, out, check_finite, dtype)
     _require_pow2(xd.shape[1], "nfft")
     _launch_nlfft(xd, yd, v, gain)

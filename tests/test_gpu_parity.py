@@ -518,3 +518,21 @@ def test_sharded_map_p2p_two_ranks_one_gpu(sa):
         p.join(300)
     assert [p.exitcode for p in ps] == [0, 0]
     assert q.get(timeout=10) is True
+
+
+@pytest.mark.parametrize("rows", [1, 129, 5000])
+def test_pinned_host_pipeline_matches_device_path(sa, rows):
+    """ndft_batch / nfft_batch on pinned host tensors run chunked H2D / compute /
+    D2H overlap; results equal the device-resident path bit for bit."""
+    torch = T()
+    g = torch.Generator().manual_seed(rows)
+    n = 1024 if rows < 5000 else 4096
+    x = torch.randn(rows, n, dtype=torch.complex64, generator=g).pin_memory()
+    out = torch.empty_like(x).pin_memory()
+    r = sa.ndft_batch(x, out=out)
+    assert r.data_ptr() == out.data_ptr()
+    assert torch.equal(out, sa.ndft_batch(x.cuda()).cpu())
+    y = sa.nfft_batch(x)
+    assert y.is_pinned() and torch.equal(y, sa.nfft_batch(x.cuda()).cpu())
+    y = sa.nfft_batch(x, variant="dif")
+    assert torch.equal(y, sa.nfft_batch(x.cuda(), variant="dif").cpu())
