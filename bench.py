@@ -503,6 +503,21 @@ def run_ours(args):
             except Exception as ex:  # keep the headline line even if an extra fails
                 extras[name] = {"error": repr(ex)}
         line["workloads"] = extras
+    # C5 map at every N (the north star asks map throughput at 1/2/4/8 GPUs):
+    # all ranks take part -- delay-bin shards, rows stored into rank 0's map
+    # over peer memory -- timed as the max over ranks (strong scaling)
+    if not args.no_extras and w == "ndft":
+        try:
+            r = wl_map(args, ws, rank, c5=True)
+            ems, _ = timed(r["step"], max(3, args.steps // 2), 2, ws)
+            e = {"ms_per_step": ems, "config": r["config"], "cells_per_s": r["cells"] / (ems * 1e-3),
+                 "n_gpus": ws, "scaling": "strong"}
+            del r
+            torch.cuda.empty_cache()
+        except Exception as ex:
+            e = {"error": repr(ex)}
+        if rank == 0:
+            line.setdefault("workloads", {})["C5_map"] = e
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
