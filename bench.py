@@ -386,15 +386,20 @@ def wl_map(args, ws, rank, c5=False):
     out = torch.empty((rows, M), dtype=cdt, device="cuda")
     ws_buf = torch.empty(rows * M * out.element_size(), dtype=torch.uint8, device="cuda")
 
-    pm = None
+    pm, transport = None, "p2p"
     if ws > 1:  # rank 0's map, IPC-shared once: every rank's kernels store their rows into it
-        from paper_1402_0532_b200.sharded import PeerMap
-        pm = PeerMap(L, M, cdt)
+        from paper_1402_0532_b200.sharded import PeerMap, PeerMapUnavailable
+        try:
+            pm = PeerMap(L, M, cdt)
+        except PeerMapUnavailable:  # (all ranks agree) NCCL gather instead
+            transport = "gather"
+    full = torch.empty((L, M), dtype=cdt, device="cuda") if (ws > 1 and rank == 0 and pm is None) else None
 
     def step():
         if ws > 1:  # delay-bin shard, rows stored straight into rank 0's map (NVLink), one barrier
             from paper_1402_0532_b200.sharded import ambiguity_map_sharded
-            ambiguity_map_sharded(surv, ref, L, M, peer_map=pm, workspace=ws_buf)
+            ambiguity_map_sharded(surv, ref, L, M, peer_map=pm, transport=transport, out_full=full,
+                                  out_local=out, workspace=ws_buf)
         else:
             sa.ambiguity_map(surv, ref, rows, M, l0=l0, out=out, workspace=ws_buf)
 
@@ -412,8 +417,8 @@ def wl_map(args, ws, rank, c5=False):
                       + ("4" if c5 else "3") + "])", "ns": ns, "delay_bins": L, "doppler_bins": M,
                       "block_T": ns // M, "doppler": "NL-FFT DIT", "dtype": str(cdt).replace("torch.", ""),
                       "parallelism": f"delay-bin shards x{ws}" + (
-                          ", rows stored by the transform kernels into rank 0's IPC-shared map over NVLink, "
-                          "one barrier" if ws > 1 else "")}}
+                          (", rows stored by the transform kernels into rank 0's IPC-shared map over NVLink, "
+                           "one barrier" if transport == "p2p" else ", NCCL gather to rank 0") if ws > 1 else "")}}
     return res
 
 

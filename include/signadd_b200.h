@@ -179,6 +179,13 @@ int sa_map_floor(int dtype, const void *map, int64_t rows, int64_t cols, const i
  * root's map (an IPC mapping of it) instead of gathering afterwards. */
 int sa_enable_peer_access(int peer_device);
 
+/* Open a peer process's device allocation (64-byte cudaIpcMemHandle_t, e.g.
+ * from torch's storage export) in the CURRENT device's context, with lazy
+ * peer access, so this device's kernels can store into it directly; close it
+ * with sa_ipc_close.  The sharded map opens the root's map this way. */
+int sa_ipc_open(const void *handle64, void **dptr);
+int sa_ipc_close(void *dptr);
+
 /* FMA-pipe peak microbenchmark (roofline denominator): `blocks` CTAs x 256
  * (dtype 2 = packed fp32x2 FFMA2)
  * threads each run `iters` iterations of 8 independent FMA chains; writes a

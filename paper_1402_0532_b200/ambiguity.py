@@ -170,13 +170,16 @@ def _lag_product(s_surv, s_ref, l, n, conjugate_ref, entry):
 
 def ambiguity_map(s_surv, s_ref, l_bins: int, m: int, *, l0: int = 0, gain: float = 1.0,
                   conjugate_ref: bool = True, doppler: str = "nfft", mode: str = "fast",
-                  lag: str = "mf", out=None, workspace=None, dtype=None):
+                  lag: str = "mf", out=None, workspace=None, dtype=None, out_ptr: int | None = None):
     """Rows l0..l0+l_bins-1 of the block-integrated range-Doppler map.
 
     Inputs: CUDA tensors (stay on device, no sync) or host arrays (result
     returned on the host).  Ns = len(s_surv); T = Ns / m must be an integer.
     lag: "mf" (⊙, eq12a/eq12b) or "exact" (numpy multiply, eq11/eq12c);
     doppler: "nfft", "ndft" or "fft" (fft_exact).
+    ``out_ptr``: raw device address of an (l_bins x m) row-major destination
+    (e.g. an IPC mapping of another GPU's map, sharded.PeerMap) -- the
+    transform kernel stores there directly and the call returns None.
     """
     T = torch()
     surv = _samples(s_surv)
@@ -195,7 +198,7 @@ def ambiguity_map(s_surv, s_ref, l_bins: int, m: int, *, l0: int = 0, gain: floa
     for l in (l0, l0 + l_bins - 1):
         _lag_guards(ns, dr.numel(), l, ns)
     d = sa_dtype_of(ds)
-    if out is None:
+    if out is None and out_ptr is None:
         out = T.empty((l_bins, m), dtype=ds.dtype, device=ds.device)
     need = ctypes.c_int64()
     _native.check(_native.lib().sa_ambiguity_workspace_bytes(d, l_bins, m, ctypes.byref(need)))
@@ -211,8 +214,11 @@ def ambiguity_map(s_surv, s_ref, l_bins: int, m: int, *, l0: int = 0, gain: floa
     tw = device_twiddles(m, d, ds.device.index)
     _native.check(_native.lib().sa_ambiguity_map_v(
         d, lk, _native.ptr(ds), _native.ptr(dr), ns, dr.numel(), l0, l_bins, m, float(gain),
-        int(conjugate_ref), dop, md, ctypes.c_void_p(tw), _native.ptr(out), _native.ptr(workspace),
+        int(conjugate_ref), dop, md, ctypes.c_void_p(tw),
+        ctypes.c_void_p(out_ptr) if out_ptr is not None else _native.ptr(out), _native.ptr(workspace),
         workspace.numel() * workspace.element_size(), _native.stream_ptr()))
+    if out_ptr is not None:
+        return None
     return out if device_io else out.cpu().numpy()
 
 

@@ -9,6 +9,8 @@
 #include <mutex>
 
 #include "sa_common.cuh"
+#include <cstring>
+
 #include "sa_internal.h"
 
 static thread_local char g_err[512] = "";
@@ -283,6 +285,20 @@ int sa_enable_peer_access(int peer_device) {
     return SA_OK;
   }
   SA_CUDA_TRY(e);
+  return SA_OK;
+}
+
+int sa_ipc_open(const void *handle64, void **dptr) {
+  SA_REQUIRE(handle64 && dptr, SA_ERR_ARG, "null pointer");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  SA_CUDA_TRY(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return SA_OK;
+}
+
+int sa_ipc_close(void *dptr) {
+  SA_REQUIRE(dptr, SA_ERR_ARG, "null pointer");
+  SA_CUDA_TRY(cudaIpcCloseMemHandle(dptr));
   return SA_OK;
 }
 

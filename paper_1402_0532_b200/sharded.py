@@ -10,7 +10,8 @@ Two transports:
   * "p2p" (default): compute and collective fused.  The root's map is shared
     once by CUDA IPC (``PeerMap``); every rank's Doppler-transform kernel
     stores its rows straight into it over NVLink/NVSwitch, so there is no
-    separate gather -- a host barrier after the kernels is the only exchange.
+    separate gather -- a 1-element, stream-ordered NCCL all-reduce after the
+    kernels is the only exchange (gloo groups: a host barrier).
   * "gather": the rows land locally and ``dist.gather`` (NCCL) moves them.
 
 The host logic (partition, gather layout) is backend-agnostic and covered with
@@ -19,6 +20,8 @@ NVLink/NVSwitch.
 """
 
 from __future__ import annotations
+
+import ctypes
 
 
 def shard_rows(l_bins: int, world: int, rank: int) -> tuple[int, int]:
@@ -68,35 +71,93 @@ def gather_rows(local, full, l_bins: int, group=None, dst: int = 0):
     return None
 
 
+class PeerMapUnavailable(RuntimeError):
+    """CUDA IPC mapping of the root's map is not possible on this system."""
+
+
 class PeerMap:
-    """The root's (L x M) map, visible to every rank: the root allocates it and
-    shares it once through CUDA IPC (torch's own tensor reduction); the other
-    ranks open it and enable peer access from their device, so their kernels
-    can store rows into it directly.  Collective to construct."""
+    """The root's (L x M) map, writable by every rank's kernels.
+
+    The root allocates it and exports its CUDA IPC handle (torch's storage
+    export: handle + offset); every other rank opens the handle in its OWN
+    device's context with lazy peer access (``sa_ipc_open``), so kernels on that
+    device store rows straight into the root's memory over NVLink/NVSwitch.
+    Collective to construct and to ``close``."""
 
     def __init__(self, l_bins: int, m: int, dtype, group=None, dst: int = 0):
         import torch
         import torch.distributed as dist
-        from torch.multiprocessing.reductions import reduce_tensor
         from . import _native
-        self.l_bins, self.m, self.dst = l_bins, m, dst
+        self.l_bins, self.m, self.dst, self.group = l_bins, m, dst, group
         self.rank = dist.get_rank(group)
         self.full = None
+        self._mapped = None
         payload = [None]
+        world = dist.get_world_size(group)
         if self.rank == dst:
             self.full = torch.empty((l_bins, m), dtype=dtype, device="cuda")
-            payload = [reduce_tensor(self.full)]
-        dist.broadcast_object_list(payload, src=dst, group=group)
+        if self.rank == dst and world > 1:
+            try:
+                payload = [self._export()]
+            except Exception:  # every rank still reaches the broadcast below
+                payload = [None]
+        ok = True
+        if world > 1:
+            dist.broadcast_object_list(payload, src=dst, group=group)
+            ok = payload[0] is not None
+        self.row_bytes = m * torch.empty((), dtype=dtype).element_size()
         if self.rank == dst:
-            self.view = self.full
-        else:
-            fn, args = payload[0]
-            self.view = fn(*args)  # IPC mapping of the root's map
-            _native.check(_native.lib().sa_enable_peer_access(self.view.device.index))
+            self.base = self.full.data_ptr()
+        elif ok:
+            handle, offset = payload[0]
+            hbuf = ctypes.create_string_buffer(handle, len(handle))
+            p = ctypes.c_void_p()
+            ok = _native.lib().sa_ipc_open(hbuf, ctypes.byref(p)) == 0
+            if ok:
+                self._mapped = p
+                self.base = p.value + offset
+        if world > 1:  # all ranks agree, so a failure cannot strand a peer in a collective
+            flag = torch.tensor([1 if ok else 0], dtype=torch.int32,
+                                device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+            if int(flag.item()) == 0:
+                if self._mapped is not None:
+                    _native.lib().sa_ipc_close(self._mapped)
+                    self._mapped = None
+                raise PeerMapUnavailable("CUDA IPC mapping of the root's map failed on some rank")
 
-    def rows(self, first: int, count: int):
-        """The root's rows [first, first + count) as seen from this rank."""
-        return self.view[first:first + count]
+    def _export(self):
+        """(64-byte IPC handle, byte offset of the map in its allocation)."""
+        info = self.full.untyped_storage()._share_cuda_()
+        handle, storage_offset = bytes(info[1]), int(info[3])
+        # torch's caching allocator exports [version byte,] a type byte ('c' =
+        # cudaMalloc segment) and the 64-byte cudaIpcMemHandle_t; expandable
+        # segments use another format
+        if len(handle) >= 65 and handle[-65:-64] == b"c":
+            handle = handle[-64:]
+        if len(handle) != 64:
+            raise RuntimeError("PeerMap needs a cudaMalloc-backed map (set "
+                               "PYTORCH_CUDA_ALLOC_CONF=expandable_segments:False)")
+        return (handle, storage_offset + self.full.storage_offset() * self.full.element_size())
+
+    def done_flag(self):
+        """A 1-element device tensor for the completion all-reduce."""
+        import torch
+        if getattr(self, "_flag", None) is None:
+            self._flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+        return self._flag
+
+    def rows_ptr(self, first: int) -> int:
+        """Device address (valid on this rank's GPU) of the root's row ``first``."""
+        return self.base + first * self.row_bytes
+
+    def close(self) -> None:
+        import torch.distributed as dist
+        from . import _native
+        dist.barrier(group=self.group)  # nobody still writes
+        if self._mapped is not None:
+            _native.check(_native.lib().sa_ipc_close(self._mapped))
+            self._mapped = None
 
 
 def ambiguity_map_sharded(surv, ref, l_bins: int, m: int, *, gain: float = 1.0,
@@ -116,13 +177,24 @@ def ambiguity_map_sharded(surv, ref, l_bins: int, m: int, *, gain: float = 1.0,
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     first, count = shard_rows(l_bins, world, rank)
+    if transport == "p2p" and peer_map is None:
+        try:
+            peer_map = PeerMap(l_bins, m, surv.dtype, group=group, dst=dst)
+        except PeerMapUnavailable:
+            transport = "gather"
     if transport == "p2p":
-        pm = peer_map if peer_map is not None else PeerMap(l_bins, m, surv.dtype, group=group, dst=dst)
+        pm = peer_map
         if count:
             ambiguity_map(surv, ref, count, m, l0=first, gain=gain, conjugate_ref=conjugate_ref,
-                          doppler=doppler, mode=mode, lag=lag, out=pm.rows(first, count), workspace=workspace)
-        torch.cuda.current_stream().synchronize()  # this rank's rows are in the root's memory
-        dist.barrier(group=group)                  # ... and so are everyone's
+                          doppler=doppler, mode=mode, lag=lag, out_ptr=pm.rows_ptr(first), workspace=workspace)
+        if dist.get_backend(group) == "nccl":
+            # stream-ordered: NCCL's stream waits for this rank's transform kernel,
+            # the caller's stream waits for the all-reduce -- once it completes on
+            # the root, every rank's row stores into its map are done (no host sync)
+            dist.all_reduce(pm.done_flag(), group=group)
+        else:
+            torch.cuda.current_stream().synchronize()  # this rank's rows are in the root's memory
+            dist.barrier(group=group)                  # ... and so are everyone's
         return pm.full if rank == dst else None
     if transport != "gather":
         raise ValueError(f"unknown transport {transport!r}")

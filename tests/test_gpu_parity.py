@@ -494,7 +494,7 @@ def _p2p_worker(rank, port, q):
             full = ambiguity_map_sharded(ds, dr, 101, 128, peer_map=pm)
         if rank == 0:
             q.put(bool(torch.equal(full, sa.ambiguity_map(ds, dr, 101, 128))))
-        dist.barrier()
+        pm.close()
     finally:
         dist.destroy_process_group()
 
