@@ -14,7 +14,8 @@
 // strongest are returned strongest first, equal magnitudes in row-major order
 // (the stable argsort of detection.py:106).
 //   k_peaks_tile: one CTA per 32x64 tile, magnitudes + halo in smem, strict
-//     maxima compacted in smem; each candidate's rank in the tile is the number
+//     maxima; for k <= 32 each warp first extracts its own top k from registers
+//     (k rounds of a warp argmax); a candidate's rank in the tile is the number
 //     of better candidates, and the top k land sorted in the tile's list;
 //   k_peaks_select: one CTA, k rounds of a block-wide argmax over the heads of
 //     the tile lists (heads cached in registers, only the winner advances).
@@ -40,6 +41,7 @@ constexpr int TILE = 32;    // tile rows
 constexpr int TILE_W = 64;  // tile columns
 constexpr int TILE_THREADS = 256;
 constexpr int MAX_CAND = TILE * TILE_W / 4;  // strict maxima are never 8-adjacent: <= 1 per 2x2
+constexpr int WARP_K = 32;  // k <= WARP_K: per-warp selection before the tile rank
 constexpr int MERGE_THREADS = 512;
 
 SA_HD Cand sentinel() { return {-1.0, LLONG_MAX}; }
@@ -76,10 +78,11 @@ __global__ void __launch_bounds__(TILE_THREADS) k_peaks_tile(const C2<T> *__rest
     mag[lr][lc] = v;
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < TILE * TILE_W; e += blockDim.x) {
+  Cand *o = out + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * k;
+  auto strict_at = [&](int e, Cand &cd) {  // tile cell e -> is it a strict maximum?
     const int lr = e / TILE_W + 1, lc = e % TILE_W + 1;
     const int64_t r = r0 + lr - 1, c = c0 + lc - 1;
-    if (r >= rows || c >= cols) continue;
+    if (r >= rows || c >= cols) return false;
     const T m = mag[lr][lc];
     bool strict = true;
 #pragma unroll
@@ -87,12 +90,75 @@ __global__ void __launch_bounds__(TILE_THREADS) k_peaks_tile(const C2<T> *__rest
 #pragma unroll
       for (int dp = -1; dp <= 1; ++dp)
         if (dl != 0 || dp != 0) strict &= m > mag[lr + dl][lc + dp];
-    if (strict) cand[atomicAdd(&cnt, 1)] = {(double)m, (long long)(r * cols + c)};
+    cd = {(double)m, (long long)(r * cols + c)};
+    return strict;
+  };
+  if (k <= WARP_K) {
+    // Small k: each warp keeps the strict maxima of its 256 cells in registers
+    // (8 per lane), extracts its own top k by k rounds of a warp argmax, and the
+    // tile ranks only those <= 8k warp winners.
+    constexpr int PER_LANE = TILE * TILE_W / TILE_THREADS;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    Cand mine[PER_LANE];
+#pragma unroll
+    for (int j = 0; j < PER_LANE; ++j) {
+      Cand cd;
+      if (!strict_at(warp * 32 * PER_LANE + lane + 32 * j, cd)) cd = sentinel();
+      mine[j] = cd;
+    }
+    Cand *wl = cand + warp * WARP_K;  // this warp's winners, best first
+    int got = 0;
+    for (int rd = 0; rd < k; ++rd) {
+      Cand b = sentinel();
+#pragma unroll
+      for (int j = 0; j < PER_LANE; ++j)
+        if (better(mine[j], b)) b = mine[j];
+      for (int sh = 16; sh > 0; sh >>= 1) {
+        Cand x;
+        x.mag = __shfl_xor_sync(0xffffffffu, b.mag, sh);
+        x.idx = __shfl_xor_sync(0xffffffffu, b.idx, sh);
+        if (better(x, b)) b = x;
+      }
+      if (b.mag < 0.0) break;  // warp exhausted (uniform)
+      if (lane == 0) wl[rd] = b;
+      ++got;
+#pragma unroll
+      for (int j = 0; j < PER_LANE; ++j)
+        if (mine[j].idx == b.idx) mine[j] = sentinel();
+    }
+    for (int rd = got + lane; rd < k; rd += 32) wl[rd] = sentinel();
+    __syncthreads();
+    if (warp == 0) {  // k-way merge of the 8 sorted warp lists: lane w holds list w's head
+      constexpr int NW = TILE_THREADS / 32;
+      int pos = 0;
+      Cand h = lane < NW ? cand[lane * WARP_K] : sentinel();
+      int rd = 0;
+      for (; rd < k; ++rd) {
+        Cand b = h;
+        for (int sh = 16; sh > 0; sh >>= 1) {
+          Cand x;
+          x.mag = __shfl_xor_sync(0xffffffffu, b.mag, sh);
+          x.idx = __shfl_xor_sync(0xffffffffu, b.idx, sh);
+          if (better(x, b)) b = x;
+        }
+        if (b.mag < 0.0) break;
+        if (lane == 0) o[rd] = b;
+        if (lane < NW && h.idx == b.idx && h.mag >= 0.0) {
+          ++pos;
+          h = pos < k ? cand[lane * WARP_K + pos] : sentinel();
+        }
+      }
+      for (int e = rd + lane; e < k; e += 32) o[e] = sentinel();
+    }
+    return;
+  }
+  for (int e = threadIdx.x; e < TILE * TILE_W; e += blockDim.x) {
+    Cand cd;
+    if (strict_at(e, cd)) cand[atomicAdd(&cnt, 1)] = cd;
   }
   __syncthreads();
   // the tile's top k by rank counting: a candidate's rank = number of better
   // candidates (a total order, so ranks are distinct); slot rank holds it
-  Cand *o = out + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * k;
   const int n = cnt;
   for (int e = threadIdx.x; e < n; e += blockDim.x) {
     const Cand me = cand[e];
