@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(256) k_lag_integrate_exact(
   z[id] = {sr, si};
 }
 
-template <typename T>
+template <typename T, bool EXACT>
 __global__ void __launch_bounds__(256) k_lag_integrate_fast(
     const C2<T> *__restrict__ surv, const C2<T> *__restrict__ ref, int64_t ref_len, int64_t l0,
     int64_t l_count, int64_t m, int tb, bool conj, C2<T> *__restrict__ z) {
@@ -163,6 +163,19 @@ __global__ void __launch_bounds__(256) k_lag_integrate_fast(
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const C4<T> &s = a[i];  // {sr, si, sgn sr, sgn si}; reference c[i-j+7] = {cr, ci, sgn cr, sgn ci}
+      if constexpr (EXACT) {  // s * c: Re += sr*cr - si*ci ; Im += sr*ci + si*cr (4 FMA)
+#pragma unroll
+        for (int j = 0; j < LAGS_PER_WARP; ++j) {
+          accr[j] = sa_fma(s.x, c[i - j + 7].x, accr[j]);
+          acci[j] = sa_fma(s.x, c[i - j + 7].y, acci[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < LAGS_PER_WARP; ++j) {
+          accr[j] = sa_fma(-s.y, c[i - j + 7].y, accr[j]);
+          acci[j] = sa_fma(s.y, c[i - j + 7].x, acci[j]);
+        }
+        continue;
+      }
 #pragma unroll
       for (int j = 0; j < LAGS_PER_WARP; ++j) {
         accr[j] = sa_fma(s.x, c[i - j + 7].z, accr[j]);
@@ -209,6 +222,7 @@ __global__ void __launch_bounds__(256) k_lag_integrate_fast(
 // complex64, T % 16 == 0: entry e of S holds samples e and e + T/2, entry u of
 // C window slots u and u + T/2, each as {x, x'}, {y, y'} (S0/C0) and the signs
 // {sx, sx'}, {sy, sy'} (S1/C1), in pad8-strided float4 arrays.
+template <bool EXACT>
 __global__ void __launch_bounds__(256, 2) k_lag_integrate_f32x2(
     const float2 *__restrict__ surv, const float2 *__restrict__ ref, int64_t ref_len, int64_t l0,
     int64_t l_count, int64_t m, int tb, bool conj, float2 *__restrict__ z) {
@@ -284,16 +298,31 @@ __global__ void __launch_bounds__(256, 2) k_lag_integrate_f32x2(
     V cx[15], cy[15], cz[15], cw[15];  // window pairs {re}, {im}, {sgn re}, {sgn im}
 #pragma unroll
     for (int u = 0; u < 15; ++u) {
-      const float4 c0 = C0[pad8(base + u)], c1 = C1[pad8(base + u)];
+      const float4 c0 = C0[pad8(base + u)];
       cx[u] = A::pack(c0.x, c0.y);
       cy[u] = A::pack(c0.z, c0.w);
-      cz[u] = A::pack(c1.x, c1.y);
-      cw[u] = A::pack(c1.z, c1.w);
+      if (!EXACT) {
+        const float4 c1 = C1[pad8(base + u)];
+        cz[u] = A::pack(c1.x, c1.y);
+        cw[u] = A::pack(c1.z, c1.w);
+      }
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const float4 s0 = S0[pad8(t0 + i)], s1 = S1[pad8(t0 + i)];
+      const float4 s0 = S0[pad8(t0 + i)];
       const V sx = A::pack(s0.x, s0.y), sy = A::pack(s0.z, s0.w);
+      if constexpr (EXACT) {  // s * c: Re += sx*cx - sy*cy ; Im += sx*cy + sy*cx (4 FFMA2 per lag)
+#pragma unroll
+        for (int j = 0; j < LAGS_PER_WARP; ++j) accr[j] = A::fma(sx, cx[i - j + 7], accr[j]);
+#pragma unroll
+        for (int j = 0; j < LAGS_PER_WARP; ++j) acci[j] = A::fma(sx, cy[i - j + 7], acci[j]);
+#pragma unroll
+        for (int j = 0; j < LAGS_PER_WARP; ++j) accr[j] = A::fma(A::neg(sy), cy[i - j + 7], accr[j]);
+#pragma unroll
+        for (int j = 0; j < LAGS_PER_WARP; ++j) acci[j] = A::fma(sy, cx[i - j + 7], acci[j]);
+        continue;
+      }
+      const float4 s1 = S1[pad8(t0 + i)];
       const V sz = A::pack(s1.x, s1.y), sw = A::pack(s1.z, s1.w);
       // consecutive FFMA2 share the surveillance pair; per lag the terms add as
       //   Re: sx*cz, sz*cx, -sy*cw, -sw*cy ;  Im: sy*cz, sw*cx, sz*cy, sx*cw
@@ -350,9 +379,8 @@ int launch_integrate(int lag_kind, const void *survv, const void *refv, int64_t 
   C2<T> *z = (C2<T> *)zv;
   const int64_t tb = ns / m;
   if (l_count == 0 || m == 0) return SA_OK;
-  // the exact-multiply lag product always takes the sequential kernel
-  const bool fast = lag_kind == SA_LAG_MF && mode == SA_NDFT_FAST && tb % 8 == 0 && tb <= 8192 &&
-                    m <= 0x7fffffff;
+  const bool exact_lag = lag_kind == SA_LAG_EXACT;
+  const bool fast = mode == SA_NDFT_FAST && tb % 8 == 0 && tb <= 8192 && m <= 0x7fffffff;
   if (!fast) {
     int64_t tot = l_count * m;
     auto kern = lag_kind == SA_LAG_EXACT ? k_lag_integrate_exact<T, true> : k_lag_integrate_exact<T, false>;
@@ -364,12 +392,12 @@ int launch_integrate(int lag_kind, const void *survv, const void *refv, int64_t 
   if (sizeof(T) == 4 && tb % 16 == 0) {
     const int h = (int)tb / 2, hw = h + LAGS_PER_CTA - 1;
     size_t bytes = 2 * sizeof(float4) * ((size_t)pad8(h) + 1 + pad8(hw) + 1);
-    SA_CUDA_TRY(cudaFuncSetAttribute(k_lag_integrate_f32x2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)bytes));
+    auto k2 = exact_lag ? k_lag_integrate_f32x2<true> : k_lag_integrate_f32x2<false>;
+    SA_CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     for (int64_t t0 = 0; t0 < ltiles; t0 += 65535) {
       int64_t nt = std::min<int64_t>(65535, ltiles - t0);
       dim3 grid((unsigned)m, (unsigned)nt);
-      k_lag_integrate_f32x2<<<grid, 256, bytes, s>>>(
+      k2<<<grid, 256, bytes, s>>>(
           (const float2 *)surv, (const float2 *)ref, ref_len, l0 + t0 * LAGS_PER_CTA,
           l_count - t0 * LAGS_PER_CTA, m, (int)tb, conj != 0, (float2 *)(z + t0 * LAGS_PER_CTA * m));
     }
@@ -378,7 +406,7 @@ int launch_integrate(int lag_kind, const void *survv, const void *refv, int64_t 
   }
   const int win = (int)tb + LAGS_PER_CTA - 1;
   size_t bytes = sizeof(C4<T>) * ((size_t)pad8((int)tb) + 1 + pad8(win) + 1);
-  auto kern = k_lag_integrate_fast<T>;
+  auto kern = exact_lag ? k_lag_integrate_fast<T, true> : k_lag_integrate_fast<T, false>;
   SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   for (int64_t t0 = 0; t0 < ltiles; t0 += 65535) {
     int64_t nt = std::min<int64_t>(65535, ltiles - t0);
