@@ -40,15 +40,20 @@ template <> struct NdftCfg<float> {
   static constexpr int TB = 4;  // vectors per lane
   static constexpr int TK = 8;  // bins per thread
 };
+#ifndef SA_D_TB  // fp64 tile (vectors per lane, bins per thread, min CTAs/SM); -D for sweeps
+#define SA_D_TB 4
+#define SA_D_TK 4
+#define SA_D_MINB 1
+#endif
 template <> struct NdftCfg<double> {
-  static constexpr int TB = 2;
-  static constexpr int TK = 8;
+  static constexpr int TB = SA_D_TB;
+  static constexpr int TK = SA_D_TK;
 };
 
 SA_HD int swz(int mm, int vv) { return vv ^ ((mm >> 1) & 7); }
 
 template <typename T, bool POW2, bool TW_SMEM>
-__global__ void __launch_bounds__(NDFT_THREADS)
+__global__ void __launch_bounds__(NDFT_THREADS, sizeof(T) == 8 ? SA_D_MINB : 1)
     k_ndft_fast(const C2<T> *__restrict__ x, C2<T> *__restrict__ y, int64_t batch, int n,
                 const C4<T> *__restrict__ quad, T gain, bool use_gain) {
   constexpr int TB = NdftCfg<T>::TB, TK = NdftCfg<T>::TK;
