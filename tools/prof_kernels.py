@@ -25,5 +25,10 @@ elif what == "map":
     r = torch.from_numpy(sc.ref).to(dt).cuda()
     for _ in range(reps):
         sa.ambiguity_map(s, r, 1024, 512)
+elif what == "detect":
+    g = torch.Generator(device="cuda").manual_seed(1)
+    m = torch.randn(4096, 2048, dtype=dt, device="cuda", generator=g)
+    for _ in range(reps):
+        sa.map_peaks(m, 8)
 torch.cuda.synchronize()
 print("ok", what)
