@@ -222,24 +222,32 @@ __global__ void __launch_bounds__(256) k_lag_integrate_fast(
 // complex64, T % 16 == 0: entry e of S holds samples e and e + T/2, entry u of
 // C window slots u and u + T/2, each as {x, x'}, {y, y'} (S0/C0) and the signs
 // {sx, sx'}, {sy, sy'} (S1/C1), in pad8-strided float4 arrays.
+#ifndef SA_LAG2_LPW  // packed kernel: lags per warp, min CTAs per SM (-D for sweeps)
+#define SA_LAG2_LPW 8
+#define SA_LAG2_MINB 2
+#endif
+constexpr int L2_LPW = SA_LAG2_LPW;
+constexpr int L2_LPC = LAG_WARPS * L2_LPW;  // lags per CTA
+constexpr int L2_WIN = 8 + L2_LPW - 1;      // window pairs per 8-sample sub-block
+
 template <bool EXACT>
-__global__ void __launch_bounds__(256, 2) k_lag_integrate_f32x2(
+__global__ void __launch_bounds__(256, SA_LAG2_MINB) k_lag_integrate_f32x2(
     const float2 *__restrict__ surv, const float2 *__restrict__ ref, int64_t ref_len, int64_t l0,
     int64_t l_count, int64_t m, int tb, bool conj, float2 *__restrict__ z) {
   using A = Ar<float>;
   using V = A::V;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int h = tb >> 1;
-  const int hw = h + LAGS_PER_CTA - 1;  // window pair entries
+  const int hw = h + L2_LPC - 1;  // window pair entries
   float4 *S0 = reinterpret_cast<float4 *>(smem_raw);
   float4 *S1 = S0 + pad8(h) + 1;
   float4 *C0 = S1 + pad8(h) + 1;
   float4 *C1 = C0 + pad8(hw) + 1;
 
   const int64_t q = blockIdx.x;
-  const int64_t lt = l0 + (int64_t)blockIdx.y * LAGS_PER_CTA;
+  const int64_t lt = l0 + (int64_t)blockIdx.y * L2_LPC;
   const int64_t i0 = q * tb;
-  const int64_t ws = i0 - lt - (LAGS_PER_CTA - 1);
+  const int64_t ws = i0 - lt - (L2_LPC - 1);
 
   constexpr int PF = 4;
   for (int e0 = threadIdx.x; e0 < h; e0 += PF * blockDim.x) {
@@ -284,20 +292,20 @@ __global__ void __launch_bounds__(256, 2) k_lag_integrate_f32x2(
   __syncthreads();
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t lw = lt + warp * LAGS_PER_WARP;
+  const int64_t lw = lt + warp * L2_LPW;
   if (lw - l0 >= l_count) return;
 
-  V accr[LAGS_PER_WARP], acci[LAGS_PER_WARP];
+  V accr[L2_LPW], acci[L2_LPW];
 #pragma unroll
-  for (int j = 0; j < LAGS_PER_WARP; ++j) accr[j] = acci[j] = 0ull;
+  for (int j = 0; j < L2_LPW; ++j) accr[j] = acci[j] = 0ull;
 
   const int nsb = h >> 3;
   for (int sb = lane; sb < nsb; sb += 32) {
     const int t0 = sb * 8;
-    const int base = t0 + (LAGS_PER_CTA - 1) - LAGS_PER_WARP * warp - (LAGS_PER_WARP - 1);
-    V cx[15], cy[15], cz[15], cw[15];  // window pairs {re}, {im}, {sgn re}, {sgn im}
+    const int base = t0 + (L2_LPC - 1) - L2_LPW * warp - (L2_LPW - 1);
+    V cx[L2_WIN], cy[L2_WIN], cz[L2_WIN], cw[L2_WIN];  // window pairs {re}, {im}, {sgn re}, {sgn im}
 #pragma unroll
-    for (int u = 0; u < 15; ++u) {
+    for (int u = 0; u < L2_WIN; ++u) {
       const float4 c0 = C0[pad8(base + u)];
       cx[u] = A::pack(c0.x, c0.y);
       cy[u] = A::pack(c0.z, c0.w);
@@ -313,13 +321,13 @@ __global__ void __launch_bounds__(256, 2) k_lag_integrate_f32x2(
       const V sx = A::pack(s0.x, s0.y), sy = A::pack(s0.z, s0.w);
       if constexpr (EXACT) {  // s * c: Re += sx*cx - sy*cy ; Im += sx*cy + sy*cx (4 FFMA2 per lag)
 #pragma unroll
-        for (int j = 0; j < LAGS_PER_WARP; ++j) accr[j] = A::fma(sx, cx[i - j + 7], accr[j]);
+        for (int j = 0; j < L2_LPW; ++j) accr[j] = A::fma(sx, cx[i - j + L2_LPW - 1], accr[j]);
 #pragma unroll
-        for (int j = 0; j < LAGS_PER_WARP; ++j) acci[j] = A::fma(sx, cy[i - j + 7], acci[j]);
+        for (int j = 0; j < L2_LPW; ++j) acci[j] = A::fma(sx, cy[i - j + L2_LPW - 1], acci[j]);
 #pragma unroll
-        for (int j = 0; j < LAGS_PER_WARP; ++j) accr[j] = A::fma(A::neg(sy), cy[i - j + 7], accr[j]);
+        for (int j = 0; j < L2_LPW; ++j) accr[j] = A::fma(A::neg(sy), cy[i - j + L2_LPW - 1], accr[j]);
 #pragma unroll
-        for (int j = 0; j < LAGS_PER_WARP; ++j) acci[j] = A::fma(sy, cx[i - j + 7], acci[j]);
+        for (int j = 0; j < L2_LPW; ++j) acci[j] = A::fma(sy, cx[i - j + L2_LPW - 1], acci[j]);
         continue;
       }
       const float4 s1 = S1[pad8(t0 + i)];
@@ -327,26 +335,26 @@ __global__ void __launch_bounds__(256, 2) k_lag_integrate_f32x2(
       // consecutive FFMA2 share the surveillance pair; per lag the terms add as
       //   Re: sx*cz, sz*cx, -sy*cw, -sw*cy ;  Im: sy*cz, sw*cx, sz*cy, sx*cw
 #pragma unroll
-      for (int j = 0; j < LAGS_PER_WARP; ++j) accr[j] = A::fma(sx, cz[i - j + 7], accr[j]);
+      for (int j = 0; j < L2_LPW; ++j) accr[j] = A::fma(sx, cz[i - j + L2_LPW - 1], accr[j]);
 #pragma unroll
-      for (int j = 0; j < LAGS_PER_WARP; ++j) acci[j] = A::fma(sy, cz[i - j + 7], acci[j]);
+      for (int j = 0; j < L2_LPW; ++j) acci[j] = A::fma(sy, cz[i - j + L2_LPW - 1], acci[j]);
 #pragma unroll
-      for (int j = 0; j < LAGS_PER_WARP; ++j) accr[j] = A::fma(sz, cx[i - j + 7], accr[j]);
+      for (int j = 0; j < L2_LPW; ++j) accr[j] = A::fma(sz, cx[i - j + L2_LPW - 1], accr[j]);
 #pragma unroll
-      for (int j = 0; j < LAGS_PER_WARP; ++j) acci[j] = A::fma(sw, cx[i - j + 7], acci[j]);
+      for (int j = 0; j < L2_LPW; ++j) acci[j] = A::fma(sw, cx[i - j + L2_LPW - 1], acci[j]);
 #pragma unroll
-      for (int j = 0; j < LAGS_PER_WARP; ++j) accr[j] = A::fma(A::neg(sy), cw[i - j + 7], accr[j]);
+      for (int j = 0; j < L2_LPW; ++j) accr[j] = A::fma(A::neg(sy), cw[i - j + L2_LPW - 1], accr[j]);
 #pragma unroll
-      for (int j = 0; j < LAGS_PER_WARP; ++j) acci[j] = A::fma(sz, cy[i - j + 7], acci[j]);
+      for (int j = 0; j < L2_LPW; ++j) acci[j] = A::fma(sz, cy[i - j + L2_LPW - 1], acci[j]);
 #pragma unroll
-      for (int j = 0; j < LAGS_PER_WARP; ++j) accr[j] = A::fma(A::neg(sw), cy[i - j + 7], accr[j]);
+      for (int j = 0; j < L2_LPW; ++j) accr[j] = A::fma(A::neg(sw), cy[i - j + L2_LPW - 1], accr[j]);
 #pragma unroll
-      for (int j = 0; j < LAGS_PER_WARP; ++j) acci[j] = A::fma(sx, cw[i - j + 7], acci[j]);
+      for (int j = 0; j < L2_LPW; ++j) acci[j] = A::fma(sx, cw[i - j + L2_LPW - 1], acci[j]);
     }
   }
-  float vr[LAGS_PER_WARP], vi[LAGS_PER_WARP];
+  float vr[L2_LPW], vi[L2_LPW];
 #pragma unroll
-  for (int j = 0; j < LAGS_PER_WARP; ++j) {
+  for (int j = 0; j < L2_LPW; ++j) {
     float a, b;
     A::unpack(accr[j], a, b);
     vr[j] = sa_add(a, b);
@@ -358,10 +366,10 @@ __global__ void __launch_bounds__(256, 2) k_lag_integrate_f32x2(
       vi[j] = sa_add(vi[j], __shfl_xor_sync(0xffffffffu, vi[j], o));
     }
   }
-  if (lane < LAGS_PER_WARP) {
+  if (lane < L2_LPW) {
     float r = vr[0], i = vi[0];
 #pragma unroll
-    for (int j = 1; j < LAGS_PER_WARP; ++j)
+    for (int j = 1; j < L2_LPW; ++j)
       if (lane == j) {
         r = vr[j];
         i = vi[j];
@@ -390,7 +398,8 @@ int launch_integrate(int lag_kind, const void *survv, const void *refv, int64_t 
   }
   int64_t ltiles = (l_count + LAGS_PER_CTA - 1) / LAGS_PER_CTA;
   if (sizeof(T) == 4 && tb % 16 == 0) {
-    const int h = (int)tb / 2, hw = h + LAGS_PER_CTA - 1;
+    const int h = (int)tb / 2, hw = h + L2_LPC - 1;
+    ltiles = (l_count + L2_LPC - 1) / L2_LPC;
     size_t bytes = 2 * sizeof(float4) * ((size_t)pad8(h) + 1 + pad8(hw) + 1);
     auto k2 = exact_lag ? k_lag_integrate_f32x2<true> : k_lag_integrate_f32x2<false>;
     SA_CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
@@ -398,8 +407,8 @@ int launch_integrate(int lag_kind, const void *survv, const void *refv, int64_t 
       int64_t nt = std::min<int64_t>(65535, ltiles - t0);
       dim3 grid((unsigned)m, (unsigned)nt);
       k2<<<grid, 256, bytes, s>>>(
-          (const float2 *)surv, (const float2 *)ref, ref_len, l0 + t0 * LAGS_PER_CTA,
-          l_count - t0 * LAGS_PER_CTA, m, (int)tb, conj != 0, (float2 *)(z + t0 * LAGS_PER_CTA * m));
+          (const float2 *)surv, (const float2 *)ref, ref_len, l0 + t0 * L2_LPC,
+          l_count - t0 * L2_LPC, m, (int)tb, conj != 0, (float2 *)(z + t0 * L2_LPC * m));
     }
     SA_LAUNCH_CHECK();
     return SA_OK;
