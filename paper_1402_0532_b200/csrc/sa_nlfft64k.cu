@@ -1,6 +1,7 @@
 // sa_nlfft64k.cu -- single-HBM-pass NL-FFT for N = 2^16 (BASELINE config C3).
 //
-// One signal per thread-block cluster of 8 CTAs, entirely on chip.  N = 256 x 256.
+// One signal per thread-block cluster (4 CTAs for c64, 8 for c128), entirely on
+// chip, 1 CTA per SM.  N = 256 x 256.
 // DIT (value-identical to transforms.py:254-298):
 //   phase A: CTA r takes columns c of X[i][c] = x[256 i + c] (the reference's
 //     bit-reversed blocks, SURVEY §7 hard part 4) in TMA-loaded tiles of TC
@@ -8,15 +9,19 @@
 //     rounds (stage 1 = the 2-point NDFT bottom), and scatters node row
 //     R = rev8(c) over the cluster with st.async into the owner's smem, crediting
 //     the owner's "full" mbarrier (no fence, no cluster barrier): q-columns
-//     [r*COLS, (r+1)*COLS) of every row live in CTA r.
+//     [r*COLS, (r+1)*COLS) of every row live in CTA r.  The CTA's own share goes
+//     through st.shared, each warp arriving on the local full barrier after its
+//     last store (SA_LOCALQ).
 //   phase B: CTA r waits for its node storage, runs global stages 9..16 along R
 //     for its columns (twiddle j = (R mod 2^(t-1))*256 + q), writes y[256 R + q].
-//   An "empty" mbarrier fed by remote relaxed arrives guards storage reuse.
-// c64 double-buffers the node storage (2 x 64 KiB per CTA) and software-pipelines
-// signals: phase B of signal s runs after phase A of signal s+1, so each
-// cluster-wide hand-off has a whole phase of slack instead of stalling 16 warps
-// on the slowest peer.  Each CTA runs NG thread groups (named barriers, own TMA
-// buffer) that split a phase's tiles.  HBM traffic = one read + one write.
+//   An "empty" mbarrier fed by remote relaxed arrives guards storage reuse; each
+//   thread group releases on its own (SA_GREL), so a group that finishes phase B
+//   early starts the next signal.  The TMA tile of the next signal is issued at
+//   the end of phase A, so HBM reads overlap phase B.
+// Each CTA runs NG thread groups (named barriers, own TMA buffer) that split a
+// phase's tiles.  HBM traffic = one read + one write.  Double-buffered node
+// storage (NS = 2, pipelining phase B of signal s behind phase A of s+1) is
+// supported but measured slower: it needs cluster 8 for c64.
 #include <algorithm>
 #include <cooperative_groups.h>
 #include <cudaTypedefs.h>
