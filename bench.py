@@ -256,7 +256,10 @@ def ncu_traffic(kernel_prefix):
         for name, k in d.items():
             if name.startswith(kernel_prefix) and "dram_read_bytes" in k:
                 best = {"bytes_per_launch": k["dram_read_bytes"] + k.get("dram_write_bytes", 0),
-                        "source": os.path.relpath(f, ROOT)}
+                        "source": os.path.relpath(f, ROOT),
+                        "ncu": {key: round(k[key], 1) for key in ("issue_active_pct", "fma_pipe_pct",
+                                                                   "alu_pipe_pct", "fp64_pipe_pct",
+                                                                   "dram_pct") if key in k}}
     return best
 
 
@@ -279,10 +282,13 @@ def roof_hbm(bytes_per_step, ms, kernel=None):
     peaks, src = measured_peaks()
     ach = bytes_per_step / (ms * 1e-3) / 1e9
     tr = ncu_traffic(kernel) if kernel else None
-    return {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": tr["bytes_per_launch"] if tr else None,
-            "traffic_unit": "bytes/launch", "algorithmic_bytes": bytes_per_step, "kernel": kernel,
-            "peak_source": src}
+    r = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+         "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": tr["bytes_per_launch"] if tr else None,
+         "traffic_unit": "bytes/launch", "algorithmic_bytes": bytes_per_step, "kernel": kernel,
+         "peak_source": src}
+    if tr and tr.get("ncu"):  # issue / pipe utilisation of the same kernel (profiles/): the
+        r["ncu_utilisation_pct"] = tr["ncu"]  # evidence SURVEY §8(d) asks for next to the HBM fraction
+    return r
 
 
 def cpu_ndft(x, P):
@@ -359,7 +365,7 @@ def wl_detect(args, k=8):
         _native.check(_native.lib().sa_map_peaks(d, _native.ptr(m), rows, cols, k, _native.ptr(idx), _native.ptr(mag),
                                                  _native.ptr(cnt), _native.ptr(ws), need.value, _native.stream_ptr()))
     mb = v.numel() * v.element_size()
-    return {"step": step, "ops": rows * cols, "bytes": mb,
+    return {"step": step, "ops": rows * cols, "map_bytes": mb,
             "config": {"workload": "§8(f)-1 detection: top-k strict local maxima of |map|", "rows": rows,
                        "cols": cols, "k": k, "dtype": "complex64" if args.dtype == "c64" else "complex128",
                        "l2_policy": "4 maps cycled (> L2)"}}
@@ -488,9 +494,9 @@ def run_ours(args):
                 r = fn()
                 ems, _ = timed(r["step"], max(3, args.steps // 2), 2, 1)
                 e = {"ms_per_step": ems, "config": r["config"], "ops_per_s": r["ops"] / (ems * 1e-3)}
-                if "bytes" in r:  # detection: one read of the map
+                if "map_bytes" in r:  # detection: one read of the map
                     e = {"ms_per_step": ems, "config": r["config"], "cells_per_s": r["ops"] / (ems * 1e-3),
-                         "roofline": roof_hbm(r["bytes"], ems, "k_peaks_tile")}
+                         "roofline": roof_hbm(r["map_bytes"], ems, "k_peaks_tile")}
                 elif "cells" in r:
                     e["cells_per_s"] = r["cells"] / (ems * 1e-3)
                     lms, _ = timed(r["lag_only"], 5, 1, 1)
