@@ -173,6 +173,20 @@ int sa_map_peaks(int dtype, const void *map, int64_t rows, int64_t cols, int k, 
 int sa_map_floor(int dtype, const void *map, int64_t rows, int64_t cols, const int32_t *centers,
                  int ncent, int g0, int g1, uint64_t *out, void *stream);
 
+/* Single-process multi-GPU map (SURVEY §8(b,e)), no NCCL: device devs[g]
+ * computes the contiguous delay rows of shard g ([g*L/G .. (g+1)*L/G), uneven L
+ * allowed) and its transform kernel stores them straight into `out`, an
+ * (l_count x m) allocation on the root devs[0]; peer access from every device to
+ * the root is enabled here.  Per shard: surv[g], ref[g] (inputs on devs[g]),
+ * tw[g] (twiddle set for m on devs[g]), workspace[g] / ws_bytes[g] (for its row
+ * count), stream[g] (on devs[g]).  Asynchronous per stream: the map is
+ * complete when all streams are.  Other arguments as sa_ambiguity_map_v.  The
+ * same device may appear more than once (shards on one GPU, separate streams). */
+int sa_ambiguity_map_multi(int ndev, const int *devs, int dtype, int lag_kind, const void *const *surv,
+                           const void *const *ref, int64_t ns, int64_t ref_len, int64_t l0, int64_t l_count,
+                           int64_t m, double gain, int conj, int doppler, int mode, const void *const *tw,
+                           void *out, void *const *workspace, const int64_t *ws_bytes, void *const *stream);
+
 /* Multi-GPU plumbing: enable direct loads/stores from the current device to
  * `peer_device` memory (NVLink / NVSwitch).  Idempotent.  Used by the sharded
  * map, whose Doppler-transform kernels write their rows straight into the

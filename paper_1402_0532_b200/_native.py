@@ -48,6 +48,8 @@ SIGNATURES = {
     "sa_peaks_workspace_bytes": (_I, [_I64, _I64, _I, ctypes.POINTER(_I64)]),
     "sa_map_peaks": (_I, [_I, _P, _I64, _I64, _I, _P, _P, _P, _P, _I64, _P]),
     "sa_map_floor": (_I, [_I, _P, _I64, _I64, _P, _I, _I, _I, _P, _P]),
+    "sa_ambiguity_map_multi": (_I, [_I, _P, _I, _I, _P, _P, _I64, _I64, _I64, _I64, _I64, ctypes.c_double, _I, _I,
+                                    _I, _P, _P, _P, _P, _P]),
     "sa_enable_peer_access": (_I, [_I]),
     "sa_ipc_open": (_I, [_P, ctypes.POINTER(_P)]),
     "sa_ipc_close": (_I, [_P]),

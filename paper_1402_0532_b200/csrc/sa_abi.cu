@@ -288,6 +288,37 @@ int sa_enable_peer_access(int peer_device) {
   return SA_OK;
 }
 
+int sa_ambiguity_map_multi(int ndev, const int *devs, int dtype, int lag_kind, const void *const *surv,
+                           const void *const *ref, int64_t ns, int64_t ref_len, int64_t l0, int64_t l_count,
+                           int64_t m, double gain, int conj, int doppler, int mode, const void *const *tw,
+                           void *out, void *const *workspace, const int64_t *ws_bytes, void *const *stream) {
+  SA_REQUIRE(ndev >= 1 && devs && surv && ref && tw && workspace && ws_bytes && stream && out, SA_ERR_ARG,
+             "bad arguments");
+  SA_REQUIRE(dtype_ok(dtype), SA_ERR_ARG, "bad dtype %d", dtype);
+  SA_REQUIRE(l_count >= 1, SA_ERR_CONTRACT, "l_bins must be >= 1");
+  int prev = 0;
+  SA_CUDA_TRY(cudaGetDevice(&prev));
+  const int64_t row_bytes = m * (dtype == SA_C64 ? 8 : 16);
+  const int64_t base = l_count / ndev, extra = l_count % ndev;
+  int rc = SA_OK;
+  for (int g = 0; g < ndev && rc == SA_OK; ++g) {
+    const int64_t count = base + (g < extra ? 1 : 0);
+    const int64_t first = g * base + (g < extra ? g : extra);
+    if (cudaSetDevice(devs[g]) != cudaSuccess) {
+      sa_set_error("cudaSetDevice(%d) failed", devs[g]);
+      rc = SA_ERR_CUDA;
+      break;
+    }
+    if (devs[g] != devs[0]) rc = sa_enable_peer_access(devs[0]);
+    if (rc == SA_OK && count > 0)
+      rc = sa_ambiguity_map_v(dtype, lag_kind, surv[g], ref[g], ns, ref_len, l0 + first, count, m, gain, conj,
+                              doppler, mode, tw[g], (char *)out + first * row_bytes, workspace[g], ws_bytes[g],
+                              stream[g]);
+  }
+  cudaSetDevice(prev);
+  return rc;
+}
+
 int sa_ipc_open(const void *handle64, void **dptr) {
   SA_REQUIRE(handle64 && dptr, SA_ERR_ARG, "null pointer");
   cudaIpcMemHandle_t h;

@@ -214,3 +214,53 @@ def broadcast_inputs(surv, ref, src: int = 0, group=None):
     dist.broadcast(_wire(surv), src=src, group=group)
     dist.broadcast(_wire(ref), src=src, group=group)
     return surv, ref
+
+
+def ambiguity_map_multi_device(survs, refs, l_bins: int, m: int, devices, *, l0: int = 0, gain: float = 1.0,
+                               conjugate_ref: bool = True, doppler: str = "nfft", mode: str = "fast",
+                               lag: str = "mf"):
+    """Single-process multi-GPU map through ``sa_ambiguity_map_multi`` (no NCCL,
+    no torch.distributed): ``survs[g]`` / ``refs[g]`` are the inputs resident on
+    ``devices[g]``; shard g's transform kernel stores its delay rows straight into
+    the returned (l_bins x m) map on ``devices[0]`` (peer access).  Each shard runs
+    on its own stream; the caller's current stream on ``devices[0]`` waits for all
+    of them, so the result is stream-ordered like any other call."""
+    import torch
+    from . import _native
+    from ._device import sa_dtype_of
+    from .twiddle import device_twiddles
+    G = len(devices)
+    if not (len(survs) == len(refs) == G >= 1):
+        raise ValueError("one surveillance / reference tensor per device")
+    d = sa_dtype_of(survs[0])
+    out = torch.empty((l_bins, m), dtype=survs[0].dtype, device=f"cuda:{devices[0]}")
+    dop = {"nfft": _native.SA_DOPPLER_NLFFT, "ndft": _native.SA_DOPPLER_NDFT,
+           "fft": _native.SA_DOPPLER_FFT_EXACT}[doppler]
+    md = {"fast": _native.SA_NDFT_FAST, "exact": _native.SA_NDFT_EXACT}[mode]
+    lk = {"mf": _native.SA_LAG_MF, "exact": _native.SA_LAG_EXACT}[lag]
+    streams, ws, tws, ws_bytes = [], [], [], []
+    for g, dev in enumerate(devices):
+        with torch.cuda.device(dev):
+            first, count = shard_rows(l_bins, G, g)
+            need = ctypes.c_int64()
+            _native.check(_native.lib().sa_ambiguity_workspace_bytes(d, max(1, count), m, ctypes.byref(need)))
+            ws.append(torch.empty(max(1, need.value), dtype=torch.uint8, device=f"cuda:{dev}"))
+            ws_bytes.append(ws[-1].numel())
+            tws.append(device_twiddles(m, d, dev))
+            s = torch.cuda.Stream(device=dev)
+            s.wait_stream(torch.cuda.current_stream(dev))  # inputs / out are ordered on the current streams
+            if dev != devices[0]:
+                s.wait_stream(torch.cuda.current_stream(devices[0]))
+            streams.append(s)
+    P = ctypes.c_void_p
+    arr = lambda xs: (P * G)(*xs)  # noqa: E731
+    _native.check(_native.lib().sa_ambiguity_map_multi(
+        G, (ctypes.c_int * G)(*devices), d, lk, arr([t.data_ptr() for t in survs]),
+        arr([t.data_ptr() for t in refs]), survs[0].numel(), refs[0].numel(), l0, l_bins, m, float(gain),
+        int(conjugate_ref), dop, md, arr(tws), P(out.data_ptr()), arr([w.data_ptr() for w in ws]),
+        (ctypes.c_int64 * G)(*ws_bytes), arr([s.cuda_stream for s in streams])))
+    root = torch.cuda.current_stream(devices[0])
+    for s, w in zip(streams, ws):
+        root.wait_stream(s)
+        w.record_stream(s)
+    return out

@@ -595,3 +595,20 @@ def test_ndft_and_map_subnormal_inputs(sa):
     r[::13] = -0.0
     got = sa.ambiguity_map(r, s, 16, 64, mode="exact")
     assert_value_equal(got, oracle.ambiguity_map(r, s, 0, 16, 64))
+
+
+@pytest.mark.parametrize("devs", [[0], [0, 0], [0, 0, 0]])
+def test_map_multi_device_single_process(sa, devs):
+    """sa_ambiguity_map_multi (single-process multi-GPU through the C ABI, no
+    NCCL): shards listed on the same GPU run on separate streams and store their
+    rows into the root's map; uneven row counts; equal to the single-call map."""
+    from paper_1402_0532_b200.sharded import ambiguity_map_multi_device
+    from paper_1402_0532_b200.workloads import radar_scene
+    sc = radar_scene(1 << 16, 2, 4545)
+    s = dev(sc.surv.astype(np.complex64))
+    r = dev(sc.ref.astype(np.complex64))
+    got = ambiguity_map_multi_device([s] * len(devs), [r] * len(devs), 101, 128, devs, l0=7)
+    assert T().equal(got, sa.ambiguity_map(s, r, 101, 128, l0=7))
+    got = ambiguity_map_multi_device([s] * len(devs), [r] * len(devs), 33, 128, devs, lag="exact", mode="exact",
+                                     doppler="fft")
+    assert T().equal(got, sa.ambiguity_map(s, r, 33, 128, lag="exact", mode="exact", doppler="fft"))
