@@ -185,7 +185,7 @@ def test_nfft_65536_reference_hash(sa, golden):
 
 
 @pytest.mark.parametrize("variant", ["dit", "dif"])
-@pytest.mark.parametrize("logn", list(range(1, 19)))
+@pytest.mark.parametrize("logn", list(range(1, 19)) + [20, 22])
 def test_nfft_batch_vs_oracle(sa, variant, logn):
     n = 1 << logn
     batch = max(1, min(64, (1 << 18) // n))
