@@ -616,3 +616,16 @@ def test_map_multi_device_single_process(sa, devs):
     got = ambiguity_map_multi_device([s] * len(devs), [r] * len(devs), 33, 128, devs, lag="exact", mode="exact",
                                      doppler="fft")
     assert T().equal(got, sa.ambiguity_map(s, r, 33, 128, lag="exact", mode="exact", doppler="fft"))
+
+
+def test_empty_batches(sa):
+    """Zero-row batches and zero-length elementwise inputs are no-ops, not errors."""
+    torch = T()
+    for dt in (torch.complex64, torch.complex128):
+        for n in (64, 1000, 1 << 16):
+            x = torch.empty((0, n), dtype=dt, device="cuda")
+            assert sa.ndft_batch(x).shape == (0, n)
+            if n & (n - 1) == 0:
+                for v in ("dit", "dif", "exact"):
+                    assert sa.nfft_batch(x, variant=v).shape == (0, n)
+    assert sa.mf_complex(np.zeros(0, complex), np.zeros(0, complex)).size == 0
