@@ -52,7 +52,11 @@ template <> struct NdftCfg<double> {
 
 SA_HD int swz(int mm, int vv) { return vv ^ ((mm >> 1) & 7); }
 
-template <typename T, bool POW2, bool TW_SMEM>
+// EX: exact mode on the same tiles -- every ⊙ rounded as the reference does
+// (each real ⊗ = one fma of exact sign products, rr/ri = one add each) and the
+// accumulator advanced sequentially over m from +0: value-identical to
+// transforms.py:223-251 (12 FP ops per ⊙ instead of 8).
+template <typename T, bool POW2, bool TW_SMEM, bool EX>
 __global__ void __launch_bounds__(NDFT_THREADS, sizeof(T) == 8 ? SA_D_MINB : 1)
     k_ndft_fast(const C2<T> *__restrict__ x, C2<T> *__restrict__ y, int64_t batch, int n,
                 const C4<T> *__restrict__ quad, T gain, bool use_gain) {
@@ -151,9 +155,23 @@ __global__ void __launch_bounds__(NDFT_THREADS, sizeof(T) == 8 ? SA_D_MINB : 1)
         }
         idx[kk] = nx;
       }
-      // d = {xr, xi, sgn xr, sgn xi} ; w = {Wr, Wi, sgn Wr, sgn Wi}.  Consecutive
-      // FMAs share the data operand (register-reuse cache, see the f32x2 kernel);
-      // per accumulator the terms add in the same order as before.
+      // d = {xr, xi, sgn xr, sgn xi} ; w = {Wr, Wi, sgn Wr, sgn Wi}.
+      if constexpr (EX) {  // rr = Wr⊗xr - Wi⊗xi ; ri = Wi⊗xr + xi⊗Wr (operator.py:128-131)
+#pragma unroll
+        for (int i = 0; i < TB; ++i)
+#pragma unroll
+          for (int kk = 0; kk < TK; ++kk) {
+            const T p1 = sa_fma(w[kk].z, d[i].x, sa_mul(d[i].z, w[kk].x));
+            const T p2 = sa_fma(w[kk].w, d[i].y, sa_mul(d[i].w, w[kk].y));
+            const T p3 = sa_fma(w[kk].w, d[i].x, sa_mul(d[i].z, w[kk].y));
+            const T p4 = sa_fma(w[kk].z, d[i].y, sa_mul(d[i].w, w[kk].x));
+            accr[kk][i] = sa_add(accr[kk][i], sa_sub(p1, p2));
+            acci[kk][i] = sa_add(acci[kk][i], sa_add(p3, p4));
+          }
+        continue;
+      }
+      // Consecutive FMAs share the data operand (register-reuse cache, see the
+      // f32x2 kernel); per accumulator the terms add in the same order as before.
 #pragma unroll
       for (int i = 0; i < TB; ++i) {
 #pragma unroll
@@ -220,7 +238,7 @@ using F2 = F2Cfg<SA_F2_TP, SA_F2_TK, SA_F2_NC>;  // default: 128 vectors x 64 bi
 #ifndef SA_F2_MINB
 #define SA_F2_MINB 2
 #endif
-template <bool POW2, bool TW_SMEM>
+template <bool POW2, bool TW_SMEM, bool EX>
 __global__ void __launch_bounds__(NDFT_THREADS, SA_F2_MINB)
     k_ndft_fast_f32x2(const float2 *__restrict__ x, float2 *__restrict__ y, int64_t batch, int n,
                       const float4 *__restrict__ quad, float gain, bool use_gain) {
@@ -323,6 +341,22 @@ __global__ void __launch_bounds__(NDFT_THREADS, SA_F2_MINB)
       // reads one 64-bit and one 32-bit register -- within the 2-cycle pipe slot.
       // Per accumulator the terms still add in the order
       //   Re: sxr*Wr, xr*sWr, -sxi*Wi, -xi*sWi ;  Im: sxr*Wi, xr*sWi, sxi*Wr, xi*sWr.
+      if constexpr (EX) {  // exact ⊙ per vector pair (see k_ndft_fast): 12 packed ops
+#pragma unroll
+        for (int i = 0; i < TP; ++i)
+#pragma unroll
+          for (int kk = 0; kk < TK; ++kk) {
+            const V Wr = A::pack(w[kk].x, w[kk].x), Wi = A::pack(w[kk].y, w[kk].y);
+            const V sWr = A::pack(w[kk].z, w[kk].z), sWi = A::pack(w[kk].w, w[kk].w);
+            const V p1 = A::fma(sWr, xr[i], A::mul(sr[i], Wr));  // Wr⊗xr
+            const V p2 = A::fma(sWi, xi[i], A::mul(si[i], Wi));  // Wi⊗xi
+            const V p3 = A::fma(sWi, xr[i], A::mul(sr[i], Wi));  // Wi⊗xr
+            const V p4 = A::fma(sWr, xi[i], A::mul(si[i], Wr));  // xi⊗Wr
+            accr[kk][i] = A::add(accr[kk][i], A::sub(p1, p2));
+            acci[kk][i] = A::add(acci[kk][i], A::add(p3, p4));
+          }
+        continue;
+      }
 #pragma unroll
       for (int i = 0; i < TP; ++i) {
 #pragma unroll
@@ -411,7 +445,14 @@ int launch(const void *xv, void *yv, int64_t batch, int64_t n64, const SaTwiddle
     return SA_ERR_UNSUPPORTED;
   }
   const int n = (int)n64;
-  if (mode == SA_NDFT_EXACT) {
+  // fp32: packed FFMA2 kernel (F2 tile); fp64: scalar DFMA kernel (NdftCfg tile)
+  constexpr bool F32X2 = sizeof(T) == 4;
+  constexpr int BV = F32X2 ? F2::BV : 32 * NdftCfg<T>::TB;
+  constexpr int BK = F32X2 ? F2::BK : NDFT_WARPS * NdftCfg<T>::TK;
+  // exact mode: the tiled kernels (EX) once a batch fills a tile, else one
+  // thread per (vector, bin)
+  const bool exact = mode == SA_NDFT_EXACT;
+  if (exact && batch < BV) {
     if (batch > 65535) {
       // grid.y limit: split into slices
       for (int64_t b = 0; b < batch; b += 65535) {
@@ -427,10 +468,6 @@ int launch(const void *xv, void *yv, int64_t batch, int64_t n64, const SaTwiddle
     SA_LAUNCH_CHECK();
     return SA_OK;
   }
-  // fp32: packed FFMA2 kernel (F2 tile); fp64: scalar DFMA kernel (NdftCfg tile)
-  constexpr bool F32X2 = sizeof(T) == 4;
-  constexpr int BV = F32X2 ? F2::BV : 32 * NdftCfg<T>::TB;
-  constexpr int BK = F32X2 ? F2::BK : NDFT_WARPS * NdftCfg<T>::TK;
   const bool pow2 = (n & (n - 1)) == 0;
   const bool tw_smem = (size_t)n * sizeof(C4<T>) <= 64 * 1024;
   size_t bytes = (F32X2 ? F2::STAGE_BYTES : sizeof(C4<T>) * 2 * NC * BV) +
@@ -447,13 +484,13 @@ int launch(const void *xv, void *yv, int64_t batch, int64_t n64, const SaTwiddle
 #define SA_NDFT_GO(P2, TS)                                                                  \
   do {                                                                                      \
     if constexpr (F32X2) {                                                                  \
-      auto kern = k_ndft_fast_f32x2<P2, TS>;                                                \
+      auto kern = exact ? k_ndft_fast_f32x2<P2, TS, true> : k_ndft_fast_f32x2<P2, TS, false>; \
       SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
                                        (int)bytes));                                        \
       kern<<<grid, NDFT_THREADS, bytes, s>>>((const float2 *)xs, (float2 *)ys, bleft, n,    \
                                              (const float4 *)quad, (float)g, use_gain);     \
     } else {                                                                                \
-      auto kern = k_ndft_fast<T, P2, TS>;                                                   \
+      auto kern = exact ? k_ndft_fast<T, P2, TS, true> : k_ndft_fast<T, P2, TS, false>;    \
       SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
                                        (int)bytes));                                        \
       kern<<<grid, NDFT_THREADS, bytes, s>>>(xs, ys, bleft, n, quad, g, use_gain);         \

@@ -629,3 +629,21 @@ def test_empty_batches(sa):
                 for v in ("dit", "dif", "exact"):
                     assert sa.nfft_batch(x, variant=v).shape == (0, n)
     assert sa.mf_complex(np.zeros(0, complex), np.zeros(0, complex)).size == 0
+
+
+@pytest.mark.parametrize("n", [64, 1000, 1024])
+def test_ndft_exact_tiled_value_identical(sa, n):
+    """Exact mode on batches that fill the vector tile (the tiled EX kernels):
+    value-identical to the sequential oracle in fp64 and fp32; zeros, a tone."""
+    g = np.random.default_rng(600 + n)
+    b = 300
+    x = g.standard_normal((b, n)) + 1j * g.standard_normal((b, n))
+    x[5] = 0
+    x[6, ::4] = 0
+    x[7] = np.conj(oracle.twiddle_table(n)[(3 * np.arange(n)) % n])
+    assert_value_equal(sa.ndft_batch(dev(x), mode="exact").cpu().numpy(), oracle.ndft(x, nthreads=8))
+    x32 = x.astype(np.complex64)
+    assert_value_equal(sa.ndft_batch(dev(x32), mode="exact").cpu().numpy(),
+                       oracle.ndft(x32, dtype="f32", nthreads=8))
+    assert_value_equal(sa.ndft_batch(dev(x), mode="exact", gain=0.75).cpu().numpy(),
+                       oracle.ndft(0.75 * x, nthreads=8))
