@@ -95,6 +95,58 @@ __global__ void __launch_bounds__(256) k_lag_integrate_exact(
   z[id] = {sr, si};
 }
 
+// Exact / sequential mode on smem tiles: one CTA = block q x LAGS_EXACT lags,
+// one thread per lag walking the block's T samples in order from +0 -- the
+// oracle's composition, value-identical -- with the surveillance block
+// (broadcast reads) and the reference window staged once with signs.
+constexpr int LAGS_EXACT = 256;
+
+template <typename T, bool EXACT>
+__global__ void __launch_bounds__(LAGS_EXACT) k_lag_integrate_seq(
+    const C2<T> *__restrict__ surv, const C2<T> *__restrict__ ref, int64_t ref_len, int64_t l0,
+    int64_t l_count, int64_t m, int tb, bool conj, C2<T> *__restrict__ z) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int win = tb + LAGS_EXACT - 1;
+  C4<T> *ss = reinterpret_cast<C4<T> *>(smem_raw);  // {sr, si, sgn sr, sgn si}
+  C4<T> *rs = ss + tb;                               // {cr, ci, sgn cr, sgn ci}, conj folded in
+  const int64_t q = blockIdx.x;
+  const int64_t lt = l0 + (int64_t)blockIdx.y * LAGS_EXACT;
+  const int64_t i0 = q * tb;
+  const int64_t ws = i0 - lt - (LAGS_EXACT - 1);
+  for (int t = threadIdx.x; t < tb; t += blockDim.x) {
+    const C2<T> a = surv[i0 + t];
+    ss[t] = {a.x, a.y, sa_sgn(a.x), sa_sgn(a.y)};
+  }
+  for (int u = threadIdx.x; u < win; u += blockDim.x) {
+    const int64_t j = ws + u;
+    T cr = T(0), ci = conj ? -T(0) : T(0);
+    if (j >= 0 && j < ref_len) {
+      const C2<T> r = ref[j];
+      cr = r.x;
+      ci = conj ? -r.y : r.y;
+    }
+    rs[u] = {cr, ci, sa_sgn(cr), sa_sgn(ci)};
+  }
+  __syncthreads();
+  const int l = threadIdx.x;
+  if (lt + l - l0 >= l_count) return;
+  const C4<T> *cw = rs + (LAGS_EXACT - 1) - l;  // sample t pairs with window slot t + 255 - l
+  T sr = T(0), si = T(0);
+  for (int t = 0; t < tb; ++t) {
+    const C4<T> a = ss[t], c = cw[t];
+    T rr, ri;
+    if (EXACT) {
+      sa_npmul<T>(a.x, a.y, c.x, c.y, rr, ri);
+    } else {  // surv ⊙ c, operand order (surv, ref): ambiguity.py:152; identity form, one rounding each
+      rr = sa_sub(sa_fma(c.z, a.x, sa_mul(a.z, c.x)), sa_fma(c.w, a.y, sa_mul(a.w, c.y)));
+      ri = sa_add(sa_fma(c.z, a.y, sa_mul(a.w, c.x)), sa_fma(a.z, c.y, sa_mul(c.w, a.x)));
+    }
+    sr = sa_add(sr, rr);
+    si = sa_add(si, ri);
+  }
+  z[(lt + l - l0) * m + q] = {sr, si};
+}
+
 template <typename T, bool EXACT>
 __global__ void __launch_bounds__(256) k_lag_integrate_fast(
     const C2<T> *__restrict__ surv, const C2<T> *__restrict__ ref, int64_t ref_len, int64_t l0,
@@ -389,6 +441,20 @@ int launch_integrate(int lag_kind, const void *survv, const void *refv, int64_t 
   if (l_count == 0 || m == 0) return SA_OK;
   const bool exact_lag = lag_kind == SA_LAG_EXACT;
   const bool fast = mode == SA_NDFT_FAST && tb % 8 == 0 && tb <= 8192 && m <= 0x7fffffff;
+  const size_t seq_bytes = sizeof(C4<T>) * (size_t)(2 * tb + LAGS_EXACT - 1);
+  if (!fast && tb >= 8 && seq_bytes <= 200 * 1024 && m <= 0x7fffffff) {
+    auto kern = exact_lag ? k_lag_integrate_seq<T, true> : k_lag_integrate_seq<T, false>;
+    SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)seq_bytes));
+    const int64_t lt = (l_count + LAGS_EXACT - 1) / LAGS_EXACT;
+    for (int64_t t0 = 0; t0 < lt; t0 += 65535) {
+      const int64_t nt = std::min<int64_t>(65535, lt - t0);
+      kern<<<dim3((unsigned)m, (unsigned)nt), LAGS_EXACT, seq_bytes, s>>>(
+          surv, ref, ref_len, l0 + t0 * LAGS_EXACT, l_count - t0 * LAGS_EXACT, m, (int)tb, conj != 0,
+          z + t0 * LAGS_EXACT * m);
+    }
+    SA_LAUNCH_CHECK();
+    return SA_OK;
+  }
   if (!fast) {
     int64_t tot = l_count * m;
     auto kern = lag_kind == SA_LAG_EXACT ? k_lag_integrate_exact<T, true> : k_lag_integrate_exact<T, false>;

@@ -412,6 +412,27 @@ def test_map_c64_block_lengths(sa, tb):
     assert_value_equal(ye, oracle.ambiguity_map(surv, ref, l0, L, m, dtype="f32", nthreads=8))
 
 
+@pytest.mark.parametrize("dt", ["c64", "c128"])
+@pytest.mark.parametrize("lag", ["mf", "exact"])
+@pytest.mark.parametrize("tb", [8, 33, 2048])
+def test_map_exact_seq_tiles(sa, dt, lag, tb):
+    """Exact (sequential) mode on the smem-tiled kernel (k_lag_integrate_seq, T >= 8):
+    lag counts spanning several 256-lag tiles with a ragged tail, l0 > 0, zeros in
+    both signals -- value-equal to the oracle's sequential composition."""
+    g = np.random.default_rng(1300 + tb)
+    m = {8: 128, 33: 32, 2048: 4}[tb]  # ns > l0 + L: every lag is below the reference length
+    ns = tb * m
+    cdt = np.complex64 if dt == "c64" else np.complex128
+    surv = (g.standard_normal(ns) + 1j * g.standard_normal(ns)).astype(cdt)
+    ref = np.exp(2j * np.pi * g.random(ns)).astype(cdt)
+    surv[[0, 7, ns // 2]] = 0
+    ref[[1, 3]] = 0
+    l0, L = 5, 600
+    y = sa.ambiguity_map(dev(surv), dev(ref), L, m, l0=l0, lag=lag, mode="exact").cpu().numpy()
+    want = oracle.ambiguity_map(surv, ref, l0, L, m, lag=lag, dtype="f32" if dt == "c64" else "f64", nthreads=8)
+    assert_value_equal(y, want)
+
+
 # --- exact-multiply variants (SURVEY §8(f)-2) --------------------------------------
 
 @pytest.mark.parametrize("n", [2, 4, 8, 64, 512, 4096])
