@@ -147,19 +147,20 @@ __global__ void __launch_bounds__(LAGS_EXACT) k_lag_integrate_seq(
   z[(lt + l - l0) * m + q] = {sr, si};
 }
 
-template <typename T, bool EXACT>
+template <typename T, bool EXACT, int NT>
 __global__ void __launch_bounds__(256) k_lag_integrate_fast(
     const C2<T> *__restrict__ surv, const C2<T> *__restrict__ ref, int64_t ref_len, int64_t l0,
     int64_t l_count, int64_t m, int tb, bool conj, C2<T> *__restrict__ z) {
+  constexpr int LPT = NT * LAGS_PER_CTA;  // lags staged per CTA (NT lag tiles, as k_lag_integrate_f32x2)
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int win = tb + LAGS_PER_CTA - 1;
+  const int win = tb + LPT - 1;
   C4<T> *ss = reinterpret_cast<C4<T> *>(smem_raw);  // surveillance block, padded
   C4<T> *rs = ss + pad8(tb) + 1;                     // reference window, padded
 
   const int64_t q = blockIdx.x;
-  const int64_t lt = l0 + (int64_t)blockIdx.y * LAGS_PER_CTA;  // first lag of the CTA
+  const int64_t lt0 = l0 + (int64_t)blockIdx.y * LPT;  // first lag of the CTA
   const int64_t i0 = q * tb;
-  const int64_t ws = i0 - lt - (LAGS_PER_CTA - 1);  // global ref index of window slot 0
+  const int64_t ws = i0 - lt0 - (LPT - 1);  // global ref index of window slot 0
 
   // Prologue: PF loads in flight per thread (all issued before the first use).
   constexpr int PF = 8;
@@ -192,8 +193,10 @@ __global__ void __launch_bounds__(256) k_lag_integrate_fast(
   __syncthreads();
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t lw = lt + warp * LAGS_PER_WARP;  // first lag of this warp
-  if (lw - l0 >= l_count) return;                // whole warp past the last row
+#pragma unroll 1
+  for (int k = 0; k < NT; ++k) {  // lag tile k: window offset (NT-1-k)*64, a multiple of 8 (pad8-safe)
+  const int64_t lw = lt0 + k * LAGS_PER_CTA + warp * LAGS_PER_WARP;  // first lag of this warp
+  if (lw - l0 >= l_count) break;  // whole warp past the last row (warp-uniform; no barrier follows)
 
   T accr[LAGS_PER_WARP], acci[LAGS_PER_WARP];
 #pragma unroll
@@ -206,7 +209,8 @@ __global__ void __launch_bounds__(256) k_lag_integrate_fast(
 #pragma unroll
     for (int i = 0; i < 8; ++i) a[i] = ss[pad8(t0 + i)];
     // window index of (sample t0+i, lag lw+j) = t0 + 63 - 8*warp - j + i
-    const int base = t0 + (LAGS_PER_CTA - 1) - LAGS_PER_WARP * warp - (LAGS_PER_WARP - 1);
+    const int base = (NT - 1 - k) * LAGS_PER_CTA + t0 + (LAGS_PER_CTA - 1) - LAGS_PER_WARP * warp -
+                     (LAGS_PER_WARP - 1);
 #pragma unroll
     for (int u = 0; u < 15; ++u) c[u] = rs[pad8(base + u)];
     // Consecutive FMAs share the surveillance operand (register-reuse cache)
@@ -269,11 +273,15 @@ __global__ void __launch_bounds__(256) k_lag_integrate_fast(
     int64_t row = lw + lane - l0;
     if (row < l_count) z[row * m + q] = {vr, vi};
   }
+  }
 }
 
 // complex64, T % 16 == 0: entry e of S holds samples e and e + T/2, entry u of
 // C window slots u and u + T/2, each as {x, x'}, {y, y'} (S0/C0) and the signs
 // {sx, sx'}, {sy, sy'} (S1/C1), in pad8-strided float4 arrays.
+#ifndef SA_LAG2_RS  // reduce-scatter epilogue (-D for A/B)
+#define SA_LAG2_RS 1
+#endif
 #ifndef SA_LAG2_LPW  // packed kernel: lags per warp, min CTAs per SM (-D for sweeps)
 #define SA_LAG2_LPW 8
 #define SA_LAG2_MINB 2
@@ -281,71 +289,37 @@ __global__ void __launch_bounds__(256) k_lag_integrate_fast(
 constexpr int L2_LPW = SA_LAG2_LPW;
 constexpr int L2_LPC = LAG_WARPS * L2_LPW;  // lags per CTA
 constexpr int L2_WIN = 8 + L2_LPW - 1;      // window pairs per 8-sample sub-block
+// Each CTA stages one block + window for NT consecutive lag tiles (template
+// NT, chosen per launch): the staging prologue's global loads, index math and
+// sign computation (IMAD/FSET/LOP3 contending with the FFMA2 stream; ~50% of
+// the warp-stall samples at NT = 1) are paid once per NT * L2_LPC lags.
+// C4 lag stage: NT 1 / 2 / 4 / 8 / 16 = 0.388 / 0.369 / 0.357 / 0.353 / 0.402 ms.
 
+// Packed pair layout views of one CTA's dynamic shared memory.
+struct Lag2Smem {
+  float4 *S0, *S1, *C0, *C1;
+  __device__ Lag2Smem(unsigned char *base, int h, int hw) {
+    S0 = reinterpret_cast<float4 *>(base);
+    S1 = S0 + pad8(h) + 1;
+    C0 = S1 + pad8(h) + 1;
+    C1 = C0 + pad8(hw) + 1;
+  }
+  __host__ __device__ static size_t bytes(int h, int hw) {
+    return 2 * sizeof(float4) * ((size_t)pad8(h) + 1 + pad8(hw) + 1);
+  }
+};
+
+// One (block q, L2_LPC lags) tile from the staged pair layout: lag ⊙ products
+// summed over the block, then the warp reduction and the store of z rows.
 template <bool EXACT>
-__global__ void __launch_bounds__(256, SA_LAG2_MINB) k_lag_integrate_f32x2(
-    const float2 *__restrict__ surv, const float2 *__restrict__ ref, int64_t ref_len, int64_t l0,
-    int64_t l_count, int64_t m, int tb, bool conj, float2 *__restrict__ z) {
+__device__ __forceinline__ void lag2_tile(const Lag2Smem &sm, int h, int64_t lt, int64_t l0, int64_t l_count,
+                                          int64_t m, int64_t q, int coff, float2 *__restrict__ z) {
   using A = Ar<float>;
   using V = A::V;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int h = tb >> 1;
-  const int hw = h + L2_LPC - 1;  // window pair entries
-  float4 *S0 = reinterpret_cast<float4 *>(smem_raw);
-  float4 *S1 = S0 + pad8(h) + 1;
-  float4 *C0 = S1 + pad8(h) + 1;
-  float4 *C1 = C0 + pad8(hw) + 1;
-
-  const int64_t q = blockIdx.x;
-  const int64_t lt = l0 + (int64_t)blockIdx.y * L2_LPC;
-  const int64_t i0 = q * tb;
-  const int64_t ws = i0 - lt - (L2_LPC - 1);
-
-  constexpr int PF = 4;
-  for (int e0 = threadIdx.x; e0 < h; e0 += PF * blockDim.x) {
-    float2 a[PF], b[PF];
-#pragma unroll
-    for (int u = 0; u < PF; ++u) {
-      const int e = e0 + u * blockDim.x;
-      if (e < h) {
-        a[u] = __ldg(&surv[i0 + e]);
-        b[u] = __ldg(&surv[i0 + e + h]);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < PF; ++u) {
-      const int e = e0 + u * blockDim.x;
-      if (e < h) {
-        S0[pad8(e)] = {a[u].x, b[u].x, a[u].y, b[u].y};
-        S1[pad8(e)] = {sa_sgn(a[u].x), sa_sgn(b[u].x), sa_sgn(a[u].y), sa_sgn(b[u].y)};
-      }
-    }
-  }
-  for (int e0 = threadIdx.x; e0 < hw; e0 += PF * blockDim.x) {
-    float2 a[PF], b[PF];
-#pragma unroll
-    for (int u = 0; u < PF; ++u) {
-      const int e = e0 + u * blockDim.x;
-      const int64_t j = ws + e, k = j + h;
-      a[u] = b[u] = {0.f, 0.f};
-      if (e < hw && j >= 0 && j < ref_len) a[u] = __ldg(&ref[j]);
-      if (e < hw && k >= 0 && k < ref_len) b[u] = __ldg(&ref[k]);
-    }
-#pragma unroll
-    for (int u = 0; u < PF; ++u) {
-      const int e = e0 + u * blockDim.x;
-      const float ai = conj ? -a[u].y : a[u].y, bi = conj ? -b[u].y : b[u].y;
-      if (e < hw) {
-        C0[pad8(e)] = {a[u].x, b[u].x, ai, bi};
-        C1[pad8(e)] = {sa_sgn(a[u].x), sa_sgn(b[u].x), sa_sgn(ai), sa_sgn(bi)};
-      }
-    }
-  }
-  __syncthreads();
-
+  const float4 *S0 = sm.S0, *S1 = sm.S1, *C0 = sm.C0, *C1 = sm.C1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t lw = lt + warp * L2_LPW;
-  if (lw - l0 >= l_count) return;
+  if (lw - l0 >= l_count) return;  // warp-uniform; no barrier follows
 
   V accr[L2_LPW], acci[L2_LPW];
 #pragma unroll
@@ -354,7 +328,7 @@ __global__ void __launch_bounds__(256, SA_LAG2_MINB) k_lag_integrate_f32x2(
   const int nsb = h >> 3;
   for (int sb = lane; sb < nsb; sb += 32) {
     const int t0 = sb * 8;
-    const int base = t0 + (L2_LPC - 1) - L2_LPW * warp - (L2_LPW - 1);
+    const int base = coff + t0 + (L2_LPC - 1) - L2_LPW * warp - (L2_LPW - 1);
     V cx[L2_WIN], cy[L2_WIN], cz[L2_WIN], cw[L2_WIN];  // window pairs {re}, {im}, {sgn re}, {sgn im}
 #pragma unroll
     for (int u = 0; u < L2_WIN; ++u) {
@@ -404,6 +378,37 @@ __global__ void __launch_bounds__(256, SA_LAG2_MINB) k_lag_integrate_f32x2(
       for (int j = 0; j < L2_LPW; ++j) acci[j] = A::fma(sx, cw[i - j + L2_LPW - 1], acci[j]);
     }
   }
+#if SA_LAG2_RS
+  // Reduce-scatter over the warp: 2*L2_LPW partial sums per lane, halved at
+  // each xor level (8+4+2+1 shuffles for 16 values, + 1 for the last pair)
+  // instead of a full butterfly per value (80).  Lane bits 4..1 select the
+  // value; lanes l and l^1 end with the same sum.
+  static_assert(L2_LPW == 8, "reduce-scatter epilogue assumes 16 values per lane");
+  float v[16];
+#pragma unroll
+  for (int j = 0; j < L2_LPW; ++j) {
+    float a, b;
+    A::unpack(accr[j], a, b);
+    v[2 * j] = sa_add(a, b);
+    A::unpack(acci[j], a, b);
+    v[2 * j + 1] = sa_add(a, b);
+  }
+#pragma unroll
+  for (int half = 8; half >= 1; half >>= 1) {
+    const bool up = lane & (half << 1);  // keep the upper half of the current values
+#pragma unroll
+    for (int k = 0; k < half; ++k) {
+      const float keep = up ? v[k + half] : v[k], send = up ? v[k] : v[k + half];
+      v[k] = sa_add(keep, __shfl_xor_sync(0xffffffffu, send, half << 1));
+    }
+  }
+  v[0] = sa_add(v[0], __shfl_xor_sync(0xffffffffu, v[0], 1));
+  if (!(lane & 1)) {
+    const int idx = lane >> 1;  // value 2j + c: lag j, component c
+    const int64_t row = lw + (idx >> 1) - l0;
+    if (row < l_count) reinterpret_cast<float *>(z + row * m + q)[idx & 1] = v[0];
+  }
+#else
   float vr[L2_LPW], vi[L2_LPW];
 #pragma unroll
   for (int j = 0; j < L2_LPW; ++j) {
@@ -429,6 +434,107 @@ __global__ void __launch_bounds__(256, SA_LAG2_MINB) k_lag_integrate_f32x2(
     const int64_t row = lw + lane - l0;
     if (row < l_count) z[row * m + q] = {r, i};
   }
+#endif
+}
+
+template <bool EXACT, int L2_NT>
+__global__ void __launch_bounds__(256, SA_LAG2_MINB) k_lag_integrate_f32x2(
+    const float2 *__restrict__ surv, const float2 *__restrict__ ref, int64_t ref_len, int64_t l0,
+    int64_t l_count, int64_t m, int tb, bool conj, float2 *__restrict__ z) {
+  constexpr int L2_LPT = L2_NT * L2_LPC;  // lags staged per CTA
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int h = tb >> 1;
+  const int hw = h + L2_LPT - 1;  // window pair entries for the CTA's L2_NT lag tiles
+  const Lag2Smem sm(smem_raw, h, hw);
+  float4 *S0 = sm.S0, *S1 = sm.S1, *C0 = sm.C0, *C1 = sm.C1;
+
+  const int64_t q = blockIdx.x;
+  const int64_t lt = l0 + (int64_t)blockIdx.y * L2_LPT;
+  const int64_t i0 = q * tb;
+  const int64_t ws = i0 - lt - (L2_LPT - 1);
+
+  constexpr int PF = 4;
+  for (int e0 = threadIdx.x; e0 < h; e0 += PF * blockDim.x) {
+    float2 a[PF], b[PF];
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < h) {
+        a[u] = __ldg(&surv[i0 + e]);
+        b[u] = __ldg(&surv[i0 + e + h]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < h) {
+        S0[pad8(e)] = {a[u].x, b[u].x, a[u].y, b[u].y};
+        S1[pad8(e)] = {sa_sgn(a[u].x), sa_sgn(b[u].x), sa_sgn(a[u].y), sa_sgn(b[u].y)};
+      }
+    }
+  }
+  for (int e0 = threadIdx.x; e0 < hw; e0 += PF * blockDim.x) {
+    float2 a[PF], b[PF];
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const int e = e0 + u * blockDim.x;
+      const int64_t j = ws + e, k = j + h;
+      a[u] = b[u] = {0.f, 0.f};
+      if (e < hw && j >= 0 && j < ref_len) a[u] = __ldg(&ref[j]);
+      if (e < hw && k >= 0 && k < ref_len) b[u] = __ldg(&ref[k]);
+    }
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const int e = e0 + u * blockDim.x;
+      const float ai = conj ? -a[u].y : a[u].y, bi = conj ? -b[u].y : b[u].y;
+      if (e < hw) {
+        C0[pad8(e)] = {a[u].x, b[u].x, ai, bi};
+        C1[pad8(e)] = {sa_sgn(a[u].x), sa_sgn(b[u].x), sa_sgn(ai), sa_sgn(bi)};
+      }
+    }
+  }
+  __syncthreads();
+  // the staged block and window serve L2_NT consecutive lag tiles (tile k's
+  // window starts (L2_NT-1-k)*L2_LPC entries in, a multiple of 8: pad8-safe)
+#pragma unroll 1
+  for (int k = 0; k < L2_NT; ++k)
+    lag2_tile<EXACT>(sm, h, lt + k * L2_LPC, l0, l_count, m, q, (L2_NT - 1 - k) * L2_LPC, z);
+}
+
+template <typename T, int NT>
+int launch_lag_fast(bool exact_lag, const C2<T> *surv, const C2<T> *ref, int64_t ref_len, int64_t l0,
+                    int64_t l_count, int64_t m, int64_t tb, int conj, C2<T> *z, size_t bytes, cudaStream_t s) {
+  constexpr int LPT = NT * LAGS_PER_CTA;
+  const int64_t ltiles = (l_count + LPT - 1) / LPT;
+  auto kern = exact_lag ? k_lag_integrate_fast<T, true, NT> : k_lag_integrate_fast<T, false, NT>;
+  SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  for (int64_t t0 = 0; t0 < ltiles; t0 += 65535) {
+    const int64_t nt = std::min<int64_t>(65535, ltiles - t0);
+    kern<<<dim3((unsigned)m, (unsigned)nt), 256, bytes, s>>>(surv, ref, ref_len, l0 + t0 * LPT,
+                                                             l_count - t0 * LPT, m, (int)tb, conj != 0,
+                                                             z + t0 * LPT * m);
+  }
+  SA_LAUNCH_CHECK();
+  return SA_OK;
+}
+
+template <int NT>
+int launch_lag2(bool exact_lag, const void *surv, const void *ref, int64_t ref_len, int64_t l0, int64_t l_count,
+                int64_t m, int64_t tb, int conj, void *z, cudaStream_t s) {
+  constexpr int LPT = NT * L2_LPC;
+  const int h = (int)tb / 2, hw = h + LPT - 1;
+  const int64_t ltiles = (l_count + LPT - 1) / LPT;
+  const size_t bytes = Lag2Smem::bytes(h, hw);
+  auto k2 = exact_lag ? k_lag_integrate_f32x2<true, NT> : k_lag_integrate_f32x2<false, NT>;
+  SA_CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  for (int64_t t0 = 0; t0 < ltiles; t0 += 65535) {
+    const int64_t nt = std::min<int64_t>(65535, ltiles - t0);
+    k2<<<dim3((unsigned)m, (unsigned)nt), 256, bytes, s>>>(
+        (const float2 *)surv, (const float2 *)ref, ref_len, l0 + t0 * LPT, l_count - t0 * LPT, m, (int)tb,
+        conj != 0, (float2 *)z + t0 * LPT * m);
+  }
+  SA_LAUNCH_CHECK();
+  return SA_OK;
 }
 
 template <typename T>
@@ -440,9 +546,52 @@ int launch_integrate(int lag_kind, const void *survv, const void *refv, int64_t 
   const int64_t tb = ns / m;
   if (l_count == 0 || m == 0) return SA_OK;
   const bool exact_lag = lag_kind == SA_LAG_EXACT;
-  const bool fast = mode == SA_NDFT_FAST && tb % 8 == 0 && tb <= 8192 && m <= 0x7fffffff;
+  int dev = 0, sms = 148, smem_max = 0;
+  SA_CUDA_TRY(cudaGetDevice(&dev));
+  SA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  SA_CUDA_TRY(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const size_t smax = (size_t)smem_max;
+  const bool tiles_ok = mode == SA_NDFT_FAST && tb % 8 == 0 && tb <= 0x3fffffff && m <= 0x7fffffff;
+
+  // fast mode, complex64, T % 16 == 0: packed pair kernel.  NT is the largest of
+  // 8/4/2/1 that leaves >= 3 waves of 2 CTAs per SM and fits shared memory.
+  if (tiles_ok && sizeof(T) == 4 && tb % 16 == 0) {
+    const int h = (int)tb / 2;
+    int nt = 8;
+    while (nt > 1 && ((l_count + L2_LPC * nt - 1) / (L2_LPC * nt) * m < 3 * 2 * (int64_t)sms ||
+                      Lag2Smem::bytes(h, h + nt * L2_LPC - 1) > smax))
+      nt >>= 1;
+    if (Lag2Smem::bytes(h, h + nt * L2_LPC - 1) <= smax) switch (nt) {
+        case 8: return launch_lag2<8>(exact_lag, surv, ref, ref_len, l0, l_count, m, tb, conj, z, s);
+        case 4: return launch_lag2<4>(exact_lag, surv, ref, ref_len, l0, l_count, m, tb, conj, z, s);
+        case 2: return launch_lag2<2>(exact_lag, surv, ref, ref_len, l0, l_count, m, tb, conj, z, s);
+        default: return launch_lag2<1>(exact_lag, surv, ref, ref_len, l0, l_count, m, tb, conj, z, s);
+      }
+  }
+  // fast mode, T % 8 == 0: scalar lag tiles, NT as above (1 CTA per SM when
+  // the complex128 block + window take > 113 KB)
+  auto fast_bytes = [&](int nt) {
+    return sizeof(C4<T>) * ((size_t)pad8((int)tb) + 1 + pad8((int)(tb + nt * LAGS_PER_CTA - 1)) + 1);
+  };
+  if (tiles_ok && fast_bytes(1) <= smax) {
+    int nt = 8;
+    while (nt > 1) {
+      const size_t b = fast_bytes(nt);
+      const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(2, (int64_t)(228 * 1024) / (int64_t)(b + 1024)));
+      if (b <= smax && (l_count + LAGS_PER_CTA * nt - 1) / (LAGS_PER_CTA * nt) * m >= 3 * per_sm * sms) break;
+      nt >>= 1;
+    }
+    switch (nt) {
+      case 8: return launch_lag_fast<T, 8>(exact_lag, surv, ref, ref_len, l0, l_count, m, tb, conj, z, fast_bytes(8), s);
+      case 4: return launch_lag_fast<T, 4>(exact_lag, surv, ref, ref_len, l0, l_count, m, tb, conj, z, fast_bytes(4), s);
+      case 2: return launch_lag_fast<T, 2>(exact_lag, surv, ref, ref_len, l0, l_count, m, tb, conj, z, fast_bytes(2), s);
+      default: return launch_lag_fast<T, 1>(exact_lag, surv, ref, ref_len, l0, l_count, m, tb, conj, z, fast_bytes(1), s);
+    }
+  }
+  // sequential order (exact mode, or fast mode when no tile shape fits): smem
+  // tiles when the block + window fit, else one thread per (lag, block)
   const size_t seq_bytes = sizeof(C4<T>) * (size_t)(2 * tb + LAGS_EXACT - 1);
-  if (!fast && tb >= 8 && seq_bytes <= 200 * 1024 && m <= 0x7fffffff) {
+  if (tb >= 8 && tb <= 0x3fffffff && seq_bytes <= smax && m <= 0x7fffffff) {
     auto kern = exact_lag ? k_lag_integrate_seq<T, true> : k_lag_integrate_seq<T, false>;
     SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)seq_bytes));
     const int64_t lt = (l_count + LAGS_EXACT - 1) / LAGS_EXACT;
@@ -455,41 +604,9 @@ int launch_integrate(int lag_kind, const void *survv, const void *refv, int64_t 
     SA_LAUNCH_CHECK();
     return SA_OK;
   }
-  if (!fast) {
-    int64_t tot = l_count * m;
-    auto kern = lag_kind == SA_LAG_EXACT ? k_lag_integrate_exact<T, true> : k_lag_integrate_exact<T, false>;
-    kern<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(surv, ref, ref_len, l0, l_count, m, tb, conj != 0, z);
-    SA_LAUNCH_CHECK();
-    return SA_OK;
-  }
-  int64_t ltiles = (l_count + LAGS_PER_CTA - 1) / LAGS_PER_CTA;
-  if (sizeof(T) == 4 && tb % 16 == 0) {
-    const int h = (int)tb / 2, hw = h + L2_LPC - 1;
-    ltiles = (l_count + L2_LPC - 1) / L2_LPC;
-    size_t bytes = 2 * sizeof(float4) * ((size_t)pad8(h) + 1 + pad8(hw) + 1);
-    auto k2 = exact_lag ? k_lag_integrate_f32x2<true> : k_lag_integrate_f32x2<false>;
-    SA_CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    for (int64_t t0 = 0; t0 < ltiles; t0 += 65535) {
-      int64_t nt = std::min<int64_t>(65535, ltiles - t0);
-      dim3 grid((unsigned)m, (unsigned)nt);
-      k2<<<grid, 256, bytes, s>>>(
-          (const float2 *)surv, (const float2 *)ref, ref_len, l0 + t0 * L2_LPC,
-          l_count - t0 * L2_LPC, m, (int)tb, conj != 0, (float2 *)(z + t0 * L2_LPC * m));
-    }
-    SA_LAUNCH_CHECK();
-    return SA_OK;
-  }
-  const int win = (int)tb + LAGS_PER_CTA - 1;
-  size_t bytes = sizeof(C4<T>) * ((size_t)pad8((int)tb) + 1 + pad8(win) + 1);
-  auto kern = exact_lag ? k_lag_integrate_fast<T, true> : k_lag_integrate_fast<T, false>;
-  SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  for (int64_t t0 = 0; t0 < ltiles; t0 += 65535) {
-    int64_t nt = std::min<int64_t>(65535, ltiles - t0);
-    dim3 grid((unsigned)m, (unsigned)nt);
-    kern<<<grid, 256, bytes, s>>>(surv, ref, ref_len, l0 + t0 * LAGS_PER_CTA,
-                                  l_count - t0 * LAGS_PER_CTA, m, (int)tb, conj != 0,
-                                  z + t0 * LAGS_PER_CTA * m);
-  }
+  const int64_t tot = l_count * m;
+  auto kern = exact_lag ? k_lag_integrate_exact<T, true> : k_lag_integrate_exact<T, false>;
+  kern<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(surv, ref, ref_len, l0, l_count, m, tb, conj != 0, z);
   SA_LAUNCH_CHECK();
   return SA_OK;
 }

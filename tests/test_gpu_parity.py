@@ -433,6 +433,26 @@ def test_map_exact_seq_tiles(sa, dt, lag, tb):
     assert_value_equal(y, want)
 
 
+@pytest.mark.parametrize("dt,tb", [("c64", 8192), ("c64", 6000), ("c128", 4096), ("c128", 16384)])
+def test_map_large_block_lengths(sa, dt, tb):
+    """Block lengths whose lag tiles exceed shared memory at some tiling: the
+    launcher steps NT down, then to the scalar tiles, then to the sequential
+    kernels -- fast mode stays within tolerance of the oracle, exact mode value-equal."""
+    g = np.random.default_rng(1700 + tb)
+    m = 4
+    ns = tb * m
+    cdt = np.complex64 if dt == "c64" else np.complex128
+    surv = (g.standard_normal(ns) + 1j * g.standard_normal(ns)).astype(cdt)
+    ref = np.exp(2j * np.pi * g.random(ns)).astype(cdt)
+    l0, L = 2, 130
+    f = "f32" if dt == "c64" else "f64"
+    y = sa.ambiguity_map(dev(surv), dev(ref), L, m, l0=l0).cpu().numpy()
+    assert_literal(y, oracle.ambiguity_map(surv.astype(np.complex128), ref.astype(np.complex128), l0, L, m,
+                                           nthreads=8), TOL_F32 if dt == "c64" else TOL_F64)
+    ye = sa.ambiguity_map(dev(surv), dev(ref), L, m, l0=l0, mode="exact").cpu().numpy()
+    assert_value_equal(ye, oracle.ambiguity_map(surv, ref, l0, L, m, dtype=f, nthreads=8))
+
+
 # --- exact-multiply variants (SURVEY §8(f)-2) --------------------------------------
 
 @pytest.mark.parametrize("n", [2, 4, 8, 64, 512, 4096])
