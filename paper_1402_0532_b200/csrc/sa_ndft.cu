@@ -238,6 +238,9 @@ using F2 = F2Cfg<SA_F2_TP, SA_F2_TK, SA_F2_NC>;  // default: 128 vectors x 64 bi
 #ifndef SA_F2_MINB
 #define SA_F2_MINB 2
 #endif
+#ifndef SA_F2_CHAIN  // chained twiddle offsets in exact mode (-D SA_F2_CHAIN=0 for A/B)
+#define SA_F2_CHAIN 1
+#endif
 template <bool POW2, bool TW_SMEM, bool EX>
 __global__ void __launch_bounds__(NDFT_THREADS, SA_F2_MINB)
     k_ndft_fast_f32x2(const float2 *__restrict__ x, float2 *__restrict__ y, int64_t batch, int n,
@@ -294,14 +297,22 @@ __global__ void __launch_bounds__(NDFT_THREADS, SA_F2_MINB)
   for (int kk = 0; kk < TK; ++kk)
 #pragma unroll
     for (int i = 0; i < TP; ++i) accr[kk][i] = acci[kk][i] = 0ull;
-  // twiddle byte offsets (k*m mod n) * 16 for the current m, stepped by k*16
+  const int nb = n * (int)sizeof(float4);
+  // Twiddle byte offsets (k*m mod n) * 16.  Fast mode keeps one per bin, each
+  // stepped by k*16 per sample, so the twiddle loads' addresses are ready a
+  // sample ahead (21.8 ms at C2).  Exact mode keeps two -- off0 for k = kbase
+  // and m16 = (m mod n)*16 -- and forms bin kbase+kk by a chain of kk adds: the
+  // per-bin table spilled its 12-op-per-⊙ loop (37.0 -> 27.7 ms at C2), while
+  // the chain costs fast mode 2 ms.
+  constexpr bool CHAIN = EX && SA_F2_CHAIN;
   int off[TK], kst[TK];
 #pragma unroll
   for (int kk = 0; kk < TK; ++kk) {
     off[kk] = 0;
-    kst[kk] = ((kbase + kk) % n) * (int)sizeof(float4);
+    kst[kk] = CHAIN ? 0 : ((kbase + kk) % n) * (int)sizeof(float4);
   }
-  const int nb = n * (int)sizeof(float4);
+  int off0 = 0, m16 = 0;
+  const int kst0 = (kbase % n) * (int)sizeof(float4);
   const int nchunks = (n + NCH - 1) / NCH;
   float2 pre[PER_T][2];
   ld_chunk(0, pre);
@@ -326,6 +337,28 @@ __global__ void __launch_bounds__(NDFT_THREADS, SA_F2_MINB)
         si[i] = A::pack(b.z, b.w);
       }
       float4 w[TK];
+      if constexpr (CHAIN) {
+        int o = off0;
+#pragma unroll
+        for (int kk = 0; kk < TK; ++kk) {
+          w[kk] = TW_SMEM ? *reinterpret_cast<const float4 *>(twb + o)
+                          : __ldg(reinterpret_cast<const float4 *>(
+                                reinterpret_cast<const unsigned char *>(quad) + o));
+          o += m16;
+          if (POW2) o &= nb - 1;
+          else o = o >= nb ? o - nb : o;
+        }
+        int nx = off0 + kst0, nm = m16 + (int)sizeof(float4);
+        if (POW2) {
+          nx &= nb - 1;
+          nm &= nb - 1;
+        } else {
+          nx = nx >= nb ? nx - nb : nx;
+          nm = nm >= nb ? nm - nb : nm;
+        }
+        off0 = nx;
+        m16 = nm;
+      } else {
 #pragma unroll
       for (int kk = 0; kk < TK; ++kk) {
         w[kk] = TW_SMEM ? *reinterpret_cast<const float4 *>(twb + off[kk])
@@ -335,6 +368,7 @@ __global__ void __launch_bounds__(NDFT_THREADS, SA_F2_MINB)
         if (POW2) nx &= nb - 1;
         else nx = nx >= nb ? nx - nb : nx;
         off[kk] = nx;
+      }
       }
       // Operand order for the register-reuse cache: consecutive FFMA2 share the
       // data pair (slot a) and differ in twiddle scalar and accumulator, so each
