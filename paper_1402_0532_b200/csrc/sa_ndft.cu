@@ -219,6 +219,9 @@ __global__ void __launch_bounds__(NDFT_THREADS, sizeof(T) == 8 ? SA_D_MINB : 1)
 // ⊙-accumulate lane-ops of the scalar kernel's 32 FFMA), halving issue slots so
 // the FMA pipe, not instruction issue/dispatch, is the limit.  smem chunk layout
 // per (m, pair p): D0 = {xr_a, xr_b, xi_a, xi_b}, D1 = {sxr_a, sxr_b, sxi_a, sxi_b}.
+#ifndef SA_F2_CPA  // stage chunks by cp.async into a raw smem ring (-D SA_F2_CPA=0 for A/B)
+#define SA_F2_CPA 1
+#endif
 template <int TP_, int TK_, int NC_> struct F2Cfg {
   static constexpr int TP = TP_;  // vector pairs per lane
   static constexpr int TK = TK_;  // bins per thread
@@ -226,7 +229,8 @@ template <int TP_, int TK_, int NC_> struct F2Cfg {
   static constexpr int BP = 32 * TP;            // pairs per CTA
   static constexpr int BV = 2 * BP;             // vectors per CTA
   static constexpr int BK = NDFT_WARPS * TK;    // bins per CTA
-  static constexpr size_t STAGE_BYTES = 2 * 2 * NCH * BP * sizeof(float4);
+  static constexpr size_t STAGE_BYTES =
+      2 * 2 * NCH * BP * sizeof(float4) + (SA_F2_CPA ? 2 * BV * NCH * sizeof(float2) : 0);
 };
 #ifndef SA_F2_TP  // tile shape (vector pairs per lane, bins per thread, chunk); -D for sweeps
 #define SA_F2_TP 2
@@ -252,7 +256,8 @@ __global__ void __launch_bounds__(NDFT_THREADS, SA_F2_MINB)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float4 *d0 = reinterpret_cast<float4 *>(smem_raw);  // [2][NCH][BP] {xr_a, xr_b, xi_a, xi_b}
   float4 *d1 = d0 + 2 * NCH * BP;                      // [2][NCH][BP] signs
-  float4 *tws = d1 + 2 * NCH * BP;                     // [n] (TW_SMEM)
+  float2 *raw = reinterpret_cast<float2 *>(d1 + 2 * NCH * BP);  // [2][NCH][BV] (SA_F2_CPA)
+  float4 *tws = SA_F2_CPA ? reinterpret_cast<float4 *>(raw + 2 * BV * NCH) : d1 + 2 * NCH * BP;  // [n]
   const unsigned char *twb = reinterpret_cast<const unsigned char *>(tws);
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -314,13 +319,68 @@ __global__ void __launch_bounds__(NDFT_THREADS, SA_F2_MINB)
   int off0 = 0, m16 = 0;
   const int kst0 = (kbase % n) * (int)sizeof(float4);
   const int nchunks = (n + NCH - 1) / NCH;
+  // Fast mode stages by cp.async (21.8 -> 21.5 ms at C2); exact mode keeps the
+  // register prefetch (27.7 vs 27.9 ms).
+  constexpr bool CPA = SA_F2_CPA && !EX;
   float2 pre[PER_T][2];
-  ld_chunk(0, pre);
-  st_chunk(0, pre);
+  // cp.async ring: each thread copies, then converts, its own (pair, sample
+  // pair) entries, so only the chunk barrier orders the smem traffic.  Chunk j
+  // lands in raw[j & 1] two chunks ahead of use; no prefetch registers.
+  constexpr int PER_C = BP * NCH / 2 / NDFT_THREADS;  // (pair, sample pair) items per thread
+  static_assert(NCH % 2 == 0 && BP * NCH / 2 % NDFT_THREADS == 0, "cp.async staging tiles");
+  auto issue = [&](int j) {
+    if (j < nchunks) {
+      const int m0 = j * NCH, rb = j & 1;
+#pragma unroll
+      for (int q = 0; q < PER_C; ++q) {
+        const int e = threadIdx.x + q * NDFT_THREADS, p = e % BP, sp = e / BP;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t gv = v0 + 2 * p + h;
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            const int m = m0 + 2 * sp + t;
+            const bool ok = gv < batch && m < n;
+            sa_cp_async8(&raw[(rb * NCH + 2 * sp + t) * BV + 2 * p + h], ok ? x + gv * n + m : x, ok ? 8 : 0);
+          }
+        }
+      }
+    }
+    sa_cp_async_commit();
+  };
+  auto convert = [&](int j) {
+    const int rb = j & 1;
+#pragma unroll
+    for (int q = 0; q < PER_C; ++q) {
+      const int e = threadIdx.x + q * NDFT_THREADS, p = e % BP, sp = e / BP;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int mm = 2 * sp + t;
+        const float4 ab = reinterpret_cast<const float4 *>(raw)[((rb * NCH + mm) * BV + 2 * p) / 2];
+        float2 a = {ab.x, ab.y}, b = {ab.z, ab.w};
+        if (use_gain) {
+          a = {sa_mul(gain, a.x), sa_mul(gain, a.y)};
+          b = {sa_mul(gain, b.x), sa_mul(gain, b.y)};
+        }
+        d0[(rb * NCH + mm) * BP + p] = {a.x, b.x, a.y, b.y};
+        d1[(rb * NCH + mm) * BP + p] = {sa_sgn(a.x), sa_sgn(b.x), sa_sgn(a.y), sa_sgn(b.y)};
+      }
+    }
+  };
+  if constexpr (CPA) {
+    issue(0);
+    issue(1);
+    sa_cp_async_wait<1>();
+    convert(0);
+  } else {
+    ld_chunk(0, pre);
+    st_chunk(0, pre);
+  }
   __syncthreads();
   for (int c = 0; c < nchunks; ++c) {
     const int buf = c & 1;
-    if (c + 1 < nchunks) ld_chunk((c + 1) * NCH, pre);
+    if constexpr (CPA) issue(c + 2);  // into raw[c & 1], converted by this thread last iteration
+    else if (c + 1 < nchunks) ld_chunk((c + 1) * NCH, pre);
     const float4 *c0 = d0 + buf * NCH * BP;
     const float4 *c1 = d1 + buf * NCH * BP;
     const int mlim = min(NCH, n - c * NCH);
@@ -415,7 +475,14 @@ __global__ void __launch_bounds__(NDFT_THREADS, SA_F2_MINB)
         }
       }
     }
-    if (c + 1 < nchunks) st_chunk(buf ^ 1, pre);
+    if (c + 1 < nchunks) {
+      if constexpr (CPA) {
+        sa_cp_async_wait<1>();  // chunk c+1 landed (c+2 may still be in flight)
+        convert(c + 1);
+      } else {
+        st_chunk(buf ^ 1, pre);
+      }
+    }
     __syncthreads();
   }
 #pragma unroll

@@ -264,3 +264,13 @@ SA_HD void sa_mbar_arrive_remote(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
+
+// cp.async (LDGSTS): global -> shared without a register round trip.
+// src_bytes < 8 zero-fills the rest of the 8-byte destination.
+SA_HD void sa_cp_async8(void *smem, const void *gmem, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa_smem_u32(smem)), "l"(gmem),
+               "r"(src_bytes)
+               : "memory");
+}
+SA_HD void sa_cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> SA_HD void sa_cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
