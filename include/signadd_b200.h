@@ -200,6 +200,51 @@ int sa_enable_peer_access(int peer_device);
 int sa_ipc_open(const void *handle64, void **dptr);
 int sa_ipc_close(void *dptr);
 
+/* --- scene synthesis (radar.py) ----------------------------
+ * Device versions of the reference's signal builders for CPI-scale inputs.
+ * Random draws are the caller's (the reference's numpy streams, uploaded);
+ * every arithmetic step follows numpy's evaluation order, so the outputs
+ * agree with the reference up to the device sin/cos (an ulp or two).  All
+ * buffers are device memory; work is stream-ordered. */
+enum sa_noise_kind {
+  SA_NOISE_NONE = 0, /* NoiseKind.NONE                                   */
+  SA_NOISE_AWGN = 1, /* add_awgn (radar.py:245-256)                      */
+  SA_NOISE_EPS = 2   /* add_contaminated (radar.py:259-267)              */
+};
+
+/* gen_stereo_fm (radar.py:179-192).  u = the 2 x n draws of
+ * default_rng(seed).uniform(-1, 1, (2, n)) (doubles, row-major).  The constant
+ * factors are the reference's Python scalars: ca = 2*pi*2*f_p, cb = 2*pi*3*f_p,
+ * cc = 2*pi*f_p (each left to right), ck = 2*pi*k_f.  out: n complex (dtype
+ * SA_C128 or SA_C64, cast on store) = (cos phase, sin phase). */
+int sa_scene_stereo_fm(int dtype, const double *u, int64_t n, double f_s, double ca, double cb, double cc,
+                       double ck, void *out, void *stream);
+
+/* The echo mixture of synth_surveillance (radar.py:215-243), before noise and
+ * gain: out[i] = sum over echoes k, in order from +0, of
+ * amp_k * ref[i - delay_k] (0 for i < delay_k) * exp(j (w_k i) / f_s).
+ * ref, out: d complex128.  Host arrays: delays[ne], amps[2 ne] (re, im),
+ * w[ne] = 2*pi*doppler_hz (0 for clutter: no Doppler factor, as the
+ * reference's doppler_hz == 0 branch), inv_fs = 1 / f_s (numpy divides by the
+ * reciprocal).  1 <= ne <= 64. */
+int sa_scene_echoes(const void *ref, int64_t d, int ne, const int64_t *delays, const double *amps,
+                    const double *w, double inv_fs, void *out, void *stream);
+
+/* sum over i of |x_i|^2 (numpy's complex abs, squared) for add_awgn's signal
+ * power: x = d complex128; *sum (device double).  workspace >=
+ * sa_scene_power_workspace_bytes(d) bytes of device memory. */
+int sa_scene_power_workspace_bytes(int64_t d, int64_t *bytes);
+int sa_scene_power(const void *x, int64_t d, double *sum, void *workspace, int64_t ws_bytes, void *stream);
+
+/* apply_noise + the surveillance gain (radar.py:243,245-275):
+ * out = (x + noise) * gain with noise = z * scale (SA_NOISE_AWGN; z = the
+ * 2 x d normals of default_rng(seed).standard_normal, scale =
+ * sqrt(p_noise / 2) as the reference computes it), z * (u < eps ? s1 : s2)
+ * (SA_NOISE_EPS; u = the 2 x d draws of .random, then z from the same
+ * generator), or none.  x: d complex128; out: dtype SA_C128 or SA_C64. */
+int sa_scene_noise_gain(int dtype, const void *x, int64_t d, int kind, const double *z, const double *u,
+                        double scale, double eps, double s1, double s2, double gain, void *out, void *stream);
+
 /* FMA-pipe peak microbenchmark (roofline denominator): `blocks` CTAs x 256
  * (dtype 2 = packed fp32x2 FFMA2)
  * threads each run `iters` iterations of 8 independent FMA chains; writes a

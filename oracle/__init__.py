@@ -38,6 +38,8 @@ __all__ = [
     "fft_exact",
     "lag_product_exact",
     "abs_np",
+    "scene_stereo_fm",
+    "scene_surveillance",
     "find_peaks",
     "map_floor",
 ]
@@ -268,3 +270,57 @@ def map_floor(values, centers, guard, dtype: str = "f64") -> tuple[float, float,
     getattr(_load(), f"or_map_floor_{dtype}")(v.shape[0], v.shape[1], v.ctypes.data, c.ctypes.data,
                                                c.shape[0], int(guard[0]), int(guard[1]), out.ctypes.data)
     return float(out[0]), float(out[1]), int(out[2])
+
+
+# --- scene synthesis: restates radar.py:179-275 ------------
+# numpy, written in the evaluation order the device kernels follow
+# (csrc/sa_scene.cu); pinned bit-for-bit against the reference's own outputs
+# in tests/test_oracle_golden.py, which is what licenses that order.
+
+def scene_stereo_fm(n: int, f_s: float, k_f: float, f_p: float, seed: int) -> np.ndarray:
+    """gen_stereo_fm (radar.py:179-192)."""
+    x1, x2 = np.random.default_rng(seed).uniform(-1.0, 1.0, size=(2, n))
+    t = np.arange(n) / f_s
+    ca, cb, cc, ck = 2.0 * np.pi * 2.0 * f_p, 2.0 * np.pi * 3.0 * f_p, 2.0 * np.pi * f_p, 2.0 * np.pi * k_f
+    m = 0.9 * (x1 + x2)
+    m = m + (0.5 * (x1 - x2)) * np.cos(ca * t)
+    m = m + 0.25 * np.cos(cb * t)
+    m = m + 0.1 * np.cos(cc * t)
+    ph = ck * m
+    out = np.empty(n, dtype=complex)
+    out.real, out.imag = np.cos(ph), np.sin(ph)
+    return out
+
+
+def scene_surveillance(ref, delays, amps, dopplers, f_s: float, noise: dict, gain: float) -> np.ndarray:
+    """synth_surveillance + apply_noise (radar.py:215-275): per obstacle
+    amplitude * shifted (* exp(j ((2 pi f) i) (1/f_s)) when f != 0), summed
+    from +0; noise from the reference's numpy streams; times the gain."""
+    ref = np.asarray(ref, dtype=complex)
+    d = ref.size
+    i = np.arange(d)
+    acc = np.zeros(d, dtype=complex)
+    for l, a, f in zip(delays, amps, dopplers):
+        sh = np.zeros(d, dtype=complex)
+        sh[l:] = ref[: d - l]
+        term = complex(a) * sh
+        if f != 0.0:
+            ph = ((2j * np.pi * f).imag * i) * (1.0 / f_s)
+            e = np.empty(d, dtype=complex)
+            e.real, e.imag = np.cos(ph), np.sin(ph)
+            term = term * e
+        acc = acc + term
+    kind = noise.get("kind", "none")
+    if kind == "awgn":
+        p_sig = float(np.mean(np.abs(acc) ** 2))
+        scale = np.sqrt(p_sig / 10.0 ** (noise["snr_db"] / 10.0) / 2.0)
+        z = np.random.default_rng(noise["seed"]).standard_normal((2, d)) * scale
+        acc = (acc.real + z[0]) + 1j * (acc.imag + z[1])
+    elif kind == "eps_contaminated":
+        rng = np.random.default_rng(noise["seed"])
+        sig = np.where(rng.random((2, d)) < noise["eps"], noise["sigma1"], noise["sigma2"])
+        z = rng.standard_normal((2, d)) * sig
+        acc = (acc.real + z[0]) + 1j * (acc.imag + z[1])
+    out = np.empty(d, dtype=complex)
+    out.real, out.imag = acc.real * gain, acc.imag * gain
+    return out

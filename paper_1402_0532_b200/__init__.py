@@ -46,6 +46,7 @@ from .ambiguity import (
     lag_product_mf,
     map_complex_ops,
 )
+from . import scene
 from .detection import Peak, ambiguity_peaks, classify_bins, find_peaks, map_peaks, sidelobe_floor_db
 
 

@@ -22,6 +22,7 @@ SA_NDFT_FAST, SA_NDFT_EXACT = 0, 1
 SA_DIT, SA_DIF, SA_FFT_EXACT = 0, 1, 2
 SA_LAG_MF, SA_LAG_EXACT = 0, 1
 SA_DOPPLER_NLFFT, SA_DOPPLER_NDFT, SA_DOPPLER_FFT_EXACT = 0, 1, 2
+SA_NOISE_NONE, SA_NOISE_AWGN, SA_NOISE_EPS = 0, 1, 2
 
 SA_OK, SA_ERR_ARG, SA_ERR_CONTRACT, SA_ERR_DOMAIN, SA_ERR_CUDA, SA_ERR_UNSUPPORTED = 0, -1, -2, -3, -4, -5
 
@@ -53,6 +54,11 @@ SIGNATURES = {
     "sa_enable_peer_access": (_I, [_I]),
     "sa_ipc_open": (_I, [_P, ctypes.POINTER(_P)]),
     "sa_ipc_close": (_I, [_P]),
+    "sa_scene_stereo_fm": (_I, [_I, _P, _I64, _D, _D, _D, _D, _D, _P, _P]),
+    "sa_scene_echoes": (_I, [_P, _I64, _I, _P, _P, _P, _D, _P, _P]),
+    "sa_scene_power_workspace_bytes": (_I, [_I64, ctypes.POINTER(_I64)]),
+    "sa_scene_power": (_I, [_P, _I64, _P, _P, _I64, _P]),
+    "sa_scene_noise_gain": (_I, [_I, _P, _I64, _I, _P, _P, _D, _D, _D, _D, _D, _P, _P]),
     "sa_fma_peak": (_I, [_I, _I64, _P, _I, _P]),
 }
 

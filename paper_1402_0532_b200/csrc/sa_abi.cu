@@ -271,6 +271,50 @@ int sa_map_floor(int dtype, const void *map, int64_t rows, int64_t cols, const i
                              (cudaStream_t)stream);
 }
 
+int sa_scene_stereo_fm(int dtype, const double *u, int64_t n, double f_s, double ca, double cb, double cc,
+                       double ck, void *out, void *stream) {
+  SA_REQUIRE(dtype_ok(dtype), SA_ERR_ARG, "bad dtype %d", dtype);
+  SA_REQUIRE(n >= 0, SA_ERR_ARG, "negative length");
+  SA_REQUIRE(n == 0 || (u && out), SA_ERR_ARG, "null pointer");
+  SA_REQUIRE(f_s > 0.0, SA_ERR_CONTRACT, "gen_stereo_fm: f_s must be positive");
+  return sa_launch_stereo_fm(dtype, u, n, f_s, ca, cb, cc, ck, out, (cudaStream_t)stream);
+}
+
+int sa_scene_echoes(const void *ref, int64_t d, int ne, const int64_t *delays, const double *amps,
+                    const double *w, double inv_fs, void *out, void *stream) {
+  SA_REQUIRE(ne >= 1, SA_ERR_CONTRACT, "synth_surveillance: need at least one obstacle");
+  SA_REQUIRE(ne <= 64, SA_ERR_UNSUPPORTED, "synth_surveillance: %d obstacles > 64", ne);
+  SA_REQUIRE(d >= 0, SA_ERR_ARG, "negative length");
+  SA_REQUIRE(delays && amps && w && (d == 0 || (ref && out)), SA_ERR_ARG, "null pointer");
+  for (int k = 0; k < ne; ++k) SA_REQUIRE(delays[k] >= 0, SA_ERR_CONTRACT, "negative delay");
+  return sa_launch_echoes(ref, d, ne, delays, amps, w, inv_fs, out, (cudaStream_t)stream);
+}
+
+int sa_scene_power_workspace_bytes(int64_t d, int64_t *bytes) {
+  SA_REQUIRE(bytes && d >= 0, SA_ERR_ARG, "bad arguments");
+  *bytes = sa_power_ws_bytes(d);
+  return SA_OK;
+}
+
+int sa_scene_power(const void *x, int64_t d, double *sum, void *workspace, int64_t ws_bytes, void *stream) {
+  SA_REQUIRE(d >= 1, SA_ERR_CONTRACT, "add_awgn: empty input");
+  SA_REQUIRE(x && sum && workspace, SA_ERR_ARG, "null pointer");
+  SA_REQUIRE(ws_bytes >= sa_power_ws_bytes(d), SA_ERR_ARG, "workspace too small");
+  return sa_launch_power(x, d, (double *)workspace, sum, (cudaStream_t)stream);
+}
+
+int sa_scene_noise_gain(int dtype, const void *x, int64_t d, int kind, const double *z, const double *u,
+                        double scale, double eps, double s1, double s2, double gain, void *out, void *stream) {
+  SA_REQUIRE(dtype_ok(dtype), SA_ERR_ARG, "bad dtype %d", dtype);
+  SA_REQUIRE(kind == SA_NOISE_NONE || kind == SA_NOISE_AWGN || kind == SA_NOISE_EPS, SA_ERR_ARG,
+             "bad noise kind %d", kind);
+  SA_REQUIRE(d >= 0, SA_ERR_ARG, "negative length");
+  SA_REQUIRE(d == 0 || (x && out), SA_ERR_ARG, "null pointer");
+  SA_REQUIRE(kind == SA_NOISE_NONE || z, SA_ERR_ARG, "null noise draws");
+  SA_REQUIRE(kind != SA_NOISE_EPS || u, SA_ERR_ARG, "null mixture draws");
+  return sa_launch_noise_gain(dtype, x, d, kind, z, u, scale, eps, s1, s2, gain, out, (cudaStream_t)stream);
+}
+
 int sa_enable_peer_access(int peer_device) {
   int dev = 0, n = 0, ok = 0;
   SA_CUDA_TRY(cudaGetDevice(&dev));

@@ -13,6 +13,7 @@
 // zeros may differ).
 #pragma once
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdint.h>
 
 #define SA_HD __device__ __forceinline__
@@ -76,6 +77,20 @@ template <typename T> SA_HD void sa_mfc_literal(T ar, T ai, T br, T bi, T &rr, T
 template <typename T> SA_HD void sa_np_complex(T rr, T ri, T &re, T &im) {
   re = sa_add(rr, sa_sub(sa_mul(T(0), ri), T(0)));
   im = sa_add(ri, T(0));
+}
+
+// numpy's complex absolute value on the reference host (SIMD loop, verified
+// bit-exact in tests/golden/make_golden.py): L = max(|re|,|im|), S = min,
+// r = S/L (0 when L == 0), |v| = sqrt(fma(r, r, 1)) * L.
+template <typename T> SA_HD T np_cabs(T re, T im) {
+  re = fabs(re);
+  im = fabs(im);
+  const T inf = T(INFINITY);
+  if (re == inf || im == inf) return inf;
+  if (re != re || im != im) return T(NAN);
+  const T L = re > im ? re : im, S = re > im ? im : re;
+  const T r = (L == T(0)) ? T(0) : S / L;
+  return sqrt(fma(r, r, T(1))) * L;
 }
 
 // numpy complex multiply a*b as the reference host's SIMD loop computes it

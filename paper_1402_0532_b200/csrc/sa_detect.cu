@@ -48,16 +48,6 @@ SA_HD Cand sentinel() { return {-1.0, LLONG_MAX}; }
 // strongest first; equal magnitudes in row-major order
 SA_HD bool better(const Cand &a, const Cand &b) { return a.mag > b.mag || (a.mag == b.mag && a.idx < b.idx); }
 
-template <typename T> SA_HD T np_cabs(T re, T im) {
-  re = fabs(re);
-  im = fabs(im);
-  const T inf = T(INFINITY);
-  if (re == inf || im == inf) return inf;
-  if (re != re || im != im) return T(NAN);
-  const T L = re > im ? re : im, S = re > im ? im : re;
-  const T r = (L == T(0)) ? T(0) : S / L;
-  return sqrt(fma(r, r, T(1))) * L;
-}
 
 template <typename T>
 __global__ void __launch_bounds__(TILE_THREADS) k_peaks_tile(const C2<T> *__restrict__ map, int64_t rows,

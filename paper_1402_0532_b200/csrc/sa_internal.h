@@ -73,6 +73,14 @@ int sa_launch_map_peaks(int dtype, const void *map, int64_t rows, int64_t cols, 
                         int *count, void *ws, cudaStream_t s);
 int sa_launch_map_floor(int dtype, const void *map, int64_t rows, int64_t cols, const int *centers, int ncent,
                         int g0, int g1, unsigned long long *out, cudaStream_t s);
+int sa_launch_stereo_fm(int dtype, const double *u, int64_t n, double f_s, double ca, double cb, double cc,
+                        double ck, void *out, cudaStream_t s);
+int sa_launch_echoes(const void *ref, int64_t d, int ne, const int64_t *delays, const double *amps, const double *w,
+                     double inv_fs, void *out, cudaStream_t s);
+int64_t sa_power_ws_bytes(int64_t d);
+int sa_launch_power(const void *x, int64_t d, double *ws, double *sum, cudaStream_t s);
+int sa_launch_noise_gain(int dtype, const void *x, int64_t d, int kind, const double *z, const double *u, double scale,
+                         double eps, double s1, double s2, double gain, void *out, cudaStream_t s);
 int sa_launch_lag_product(int dtype, int lag_kind, const void *surv, const void *ref, int64_t n, int64_t ref_len,
                           int64_t lag, int conj, void *out, cudaStream_t s);
 int sa_launch_lag_integrate(int dtype, int lag_kind, const void *surv, const void *ref, int64_t ns,

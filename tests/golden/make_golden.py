@@ -225,6 +225,38 @@ def main() -> None:
     for gd in ((1, 1), (2, 2), (3, 5)):
         g[f"det_scn_floor_{gd[0]}_{gd[1]}"] = np.array(det.sidelobe_floor_db(sf, scn, gd))
 
+    # --- scene synthesis (radar.py) -----------------------------
+    from signadd import radar
+    scenes = {
+        "awgn_2t1c": radar.two_targets_one_clutter(
+            noise=radar.NoiseModel(kind="awgn", snr_db=-12.0, seed=31), seed=5, n=1024, l_bins=64),
+        "eps_4t2c": radar.four_targets_two_clutters(
+            noise=radar.NoiseModel(kind="eps_contaminated", eps=0.8, sigma1=0.3, sigma2=4.0, seed=7),
+            seed=9, n=2048, l_bins=64),
+        "none_custom": radar.Scenario(
+            tx_km=(0.0, 10.0), rx_km=(0.0, 0.0),
+            obstacles=(radar.Obstacle(10.0, 0.0, doppler_hz=-333.25, amplitude=0.3 - 0.2j),
+                       radar.Obstacle(3.0, 4.0, doppler_hz=12.5, amplitude=-1.5 + 0.75j),
+                       radar.Obstacle(28.0, 33.0, doppler_hz=0.0, amplitude=0.5j)),
+            fm=radar.StereoFmConfig(duration_samples=4096 + 100, seed=13, k_f=0.6),
+            n=4096, l_bins=64, surv_gain=3.0),
+    }
+    for name, scn in scenes.items():
+        s_ref, s_surv = radar.build_signals(scn)
+        g[f"scn_{name}_ref"] = s_ref.samples
+        g[f"scn_{name}_surv"] = s_surv.samples
+        g[f"scn_{name}_delays"] = np.array(scn.delay_bins())
+        g[f"scn_{name}_amps"] = np.array([complex(o.amplitude) for o in scn.obstacles])
+        g[f"scn_{name}_dopp"] = np.array([o.doppler_hz for o in scn.obstacles])
+        g[f"scn_{name}_geom"] = np.array([[o.x_km, o.y_km] for o in scn.obstacles])
+        g[f"scn_{name}_txrx"] = np.array([scn.tx_km, scn.rx_km])
+        nz = scn.noise
+        g[f"scn_{name}_noise"] = np.array([str(nz.kind.value), repr(nz.snr_db), repr(nz.eps), repr(nz.sigma1),
+                                           repr(nz.sigma2), str(nz.seed)])
+        fm = scn.fm
+        g[f"scn_{name}_fm"] = np.array([fm.f_s, fm.duration_samples, fm.k_f, fm.f_p, fm.seed], dtype=float)
+        g[f"scn_{name}_n_gain"] = np.array([scn.n, scn.surv_gain], dtype=float)
+
     np.savez_compressed(OUT, **g)
     print("wrote", OUT, os.path.getsize(OUT), "bytes,", len(g), "arrays")
 

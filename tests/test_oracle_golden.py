@@ -190,3 +190,43 @@ def test_exact_variant_surfaces_golden(golden, var):
     got = oracle.ambiguity_map(sv, rf, 0, 6, 256, conj=False, lag="exact", doppler="nfft") if var == "eq12c" else None
     if got is not None:
         _eq(got, golden["amb_eq12c_noconj_g1"])
+
+
+# --- scene synthesis (radar.py:179-275) -------------------------
+
+SCENES = ["awgn_2t1c", "eps_4t2c", "none_custom"]
+
+
+def scene_params(golden, name):
+    """The golden scene as plain numbers (what the GPU tests rebuild it from)."""
+    f_s, dur, k_f, f_p, seed = golden[f"scn_{name}_fm"]
+    kind, snr, eps, s1, s2, nseed = [str(v) for v in golden[f"scn_{name}_noise"]]
+    noise = {"kind": kind, "snr_db": float(snr), "eps": float(eps), "sigma1": float(s1), "sigma2": float(s2),
+             "seed": int(nseed)}
+    n, gain = golden[f"scn_{name}_n_gain"]
+    return dict(f_s=float(f_s), dur=int(dur), k_f=float(k_f), f_p=float(f_p), seed=int(seed), noise=noise,
+                n=int(n), gain=float(gain), delays=[int(v) for v in golden[f"scn_{name}_delays"]],
+                amps=list(golden[f"scn_{name}_amps"]), dopp=[float(v) for v in golden[f"scn_{name}_dopp"]])
+
+
+@pytest.mark.parametrize("name", SCENES)
+def test_scene_oracle_golden(golden, name):
+    """The evaluation order the scene kernels follow reproduces the reference bit for bit on the host."""
+    p = scene_params(golden, name)
+    ref = oracle.scene_stereo_fm(p["dur"], p["f_s"], p["k_f"], p["f_p"], p["seed"])
+    _eq(ref, golden[f"scn_{name}_ref"])
+    surv = oracle.scene_surveillance(golden[f"scn_{name}_ref"], p["delays"], p["amps"], p["dopp"], p["f_s"],
+                                     p["noise"], p["gain"])
+    _eq(surv, golden[f"scn_{name}_surv"])
+
+
+@pytest.mark.parametrize("name", SCENES)
+def test_scene_delay_bins_golden(golden, name):
+    """scene.bistatic_delay_bins (host) = the reference's geometry (radar.py:195-199)."""
+    from types import SimpleNamespace
+    from paper_1402_0532_b200 import scene
+    tx, rx = golden[f"scn_{name}_txrx"]
+    f_s = float(golden[f"scn_{name}_fm"][0])
+    got = [scene.bistatic_delay_bins(tuple(tx), tuple(rx), SimpleNamespace(x_km=x, y_km=y), f_s)
+           for x, y in golden[f"scn_{name}_geom"]]
+    assert got == [int(v) for v in golden[f"scn_{name}_delays"]]
