@@ -235,6 +235,7 @@ def wl_ndft(args, ws, rank):
         hin = xh.pin_memory()
         hout = torch.empty_like(hin).pin_memory()
         res["e2e_step"] = lambda: sa.ndft_batch(hin, out=hout)
+        res["e2e_rows"], res["e2e_row_bytes"] = hin.shape[0], hin.shape[1] * hin.element_size()
         res["h2d"] = hin.numel() * hin.element_size()
         res["d2h"] = hout.numel() * hout.element_size()
     res["roofline"] = lambda ms: roof_alu(args.dtype, ops * 16 / (ms * 1e-3) / 1e12, args)
@@ -476,9 +477,10 @@ def run_ours(args):
         line["e2e"] = {"value": res["ops"] * ws / (ems * 1e-3), "unit": unit, "ms_per_step": ems,
                        "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"],
                        "api": "paper_1402_0532_b200.ndft_batch(pinned host tensor, out=pinned host tensor)",
-                       "pipeline": "H2D / transform / D2H overlapped over 16 MiB row chunks"}
-        from paper_1402_0532_b200.transforms import pipeline_chunks
-        line["gpu_launches"] += max(2, args.steps // 2) * pipeline_chunks(res["h2d"])
+                       "pipeline": "H2D / transform / D2H overlapped over row chunks (16 MiB steady, "
+                                   "halving to 2 MiB at both ends)"}
+        from paper_1402_0532_b200.transforms import pipeline_plan
+        line["gpu_launches"] += max(2, args.steps // 2) * len(pipeline_plan(res["e2e_rows"], res["e2e_row_bytes"], 128))
     # CPU baseline: rank 0, N=1 only
     if rank == 0 and ws == 1 and "cpu" in res and not args.no_cpu:
         P = len(os.sched_getaffinity(0))

@@ -243,10 +243,50 @@ def _pinned_host(t) -> bool:
 
 
 def pipeline_chunks(nbytes: int) -> int:
-    """Row chunks of a pinned-host batched call: 16 MiB each, at most 64 --
-    measured best on C2 (512 MiB each way): 22.6 ms end to end vs 21.8 ms for
-    the device-resident transform.  One transform launch per chunk."""
-    return int(max(1, min(64, nbytes // (16 << 20))))
+    """Steady-state row chunks of a pinned-host batched call: 16 MiB each, at
+    most 64 -- measured best on C2 (512 MiB each way)."""
+    return int(max(1, min(64, nbytes // (PIPELINE_MIB << 20))))
+
+
+PIPELINE_MIB = int(__import__("os").environ.get("SA_PIPELINE_MIB", "16"))
+PIPELINE_RAMP = int(__import__("os").environ.get("SA_PIPELINE_RAMP", "1"))
+
+
+def pipeline_plan(rows: int, row_bytes: int, row_align: int) -> list[tuple[int, int]]:
+    """Row ranges of a pinned-host batched call.  Steady chunks of
+    ``pipeline_chunks``' size; the first and last PIPELINE_RAMP chunks halve
+    towards the ends (16 -> 8 -> 4 -> 2 MiB), so the pipeline fills after a
+    small upload and drains after a small download.  One transform launch per
+    chunk."""
+    total = rows * row_bytes
+    step = -(-rows // pipeline_chunks(total))
+    step = -(-step // row_align) * row_align
+    ramp = []
+    for k in range(1, PIPELINE_RAMP + 1):
+        r = (step >> k) // row_align * row_align
+        if r < row_align or 2 * sum(ramp) + 2 * r > rows // 2:
+            break
+        ramp.append(r)
+    sizes_head = ramp[::-1]
+    head = sum(sizes_head)
+    tail = head
+    mid_rows = rows - head - tail
+    out, r0 = [], 0
+    for sz in sizes_head:
+        out.append((r0, r0 + sz))
+        r0 += sz
+    mid_end = r0 + mid_rows
+    nmid = max(1, -(-mid_rows // step))
+    even = -(-(-(-mid_rows // nmid)) // row_align) * row_align  # equal chunks, aligned
+    while r0 < mid_end:
+        r1 = min(mid_end, r0 + even)
+        out.append((r0, r1))
+        r0 = r1
+    for sz in ramp:
+        out.append((r0, r0 + sz))
+        r0 += sz
+    assert r0 == rows
+    return out
 
 
 def _host_pipelined(x, out, launch_rows, row_align: int, dtype):
@@ -265,10 +305,7 @@ def _host_pipelined(x, out, launch_rows, row_align: int, dtype):
         out = T.empty(xh.shape, dtype=xh.dtype, pin_memory=True)
     oh = out if out.dim() == 2 else out.view(xh.shape)
     rows, n = xh.shape
-    total = xh.numel() * xh.element_size()
-    chunks = pipeline_chunks(total)
-    step = -(-rows // chunks)
-    step = -(-step // row_align) * row_align
+    plan = pipeline_plan(rows, n * xh.element_size(), row_align)
     dev = T.cuda.current_device()
     if dev not in _SIDE_STREAMS:
         _SIDE_STREAMS[dev] = (T.cuda.Stream(), T.cuda.Stream(), T.cuda.Stream())
@@ -278,15 +315,14 @@ def _host_pipelined(x, out, launch_rows, row_align: int, dtype):
     xd = T.empty(xh.shape, dtype=xh.dtype, device="cuda")
     yd = T.empty_like(xd)
     up.wait_stream(cur)  # device buffers are fresh allocations on `cur`
-    for r0 in range(0, rows, step):
-        r1 = min(rows, r0 + step)
+    for ci, (r0, r1) in enumerate(plan):
         with T.cuda.stream(up):
             xd[r0:r1].copy_(xh[r0:r1], non_blocking=True)
             ev_in = T.cuda.Event()
             ev_in.record(up)
         # consecutive chunks alternate between two compute streams, so one
         # chunk's last wave overlaps the next chunk's first
-        ks = alt if (r0 // step) % 2 else cur
+        ks = alt if ci % 2 else cur
         ks.wait_event(ev_in)
         with T.cuda.stream(ks):
             launch_rows(xd[r0:r1], yd[r0:r1])
