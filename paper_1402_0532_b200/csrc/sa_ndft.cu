@@ -219,6 +219,13 @@ __global__ void __launch_bounds__(NDFT_THREADS, sizeof(T) == 8 ? SA_D_MINB : 1)
 // ⊙-accumulate lane-ops of the scalar kernel's 32 FFMA), halving issue slots so
 // the FMA pipe, not instruction issue/dispatch, is the limit.  smem chunk layout
 // per (m, pair p): D0 = {xr_a, xr_b, xi_a, xi_b}, D1 = {sxr_a, sxr_b, sxi_a, sxi_b}.
+// sample-loop unroll of the fp32 tile loop: fast 1 / 2 / 4 / 8 = 21.46 / 21.51 /
+// 22.04 / 21.53 ms, exact 26.99 / 27.71 / 27.37 / 26.91 ms (C2)
+#ifndef SA_F2_UNROLL_FAST
+#define SA_F2_UNROLL_FAST 1
+#define SA_F2_UNROLL_EXACT 8
+#endif
+constexpr int F2_UNR_FAST = SA_F2_UNROLL_FAST, F2_UNR_EXACT = SA_F2_UNROLL_EXACT;
 #ifndef SA_F2_CPA  // stage chunks by cp.async into a raw smem ring (-D SA_F2_CPA=0 for A/B)
 #define SA_F2_CPA 1
 #endif
@@ -310,6 +317,7 @@ __global__ void __launch_bounds__(NDFT_THREADS, SA_F2_MINB)
   // per-bin table spilled its 12-op-per-⊙ loop (37.0 -> 27.7 ms at C2), while
   // the chain costs fast mode 2 ms.
   constexpr bool CHAIN = EX && SA_F2_CHAIN;
+  constexpr int UNR = EX ? F2_UNR_EXACT : F2_UNR_FAST;
   int off[TK], kst[TK];
 #pragma unroll
   for (int kk = 0; kk < TK; ++kk) {
@@ -384,7 +392,7 @@ __global__ void __launch_bounds__(NDFT_THREADS, SA_F2_MINB)
     const float4 *c0 = d0 + buf * NCH * BP;
     const float4 *c1 = d1 + buf * NCH * BP;
     const int mlim = min(NCH, n - c * NCH);
-#pragma unroll 2
+#pragma unroll UNR
     for (int mm = 0; mm < mlim; ++mm) {
       V xr[TP], xi[TP], sr[TP], si[TP];
 #pragma unroll
