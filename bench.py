@@ -478,7 +478,7 @@ def run_ours(args):
                        "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"],
                        "api": "paper_1402_0532_b200.ndft_batch(pinned host tensor, out=pinned host tensor)",
                        "pipeline": "H2D / transform / D2H overlapped over row chunks (16 MiB steady, "
-                                   "halving to 2 MiB at both ends)"}
+                                   "8 MiB first and last)"}
         from paper_1402_0532_b200.transforms import pipeline_plan
         line["gpu_launches"] += max(2, args.steps // 2) * len(pipeline_plan(res["e2e_rows"], res["e2e_row_bytes"], 128))
     # CPU baseline: rank 0, N=1 only
