@@ -477,8 +477,8 @@ def run_ours(args):
         line["e2e"] = {"value": res["ops"] * ws / (ems * 1e-3), "unit": unit, "ms_per_step": ems,
                        "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"],
                        "api": "paper_1402_0532_b200.ndft_batch(pinned host tensor, out=pinned host tensor)",
-                       "pipeline": "H2D / transform / D2H overlapped over row chunks (16 MiB steady, "
-                                   "8 MiB first and last)"}
+                       "pipeline": "H2D / transform / D2H overlapped over row chunks (32 MiB steady, "
+                                   "16 MiB first and last)"}
         from paper_1402_0532_b200.transforms import pipeline_plan
         line["gpu_launches"] += max(2, args.steps // 2) * len(pipeline_plan(res["e2e_rows"], res["e2e_row_bytes"], 128))
     # CPU baseline: rank 0, N=1 only

@@ -239,21 +239,28 @@ template <int TP_, int TK_, int NC_> struct F2Cfg {
   static constexpr size_t STAGE_BYTES =
       2 * 2 * NCH * BP * sizeof(float4) + (SA_F2_CPA ? 2 * BV * NCH * sizeof(float2) : 0);
 };
-#ifndef SA_F2_TP  // tile shape (vector pairs per lane, bins per thread, chunk); -D for sweeps
+// Two tiles.  Large n (>= 256): 128 vectors x 128 bins per CTA, 16 bins per
+// thread, 16-sample chunks, 1 CTA/SM (250 registers): C2 fast 20.0 ms, exact
+// 26.5 ms.  Small n: 128 x 64, 8 bins per thread, 8-sample chunks, 2 CTAs/SM
+// (128 registers; 21.5 / 26.9 ms at C2), so n = 64 wastes no bins.  Sweep of
+// (pairs/lane, bins/thread, chunk, CTAs/SM) at C2: (2,16,16,1) 20.0,
+// (2,16,8,1) 20.4, (2,16,32,1) 20.5, (4,8,8,1) 21.0, (2,8,8,2) 21.5,
+// (2,12,8,1) 22.5, (4,8,16,1) 24.4 ms.
+#ifndef SA_F2_TP  // large-n tile shape (vector pairs per lane, bins per thread, chunk, CTAs/SM); -D for sweeps
 #define SA_F2_TP 2
-#define SA_F2_TK 8
-#define SA_F2_NC 8
+#define SA_F2_TK 16
+#define SA_F2_NC 16
+#define SA_F2_MINB 1
 #endif
-using F2 = F2Cfg<SA_F2_TP, SA_F2_TK, SA_F2_NC>;  // default: 128 vectors x 64 bins per CTA
-
-#ifndef SA_F2_MINB
-#define SA_F2_MINB 2
-#endif
+using F2Big = F2Cfg<SA_F2_TP, SA_F2_TK, SA_F2_NC>;
+using F2Small = F2Cfg<2, 8, 8>;
+constexpr int F2BIG_MINB = SA_F2_MINB, F2SMALL_MINB = 2;
+constexpr int F2_BIG_MIN_N = 256;
 #ifndef SA_F2_CHAIN  // chained twiddle offsets in exact mode (-D SA_F2_CHAIN=0 for A/B)
 #define SA_F2_CHAIN 1
 #endif
-template <bool POW2, bool TW_SMEM, bool EX>
-__global__ void __launch_bounds__(NDFT_THREADS, SA_F2_MINB)
+template <class F2, int MINB, bool POW2, bool TW_SMEM, bool EX>
+__global__ void __launch_bounds__(NDFT_THREADS, MINB)
     k_ndft_fast_f32x2(const float2 *__restrict__ x, float2 *__restrict__ y, int64_t batch, int n,
                       const float4 *__restrict__ quad, float gain, bool use_gain) {
   using A = Ar<float>;
@@ -541,6 +548,37 @@ __global__ void __launch_bounds__(256) k_ndft_exact(const C2<T> *__restrict__ x,
   if (k < n) y[v * n + k] = {accr, acci};
 }
 
+template <class F2, int MINB>
+int launch_f32x2(const float2 *x, float2 *y, int64_t batch, int n, const SaTwiddles *tw, bool exact, float g,
+                 bool use_gain, cudaStream_t s) {
+  const bool pow2 = (n & (n - 1)) == 0;
+  const bool tw_smem = (size_t)n * sizeof(float4) <= 64 * 1024;
+  const size_t bytes = F2::STAGE_BYTES + sizeof(float4) * (tw_smem ? n : 0);
+  const float4 *quad = (const float4 *)tw->quad;
+  const int64_t vblocks = (batch + F2::BV - 1) / F2::BV;
+  const unsigned kblocks = (unsigned)((n + F2::BK - 1) / F2::BK);
+  for (int64_t vb = 0; vb < vblocks; vb += 65535) {
+    const int64_t nvb = std::min<int64_t>(65535, vblocks - vb);
+    const dim3 grid(kblocks, (unsigned)nvb);
+    const float2 *xs = x + vb * F2::BV * n;
+    float2 *ys = y + vb * F2::BV * n;
+    const int64_t bleft = batch - vb * F2::BV;
+#define SA_NDFT_GO(P2, TS)                                                                              \
+  do {                                                                                                  \
+    auto kern = exact ? k_ndft_fast_f32x2<F2, MINB, P2, TS, true> : k_ndft_fast_f32x2<F2, MINB, P2, TS, false>; \
+    SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));   \
+    kern<<<grid, NDFT_THREADS, bytes, s>>>(xs, ys, bleft, n, quad, g, use_gain);                       \
+  } while (0)
+    if (pow2 && tw_smem) SA_NDFT_GO(true, true);
+    else if (pow2) SA_NDFT_GO(true, false);
+    else if (tw_smem) SA_NDFT_GO(false, true);
+    else SA_NDFT_GO(false, false);
+#undef SA_NDFT_GO
+  }
+  SA_LAUNCH_CHECK();
+  return SA_OK;
+}
+
 template <typename T>
 int launch(const void *xv, void *yv, int64_t batch, int64_t n64, const SaTwiddles *tw, int mode,
            double gain, cudaStream_t s) {
@@ -554,10 +592,10 @@ int launch(const void *xv, void *yv, int64_t batch, int64_t n64, const SaTwiddle
     return SA_ERR_UNSUPPORTED;
   }
   const int n = (int)n64;
-  // fp32: packed FFMA2 kernel (F2 tile); fp64: scalar DFMA kernel (NdftCfg tile)
+  // fp32: packed FFMA2 kernel (F2Big / F2Small tile); fp64: scalar DFMA kernel (NdftCfg tile)
   constexpr bool F32X2 = sizeof(T) == 4;
-  constexpr int BV = F32X2 ? F2::BV : 32 * NdftCfg<T>::TB;
-  constexpr int BK = F32X2 ? F2::BK : NDFT_WARPS * NdftCfg<T>::TK;
+  static_assert(F2Big::BV == F2Small::BV, "both fp32 tiles take 128 vectors");
+  constexpr int BV = F32X2 ? F2Big::BV : 32 * NdftCfg<T>::TB;
   // exact mode: the tiled kernels (EX) once a batch fills a tile, else one
   // thread per (vector, bin)
   const bool exact = mode == SA_NDFT_EXACT;
@@ -577,10 +615,17 @@ int launch(const void *xv, void *yv, int64_t batch, int64_t n64, const SaTwiddle
     SA_LAUNCH_CHECK();
     return SA_OK;
   }
+  if constexpr (F32X2) {
+    if (n >= F2_BIG_MIN_N)
+      return launch_f32x2<F2Big, F2BIG_MINB>((const float2 *)x, (float2 *)y, batch, n, tw, exact, (float)g,
+                                             use_gain, s);
+    return launch_f32x2<F2Small, F2SMALL_MINB>((const float2 *)x, (float2 *)y, batch, n, tw, exact, (float)g,
+                                               use_gain, s);
+  }
+  constexpr int BK = NDFT_WARPS * NdftCfg<T>::TK;
   const bool pow2 = (n & (n - 1)) == 0;
   const bool tw_smem = (size_t)n * sizeof(C4<T>) <= 64 * 1024;
-  size_t bytes = (F32X2 ? F2::STAGE_BYTES : sizeof(C4<T>) * 2 * NC * BV) +
-                 sizeof(C4<T>) * (tw_smem ? n : 0);
+  size_t bytes = sizeof(C4<T>) * 2 * NC * BV + sizeof(C4<T>) * (tw_smem ? n : 0);
   const C4<T> *quad = (const C4<T> *)tw->quad;
   int64_t vblocks = (batch + BV - 1) / BV;
   unsigned kblocks = (unsigned)((n + BK - 1) / BK);
@@ -592,18 +637,9 @@ int launch(const void *xv, void *yv, int64_t batch, int64_t n64, const SaTwiddle
     int64_t bleft = batch - vb * BV;
 #define SA_NDFT_GO(P2, TS)                                                                  \
   do {                                                                                      \
-    if constexpr (F32X2) {                                                                  \
-      auto kern = exact ? k_ndft_fast_f32x2<P2, TS, true> : k_ndft_fast_f32x2<P2, TS, false>; \
-      SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                                       (int)bytes));                                        \
-      kern<<<grid, NDFT_THREADS, bytes, s>>>((const float2 *)xs, (float2 *)ys, bleft, n,    \
-                                             (const float4 *)quad, (float)g, use_gain);     \
-    } else {                                                                                \
-      auto kern = exact ? k_ndft_fast<T, P2, TS, true> : k_ndft_fast<T, P2, TS, false>;    \
-      SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                                       (int)bytes));                                        \
-      kern<<<grid, NDFT_THREADS, bytes, s>>>(xs, ys, bleft, n, quad, g, use_gain);         \
-    }                                                                                       \
+    auto kern = exact ? k_ndft_fast<T, P2, TS, true> : k_ndft_fast<T, P2, TS, false>;      \
+    SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes)); \
+    kern<<<grid, NDFT_THREADS, bytes, s>>>(xs, ys, bleft, n, quad, g, use_gain);           \
   } while (0)
     if (pow2 && tw_smem) SA_NDFT_GO(true, true);
     else if (pow2) SA_NDFT_GO(true, false);

@@ -243,19 +243,19 @@ def _pinned_host(t) -> bool:
 
 
 def pipeline_chunks(nbytes: int) -> int:
-    """Steady-state row chunks of a pinned-host batched call: 16 MiB each, at
+    """Steady-state row chunks of a pinned-host batched call: 32 MiB each, at
     most 64 -- measured best on C2 (512 MiB each way)."""
     return int(max(1, min(64, nbytes // (PIPELINE_MIB << 20))))
 
 
-PIPELINE_MIB = int(__import__("os").environ.get("SA_PIPELINE_MIB", "16"))
+PIPELINE_MIB = int(__import__("os").environ.get("SA_PIPELINE_MIB", "32"))
 PIPELINE_RAMP = int(__import__("os").environ.get("SA_PIPELINE_RAMP", "1"))
 
 
 def pipeline_plan(rows: int, row_bytes: int, row_align: int) -> list[tuple[int, int]]:
     """Row ranges of a pinned-host batched call.  Steady chunks of
     ``pipeline_chunks``' size; the first and last PIPELINE_RAMP chunks halve
-    towards the ends (16 -> 8 -> 4 -> 2 MiB), so the pipeline fills after a
+    towards the ends (32 -> 16 -> 8 MiB), so the pipeline fills after a
     small upload and drains after a small download.  One transform launch per
     chunk."""
     total = rows * row_bytes
