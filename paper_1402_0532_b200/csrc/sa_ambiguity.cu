@@ -279,12 +279,12 @@ __global__ void __launch_bounds__(256) k_lag_integrate_fast(
 // complex64, T % 16 == 0: entry e of S holds samples e and e + T/2, entry u of
 // C window slots u and u + T/2, each as {x, x'}, {y, y'} (S0/C0) and the signs
 // {sx, sx'}, {sy, sy'} (S1/C1), in pad8-strided float4 arrays.
-#ifndef SA_LAG2_RS  // reduce-scatter epilogue (-D for A/B)
-#define SA_LAG2_RS 1
-#endif
 #ifndef SA_LAG2_LPW  // packed kernel: lags per warp, min CTAs per SM (-D for sweeps)
 #define SA_LAG2_LPW 8
 #define SA_LAG2_MINB 2
+#endif
+#ifndef SA_LAG2_RS  // reduce-scatter epilogue (16 values per lane; -D for A/B)
+#define SA_LAG2_RS (SA_LAG2_LPW == 8)
 #endif
 constexpr int L2_LPW = SA_LAG2_LPW;
 constexpr int L2_LPC = LAG_WARPS * L2_LPW;  // lags per CTA
