@@ -58,10 +58,14 @@ template <> struct K64<float> {
   static constexpr int NS = SA_K64F_NS;  // node storages (2 = pipelined signals; needs CL >= 8 for c64)
   static constexpr int MINB = SA_K64F_MINB;  // resident CTAs per SM
 };
+#ifndef SA_K64D_TC  // complex128 shape (-D for sweeps)
+#define SA_K64D_TC 8
+#define SA_K64D_NG 2
+#endif
 template <> struct K64<double> {
-  static constexpr int TC = 8;
+  static constexpr int TC = SA_K64D_TC;
   static constexpr int CL = 8;
-  static constexpr int NG = 2;
+  static constexpr int NG = SA_K64D_NG;
   static constexpr int NS = 1;
   static constexpr int MINB = 1;
 };
