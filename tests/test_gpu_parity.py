@@ -110,7 +110,7 @@ def test_ndft_batch_c1(sa, golden):
     assert_literal(sa.ndft_batch(dev(golden["c1_x"])).cpu().numpy(), golden["c1_y"], TOL_F64)
 
 
-@pytest.mark.parametrize("n", [1, 2, 7, 100, 1000, 1024, 2048, 5003, 16384])
+@pytest.mark.parametrize("n", [1, 2, 7, 100, 255, 256, 300, 1000, 1024, 2048, 5003, 16384])
 def test_ndft_batch_sizes(sa, n):
     """Ragged batches, tiny / prime / large N (16384: twiddles read from global,
     the table no longer fits in smem), zeros; fast within tolerance, exact
@@ -672,7 +672,7 @@ def test_empty_batches(sa):
     assert sa.mf_complex(np.zeros(0, complex), np.zeros(0, complex)).size == 0
 
 
-@pytest.mark.parametrize("n", [64, 1000, 1024])
+@pytest.mark.parametrize("n", [64, 255, 256, 1000, 1024])
 def test_ndft_exact_tiled_value_identical(sa, n):
     """Exact mode on batches that fill the vector tile (the tiled EX kernels):
     value-identical to the sequential oracle in fp64 and fp32; zeros, a tone."""
