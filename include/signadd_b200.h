@@ -41,8 +41,11 @@ enum sa_status {
 
 enum sa_ndft_mode {
   SA_NDFT_FAST = 0,  /* sign-split regrouped accumulation (8 FMA per ⊙)        */
-  SA_NDFT_EXACT = 1  /* per-⊙ rounding, sequential accumulation: value-identical
+  SA_NDFT_EXACT = 1, /* per-⊙ rounding, sequential accumulation: value-identical
                         to transforms.py:223-251                               */
+  SA_NDFT_TC = 2     /* the fast-mode sum as a sign-split bf16 GEMM on tcgen05
+                        tensor cores (complex64, n % 128 == 0, n <= 4096; other
+                        shapes run SA_NDFT_FAST).  Same ≤1e-4 fp32 tolerance. */
 };
 
 enum sa_nlfft_variant {

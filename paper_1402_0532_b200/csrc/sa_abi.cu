@@ -61,7 +61,7 @@ int sa_twiddle_create(int device, int dtype, int64_t n, const double *host_table
   int prev = 0;
   SA_CUDA_TRY(cudaGetDevice(&prev));
   SA_CUDA_TRY(cudaSetDevice(device));
-  SaTwiddles *tw = new SaTwiddles{dtype, n, device, nullptr, nullptr, nullptr, nullptr};
+  SaTwiddles *tw = new SaTwiddles{dtype, n, device, nullptr, nullptr, nullptr, nullptr, nullptr};
   int rc = sa_twiddles_build(tw, host_table, (cudaStream_t)stream);
   cudaSetDevice(prev);
   if (rc != SA_OK) {
@@ -69,6 +69,7 @@ int sa_twiddle_create(int device, int dtype, int64_t n, const double *host_table
     cudaFree(tw->quad);
     cudaFree(tw->stage);
     cudaFree(tw->stage2);
+    cudaFree(tw->tcw);
     delete tw;
     return rc;
   }
@@ -86,6 +87,7 @@ int sa_twiddle_destroy(void *handle) {
   cudaFree(tw->quad);
   cudaFree(tw->stage);
   cudaFree(tw->stage2);
+  cudaFree(tw->tcw);
   cudaSetDevice(prev);
   delete tw;
   return SA_OK;
@@ -111,11 +113,17 @@ int sa_ndft(int dtype, const void *x, void *y, int64_t batch, int64_t n, const v
   SA_REQUIRE(dtype_ok(dtype), SA_ERR_ARG, "bad dtype %d", dtype);
   SA_REQUIRE(n >= 1, SA_ERR_CONTRACT, "transform input must be a 1-d sequence of length >= 1");
   SA_REQUIRE(batch >= 0, SA_ERR_ARG, "negative batch");
-  SA_REQUIRE(mode == SA_NDFT_FAST || mode == SA_NDFT_EXACT, SA_ERR_ARG, "bad mode %d", mode);
+  SA_REQUIRE(mode == SA_NDFT_FAST || mode == SA_NDFT_EXACT || mode == SA_NDFT_TC, SA_ERR_ARG, "bad mode %d",
+             mode);
   SA_REQUIRE(batch == 0 || (x && y), SA_ERR_ARG, "null pointer");
   SA_REQUIRE(x != y || batch == 0, SA_ERR_ARG, "sa_ndft: x and y must not overlap");
   int rc = check_tw(tw, dtype, n, false);
   if (rc) return rc;
+  if (mode == SA_NDFT_TC) {
+    if (sa_ndft_tc_supported(dtype, n))
+      return sa_launch_ndft_tc(x, y, batch, n, (const SaTwiddles *)tw, gain, (cudaStream_t)stream);
+    mode = SA_NDFT_FAST;  // same regrouped sum on the FFMA2 kernels
+  }
   return sa_launch_ndft(dtype, x, y, batch, n, (const SaTwiddles *)tw, mode, gain,
                         (cudaStream_t)stream);
 }

@@ -17,6 +17,7 @@ struct SaTwiddles {
   void *stage;  // (n-1) x {|wr|, |wi|, sgn wr, sgn wi}, stage-packed:
                 //   stage s (1..log2 n) at offset 2^(s-1)-1, entry j = table[j*n/2^s]
   void *stage2; // (n-1) x {wr, wi}, same stage-packed order (8/16-byte entries)
+  void *tcw;    // tensor-core NDFT operands [W0; W1; sgn Wv] (bf16, 3 x 2n x 2n), built on first use
 };
 
 void sa_set_error(const char *fmt, ...);
@@ -53,6 +54,11 @@ int sa_launch_fma_peak(int dtype, int64_t iters, void *d_sink, int blocks, cudaS
 // sa_ndft.cu
 int sa_launch_ndft(int dtype, const void *x, void *y, int64_t batch, int64_t n,
                    const SaTwiddles *tw, int mode, double gain, cudaStream_t s);
+
+// sa_ndft_tc.cu (tensor-core fast mode; SA_ERR_UNSUPPORTED -> use the FFMA2 kernels)
+bool sa_ndft_tc_supported(int dtype, int64_t n);
+int sa_launch_ndft_tc(const void *x, void *y, int64_t batch, int64_t n, const SaTwiddles *tw, double gain,
+                      cudaStream_t s);
 
 // sa_nlfft.cu
 int sa_launch_nlfft(int dtype, int variant, const void *x, void *y, int64_t batch, int64_t n,

@@ -1,0 +1,349 @@
+// sa_ndft_tc.cu -- fast-mode NDFT (transforms.py:223-251, regrouped) on the
+// 5th-generation tensor cores: tcgen05.mma with TMEM accumulators, TMA-loaded
+// twiddle operands and CUDA-core warps that build the signal operand in smem.
+//
+// Fast mode already evaluates every complex ⊙ as four exact sign products
+// (sa_ndft.cu):
+//   Re X_k = Σ_n sgn(xr) Wr + sgn(Wr) xr − sgn(xi) Wi − sgn(Wi) xi
+//   Im X_k = Σ_n sgn(xr) Wi + sgn(Wi) xr + sgn(xi) Wr + sgn(Wr) xi ,  W = W^(kn mod N)
+// which is one real GEMM per batch of vectors, D[v, o] = Σ_K A[v, K] B[o, K], with
+// o = 2k + (re|im) (so D rows are complex64 spectra as stored) and K = 2n + (re|im):
+//   D = S · Wv^T + X · sgn(Wv)^T,   S = sgn(x) (exact in bf16),  Wv = [[Wr, −Wi], [Wi, Wr]].
+// The non-sign operands are split into two bf16 terms (Wv = W0 + W1, x = X0 + X1,
+// each residual exact in fp32), so every product the tensor core forms is a
+// sign times a 16-bit-mantissa piece, and the four GEMM terms
+//   S·W0 + S·W1 + X0·sgn(Wv) + X1·sgn(Wv)
+// accumulate in fp32 in TMEM.  Error vs the fp64 oracle: ≤ 2^-17 relative per
+// term from the splits plus fp32 accumulation (tests: ≤ 1e-4 of ‖y‖₁, the
+// north-star fp32 bound; measured ~3e-8).  Multiplication-free in the ⊙ sense:
+// one factor of every product is a sign.
+//
+// Kernel (persistent, 1 CTA per SM, 448 threads):
+//   warp 0      TMA producer: W0 / W1 / sgn(Wv) tiles (256 outputs x 16 samples)
+//   warp 1      TMEM allocator + single-thread MMA issuer (M=128, N=256, K=16)
+//   warps 2-5   epilogue: tcgen05.ld 32x32b -> fp32 rows of y (2 TMEM accumulators)
+//   warps 6-13  converters: x (c64, gain applied) -> S, X0, X1 bf16 tiles in the
+//               SWIZZLE_64B K-major layout, fence.proxy.async, arrive
+// Three smem slots of 72 KB (3 A tiles of 8 KB + 3 B tiles of 16 KB).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "sa_internal.h"
+#include "sa_regs.cuh"
+
+namespace {
+
+constexpr int BM = 128;          // vectors per tile (TMEM lanes)
+constexpr int BN = 256;          // outputs per tile (128 bins x {re, im}; TMEM columns)
+constexpr int KC = 16;           // samples per slot
+constexpr int KS = 2 * KC;       // bf16 per operand row per slot = 64 B (SWIZZLE_64B)
+constexpr int NSLOT = 3;
+constexpr int A_TILE = BM * KS * 2;  // 8 KB
+constexpr int B_TILE = BN * KS * 2;  // 16 KB
+constexpr int SLOT = 3 * A_TILE + 3 * B_TILE;
+constexpr int CONV_WARPS = 8;
+constexpr int THREADS = 32 * (6 + CONV_WARPS);
+constexpr int SMEM = NSLOT * SLOT + 1024 + 256;
+constexpr int TMEM_COLS = 512;   // two accumulators of BN columns
+
+// instruction descriptor: kind::f16, A = B = bf16, D = f32, both K-major, M = 128, N = 256
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+
+// smem matrix descriptor, K-major SWIZZLE_64B: rows of 64 B, 8-row atoms 512 B apart
+SA_HD uint64_t sdesc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+}
+
+SA_HD void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+SA_HD void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+SA_HD void tc_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   sa_smem_u32(bar))
+               : "memory");
+}
+SA_HD void tc_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(IDESC), "r"(acc)
+      : "memory");
+}
+SA_HD void mbar_init(uint64_t *bar, uint32_t count) { sa_mbar_init(bar, count); }
+SA_HD void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa_smem_u32(bar)) : "memory");
+}
+
+SA_HD uint32_t bf2(float hi, float lo) {  // {lo -> bits 0..15, hi -> bits 16..31}, RN
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+#define SA_LD32(v, taddr)                                                                                  \
+  asm volatile(                                                                                            \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"     \
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                           \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),    \
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),           \
+        "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),         \
+        "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),         \
+        "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                                                              \
+      : "r"(taddr))
+
+__global__ void __launch_bounds__(THREADS, 1)
+    k_ndft_tc(const __grid_constant__ CUtensorMap wmap, const float4 *__restrict__ x, float *__restrict__ y,
+              int64_t batch, int n, float gain, int use_gain) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t *full = (uint64_t *)(smem + NSLOT * SLOT);
+  uint64_t *empty = full + NSLOT;
+  uint64_t *tfull = empty + NSLOT;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_holder = (uint32_t *)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ot_count = (2 * n) / BN;
+  const int64_t vt_count = (batch + BM - 1) / BM;
+  const int64_t ntiles = vt_count * ot_count;
+  const int kslots = n / KC;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSLOT; ++s) {
+      mbar_init(&full[s], 1 + CONV_WARPS);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    sa_fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     sa_smem_u32(tmem_holder)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    // ---- TMA producer: twiddle operand tiles ----
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&wmap) : "memory");
+      uint32_t it = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int o0 = (int)(t % ot_count) * BN;
+        for (int kc = 0; kc < kslots; ++kc, ++it) {
+          const int s = it % NSLOT;
+          sa_mbar_wait(&empty[s], ((it / NSLOT) & 1) ^ 1);
+          unsigned char *b = smem + s * SLOT + 3 * A_TILE;
+          sa_mbar_expect_tx(&full[s], 3 * B_TILE);
+#pragma unroll
+          for (int p = 0; p < 3; ++p) sa_tma_load_2d(b + p * B_TILE, &wmap, kc * KS, p * 2 * n + o0, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer ----
+    if (lane == 0) {
+      uint32_t it = 0, lt = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+        const uint32_t acc = lt & 1;
+        sa_mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (int kc = 0; kc < kslots; ++kc, ++it) {
+          const int s = it % NSLOT;
+          sa_mbar_wait(&full[s], (it / NSLOT) & 1);
+          tc_fence_after();
+          const uint32_t base = sa_smem_u32(smem + s * SLOT);
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            const uint32_t off = ks * 32;  // 16 bf16 along K inside the 64-B swizzled row
+            const uint64_t aS = sdesc(base + off), aX0 = sdesc(base + A_TILE + off),
+                           aX1 = sdesc(base + 2 * A_TILE + off);
+            const uint64_t bW0 = sdesc(base + 3 * A_TILE + off), bW1 = sdesc(base + 3 * A_TILE + B_TILE + off),
+                           bWs = sdesc(base + 3 * A_TILE + 2 * B_TILE + off);
+            tc_mma(d, aS, bW0, (kc | ks) != 0);
+            tc_mma(d, aS, bW1, 1);
+            tc_mma(d, aX0, bWs, 1);
+            tc_mma(d, aX1, bWs, 1);
+          }
+          tc_commit(&empty[s]);
+        }
+        tc_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp < 6) {
+    // ---- epilogue: TMEM -> y ----
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    uint32_t lt = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+      const uint32_t acc = lt & 1;
+      const int64_t v = (t / ot_count) * BM + q * 32 + lane;
+      const int o0 = (int)(t % ot_count) * BN;
+      sa_mbar_wait(&tfull[acc], (lt >> 1) & 1);
+      tc_fence_after();
+      float4 *dst = (float4 *)(y + v * 2 * n + o0);
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        SA_LD32(r, tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (v < batch) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            dst[c * 8 + j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                         __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  } else {
+    // ---- converters: x -> S, X0, X1 (bf16, SWIZZLE_64B K-major) ----
+    const int ct = threadIdx.x - 6 * 32;  // 0..255
+    const int h = ct & 7;                 // sample pair 2h, 2h+1 of the slot
+    const int r0 = ct >> 3;               // rows r0 + 32 i
+    uint32_t it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t vbase = (t / ot_count) * BM;
+      for (int kc = 0; kc < kslots; ++kc, ++it) {
+        const int s = it % NSLOT;
+        float4 xv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {  // loads first: they do not touch the slot
+          const int64_t v = vbase + r0 + 32 * i;
+          xv[i] = v < batch ? __ldg(&x[(v * n + (int64_t)kc * KC) / 2 + h]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        sa_mbar_wait(&empty[s], ((it / NSLOT) & 1) ^ 1);
+        unsigned char *a = smem + s * SLOT;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = r0 + 32 * i;
+          float4 f = xv[i];
+          if (use_gain) f = make_float4(sa_mul(gain, f.x), sa_mul(gain, f.y), sa_mul(gain, f.z), sa_mul(gain, f.w));
+          const uint32_t s01 = bf2(sa_sgn(f.y), sa_sgn(f.x)), s23 = bf2(sa_sgn(f.w), sa_sgn(f.z));
+          const uint32_t h01 = bf2(f.y, f.x), h23 = bf2(f.w, f.z);
+          const float e0 = sa_sub(f.x, __uint_as_float(h01 << 16)), e1 = sa_sub(f.y, __uint_as_float(h01 & 0xFFFF0000u));
+          const float e2 = sa_sub(f.z, __uint_as_float(h23 << 16)), e3 = sa_sub(f.w, __uint_as_float(h23 & 0xFFFF0000u));
+          const uint32_t l01 = bf2(e1, e0), l23 = bf2(e3, e2);
+          const int off = r * 64 + ((((h >> 1) ^ (r >> 1)) & 3) << 4) + (h & 1) * 8;
+          *(uint2 *)(a + off) = make_uint2(s01, s23);
+          *(uint2 *)(a + A_TILE + off) = make_uint2(h01, h23);
+          *(uint2 *)(a + 2 * A_TILE + off) = make_uint2(l01, l23);
+        }
+        sa_fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05.mma
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[s]);
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+  }
+}
+
+// Twiddle operands [W0; W1; sgn(Wv)], each 2n x 2n bf16, row o = 2k + c_out, column K = 2m + c_in:
+// Wv = [[Wr, -Wi], [Wi, Wr]] of W = raw[(k m) mod n] (the fp32 table, as the FFMA2 kernels use).
+__global__ void k_tc_wbuild(const float2 *__restrict__ raw, int n, uint16_t *__restrict__ w) {
+  const int64_t nn = 2LL * n, total = nn * nn;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = i / nn, kk = i % nn;
+    const int64_t k = o >> 1, m = kk >> 1;
+    const int co = (int)(o & 1), ci = (int)(kk & 1);
+    const float2 tw = raw[(k * m) % n];
+    const float val = co == ci ? tw.x : (co == 0 ? -tw.y : tw.y);
+    const uint32_t hi = bf2(0.f, val);
+    const uint32_t lo = bf2(0.f, sa_sub(val, __uint_as_float(hi << 16)));
+    const uint32_t sg = bf2(0.f, sa_sgn(val));
+    w[i] = (uint16_t)hi;
+    w[total + i] = (uint16_t)lo;
+    w[2 * total + i] = (uint16_t)sg;
+  }
+}
+
+std::mutex g_tc_mutex;
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn_tc() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+}  // namespace
+
+bool sa_ndft_tc_supported(int dtype, int64_t n) {
+  return dtype == SA_C64 && n >= 128 && n <= 4096 && n % 128 == 0;
+}
+
+int64_t sa_ndft_tc_wbytes(int64_t n) { return 3 * (2 * n) * (2 * n) * 2; }
+
+int sa_launch_ndft_tc(const void *x, void *y, int64_t batch, int64_t n, const SaTwiddles *tw_c, double gain,
+                      cudaStream_t s) {
+  if (!sa_ndft_tc_supported(tw_c->dtype, n)) return SA_ERR_UNSUPPORTED;
+  if (batch == 0) return SA_OK;
+  SaTwiddles *tw = const_cast<SaTwiddles *>(tw_c);
+  {
+    std::lock_guard<std::mutex> g(g_tc_mutex);
+    if (!tw->tcw) {
+      void *w = nullptr;
+      SA_CUDA_TRY(cudaMalloc(&w, sa_ndft_tc_wbytes(n)));
+      k_tc_wbuild<<<1184, 256, 0, s>>>((const float2 *)tw->raw, (int)n, (uint16_t *)w);
+      SA_LAUNCH_CHECK();
+      SA_CUDA_TRY(cudaStreamSynchronize(s));  // once per set: other streams may use it next
+      tw->tcw = w;
+    }
+  }
+  auto enc = encode_fn_tc();
+  if (!enc) {
+    sa_set_error("cuTensorMapEncodeTiled unavailable");
+    return SA_ERR_CUDA;
+  }
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)(2 * n), (cuuint64_t)(6 * n)};
+  cuuint64_t strides[1] = {(cuuint64_t)(2 * n * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)KS, (cuuint32_t)BN};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, tw->tcw, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    sa_set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return SA_ERR_CUDA;
+  }
+  static bool smem_set[64] = {};
+  int dev = 0;
+  SA_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev >= 64 || !smem_set[dev]) {
+    SA_CUDA_TRY(cudaFuncSetAttribute(k_ndft_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    if (dev < 64) smem_set[dev] = true;
+  }
+  int sms = 0;
+  SA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t ntiles = ((batch + BM - 1) / BM) * ((2 * n) / BN);
+  const int grid = (int)(ntiles < sms ? ntiles : sms);
+  k_ndft_tc<<<grid, THREADS, SMEM, s>>>(map, (const float4 *)x, (float *)y, batch, (int)n, (float)gain,
+                                        gain != 1.0);
+  SA_LAUNCH_CHECK();
+  return SA_OK;
+}
