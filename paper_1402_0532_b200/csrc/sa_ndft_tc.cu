@@ -211,40 +211,62 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else {
     // ---- converters: x -> S, X0, X1 (bf16, SWIZZLE_64B K-major) ----
+    // Each thread owns sample pair h of rows r0 + 32 i; x for slot it+3 is in
+    // flight (three register sets) while slot it is converted.
     const int ct = threadIdx.x - 6 * 32;  // 0..255
     const int h = ct & 7;                 // sample pair 2h, 2h+1 of the slot
     const int r0 = ct >> 3;               // rows r0 + 32 i
-    uint32_t it = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const int64_t vbase = (t / ot_count) * BM;
-      for (int kc = 0; kc < kslots; ++kc, ++it) {
-        const int s = it % NSLOT;
-        float4 xv[4];
+    const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int64_t total = my_tiles * kslots;
+    const uint32_t sbase = sa_smem_u32(smem);
+    auto load = [&](float4(&b)[4], int64_t it) {
+      if (it >= total) return;
+      const int64_t lt = it / kslots;
+      const int kc = (int)(it - lt * kslots);
+      const int64_t vbase = ((blockIdx.x + lt * gridDim.x) / ot_count) * BM;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {  // loads first: they do not touch the slot
-          const int64_t v = vbase + r0 + 32 * i;
-          xv[i] = v < batch ? __ldg(&x[(v * n + (int64_t)kc * KC) / 2 + h]) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-        sa_mbar_wait(&empty[s], ((it / NSLOT) & 1) ^ 1);
-        unsigned char *a = smem + s * SLOT;
+      for (int i = 0; i < 4; ++i) {
+        const int64_t v = vbase + r0 + 32 * i;
+        b[i] = v < batch ? __ldg(&x[(v * n + (int64_t)kc * KC) / 2 + h]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    };
+    auto convert = [&](const float4(&b)[4], int64_t it) {
+      const int s = (int)(it % NSLOT);
+      sa_mbar_wait(&empty[s], ((it / NSLOT) & 1) ^ 1);
+      const uint32_t a = sbase + s * SLOT;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int r = r0 + 32 * i;
-          float4 f = xv[i];
-          if (use_gain) f = make_float4(sa_mul(gain, f.x), sa_mul(gain, f.y), sa_mul(gain, f.z), sa_mul(gain, f.w));
-          const uint32_t s01 = bf2(sa_sgn(f.y), sa_sgn(f.x)), s23 = bf2(sa_sgn(f.w), sa_sgn(f.z));
-          const uint32_t h01 = bf2(f.y, f.x), h23 = bf2(f.w, f.z);
-          const float e0 = sa_sub(f.x, __uint_as_float(h01 << 16)), e1 = sa_sub(f.y, __uint_as_float(h01 & 0xFFFF0000u));
-          const float e2 = sa_sub(f.z, __uint_as_float(h23 << 16)), e3 = sa_sub(f.w, __uint_as_float(h23 & 0xFFFF0000u));
-          const uint32_t l01 = bf2(e1, e0), l23 = bf2(e3, e2);
-          const int off = r * 64 + ((((h >> 1) ^ (r >> 1)) & 3) << 4) + (h & 1) * 8;
-          *(uint2 *)(a + off) = make_uint2(s01, s23);
-          *(uint2 *)(a + A_TILE + off) = make_uint2(h01, h23);
-          *(uint2 *)(a + 2 * A_TILE + off) = make_uint2(l01, l23);
-        }
-        sa_fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05.mma
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&full[s]);
+      for (int i = 0; i < 4; ++i) {
+        const int r = r0 + 32 * i;
+        float4 f = b[i];
+        if (use_gain) f = make_float4(sa_mul(gain, f.x), sa_mul(gain, f.y), sa_mul(gain, f.z), sa_mul(gain, f.w));
+        const uint32_t s01 = bf2(sa_sgn(f.y), sa_sgn(f.x)), s23 = bf2(sa_sgn(f.w), sa_sgn(f.z));
+        const uint32_t h01 = bf2(f.y, f.x), h23 = bf2(f.w, f.z);
+        const float e0 = sa_sub(f.x, __uint_as_float(h01 << 16)), e1 = sa_sub(f.y, __uint_as_float(h01 & 0xFFFF0000u));
+        const float e2 = sa_sub(f.z, __uint_as_float(h23 << 16)), e3 = sa_sub(f.w, __uint_as_float(h23 & 0xFFFF0000u));
+        const uint32_t l01 = bf2(e1, e0), l23 = bf2(e3, e2);
+        const uint32_t off = a + r * 64 + ((((h >> 1) ^ (r >> 1)) & 3) << 4) + (h & 1) * 8;
+        asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(off), "r"(s01), "r"(s23) : "memory");
+        asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(off + A_TILE), "r"(h01), "r"(h23) : "memory");
+        asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(off + 2 * A_TILE), "r"(l01), "r"(l23) : "memory");
+      }
+      sa_fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05.mma
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[s]);
+    };
+    float4 b0[4], b1[4], b2[4];
+    load(b0, 0);
+    load(b1, 1);
+    load(b2, 2);
+    for (int64_t it = 0; it < total; it += 3) {
+      convert(b0, it);
+      load(b0, it + 3);
+      if (it + 1 < total) {
+        convert(b1, it + 1);
+        load(b1, it + 4);
+      }
+      if (it + 2 < total) {
+        convert(b2, it + 2);
+        load(b2, it + 5);
       }
     }
   }
