@@ -211,37 +211,63 @@ def complex_dtype(name):
     return torch.complex64 if name == "c64" else torch.complex128
 
 
-def wl_ndft(args, ws, rank):
-    """C2: batched NDFT N=1024 x 65536."""
+def wl_ndft(args, ws, rank, mode=None, e2e=True):
+    """C2: batched NDFT N=1024 x 65536.  mode "tc" (complex64 default): the
+    fast-mode sum as a sign-split bf16 GEMM on tcgen05 (sa_ndft_tc.cu); "fast":
+    the FFMA2 CUDA-core kernel (sa_ndft.cu)."""
     import torch
     import paper_1402_0532_b200 as sa
     from paper_1402_0532_b200.workloads import c2_ndft
     n, batch = 1024, 65536
     cdt = complex_dtype(args.dtype)
+    mode = mode or (args.ndft_mode if args.dtype == "c64" else "fast")
     t0 = time.time()
     xh = torch.from_numpy(c2_ndft(n, batch)).to(cdt)
     log(f"[rank {rank}] C2 input generated in {time.time() - t0:.1f}s")
     xd = xh.cuda()
     yd = torch.empty_like(xd)
     ops = batch * n * n
-    step = lambda: sa.ndft_batch(xd, out=yd)  # noqa: E731
+    step = lambda: sa.ndft_batch(xd, out=yd, mode=mode)  # noqa: E731
+    desc = ("tc (fast-mode sum as a sign-split bf16 GEMM on tcgen05 tensor cores, fp32 accumulation)"
+            if mode == "tc" else "fast (sign-split regrouped accumulation, FFMA2)")
     res = {"ops": ops, "step": step, "launches_per_step": 1,
            "config": {"workload": "C2 batched NDFT (BASELINE.json configs[1])", "n": n,
-                      "batch": batch, "mode": "fast (sign-split regrouped accumulation)",
+                      "batch": batch, "mode": desc,
                       "dtype": "complex64" if args.dtype == "c64" else "complex128",
                       "l2_policy": "inputs (512 MiB c64) larger than L2; no flush",
                       "parallelism": f"dp{ws} (independent vectors, weak scaling)"}}
-    if not args.no_e2e:
+    if e2e and not args.no_e2e:
         hin = xh.pin_memory()
         hout = torch.empty_like(hin).pin_memory()
-        res["e2e_step"] = lambda: sa.ndft_batch(hin, out=hout)
+        res["e2e_step"] = lambda: sa.ndft_batch(hin, out=hout, mode=mode)
         res["e2e_rows"], res["e2e_row_bytes"] = hin.shape[0], hin.shape[1] * hin.element_size()
         res["h2d"] = hin.numel() * hin.element_size()
         res["d2h"] = hout.numel() * hout.element_size()
-    res["roofline"] = lambda ms: roof_alu(args.dtype, ops * 16 / (ms * 1e-3) / 1e12, args)
+        res["e2e_api"] = f"paper_1402_0532_b200.ndft_batch(pinned host tensor, out=pinned host tensor, mode={mode!r})"
+    if mode == "tc":
+        res["roofline"] = lambda ms: roof_tensor(ops * 32 / (ms * 1e-3) / 1e12)
+    else:
+        res["roofline"] = lambda ms: roof_alu(args.dtype, ops * 16 / (ms * 1e-3) / 1e12, args)
     res["cpu"] = lambda P: cpu_ndft(xh.numpy(), P)
     res["dtype"] = "f32" if args.dtype == "c64" else "f64"
     return res
+
+
+def roof_tensor(achieved_tflops):
+    """tcgen05 NDFT against the measured dense bf16 peak (MEASURED_PEAKS.json,
+    burst figure: one C2 step is a ~2 ms kernel timed alone)."""
+    peaks, src = measured_peaks()
+    peak = peaks.get("bf16_tflops", 1590.0)
+    tr = ncu_traffic("k_ndft_tc")
+    return {"bound": "tensor", "achieved": round(achieved_tflops, 1), "peak": peak, "unit": "TFLOP/s",
+            "frac": round(achieved_tflops / peak, 4),
+            "traffic": tr["bytes_per_launch"] if tr else None, "traffic_unit": "bytes/launch",
+            "traffic_source": tr["source"] if tr else None,
+            "algorithmic_bytes": 2 * 65536 * 1024 * 8, "kernel": "k_ndft_tc",
+            "peak_source": f"{src} bf16_tflops (burst; sustained {peaks.get('bf16_tflops_sustained')})",
+            "algorithmic": "32 bf16 tensor flop per complex ⊙: re/im outputs x re/im inputs x "
+                           "{sgn(x)·W0, sgn(x)·W1, X0·sgn(W), X1·sgn(W)} MACs (two-term bf16 splits)",
+            **({"ncu_utilisation_pct": tr["ncu"]} if tr and tr.get("ncu") else {})}
 
 
 def ncu_traffic(kernel_prefix):
@@ -259,7 +285,7 @@ def ncu_traffic(kernel_prefix):
                 best = {"bytes_per_launch": k["dram_read_bytes"] + k.get("dram_write_bytes", 0),
                         "source": os.path.relpath(f, ROOT),
                         "ncu": {key: round(k[key], 1) for key in ("issue_active_pct", "fma_pipe_pct",
-                                                                   "alu_pipe_pct", "fp64_pipe_pct",
+                                                                   "alu_pipe_pct", "fp64_pipe_pct", "tensor_pipe_pct", "lts_pct",
                                                                    "dram_pct") if key in k}}
     return best
 
@@ -476,7 +502,7 @@ def run_ours(args):
         ems, _ = timed(res["e2e_step"], max(2, args.steps // 2), 1, ws)
         line["e2e"] = {"value": res["ops"] * ws / (ems * 1e-3), "unit": unit, "ms_per_step": ems,
                        "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"],
-                       "api": "paper_1402_0532_b200.ndft_batch(pinned host tensor, out=pinned host tensor)",
+                       "api": res.get("e2e_api"),
                        "pipeline": "H2D / transform / D2H overlapped over row chunks (32 MiB steady, "
                                    "16 MiB first and last)"}
         from paper_1402_0532_b200.transforms import pipeline_plan
@@ -488,7 +514,9 @@ def run_ours(args):
     # extras (N=1)
     if rank == 0 and ws == 1 and not args.no_extras and w == "ndft":
         extras = {}
-        for name, fn in (("C3_nlfft_dit", lambda: wl_nlfft(args, ws, rank, "dit")),
+        other = "fast" if (args.ndft_mode == "tc" and args.dtype == "c64") else None
+        for name, fn in ((("C2_ndft_ffma2", lambda: wl_ndft(args, ws, rank, mode="fast", e2e=False)),) if other else ()) + (
+                         ("C3_nlfft_dit", lambda: wl_nlfft(args, ws, rank, "dit")),
                          ("C3_nlfft_dif", lambda: wl_nlfft(args, ws, rank, "dif")),
                          ("C4_map", lambda: wl_map(args, ws, rank)),
                          ("C5_detect", lambda: wl_detect(args))):
@@ -609,6 +637,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="ndft", choices=["ndft", "nlfft", "map", "map5"])
     ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
+    ap.add_argument("--ndft-mode", default="tc", choices=["tc", "fast"],
+                    help="C2 NDFT kernel: tc = tcgen05 sign-split GEMM (complex64), fast = FFMA2 CUDA-core kernel")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -24,6 +24,8 @@ KEYS = {
     "fma_pipe_pct": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
     "alu_pipe_pct": "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
     "fp64_pipe_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "tensor_pipe_pct": "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "lts_pct": "lts__throughput.avg.pct_of_peak_sustained_elapsed",
     "dram_pct": "dram__cycles_active.avg.pct_of_peak_sustained_elapsed",
     "dram_gbs": "dram__bytes.sum.per_second",
     "warps_active_per_sched": "smsp__warps_active.avg.per_cycle_active",
