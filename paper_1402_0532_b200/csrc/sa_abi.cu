@@ -120,9 +120,9 @@ int sa_ndft(int dtype, const void *x, void *y, int64_t batch, int64_t n, const v
   int rc = check_tw(tw, dtype, n, false);
   if (rc) return rc;
   if (mode == SA_NDFT_TC) {
-    if (sa_ndft_tc_supported(dtype, n))
-      return sa_launch_ndft_tc(x, y, batch, n, (const SaTwiddles *)tw, gain, (cudaStream_t)stream);
-    mode = SA_NDFT_FAST;  // same regrouped sum on the FFMA2 kernels
+    rc = sa_launch_ndft_tc(x, y, batch, n, (const SaTwiddles *)tw, gain, (cudaStream_t)stream);
+    if (rc != SA_ERR_UNSUPPORTED) return rc;
+    mode = SA_NDFT_FAST;  // other shapes / unaligned views: the same regrouped sum on the FFMA2 kernels
   }
   return sa_launch_ndft(dtype, x, y, batch, n, (const SaTwiddles *)tw, mode, gain,
                         (cudaStream_t)stream);

@@ -35,22 +35,33 @@
 
 namespace {
 
-constexpr int BM = 128;          // vectors per tile (TMEM lanes)
+constexpr int BM = 128;          // vectors per CTA per tile (TMEM lanes)
 constexpr int BN = 256;          // outputs per tile (128 bins x {re, im}; TMEM columns)
 constexpr int KC = 16;           // samples per slot
 constexpr int KS = 2 * KC;       // bf16 per operand row per slot = 64 B (SWIZZLE_64B)
-constexpr int NSLOT = 3;
 constexpr int A_TILE = BM * KS * 2;  // 8 KB
-constexpr int B_TILE = BN * KS * 2;  // 16 KB
-constexpr int SLOT = 3 * A_TILE + 3 * B_TILE;
-constexpr int CONV_WARPS = 8;
+#ifndef SA_TC_CONV_WARPS
+#define SA_TC_CONV_WARPS 8
+#endif
+constexpr int CONV_WARPS = SA_TC_CONV_WARPS;
+constexpr int CROWS = CONV_WARPS * 4;   // rows covered per pass (8 threads per row)
+constexpr int RPT = BM / CROWS;         // rows per converter thread
 constexpr int THREADS = 32 * (6 + CONV_WARPS);
-constexpr int SMEM = NSLOT * SLOT + 1024 + 256;
 constexpr int TMEM_COLS = 512;   // two accumulators of BN columns
 
-// instruction descriptor: kind::f16, A = B = bf16, D = f32, both K-major, M = 128, N = 256
-constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(BM >> 4) << 24);
+// CG = CTAs per MMA (tcgen05 cta_group).  CG = 2: a CTA pair (cluster of 2) issues
+// M = 256 MMAs from the leader; each CTA holds its 128 vector rows of A and half
+// (128 rows) of every twiddle tile, so each SM streams half the B bytes.
+template <int CG> struct TcCfg {
+  static constexpr int BROWS = BN / CG;               // twiddle rows per CTA per tile
+  static constexpr int B_TILE = BROWS * KS * 2;       // 16 KB (CG 1) / 8 KB (CG 2)
+  static constexpr int SLOT = 3 * A_TILE + 3 * B_TILE;
+  static constexpr int NSLOT = CG == 1 ? 3 : 4;
+  static constexpr int SMEM = NSLOT * SLOT + 1024 + 256;
+  // instruction descriptor: kind::f16, A = B = bf16, D = f32, both K-major, M = 128 CG, N = 256
+  static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                    ((uint32_t)((BM * CG) >> 4) << 24);
+};
 
 // smem matrix descriptor, K-major SWIZZLE_64B: rows of 64 B, 8-row atoms 512 B apart
 SA_HD uint64_t sdesc(uint32_t saddr) {
@@ -60,21 +71,54 @@ SA_HD uint64_t sdesc(uint32_t saddr) {
 
 SA_HD void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 SA_HD void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-SA_HD void tc_commit(uint64_t *bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   sa_smem_u32(bar))
-               : "memory");
+// MMA completion -> mbarrier (CG 2: the barrier at the same offset in both CTAs)
+template <int CG> SA_HD void tc_commit(uint64_t *bar) {
+  if (CG == 1)
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     sa_smem_u32(bar))
+                 : "memory");
+  else
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            sa_smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
 }
-SA_HD void tc_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-      "l"(a), "l"(b), "r"(IDESC), "r"(acc)
-      : "memory");
+template <int CG> SA_HD void tc_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+  if (CG == 1)
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+        "l"(a), "l"(b), "r"(TcCfg<1>::IDESC), "r"(acc)
+        : "memory");
+  else
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+        "l"(a), "l"(b), "r"(TcCfg<2>::IDESC), "r"(acc)
+        : "memory");
 }
 SA_HD void mbar_init(uint64_t *bar, uint32_t count) { sa_mbar_init(bar, count); }
-SA_HD void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa_smem_u32(bar)) : "memory");
+// arrive on a barrier given by its shared::cluster address (own or the leader's)
+SA_HD void mbar_arrive_cl(uint32_t cl_addr) {
+  // default .release.cta semantics, as CUTLASS's ClusterBarrier::arrive(cta_id): the
+  // .cluster-scope form costs a MEMBAR.GPU per arrive (measured: 2.8 vs 1.7 ms)
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
+}
+SA_HD void tma_load_2d_cg2(uint32_t dst, const CUtensorMap *map, int c0, int c1, uint32_t lead_bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(lead_bar)
+      : "memory");
+}
+SA_HD uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+SA_HD void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 SA_HD uint32_t bf2(float hi, float lo) {  // {lo -> bits 0..15, hi -> bits 16..31}, RN
@@ -94,9 +138,12 @@ SA_HD uint32_t bf2(float hi, float lo) {  // {lo -> bits 0..15, hi -> bits 16..3
         "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                                                              \
       : "r"(taddr))
 
+template <int CG>
 __global__ void __launch_bounds__(THREADS, 1)
     k_ndft_tc(const __grid_constant__ CUtensorMap wmap, const float4 *__restrict__ x, float *__restrict__ y,
               int64_t batch, int n, float gain, int use_gain) {
+  using C = TcCfg<CG>;
+  constexpr int NSLOT = C::NSLOT, SLOT = C::SLOT, B_TILE = C::B_TILE;
   extern __shared__ unsigned char smem_raw[];
   unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t *full = (uint64_t *)(smem + NSLOT * SLOT);
@@ -106,56 +153,75 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t *tmem_holder = (uint32_t *)(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 1 ? 0 : cluster_rank();
+  const int64_t cl = blockIdx.x / CG, ncl = gridDim.x / CG;
   const int ot_count = (2 * n) / BN;
-  const int64_t vt_count = (batch + BM - 1) / BM;
+  const int64_t vt_count = (batch + BM * CG - 1) / (BM * CG);
   const int64_t ntiles = vt_count * ot_count;
   const int kslots = n / KC;
+  // the leader CTA's full / tempty barriers as shared::cluster addresses
+  auto lead = [&](uint64_t *bar) { return CG == 1 ? sa_smem_u32(bar) : sa_mapa(sa_smem_u32(bar), 0); };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSLOT; ++s) {
-      mbar_init(&full[s], 1 + CONV_WARPS);
+      mbar_init(&full[s], 1 + CG * CONV_WARPS);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], 4 * CG);
     }
     sa_fence_mbar_init();
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     sa_smem_u32(tmem_holder)),
-                 "r"(TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       sa_smem_u32(tmem_holder)),
+                   "r"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       sa_smem_u32(tmem_holder)),
+                   "r"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 1) __syncthreads();
+  else cluster_sync_all();  // barrier inits + TMEM allocation visible pair-wide
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
+  // this CTA's slots: it -> (tile cl + (it / kslots) ncl, K chunk it % kslots)
+  const int64_t my_tiles = cl < ntiles ? (ntiles - 1 - cl) / ncl + 1 : 0;
+  const int64_t total = my_tiles * kslots;
+
   if (warp == 0) {
-    // ---- TMA producer: twiddle operand tiles ----
+    // ---- TMA producer: this CTA's rows of the twiddle operand tiles ----
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(&wmap) : "memory");
-      uint32_t it = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int o0 = (int)(t % ot_count) * BN;
-        for (int kc = 0; kc < kslots; ++kc, ++it) {
-          const int s = it % NSLOT;
-          sa_mbar_wait(&empty[s], ((it / NSLOT) & 1) ^ 1);
-          unsigned char *b = smem + s * SLOT + 3 * A_TILE;
-          sa_mbar_expect_tx(&full[s], 3 * B_TILE);
+      for (int64_t it = 0; it < total; ++it) {
+        const int64_t lt = it / kslots;
+        const int kc = (int)(it - lt * kslots);
+        const int o0 = (int)((cl + lt * ncl) % ot_count) * BN + (int)rank * C::BROWS;
+        const int s = (int)(it % NSLOT);
+        sa_mbar_wait(&empty[s], ((it / NSLOT) & 1) ^ 1);
+        unsigned char *b = smem + s * SLOT + 3 * A_TILE;
+        if (rank == 0) sa_mbar_expect_tx(&full[s], CG * 3 * B_TILE);
 #pragma unroll
-          for (int p = 0; p < 3; ++p) sa_tma_load_2d(b + p * B_TILE, &wmap, kc * KS, p * 2 * n + o0, &full[s]);
+        for (int p = 0; p < 3; ++p) {
+          if (CG == 1) sa_tma_load_2d(b + p * B_TILE, &wmap, kc * KS, p * 2 * n + o0, &full[s]);
+          else tma_load_2d_cg2(sa_smem_u32(b + p * B_TILE), &wmap, kc * KS, p * 2 * n + o0, lead(&full[s]));
         }
       }
     }
   } else if (warp == 1) {
-    // ---- MMA issuer ----
-    if (lane == 0) {
+    // ---- MMA issuer (the leader CTA) ----
+    if (lane == 0 && rank == 0) {
       uint32_t it = 0, lt = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+      for (int64_t t = cl; t < ntiles; t += ncl, ++lt) {
         const uint32_t acc = lt & 1;
         sa_mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -172,23 +238,23 @@ __global__ void __launch_bounds__(THREADS, 1)
                            aX1 = sdesc(base + 2 * A_TILE + off);
             const uint64_t bW0 = sdesc(base + 3 * A_TILE + off), bW1 = sdesc(base + 3 * A_TILE + B_TILE + off),
                            bWs = sdesc(base + 3 * A_TILE + 2 * B_TILE + off);
-            tc_mma(d, aS, bW0, (kc | ks) != 0);
-            tc_mma(d, aS, bW1, 1);
-            tc_mma(d, aX0, bWs, 1);
-            tc_mma(d, aX1, bWs, 1);
+            tc_mma<CG>(d, aS, bW0, (kc | ks) != 0);
+            tc_mma<CG>(d, aS, bW1, 1);
+            tc_mma<CG>(d, aX0, bWs, 1);
+            tc_mma<CG>(d, aX1, bWs, 1);
           }
-          tc_commit(&empty[s]);
+          tc_commit<CG>(&empty[s]);
         }
-        tc_commit(&tfull[acc]);
+        tc_commit<CG>(&tfull[acc]);
       }
     }
   } else if (warp < 6) {
-    // ---- epilogue: TMEM -> y ----
+    // ---- epilogue: this CTA's 128 TMEM lanes -> y ----
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     uint32_t lt = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+    for (int64_t t = cl; t < ntiles; t += ncl, ++lt) {
       const uint32_t acc = lt & 1;
-      const int64_t v = (t / ot_count) * BM + q * 32 + lane;
+      const int64_t v = (t / ot_count) * (BM * CG) + rank * BM + q * 32 + lane;
       const int o0 = (int)(t % ot_count) * BN;
       sa_mbar_wait(&tfull[acc], (lt >> 1) & 1);
       tc_fence_after();
@@ -207,36 +273,36 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) mbar_arrive_cl(lead(&tempty[acc]));
     }
   } else {
     // ---- converters: x -> S, X0, X1 (bf16, SWIZZLE_64B K-major) ----
-    // Each thread owns sample pair h of rows r0 + 32 i; x for slot it+3 is in
-    // flight (three register sets) while slot it is converted.
-    const int ct = threadIdx.x - 6 * 32;  // 0..255
+    // Each thread owns sample pair h of rows r0 + 32 i.  x for slot it+3 is in
+    // flight (three register sets) while slot it is converted.  Loads are
+    // unconditional (row and slot clamped) so no select waits on them; rows
+    // >= batch convert a copy of the last row, whose outputs are never stored.
+    const int ct = threadIdx.x - 6 * 32;  // 0..32 CONV_WARPS - 1
     const int h = ct & 7;                 // sample pair 2h, 2h+1 of the slot
-    const int r0 = ct >> 3;               // rows r0 + 32 i
-    const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const int64_t total = my_tiles * kslots;
+    const int r0 = ct >> 3;               // rows r0 + CROWS i
     const uint32_t sbase = sa_smem_u32(smem);
-    auto load = [&](float4(&b)[4], int64_t it) {
-      if (it >= total) return;
+    auto load = [&](float4(&b)[RPT], int64_t it) {
+      if (it >= total) it = total > 0 ? total - 1 : 0;
       const int64_t lt = it / kslots;
       const int kc = (int)(it - lt * kslots);
-      const int64_t vbase = ((blockIdx.x + lt * gridDim.x) / ot_count) * BM;
+      const int64_t vbase = ((cl + lt * ncl) / ot_count) * (BM * CG) + rank * BM;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int64_t v = vbase + r0 + 32 * i;
-        b[i] = v < batch ? __ldg(&x[(v * n + (int64_t)kc * KC) / 2 + h]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int i = 0; i < RPT; ++i) {
+        const int64_t v = vbase + r0 + CROWS * i;
+        b[i] = __ldg(&x[((v < batch ? v : batch - 1) * n + (int64_t)kc * KC) / 2 + h]);
       }
     };
-    auto convert = [&](const float4(&b)[4], int64_t it) {
+    auto convert = [&](const float4(&b)[RPT], int64_t it) {
       const int s = (int)(it % NSLOT);
       sa_mbar_wait(&empty[s], ((it / NSLOT) & 1) ^ 1);
       const uint32_t a = sbase + s * SLOT;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int r = r0 + 32 * i;
+      for (int i = 0; i < RPT; ++i) {
+        const int r = r0 + CROWS * i;
         float4 f = b[i];
         if (use_gain) f = make_float4(sa_mul(gain, f.x), sa_mul(gain, f.y), sa_mul(gain, f.z), sa_mul(gain, f.w));
         const uint32_t s01 = bf2(sa_sgn(f.y), sa_sgn(f.x)), s23 = bf2(sa_sgn(f.w), sa_sgn(f.z));
@@ -251,9 +317,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       sa_fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05.mma
       __syncwarp();
-      if (lane == 0) mbar_arrive(&full[s]);
+      if (lane == 0) mbar_arrive_cl(lead(&full[s]));
     };
-    float4 b0[4], b1[4], b2[4];
+    float4 b0[RPT], b1[RPT], b2[RPT];
     load(b0, 0);
     load(b1, 1);
     load(b2, 2);
@@ -272,10 +338,14 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (CG == 1) __syncthreads();
+  else cluster_sync_all();  // no CTA leaves while its pair may still signal it
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+    if (CG == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
   }
 }
 
@@ -323,6 +393,7 @@ int64_t sa_ndft_tc_wbytes(int64_t n) { return 3 * (2 * n) * (2 * n) * 2; }
 int sa_launch_ndft_tc(const void *x, void *y, int64_t batch, int64_t n, const SaTwiddles *tw_c, double gain,
                       cudaStream_t s) {
   if (!sa_ndft_tc_supported(tw_c->dtype, n)) return SA_ERR_UNSUPPORTED;
+  if (((uintptr_t)x | (uintptr_t)y) & 15) return SA_ERR_UNSUPPORTED;  // TMA / float4 epilogue alignment
   if (batch == 0) return SA_OK;
   SaTwiddles *tw = const_cast<SaTwiddles *>(tw_c);
   {
@@ -341,10 +412,15 @@ int sa_launch_ndft_tc(const void *x, void *y, int64_t batch, int64_t n, const Sa
     sa_set_error("cuTensorMapEncodeTiled unavailable");
     return SA_ERR_CUDA;
   }
+#ifndef SA_NDFT_TC_CG
+#define SA_NDFT_TC_CG 2
+#endif
+  constexpr int CG = SA_NDFT_TC_CG;
+  using Cf = TcCfg<CG>;
   CUtensorMap map;
   cuuint64_t dims[2] = {(cuuint64_t)(2 * n), (cuuint64_t)(6 * n)};
   cuuint64_t strides[1] = {(cuuint64_t)(2 * n * 2)};
-  cuuint32_t box[2] = {(cuuint32_t)KS, (cuuint32_t)BN};
+  cuuint32_t box[2] = {(cuuint32_t)KS, (cuuint32_t)Cf::BROWS};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, tw->tcw, dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -357,15 +433,27 @@ int sa_launch_ndft_tc(const void *x, void *y, int64_t batch, int64_t n, const Sa
   int dev = 0;
   SA_CUDA_TRY(cudaGetDevice(&dev));
   if (dev >= 64 || !smem_set[dev]) {
-    SA_CUDA_TRY(cudaFuncSetAttribute(k_ndft_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    SA_CUDA_TRY(cudaFuncSetAttribute(k_ndft_tc<CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
     if (dev < 64) smem_set[dev] = true;
   }
   int sms = 0;
   SA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int64_t ntiles = ((batch + BM - 1) / BM) * ((2 * n) / BN);
-  const int grid = (int)(ntiles < sms ? ntiles : sms);
-  k_ndft_tc<<<grid, THREADS, SMEM, s>>>(map, (const float4 *)x, (float *)y, batch, (int)n, (float)gain,
-                                        gain != 1.0);
+  const int64_t ntiles = ((batch + BM * CG - 1) / (BM * CG)) * ((2 * n) / BN);
+  const int64_t units = ntiles < sms / CG ? ntiles : sms / CG;  // persistent: one CTA group per SM group
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(units * CG));
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = Cf::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SA_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_ndft_tc<CG>, map, (const float4 *)x, (float *)y, batch, (int)n,
+                                 (float)gain, (int)(gain != 1.0)));
   SA_LAUNCH_CHECK();
   return SA_OK;
 }
