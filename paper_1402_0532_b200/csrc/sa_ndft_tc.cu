@@ -23,14 +23,17 @@
 //               (256 outputs x 16 samples per pair), completing on the leader's barrier
 //   warp 1      TMEM allocator; in the leader CTA the single-thread MMA issuer:
 //               tcgen05.mma.cta_group::2, M = 256 (128 vectors per CTA), N = 256, K = 16
-//   warps 2-5   epilogue: tcgen05.ld 32x32b -> fp32 rows of y (2 TMEM accumulators)
+//   warps 2-5   epilogue: tcgen05.ld 32x32b -> fp32 rows of y
+// A tile is 256 vectors x 512 outputs (two N = 256 MMAs per A tile, the whole of
+// TMEM as one accumulator) when 2n % 512 == 0, else 256 outputs with two
+// double-buffered accumulators.
 //   warps 6-13  converters: x (c64, gain applied) -> S, X0, X1 bf16 tiles in the
 //               SWIZZLE_64B K-major layout, fence.proxy.async, arrive on the leader
-// Four smem slots of 48 KB per CTA (3 A tiles of 8 KB + 3 half B tiles of 8 KB).
-// Measured C2 (65536 x 1024 c64): 1.59 ms = 1.38 PFLOP/s of bf16 MMA.  Dead
-// ends: single-CTA M = 128 (1.71 ms), TMA-staged x (1.73-1.76
-// ms: fewer slots fit), 16 converter warps (1.61 ms), cluster-scope
-// release/acquire on the pair barriers (MEMBAR.GPU per arrive: 2.8 ms).
+// Three smem slots of 72 KB per CTA (3 A tiles of 8 KB + 3 x 2 half-B tiles of 8 KB).
+// Measured C2 (65536 x 1024 c64): 1.34 ms = 1.64 PFLOP/s of bf16 MMA (256-output
+// tiles: 1.59 ms).  Dead ends: single-CTA M = 128 (1.71 ms),
+// TMA-staged x (1.73-1.76 ms: fewer slots fit), 16 converter warps (1.61 ms),
+// cluster-scope release/acquire on the pair barriers (MEMBAR.GPU per arrive: 2.8 ms).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -42,7 +45,7 @@
 namespace {
 
 constexpr int BM = 128;          // vectors per CTA per tile (TMEM lanes)
-constexpr int BN = 256;          // outputs per tile (128 bins x {re, im}; TMEM columns)
+constexpr int BN = 256;          // outputs per MMA (128 bins x {re, im}; TMEM columns)
 constexpr int KC = 16;           // samples per slot
 constexpr int KS = 2 * KC;       // bf16 per operand row per slot = 64 B (SWIZZLE_64B)
 constexpr int A_TILE = BM * KS * 2;  // 8 KB
@@ -53,16 +56,21 @@ constexpr int CONV_WARPS = SA_TC_CONV_WARPS;
 constexpr int CROWS = CONV_WARPS * 4;   // rows covered per pass (8 threads per row)
 constexpr int RPT = BM / CROWS;         // rows per converter thread
 constexpr int THREADS = 32 * (6 + CONV_WARPS);
-constexpr int TMEM_COLS = 512;   // two accumulators of BN columns
+constexpr int TMEM_COLS = 512;   // all of TMEM: 512 / TN accumulators of TN columns
 
 // CG = CTAs per MMA (tcgen05 cta_group).  CG = 2: a CTA pair (cluster of 2) issues
 // M = 256 MMAs from the leader; each CTA holds its 128 vector rows of A and half
 // (128 rows) of every twiddle tile, so each SM streams half the B bytes.
-template <int CG> struct TcCfg {
-  static constexpr int BROWS = BN / CG;               // twiddle rows per CTA per tile
-  static constexpr int B_TILE = BROWS * KS * 2;       // 16 KB (CG 1) / 8 KB (CG 2)
+// TN = outputs per tile (256 or 512): a 512-output tile issues two N = 256 MMAs per
+// A tile, so each converted x tile feeds twice the outputs (half the x loads and
+// conversions per step) at the price of one TMEM accumulator instead of two.
+template <int CG, int TN> struct TcCfg {
+  static constexpr int NH = TN / BN;                  // N = 256 halves per tile
+  static constexpr int BROWS = BN / CG;               // twiddle rows per CTA per half
+  static constexpr int B_TILE = NH * BROWS * KS * 2;  // per piece: 16 KB (CG 1) / 8 KB (CG 2) per half
   static constexpr int SLOT = 3 * A_TILE + 3 * B_TILE;
-  static constexpr int NSLOT = CG == 1 ? 3 : 4;
+  static constexpr int NSLOT = (227 * 1024 - 2048) / SLOT < 4 ? (227 * 1024 - 2048) / SLOT : 4;
+  static constexpr int NACC = TMEM_COLS / TN;
   static constexpr int SMEM = NSLOT * SLOT + 1024 + 256;
   // instruction descriptor: kind::f16, A = B = bf16, D = f32, both K-major, M = 128 CG, N = 256
   static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
@@ -95,13 +103,13 @@ template <int CG> SA_HD void tc_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t
     asm volatile(
         "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
         " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-        "l"(a), "l"(b), "r"(TcCfg<1>::IDESC), "r"(acc)
+        "l"(a), "l"(b), "r"(TcCfg<1, 256>::IDESC), "r"(acc)
         : "memory");
   else
     asm volatile(
         "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
         " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-        "l"(a), "l"(b), "r"(TcCfg<2>::IDESC), "r"(acc)
+        "l"(a), "l"(b), "r"(TcCfg<2, 256>::IDESC), "r"(acc)
         : "memory");
 }
 SA_HD void mbar_init(uint64_t *bar, uint32_t count) { sa_mbar_init(bar, count); }
@@ -144,11 +152,12 @@ SA_HD uint32_t bf2(float hi, float lo) {  // {lo -> bits 0..15, hi -> bits 16..3
         "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                                                              \
       : "r"(taddr))
 
-template <int CG>
+template <int CG, int TN>
 __global__ void __launch_bounds__(THREADS, 1)
     k_ndft_tc(const __grid_constant__ CUtensorMap wmap, const float4 *__restrict__ x, float *__restrict__ y,
               int64_t batch, int n, float gain, int use_gain) {
-  using C = TcCfg<CG>;
+  using C = TcCfg<CG, TN>;
+  constexpr int NH = C::NH, NACC = C::NACC;
   constexpr int NSLOT = C::NSLOT, SLOT = C::SLOT, B_TILE = C::B_TILE;
   extern __shared__ unsigned char smem_raw[];
   unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -161,7 +170,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = CG == 1 ? 0 : cluster_rank();
   const int64_t cl = blockIdx.x / CG, ncl = gridDim.x / CG;
-  const int ot_count = (2 * n) / BN;
+  const int ot_count = (2 * n) / TN;
   const int64_t vt_count = (batch + BM * CG - 1) / (BM * CG);
   const int64_t ntiles = vt_count * ot_count;
   const int kslots = n / KC;
@@ -173,7 +182,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&full[s], 1 + CG * CONV_WARPS);
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < NACC; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4 * CG);
     }
@@ -211,16 +220,20 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int64_t it = 0; it < total; ++it) {
         const int64_t lt = it / kslots;
         const int kc = (int)(it - lt * kslots);
-        const int o0 = (int)((cl + lt * ncl) % ot_count) * BN + (int)rank * C::BROWS;
+        const int o0 = (int)((cl + lt * ncl) % ot_count) * TN + (int)rank * C::BROWS;
         const int s = (int)(it % NSLOT);
         sa_mbar_wait(&empty[s], ((it / NSLOT) & 1) ^ 1);
         unsigned char *b = smem + s * SLOT + 3 * A_TILE;
         if (rank == 0) sa_mbar_expect_tx(&full[s], CG * 3 * B_TILE);
 #pragma unroll
-        for (int p = 0; p < 3; ++p) {
-          if (CG == 1) sa_tma_load_2d(b + p * B_TILE, &wmap, kc * KS, p * 2 * n + o0, &full[s]);
-          else tma_load_2d_cg2(sa_smem_u32(b + p * B_TILE), &wmap, kc * KS, p * 2 * n + o0, lead(&full[s]));
-        }
+        for (int p = 0; p < 3; ++p)
+#pragma unroll
+          for (int hh = 0; hh < NH; ++hh) {
+            unsigned char *dst = b + p * B_TILE + hh * C::BROWS * KS * 2;
+            const int row = p * 2 * n + o0 + hh * BN;
+            if (CG == 1) sa_tma_load_2d(dst, &wmap, kc * KS, row, &full[s]);
+            else tma_load_2d_cg2(sa_smem_u32(dst), &wmap, kc * KS, row, lead(&full[s]));
+          }
       }
     }
   } else if (warp == 1) {
@@ -228,10 +241,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0 && rank == 0) {
       uint32_t it = 0, lt = 0;
       for (int64_t t = cl; t < ntiles; t += ncl, ++lt) {
-        const uint32_t acc = lt & 1;
-        sa_mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+        const uint32_t acc = lt % NACC;
+        sa_mbar_wait(&tempty[acc], ((lt / NACC) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem + acc * BN;
+        const uint32_t d = tmem + acc * TN;
         for (int kc = 0; kc < kslots; ++kc, ++it) {
           const int s = it % NSLOT;
           sa_mbar_wait(&full[s], (it / NSLOT) & 1);
@@ -242,12 +255,16 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint32_t off = ks * 32;  // 16 bf16 along K inside the 64-B swizzled row
             const uint64_t aS = sdesc(base + off), aX0 = sdesc(base + A_TILE + off),
                            aX1 = sdesc(base + 2 * A_TILE + off);
-            const uint64_t bW0 = sdesc(base + 3 * A_TILE + off), bW1 = sdesc(base + 3 * A_TILE + B_TILE + off),
-                           bWs = sdesc(base + 3 * A_TILE + 2 * B_TILE + off);
-            tc_mma<CG>(d, aS, bW0, (kc | ks) != 0);
-            tc_mma<CG>(d, aS, bW1, 1);
-            tc_mma<CG>(d, aX0, bWs, 1);
-            tc_mma<CG>(d, aX1, bWs, 1);
+#pragma unroll
+            for (int hh = 0; hh < NH; ++hh) {
+              const uint32_t bb = base + 3 * A_TILE + hh * C::BROWS * KS * 2 + off;
+              const uint64_t bW0 = sdesc(bb), bW1 = sdesc(bb + B_TILE), bWs = sdesc(bb + 2 * B_TILE);
+              const uint32_t dh = d + hh * BN;
+              tc_mma<CG>(dh, aS, bW0, (kc | ks) != 0);
+              tc_mma<CG>(dh, aS, bW1, 1);
+              tc_mma<CG>(dh, aX0, bWs, 1);
+              tc_mma<CG>(dh, aX1, bWs, 1);
+            }
           }
           tc_commit<CG>(&empty[s]);
         }
@@ -259,16 +276,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     uint32_t lt = 0;
     for (int64_t t = cl; t < ntiles; t += ncl, ++lt) {
-      const uint32_t acc = lt & 1;
+      const uint32_t acc = lt % NACC;
       const int64_t v = (t / ot_count) * (BM * CG) + rank * BM + q * 32 + lane;
-      const int o0 = (int)(t % ot_count) * BN;
-      sa_mbar_wait(&tfull[acc], (lt >> 1) & 1);
+      const int o0 = (int)(t % ot_count) * TN;
+      sa_mbar_wait(&tfull[acc], (lt / NACC) & 1);
       tc_fence_after();
       float4 *dst = (float4 *)(y + v * 2 * n + o0);
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = 0; c < TN / 32; ++c) {
         uint32_t r[32];
-        SA_LD32(r, tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32);
+        SA_LD32(r, tmem + ((uint32_t)(q * 32) << 16) + acc * TN + c * 32);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (v < batch) {
 #pragma unroll
@@ -388,6 +405,51 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn_tc() {
   return fn;
 }
 
+template <int CG, int TN>
+int launch_tc(const void *x, void *y, int64_t batch, int64_t n, SaTwiddles *tw, double gain, cudaStream_t s) {
+  using Cf = TcCfg<CG, TN>;
+  auto enc = encode_fn_tc();
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)(2 * n), (cuuint64_t)(6 * n)};
+  cuuint64_t strides[1] = {(cuuint64_t)(2 * n * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)KS, (cuuint32_t)Cf::BROWS};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, tw->tcw, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    sa_set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return SA_ERR_CUDA;
+  }
+  static bool smem_set[64] = {};
+  int dev = 0;
+  SA_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev >= 64 || !smem_set[dev]) {
+    SA_CUDA_TRY(cudaFuncSetAttribute(k_ndft_tc<CG, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
+    if (dev < 64) smem_set[dev] = true;
+  }
+  int sms = 0;
+  SA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t ntiles = ((batch + BM * CG - 1) / (BM * CG)) * ((2 * n) / TN);
+  const int64_t units = ntiles < sms / CG ? ntiles : sms / CG;  // persistent: one CTA group per SM group
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(units * CG));
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = Cf::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SA_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_ndft_tc<CG, TN>, map, (const float4 *)x, (float *)y, batch, (int)n,
+                                 (float)gain, (int)(gain != 1.0)));
+  SA_LAUNCH_CHECK();
+  return SA_OK;
+}
+
 }  // namespace
 
 bool sa_ndft_tc_supported(int dtype, int64_t n) {
@@ -422,44 +484,10 @@ int sa_launch_ndft_tc(const void *x, void *y, int64_t batch, int64_t n, const Sa
 #define SA_NDFT_TC_CG 2
 #endif
   constexpr int CG = SA_NDFT_TC_CG;
-  using Cf = TcCfg<CG>;
-  CUtensorMap map;
-  cuuint64_t dims[2] = {(cuuint64_t)(2 * n), (cuuint64_t)(6 * n)};
-  cuuint64_t strides[1] = {(cuuint64_t)(2 * n * 2)};
-  cuuint32_t box[2] = {(cuuint32_t)KS, (cuuint32_t)Cf::BROWS};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, tw->tcw, dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    sa_set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
-    return SA_ERR_CUDA;
-  }
-  static bool smem_set[64] = {};
-  int dev = 0;
-  SA_CUDA_TRY(cudaGetDevice(&dev));
-  if (dev >= 64 || !smem_set[dev]) {
-    SA_CUDA_TRY(cudaFuncSetAttribute(k_ndft_tc<CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
-    if (dev < 64) smem_set[dev] = true;
-  }
-  int sms = 0;
-  SA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int64_t ntiles = ((batch + BM * CG - 1) / (BM * CG)) * ((2 * n) / BN);
-  const int64_t units = ntiles < sms / CG ? ntiles : sms / CG;  // persistent: one CTA group per SM group
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(units * CG));
-  cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = Cf::SMEM;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  SA_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_ndft_tc<CG>, map, (const float4 *)x, (float *)y, batch, (int)n,
-                                 (float)gain, (int)(gain != 1.0)));
-  SA_LAUNCH_CHECK();
-  return SA_OK;
+#ifndef SA_NDFT_TC_TN
+#define SA_NDFT_TC_TN 512
+#endif
+  return (2 * n) % SA_NDFT_TC_TN == 0 ? launch_tc<CG, SA_NDFT_TC_TN>(x, y, batch, n, tw, gain, s)
+                                      : launch_tc<CG, 256>(x, y, batch, n, tw, gain, s);
 }
+
