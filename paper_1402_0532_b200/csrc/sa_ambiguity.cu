@@ -552,6 +552,11 @@ int launch_integrate(int lag_kind, const void *survv, const void *refv, int64_t 
   SA_CUDA_TRY(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const size_t smax = (size_t)smem_max;
   const bool tiles_ok = mode == SA_NDFT_FAST && tb % 8 == 0 && tb <= 0x3fffffff && m <= 0x7fffffff;
+#ifndef SA_NO_LAG_TC
+  // fast mode, complex64, T % 128 == 0: Hankel GEMM on the tcgen05 tensor cores (sa_lag_tc.cu)
+  if (mode == SA_NDFT_FAST && !exact_lag && sa_lag_tc_supported(sizeof(T) == 4 ? SA_C64 : SA_C128, tb, m, survv))
+    return sa_launch_lag_tc(survv, refv, l0, l_count, m, tb, conj, zv, s);
+#endif
 
   // fast mode, complex64, T % 16 == 0: packed pair kernel.  NT is the largest of
   // 8/4/2/1 that leaves >= 3 waves of 2 CTAs per SM and fits shared memory.

@@ -1,0 +1,271 @@
+// sa_lag_tc.cu -- block-integrated ⊙ lag products (the range-Doppler map's lag
+// stage, sa_ambiguity.cu) on the tcgen05 tensor cores, fast mode, complex64.
+//
+//   z_l[q] = Σ_{t<T} s[qT+t] ⊙ c[qT+t-l],   c = conj(ref) (ref[<0] = 0)
+//
+// Fast mode evaluates each ⊙ through the sign-split identity (sa_ambiguity.cu):
+//   Re = Σ sgn(sr) cr + sr sgn(cr) − sgn(si) ci − si sgn(ci)
+//   Im = Σ sgn(si) cr + si sgn(cr) + sgn(sr) ci + sr sgn(ci)
+// so for one block q every real term is a correlation Σ_t a[t] b[t − l].  With
+// lag l = lbase + 8 l1 + l0 (l1 < 128, l0 < 8) and u = t − 8 l1 it is a GEMM
+//   Z[l1, l0] = Σ_u A[l1, u] B[l0, u],   A[l1, u] = a[u + 8 l1],  B[l0, u] = b[u − l0]
+// over u in [−1024, T).  A is a Hankel matrix: in the K-major no-swizzle UMMA
+// layout the 8 rows of a core matrix sit 16 B (= 8 bf16 = one l1 step) apart, so
+// the descriptor (LBO 16 B, SBO 128 B) reads A straight out of one zero-padded
+// linear array per operand kind -- nothing is materialised.  B (8 shifts x 2
+// components x pieces) is built per K chunk of 128 u.  As in sa_ndft_tc.cu the
+// non-sign operands are split in two bf16 pieces (hi + lo) and one factor of
+// every product is a sign; accumulation is fp32 in TMEM.
+//
+// Per K step (16 u) six MMAs, M = 128 (l1) x K = 16:
+//   D1 (32 cols: Re_hi, Im_hi, Re_lo, Im_lo x 8 l0) += sgn(sr) x B1 + sgn(si) x B2   (N = 32)
+//   D2 (16 cols: Re, Im x 8 l0)                    += sr_hi x B3 + sr_lo x B3 + si_hi x B4 + si_lo x B4
+//   B1 = [cr_hi, ci_hi, cr_lo, ci_lo], B2 = [−ci_hi, cr_hi, −ci_lo, cr_lo],
+//   B3 = [sgn cr, sgn ci], B4 = [−sgn ci, sgn cr]   (each block of 8 rows = l0 0..7)
+// Epilogue: Re = D1[l0] + D1[16+l0] + D2[l0], Im = D1[8+l0] + D1[24+l0] + D2[8+l0].
+//
+// One CTA per integration block q (256 threads, 2 CTAs per SM), looping over
+// groups of 1024 lags; the last group may be partial (rows >= l_count dropped).
+#include <cuda.h>
+
+#include "sa_internal.h"
+#include "sa_regs.cuh"
+
+namespace {
+
+constexpr int LGRP = 1024;       // lags per group (128 l1 x 8 l0)
+constexpr int PAD = 1024;        // zero padding in front of the A arrays (u >= -1024)
+constexpr int KCH = 128;         // u per K chunk
+constexpr int NKIND = 6;         // A kinds: sgn sr, sgn si, sr_hi, sr_lo, si_hi, si_lo
+constexpr int BROWS = 96;        // B rows per chunk: B1 32 + B2 32 + B3 16 + B4 16
+constexpr int B_BYTES = BROWS * KCH * 2;  // 24 KB
+constexpr int THREADS = 256;
+constexpr int TMEM_COLS = 64;
+
+__host__ __device__ inline int a_len(int tb) { return tb + 2 * PAD; }  // u + 8 l1 in [-1024, T + 1016), padded
+__host__ __device__ inline size_t smem_bytes(int tb) { return (size_t)NKIND * a_len(tb) * 2 + 2 * B_BYTES + 1024 + 64; }
+
+// instruction descriptor: kind::f16, bf16 x bf16 -> f32, K-major, M = 128, N = n
+constexpr uint32_t idesc(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+// K-major, no swizzle: core matrices of 8 rows x 16 B; LBO = next 8 K elements, SBO = next 8 rows
+SA_HD uint64_t sdesc_ns(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(sbo >> 4) << 32) |
+         ((uint64_t)1 << 46);
+}
+SA_HD void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(acc)
+      : "memory");
+}
+SA_HD void commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   sa_smem_u32(bar))
+               : "memory");
+}
+SA_HD void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+SA_HD void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+SA_HD uint32_t bf2(float hi, float lo) {  // {lo -> bits 0..15, hi -> bits 16..31}, RN
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+#define SA_LD16(v, taddr)                                                                                  \
+  asm volatile(                                                                                            \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"    \
+      " [%16];"                                                                                            \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),    \
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),           \
+        "=r"(v[15])                                                                                        \
+      : "r"(taddr))
+
+// the 8 conj-ref values a B-builder thread needs: c[g0 .. g0+7] (0 before the signal start)
+SA_HD void load_c(float2 (&cv)[8], const float2 *__restrict__ ref, int64_t g0, float csign) {
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int64_t g = g0 + e;
+    float2 v = g >= 0 ? __ldg(&ref[g]) : make_float2(0.f, 0.f);
+    cv[e] = make_float2(v.x, csign * v.y);
+  }
+}
+
+__global__ void __launch_bounds__(THREADS, 2)
+    k_lag_tc(const float2 *__restrict__ surv, const float2 *__restrict__ ref, int64_t l0g, int64_t l_count,
+             int64_t m, int tb, float csign, float2 *__restrict__ z) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int al = a_len(tb);
+  uint16_t *A = (uint16_t *)smem;                      // NKIND x al bf16
+  unsigned char *Bb = smem + (size_t)NKIND * al * 2;   // 2 x B_BYTES (1024-aligned: al * 2 * 6 % 1024 == 0)
+  uint64_t *bar = (uint64_t *)(Bb + 2 * B_BYTES);      // MMA completion per B buffer
+  uint32_t *tmem_holder = (uint32_t *)(bar + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t q = blockIdx.x;
+  const int nch = (tb + PAD) / KCH;
+
+  if (tid == 0) {
+    sa_mbar_init(&bar[0], 1);
+    sa_mbar_init(&bar[1], 1);
+    sa_fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa_smem_u32(tmem_holder)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  // A: the surveillance block as six zero-padded linear bf16 arrays, a[t] at PAD + t
+  for (int j = 2 * tid; j < al; j += 2 * THREADS) {
+    const int t = j - PAD;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (t >= 0 && t < tb) v = __ldg((const float4 *)&surv[q * tb + t]);  // t even, tb even: 16-B aligned
+    const uint32_t sr = bf2(sa_sgn(v.z), sa_sgn(v.x)), si = bf2(sa_sgn(v.w), sa_sgn(v.y));
+    const uint32_t rh = bf2(v.z, v.x), ih = bf2(v.w, v.y);
+    const uint32_t rl = bf2(sa_sub(v.z, __uint_as_float(rh & 0xFFFF0000u)), sa_sub(v.x, __uint_as_float(rh << 16)));
+    const uint32_t il = bf2(sa_sub(v.w, __uint_as_float(ih & 0xFFFF0000u)), sa_sub(v.y, __uint_as_float(ih << 16)));
+    const uint32_t w[NKIND] = {sr, si, rh, rl, ih, il};
+#pragma unroll
+    for (int k = 0; k < NKIND; ++k) *(uint32_t *)&A[(size_t)k * al + j] = w[k];
+  }
+  sa_fence_proxy_async();
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_holder;
+  const uint32_t abase = sa_smem_u32(A), bbase = sa_smem_u32(Bb);
+
+  // B builders: thread (l0 = tid % 8, octet = (tid / 8) % 16, half = tid / 128)
+  const int bl0 = tid & 7, boct = (tid >> 3) & 15, bhalf = tid >> 7;
+  const int ngrp = (int)((l_count + LGRP - 1) / LGRP);
+  uint32_t cc = 0;  // chunk counter across groups (B buffer = cc & 1)
+  for (int gi = 0; gi < ngrp; ++gi) {
+    const int64_t lbase = l0g + (int64_t)gi * LGRP;
+    // c index of (u, l0): q T - lbase + u - l0
+    const int64_t cbase = q * tb - lbase - PAD - bl0 + boct * 8;
+    float2 cv[8];
+    load_c(cv, ref, cbase, csign);
+    for (int ch = 0; ch < nch; ++ch, ++cc) {
+      const int b = cc & 1;
+      if (cc >= 2) sa_mbar_wait(&bar[b], ((cc >> 1) - 1) & 1);  // MMAs that read this buffer are done
+      // build chunk ch of B into buffer b: rows (block of 8 = one component, row = l0), octet boct
+      {
+        unsigned char *B = Bb + b * B_BYTES;
+        float cr[8], ci[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) cr[e] = cv[e].x, ci[e] = cv[e].y;
+        uint32_t o = (uint32_t)boct * 128 + (uint32_t)bl0 * 16;  // (row l0, octet) inside an 8-row block
+        auto put = [&](int matrow0, int blk, const uint32_t(&w)[4]) {  // matrix at row offset matrow0 (rows), block blk
+          *(uint4 *)(B + (size_t)(matrow0 + blk * 8) / 8 * 2048 + o) = make_uint4(w[0], w[1], w[2], w[3]);
+        };
+        if (bhalf == 0) {
+          uint32_t rh[4], rl[4], ihh[4], il[4], nih[4], nil[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            rh[e] = bf2(cr[2 * e + 1], cr[2 * e]);
+            ihh[e] = bf2(ci[2 * e + 1], ci[2 * e]);
+            rl[e] = bf2(sa_sub(cr[2 * e + 1], __uint_as_float(rh[e] & 0xFFFF0000u)),
+                        sa_sub(cr[2 * e], __uint_as_float(rh[e] << 16)));
+            il[e] = bf2(sa_sub(ci[2 * e + 1], __uint_as_float(ihh[e] & 0xFFFF0000u)),
+                        sa_sub(ci[2 * e], __uint_as_float(ihh[e] << 16)));
+            nih[e] = ihh[e] ^ 0x80008000u;  // exact negation of both bf16 halves
+            nil[e] = il[e] ^ 0x80008000u;
+          }
+          put(0, 0, rh);     // B1: cr_hi
+          put(0, 1, ihh);    //     ci_hi
+          put(0, 2, rl);     //     cr_lo
+          put(0, 3, il);     //     ci_lo
+          put(32, 0, nih);   // B2: -ci_hi
+          put(32, 1, rh);    //     cr_hi
+          put(32, 2, nil);   //     -ci_lo
+          put(32, 3, rl);    //     cr_lo
+        } else {
+          uint32_t sr[4], si[4], nsi[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            sr[e] = bf2(sa_sgn(cr[2 * e + 1]), sa_sgn(cr[2 * e]));
+            si[e] = bf2(sa_sgn(ci[2 * e + 1]), sa_sgn(ci[2 * e]));
+            nsi[e] = si[e] ^ 0x80008000u;
+          }
+          put(64, 0, sr);    // B3: sgn cr
+          put(64, 1, si);    //     sgn ci
+          put(80, 0, nsi);   // B4: -sgn ci
+          put(80, 1, sr);    //     sgn cr
+        }
+      }
+      if (ch + 1 < nch) load_c(cv, ref, cbase + (int64_t)(ch + 1) * KCH, csign);  // next chunk's values
+      sa_fence_proxy_async();
+      fence_before();
+      __syncthreads();
+      if (tid == 0) {
+        fence_after();
+        const uint32_t bb = bbase + b * B_BYTES;
+#pragma unroll
+        for (int ks = 0; ks < KCH / 16; ++ks) {
+          const uint32_t ua = (uint32_t)(ch * KCH + ks * 16) * 2;  // byte offset of u0 + PAD in the A arrays
+          const uint32_t bo = bb + ks * 256;                      // 16 u = two 128-B core columns
+          const uint32_t acc = (ch | ks) != 0;
+          const uint64_t b1 = sdesc_ns(bo, 128, 2048), b2 = sdesc_ns(bo + 32 * KCH * 2, 128, 2048),
+                         b3 = sdesc_ns(bo + 64 * KCH * 2, 128, 2048), b4 = sdesc_ns(bo + 80 * KCH * 2, 128, 2048);
+          auto ad = [&](int k) { return sdesc_ns(abase + (uint32_t)k * al * 2 + ua, 16, 128); };
+          mma(tmem, ad(0), b1, idesc(32), acc);
+          mma(tmem, ad(1), b2, idesc(32), 1);
+          mma(tmem + 32, ad(2), b3, idesc(16), acc);
+          mma(tmem + 32, ad(3), b3, idesc(16), 1);
+          mma(tmem + 32, ad(4), b4, idesc(16), 1);
+          mma(tmem + 32, ad(5), b4, idesc(16), 1);
+        }
+        commit(&bar[b]);
+      }
+    }
+    // epilogue of this lag group: wait for the last chunk's MMAs (commit tracks all prior)
+    const uint32_t last = cc - 1;
+    sa_mbar_wait(&bar[last & 1], (last >> 1) & 1);
+    fence_after();
+    if (warp < 4) {
+      uint32_t d1[16], d2[16], d3[16];
+      const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
+      SA_LD16(d1, ta);
+      SA_LD16(d2, ta + 16);
+      SA_LD16(d3, ta + 32);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      const int l1 = warp * 32 + lane;
+#pragma unroll
+      for (int l0 = 0; l0 < 8; ++l0) {
+        const int64_t lag = lbase + 8 * l1 + l0 - l0g;  // row of z
+        if (lag < l_count) {
+          const float re = (__uint_as_float(d1[l0]) + __uint_as_float(d2[l0])) + __uint_as_float(d3[l0]);
+          const float im = (__uint_as_float(d1[8 + l0]) + __uint_as_float(d2[8 + l0])) + __uint_as_float(d3[8 + l0]);
+          z[lag * m + q] = make_float2(re, im);
+        }
+      }
+    }
+    fence_before();
+    __syncthreads();  // TMEM drained before the next group's first MMA overwrites it
+    fence_after();
+  }
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+}
+
+}  // namespace
+
+bool sa_lag_tc_supported(int dtype, int64_t tb, int64_t m, const void *surv) {
+  return dtype == SA_C64 && tb >= 128 && tb % KCH == 0 && tb <= 4096 && m <= 0x7fffffff &&
+         ((uintptr_t)surv & 15) == 0;
+}
+
+int sa_launch_lag_tc(const void *surv, const void *ref, int64_t l0, int64_t l_count, int64_t m, int64_t tb, int conj,
+                     void *z, cudaStream_t s) {
+  if (l_count == 0 || m == 0) return SA_OK;
+  const size_t bytes = smem_bytes((int)tb);
+  SA_CUDA_TRY(cudaFuncSetAttribute(k_lag_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  k_lag_tc<<<(unsigned)m, THREADS, bytes, s>>>((const float2 *)surv, (const float2 *)ref, l0, l_count, m, (int)tb,
+                                               conj ? -1.f : 1.f, (float2 *)z);
+  SA_LAUNCH_CHECK();
+  return SA_OK;
+}
