@@ -25,7 +25,8 @@
 // Epilogue: Re = D1[l0] + D1[16+l0] + D2[l0], Im = D1[8+l0] + D1[24+l0] + D2[8+l0].
 //
 // One CTA per integration block q (256 threads, 2 CTAs per SM), looping over
-// groups of 1024 lags; the last group may be partial (rows >= l_count dropped).
+// groups of 1024 lags aligned to lag multiples of 16; rows outside the call's
+// lag range are dropped.
 #include <cuda.h>
 
 #include "sa_internal.h"
@@ -141,10 +142,14 @@ __global__ void __launch_bounds__(THREADS, 2)
 
   // B builders: thread (l0 = tid % 8, octet = (tid / 8) % 16, half = tid / 128)
   const int bl0 = tid & 7, boct = (tid >> 3) & 15, bhalf = tid >> 7;
-  const int ngrp = (int)((l_count + LGRP - 1) / LGRP);
+  // Groups start at lag multiples of 16, so every (lag, t) product lands in the
+  // same row parity, column and K-step position whatever l0 the call starts at:
+  // lag shards (sharded.py) reproduce the single-call rows bit for bit.
+  const int64_t lalign = l0g - (l0g & 15);
+  const int ngrp = (int)((l0g - lalign + l_count + LGRP - 1) / LGRP);
   uint32_t cc = 0;  // chunk counter across groups (B buffer = cc & 1)
   for (int gi = 0; gi < ngrp; ++gi) {
-    const int64_t lbase = l0g + (int64_t)gi * LGRP;
+    const int64_t lbase = lalign + (int64_t)gi * LGRP;
     // c index of (u, l0): q T - lbase + u - l0
     const int64_t cbase = q * tb - lbase - PAD - bl0 + boct * 8;
     float2 cv[8];
@@ -237,7 +242,7 @@ __global__ void __launch_bounds__(THREADS, 2)
 #pragma unroll
       for (int l0 = 0; l0 < 8; ++l0) {
         const int64_t lag = lbase + 8 * l1 + l0 - l0g;  // row of z
-        if (lag < l_count) {
+        if (lag >= 0 && lag < l_count) {
           const float re = (__uint_as_float(d1[l0]) + __uint_as_float(d2[l0])) + __uint_as_float(d3[l0]);
           const float im = (__uint_as_float(d1[8 + l0]) + __uint_as_float(d2[8 + l0])) + __uint_as_float(d3[8 + l0]);
           z[lag * m + q] = make_float2(re, im);

@@ -71,12 +71,12 @@ def test_lag_tc_vs_fp64(sa, tb, m, l0, L, conj):
 
 
 def test_lag_tc_shard_offsets_bit_identical(sa):
-    """Lag shards starting at multiples of 16 reproduce the single-call rows
-    bit for bit (same u alignment of every product inside the MMA K steps), so
-    sharded maps equal the single-GPU map."""
+    """Lag shards reproduce the single-call rows bit for bit, whatever lag they
+    start at (groups are aligned to lag multiples of 16, so every product keeps
+    its u alignment inside the MMA K steps): sharded maps equal the single-GPU map."""
     surv, ref = signals(7, 2048 * 8)
     full = integrate(sa, surv, ref, 0, 2048, 8)
-    for a, b in ((0, 512), (512, 1024), (1024, 2048), (1536, 2048)):
+    for a, b in ((0, 512), (512, 1024), (1024, 2048), (1536, 2048), (3, 101), (101, 1337), (1337, 2048)):
         assert np.array_equal(integrate(sa, surv, ref, a, b - a, 8), full[a:b]), (a, b)
 
 
