@@ -40,7 +40,8 @@ constexpr int KCH = 128;         // u per K chunk
 constexpr int NKIND = 6;         // A kinds: sgn sr, sgn si, sr_hi, sr_lo, si_hi, si_lo
 constexpr int BROWS = 96;        // B rows per chunk: B1 32 + B2 32 + B3 16 + B4 16
 constexpr int B_BYTES = BROWS * KCH * 2;  // 24 KB
-constexpr int THREADS = 256;
+constexpr int BUILDERS = 256;    // warps 0-7 build the operands (warps 0-3 also drain TMEM)
+constexpr int THREADS = BUILDERS + 32;  // warp 8 issues the MMAs
 constexpr int TMEM_COLS = 64;
 
 __host__ __device__ inline int a_len(int tb) { return tb + 2 * PAD; }  // u + 8 l1 in [-1024, T + 1016), padded
@@ -102,8 +103,10 @@ __global__ void __launch_bounds__(THREADS, 2)
   const int al = a_len(tb);
   uint16_t *A = (uint16_t *)smem;                      // NKIND x al bf16
   unsigned char *Bb = smem + (size_t)NKIND * al * 2;   // 2 x B_BYTES (1024-aligned: al * 2 * 6 % 1024 == 0)
-  uint64_t *bar = (uint64_t *)(Bb + 2 * B_BYTES);      // MMA completion per B buffer
-  uint32_t *tmem_holder = (uint32_t *)(bar + 2);
+  uint64_t *bar = (uint64_t *)(Bb + 2 * B_BYTES);      // "empty": MMAs that read B buffer b are done
+  uint64_t *full = bar + 2;                            // B buffer b built (one arrive per builder warp)
+  uint64_t *dempty = full + 2;                         // TMEM drained by the epilogue warps
+  uint32_t *tmem_holder = (uint32_t *)(dempty + 1);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t q = blockIdx.x;
@@ -112,6 +115,9 @@ __global__ void __launch_bounds__(THREADS, 2)
   if (tid == 0) {
     sa_mbar_init(&bar[0], 1);
     sa_mbar_init(&bar[1], 1);
+    sa_mbar_init(&full[0], BUILDERS / 32);
+    sa_mbar_init(&full[1], BUILDERS / 32);
+    sa_mbar_init(dempty, 4);
     sa_fence_mbar_init();
   }
   if (warp == 0) {
@@ -121,7 +127,7 @@ __global__ void __launch_bounds__(THREADS, 2)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   // A: the surveillance block as six zero-padded linear bf16 arrays, a[t] at PAD + t
-  for (int j = 2 * tid; j < al; j += 2 * THREADS) {
+  for (int j = 2 * tid; j < al; j += 2 * THREADS) {  // (the MMA warp helps here)
     const int t = j - PAD;
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     if (t >= 0 && t < tb) v = __ldg((const float4 *)&surv[q * tb + t]);  // t even, tb even: 16-B aligned
@@ -140,119 +146,136 @@ __global__ void __launch_bounds__(THREADS, 2)
   const uint32_t tmem = *tmem_holder;
   const uint32_t abase = sa_smem_u32(A), bbase = sa_smem_u32(Bb);
 
-  // B builders: thread (l0 = tid % 8, octet = (tid / 8) % 16, half = tid / 128)
-  const int bl0 = tid & 7, boct = (tid >> 3) & 15, bhalf = tid >> 7;
   // Groups start at lag multiples of 16, so every (lag, t) product lands in the
   // same row parity, column and K-step position whatever l0 the call starts at:
   // lag shards (sharded.py) reproduce the single-call rows bit for bit.
   const int64_t lalign = l0g - (l0g & 15);
   const int ngrp = (int)((l0g - lalign + l_count + LGRP - 1) / LGRP);
-  uint32_t cc = 0;  // chunk counter across groups (B buffer = cc & 1)
-  for (int gi = 0; gi < ngrp; ++gi) {
-    const int64_t lbase = lalign + (int64_t)gi * LGRP;
-    // c index of (u, l0): q T - lbase + u - l0
-    const int64_t cbase = q * tb - lbase - PAD - bl0 + boct * 8;
-    float2 cv[8];
-    load_c(cv, ref, cbase, csign);
-    for (int ch = 0; ch < nch; ++ch, ++cc) {
-      const int b = cc & 1;
-      if (cc >= 2) sa_mbar_wait(&bar[b], ((cc >> 1) - 1) & 1);  // MMAs that read this buffer are done
-      // build chunk ch of B into buffer b: rows (block of 8 = one component, row = l0), octet boct
-      {
-        unsigned char *B = Bb + b * B_BYTES;
-        float cr[8], ci[8];
+
+  if (warp == BUILDERS / 32) {
+    // ---- MMA issuer: one thread, six MMAs per 16 u, commit frees the B buffer ----
+    if (lane == 0) {
+      uint32_t cc = 0;
+      for (int gi = 0; gi < ngrp; ++gi) {
+        if (gi > 0) sa_mbar_wait(dempty, (gi - 1) & 1);  // epilogue has read the previous group's D
+        for (int ch = 0; ch < nch; ++ch, ++cc) {
+          const int b = cc & 1;
+          sa_mbar_wait(&full[b], (cc >> 1) & 1);
+          fence_after();
+          const uint32_t bb = bbase + b * B_BYTES;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) cr[e] = cv[e].x, ci[e] = cv[e].y;
-        uint32_t o = (uint32_t)boct * 128 + (uint32_t)bl0 * 16;  // (row l0, octet) inside an 8-row block
-        auto put = [&](int matrow0, int blk, const uint32_t(&w)[4]) {  // matrix at row offset matrow0 (rows), block blk
-          *(uint4 *)(B + (size_t)(matrow0 + blk * 8) / 8 * 2048 + o) = make_uint4(w[0], w[1], w[2], w[3]);
-        };
-        if (bhalf == 0) {
-          uint32_t rh[4], rl[4], ihh[4], il[4], nih[4], nil[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            rh[e] = bf2(cr[2 * e + 1], cr[2 * e]);
-            ihh[e] = bf2(ci[2 * e + 1], ci[2 * e]);
-            rl[e] = bf2(sa_sub(cr[2 * e + 1], __uint_as_float(rh[e] & 0xFFFF0000u)),
-                        sa_sub(cr[2 * e], __uint_as_float(rh[e] << 16)));
-            il[e] = bf2(sa_sub(ci[2 * e + 1], __uint_as_float(ihh[e] & 0xFFFF0000u)),
-                        sa_sub(ci[2 * e], __uint_as_float(ihh[e] << 16)));
-            nih[e] = ihh[e] ^ 0x80008000u;  // exact negation of both bf16 halves
-            nil[e] = il[e] ^ 0x80008000u;
+          for (int ks = 0; ks < KCH / 16; ++ks) {
+            const uint32_t ua = (uint32_t)(ch * KCH + ks * 16) * 2;  // byte offset of u0 + PAD in the A arrays
+            const uint32_t bo = bb + ks * 256;                      // 16 u = two 128-B core columns
+            const uint32_t acc = (ch | ks) != 0;
+            const uint64_t b1 = sdesc_ns(bo, 128, 2048), b2 = sdesc_ns(bo + 32 * KCH * 2, 128, 2048),
+                           b3 = sdesc_ns(bo + 64 * KCH * 2, 128, 2048), b4 = sdesc_ns(bo + 80 * KCH * 2, 128, 2048);
+            auto ad = [&](int k) { return sdesc_ns(abase + (uint32_t)k * al * 2 + ua, 16, 128); };
+            mma(tmem, ad(0), b1, idesc(32), acc);
+            mma(tmem, ad(1), b2, idesc(32), 1);
+            mma(tmem + 32, ad(2), b3, idesc(16), acc);
+            mma(tmem + 32, ad(3), b3, idesc(16), 1);
+            mma(tmem + 32, ad(4), b4, idesc(16), 1);
+            mma(tmem + 32, ad(5), b4, idesc(16), 1);
           }
-          put(0, 0, rh);     // B1: cr_hi
-          put(0, 1, ihh);    //     ci_hi
-          put(0, 2, rl);     //     cr_lo
-          put(0, 3, il);     //     ci_lo
-          put(32, 0, nih);   // B2: -ci_hi
-          put(32, 1, rh);    //     cr_hi
-          put(32, 2, nil);   //     -ci_lo
-          put(32, 3, rl);    //     cr_lo
-        } else {
-          uint32_t sr[4], si[4], nsi[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            sr[e] = bf2(sa_sgn(cr[2 * e + 1]), sa_sgn(cr[2 * e]));
-            si[e] = bf2(sa_sgn(ci[2 * e + 1]), sa_sgn(ci[2 * e]));
-            nsi[e] = si[e] ^ 0x80008000u;
-          }
-          put(64, 0, sr);    // B3: sgn cr
-          put(64, 1, si);    //     sgn ci
-          put(80, 0, nsi);   // B4: -sgn ci
-          put(80, 1, sr);    //     sgn cr
+          commit(&bar[b]);
         }
       }
-      if (ch + 1 < nch) load_c(cv, ref, cbase + (int64_t)(ch + 1) * KCH, csign);  // next chunk's values
-      sa_fence_proxy_async();
-      fence_before();
-      __syncthreads();
-      if (tid == 0) {
+    }
+  } else {
+    // ---- builders: thread (l0 = tid % 8, octet = (tid / 8) % 16, half = tid / 128) ----
+    const int bl0 = tid & 7, boct = (tid >> 3) & 15, bhalf = tid >> 7;
+    uint32_t cc = 0;  // chunk counter across groups (B buffer = cc & 1)
+    for (int gi = 0; gi < ngrp; ++gi) {
+      const int64_t lbase = lalign + (int64_t)gi * LGRP;
+      // c index of (u, l0): q T - lbase + u - l0
+      const int64_t cbase = q * tb - lbase - PAD - bl0 + boct * 8;
+      float2 cv[8];
+      load_c(cv, ref, cbase, csign);
+      for (int ch = 0; ch < nch; ++ch, ++cc) {
+        const int b = cc & 1;
+        if (cc >= 2) sa_mbar_wait(&bar[b], ((cc >> 1) - 1) & 1);  // MMAs that read this buffer are done
+        // build chunk ch of B into buffer b: rows (block of 8 = one component, row = l0), octet boct
+        {
+          unsigned char *B = Bb + b * B_BYTES;
+          float cr[8], ci[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) cr[e] = cv[e].x, ci[e] = cv[e].y;
+          uint32_t o = (uint32_t)boct * 128 + (uint32_t)bl0 * 16;  // (row l0, octet) inside an 8-row block
+          auto put = [&](int matrow0, int blk, const uint32_t(&w)[4]) {  // matrix at row offset matrow0 (rows), block blk
+            *(uint4 *)(B + (size_t)(matrow0 + blk * 8) / 8 * 2048 + o) = make_uint4(w[0], w[1], w[2], w[3]);
+          };
+          if (bhalf == 0) {
+            uint32_t rh[4], rl[4], ihh[4], il[4], nih[4], nil[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              rh[e] = bf2(cr[2 * e + 1], cr[2 * e]);
+              ihh[e] = bf2(ci[2 * e + 1], ci[2 * e]);
+              rl[e] = bf2(sa_sub(cr[2 * e + 1], __uint_as_float(rh[e] & 0xFFFF0000u)),
+                          sa_sub(cr[2 * e], __uint_as_float(rh[e] << 16)));
+              il[e] = bf2(sa_sub(ci[2 * e + 1], __uint_as_float(ihh[e] & 0xFFFF0000u)),
+                          sa_sub(ci[2 * e], __uint_as_float(ihh[e] << 16)));
+              nih[e] = ihh[e] ^ 0x80008000u;  // exact negation of both bf16 halves
+              nil[e] = il[e] ^ 0x80008000u;
+            }
+            put(0, 0, rh);     // B1: cr_hi
+            put(0, 1, ihh);    //     ci_hi
+            put(0, 2, rl);     //     cr_lo
+            put(0, 3, il);     //     ci_lo
+            put(32, 0, nih);   // B2: -ci_hi
+            put(32, 1, rh);    //     cr_hi
+            put(32, 2, nil);   //     -ci_lo
+            put(32, 3, rl);    //     cr_lo
+          } else {
+            uint32_t sr[4], si[4], nsi[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              sr[e] = bf2(sa_sgn(cr[2 * e + 1]), sa_sgn(cr[2 * e]));
+              si[e] = bf2(sa_sgn(ci[2 * e + 1]), sa_sgn(ci[2 * e]));
+              nsi[e] = si[e] ^ 0x80008000u;
+            }
+            put(64, 0, sr);    // B3: sgn cr
+            put(64, 1, si);    //     sgn ci
+            put(80, 0, nsi);   // B4: -sgn ci
+            put(80, 1, sr);    //     sgn cr
+          }
+        }
+        if (ch + 1 < nch) load_c(cv, ref, cbase + (int64_t)(ch + 1) * KCH, csign);  // next chunk's values
+        sa_fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05.mma
+        __syncwarp();
+        if (lane == 0) sa_mbar_arrive_local(&full[b]);
+      }
+      // epilogue of this lag group (warps 0-3): the last chunk's commit tracks all prior MMAs
+      if (warp < 4) {
+        const uint32_t last = cc - 1;
+        sa_mbar_wait(&bar[last & 1], (last >> 1) & 1);
         fence_after();
-        const uint32_t bb = bbase + b * B_BYTES;
+        uint32_t d1[16], d2[16], d3[16];
+        const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
+        SA_LD16(d1, ta);
+        SA_LD16(d2, ta + 16);
+        SA_LD16(d3, ta + 32);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const int l1 = warp * 32 + lane;
 #pragma unroll
-        for (int ks = 0; ks < KCH / 16; ++ks) {
-          const uint32_t ua = (uint32_t)(ch * KCH + ks * 16) * 2;  // byte offset of u0 + PAD in the A arrays
-          const uint32_t bo = bb + ks * 256;                      // 16 u = two 128-B core columns
-          const uint32_t acc = (ch | ks) != 0;
-          const uint64_t b1 = sdesc_ns(bo, 128, 2048), b2 = sdesc_ns(bo + 32 * KCH * 2, 128, 2048),
-                         b3 = sdesc_ns(bo + 64 * KCH * 2, 128, 2048), b4 = sdesc_ns(bo + 80 * KCH * 2, 128, 2048);
-          auto ad = [&](int k) { return sdesc_ns(abase + (uint32_t)k * al * 2 + ua, 16, 128); };
-          mma(tmem, ad(0), b1, idesc(32), acc);
-          mma(tmem, ad(1), b2, idesc(32), 1);
-          mma(tmem + 32, ad(2), b3, idesc(16), acc);
-          mma(tmem + 32, ad(3), b3, idesc(16), 1);
-          mma(tmem + 32, ad(4), b4, idesc(16), 1);
-          mma(tmem + 32, ad(5), b4, idesc(16), 1);
+        for (int l0 = 0; l0 < 8; ++l0) {
+          const int64_t lag = lbase + 8 * l1 + l0 - l0g;  // row of z
+          if (lag >= 0 && lag < l_count) {
+            const float re = (__uint_as_float(d1[l0]) + __uint_as_float(d2[l0])) + __uint_as_float(d3[l0]);
+            const float im =
+                (__uint_as_float(d1[8 + l0]) + __uint_as_float(d2[8 + l0])) + __uint_as_float(d3[8 + l0]);
+            z[lag * m + q] = make_float2(re, im);
+          }
         }
-        commit(&bar[b]);
+        fence_before();
+        __syncwarp();
+        if (lane == 0) sa_mbar_arrive_local(dempty);
       }
     }
-    // epilogue of this lag group: wait for the last chunk's MMAs (commit tracks all prior)
-    const uint32_t last = cc - 1;
-    sa_mbar_wait(&bar[last & 1], (last >> 1) & 1);
-    fence_after();
-    if (warp < 4) {
-      uint32_t d1[16], d2[16], d3[16];
-      const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
-      SA_LD16(d1, ta);
-      SA_LD16(d2, ta + 16);
-      SA_LD16(d3, ta + 32);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      const int l1 = warp * 32 + lane;
-#pragma unroll
-      for (int l0 = 0; l0 < 8; ++l0) {
-        const int64_t lag = lbase + 8 * l1 + l0 - l0g;  // row of z
-        if (lag >= 0 && lag < l_count) {
-          const float re = (__uint_as_float(d1[l0]) + __uint_as_float(d2[l0])) + __uint_as_float(d3[l0]);
-          const float im = (__uint_as_float(d1[8 + l0]) + __uint_as_float(d2[8 + l0])) + __uint_as_float(d3[8 + l0]);
-          z[lag * m + q] = make_float2(re, im);
-        }
-      }
-    }
-    fence_before();
-    __syncthreads();  // TMEM drained before the next group's first MMA overwrites it
-    fence_after();
   }
+  fence_before();
+  __syncthreads();
+  fence_after();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
 }
