@@ -36,16 +36,15 @@ namespace {
 
 constexpr int LGRP = 1024;       // lags per group (128 l1 x 8 l0)
 constexpr int PAD = 1024;        // zero padding in front of the A arrays (u >= -1024)
-constexpr int KCH = 128;         // u per K chunk
 constexpr int NKIND = 6;         // A kinds: sgn sr, sgn si, sr_hi, sr_lo, si_hi, si_lo
-constexpr int BROWS = 96;        // B rows per chunk: B1 32 + B2 32 + B3 16 + B4 16
-constexpr int B_BYTES = BROWS * KCH * 2;  // 24 KB
+constexpr int BROWS = 96;        // B rows per lag group: B1 32 + B2 32 + B3 16 + B4 16
+constexpr int B_BYTES = BROWS * 128 * 2;  // 24 KB per buffer: G groups x 128 / G u per K chunk
 constexpr int BUILDERS = 256;    // warps 0-7 build the operands (warps 0-3 also drain TMEM)
 constexpr int THREADS = BUILDERS + 32;  // warp 8 issues the MMAs
-constexpr int TMEM_COLS = 64;
 
 __host__ __device__ inline int a_len(int tb) { return tb + 2 * PAD; }  // u + 8 l1 in [-1024, T + 1016), padded
 __host__ __device__ inline size_t smem_bytes(int tb) { return (size_t)NKIND * a_len(tb) * 2 + 2 * B_BYTES + 1024 + 64; }
+constexpr int tmem_cols(int g) { return g == 1 ? 64 : (g == 2 ? 128 : 256); }  // >= 48 G, power of 2
 
 // instruction descriptor: kind::f16, bf16 x bf16 -> f32, K-major, M = 128, N = n
 constexpr uint32_t idesc(int n) {
@@ -95,6 +94,8 @@ SA_HD void load_c(float2 (&cv)[8], const float2 *__restrict__ ref, int64_t g0, f
   }
 }
 
+// G lag groups share each A read (one pass): the MMAs widen to N = 32 G / 16 G.
+template <int G>
 __global__ void __launch_bounds__(THREADS, 2)
     k_lag_tc(const float2 *__restrict__ surv, const float2 *__restrict__ ref, int64_t l0g, int64_t l_count,
              int64_t m, int tb, float csign, float2 *__restrict__ z) {
@@ -110,6 +111,9 @@ __global__ void __launch_bounds__(THREADS, 2)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t q = blockIdx.x;
+  constexpr int KCH = 128 / G;          // u per K chunk (B buffer stays 24 KB)
+  constexpr int SBO = (KCH / 8) * 128;    // bytes per 8-row block of a B buffer
+  constexpr int TMEM_COLS = tmem_cols(G);
   const int nch = (tb + PAD) / KCH;
 
   if (tid == 0) {
@@ -151,13 +155,14 @@ __global__ void __launch_bounds__(THREADS, 2)
   // lag shards (sharded.py) reproduce the single-call rows bit for bit.
   const int64_t lalign = l0g - (l0g & 15);
   const int ngrp = (int)((l0g - lalign + l_count + LGRP - 1) / LGRP);
+  const int npass = (ngrp + G - 1) / G;
 
   if (warp == BUILDERS / 32) {
     // ---- MMA issuer: one thread, six MMAs per 16 u, commit frees the B buffer ----
     if (lane == 0) {
       uint32_t cc = 0;
-      for (int gi = 0; gi < ngrp; ++gi) {
-        if (gi > 0) sa_mbar_wait(dempty, (gi - 1) & 1);  // epilogue has read the previous group's D
+      for (int pi = 0; pi < npass; ++pi) {
+        if (pi > 0) sa_mbar_wait(dempty, (pi - 1) & 1);  // epilogue has read the previous pass's D
         for (int ch = 0; ch < nch; ++ch, ++cc) {
           const int b = cc & 1;
           sa_mbar_wait(&full[b], (cc >> 1) & 1);
@@ -168,28 +173,28 @@ __global__ void __launch_bounds__(THREADS, 2)
             const uint32_t ua = (uint32_t)(ch * KCH + ks * 16) * 2;  // byte offset of u0 + PAD in the A arrays
             const uint32_t bo = bb + ks * 256;                      // 16 u = two 128-B core columns
             const uint32_t acc = (ch | ks) != 0;
-            const uint64_t b1 = sdesc_ns(bo, 128, 2048), b2 = sdesc_ns(bo + 32 * KCH * 2, 128, 2048),
-                           b3 = sdesc_ns(bo + 64 * KCH * 2, 128, 2048), b4 = sdesc_ns(bo + 80 * KCH * 2, 128, 2048);
+            const uint64_t b1 = sdesc_ns(bo, 128, SBO), b2 = sdesc_ns(bo + 4 * G * SBO, 128, SBO),
+                           b3 = sdesc_ns(bo + 8 * G * SBO, 128, SBO), b4 = sdesc_ns(bo + 10 * G * SBO, 128, SBO);
             auto ad = [&](int k) { return sdesc_ns(abase + (uint32_t)k * al * 2 + ua, 16, 128); };
-            mma(tmem, ad(0), b1, idesc(32), acc);
-            mma(tmem, ad(1), b2, idesc(32), 1);
-            mma(tmem + 32, ad(2), b3, idesc(16), acc);
-            mma(tmem + 32, ad(3), b3, idesc(16), 1);
-            mma(tmem + 32, ad(4), b4, idesc(16), 1);
-            mma(tmem + 32, ad(5), b4, idesc(16), 1);
+            mma(tmem, ad(0), b1, idesc(32 * G), acc);
+            mma(tmem, ad(1), b2, idesc(32 * G), 1);
+            mma(tmem + 32 * G, ad(2), b3, idesc(16 * G), acc);
+            mma(tmem + 32 * G, ad(3), b3, idesc(16 * G), 1);
+            mma(tmem + 32 * G, ad(4), b4, idesc(16 * G), 1);
+            mma(tmem + 32 * G, ad(5), b4, idesc(16 * G), 1);
           }
           commit(&bar[b]);
         }
       }
     }
   } else {
-    // ---- builders: thread (l0 = tid % 8, octet = (tid / 8) % 16, half = tid / 128) ----
-    const int bl0 = tid & 7, boct = (tid >> 3) & 15, bhalf = tid >> 7;
-    uint32_t cc = 0;  // chunk counter across groups (B buffer = cc & 1)
-    for (int gi = 0; gi < ngrp; ++gi) {
-      const int64_t lbase = lalign + (int64_t)gi * LGRP;
-      // c index of (u, l0): q T - lbase + u - l0
-      const int64_t cbase = q * tb - lbase - PAD - bl0 + boct * 8;
+    // ---- builders: thread (l0, octet of the chunk, group of the pass, half) ----
+    const int bl0 = tid & 7, boct = (tid >> 3) % (KCH / 8), bg = ((tid >> 3) / (KCH / 8)) % G, bhalf = tid >> 7;
+    uint32_t cc = 0;  // chunk counter across passes (B buffer = cc & 1)
+    for (int pi = 0; pi < npass; ++pi) {
+      const int64_t lpass = lalign + (int64_t)pi * G * LGRP;
+      // c index of (u, l0) for this thread's group: q T - lbase + u - l0
+      const int64_t cbase = q * tb - (lpass + (int64_t)bg * LGRP) - PAD - bl0 + boct * 8;
       float2 cv[8];
       load_c(cv, ref, cbase, csign);
       for (int ch = 0; ch < nch; ++ch, ++cc) {
@@ -201,9 +206,10 @@ __global__ void __launch_bounds__(THREADS, 2)
           float cr[8], ci[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) cr[e] = cv[e].x, ci[e] = cv[e].y;
-          uint32_t o = (uint32_t)boct * 128 + (uint32_t)bl0 * 16;  // (row l0, octet) inside an 8-row block
-          auto put = [&](int matrow0, int blk, const uint32_t(&w)[4]) {  // matrix at row offset matrow0 (rows), block blk
-            *(uint4 *)(B + (size_t)(matrow0 + blk * 8) / 8 * 2048 + o) = make_uint4(w[0], w[1], w[2], w[3]);
+          const uint32_t o = (uint32_t)boct * 128 + (uint32_t)bl0 * 16;  // (row l0, octet) inside an 8-row block
+          // matrix at row offset mrow0 (B1 0, B2 32 G, B3 64 G, B4 80 G), this group's block blk
+          auto put = [&](int mrow0, int gstride, int blk, const uint32_t(&w)[4]) {
+            *(uint4 *)(B + (size_t)((mrow0 + bg * gstride) / 8 + blk) * SBO + o) = make_uint4(w[0], w[1], w[2], w[3]);
           };
           if (bhalf == 0) {
             uint32_t rh[4], rl[4], ihh[4], il[4], nih[4], nil[4];
@@ -218,14 +224,14 @@ __global__ void __launch_bounds__(THREADS, 2)
               nih[e] = ihh[e] ^ 0x80008000u;  // exact negation of both bf16 halves
               nil[e] = il[e] ^ 0x80008000u;
             }
-            put(0, 0, rh);     // B1: cr_hi
-            put(0, 1, ihh);    //     ci_hi
-            put(0, 2, rl);     //     cr_lo
-            put(0, 3, il);     //     ci_lo
-            put(32, 0, nih);   // B2: -ci_hi
-            put(32, 1, rh);    //     cr_hi
-            put(32, 2, nil);   //     -ci_lo
-            put(32, 3, rl);    //     cr_lo
+            put(0, 32, 0, rh);          // B1: cr_hi
+            put(0, 32, 1, ihh);         //     ci_hi
+            put(0, 32, 2, rl);          //     cr_lo
+            put(0, 32, 3, il);          //     ci_lo
+            put(32 * G, 32, 0, nih);    // B2: -ci_hi
+            put(32 * G, 32, 1, rh);     //     cr_hi
+            put(32 * G, 32, 2, nil);    //     -ci_lo
+            put(32 * G, 32, 3, rl);     //     cr_lo
           } else {
             uint32_t sr[4], si[4], nsi[4];
 #pragma unroll
@@ -234,10 +240,10 @@ __global__ void __launch_bounds__(THREADS, 2)
               si[e] = bf2(sa_sgn(ci[2 * e + 1]), sa_sgn(ci[2 * e]));
               nsi[e] = si[e] ^ 0x80008000u;
             }
-            put(64, 0, sr);    // B3: sgn cr
-            put(64, 1, si);    //     sgn ci
-            put(80, 0, nsi);   // B4: -sgn ci
-            put(80, 1, sr);    //     sgn cr
+            put(64 * G, 16, 0, sr);     // B3: sgn cr
+            put(64 * G, 16, 1, si);     //     sgn ci
+            put(80 * G, 16, 0, nsi);    // B4: -sgn ci
+            put(80 * G, 16, 1, sr);     //     sgn cr
           }
         }
         if (ch + 1 < nch) load_c(cv, ref, cbase + (int64_t)(ch + 1) * KCH, csign);  // next chunk's values
@@ -245,26 +251,29 @@ __global__ void __launch_bounds__(THREADS, 2)
         __syncwarp();
         if (lane == 0) sa_mbar_arrive_local(&full[b]);
       }
-      // epilogue of this lag group (warps 0-3): the last chunk's commit tracks all prior MMAs
+      // epilogue of this pass (warps 0-3): the last chunk's commit tracks all prior MMAs
       if (warp < 4) {
         const uint32_t last = cc - 1;
         sa_mbar_wait(&bar[last & 1], (last >> 1) & 1);
         fence_after();
-        uint32_t d1[16], d2[16], d3[16];
         const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
-        SA_LD16(d1, ta);
-        SA_LD16(d2, ta + 16);
-        SA_LD16(d3, ta + 32);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         const int l1 = warp * 32 + lane;
+#pragma unroll 1
+        for (int gs = 0; gs < G; ++gs) {
+          uint32_t d1[16], d2[16], d3[16];
+          SA_LD16(d1, ta + 32 * gs);
+          SA_LD16(d2, ta + 32 * gs + 16);
+          SA_LD16(d3, ta + 32 * G + 16 * gs);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int l0 = 0; l0 < 8; ++l0) {
-          const int64_t lag = lbase + 8 * l1 + l0 - l0g;  // row of z
-          if (lag >= 0 && lag < l_count) {
-            const float re = (__uint_as_float(d1[l0]) + __uint_as_float(d2[l0])) + __uint_as_float(d3[l0]);
-            const float im =
-                (__uint_as_float(d1[8 + l0]) + __uint_as_float(d2[8 + l0])) + __uint_as_float(d3[8 + l0]);
-            z[lag * m + q] = make_float2(re, im);
+          for (int l0 = 0; l0 < 8; ++l0) {
+            const int64_t lag = lpass + (int64_t)gs * LGRP + 8 * l1 + l0 - l0g;  // row of z
+            if (lag >= 0 && lag < l_count) {
+              const float re = (__uint_as_float(d1[l0]) + __uint_as_float(d2[l0])) + __uint_as_float(d3[l0]);
+              const float im =
+                  (__uint_as_float(d1[8 + l0]) + __uint_as_float(d2[8 + l0])) + __uint_as_float(d3[8 + l0]);
+              z[lag * m + q] = make_float2(re, im);
+            }
           }
         }
         fence_before();
@@ -283,7 +292,7 @@ __global__ void __launch_bounds__(THREADS, 2)
 }  // namespace
 
 bool sa_lag_tc_supported(int dtype, int64_t tb, int64_t m, const void *surv) {
-  return dtype == SA_C64 && tb >= 128 && tb % KCH == 0 && tb <= 4096 && m <= 0x7fffffff &&
+  return dtype == SA_C64 && tb >= 128 && tb % 128 == 0 && tb <= 4096 && m <= 0x7fffffff &&
          ((uintptr_t)surv & 15) == 0;
 }
 
@@ -291,9 +300,13 @@ int sa_launch_lag_tc(const void *surv, const void *ref, int64_t l0, int64_t l_co
                      void *z, cudaStream_t s) {
   if (l_count == 0 || m == 0) return SA_OK;
   const size_t bytes = smem_bytes((int)tb);
-  SA_CUDA_TRY(cudaFuncSetAttribute(k_lag_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  k_lag_tc<<<(unsigned)m, THREADS, bytes, s>>>((const float2 *)surv, (const float2 *)ref, l0, l_count, m, (int)tb,
-                                               conj ? -1.f : 1.f, (float2 *)z);
+  // lag groups (of 1024, aligned to 16) per call -> groups merged per pass
+  const int64_t ngrp = ((l0 & 15) + l_count + LGRP - 1) / LGRP;
+  const int g = ngrp >= 3 ? 4 : (int)ngrp;
+  auto kern = g == 4 ? k_lag_tc<4> : (g == 2 ? k_lag_tc<2> : k_lag_tc<1>);
+  SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  kern<<<(unsigned)m, THREADS, bytes, s>>>((const float2 *)surv, (const float2 *)ref, l0, l_count, m, (int)tb,
+                                           conj ? -1.f : 1.f, (float2 *)z);
   SA_LAUNCH_CHECK();
   return SA_OK;
 }
