@@ -440,20 +440,25 @@ def wl_map(args, ws, rank, c5=False):
     out = torch.empty((rows, M), dtype=cdt, device="cuda")
     ws_buf = torch.empty(rows * M * out.element_size(), dtype=torch.uint8, device="cuda")
 
-    pm, transport = None, "p2p"
+    pm, zx, transport = None, None, "p2p"
     if ws > 1:  # rank 0's map, IPC-shared once: every rank's kernels store their rows into it
-        from paper_1402_0532_b200.sharded import PeerMap, PeerMapUnavailable
+        from paper_1402_0532_b200.sharded import PeerMap, PeerMapUnavailable, ZExchange, blocks_shardable
         try:
             pm = PeerMap(L, M, cdt)
         except PeerMapUnavailable:  # (all ranks agree) NCCL gather instead
             transport = "gather"
+        if pm is not None and blocks_shardable(surv, M, "fast", "mf", "nfft"):
+            try:  # the z-row blocks of every rank, IPC-shared once (block-sharded lag stage)
+                zx = ZExchange(L, M, cdt)
+            except PeerMapUnavailable:
+                zx = None
     full = torch.empty((L, M), dtype=cdt, device="cuda") if (ws > 1 and rank == 0 and pm is None) else None
 
     def step():
-        if ws > 1:  # delay-bin shard, rows stored straight into rank 0's map (NVLink), one barrier
+        if ws > 1:  # block-sharded lag stage + z rows to their owners, or delay-bin shards; rows into rank 0's map
             from paper_1402_0532_b200.sharded import ambiguity_map_sharded
             ambiguity_map_sharded(surv, ref, L, M, peer_map=pm, transport=transport, out_full=full,
-                                  out_local=out, workspace=ws_buf)
+                                  out_local=out, workspace=ws_buf, z_exchange=zx)
         else:
             sa.ambiguity_map(surv, ref, rows, M, l0=l0, out=out, workspace=ws_buf)
 
@@ -470,9 +475,13 @@ def wl_map(args, ws, rank, c5=False):
            "config": {"workload": ("C5" if c5 else "C4") + " ⊙ range-Doppler map (BASELINE.json configs["
                       + ("4" if c5 else "3") + "])", "ns": ns, "delay_bins": L, "doppler_bins": M,
                       "block_T": ns // M, "doppler": "NL-FFT DIT", "dtype": str(cdt).replace("torch.", ""),
-                      "parallelism": f"delay-bin shards x{ws}" + (
-                          (", rows stored by the transform kernels into rank 0's IPC-shared map over NVLink, "
-                           "one barrier" if transport == "p2p" else ", NCCL gather to rank 0") if ws > 1 else "")}}
+                      "parallelism": (f"Doppler-block shards x{ws} for the lag stage, z rows stored by the lag "
+                                      "kernel into their owners' blocks over NVLink (fused all-to-all), delay-bin "
+                                      "shards for the Doppler NL-FFT, rows stored into rank 0's IPC-shared map, "
+                                      "two completion all-reduces") if zx is not None else (
+                          f"delay-bin shards x{ws}" + (
+                              (", rows stored by the transform kernels into rank 0's IPC-shared map over NVLink, "
+                               "one barrier" if transport == "p2p" else ", NCCL gather to rank 0") if ws > 1 else ""))}}
     return res
 
 

@@ -152,6 +152,17 @@ int sa_ambiguity_integrate_v(int dtype, int lag_kind, const void *surv, const vo
                              int64_t ref_len, int64_t l0, int64_t l_count, int64_t m, int conj,
                              int mode, void *z, void *stream);
 
+/* Block-sharded lag stage for multi-GPU maps (ambiguity.py:27-28: delay rows and
+ * integration blocks are independent): fast-mode ⊙ lag integration of blocks
+ * [q0, q0 + q_count) for lags [l0, l0 + l_count), each lag row stored into the
+ * z rows of its owner -- dst_rows is a DEVICE array of n_dst row-block bases
+ * (peer / IPC pointers), owner o holding lags per sharded.shard_rows(l_count,
+ * n_dst, o), row stride m.  Tensor-core path only (complex64, T % 128 == 0);
+ * anything else returns SA_ERR_UNSUPPORTED and the caller shards delay rows. */
+int sa_ambiguity_integrate_blocks(int dtype, const void *surv, const void *ref, int64_t ns, int64_t ref_len,
+                                  int64_t l0, int64_t l_count, int64_t m, int64_t q0, int64_t q_count, int conj,
+                                  void *const *dst_rows, int64_t n_dst, void *stream);
+
 /* Workspace bytes for sa_map_peaks. */
 int sa_peaks_workspace_bytes(int64_t rows, int64_t cols, int k, int64_t *bytes);
 

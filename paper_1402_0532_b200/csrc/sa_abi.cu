@@ -251,6 +251,25 @@ int sa_ambiguity_integrate_v(int dtype, int lag_kind, const void *surv, const vo
                                  (cudaStream_t)stream);
 }
 
+int sa_ambiguity_integrate_blocks(int dtype, const void *surv, const void *ref, int64_t ns, int64_t ref_len,
+                                  int64_t l0, int64_t l_count, int64_t m, int64_t q0, int64_t q_count, int conj,
+                                  void *const *dst_rows, int64_t n_dst, void *stream) {
+  SA_REQUIRE(dtype_ok(dtype), SA_ERR_ARG, "bad dtype %d", dtype);
+  SA_REQUIRE(l_count >= 1, SA_ERR_CONTRACT, "l_bins must be >= 1");
+  SA_REQUIRE(m >= 1 && ns >= m && ns % m == 0, SA_ERR_CONTRACT,
+             "map: ns=%lld must be a positive multiple of m=%lld", (long long)ns, (long long)m);
+  SA_REQUIRE(q0 >= 0 && q_count >= 0 && q0 + q_count <= m, SA_ERR_ARG, "bad block range");
+  SA_REQUIRE(n_dst >= 1 && n_dst <= l_count && dst_rows, SA_ERR_ARG, "bad destination rows");
+  int rc = lag_guards(ns, ns, ref_len, l0 + l_count - 1);
+  if (rc) return rc;
+  rc = lag_guards(ns, ns, ref_len, l0);
+  if (rc) return rc;
+  SA_REQUIRE(surv && ref, SA_ERR_ARG, "null pointer");
+  if (!sa_lag_tc_supported(dtype, ns / m, m, surv)) return SA_ERR_UNSUPPORTED;
+  return sa_launch_lag_tc_blocks(surv, ref, l0, l_count, m, q0, q_count, ns / m, conj, nullptr, dst_rows,
+                                 l_count / n_dst, l_count % n_dst, (cudaStream_t)stream);
+}
+
 int sa_peaks_workspace_bytes(int64_t rows, int64_t cols, int k, int64_t *bytes) {
   SA_REQUIRE(bytes && rows >= 1 && cols >= 1 && k >= 1, SA_ERR_ARG, "bad arguments");
   *bytes = sa_peaks_ws_bytes(rows, cols, k);

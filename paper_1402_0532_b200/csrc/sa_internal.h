@@ -64,6 +64,9 @@ int sa_launch_ndft_tc(const void *x, void *y, int64_t batch, int64_t n, const Sa
 bool sa_lag_tc_supported(int dtype, int64_t tb, int64_t m, const void *surv);
 int sa_launch_lag_tc(const void *surv, const void *ref, int64_t l0, int64_t l_count, int64_t m, int64_t tb, int conj,
                      void *z, cudaStream_t s);
+int sa_launch_lag_tc_blocks(const void *surv, const void *ref, int64_t l0, int64_t l_count, int64_t m, int64_t q0,
+                            int64_t q_count, int64_t tb, int conj, void *z, void *const *dst_rows, int64_t rows_base,
+                            int64_t rows_extra, cudaStream_t s);
 
 // sa_nlfft.cu
 int sa_launch_nlfft(int dtype, int variant, const void *x, void *y, int64_t batch, int64_t n,

@@ -94,11 +94,27 @@ SA_HD void load_c(float2 (&cv)[8], const float2 *__restrict__ ref, int64_t g0, f
   }
 }
 
+// Where row `lag` of z goes: the local (l_count x m) z, or -- block-sharded
+// multi-GPU maps (sharded.py) -- the z rows of the rank that owns the lag
+// (shard_rows partition: the first `extra` owners hold base + 1 rows), written
+// over NVLink/NVSwitch peer memory.
+struct LagDst {
+  float2 *const *ptr;  // device array of per-owner row-block bases (null: local z)
+  int64_t base, extra;
+  SA_HD float2 *row(float2 *z, int64_t lag, int64_t m, int64_t q) const {
+    if (!ptr) return z + lag * m + q;
+    const int64_t big = extra * (base + 1);
+    const int64_t o = lag < big ? lag / (base + 1) : extra + (lag - big) / base;
+    const int64_t first = o * base + (o < extra ? o : extra);
+    return ptr[o] + (lag - first) * m + q;
+  }
+};
+
 // G lag groups share each A read (one pass): the MMAs widen to N = 32 G / 16 G.
 template <int G>
 __global__ void __launch_bounds__(THREADS, 2)
     k_lag_tc(const float2 *__restrict__ surv, const float2 *__restrict__ ref, int64_t l0g, int64_t l_count,
-             int64_t m, int tb, float csign, float2 *__restrict__ z) {
+             int64_t m, int tb, float csign, float2 *__restrict__ z, int64_t q0, LagDst dst) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int al = a_len(tb);
@@ -110,7 +126,7 @@ __global__ void __launch_bounds__(THREADS, 2)
   uint32_t *tmem_holder = (uint32_t *)(dempty + 1);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t q = blockIdx.x;
+  const int64_t q = q0 + blockIdx.x;
   constexpr int KCH = 128 / G;          // u per K chunk (B buffer stays 24 KB)
   constexpr int SBO = (KCH / 8) * 128;    // bytes per 8-row block of a B buffer
   constexpr int TMEM_COLS = tmem_cols(G);
@@ -272,7 +288,7 @@ __global__ void __launch_bounds__(THREADS, 2)
               const float re = (__uint_as_float(d1[l0]) + __uint_as_float(d2[l0])) + __uint_as_float(d3[l0]);
               const float im =
                   (__uint_as_float(d1[8 + l0]) + __uint_as_float(d2[8 + l0])) + __uint_as_float(d3[8 + l0]);
-              z[lag * m + q] = make_float2(re, im);
+              *dst.row(z, lag, m, q) = make_float2(re, im);
             }
           }
         }
@@ -298,15 +314,22 @@ bool sa_lag_tc_supported(int dtype, int64_t tb, int64_t m, const void *surv) {
 
 int sa_launch_lag_tc(const void *surv, const void *ref, int64_t l0, int64_t l_count, int64_t m, int64_t tb, int conj,
                      void *z, cudaStream_t s) {
-  if (l_count == 0 || m == 0) return SA_OK;
+  return sa_launch_lag_tc_blocks(surv, ref, l0, l_count, m, 0, m, tb, conj, z, nullptr, 0, 0, s);
+}
+
+int sa_launch_lag_tc_blocks(const void *surv, const void *ref, int64_t l0, int64_t l_count, int64_t m, int64_t q0,
+                            int64_t q_count, int64_t tb, int conj, void *z, void *const *dst_rows, int64_t rows_base,
+                            int64_t rows_extra, cudaStream_t s) {
+  if (l_count == 0 || q_count == 0) return SA_OK;
   const size_t bytes = smem_bytes((int)tb);
   // lag groups (of 1024, aligned to 16) per call -> groups merged per pass
   const int64_t ngrp = ((l0 & 15) + l_count + LGRP - 1) / LGRP;
   const int g = ngrp >= 3 ? 4 : (int)ngrp;
   auto kern = g == 4 ? k_lag_tc<4> : (g == 2 ? k_lag_tc<2> : k_lag_tc<1>);
   SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  kern<<<(unsigned)m, THREADS, bytes, s>>>((const float2 *)surv, (const float2 *)ref, l0, l_count, m, (int)tb,
-                                           conj ? -1.f : 1.f, (float2 *)z);
+  const LagDst d{(float2 *const *)dst_rows, rows_base, rows_extra};
+  kern<<<(unsigned)q_count, THREADS, bytes, s>>>((const float2 *)surv, (const float2 *)ref, l0, l_count, m, (int)tb,
+                                                 conj ? -1.f : 1.f, (float2 *)z, q0, d);
   SA_LAUNCH_CHECK();
   return SA_OK;
 }

@@ -6,7 +6,17 @@ contiguous delay rows [r*L/G, (r+1)*L/G) with no exchange, and the map's only
 data movement is getting the row blocks to the root -- a rank's block lands at
 offset r*rows, which is exactly the row-major map.
 
-Two transports:
+Block-sharded lag stage (complex64 fast mode, T % 128 == 0: the tensor-core lag
+kernel).  That kernel amortises each surveillance read over all lags of a block,
+so splitting delay rows would leave every rank re-reading its blocks for a
+fraction of the lags.  Instead rank r integrates Doppler blocks
+[shard_rows(M, G, r)] for ALL delay rows and its kernel stores each z row
+straight into the z buffer of the rank that owns that delay row (CUDA IPC,
+NVLink/NVSwitch peer stores: the all-to-all is fused into the compute).  After
+one stream-ordered completion all-reduce every rank runs the Doppler transform
+of its own delay rows into the root's map (``ZExchange``, ``ambiguity_map_sharded``).
+
+Two transports for the map rows:
   * "p2p" (default): compute and collective fused.  The root's map is shared
     once by CUDA IPC (``PeerMap``); every rank's Doppler-transform kernel
     stores its rows straight into it over NVLink/NVSwitch, so there is no
@@ -160,10 +170,132 @@ class PeerMap:
             self._mapped = None
 
 
+def _ipc_export(t):
+    """(64-byte cudaIpcMemHandle_t, byte offset of ``t`` in its allocation)."""
+    info = t.untyped_storage()._share_cuda_()
+    handle, storage_offset = bytes(info[1]), int(info[3])
+    if len(handle) >= 65 and handle[-65:-64] == b"c":
+        handle = handle[-64:]
+    if len(handle) != 64:
+        raise RuntimeError("IPC export needs a cudaMalloc-backed tensor (set "
+                           "PYTORCH_CUDA_ALLOC_CONF=expandable_segments:False)")
+    return handle, storage_offset + t.storage_offset() * t.element_size()
+
+
+class ZExchange:
+    """Every rank's block of lag-integrated rows z (its delay rows x M), mapped
+    into every other rank by CUDA IPC: the block-sharded lag kernel stores z rows
+    straight into their owner's block.  ``table`` is the device array of the G
+    row-block bases as seen from this rank's GPU.  Collective to construct/close."""
+
+    def __init__(self, l_bins: int, m: int, dtype, group=None):
+        import torch
+        import torch.distributed as dist
+        from . import _native
+        self.group = group
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        self.first, self.count = shard_rows(l_bins, world, rank)
+        self.z = torch.empty((max(1, self.count), m), dtype=dtype, device="cuda")
+        self._mapped = []
+        mine = None
+        try:
+            mine = _ipc_export(self.z)
+        except Exception:
+            mine = None
+        allp = [None] * world
+        dist.all_gather_object(allp, mine, group=group)
+        ok = all(a is not None for a in allp)
+        bases = []
+        if ok:
+            for r, (handle, offset) in enumerate(allp):
+                if r == rank:
+                    bases.append(self.z.data_ptr())
+                    continue
+                hbuf = ctypes.create_string_buffer(handle, len(handle))
+                p = ctypes.c_void_p()
+                if _native.lib().sa_ipc_open(hbuf, ctypes.byref(p)) != 0:
+                    ok = False
+                    break
+                self._mapped.append(p)
+                bases.append(p.value + offset)
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32,
+                            device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        if int(flag.item()) == 0:
+            self.close(barrier=False)
+            raise PeerMapUnavailable("CUDA IPC mapping of the z row blocks failed on some rank")
+        self.table = torch.tensor(bases, dtype=torch.int64, device="cuda")
+
+    def close(self, barrier: bool = True) -> None:
+        import torch.distributed as dist
+        from . import _native
+        if barrier:
+            dist.barrier(group=self.group)
+        for p in self._mapped:
+            _native.lib().sa_ipc_close(p)
+        self._mapped = []
+
+
+def _done(flag, group):
+    """Stream-ordered completion point across ranks (NCCL: the all-reduce waits
+    for this rank's kernels; gloo: host sync + barrier)."""
+    import torch
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        dist.all_reduce(flag, group=group)
+    else:
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=group)
+
+
+def blocks_shardable(surv, m: int, mode: str, lag: str, doppler: str) -> bool:
+    """Whether the block-sharded map applies: the tensor-core lag path
+    (sa_lag_tc_supported: complex64 fast ⊙ lags, T % 128 == 0, T <= 4096) and a
+    Doppler transform of the z rows.  Shapes only, so every rank agrees."""
+    import torch
+    tb = surv.numel() // m if m else 0
+    return (surv.dtype == torch.complex64 and mode == "fast" and lag == "mf" and doppler in ("nfft", "ndft")
+            and 128 <= tb <= 4096 and tb % 128 == 0)
+
+
+def map_blocks_sharded(surv, ref, l_bins: int, m: int, zx: ZExchange, pm: PeerMap, *, gain: float = 1.0,
+                       conjugate_ref: bool = True, doppler: str = "nfft", group=None) -> None:
+    """Block-sharded map (see module doc): lag stage over this rank's Doppler
+    blocks for all delay rows, z rows delivered to their owners, then the Doppler
+    transform of this rank's delay rows into the root's map (``blocks_shardable``
+    must hold)."""
+    import torch.distributed as dist
+    from . import _native
+    from ._device import sa_dtype_of
+    from .twiddle import device_twiddles
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    q0, qc = shard_rows(m, world, rank)
+    d = sa_dtype_of(surv)
+    ns = surv.numel()
+    rc = _native.lib().sa_ambiguity_integrate_blocks(
+        d, _native.ptr(surv), _native.ptr(ref), ns, ref.numel(), 0, l_bins, m, q0, qc, int(conjugate_ref),
+        _native.ptr(zx.table), world, _native.stream_ptr())
+    _native.check(rc)
+    _done(pm.done_flag(), group)  # every rank's z rows are in their owners' blocks
+    if zx.count:
+        tw = device_twiddles(m, d, surv.device.index)
+        if doppler == "nfft":
+            _native.check(_native.lib().sa_nlfft(d, _native.SA_DIT, _native.ptr(zx.z), ctypes.c_void_p(
+                pm.rows_ptr(zx.first)), zx.count, m, ctypes.c_void_p(tw), float(gain), _native.stream_ptr()))
+        else:
+            _native.check(_native.lib().sa_ndft(d, _native.ptr(zx.z), ctypes.c_void_p(pm.rows_ptr(zx.first)),
+                                                zx.count, m, ctypes.c_void_p(tw), _native.SA_NDFT_FAST,
+                                                float(gain), _native.stream_ptr()))
+    _done(pm.done_flag(), group)  # every rank's rows are in the root's map
+
+
 def ambiguity_map_sharded(surv, ref, l_bins: int, m: int, *, gain: float = 1.0,
                           conjugate_ref: bool = True, doppler: str = "nfft", mode: str = "fast",
                           lag: str = "mf", group=None, dst: int = 0, transport: str = "p2p",
-                          peer_map: PeerMap | None = None, out_full=None, out_local=None, workspace=None):
+                          peer_map: PeerMap | None = None, out_full=None, out_local=None, workspace=None,
+                          z_exchange: ZExchange | None = None):
     """Compute this rank's delay rows on its GPU and deliver them to ``dst``.
 
     surv/ref: full CUDA tensors on every rank (broadcast beforehand if needed).
@@ -182,6 +314,21 @@ def ambiguity_map_sharded(surv, ref, l_bins: int, m: int, *, gain: float = 1.0,
             peer_map = PeerMap(l_bins, m, surv.dtype, group=group, dst=dst)
         except PeerMapUnavailable:
             transport = "gather"
+    if transport == "p2p" and world > 1 and blocks_shardable(surv, m, mode, lag, doppler):
+        if surv.data_ptr() % 16:  # the tensor-core lag kernel reads 16-byte sample pairs
+            surv = surv.clone()
+        zx = z_exchange
+        try:
+            if zx is None:
+                zx = ZExchange(l_bins, m, surv.dtype, group=group)
+        except PeerMapUnavailable:  # (all ranks agree) delay-row shards instead
+            zx = None
+        if zx is not None:
+            map_blocks_sharded(surv, ref, l_bins, m, zx, peer_map, gain=gain, conjugate_ref=conjugate_ref,
+                               doppler=doppler, group=group)
+            if z_exchange is None:
+                zx.close()
+            return peer_map.full if rank == dst else None
     if transport == "p2p":
         pm = peer_map
         if count:

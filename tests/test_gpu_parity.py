@@ -534,6 +534,8 @@ def _p2p_worker(rank, port, q):
         sc = radar_scene(1 << 16, 2, 4343)
         ds = torch.from_numpy(sc.surv.astype(np.complex64)).cuda()
         dr = torch.from_numpy(sc.ref.astype(np.complex64)).cuda()
+        from paper_1402_0532_b200.sharded import blocks_shardable
+        assert blocks_shardable(ds, 128, "fast", "mf", "nfft")  # c64, T = 512: block-sharded lag stage
         pm = PeerMap(101, 128, ds.dtype)  # odd row count: uneven shards
         for _ in range(2):  # the shared map is reused across calls
             full = ambiguity_map_sharded(ds, dr, 101, 128, peer_map=pm)
@@ -546,8 +548,10 @@ def _p2p_worker(rank, port, q):
 
 def test_sharded_map_p2p_two_ranks_one_gpu(sa):
     """Fused compute + delivery: two ranks (two processes sharing the GPU, gloo
-    for the host handshake) store their Doppler rows straight into rank 0's
-    IPC-shared map; the result equals the single-call map bit for bit."""
+    for the host handshake) integrate their Doppler blocks for all delay rows,
+    the tensor-core lag kernel stores each z row into its owner's IPC-shared
+    block, then each rank's Doppler NL-FFT stores its rows straight into rank
+    0's IPC-shared map; the result equals the single-call map bit for bit."""
     import socket
     import torch.multiprocessing as mp
     sock = socket.socket()

@@ -70,3 +70,65 @@ def test_gather_rows_world2(L):
         p.join(120)
     assert all(p.exitcode == 0 for p in procs)
     assert q.get(timeout=10) is True
+
+
+def _owner_kernel(lag, base, extra):
+    """Restatement of LagDst::row (sa_lag_tc.cu): owner rank of a z row and its
+    row inside the owner's block, for the shard_rows partition (base, extra)."""
+    big = extra * (base + 1)
+    o = lag // (base + 1) if lag < big else extra + (lag - big) // base
+    first = o * base + min(o, extra)
+    return o, lag - first
+
+
+def test_block_sharded_row_owners_match_shard_rows():
+    """The block-sharded lag kernel stores z row `lag` into the block of the rank
+    that shard_rows gives that delay row (the rank that runs its Doppler transform)."""
+    for L in (1, 7, 101, 1024, 4096, 4097):
+        for G in (1, 2, 3, 4, 8):
+            if G > L:
+                continue
+            base, extra = divmod(L, G)
+            for r in range(G):
+                f, c = shard_rows(L, G, r)
+                for lag in range(f, f + c):
+                    assert _owner_kernel(lag, base, extra) == (r, lag - f)
+
+
+def _blocks_worker(rank, world, port, L, M, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # rank integrates Doppler blocks shard_rows(M) for every delay row ...
+        q0, qc = shard_rows(M, world, rank)
+        zpart = torch.tensor([[1000.0 * l + qq for qq in range(q0, q0 + qc)] for l in range(L)])
+        # ... and each z row reaches its owner (CPU stand-in for the kernel's peer stores)
+        parts = [None] * world
+        dist.all_gather_object(parts, (q0, zpart))
+        f, c = shard_rows(L, world, rank)
+        mine = torch.zeros((c, M))
+        for (p0, zp) in parts:
+            for lag in range(f, f + c):
+                o, row = _owner_kernel(lag, L // world, L % world)
+                assert o == rank
+                mine[row, p0:p0 + zp.shape[1]] = zp[lag]
+        want = torch.tensor([[1000.0 * l + qq for qq in range(M)] for l in range(f, f + c)])
+        q.put(bool(torch.equal(mine, want)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_block_sharded_exchange_world2():
+    """World 2 (gloo): block partition of the lag stage + owner rows give every
+    rank exactly its delay rows over all Doppler blocks (uneven L and M)."""
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_blocks_worker, args=(r, 2, port, 13, 9, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    assert all(res)
