@@ -10,4 +10,4 @@ $B > gpurun_out/plain_bench.log 2>&1 && \
 echo "launch list rc=$?"
 bash tools/gpu_prof.sh ndft_tc:k_ndft_tc:ndft_tc:c64 ndft:k_ndft_fast:ndft:c64 ndft64:k_ndft_fast:ndft:c128 \
     nlfft64k:k_nlfft64k:nlfft:c64 nlfft64k_c128:k_nlfft64k:nlfft:c128 \
-    nlfft64k_dif:k_nlfft64k:nlfft_dif:c64 lag:k_lag_integrate:map:c64 detect:k_peaks_tile:detect:c64
+    nlfft64k_dif:k_nlfft64k:nlfft_dif:c64 lag:k_lag_tc:map:c64 detect:k_peaks_tile:detect:c64
