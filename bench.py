@@ -264,7 +264,8 @@ def roof_tensor(achieved_tflops):
             "traffic": tr["bytes_per_launch"] if tr else None, "traffic_unit": "bytes/launch",
             "traffic_source": tr["source"] if tr else None,
             "algorithmic_bytes": 2 * 65536 * 1024 * 8, "kernel": "k_ndft_tc",
-            "peak_source": f"{src} bf16_tflops (burst; sustained {peaks.get('bf16_tflops_sustained')})",
+            "peak_source": f"{src} bf16_tflops (burst, cuBLAS 8192^3; sustained {peaks.get('bf16_tflops_sustained')})",
+            "nominal_peak": 2250.0, "frac_nominal": round(achieved_tflops / 2250.0, 4),
             "algorithmic": "32 bf16 tensor flop per complex ⊙: re/im outputs x re/im inputs x "
                            "{sgn(x)·W0, sgn(x)·W1, X0·sgn(W), X1·sgn(W)} MACs (two-term bf16 splits)",
             **({"ncu_utilisation_pct": tr["ncu"]} if tr and tr.get("ncu") else {})}
@@ -414,7 +415,8 @@ def roof_lag(dtype, ns, lags, lms):
         ach = 32 * ns * lags / (lms * 1e-3) / 1e12
         return {"bound": "tensor", "achieved": round(ach, 1), "peak": peak, "unit": "TFLOP/s",
                 "frac": round(ach / peak, 4), "traffic": None, "kernel": lag_kernel(dtype), "kernel_ms": lms,
-                "peak_source": f"{src} bf16_tflops (burst)",
+                "peak_source": f"{src} bf16_tflops (burst)", "nominal_peak": 2250.0,
+                "frac_nominal": round(ach / 2250.0, 4),
                 "algorithmic": "32 bf16 tensor flop per lag ⊙ (8 sign-split terms x 2 pieces); the Hankel "
                                "K range (T + 1024 per T samples) is overhead, not counted"}
     peak = fma_peak_tflops(dtype)
