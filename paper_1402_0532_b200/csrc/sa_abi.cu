@@ -222,6 +222,10 @@ int sa_ambiguity_map_v(int dtype, int lag_kind, const void *surv, const void *re
   if (doppler != SA_DOPPLER_NDFT)
     return sa_launch_nlfft(dtype, doppler == SA_DOPPLER_NLFFT ? SA_DIT : SA_FFT_EXACT, workspace, out, l_count,
                            m, (const SaTwiddles *)tw, gain, s);
+  if (ns != m && mode == SA_NDFT_FAST) {  // fast-mode Doppler NDFT: the tensor-core kernel where it applies
+    rc = sa_launch_ndft_tc(workspace, out, l_count, m, (const SaTwiddles *)tw, gain, s);
+    if (rc != SA_ERR_UNSUPPORTED) return rc;
+  }
   return sa_launch_ndft(dtype, workspace, out, l_count, m, (const SaTwiddles *)tw,
                         ns == m ? SA_NDFT_EXACT : mode, gain, s);
 }

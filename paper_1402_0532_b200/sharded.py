@@ -286,7 +286,7 @@ def map_blocks_sharded(surv, ref, l_bins: int, m: int, zx: ZExchange, pm: PeerMa
                 pm.rows_ptr(zx.first)), zx.count, m, ctypes.c_void_p(tw), float(gain), _native.stream_ptr()))
         else:
             _native.check(_native.lib().sa_ndft(d, _native.ptr(zx.z), ctypes.c_void_p(pm.rows_ptr(zx.first)),
-                                                zx.count, m, ctypes.c_void_p(tw), _native.SA_NDFT_FAST,
+                                                zx.count, m, ctypes.c_void_p(tw), _native.SA_NDFT_TC,
                                                 float(gain), _native.stream_ptr()))
     _done(pm.done_flag(), group)  # every rank's rows are in the root's map
 

@@ -92,3 +92,23 @@ def test_lag_tc_map_c4_rows(sa):
     for l in [0, 1, 511, 1023] + [int(t) for t in sc.delays]:
         r = oracle.ambiguity_map(surv.astype(np.complex128), ref.astype(np.complex128), l, 1, 512, nthreads=8)
         assert_literal(y[l:l + 1], r, TOL_F32)
+
+
+def test_map_ndft_doppler_tc_rows(sa):
+    """C4 map with the NDFT along Doppler (fast mode, complex64, M = 512): both
+    the lag stage and the Doppler NDFT run on the tensor cores; rows vs the oracle,
+    and a row range alone equals the same rows of the full map bit for bit."""
+    import oracle
+    import torch
+    from paper_1402_0532_b200.workloads import c4_scene
+    sc = c4_scene()
+    surv = sc.surv.astype(np.complex64)
+    ref = sc.ref.astype(np.complex64)
+    ds, dr = torch.from_numpy(surv).cuda(), torch.from_numpy(ref).cuda()
+    y = sa.ambiguity_map(ds, dr, 1024, 512, doppler="ndft")
+    for l in [0, 1023] + [int(t) for t in sc.delays]:
+        r = oracle.ambiguity_map(surv.astype(np.complex128), ref.astype(np.complex128), l, 1, 512,
+                                 doppler="ndft", nthreads=8)
+        assert_literal(y[l:l + 1].cpu().numpy(), r, TOL_F32)
+    part = sa.ambiguity_map(ds, dr, 200, 512, l0=300, doppler="ndft")
+    assert torch.equal(part, y[300:500])
