@@ -119,12 +119,18 @@ SA_HD void mbar_arrive_cl(uint32_t cl_addr) {
   // .cluster-scope form costs a MEMBAR.GPU per arrive (measured: 2.8 vs 1.7 ms)
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
 }
-SA_HD void tma_load_2d_cg2(uint32_t dst, const CUtensorMap *map, int c0, int c1, uint32_t lead_bar) {
+// twiddle operand tiles are re-read by every vector tile: keep them in L2 (evict_last)
+SA_HD void tma_load_2d_cg2(uint32_t dst, const CUtensorMap *map, int c0, int c1, uint32_t lead_bar, uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
-      "%3}], [%4];" ::"r"(dst),
-      "l"(map), "r"(c0), "r"(c1), "r"(lead_bar)
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(lead_bar), "l"(pol)
       : "memory");
+}
+SA_HD uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 SA_HD uint32_t cluster_rank() {
   uint32_t r;
@@ -217,6 +223,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---- TMA producer: this CTA's rows of the twiddle operand tiles ----
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(&wmap) : "memory");
+      const uint64_t wpol = l2_policy_evict_last();
       for (int64_t it = 0; it < total; ++it) {
         const int64_t lt = it / kslots;
         const int kc = (int)(it - lt * kslots);
@@ -232,7 +239,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             unsigned char *dst = b + p * B_TILE + hh * C::BROWS * KS * 2;
             const int row = p * 2 * n + o0 + hh * BN;
             if (CG == 1) sa_tma_load_2d(dst, &wmap, kc * KS, row, &full[s]);
-            else tma_load_2d_cg2(sa_smem_u32(dst), &wmap, kc * KS, row, lead(&full[s]));
+            else tma_load_2d_cg2(sa_smem_u32(dst), &wmap, kc * KS, row, lead(&full[s]), wpol);
           }
       }
     }
@@ -289,9 +296,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (v < batch) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            dst[c * 8 + j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                         __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+          for (int j = 0; j < 8; ++j)  // streaming stores (evict-first): keep x, re-read by the
+            __stcs(&dst[c * 8 + j],      // other output tiles of this vector tile, in L2
+                   make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                               __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])));
         }
       }
       tc_fence_before();
