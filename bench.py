@@ -449,7 +449,7 @@ def wl_map(args, ws, rank, c5=False):
             pm = PeerMap(L, M, cdt)
         except PeerMapUnavailable:  # (all ranks agree) NCCL gather instead
             transport = "gather"
-        if pm is not None and blocks_shardable(surv, M, "fast", "mf", "nfft"):
+        if pm is not None and blocks_shardable(surv, M, "fast", "mf", "nfft", L, ws):
             try:  # the z-row blocks of every rank, IPC-shared once (block-sharded lag stage)
                 zx = ZExchange(L, M, cdt)
             except PeerMapUnavailable:

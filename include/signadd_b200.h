@@ -123,7 +123,11 @@ int sa_ambiguity_workspace_bytes(int dtype, int64_t l_count, int64_t m, int64_t 
  * With m == ns (T == 1) this is ambiguity_eq12a (ambiguity.py:197-202) for the
  * rows requested, value-identical for the NL-FFT Doppler transform.
  * mode: SA_NDFT_FAST uses the regrouped 8-FMA lag accumulation for T > 1;
- * SA_NDFT_EXACT rounds every ⊙ (always used when T == 1).
+ * SA_NDFT_EXACT rounds every ⊙ (always used when T == 1).  In SA_NDFT_FAST,
+ * complex64, T > 1: the lag stage runs on tcgen05 when T % 128 == 0, and an
+ * NDFT Doppler stage runs as SA_NDFT_TC when m % 128 == 0 (both within the
+ * fp32 tolerance; the first tensor-core call per twiddle set builds its
+ * 3 x (2m)^2 bf16 operands, kept until sa_twiddle_destroy, stream-ordered).
  * tw: twiddle set for m.  Rows are independent (ambiguity.py:27-28): any row
  * range may be computed on any device (delay-bin sharding). */
 int sa_ambiguity_map(int dtype, const void *surv, const void *ref, int64_t ns, int64_t ref_len,

@@ -61,7 +61,7 @@ int sa_twiddle_create(int device, int dtype, int64_t n, const double *host_table
   int prev = 0;
   SA_CUDA_TRY(cudaGetDevice(&prev));
   SA_CUDA_TRY(cudaSetDevice(device));
-  SaTwiddles *tw = new SaTwiddles{dtype, n, device, nullptr, nullptr, nullptr, nullptr, nullptr};
+  SaTwiddles *tw = new SaTwiddles{dtype, n, device, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   int rc = sa_twiddles_build(tw, host_table, (cudaStream_t)stream);
   cudaSetDevice(prev);
   if (rc != SA_OK) {
@@ -88,6 +88,7 @@ int sa_twiddle_destroy(void *handle) {
   cudaFree(tw->stage);
   cudaFree(tw->stage2);
   cudaFree(tw->tcw);
+  if (tw->tcw_ready) cudaEventDestroy((cudaEvent_t)tw->tcw_ready);
   cudaSetDevice(prev);
   delete tw;
   return SA_OK;
@@ -270,7 +271,7 @@ int sa_ambiguity_integrate_blocks(int dtype, const void *surv, const void *ref, 
   if (rc) return rc;
   SA_REQUIRE(surv && ref, SA_ERR_ARG, "null pointer");
   if (!sa_lag_tc_supported(dtype, ns / m, m, surv)) return SA_ERR_UNSUPPORTED;
-  return sa_launch_lag_tc_blocks(surv, ref, l0, l_count, m, q0, q_count, ns / m, conj, nullptr, dst_rows,
+  return sa_launch_lag_tc_blocks(surv, ref, ref_len, l0, l_count, m, q0, q_count, ns / m, conj, nullptr, dst_rows,
                                  l_count / n_dst, l_count % n_dst, (cudaStream_t)stream);
 }
 

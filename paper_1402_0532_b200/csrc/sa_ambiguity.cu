@@ -555,7 +555,7 @@ int launch_integrate(int lag_kind, const void *survv, const void *refv, int64_t 
 #ifndef SA_NO_LAG_TC
   // fast mode, complex64, T % 128 == 0: Hankel GEMM on the tcgen05 tensor cores (sa_lag_tc.cu)
   if (mode == SA_NDFT_FAST && !exact_lag && sa_lag_tc_supported(sizeof(T) == 4 ? SA_C64 : SA_C128, tb, m, survv))
-    return sa_launch_lag_tc(survv, refv, l0, l_count, m, tb, conj, zv, s);
+    return sa_launch_lag_tc(survv, refv, ref_len, l0, l_count, m, tb, conj, zv, s);
 #endif
 
   // fast mode, complex64, T % 16 == 0: packed pair kernel.  NT is the largest of

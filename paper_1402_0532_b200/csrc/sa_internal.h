@@ -18,6 +18,7 @@ struct SaTwiddles {
                 //   stage s (1..log2 n) at offset 2^(s-1)-1, entry j = table[j*n/2^s]
   void *stage2; // (n-1) x {wr, wi}, same stage-packed order (8/16-byte entries)
   void *tcw;    // tensor-core NDFT operands [W0; W1; sgn Wv] (bf16, 3 x 2n x 2n), built on first use
+  void *tcw_ready;  // cudaEvent_t recorded after the tcw build (streams wait on it)
 };
 
 void sa_set_error(const char *fmt, ...);
@@ -62,9 +63,10 @@ int sa_launch_ndft_tc(const void *x, void *y, int64_t batch, int64_t n, const Sa
 
 // sa_lag_tc.cu (tensor-core fast-mode lag integration, complex64)
 bool sa_lag_tc_supported(int dtype, int64_t tb, int64_t m, const void *surv);
-int sa_launch_lag_tc(const void *surv, const void *ref, int64_t l0, int64_t l_count, int64_t m, int64_t tb, int conj,
-                     void *z, cudaStream_t s);
-int sa_launch_lag_tc_blocks(const void *surv, const void *ref, int64_t l0, int64_t l_count, int64_t m, int64_t q0,
+int sa_launch_lag_tc(const void *surv, const void *ref, int64_t ref_len, int64_t l0, int64_t l_count, int64_t m,
+                     int64_t tb, int conj, void *z, cudaStream_t s);
+int sa_launch_lag_tc_blocks(const void *surv, const void *ref, int64_t ref_len, int64_t l0, int64_t l_count, int64_t m,
+                            int64_t q0,
                             int64_t q_count, int64_t tb, int conj, void *z, void *const *dst_rows, int64_t rows_base,
                             int64_t rows_extra, cudaStream_t s);
 

@@ -85,11 +85,13 @@ SA_HD uint32_t bf2(float hi, float lo) {  // {lo -> bits 0..15, hi -> bits 16..3
       : "r"(taddr))
 
 // the 8 conj-ref values a B-builder thread needs: c[g0 .. g0+7] (0 before the signal start)
-SA_HD void load_c(float2 (&cv)[8], const float2 *__restrict__ ref, int64_t g0, float csign) {
+// and from ref_len on: lags below the call's range (groups start at multiples of 16)
+// reach past the end, and 0 x NaN in the MMA would poison the kept rows
+SA_HD void load_c(float2 (&cv)[8], const float2 *__restrict__ ref, int64_t g0, int64_t ref_len, float csign) {
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     const int64_t g = g0 + e;
-    float2 v = g >= 0 ? __ldg(&ref[g]) : make_float2(0.f, 0.f);
+    float2 v = (g >= 0 && g < ref_len) ? __ldg(&ref[g]) : make_float2(0.f, 0.f);
     cv[e] = make_float2(v.x, csign * v.y);
   }
 }
@@ -113,7 +115,7 @@ struct LagDst {
 // G lag groups share each A read (one pass): the MMAs widen to N = 32 G / 16 G.
 template <int G>
 __global__ void __launch_bounds__(THREADS, 2)
-    k_lag_tc(const float2 *__restrict__ surv, const float2 *__restrict__ ref, int64_t l0g, int64_t l_count,
+    k_lag_tc(const float2 *__restrict__ surv, const float2 *__restrict__ ref, int64_t ref_len, int64_t l0g, int64_t l_count,
              int64_t m, int tb, float csign, float2 *__restrict__ z, int64_t q0, LagDst dst) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -212,7 +214,7 @@ __global__ void __launch_bounds__(THREADS, 2)
       // c index of (u, l0) for this thread's group: q T - lbase + u - l0
       const int64_t cbase = q * tb - (lpass + (int64_t)bg * LGRP) - PAD - bl0 + boct * 8;
       float2 cv[8];
-      load_c(cv, ref, cbase, csign);
+      load_c(cv, ref, cbase, ref_len, csign);
       for (int ch = 0; ch < nch; ++ch, ++cc) {
         const int b = cc & 1;
         if (cc >= 2) sa_mbar_wait(&bar[b], ((cc >> 1) - 1) & 1);  // MMAs that read this buffer are done
@@ -262,7 +264,7 @@ __global__ void __launch_bounds__(THREADS, 2)
             put(80 * G, 16, 1, sr);     //     sgn cr
           }
         }
-        if (ch + 1 < nch) load_c(cv, ref, cbase + (int64_t)(ch + 1) * KCH, csign);  // next chunk's values
+        if (ch + 1 < nch) load_c(cv, ref, cbase + (int64_t)(ch + 1) * KCH, ref_len, csign);  // next chunk's values
         sa_fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05.mma
         __syncwarp();
         if (lane == 0) sa_mbar_arrive_local(&full[b]);
@@ -312,12 +314,13 @@ bool sa_lag_tc_supported(int dtype, int64_t tb, int64_t m, const void *surv) {
          ((uintptr_t)surv & 15) == 0;
 }
 
-int sa_launch_lag_tc(const void *surv, const void *ref, int64_t l0, int64_t l_count, int64_t m, int64_t tb, int conj,
-                     void *z, cudaStream_t s) {
-  return sa_launch_lag_tc_blocks(surv, ref, l0, l_count, m, 0, m, tb, conj, z, nullptr, 0, 0, s);
+int sa_launch_lag_tc(const void *surv, const void *ref, int64_t ref_len, int64_t l0, int64_t l_count, int64_t m,
+                     int64_t tb, int conj, void *z, cudaStream_t s) {
+  return sa_launch_lag_tc_blocks(surv, ref, ref_len, l0, l_count, m, 0, m, tb, conj, z, nullptr, 0, 0, s);
 }
 
-int sa_launch_lag_tc_blocks(const void *surv, const void *ref, int64_t l0, int64_t l_count, int64_t m, int64_t q0,
+int sa_launch_lag_tc_blocks(const void *surv, const void *ref, int64_t ref_len, int64_t l0, int64_t l_count, int64_t m,
+                            int64_t q0,
                             int64_t q_count, int64_t tb, int conj, void *z, void *const *dst_rows, int64_t rows_base,
                             int64_t rows_extra, cudaStream_t s) {
   if (l_count == 0 || q_count == 0) return SA_OK;
@@ -326,9 +329,16 @@ int sa_launch_lag_tc_blocks(const void *surv, const void *ref, int64_t l0, int64
   const int64_t ngrp = ((l0 & 15) + l_count + LGRP - 1) / LGRP;
   const int g = ngrp >= 3 ? 4 : (int)ngrp;
   auto kern = g == 4 ? k_lag_tc<4> : (g == 2 ? k_lag_tc<2> : k_lag_tc<1>);
-  SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  static int smem_set[64][3] = {};  // largest smem size set per (device, instantiation)
+  int dev = 0;
+  SA_CUDA_TRY(cudaGetDevice(&dev));
+  const int gi = g == 4 ? 2 : g - 1;
+  if (dev >= 64 || smem_set[dev][gi] < (int)bytes) {
+    SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    if (dev < 64) smem_set[dev][gi] = (int)bytes;
+  }
   const LagDst d{(float2 *const *)dst_rows, rows_base, rows_extra};
-  kern<<<(unsigned)q_count, THREADS, bytes, s>>>((const float2 *)surv, (const float2 *)ref, l0, l_count, m, (int)tb,
+  kern<<<(unsigned)q_count, THREADS, bytes, s>>>((const float2 *)surv, (const float2 *)ref, ref_len, l0, l_count, m, (int)tb,
                                                  conj ? -1.f : 1.f, (float2 *)z, q0, d);
   SA_LAUNCH_CHECK();
   return SA_OK;

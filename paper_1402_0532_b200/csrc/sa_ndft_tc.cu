@@ -35,6 +35,9 @@
 // TMA-staged x (1.73-1.76 ms: fewer slots fit), 16 converter warps (1.61 ms),
 // cluster-scope release/acquire on the pair barriers (MEMBAR.GPU per arrive: 2.8 ms).
 #include <cuda.h>
+
+#include <map>
+#include <tuple>
 #include <cudaTypedefs.h>
 
 #include <mutex>
@@ -413,21 +416,34 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn_tc() {
   return fn;
 }
 
+// Tensor maps of the twiddle operands, encoded once per (operand buffer, n, box rows).
+std::map<std::tuple<const void *, int64_t, int>, CUtensorMap> g_tc_maps;
+
 template <int CG, int TN>
 int launch_tc(const void *x, void *y, int64_t batch, int64_t n, SaTwiddles *tw, double gain, cudaStream_t s) {
   using Cf = TcCfg<CG, TN>;
-  auto enc = encode_fn_tc();
   CUtensorMap map;
-  cuuint64_t dims[2] = {(cuuint64_t)(2 * n), (cuuint64_t)(6 * n)};
-  cuuint64_t strides[1] = {(cuuint64_t)(2 * n * 2)};
-  cuuint32_t box[2] = {(cuuint32_t)KS, (cuuint32_t)Cf::BROWS};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, tw->tcw, dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    sa_set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
-    return SA_ERR_CUDA;
+  {
+    std::lock_guard<std::mutex> g(g_tc_mutex);
+    const auto key = std::make_tuple((const void *)tw->tcw, n, (int)Cf::BROWS);
+    auto it = g_tc_maps.find(key);
+    if (it == g_tc_maps.end()) {
+      auto enc = encode_fn_tc();
+      cuuint64_t dims[2] = {(cuuint64_t)(2 * n), (cuuint64_t)(6 * n)};
+      cuuint64_t strides[1] = {(cuuint64_t)(2 * n * 2)};
+      cuuint32_t box[2] = {(cuuint32_t)KS, (cuuint32_t)Cf::BROWS};
+      cuuint32_t estr[2] = {1, 1};
+      CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, tw->tcw, dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) {
+        sa_set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+        return SA_ERR_CUDA;
+      }
+      g_tc_maps.emplace(key, map);
+    } else {
+      map = it->second;
+    }
   }
   static bool smem_set[64] = {};
   int dev = 0;
@@ -473,16 +489,22 @@ int sa_launch_ndft_tc(const void *x, void *y, int64_t batch, int64_t n, const Sa
   if (batch == 0) return SA_OK;
   SaTwiddles *tw = const_cast<SaTwiddles *>(tw_c);
   {
+    // operands built once per twiddle set, stream-ordered (no host sync): on the
+    // first caller's stream, with an event every later launch's stream waits on
     std::lock_guard<std::mutex> g(g_tc_mutex);
     if (!tw->tcw) {
       void *w = nullptr;
+      cudaEvent_t ev = nullptr;
       SA_CUDA_TRY(cudaMalloc(&w, sa_ndft_tc_wbytes(n)));
       k_tc_wbuild<<<1184, 256, 0, s>>>((const float2 *)tw->raw, (int)n, (uint16_t *)w);
       SA_LAUNCH_CHECK();
-      SA_CUDA_TRY(cudaStreamSynchronize(s));  // once per set: other streams may use it next
+      SA_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      SA_CUDA_TRY(cudaEventRecord(ev, s));
       tw->tcw = w;
+      tw->tcw_ready = ev;
     }
   }
+  if (tw->tcw_ready) SA_CUDA_TRY(cudaStreamWaitEvent(s, (cudaEvent_t)tw->tcw_ready, 0));
   auto enc = encode_fn_tc();
   if (!enc) {
     sa_set_error("cuTensorMapEncodeTiled unavailable");

@@ -161,10 +161,15 @@ class PeerMap:
         """Device address (valid on this rank's GPU) of the root's row ``first``."""
         return self.base + first * self.row_bytes
 
-    def close(self) -> None:
+    def close(self, barrier: bool = True) -> None:
+        """Unmap the root's map on this rank (after this rank's kernels finished;
+        with ``barrier``, after every rank's).  The root keeps ``full``."""
+        import torch
         import torch.distributed as dist
         from . import _native
-        dist.barrier(group=self.group)  # nobody still writes
+        torch.cuda.current_stream().synchronize()  # this rank's stores into the mapping are done
+        if barrier:
+            dist.barrier(group=self.group)  # nobody still writes
         if self._mapped is not None:
             _native.check(_native.lib().sa_ipc_close(self._mapped))
             self._mapped = None
@@ -228,8 +233,10 @@ class ZExchange:
         self.table = torch.tensor(bases, dtype=torch.int64, device="cuda")
 
     def close(self, barrier: bool = True) -> None:
+        import torch
         import torch.distributed as dist
         from . import _native
+        torch.cuda.current_stream().synchronize()  # this rank's peer stores are done
         if barrier:
             dist.barrier(group=self.group)
         for p in self._mapped:
@@ -249,14 +256,17 @@ def _done(flag, group):
         dist.barrier(group=group)
 
 
-def blocks_shardable(surv, m: int, mode: str, lag: str, doppler: str) -> bool:
+def blocks_shardable(surv, m: int, mode: str, lag: str, doppler: str, l_bins: int | None = None,
+                     world: int = 1) -> bool:
     """Whether the block-sharded map applies: the tensor-core lag path
-    (sa_lag_tc_supported: complex64 fast ⊙ lags, T % 128 == 0, T <= 4096) and a
-    Doppler transform of the z rows.  Shapes only, so every rank agrees."""
+    (sa_lag_tc_supported: complex64 fast ⊙ lags, T % 128 == 0, T <= 4096), a
+    Doppler transform of the z rows, and at least one delay row per rank
+    (sa_ambiguity_integrate_blocks needs n_dst <= l_count).  Shapes only, so every
+    rank agrees."""
     import torch
     tb = surv.numel() // m if m else 0
     return (surv.dtype == torch.complex64 and mode == "fast" and lag == "mf" and doppler in ("nfft", "ndft")
-            and 128 <= tb <= 4096 and tb % 128 == 0)
+            and 128 <= tb <= 4096 and tb % 128 == 0 and (l_bins is None or l_bins >= world))
 
 
 def map_blocks_sharded(surv, ref, l_bins: int, m: int, zx: ZExchange, pm: PeerMap, *, gain: float = 1.0,
@@ -291,6 +301,48 @@ def map_blocks_sharded(surv, ref, l_bins: int, m: int, zx: ZExchange, pm: PeerMa
     _done(pm.done_flag(), group)  # every rank's rows are in the root's map
 
 
+def _map_p2p(surv, ref, l_bins, m, pm, z_exchange, *, gain, conjugate_ref, doppler, mode, lag, group, dst,
+             workspace):
+    import torch
+    import torch.distributed as dist
+    from .ambiguity import ambiguity_map
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    first, count = shard_rows(l_bins, world, rank)
+    if world > 1 and blocks_shardable(surv, m, mode, lag, doppler, l_bins, world):
+        if surv.data_ptr() % 16:  # the tensor-core lag kernel reads 16-byte sample pairs
+            surv = surv.clone()
+        zx = z_exchange
+        try:
+            if zx is None:
+                zx = ZExchange(l_bins, m, surv.dtype, group=group)
+        except PeerMapUnavailable:  # (all ranks agree) delay-row shards instead
+            zx = None
+        if zx is not None:
+            try:
+                map_blocks_sharded(surv, ref, l_bins, m, zx, pm, gain=gain, conjugate_ref=conjugate_ref,
+                                   doppler=doppler, group=group)
+            except BaseException:
+                if z_exchange is None:  # built here: released on the error path too (no collective)
+                    zx.close(barrier=False)
+                raise
+            if z_exchange is None:
+                zx.close()
+            return pm.full if rank == dst else None
+    if count:
+        ambiguity_map(surv, ref, count, m, l0=first, gain=gain, conjugate_ref=conjugate_ref,
+                      doppler=doppler, mode=mode, lag=lag, out_ptr=pm.rows_ptr(first), workspace=workspace)
+    if dist.get_backend(group) == "nccl":
+        # stream-ordered: NCCL's stream waits for this rank's transform kernel,
+        # the caller's stream waits for the all-reduce -- once it completes on
+        # the root, every rank's row stores into its map are done (no host sync)
+        dist.all_reduce(pm.done_flag(), group=group)
+    else:
+        torch.cuda.current_stream().synchronize()  # this rank's rows are in the root's memory
+        dist.barrier(group=group)                  # ... and so are everyone's
+    return pm.full if rank == dst else None
+
+
 def ambiguity_map_sharded(surv, ref, l_bins: int, m: int, *, gain: float = 1.0,
                           conjugate_ref: bool = True, doppler: str = "nfft", mode: str = "fast",
                           lag: str = "mf", group=None, dst: int = 0, transport: str = "p2p",
@@ -309,40 +361,26 @@ def ambiguity_map_sharded(surv, ref, l_bins: int, m: int, *, gain: float = 1.0,
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     first, count = shard_rows(l_bins, world, rank)
+    own_pm = False
     if transport == "p2p" and peer_map is None:
         try:
             peer_map = PeerMap(l_bins, m, surv.dtype, group=group, dst=dst)
+            own_pm = True
         except PeerMapUnavailable:
             transport = "gather"
-    if transport == "p2p" and world > 1 and blocks_shardable(surv, m, mode, lag, doppler):
-        if surv.data_ptr() % 16:  # the tensor-core lag kernel reads 16-byte sample pairs
-            surv = surv.clone()
-        zx = z_exchange
-        try:
-            if zx is None:
-                zx = ZExchange(l_bins, m, surv.dtype, group=group)
-        except PeerMapUnavailable:  # (all ranks agree) delay-row shards instead
-            zx = None
-        if zx is not None:
-            map_blocks_sharded(surv, ref, l_bins, m, zx, peer_map, gain=gain, conjugate_ref=conjugate_ref,
-                               doppler=doppler, group=group)
-            if z_exchange is None:
-                zx.close()
-            return peer_map.full if rank == dst else None
     if transport == "p2p":
-        pm = peer_map
-        if count:
-            ambiguity_map(surv, ref, count, m, l0=first, gain=gain, conjugate_ref=conjugate_ref,
-                          doppler=doppler, mode=mode, lag=lag, out_ptr=pm.rows_ptr(first), workspace=workspace)
-        if dist.get_backend(group) == "nccl":
-            # stream-ordered: NCCL's stream waits for this rank's transform kernel,
-            # the caller's stream waits for the all-reduce -- once it completes on
-            # the root, every rank's row stores into its map are done (no host sync)
-            dist.all_reduce(pm.done_flag(), group=group)
-        else:
-            torch.cuda.current_stream().synchronize()  # this rank's rows are in the root's memory
-            dist.barrier(group=group)                  # ... and so are everyone's
-        return pm.full if rank == dst else None
+        from .ambiguity import _dev
+        surv, ref = _dev(surv, surv.dtype), _dev(ref, surv.dtype)  # as ambiguity_map: flat, contiguous, one dtype
+        try:
+            out = _map_p2p(surv, ref, l_bins, m, peer_map, z_exchange, gain=gain, conjugate_ref=conjugate_ref,
+                           doppler=doppler, mode=mode, lag=lag, group=group, dst=dst, workspace=workspace)
+        except BaseException:
+            if own_pm:  # a mapping opened here is released on the error path too (no collective)
+                peer_map.close(barrier=False)
+            raise
+        if own_pm:  # ... and after the final completion point otherwise
+            peer_map.close()
+        return out
     if transport != "gather":
         raise ValueError(f"unknown transport {transport!r}")
     if out_local is None:

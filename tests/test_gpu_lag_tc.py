@@ -112,3 +112,28 @@ def test_map_ndft_doppler_tc_rows(sa):
         assert_literal(y[l:l + 1].cpu().numpy(), r, TOL_F32)
     part = sa.ambiguity_map(ds, dr, 200, 512, l0=300, doppler="ndft")
     assert torch.equal(part, y[300:500])
+
+
+@pytest.mark.parametrize("l0", [3, 13])
+def test_lag_tc_short_ref_never_read_past_end(sa, l0):
+    """lag groups start at multiples of 16, so lags below l0 reach
+    ref[ns - lalign - 1] > ref_len - 1 when ref is trimmed to ns - l0 (allowed by
+    the lag_product_mf guards, ambiguity.py:121-128).  The words past ref_len are
+    NaN here; the kept rows must stay finite and equal the restatement."""
+    import torch
+    from paper_1402_0532_b200 import _native
+    ns, m = 2048 * 8, 8
+    surv, ref = signals(21 + l0, ns)
+    rl = ns - l0
+    buf = np.full(ns + 64, np.nan + 1j * np.nan, np.complex64)
+    buf[:rl] = ref[:rl]
+    ds = torch.from_numpy(surv).cuda()
+    db = torch.from_numpy(buf).cuda()
+    L = 40
+    z = torch.empty((L, m), dtype=torch.complex64, device="cuda")
+    _native.check(_native.lib().sa_ambiguity_integrate(
+        _native.SA_C64, _native.ptr(ds), _native.ptr(db), ns, rl, l0, L, m, 1, _native.SA_NDFT_FAST,
+        _native.ptr(z), _native.stream_ptr()))
+    got = z.cpu().numpy()
+    assert np.isfinite(got).all()
+    assert_literal(got, z_ref(surv, ref[:rl], l0, L, m), TOL_F32)
