@@ -125,6 +125,8 @@ def _dev(x, dtype):
     if is_device_tensor(x):
         t = x.reshape(-1)
         return (t if t.dtype == dtype else t.to(dtype)).contiguous()
+    if isinstance(x, T.Tensor):  # host tensor (pinned: the upload is asynchronous)
+        return to_device(x.reshape(-1), dtype)
     return to_device(np.ascontiguousarray(np.asarray(x).reshape(-1)), dtype)
 
 
@@ -173,8 +175,9 @@ def ambiguity_map(s_surv, s_ref, l_bins: int, m: int, *, l0: int = 0, gain: floa
                   lag: str = "mf", out=None, workspace=None, dtype=None, out_ptr: int | None = None):
     """Rows l0..l0+l_bins-1 of the block-integrated range-Doppler map.
 
-    Inputs: CUDA tensors (stay on device, no sync) or host arrays (result
-    returned on the host).  Ns = len(s_surv); T = Ns / m must be an integer.
+    Inputs: CUDA tensors (stay on device, no sync) or host arrays / tensors
+    (result returned on the host; a host tensor ``out`` -- pinned for an
+    asynchronous download -- receives it).  Ns = len(s_surv); T = Ns / m must be an integer.
     lag: "mf" (⊙, eq12a/eq12b) or "exact" (numpy multiply, eq11/eq12c);
     doppler: "nfft", "ndft" or "fft" (fft_exact).
     ``out_ptr``: raw device address of an (l_bins x m) row-major destination
@@ -186,8 +189,11 @@ def ambiguity_map(s_surv, s_ref, l_bins: int, m: int, *, l0: int = 0, gain: floa
     ref = _samples(s_ref)
     device_io = is_device_tensor(surv) or is_device_tensor(ref)
     if dtype is None:
-        dtype = surv.dtype if is_device_tensor(surv) else T.complex128
+        dtype = surv.dtype if isinstance(surv, T.Tensor) and surv.is_complex() else T.complex128
     require_cuda()
+    host_out = out if (out is not None and not is_device_tensor(out)) else None
+    if host_out is not None:
+        out = None
     ds = _dev(surv, dtype)
     dr = _dev(ref, dtype)
     ns = ds.numel()
@@ -219,6 +225,10 @@ def ambiguity_map(s_surv, s_ref, l_bins: int, m: int, *, l0: int = 0, gain: floa
         workspace.numel() * workspace.element_size(), _native.stream_ptr()))
     if out_ptr is not None:
         return None
+    if host_out is not None:
+        host_out.copy_(out, non_blocking=True)
+        T.cuda.current_stream().synchronize()
+        return host_out
     return out if device_io else out.cpu().numpy()
 
 

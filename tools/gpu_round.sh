@@ -3,10 +3,12 @@
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 nvidia-smi > gpurun_out/smi.txt 2>&1
-timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 900 --maxfail 40 -rf ${PYTEST_K:+-k "$PYTEST_K"} > gpurun_out/pytest_gpu.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 900 --maxfail 40 -rfs ${PYTEST_K:+-k "$PYTEST_K"} > gpurun_out/pytest_gpu.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 echo "smoke rc=$?" >> gpurun_out/smoke.log
+if [ -z "$NO_BENCH" ]; then
 timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
 echo "bench rc=$?" >> gpurun_out/bench.err
+fi
 tail -3 gpurun_out/pytest_gpu.log; tail -1 gpurun_out/smoke.log; cat gpurun_out/bench.json

@@ -14,5 +14,7 @@ rm -rf "$ROOT/baseline/_ref"
 python -m pip install -q --no-index --no-build-isolation --no-deps --find-links /opt/wheelhouse \
     --target "$ROOT/baseline/_ref" "$TMP/pkg"
 cp -r "$SRC/tests" "$ROOT/baseline/_ref/ref_tests"
+# the reference's own recorded CPU outcomes (the conformance run must reproduce them)
+cp "$SRC/test_output.txt" "$ROOT/baseline/_ref/ref_tests/reference_test_output.txt"
 rm -rf "$TMP"
 echo "install_ref: signadd installed into baseline/_ref (+ ref_tests)"
