@@ -211,16 +211,17 @@ def complex_dtype(name):
     return torch.complex64 if name == "c64" else torch.complex128
 
 
-def wl_ndft(args, ws, rank, mode=None, e2e=True):
+def wl_ndft(args, ws, rank, mode=None, e2e=True, dtype=None):
     """C2: batched NDFT N=1024 x 65536.  mode "tc" (complex64 default): the
     fast-mode sum as a sign-split bf16 GEMM on tcgen05 (sa_ndft_tc.cu); "fast":
-    the FFMA2 CUDA-core kernel (sa_ndft.cu)."""
+    the FFMA2 / DFMA CUDA-core kernel (sa_ndft.cu)."""
     import torch
     import paper_1402_0532_b200 as sa
     from paper_1402_0532_b200.workloads import c2_ndft
     n, batch = 1024, 65536
-    cdt = complex_dtype(args.dtype)
-    mode = mode or (args.ndft_mode if args.dtype == "c64" else "fast")
+    dtype = dtype or args.dtype
+    cdt = complex_dtype(dtype)
+    mode = mode or (args.ndft_mode if dtype == "c64" else "fast")
     t0 = time.time()
     xh = torch.from_numpy(c2_ndft(n, batch)).to(cdt)
     log(f"[rank {rank}] C2 input generated in {time.time() - t0:.1f}s")
@@ -228,13 +229,15 @@ def wl_ndft(args, ws, rank, mode=None, e2e=True):
     yd = torch.empty_like(xd)
     ops = batch * n * n
     step = lambda: sa.ndft_batch(xd, out=yd, mode=mode)  # noqa: E731
-    desc = ("tc (fast-mode sum as a sign-split bf16 GEMM on tcgen05 tensor cores, fp32 accumulation)"
-            if mode == "tc" else "fast (sign-split regrouped accumulation, FFMA2)")
+    desc = {"tc": "tc (fast-mode sum as a sign-split GEMM on tcgen05 tensor cores: bf16x2-split operands, "
+                  "fp32 accumulate)",
+            "fast": "fast (sign-split regrouped accumulation, " + ("FFMA2)" if dtype == "c64" else "DFMA)")}[mode]
     res = {"ops": ops, "step": step, "launches_per_step": 1,
            "config": {"workload": "C2 batched NDFT (BASELINE.json configs[1])", "n": n,
                       "batch": batch, "mode": desc,
-                      "dtype": "complex64" if args.dtype == "c64" else "complex128",
-                      "l2_policy": "inputs (512 MiB c64) larger than L2; no flush",
+                      "dtype": "complex64" if dtype == "c64" else "complex128",
+                      "l2_policy": f"inputs ({2 * n * batch * xh.element_size() >> 21} MiB in + out) larger "
+                                   "than L2; no flush",
                       "parallelism": f"dp{ws} (independent vectors, weak scaling)"}}
     if e2e and not args.no_e2e:
         hin = xh.pin_memory()
@@ -244,13 +247,50 @@ def wl_ndft(args, ws, rank, mode=None, e2e=True):
         res["h2d"] = hin.numel() * hin.element_size()
         res["d2h"] = hout.numel() * hout.element_size()
         res["e2e_api"] = f"paper_1402_0532_b200.ndft_batch(pinned host tensor, out=pinned host tensor, mode={mode!r})"
+        res["e2e_launches"] = len(_pipeline_plan(res["e2e_rows"], res["e2e_row_bytes"]))
     if mode == "tc":
         res["roofline"] = lambda ms: roof_tensor(ops * 32 / (ms * 1e-3) / 1e12)
+        res["dtype"] = "bf16x2-split x sign, f32 accumulate"
     else:
-        res["roofline"] = lambda ms: roof_alu(args.dtype, ops * 16 / (ms * 1e-3) / 1e12, args)
+        res["roofline"] = lambda ms: roof_alu(dtype, ops * 16 / (ms * 1e-3) / 1e12, "ndft")
+        res["dtype"] = "f32" if dtype == "c64" else "f64"
     res["cpu"] = lambda P: cpu_ndft(xh.numpy(), P)
-    res["dtype"] = "f32" if args.dtype == "c64" else "f64"
+    res["cpu_numpy"] = lambda P: numpy_ref_rows("ndft", xh.numpy(), P, per_task=2, tasks_per_worker=4)
     return res
+
+
+def wl_ndft64(args):
+    """C1: NDFT N=64 complex128, the exact-grid tone exp(j2π·7n/64) + 4096 CN(0,1)
+    vectors (BASELINE.json configs[0]); fast mode (DFMA kernel).  Launch-bound at
+    this size: reported, not a roofline target."""
+    import torch
+    import paper_1402_0532_b200 as sa
+    from paper_1402_0532_b200.workloads import c1_ndft64
+    xh = torch.from_numpy(c1_ndft64())
+    xd = xh.cuda()
+    yd = torch.empty_like(xd)
+    b, n = xd.shape
+    ops = b * n * n
+    res = {"ops": ops, "step": lambda: sa.ndft_batch(xd, out=yd, mode="fast"), "launches_per_step": 1,
+           "config": {"workload": "C1 NDFT N=64 (BASELINE.json configs[0])", "n": n, "batch": b,
+                      "dtype": "complex128", "mode": "fast (DFMA)", "rows": "row 0 = unit_tone(7, 64), then 4096 CN(0,1)"},
+           "dtype": "f64"}
+    res["roofline"] = lambda ms: roof_alu("c128", ops * 16 / (ms * 1e-3) / 1e12, "ndft")
+    res["cpu"] = lambda P: cpu_ndft(xh.numpy(), P, rows=b)
+    res["cpu_numpy"] = lambda P: numpy_ref_rows("ndft", xh.numpy(), P, per_task=max(1, b // (4 * P)),
+                                                tasks_per_worker=4, all_rows=True)
+    hin = xh.pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    res["e2e_step"] = lambda: sa.ndft_batch(hin, out=hout, mode="fast")
+    res["h2d"] = res["d2h"] = hin.numel() * hin.element_size()
+    res["e2e_api"] = "paper_1402_0532_b200.ndft_batch(pinned host tensor, out=pinned host tensor, mode='fast')"
+    res["e2e_launches"] = len(_pipeline_plan(b, n * 16))
+    return res
+
+
+def _pipeline_plan(rows, row_bytes):
+    from paper_1402_0532_b200.transforms import pipeline_plan
+    return pipeline_plan(rows, row_bytes, 128)
 
 
 def roof_tensor(achieved_tflops):
@@ -273,7 +313,8 @@ def roof_tensor(achieved_tflops):
 
 def ncu_traffic(kernel_prefix):
     """DRAM bytes (read + write) per launch of a kernel, from the committed ncu
-    --set full summary (profiles/*_kernels.json, tools/ncu_summary.py), or None."""
+    --set full summary (profiles/*_kernels.json, tools/ncu_summary.py), or None.
+    The newest round's file wins (files sort by round)."""
     import glob
     best = None
     for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_kernels.json"))):
@@ -291,15 +332,17 @@ def ncu_traffic(kernel_prefix):
     return best
 
 
-def roof_alu(dtype, achieved_tflops, args):
+NDFT_KERNELS = {"c64": "k_ndft_fast_f32x2", "c128": "k_ndft_fast<double"}
+
+
+def roof_alu(dtype, achieved_tflops, what="ndft"):
     peak = fma_peak_tflops(dtype)
-    kern = "k_ndft_fast_f32x2" if dtype == "c64" else "k_ndft_fast<double"
+    kern = NDFT_KERNELS[dtype] if what == "ndft" else what
     tr = ncu_traffic(kern)
     return {"bound": "fp32_alu" if dtype == "c64" else "fp64_alu", "achieved": round(achieved_tflops, 3),
             "peak": round(peak, 3), "unit": "TFLOP/s", "frac": round(achieved_tflops / peak, 4),
             "traffic": tr["bytes_per_launch"] if tr else None, "traffic_unit": "bytes/launch",
             "traffic_source": tr["source"] if tr else None,
-            "algorithmic_bytes": 2 * 65536 * 1024 * (8 if dtype == "c64" else 16),
             "kernel": kern,
             "peak_source": "measured live: sa_fma_peak, max(FFMA, FFMA2) for fp32 / DFMA for fp64 "
                            "(MEASURED_PEAKS.json has no CUDA-core figure)",
@@ -319,25 +362,87 @@ def roof_hbm(bytes_per_step, ms, kernel=None):
     return r
 
 
-def cpu_ndft(x, P):
+# --------------------------------------------------------------------------- CPU baselines
+def cpu_ndft(x, P, rows=None):
     import oracle
-    rows = min(x.shape[0], 4096, max(256, 40 * P))  # ~10-30 s of CPU work at ~30 ms/vector/core
+    rows = rows or min(x.shape[0], 4096, max(256, 40 * P))  # ~10-30 s of CPU work at ~30 ms/vector/core
     sample = np.ascontiguousarray(x[:rows])
     t = time.perf_counter()
     oracle.ndft(sample, dtype="f32" if sample.dtype == np.complex64 else "f64", nthreads=P)
     dt = time.perf_counter() - t
     n = x.shape[1]
     return {"value": rows * n * n / dt, "unit": "⊙/s", "cores": P, "kind": "port",
-            "sample": f"first {rows} of the C2 vectors (N={n}), oracle/signadd_oracle.c or_ndft "
+            "sample": f"first {rows} of the vectors (N={n}), oracle/signadd_oracle.c or_ndft "
                       f"(sequential, op-for-op restatement of transforms.py:223-251), {P} threads, "
                       f"{dt:.2f}s wall"}
 
 
-def wl_nlfft(args, ws, rank, variant="dit", batch=4096, n=1 << 16):
+def cpu_nlfft(x, variant, P):
+    import oracle
+    n = x.shape[1]
+    rows = min(x.shape[0], 8 * P)
+    sample = np.ascontiguousarray(x[:rows])
+    dts = "f32" if sample.dtype == np.complex64 else "f64"
+    t = time.perf_counter()
+    oracle.nfft(sample, variant, dtype=dts, nthreads=P)
+    dt = time.perf_counter() - t
+    per = n * (n.bit_length()) if variant == "dit" else (n // 2) * (n.bit_length() - 2) + 2 * n
+    return {"value": rows * per / dt, "unit": "⊙/s", "cores": P, "kind": "port",
+            "sample": f"first {rows} C3 vectors (N={n}), oracle/signadd_oracle.c or_nfft {variant.upper()} "
+                      f"({'op-for-op restatement of transforms.py:254-298' if variant == 'dit' else 'the DIF convention, DESIGN §3.3 (no reference)'}), "
+                      f"{P} threads, {dt:.2f}s wall"}
+
+
+def cpu_map(surv, ref, L, M, P):
+    import oracle
+    rows = min(L, 4 * P)
+    dts = "f32" if surv.dtype == np.complex64 else "f64"
+    t = time.perf_counter()
+    oracle.ambiguity_map(surv, ref, 0, rows, M, dtype=dts, nthreads=P)
+    dt = time.perf_counter() - t
+    ns = surv.size
+    ops = rows * ns + rows * M * (M.bit_length())
+    return {"value": rows * M / dt, "unit": "cells/s", "ops_per_s": ops / dt, "cores": P, "kind": "port",
+            "sample": f"delay rows 0..{rows - 1} of {L} (Ns={ns}, M={M}), oracle/signadd_oracle.c "
+                      f"or_ambiguity_map (lag_product_mf + block sums + nfft, ambiguity.py:146-187 composition), "
+                      f"{P} threads, {dt:.2f}s wall"}
+
+
+def numpy_ref_rows(kind, x, P, per_task, tasks_per_worker, all_rows=False):
+    """The unmodified numpy reference on Pool(P) (tools/refcpu.py)."""
+    from tools import refcpu
+    ntask = P * tasks_per_worker
+    rows = x.shape[0] if all_rows else min(x.shape[0], ntask * per_task)
+    per_task = -(-rows // ntask)
+    xs = x[:rows]
+    tasks = lambda P_: [(kind, i, min(rows, i + per_task)) for i in range(0, rows, per_task)]  # noqa: E731
+    try:
+        r = refcpu.measure(kind, {"x": xs}, tasks, P)
+    except Exception as ex:  # a baseline must not take the bench line down
+        return {"unavailable": repr(ex)}
+    r["sample"] = f"{rows} vectors, {per_task} per task, {len(tasks(P))} tasks on {P} workers"
+    return r
+
+
+def numpy_ref_map(surv, ref, L, M, P, rows_per_worker=4):
+    from tools import refcpu
+    lags = list(range(min(L, P * rows_per_worker)))
+    tasks = lambda P_: [("map", lags[i:i + rows_per_worker], M) for i in range(0, len(lags), rows_per_worker)]  # noqa: E731
+    try:
+        r = refcpu.measure("map", {"surv": surv, "ref": ref}, tasks, P)
+    except Exception as ex:
+        return {"unavailable": repr(ex)}
+    r["sample"] = (f"delay rows 0..{len(lags) - 1}: lag_product_mf(n={surv.size}) -> {surv.size // M}-sample block "
+                   f"sums -> nfft({M}), {rows_per_worker} rows per worker")
+    return r
+
+
+def wl_nlfft(args, ws, rank, variant="dit", batch=4096, n=1 << 16, dtype=None):
     """C3: NL-FFT 2^16 x 4096 (inputs synthesised on the GPU, same model as workloads.c3)."""
     import torch
     import paper_1402_0532_b200 as sa
-    cdt = complex_dtype(args.dtype)
+    dtype = dtype or args.dtype
+    cdt = complex_dtype(dtype)
     g = torch.Generator(device="cuda").manual_seed(14020534 + rank)
     re = torch.randn(batch, n, device="cuda", dtype=torch.float64, generator=g)
     im = torch.randn(batch, n, device="cuda", dtype=torch.float64, generator=g)
@@ -353,16 +458,34 @@ def wl_nlfft(args, ws, rank, variant="dit", batch=4096, n=1 << 16):
         xd += on * a * torch.exp(1j * (2 * math.pi * f * t[None] / n + ph))
     xd = xd.to(cdt)
     xd = xd.contiguous()
+    torch.cuda.empty_cache()
     yd = torch.empty_like(xd)
     ops = batch * n * (int(math.log2(n)) + 1) if variant == "dit" else batch * sa.nfft_dif_complex_ops(n)
     step = lambda: sa.nfft_batch(xd, out=yd, variant=variant)  # noqa: E731
     bytes_step = 2 * xd.numel() * xd.element_size()
-    res = {"ops": ops, "step": step, "launches_per_step": 2, "bytes": bytes_step,
+    res = {"ops": ops, "step": step, "launches_per_step": 1, "bytes": bytes_step,
            "config": {"workload": f"C3 NL-FFT {variant.upper()} (BASELINE.json configs[2])", "n": n,
-                      "batch": batch, "dtype": str(cdt).replace("torch.", "")}}
+                      "batch": batch, "dtype": str(cdt).replace("torch.", ""),
+                      "inputs": "CN(0,1) + 1-4 off-grid tones, A~U[0.1,1] (SURVEY §8d model), torch RNG on the GPU",
+                      "l2_policy": f"inputs ({bytes_step >> 20} MiB in + out) larger than L2; no flush"},
+           "dtype": "f32" if dtype == "c64" else "f64"}
     kname = ("k_nlfft64k_dit" if variant == "dit" else "k_nlfft64k_dif") + (
-        "<float" if args.dtype == "c64" else "<double")
+        "<float" if dtype == "c64" else "<double")
     res["roofline"] = lambda ms: roof_hbm(bytes_step, ms, kname)
+    sample = xd[: 64].cpu().numpy()  # host copy of the first rows for the CPU baselines
+    res["cpu"] = lambda P: cpu_nlfft(sample, variant, P)
+    if variant == "dit":
+        res["cpu_numpy"] = lambda P: numpy_ref_rows("nfft", sample, P, per_task=1, tasks_per_worker=4)
+    else:
+        res["cpu_numpy"] = lambda P: {"unavailable": "the reference has no DIF NL-FFT (SPEC.md:14)"}
+    if variant == "dit" and dtype == "c64" and not args.no_e2e:
+        hin = torch.empty(xd.shape, dtype=xd.dtype, pin_memory=True)
+        hin.copy_(xd)
+        hout = torch.empty_like(hin).pin_memory()
+        res["e2e_step"] = lambda: sa.nfft_batch(hin, out=hout, variant=variant)
+        res["h2d"] = res["d2h"] = hin.numel() * hin.element_size()
+        res["e2e_api"] = "paper_1402_0532_b200.nfft_batch(pinned host tensor, out=pinned host tensor)"
+        res["e2e_launches"] = len(_pipeline_plan(batch, n * xd.element_size()))
     return res
 
 
@@ -393,7 +516,7 @@ def wl_detect(args, k=8):
         _native.check(_native.lib().sa_map_peaks(d, _native.ptr(m), rows, cols, k, _native.ptr(idx), _native.ptr(mag),
                                                  _native.ptr(cnt), _native.ptr(ws), need.value, _native.stream_ptr()))
     mb = v.numel() * v.element_size()
-    return {"step": step, "ops": rows * cols, "map_bytes": mb,
+    return {"step": step, "ops": rows * cols, "map_bytes": mb, "launches_per_step": 2,
             "config": {"workload": "§8(f)-1 detection: top-k strict local maxima of |map|", "rows": rows,
                        "cols": cols, "k": k, "dtype": "complex64" if args.dtype == "c64" else "complex128",
                        "l2_policy": "4 maps cycled (> L2)"}}
@@ -413,8 +536,11 @@ def roof_lag(dtype, ns, lags, lms):
         peaks, src = measured_peaks()
         peak = peaks.get("bf16_tflops", 1590.0)
         ach = 32 * ns * lags / (lms * 1e-3) / 1e12
+        tr = ncu_traffic(lag_kernel(dtype))
         return {"bound": "tensor", "achieved": round(ach, 1), "peak": peak, "unit": "TFLOP/s",
-                "frac": round(ach / peak, 4), "traffic": None, "kernel": lag_kernel(dtype), "kernel_ms": lms,
+                "frac": round(ach / peak, 4), "traffic": tr["bytes_per_launch"] if tr else None,
+                "traffic_unit": "bytes/launch", "traffic_source": tr["source"] if tr else None,
+                "kernel": lag_kernel(dtype), "kernel_ms": lms,
                 "peak_source": f"{src} bf16_tflops (burst)", "nominal_peak": 2250.0,
                 "frac_nominal": round(ach / 2250.0, 4),
                 "algorithmic": "32 bf16 tensor flop per lag ⊙ (8 sign-split terms x 2 pieces); the Hankel "
@@ -426,7 +552,7 @@ def roof_lag(dtype, ns, lags, lms):
             "peak_source": "measured live sa_fma_peak"}
 
 
-def wl_map(args, ws, rank, c5=False):
+def wl_map(args, ws, rank, c5=False, e2e=False):
     """C4 (1 GPU) / C5 (sharded) ⊙ range-Doppler map."""
     import torch
     import paper_1402_0532_b200 as sa
@@ -445,10 +571,12 @@ def wl_map(args, ws, rank, c5=False):
     pm, zx, transport = None, None, "p2p"
     if ws > 1:  # rank 0's map, IPC-shared once: every rank's kernels store their rows into it
         from paper_1402_0532_b200.sharded import PeerMap, PeerMapUnavailable, ZExchange, blocks_shardable
-        try:
-            pm = PeerMap(L, M, cdt)
-        except PeerMapUnavailable:  # (all ranks agree) NCCL gather instead
-            transport = "gather"
+        transport = args.map_transport
+        if transport == "p2p":
+            try:
+                pm = PeerMap(L, M, cdt)
+            except PeerMapUnavailable:  # (all ranks agree) NCCL gather instead
+                transport = "gather"
         if pm is not None and blocks_shardable(surv, M, "fast", "mf", "nfft", L, ws):
             try:  # the z-row blocks of every rank, IPC-shared once (block-sharded lag stage)
                 zx = ZExchange(L, M, cdt)
@@ -477,17 +605,95 @@ def wl_map(args, ws, rank, c5=False):
            "config": {"workload": ("C5" if c5 else "C4") + " ⊙ range-Doppler map (BASELINE.json configs["
                       + ("4" if c5 else "3") + "])", "ns": ns, "delay_bins": L, "doppler_bins": M,
                       "block_T": ns // M, "doppler": "NL-FFT DIT", "dtype": str(cdt).replace("torch.", ""),
+                      "targets": len(sc.delays),
                       "parallelism": (f"Doppler-block shards x{ws} for the lag stage, z rows stored by the lag "
                                       "kernel into their owners' blocks over NVLink (fused all-to-all), delay-bin "
                                       "shards for the Doppler NL-FFT, rows stored into rank 0's IPC-shared map, "
                                       "two completion all-reduces") if zx is not None else (
                           f"delay-bin shards x{ws}" + (
                               (", rows stored by the transform kernels into rank 0's IPC-shared map over NVLink, "
-                               "one barrier" if transport == "p2p" else ", NCCL gather to rank 0") if ws > 1 else ""))}}
+                               "one completion all-reduce" if transport == "p2p" else ", NCCL gather to rank 0")
+                              if ws > 1 else ""))},
+           "dtype": "bf16x2-split x sign, f32 accumulate (lag); f32 (NL-FFT)" if args.dtype == "c64" else "f64"}
+    if e2e and not args.no_e2e:
+        hs = torch.from_numpy(sc.surv).to(cdt).pin_memory()
+        hr = torch.from_numpy(sc.ref).to(cdt).pin_memory()
+        hout = torch.empty((L, M), dtype=cdt).pin_memory()
+        res["e2e_step"] = lambda: sa.ambiguity_map(hs, hr, L, M, out=hout)
+        res["h2d"] = 2 * hs.numel() * hs.element_size()
+        res["d2h"] = hout.numel() * hout.element_size()
+        res["e2e_api"] = ("paper_1402_0532_b200.ambiguity_map(pinned host surv, pinned host ref, L, M, "
+                          "out=pinned host map)")
+        res["e2e_launches"] = 2
+    sv = sc.surv.astype(np.complex64 if args.dtype == "c64" else np.complex128)
+    rv = sc.ref.astype(sv.dtype)
+    res["cpu"] = lambda P: cpu_map(sv, rv, L, M, P)
+    res["cpu_numpy"] = lambda P: numpy_ref_map(sc.surv, sc.ref, L, M, P)
     return res
 
 
+def summarise(name, e):
+    """One compact record per workload for the line's trailing ``summary`` key."""
+    if "error" in e:
+        return {"error": e["error"][:120]}
+    r = {"ms": round(e["ms_per_step"], 4)}
+    for k in ("ops_per_s", "cells_per_s"):
+        if k in e:
+            r[k] = float(f"{e[k]:.4g}")
+    rf = e.get("roofline")
+    if rf:
+        r["roofline"] = f"{rf['frac']:.3f} of {rf['bound']} ({rf['kernel']})"
+    cb = e.get("cpu_baseline")
+    if cb and "value" in cb:
+        r["cpu_port"] = float(f"{cb['value']:.4g}")
+        rn = cb.get("reference_numpy") or {}
+        if "value" in rn:
+            r["cpu_numpy"] = float(f"{rn.get('cells_per_s', rn['value']):.4g}")
+            r["cpu_numpy_1core"] = float(f"{rn.get('one_core_cells_per_s', rn['one_core_value']):.4g}")
+    if "e2e" in e:
+        r["e2e_ms"] = round(e["e2e"]["ms_per_step"], 3)
+    return r
+
+
 # --------------------------------------------------------------------------- main
+def run_extra(name, make, args, ws, rank):
+    """One N=1 workload line: device-resident timing, roofline, CPU baselines
+    (oracle port + unmodified numpy reference), e2e through the public API."""
+    import torch
+    r = make()
+    steps = max(3, args.steps // 2)
+    ems, _ = timed(r["step"], steps, 3, 1)
+    e = {"ms_per_step": ems, "config": r["config"], "dtype": r.get("dtype")}
+    if "map_bytes" in r:  # detection: one read of the map
+        e["cells_per_s"] = r["ops"] / (ems * 1e-3)
+        e["roofline"] = roof_hbm(r["map_bytes"], ems, "k_peaks_tile")
+    elif "cells" in r:
+        e["cells_per_s"] = r["cells"] / (ems * 1e-3)
+        e["ops_per_s"] = r["ops"] / (ems * 1e-3)
+        lms, _ = timed(r["lag_only"], steps, 3, 1)
+        e["roofline"] = roof_lag(args.dtype, r["config"]["ns"], r["config"]["delay_bins"], lms)
+        e["roofline"]["share_of_step"] = round(lms / ems, 4)
+        e["roofline"]["hbm_gbs_of_step"] = round((2 * r["config"]["ns"] * 8 + r["cells"] * 8) / (ems * 1e-3) / 1e9, 1)
+    else:
+        e["ops_per_s"] = r["ops"] / (ems * 1e-3)
+        e["roofline"] = r["roofline"](ems)
+    if "e2e_step" in r:
+        xms, _ = timed(r["e2e_step"], max(2, steps // 2), 1, 1)
+        unit = "cells/s" if "cells" in r else "⊙/s"
+        e["e2e"] = {"value": (r["cells"] if "cells" in r else r["ops"]) / (xms * 1e-3), "unit": unit,
+                    "ms_per_step": xms, "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"],
+                    "api": r["e2e_api"]}
+    if not args.no_cpu and "cpu" in r:
+        P = len(os.sched_getaffinity(0))
+        cb = r["cpu"](P)
+        if "cpu_numpy" in r and not args.no_numpy_ref:
+            cb["reference_numpy"] = r["cpu_numpy"](P)
+        e["cpu_baseline"] = cb
+    del r
+    torch.cuda.empty_cache()
+    return e
+
+
 def run_ours(args):
     import torch
     ws, rank, local = dist_init()
@@ -499,7 +705,7 @@ def run_ours(args):
     elif w == "nlfft":
         res = wl_nlfft(args, ws, rank)
     elif w in ("map", "map5"):
-        res = wl_map(args, ws, rank, c5=(w == "map5"))
+        res = wl_map(args, ws, rank, c5=(w == "map5"), e2e=(ws == 1))
     else:
         raise SystemExit(f"unknown workload {w}")
     sampler = ClockSampler(local) if rank == 0 else None
@@ -513,7 +719,8 @@ def run_ours(args):
     line = {"metric": METRIC, "value": value, "unit": unit, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak" if w in ("ndft", "nlfft") else "strong", "vs_baseline": None,
-            "dtype": res.get("dtype", "f32" if args.dtype == "c64" else "f64"), "data": "synthetic (seeded, SURVEY §8d model)",
+            "dtype": res.get("dtype", "f32" if args.dtype == "c64" else "f64"),
+            "data": "synthetic (seeded, SURVEY §8d model)",
             "config": res["config"], "clocks": clocks,
             "gpu_launches": res["launches_per_step"] * args.steps}
     if w in ("map", "map5"):
@@ -521,69 +728,76 @@ def run_ours(args):
     if rank == 0 and "roofline" in res:
         line["roofline"] = res["roofline"](ms)
     if w in ("map", "map5") and rank == 0:
-        lms, _ = timed(res["lag_only"], args.steps, 1, 1)
+        lms, _ = timed(res["lag_only"], args.steps, 3, 1)
         line["roofline"] = roof_lag(args.dtype, res["config"]["ns"], res["config"]["delay_bins"] // ws, lms)
         line["roofline"]["share_of_step"] = round(lms / ms, 4) if ws == 1 else None
     # e2e through the public API with host buffers
     if "e2e_step" in res:
         ems, _ = timed(res["e2e_step"], max(2, args.steps // 2), 1, ws)
-        line["e2e"] = {"value": res["ops"] * ws / (ems * 1e-3), "unit": unit, "ms_per_step": ems,
-                       "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"],
-                       "api": res.get("e2e_api"),
-                       "pipeline": "H2D / transform / D2H overlapped over row chunks (32 MiB steady, "
-                                   "16 MiB first and last)"}
-        from paper_1402_0532_b200.transforms import pipeline_plan
-        line["gpu_launches"] += max(2, args.steps // 2) * len(pipeline_plan(res["e2e_rows"], res["e2e_row_bytes"], 128))
+        line["e2e"] = {"value": (res["cells"] if "cells" in res else res["ops"] * ws) / (ems * 1e-3), "unit": unit,
+                       "ms_per_step": ems, "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"],
+                       "api": res.get("e2e_api")}
+        if w == "ndft":
+            line["e2e"]["pipeline"] = ("H2D / transform / D2H overlapped over row chunks (32 MiB steady, "
+                                       "16 MiB first and last)")
+        line["gpu_launches"] += max(2, args.steps // 2) * res.get("e2e_launches", 1)
     # CPU baseline: rank 0, N=1 only
     if rank == 0 and ws == 1 and "cpu" in res and not args.no_cpu:
         P = len(os.sched_getaffinity(0))
         line["cpu_baseline"] = res["cpu"](P)
+        if "cpu_numpy" in res and not args.no_numpy_ref:
+            line["cpu_baseline"]["reference_numpy"] = res["cpu_numpy"](P)
+    del res
+    torch.cuda.empty_cache()
     # extras (N=1)
+    extras = {}
     if rank == 0 and ws == 1 and not args.no_extras and w == "ndft":
-        extras = {}
-        other = "fast" if (args.ndft_mode == "tc" and args.dtype == "c64") else None
-        for name, fn in ((("C2_ndft_ffma2", lambda: wl_ndft(args, ws, rank, mode="fast", e2e=False)),) if other else ()) + (
-                         ("C3_nlfft_dit", lambda: wl_nlfft(args, ws, rank, "dit")),
-                         ("C3_nlfft_dif", lambda: wl_nlfft(args, ws, rank, "dif")),
-                         ("C4_map", lambda: wl_map(args, ws, rank)),
-                         ("C5_detect", lambda: wl_detect(args))):
+        specs = [("C1_ndft_c128", lambda: wl_ndft64(args))]
+        if args.ndft_mode == "tc" and args.dtype == "c64":
+            specs.append(("C2_ndft_ffma2", lambda: {**wl_ndft(args, ws, rank, mode="fast", e2e=False), "cpu_skip": 1}))
+        specs += [("C2_ndft_c128", lambda: wl_ndft(args, ws, rank, mode="fast", dtype="c128")),
+                  ("C3_nlfft_dit", lambda: wl_nlfft(args, ws, rank, "dit", dtype="c64")),
+                  ("C3_nlfft_dif", lambda: wl_nlfft(args, ws, rank, "dif", dtype="c64")),
+                  ("C3_nlfft_dit_c128", lambda: wl_nlfft(args, ws, rank, "dit", dtype="c128")),
+                  ("C3_nlfft_dif_c128", lambda: wl_nlfft(args, ws, rank, "dif", dtype="c128")),
+                  ("C4_map", lambda: wl_map(args, ws, rank, e2e=True)),
+                  ("C5_map_1gpu", lambda: wl_map(args, ws, rank, c5=True, e2e=True)),
+                  ("C5_detect", lambda: wl_detect(args))]
+        for name, fn in specs:
+            if args.only and name not in args.only.split(","):
+                continue
             try:
-                r = fn()
-                ems, _ = timed(r["step"], max(3, args.steps // 2), 2, 1)
-                e = {"ms_per_step": ems, "config": r["config"], "ops_per_s": r["ops"] / (ems * 1e-3)}
-                if "map_bytes" in r:  # detection: one read of the map
-                    e = {"ms_per_step": ems, "config": r["config"], "cells_per_s": r["ops"] / (ems * 1e-3),
-                         "roofline": roof_hbm(r["map_bytes"], ems, "k_peaks_tile")}
-                elif "cells" in r:
-                    e["cells_per_s"] = r["cells"] / (ems * 1e-3)
-                    lms, _ = timed(r["lag_only"], 5, 1, 1)
-                    e["roofline"] = roof_lag(args.dtype, r["config"]["ns"], r["config"]["delay_bins"], lms)
-                    e["roofline"]["hbm_gbs_of_step"] = round(
-                        (2 * r["config"]["ns"] * 8 + r["cells"] * 8) / (ems * 1e-3) / 1e9, 1)
-                else:
-                    e["roofline"] = r["roofline"](ems)
-                extras[name] = e
-                del r
-                torch.cuda.empty_cache()
+                def make(fn=fn):
+                    r = fn()
+                    if r.pop("cpu_skip", None):  # same sample as the headline's baseline
+                        r.pop("cpu", None)
+                        r.pop("cpu_numpy", None)
+                    return r
+                extras[name] = run_extra(name, make, args, ws, rank)
+                log(f"[bench] {name}: {extras[name]['ms_per_step']:.4f} ms")
             except Exception as ex:  # keep the headline line even if an extra fails
                 extras[name] = {"error": repr(ex)}
-        line["workloads"] = extras
+                torch.cuda.empty_cache()
     # C5 map at every N (the north star asks map throughput at 1/2/4/8 GPUs):
-    # all ranks take part -- delay-bin shards, rows stored into rank 0's map
-    # over peer memory -- timed as the max over ranks (strong scaling)
+    # all ranks take part -- Doppler-block shards for the lag stage, rows stored
+    # into rank 0's map over peer memory -- timed as the max over ranks (strong scaling)
     if not args.no_extras and w == "ndft":
         try:
             r = wl_map(args, ws, rank, c5=True)
-            ems, _ = timed(r["step"], max(3, args.steps // 2), 2, ws)
+            ems, _ = timed(r["step"], max(3, args.steps // 2), 3, ws)
             e = {"ms_per_step": ems, "config": r["config"], "cells_per_s": r["cells"] / (ems * 1e-3),
                  "n_gpus": ws, "scaling": "strong"}
             del r
             torch.cuda.empty_cache()
         except Exception as ex:
             e = {"error": repr(ex)}
-        if rank == 0:
-            line.setdefault("workloads", {})["C5_map"] = e
+        extras["C5_map"] = e
     if rank == 0:
+        if extras:
+            line["workloads"] = extras
+        # compact per-workload record LAST, so a truncated stdout tail still shows it
+        line["summary"] = {"headline": summarise("headline", {**line, "ops_per_s": line["value"]}),
+                           **{k: summarise(k, v) for k, v in extras.items()}}
         print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist
@@ -602,16 +816,15 @@ def run_reference(args):
     if w == "ndft":
         from paper_1402_0532_b200.workloads import c2_ndft
         n, rows = 1024, max(64, 4 * P)
-        g = np.random.default_rng(14020532 + 1)
-        x = (g.standard_normal((rows, n)) + 1j * g.standard_normal((rows, n))) / np.sqrt(2)
-        x = x.astype(np.complex64 if args.dtype == "c64" else np.complex128)
+        x = c2_ndft(n, 65536, rows=slice(0, rows)).astype(np.complex64 if args.dtype == "c64" else np.complex128)
         dts = "f32" if args.dtype == "c64" else "f64"
         fn = lambda: oracle.ndft(x, dtype=dts, nthreads=P)  # noqa: E731
         ops = rows * n * n
         unit = "⊙/s"
         cfg = {"workload": "C2 batched NDFT (BASELINE.json configs[1])", "n": n, "batch": 65536,
-               "sample_rows_per_step": rows}
-        sample = f"{rows} CN(0,1) vectors of N={n} per step (bounded sample of C2)"
+               "dtype": "complex64" if args.dtype == "c64" else "complex128", "sample_rows_per_step": rows,
+               "same_config": "rate vs rate: each step is the first rows of the same seeded C2 batch"}
+        sample = f"first {rows} vectors of the C2 batch (N={n}) per step, oracle C port (sequential, op for op)"
     elif w == "nlfft":
         n, rows = 1 << 16, max(8, P)
         g = np.random.default_rng(1)
@@ -666,6 +879,12 @@ def main():
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-numpy-ref", action="store_true",
+                    help="skip the unmodified-numpy-reference Pool(P) figures (tools/refcpu.py)")
+    ap.add_argument("--only", default="", help="comma-separated extra workloads to run (default: all)")
+    ap.add_argument("--map-transport", default="p2p", choices=["p2p", "gather"],
+                    help="N>1 map delivery: p2p = rows stored into rank 0's map over peer memory; "
+                         "gather = delay-bin shards + NCCL gather (the north star's stated split)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: contract requires >= 3 warm-up steps")

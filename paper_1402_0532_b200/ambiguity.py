@@ -102,6 +102,9 @@ def _samples(sig):
         return sig.samples
     if is_device_tensor(sig):
         return sig
+    T = torch()
+    if isinstance(sig, T.Tensor) and sig.is_complex():  # host tensor: kept (pinned -> async upload)
+        return sig
     return np.asarray(sig, dtype=complex)
 
 
