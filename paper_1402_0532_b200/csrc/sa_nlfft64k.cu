@@ -39,6 +39,9 @@ constexpr int NN = 1 << LOGN;
 #ifndef SA_GREL
 #define SA_GREL 1
 #endif
+#ifndef SA_WAIT1
+#define SA_WAIT1 0  // 1: one warp per group polls, the rest block in bar.sync (measured slower: 1.790 vs 1.757 ms C3 DIT)
+#endif
 #ifndef SA_LOCALQ
 #define SA_LOCALQ 1  // the CTA's own share of the scatter: st.shared + warp arrivals
 #endif
@@ -145,10 +148,20 @@ template <typename T> struct Pipe {
   }
   SA_HD C2 *work() const { return reinterpret_cast<C2 *>(smem + P::OFF_WORK + gi * P::WORK); }
   // cluster-window address of peer r's node storage b (byte offset off) / its full mbarrier
-  SA_HD uint32_t peer_inter(int b, int r, uint32_t off) const {
-    return sa_mapa(sa_smem_u32(smem + b * P::INTER1) + off, r);
+  // (mapa is linear inside a CTA's window: the peer bases are mapped once, in init)
+  uint32_t pinter[P::CL], pfull[P::CL];
+  SA_HD uint32_t peer_inter(int b, int r, uint32_t off) const { return pinter[r] + (uint32_t)(b * P::INTER1) + off; }
+  SA_HD uint32_t peer_full(int b, int r) const { return pfull[r] + 8u * (uint32_t)b; }
+  // wait for an mbarrier phase: one warp of the thread group polls, the rest block
+  // in the group's named barrier (no issue slots spent spinning)
+  SA_HD void group_wait(uint64_t *bar, uint32_t parity) const {
+#if SA_WAIT1
+    if ((gt >> 5) == 0) sa_mbar_wait(bar, parity);
+    group_sync(1 + gi, P::GT);
+#else
+    sa_mbar_wait(bar, parity);
+#endif
   }
-  SA_HD uint32_t peer_full(int b, int r) const { return sa_mapa(sa_smem_u32(&full_bar[b]), r); }
 
   SA_HD void init(unsigned char *smem_raw, const C4 *stage) {
     cg::cluster_group cluster = cg::this_cluster();
@@ -162,6 +175,11 @@ template <typename T> struct Pipe {
     ncl = gridDim.x / P::CL;
     gi = threadIdx.x / P::GT;
     gt = threadIdx.x % P::GT;
+#pragma unroll
+    for (int r = 0; r < P::CL; ++r) {
+      pinter[r] = sa_mapa(sa_smem_u32(smem), r);
+      pfull[r] = sa_mapa(sa_smem_u32(smem + P::OFF_BAR + 8 * P::NG), r);
+    }
     for (int e = threadIdx.x; e < 255; e += P::THREADS) twA[e] = stage[e];  // global stages 1..8
     if (threadIdx.x == 0) {
       for (int g = 0; g < P::NG; ++g) sa_mbar_init(&tma_bar[g], 1);
@@ -184,7 +202,7 @@ template <typename T> struct Pipe {
     }
   }
   SA_HD void wait_tile() {
-    sa_mbar_wait(&tma_bar[gi], tile_it & 1);
+    group_wait(&tma_bar[gi], tile_it & 1);
     ++tile_it;
   }
   // "storage b may be overwritten": the CTA (SA_GREL: this thread group)
@@ -300,7 +318,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
           if (!(k & hr)) r_dit<T>(v[k], v[k + hr], twA[(h - 1) + m2_g + 16 * (k & (hr - 1))]);
       }
       // scatter node row R = rev8(c): column q lives in CTA q / COLS
-      if (u == 0) sa_mbar_wait(&pp.empty_bar[b], use & 1);  // peers released storage b
+      if (u == 0) pp.group_wait(&pp.empty_bar[b], use & 1);  // peers released storage b
       const int R = rev8(pp.rank * COLS + tt * TC + m2_cc);
       constexpr int KPC = COLS / 16;  // registers per owner CTA
 #pragma unroll
@@ -321,7 +339,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
       const int q0 = pp.rank * COLS + pp.gi * TC + m1_cc;  // independent of the node storage
       load_wf<T>(wf, stage2, q0, m1_g);
     }
-    sa_mbar_wait(&pp.full_bar[b], use & 1);  // all INTER1 bytes of this signal landed
+    pp.group_wait(&pp.full_bar[b], use & 1);  // all INTER1 bytes of this signal landed
     for (int u = 0; u < TPG; ++u) {
       const int tt = pp.gi + NG * u;
       const int lq = tt * TC + m1_cc;
@@ -462,7 +480,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
             if (!(k & h)) r_dif_fast<T>(v[k], v[k + h], wf[h - 1 + (k & (h - 1))]);
         }
       }
-      if (u == 0) sa_mbar_wait(&pp.empty_bar[b], use & 1);
+      if (u == 0) pp.group_wait(&pp.empty_bar[b], use & 1);
 #pragma unroll
       for (int k = 0; k < 16; ++k) {  // row R = 16g + k -> CTA owning cr = rev8(R), local row cr mod COLS
         const int cr = crev4(k) * 16 + rg1;
@@ -478,7 +496,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
   auto phaseB = [&](int64_t sig, int b, uint32_t use) {
     C2 *inter = pp.inter(b);
     C2 *ysig = y + sig * NN;
-    sa_mbar_wait(&pp.full_bar[b], use & 1);
+    pp.group_wait(&pp.full_bar[b], use & 1);
     for (int u = 0; u < TPG; ++u) {
       const int tt = pp.gi + NG * u;
       V v[16];
