@@ -566,7 +566,7 @@ def wl_map(args, ws, rank, c5=False, e2e=False):
     rows = L // ws
     l0 = rank * rows
     out = torch.empty((rows, M), dtype=cdt, device="cuda")
-    ws_buf = torch.empty(rows * M * out.element_size(), dtype=torch.uint8, device="cuda")
+    ws_buf = torch.empty((rows + 30) * M * out.element_size(), dtype=torch.uint8, device="cuda")  # blocked z pads to whole tiles
 
     pm, zx, transport = None, None, "p2p"
     if ws > 1:  # rank 0's map, IPC-shared once: every rank's kernels store their rows into it

@@ -158,14 +158,24 @@ int sa_ambiguity_integrate_v(int dtype, int lag_kind, const void *surv, const vo
 
 /* Block-sharded lag stage for multi-GPU maps (ambiguity.py:27-28: delay rows and
  * integration blocks are independent): fast-mode ⊙ lag integration of blocks
- * [q0, q0 + q_count) for lags [l0, l0 + l_count), each lag row stored into the
- * z rows of its owner -- dst_rows is a DEVICE array of n_dst row-block bases
- * (peer / IPC pointers), owner o holding lags per sharded.shard_rows(l_count,
- * n_dst, o), row stride m.  Tensor-core path only (complex64, T % 128 == 0);
+ * [q0, q0 + q_count) for lags [0, l_count), each lag row stored into the z
+ * rows of its owner -- dst_rows is a DEVICE array of n_dst row-block bases
+ * (peer / IPC pointers); owner o holds lags [o*l_count/n_dst, (o+1)*l_count/n_dst)
+ * in the BLOCKED layout: tiles of 16 lags, element q of a tile's rows one 128-B
+ * line, zb[(k * m + q) * 16 + j] = z[16 k + j][q] (k counted from the owner's
+ * first row), so every peer store is a whole 32-B sector.  Needs l0 == 0 and
+ * l_count % (16 * n_dst) == 0; tensor-core path only (complex64, T % 128 == 0);
  * anything else returns SA_ERR_UNSUPPORTED and the caller shards delay rows. */
 int sa_ambiguity_integrate_blocks(int dtype, const void *surv, const void *ref, int64_t ns, int64_t ref_len,
                                   int64_t l0, int64_t l_count, int64_t m, int64_t q0, int64_t q_count, int conj,
                                   void *const *dst_rows, int64_t n_dst, void *stream);
+
+/* The map's Doppler stage on a blocked z (sa_ambiguity_integrate_blocks'
+ * layout): out (l_count x m, row-major) = nfft(gain * z row) per row, DIT,
+ * value-identical to nfft (transforms.py:254-298); m = 64 .. 2048, a power of
+ * two (SA_ERR_UNSUPPORTED otherwise). */
+int sa_doppler_nlfft_blocked(int dtype, const void *zb, void *out, int64_t l_count, int64_t m, const void *tw,
+                             double gain, void *stream);
 
 /* Workspace bytes for sa_map_peaks. */
 int sa_peaks_workspace_bytes(int64_t rows, int64_t cols, int k, int64_t *bytes);

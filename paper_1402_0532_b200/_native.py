@@ -47,6 +47,7 @@ SIGNATURES = {
                                 _P, _P, _I64, _P]),
     "sa_ambiguity_integrate_v": (_I, [_I, _I, _P, _P, _I64, _I64, _I64, _I64, _I64, _I, _I, _P, _P]),
     "sa_ambiguity_integrate_blocks": (_I, [_I, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I, _P, _I64, _P]),
+    "sa_doppler_nlfft_blocked": (_I, [_I, _P, _P, _I64, _I64, _P, ctypes.c_double, _P]),
     "sa_peaks_workspace_bytes": (_I, [_I64, _I64, _I, ctypes.POINTER(_I64)]),
     "sa_map_peaks": (_I, [_I, _P, _I64, _I64, _I, _P, _P, _P, _P, _I64, _P]),
     "sa_map_floor": (_I, [_I, _P, _I64, _I64, _P, _I, _I, _I, _P, _P]),

@@ -217,6 +217,18 @@ int sa_ambiguity_map_v(int dtype, int lag_kind, const void *surv, const void *re
   rc = check_tw(tw, dtype, m, doppler != SA_DOPPLER_NDFT);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
+  if (doppler == SA_DOPPLER_NLFFT && sa_doppler_supported(m)) {
+    // lag stage -> Doppler NL-FFT (sa_doppler.cu, register radix-16 rounds); on the
+    // tensor-core lag path z travels in the blocked layout (whole-sector stores)
+    const bool blk = mode == SA_NDFT_FAST && lag_kind == SA_LAG_MF && ns != m &&
+                     sa_lag_tc_supported(dtype, ns / m, m, surv);
+    rc = blk ? sa_launch_lag_tc(surv, ref, ref_len, l0, l_count, m, ns / m, conj, workspace, 1, s)
+             : sa_launch_lag_integrate(dtype, lag_kind, surv, ref, ns, ref_len, l0, l_count, m, conj, mode,
+                                       workspace, s);
+    if (rc) return rc;
+    return sa_launch_doppler_nlfft(dtype, workspace, out, blk ? (int)(l0 & 15) : 0, l_count, m, blk ? 1 : 0,
+                                   (const SaTwiddles *)tw, gain, s);
+  }
   rc = sa_launch_lag_integrate(dtype, lag_kind, surv, ref, ns, ref_len, l0, l_count, m, conj, mode,
                                workspace, s);
   if (rc) return rc;
@@ -265,6 +277,9 @@ int sa_ambiguity_integrate_blocks(int dtype, const void *surv, const void *ref, 
              "map: ns=%lld must be a positive multiple of m=%lld", (long long)ns, (long long)m);
   SA_REQUIRE(q0 >= 0 && q_count >= 0 && q0 + q_count <= m, SA_ERR_ARG, "bad block range");
   SA_REQUIRE(n_dst >= 1 && n_dst <= l_count && dst_rows, SA_ERR_ARG, "bad destination rows");
+  // owners' rows are whole 16-lag tiles of the blocked z layout
+  SA_REQUIRE(l0 == 0 && l_count % (16 * n_dst) == 0, SA_ERR_UNSUPPORTED,
+             "block-sharded lag stage needs l0 = 0 and l_count a multiple of 16 x n_dst");
   int rc = lag_guards(ns, ns, ref_len, l0 + l_count - 1);
   if (rc) return rc;
   rc = lag_guards(ns, ns, ref_len, l0);
@@ -272,7 +287,19 @@ int sa_ambiguity_integrate_blocks(int dtype, const void *surv, const void *ref, 
   SA_REQUIRE(surv && ref, SA_ERR_ARG, "null pointer");
   if (!sa_lag_tc_supported(dtype, ns / m, m, surv)) return SA_ERR_UNSUPPORTED;
   return sa_launch_lag_tc_blocks(surv, ref, ref_len, l0, l_count, m, q0, q_count, ns / m, conj, nullptr, dst_rows,
-                                 l_count / n_dst, l_count % n_dst, (cudaStream_t)stream);
+                                 l_count / n_dst, l_count % n_dst, 1, (cudaStream_t)stream);
+}
+
+int sa_doppler_nlfft_blocked(int dtype, const void *zb, void *out, int64_t l_count, int64_t m, const void *tw,
+                             double gain, void *stream) {
+  SA_REQUIRE(dtype_ok(dtype), SA_ERR_ARG, "bad dtype %d", dtype);
+  SA_REQUIRE(l_count >= 0 && sa_doppler_supported(m), SA_ERR_UNSUPPORTED,
+             "blocked Doppler NL-FFT needs m = 64 .. 2048, a power of two (got %lld)", (long long)m);
+  SA_REQUIRE(zb && out, SA_ERR_ARG, "null pointer");
+  int rc = check_tw(tw, dtype, m, true);
+  if (rc) return rc;
+  return sa_launch_doppler_nlfft(dtype, zb, out, 0, l_count, m, 1, (const SaTwiddles *)tw, gain,
+                                 (cudaStream_t)stream);
 }
 
 int sa_peaks_workspace_bytes(int64_t rows, int64_t cols, int k, int64_t *bytes) {

@@ -555,7 +555,7 @@ int launch_integrate(int lag_kind, const void *survv, const void *refv, int64_t 
 #ifndef SA_NO_LAG_TC
   // fast mode, complex64, T % 128 == 0: Hankel GEMM on the tcgen05 tensor cores (sa_lag_tc.cu)
   if (mode == SA_NDFT_FAST && !exact_lag && sa_lag_tc_supported(sizeof(T) == 4 ? SA_C64 : SA_C128, tb, m, survv))
-    return sa_launch_lag_tc(survv, refv, ref_len, l0, l_count, m, tb, conj, zv, s);
+    return sa_launch_lag_tc(survv, refv, ref_len, l0, l_count, m, tb, conj, zv, 0, s);
 #endif
 
   // fast mode, complex64, T % 16 == 0: packed pair kernel.  NT is the largest of
@@ -619,7 +619,8 @@ int launch_integrate(int lag_kind, const void *survv, const void *refv, int64_t 
 }  // namespace
 
 int64_t sa_ambiguity_ws_bytes(int dtype, int64_t l_count, int64_t m) {
-  return l_count * m * (dtype == SA_C64 ? (int64_t)sizeof(float2) : (int64_t)sizeof(double2));
+  // + 30 rows: the blocked z layout pads the call's rows to whole 16-lag tiles (sa_lag_tc.cu)
+  return (l_count + 30) * m * (dtype == SA_C64 ? (int64_t)sizeof(float2) : (int64_t)sizeof(double2));
 }
 
 template <typename T>

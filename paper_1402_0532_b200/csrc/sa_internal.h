@@ -64,11 +64,17 @@ int sa_launch_ndft_tc(const void *x, void *y, int64_t batch, int64_t n, const Sa
 // sa_lag_tc.cu (tensor-core fast-mode lag integration, complex64)
 bool sa_lag_tc_supported(int dtype, int64_t tb, int64_t m, const void *surv);
 int sa_launch_lag_tc(const void *surv, const void *ref, int64_t ref_len, int64_t l0, int64_t l_count, int64_t m,
-                     int64_t tb, int conj, void *z, cudaStream_t s);
+                     int64_t tb, int conj, void *z, int blocked, cudaStream_t s);
 int sa_launch_lag_tc_blocks(const void *surv, const void *ref, int64_t ref_len, int64_t l0, int64_t l_count, int64_t m,
-                            int64_t q0,
-                            int64_t q_count, int64_t tb, int conj, void *z, void *const *dst_rows, int64_t rows_base,
-                            int64_t rows_extra, cudaStream_t s);
+                            int64_t q0, int64_t q_count, int64_t tb, int conj, void *z, void *const *dst_rows,
+                            int64_t rows_base, int64_t rows_extra, int blocked, cudaStream_t s);
+// blocked z: tiles of 16 lags from the 16-aligned base (sa_lag_tc.cu), rows padded to whole tiles
+inline int64_t sa_zblk_rows(int64_t l0, int64_t l_count) { return (((l0 & 15) + l_count + 15) / 16) * 16; }
+
+// sa_doppler.cu (the map's Doppler NL-FFT straight from (blocked) z, M = 64 .. 2048)
+bool sa_doppler_supported(int64_t m);
+int sa_launch_doppler_nlfft(int dtype, const void *z, void *out, int row_off, int64_t l_count, int64_t m,
+                            int blocked, const SaTwiddles *tw, double gain, cudaStream_t s);
 
 // sa_nlfft.cu
 int sa_launch_nlfft(int dtype, int variant, const void *x, void *y, int64_t batch, int64_t n,

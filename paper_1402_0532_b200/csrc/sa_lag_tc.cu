@@ -100,6 +100,10 @@ SA_HD void load_c(float2 (&cv)[8], const float2 *__restrict__ ref, int64_t g0, i
 // multi-GPU maps (sharded.py) -- the z rows of the rank that owns the lag
 // (shard_rows partition: the first `extra` owners hold base + 1 rows), written
 // over NVLink/NVSwitch peer memory.
+// Blocked layout (sa_doppler.cu): tiles of 16 consecutive lags counted from the
+// call's 16-aligned base lalign; element q of a tile's 16 rows is one 128-B line
+//   zb[(k * m + q) * 16 + j] = z[lalign + 16 k + j][q]
+// Peer owners then hold `base` rows each (16-aligned shards, l0 = 0, extra = 0).
 struct LagDst {
   float2 *const *ptr;  // device array of per-owner row-block bases (null: local z)
   int64_t base, extra;
@@ -110,10 +114,15 @@ struct LagDst {
     const int64_t first = o * base + (o < extra ? o : extra);
     return ptr[o] + (lag - first) * m + q;
   }
+  SA_HD float2 *line(float2 *z, int64_t k, int64_t m, int64_t q) const {
+    if (!ptr) return z + (k * m + q) * 16;
+    const int64_t o = (16 * k) / base;
+    return ptr[o] + ((k - o * (base >> 4)) * m + q) * 16;
+  }
 };
 
 // G lag groups share each A read (one pass): the MMAs widen to N = 32 G / 16 G.
-template <int G>
+template <int G, bool BLK>
 __global__ void __launch_bounds__(THREADS, 2)
     k_lag_tc(const float2 *__restrict__ surv, const float2 *__restrict__ ref, int64_t ref_len, int64_t l0g, int64_t l_count,
              int64_t m, int tb, float csign, float2 *__restrict__ z, int64_t q0, LagDst dst) {
@@ -283,14 +292,49 @@ __global__ void __launch_bounds__(THREADS, 2)
           SA_LD16(d2, ta + 32 * gs + 16);
           SA_LD16(d3, ta + 32 * G + 16 * gs);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          float re[8], im[8];
 #pragma unroll
           for (int l0 = 0; l0 < 8; ++l0) {
-            const int64_t lag = lpass + (int64_t)gs * LGRP + 8 * l1 + l0 - l0g;  // row of z
-            if (lag >= 0 && lag < l_count) {
-              const float re = (__uint_as_float(d1[l0]) + __uint_as_float(d2[l0])) + __uint_as_float(d3[l0]);
-              const float im =
-                  (__uint_as_float(d1[8 + l0]) + __uint_as_float(d2[8 + l0])) + __uint_as_float(d3[8 + l0]);
-              *dst.row(z, lag, m, q) = make_float2(re, im);
+            re[l0] = (__uint_as_float(d1[l0]) + __uint_as_float(d2[l0])) + __uint_as_float(d3[l0]);
+            im[l0] = (__uint_as_float(d1[8 + l0]) + __uint_as_float(d2[8 + l0])) + __uint_as_float(d3[8 + l0]);
+          }
+          const int64_t lagb = lpass + (int64_t)gs * LGRP + 8 * l1;  // absolute lag of re[0]
+          if constexpr (!BLK) {
+#pragma unroll
+            for (int l0 = 0; l0 < 8; ++l0) {
+              const int64_t lag = lagb + l0 - l0g;  // row of z
+              if (lag >= 0 && lag < l_count) *dst.row(z, lag, m, q) = make_float2(re[l0], im[l0]);
+            }
+          } else {
+            // lanes (2i, 2i+1) hold the 16 lags of tile k: swap halves so that every
+            // store instruction writes one whole 32-B sector of the tile's 128-B line
+            const int64_t k = (lagb - lalign) >> 4;
+            const bool odd = l1 & 1;
+            float4 c[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) c[i] = make_float4(re[2 * i], im[2 * i], re[2 * i + 1], im[2 * i + 1]);
+            float4 snd[2] = {odd ? c[0] : c[1], odd ? c[2] : c[3]}, rcv[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              rcv[i].x = __shfl_xor_sync(0xffffffffu, snd[i].x, 1);
+              rcv[i].y = __shfl_xor_sync(0xffffffffu, snd[i].y, 1);
+              rcv[i].z = __shfl_xor_sync(0xffffffffu, snd[i].z, 1);
+              rcv[i].w = __shfl_xor_sync(0xffffffffu, snd[i].w, 1);
+            }
+            const int64_t t0 = lalign + 16 * k;  // tile intersects the call's rows?
+            if (t0 + 16 > l0g && t0 < l0g + l_count) {
+              float4 *ln = reinterpret_cast<float4 *>(dst.line(z, k, m, q));
+              if (!odd) {
+                ln[0] = c[0];
+                ln[2] = c[2];
+                ln[4] = rcv[0];
+                ln[6] = rcv[1];
+              } else {
+                ln[1] = rcv[0];
+                ln[3] = rcv[1];
+                ln[5] = c[1];
+                ln[7] = c[3];
+              }
             }
           }
         }
@@ -315,31 +359,40 @@ bool sa_lag_tc_supported(int dtype, int64_t tb, int64_t m, const void *surv) {
 }
 
 int sa_launch_lag_tc(const void *surv, const void *ref, int64_t ref_len, int64_t l0, int64_t l_count, int64_t m,
-                     int64_t tb, int conj, void *z, cudaStream_t s) {
-  return sa_launch_lag_tc_blocks(surv, ref, ref_len, l0, l_count, m, 0, m, tb, conj, z, nullptr, 0, 0, s);
+                     int64_t tb, int conj, void *z, int blocked, cudaStream_t s) {
+  return sa_launch_lag_tc_blocks(surv, ref, ref_len, l0, l_count, m, 0, m, tb, conj, z, nullptr, 0, 0, blocked, s);
+}
+
+template <int G, bool BLK>
+int launch_g(const void *surv, const void *ref, int64_t ref_len, int64_t l0, int64_t l_count, int64_t m, int64_t q0,
+             int64_t q_count, int64_t tb, int conj, void *z, const LagDst &d, cudaStream_t s) {
+  const size_t bytes = smem_bytes((int)tb);
+  static int smem_set[64] = {};  // largest smem size set per device
+  int dev = 0;
+  SA_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev >= 64 || smem_set[dev] < (int)bytes) {
+    SA_CUDA_TRY(cudaFuncSetAttribute(k_lag_tc<G, BLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    if (dev < 64) smem_set[dev] = (int)bytes;
+  }
+  k_lag_tc<G, BLK><<<(unsigned)q_count, THREADS, bytes, s>>>((const float2 *)surv, (const float2 *)ref, ref_len, l0,
+                                                             l_count, m, (int)tb, conj ? -1.f : 1.f, (float2 *)z, q0, d);
+  SA_LAUNCH_CHECK();
+  return SA_OK;
 }
 
 int sa_launch_lag_tc_blocks(const void *surv, const void *ref, int64_t ref_len, int64_t l0, int64_t l_count, int64_t m,
-                            int64_t q0,
-                            int64_t q_count, int64_t tb, int conj, void *z, void *const *dst_rows, int64_t rows_base,
-                            int64_t rows_extra, cudaStream_t s) {
+                            int64_t q0, int64_t q_count, int64_t tb, int conj, void *z, void *const *dst_rows,
+                            int64_t rows_base, int64_t rows_extra, int blocked, cudaStream_t s) {
   if (l_count == 0 || q_count == 0) return SA_OK;
-  const size_t bytes = smem_bytes((int)tb);
   // lag groups (of 1024, aligned to 16) per call -> groups merged per pass
   const int64_t ngrp = ((l0 & 15) + l_count + LGRP - 1) / LGRP;
   const int g = ngrp >= 3 ? 4 : (int)ngrp;
-  auto kern = g == 4 ? k_lag_tc<4> : (g == 2 ? k_lag_tc<2> : k_lag_tc<1>);
-  static int smem_set[64][3] = {};  // largest smem size set per (device, instantiation)
-  int dev = 0;
-  SA_CUDA_TRY(cudaGetDevice(&dev));
-  const int gi = g == 4 ? 2 : g - 1;
-  if (dev >= 64 || smem_set[dev][gi] < (int)bytes) {
-    SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    if (dev < 64) smem_set[dev][gi] = (int)bytes;
-  }
   const LagDst d{(float2 *const *)dst_rows, rows_base, rows_extra};
-  kern<<<(unsigned)q_count, THREADS, bytes, s>>>((const float2 *)surv, (const float2 *)ref, ref_len, l0, l_count, m, (int)tb,
-                                                 conj ? -1.f : 1.f, (float2 *)z, q0, d);
-  SA_LAUNCH_CHECK();
-  return SA_OK;
+#define SA_LAG_LAUNCH(G)                                                                                         \
+  return blocked ? launch_g<G, true>(surv, ref, ref_len, l0, l_count, m, q0, q_count, tb, conj, z, d, s)        \
+                 : launch_g<G, false>(surv, ref, ref_len, l0, l_count, m, q0, q_count, tb, conj, z, d, s)
+  if (g == 4) SA_LAG_LAUNCH(4);
+  if (g == 2) SA_LAG_LAUNCH(2);
+  SA_LAG_LAUNCH(1);
+#undef SA_LAG_LAUNCH
 }

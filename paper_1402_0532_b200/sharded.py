@@ -259,14 +259,15 @@ def _done(flag, group):
 def blocks_shardable(surv, m: int, mode: str, lag: str, doppler: str, l_bins: int | None = None,
                      world: int = 1) -> bool:
     """Whether the block-sharded map applies: the tensor-core lag path
-    (sa_lag_tc_supported: complex64 fast ⊙ lags, T % 128 == 0, T <= 4096), a
-    Doppler transform of the z rows, and at least one delay row per rank
-    (sa_ambiguity_integrate_blocks needs n_dst <= l_count).  Shapes only, so every
-    rank agrees."""
+    (sa_lag_tc_supported: complex64 fast ⊙ lags, T % 128 == 0, T <= 4096), the
+    NL-FFT Doppler transform on the blocked z layout (sa_doppler_nlfft_blocked:
+    M = 64 .. 2048), and whole 16-lag tiles per rank (sa_ambiguity_integrate_blocks:
+    L % (16 G) == 0).  Shapes only, so every rank agrees."""
     import torch
     tb = surv.numel() // m if m else 0
-    return (surv.dtype == torch.complex64 and mode == "fast" and lag == "mf" and doppler in ("nfft", "ndft")
-            and 128 <= tb <= 4096 and tb % 128 == 0 and (l_bins is None or l_bins >= world))
+    return (surv.dtype == torch.complex64 and mode == "fast" and lag == "mf" and doppler == "nfft"
+            and 128 <= tb <= 4096 and tb % 128 == 0 and 64 <= m <= 2048 and (m & (m - 1)) == 0
+            and (l_bins is None or (l_bins >= world and l_bins % (16 * world) == 0)))
 
 
 def map_blocks_sharded(surv, ref, l_bins: int, m: int, zx: ZExchange, pm: PeerMap, *, gain: float = 1.0,
@@ -289,15 +290,10 @@ def map_blocks_sharded(surv, ref, l_bins: int, m: int, zx: ZExchange, pm: PeerMa
         _native.ptr(zx.table), world, _native.stream_ptr())
     _native.check(rc)
     _done(pm.done_flag(), group)  # every rank's z rows are in their owners' blocks
-    if zx.count:
+    if zx.count:  # Doppler NL-FFT of this rank's delay rows (blocked z) into the root's map
         tw = device_twiddles(m, d, surv.device.index)
-        if doppler == "nfft":
-            _native.check(_native.lib().sa_nlfft(d, _native.SA_DIT, _native.ptr(zx.z), ctypes.c_void_p(
-                pm.rows_ptr(zx.first)), zx.count, m, ctypes.c_void_p(tw), float(gain), _native.stream_ptr()))
-        else:
-            _native.check(_native.lib().sa_ndft(d, _native.ptr(zx.z), ctypes.c_void_p(pm.rows_ptr(zx.first)),
-                                                zx.count, m, ctypes.c_void_p(tw), _native.SA_NDFT_TC,
-                                                float(gain), _native.stream_ptr()))
+        _native.check(_native.lib().sa_doppler_nlfft_blocked(d, _native.ptr(zx.z), ctypes.c_void_p(
+            pm.rows_ptr(zx.first)), zx.count, m, ctypes.c_void_p(tw), float(gain), _native.stream_ptr()))
     _done(pm.done_flag(), group)  # every rank's rows are in the root's map
 
 

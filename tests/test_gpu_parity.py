@@ -535,13 +535,20 @@ def _p2p_worker(rank, port, q):
         ds = torch.from_numpy(sc.surv.astype(np.complex64)).cuda()
         dr = torch.from_numpy(sc.ref.astype(np.complex64)).cuda()
         from paper_1402_0532_b200.sharded import blocks_shardable
-        assert blocks_shardable(ds, 128, "fast", "mf", "nfft")  # c64, T = 512: block-sharded lag stage
-        pm = PeerMap(101, 128, ds.dtype)  # odd row count: uneven shards
-        for _ in range(2):  # the shared map is reused across calls
-            full = ambiguity_map_sharded(ds, dr, 101, 128, peer_map=pm)
+        # c64, T = 512, 96 rows = 3 tiles of 16 per rank: block-sharded lag stage;
+        # 101 rows (uneven): delay-row shards
+        assert blocks_shardable(ds, 128, "fast", "mf", "nfft", 96, 2)
+        assert not blocks_shardable(ds, 128, "fast", "mf", "nfft", 101, 2)
+        ok = []
+        for L in (96, 101):
+            pm = PeerMap(L, 128, ds.dtype)
+            for _ in range(2):  # the shared map is reused across calls
+                full = ambiguity_map_sharded(ds, dr, L, 128, peer_map=pm)
+            if rank == 0:
+                ok.append(bool(torch.equal(full, sa.ambiguity_map(ds, dr, L, 128))))
+            pm.close()
         if rank == 0:
-            q.put(bool(torch.equal(full, sa.ambiguity_map(ds, dr, 101, 128))))
-        pm.close()
+            q.put(all(ok) and len(ok) == 2)
     finally:
         dist.destroy_process_group()
 

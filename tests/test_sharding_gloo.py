@@ -72,27 +72,29 @@ def test_gather_rows_world2(L):
     assert q.get(timeout=10) is True
 
 
-def _owner_kernel(lag, base, extra):
-    """Restatement of LagDst::row (sa_lag_tc.cu): owner rank of a z row and its
-    row inside the owner's block, for the shard_rows partition (base, extra)."""
-    big = extra * (base + 1)
-    o = lag // (base + 1) if lag < big else extra + (lag - big) // base
-    first = o * base + min(o, extra)
-    return o, lag - first
+def _owner_line(k, base):
+    """Restatement of LagDst::line (sa_lag_tc.cu): owner rank of the 16-lag tile k
+    of the blocked z layout and the tile's index inside the owner's block
+    (16-aligned shards: base = L / G rows each, base % 16 == 0)."""
+    o = (16 * k) // base
+    return o, k - o * (base // 16)
 
 
-def test_block_sharded_row_owners_match_shard_rows():
-    """The block-sharded lag kernel stores z row `lag` into the block of the rank
-    that shard_rows gives that delay row (the rank that runs its Doppler transform)."""
-    for L in (1, 7, 101, 1024, 4096, 4097):
-        for G in (1, 2, 3, 4, 8):
-            if G > L:
+def test_block_sharded_tile_owners_match_shard_rows():
+    """The block-sharded lag kernel stores the 16-lag tile k into the block of
+    the rank that shard_rows gives those delay rows (the rank that runs their
+    Doppler transform), at the owner-local tile index."""
+    for L in (16, 64, 1024, 4096):
+        for G in (1, 2, 4, 8):
+            if L % (16 * G):
                 continue
-            base, extra = divmod(L, G)
+            base = L // G
             for r in range(G):
                 f, c = shard_rows(L, G, r)
                 for lag in range(f, f + c):
-                    assert _owner_kernel(lag, base, extra) == (r, lag - f)
+                    k, j = divmod(lag, 16)
+                    o, kl = _owner_line(k, base)
+                    assert o == r and 16 * kl + j == lag - f
 
 
 def _blocks_worker(rank, world, port, L, M, q):
@@ -103,16 +105,22 @@ def _blocks_worker(rank, world, port, L, M, q):
         # rank integrates Doppler blocks shard_rows(M) for every delay row ...
         q0, qc = shard_rows(M, world, rank)
         zpart = torch.tensor([[1000.0 * l + qq for qq in range(q0, q0 + qc)] for l in range(L)])
-        # ... and each z row reaches its owner (CPU stand-in for the kernel's peer stores)
+        # ... and each 16-lag tile reaches its owner in the blocked layout
+        # zb[(k * M + q) * 16 + j] (CPU stand-in for the kernel's peer sector stores)
         parts = [None] * world
         dist.all_gather_object(parts, (q0, zpart))
         f, c = shard_rows(L, world, rank)
-        mine = torch.zeros((c, M))
+        zb = torch.zeros(c * M)
         for (p0, zp) in parts:
-            for lag in range(f, f + c):
-                o, row = _owner_kernel(lag, L // world, L % world)
-                assert o == rank
-                mine[row, p0:p0 + zp.shape[1]] = zp[lag]
+            for k in range(L // 16):
+                o, kl = _owner_line(k, L // world)
+                if o != rank:
+                    continue
+                for j in range(16):
+                    for qq in range(zp.shape[1]):
+                        zb[(kl * M + p0 + qq) * 16 + j] = zp[16 * k + j, qq]
+        # the owner's Doppler stage reads row (16 kl + j) element q from the same place
+        mine = torch.tensor([[float(zb[((r // 16) * M + qq) * 16 + r % 16]) for qq in range(M)] for r in range(c)])
         want = torch.tensor([[1000.0 * l + qq for qq in range(M)] for l in range(f, f + c)])
         q.put(bool(torch.equal(mine, want)))
     finally:
@@ -120,12 +128,12 @@ def _blocks_worker(rank, world, port, L, M, q):
 
 
 def test_block_sharded_exchange_world2():
-    """World 2 (gloo): block partition of the lag stage + owner rows give every
-    rank exactly its delay rows over all Doppler blocks (uneven L and M)."""
+    """World 2 (gloo): block partition of the lag stage + owner tiles give every
+    rank exactly its delay rows over all Doppler blocks (uneven M)."""
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    ps = [ctx.Process(target=_blocks_worker, args=(r, 2, port, 13, 9, q)) for r in range(2)]
+    ps = [ctx.Process(target=_blocks_worker, args=(r, 2, port, 64, 9, q)) for r in range(2)]
     for p in ps:
         p.start()
     res = [q.get(timeout=120) for _ in ps]
