@@ -34,21 +34,23 @@
 
 namespace {
 
-constexpr int LGRP = 1024;       // lags per group (128 l1 x 8 l0)
-constexpr int PAD = 1024;        // zero padding in front of the A arrays (u >= -1024)
+// A lag group is MR rows l1 (MMA M = 128, or 64 for short lag ranges: half the
+// A-operand bytes per MMA, twice the groups stacked along N) x 8 l0: 8 MR lags;
+// the A arrays carry 8 MR zeros on each side (u >= -8 MR).
 constexpr int NKIND = 6;         // A kinds: sgn sr, sgn si, sr_hi, sr_lo, si_hi, si_lo
 constexpr int BROWS = 96;        // B rows per lag group: B1 32 + B2 32 + B3 16 + B4 16
 constexpr int B_BYTES = BROWS * 128 * 2;  // 24 KB per buffer: G groups x 128 / G u per K chunk
 constexpr int BUILDERS = 256;    // warps 0-7 build the operands (warps 0-3 also drain TMEM)
 constexpr int THREADS = BUILDERS + 32;  // warp 8 issues the MMAs
 
-__host__ __device__ inline int a_len(int tb) { return tb + 2 * PAD; }  // u + 8 l1 in [-1024, T + 1016), padded
-__host__ __device__ inline size_t smem_bytes(int tb) { return (size_t)NKIND * a_len(tb) * 2 + 2 * B_BYTES + 1024 + 64; }
+__host__ __device__ inline int a_len(int tb, int mr) { return tb + 16 * mr; }  // u + 8 l1 in [-8 MR, T + 8 MR), padded
+__host__ __device__ inline size_t a_bytes(int tb, int mr) { return ((size_t)NKIND * a_len(tb, mr) * 2 + 1023) & ~(size_t)1023; }
+__host__ __device__ inline size_t smem_bytes(int tb, int mr) { return a_bytes(tb, mr) + 2 * B_BYTES + 1024 + 64; }
 constexpr int tmem_cols(int g) { return g == 1 ? 64 : (g == 2 ? 128 : 256); }  // >= 48 G, power of 2
 
-// instruction descriptor: kind::f16, bf16 x bf16 -> f32, K-major, M = 128, N = n
-constexpr uint32_t idesc(int n) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+// instruction descriptor: kind::f16, bf16 x bf16 -> f32, K-major, M = mr, N = n
+constexpr uint32_t idesc(int n, int mr) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(mr >> 4) << 24);
 }
 // K-major, no swizzle: core matrices of 8 rows x 16 B; LBO = next 8 K elements, SBO = next 8 rows
 SA_HD uint64_t sdesc_ns(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -122,15 +124,18 @@ struct LagDst {
 };
 
 // G lag groups share each A read (one pass): the MMAs widen to N = 32 G / 16 G.
-template <int G, bool BLK>
+// MR = 64: accumulator row r sits in TMEM lane 32 (r / 16) + r % 16 (the lower
+// half of each warp's sub-partition; measured, tools/probes/probe_m64.cu).
+template <int G, bool BLK, int MR>
 __global__ void __launch_bounds__(THREADS, 2)
     k_lag_tc(const float2 *__restrict__ surv, const float2 *__restrict__ ref, int64_t ref_len, int64_t l0g, int64_t l_count,
              int64_t m, int tb, float csign, float2 *__restrict__ z, int64_t q0, LagDst dst) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const int al = a_len(tb);
+  constexpr int LGRP = 8 * MR, PAD = 8 * MR;
+  const int al = a_len(tb, MR);
   uint16_t *A = (uint16_t *)smem;                      // NKIND x al bf16
-  unsigned char *Bb = smem + (size_t)NKIND * al * 2;   // 2 x B_BYTES (1024-aligned: al * 2 * 6 % 1024 == 0)
+  unsigned char *Bb = smem + a_bytes(tb, MR);          // 2 x B_BYTES (1024-aligned)
   uint64_t *bar = (uint64_t *)(Bb + 2 * B_BYTES);      // "empty": MMAs that read B buffer b are done
   uint64_t *full = bar + 2;                            // B buffer b built (one arrive per builder warp)
   uint64_t *dempty = full + 2;                         // TMEM drained by the epilogue warps
@@ -203,12 +208,12 @@ __global__ void __launch_bounds__(THREADS, 2)
             const uint64_t b1 = sdesc_ns(bo, 128, SBO), b2 = sdesc_ns(bo + 4 * G * SBO, 128, SBO),
                            b3 = sdesc_ns(bo + 8 * G * SBO, 128, SBO), b4 = sdesc_ns(bo + 10 * G * SBO, 128, SBO);
             auto ad = [&](int k) { return sdesc_ns(abase + (uint32_t)k * al * 2 + ua, 16, 128); };
-            mma(tmem, ad(0), b1, idesc(32 * G), acc);
-            mma(tmem, ad(1), b2, idesc(32 * G), 1);
-            mma(tmem + 32 * G, ad(2), b3, idesc(16 * G), acc);
-            mma(tmem + 32 * G, ad(3), b3, idesc(16 * G), 1);
-            mma(tmem + 32 * G, ad(4), b4, idesc(16 * G), 1);
-            mma(tmem + 32 * G, ad(5), b4, idesc(16 * G), 1);
+            mma(tmem, ad(0), b1, idesc(32 * G, MR), acc);
+            mma(tmem, ad(1), b2, idesc(32 * G, MR), 1);
+            mma(tmem + 32 * G, ad(2), b3, idesc(16 * G, MR), acc);
+            mma(tmem + 32 * G, ad(3), b3, idesc(16 * G, MR), 1);
+            mma(tmem + 32 * G, ad(4), b4, idesc(16 * G, MR), 1);
+            mma(tmem + 32 * G, ad(5), b4, idesc(16 * G, MR), 1);
           }
           commit(&bar[b]);
         }
@@ -284,7 +289,8 @@ __global__ void __launch_bounds__(THREADS, 2)
         sa_mbar_wait(&bar[last & 1], (last >> 1) & 1);
         fence_after();
         const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
-        const int l1 = warp * 32 + lane;
+        const int l1 = MR == 128 ? warp * 32 + lane : warp * 16 + (lane & 15);
+        const bool live = MR == 128 || lane < 16;  // MR = 64: lanes 16-31 hold no rows
 #pragma unroll 1
         for (int gs = 0; gs < G; ++gs) {
           uint32_t d1[16], d2[16], d3[16];
@@ -303,7 +309,7 @@ __global__ void __launch_bounds__(THREADS, 2)
 #pragma unroll
             for (int l0 = 0; l0 < 8; ++l0) {
               const int64_t lag = lagb + l0 - l0g;  // row of z
-              if (lag >= 0 && lag < l_count) *dst.row(z, lag, m, q) = make_float2(re[l0], im[l0]);
+              if (live && lag >= 0 && lag < l_count) *dst.row(z, lag, m, q) = make_float2(re[l0], im[l0]);
             }
           } else {
             // lanes (2i, 2i+1) hold the 16 lags of tile k: swap halves so that every
@@ -322,7 +328,7 @@ __global__ void __launch_bounds__(THREADS, 2)
               rcv[i].w = __shfl_xor_sync(0xffffffffu, snd[i].w, 1);
             }
             const int64_t t0 = lalign + 16 * k;  // tile intersects the call's rows?
-            if (t0 + 16 > l0g && t0 < l0g + l_count) {
+            if (live && t0 + 16 > l0g && t0 < l0g + l_count) {
               float4 *ln = reinterpret_cast<float4 *>(dst.line(z, k, m, q));
               if (!odd) {
                 ln[0] = c[0];
@@ -363,36 +369,66 @@ int sa_launch_lag_tc(const void *surv, const void *ref, int64_t ref_len, int64_t
   return sa_launch_lag_tc_blocks(surv, ref, ref_len, l0, l_count, m, 0, m, tb, conj, z, nullptr, 0, 0, blocked, s);
 }
 
-template <int G, bool BLK>
+template <int G, bool BLK, int MR>
 int launch_g(const void *surv, const void *ref, int64_t ref_len, int64_t l0, int64_t l_count, int64_t m, int64_t q0,
              int64_t q_count, int64_t tb, int conj, void *z, const LagDst &d, cudaStream_t s) {
-  const size_t bytes = smem_bytes((int)tb);
+  const size_t bytes = smem_bytes((int)tb, MR);
   static int smem_set[64] = {};  // largest smem size set per device
   int dev = 0;
   SA_CUDA_TRY(cudaGetDevice(&dev));
   if (dev >= 64 || smem_set[dev] < (int)bytes) {
-    SA_CUDA_TRY(cudaFuncSetAttribute(k_lag_tc<G, BLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    SA_CUDA_TRY(cudaFuncSetAttribute(k_lag_tc<G, BLK, MR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     if (dev < 64) smem_set[dev] = (int)bytes;
   }
-  k_lag_tc<G, BLK><<<(unsigned)q_count, THREADS, bytes, s>>>((const float2 *)surv, (const float2 *)ref, ref_len, l0,
-                                                             l_count, m, (int)tb, conj ? -1.f : 1.f, (float2 *)z, q0, d);
+  k_lag_tc<G, BLK, MR><<<(unsigned)q_count, THREADS, bytes, s>>>((const float2 *)surv, (const float2 *)ref, ref_len,
+                                                                 l0, l_count, m, (int)tb, conj ? -1.f : 1.f,
+                                                                 (float2 *)z, q0, d);
   SA_LAUNCH_CHECK();
   return SA_OK;
+}
+
+// Lag-group shape of a call: rows per group MR and groups per pass G, from the
+// smem-operand cost per block (A: 6 kinds x MR x 32 B per 16 u; B: 96 G rows x
+// 32 B) against the tensor floor (N/2 cycles per M = 64/128, K = 16 MMA).
+struct LagShape {
+  int mr, g;
+};
+LagShape lag_shape(int64_t l0, int64_t l_count, int64_t tb) {
+#ifdef SA_LAG_MR
+  const int only = SA_LAG_MR;
+#else
+  const int only = 0;
+#endif
+  LagShape best{128, 1};
+  double best_cost = 1e300;
+  for (int mr : {64, 128}) {
+    if (only && mr != only) continue;
+    const int64_t ngrp = ((l0 & 15) + l_count + 8 * mr - 1) / (8 * mr);
+    const int g = ngrp >= 3 ? 4 : (int)ngrp;
+    const int64_t npass = (ngrp + g - 1) / g;
+    const double smem_cyc = (6.0 * mr * 32 + 96.0 * g * 32) / 128.0, tc_cyc = 64.0 * g;
+    const double cost = (double)npass * (double)(tb + 8 * mr) / 16.0 * (smem_cyc > tc_cyc ? smem_cyc : tc_cyc);
+    if (cost < best_cost) best_cost = cost, best = {mr, g};
+  }
+  return best;
 }
 
 int sa_launch_lag_tc_blocks(const void *surv, const void *ref, int64_t ref_len, int64_t l0, int64_t l_count, int64_t m,
                             int64_t q0, int64_t q_count, int64_t tb, int conj, void *z, void *const *dst_rows,
                             int64_t rows_base, int64_t rows_extra, int blocked, cudaStream_t s) {
   if (l_count == 0 || q_count == 0) return SA_OK;
-  // lag groups (of 1024, aligned to 16) per call -> groups merged per pass
-  const int64_t ngrp = ((l0 & 15) + l_count + LGRP - 1) / LGRP;
-  const int g = ngrp >= 3 ? 4 : (int)ngrp;
+  const LagShape sh = lag_shape(l0, l_count, tb);
   const LagDst d{(float2 *const *)dst_rows, rows_base, rows_extra};
-#define SA_LAG_LAUNCH(G)                                                                                         \
-  return blocked ? launch_g<G, true>(surv, ref, ref_len, l0, l_count, m, q0, q_count, tb, conj, z, d, s)        \
-                 : launch_g<G, false>(surv, ref, ref_len, l0, l_count, m, q0, q_count, tb, conj, z, d, s)
-  if (g == 4) SA_LAG_LAUNCH(4);
-  if (g == 2) SA_LAG_LAUNCH(2);
-  SA_LAG_LAUNCH(1);
+#define SA_LAG_LAUNCH(G, MR)                                                                                     \
+  return blocked ? launch_g<G, true, MR>(surv, ref, ref_len, l0, l_count, m, q0, q_count, tb, conj, z, d, s)    \
+                 : launch_g<G, false, MR>(surv, ref, ref_len, l0, l_count, m, q0, q_count, tb, conj, z, d, s)
+  if (sh.mr == 64) {
+    if (sh.g == 4) SA_LAG_LAUNCH(4, 64);
+    if (sh.g == 2) SA_LAG_LAUNCH(2, 64);
+    SA_LAG_LAUNCH(1, 64);
+  }
+  if (sh.g == 4) SA_LAG_LAUNCH(4, 128);
+  if (sh.g == 2) SA_LAG_LAUNCH(2, 128);
+  SA_LAG_LAUNCH(1, 128);
 #undef SA_LAG_LAUNCH
 }
