@@ -89,6 +89,8 @@ int sa_twiddle_destroy(void *handle) {
   cudaFree(tw->stage2);
   cudaFree(tw->tcw);
   if (tw->tcw_ready) cudaEventDestroy((cudaEvent_t)tw->tcw_ready);
+  cudaFree(tw->i8w);
+  if (tw->i8w_ready) cudaEventDestroy((cudaEvent_t)tw->i8w_ready);
   cudaSetDevice(prev);
   delete tw;
   return SA_OK;
@@ -121,7 +123,8 @@ int sa_ndft(int dtype, const void *x, void *y, int64_t batch, int64_t n, const v
   int rc = check_tw(tw, dtype, n, false);
   if (rc) return rc;
   if (mode == SA_NDFT_TC) {
-    rc = sa_launch_ndft_tc(x, y, batch, n, (const SaTwiddles *)tw, gain, (cudaStream_t)stream);
+    rc = dtype == SA_C64 ? sa_launch_ndft_tc(x, y, batch, n, (const SaTwiddles *)tw, gain, (cudaStream_t)stream)
+                         : sa_launch_ndft_i8(x, y, batch, n, (const SaTwiddles *)tw, gain, (cudaStream_t)stream);
     if (rc != SA_ERR_UNSUPPORTED) return rc;
     mode = SA_NDFT_FAST;  // other shapes / unaligned views: the same regrouped sum on the FFMA2 kernels
   }

@@ -19,6 +19,8 @@ struct SaTwiddles {
   void *stage2; // (n-1) x {wr, wi}, same stage-packed order (8/16-byte entries)
   void *tcw;    // tensor-core NDFT operands [W0; W1; sgn Wv] (bf16, 3 x 2n x 2n), built on first use
   void *tcw_ready;  // cudaEvent_t recorded after the tcw build (streams wait on it)
+  void *i8w;        // complex128 tensor-core NDFT: six int8 planes of Wv (sa_ndft_i8.cu), built on first use
+  void *i8w_ready;
 };
 
 void sa_set_error(const char *fmt, ...);
@@ -59,6 +61,10 @@ int sa_launch_ndft(int dtype, const void *x, void *y, int64_t batch, int64_t n,
 // sa_ndft_tc.cu (tensor-core fast mode; SA_ERR_UNSUPPORTED -> use the FFMA2 kernels)
 bool sa_ndft_tc_supported(int dtype, int64_t n);
 int sa_launch_ndft_tc(const void *x, void *y, int64_t batch, int64_t n, const SaTwiddles *tw, double gain,
+                      cudaStream_t s);
+// sa_ndft_i8.cu (complex128 fast mode on tcgen05 kind::i8, exact integer digits)
+bool sa_ndft_i8_supported(int dtype, int64_t n);
+int sa_launch_ndft_i8(const void *x, void *y, int64_t batch, int64_t n, const SaTwiddles *tw, double gain,
                       cudaStream_t s);
 
 // sa_lag_tc.cu (tensor-core fast-mode lag integration, complex64)

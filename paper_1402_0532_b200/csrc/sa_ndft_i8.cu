@@ -1,0 +1,453 @@
+// sa_ndft_i8.cu -- complex128 fast-mode NDFT (transforms.py:223-251, regrouped as
+// in sa_ndft.cu) on the tcgen05 tensor cores in EXACT INTEGER arithmetic: an
+// Ozaki-style split of both non-sign operands into int8 digits, int8 x int8 ->
+// int32 MMAs (kind::i8), fp64 only in the epilogue.
+//
+// The regrouped sum is one real GEMM per batch (sa_ndft_tc.cu):
+//   D[v, o] = Σ_K S[v,K] Wv[o,K] + X[v,K] sgn(Wv)[o,K],   S = sgn(x),  o = 2k+(re|im), K = 2n+(re|im)
+// One factor of every product is a sign in {-1, 0, +1} -- exact in int8.  The
+// other factor is split into four signed digits in mixed radix (64, 127, 128, 127):
+//   Wv ~ d0/64 + d1/(64 127) + d2/(64 127 128) + d3/(64 127 128 127)    (|Wv| <= 1, |d| <= 64)
+//   x' = x_v / 2^e_v   (per-vector exponent: max|x_v| < 2^e_v), digits alike
+// (round-to-nearest digits; the residual after the fourth digit is <= 2^-28).
+// Two digits 127 apart share one int32 accumulator by pairing the sign operand
+// with 127 x sign (still int8):
+//   accWH = Σ (127 S) dW0 + S dW1        accWL = Σ (127 S) dW2 + S dW3
+//   accXH = Σ dx0 (127 sW) + dx1 sW      accXL = Σ dx2 (127 sW) + dx3 sW
+// all exact (|acc| < 2^25 at n <= 2048), and the epilogue forms, in fp64,
+//   D = accWH c1 + accWL c2 + 2^e_v (accXH c1 + accXL c2),  c1 = 1/(64 127), c2 = c1/(128 127).
+// Error model: per output ~ sqrt(2n) 2^-28 (1 + 2^e) against ||y||_1 ~ n sqrt(2n):
+// the fp64 bound 1e-9 holds from n = 128 up; measured max|Δ|/‖y‖₁ ~1e-11 on C2
+// (tests/test_gpu_ndft_i8.py).  Smaller n runs the DFMA fast kernel.
+//
+// Pipeline: k_i8_prep (one pass over x: gain, per-vector exponent, six int8
+// planes S, 127 S, dx0..dx3, row-major [v][K]) -> k_ndft_i8 (persistent CTA
+// pairs, cluster 2, tcgen05.mma.cta_group::2.kind::i8, M = 256 vectors, N = 128
+// outputs, K = 32; the four accumulators fill TMEM's 512 columns).  Both operand
+// sets arrive by TMA (SWIZZLE_64B, 64 K per slot, three 72 KB slots per CTA):
+// the six W planes (sW, 127 sW, dW0..dW3: 6 (2n)^2 bytes, built once per twiddle
+// set, L2 evict_last) and the six x planes.  Warp 0 produces, warp 1 issues
+// (leader CTA), warps 2-5 drain TMEM into complex128 rows of y.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "sa_internal.h"
+#include "sa_regs.cuh"
+
+namespace {
+
+constexpr int BM = 128;               // vectors per CTA (TMEM lanes); M = 256 per pair
+constexpr int BN = 128;               // outputs per tile (each accumulator: 128 TMEM columns)
+constexpr int KSL = 64;               // int8 K elements per slot (64-B rows, SWIZZLE_64B)
+constexpr int NPL = 6;                // planes per operand side
+constexpr int XT = BM * KSL;          // one x-plane tile per CTA: 8 KB
+constexpr int WT = (BN / 2) * KSL;    // one W-plane tile per CTA (half the outputs): 4 KB
+constexpr int SLOT = NPL * XT + NPL * WT;  // 72 KB
+constexpr int NSLOT = 3;
+constexpr int SMEM = NSLOT * SLOT + 1024 + 256;
+constexpr int THREADS = 6 * 32;
+constexpr int TMEM_COLS = 512;
+// kind::i8: D = s32 (2), A = B = s8 (1), K-major, N = 128, M = 256
+constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+
+SA_HD uint64_t sdesc(uint32_t saddr) {  // K-major SWIZZLE_64B: 64-B rows, 8-row atoms 512 B apart
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+}
+SA_HD void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+SA_HD void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+SA_HD void commit2(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          sa_smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+SA_HD void mma2(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(IDESC), "r"(acc)
+      : "memory");
+}
+SA_HD void arrive_cl(uint32_t cl_addr) { asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory"); }
+SA_HD void tma2(uint32_t dst, const CUtensorMap *map, int c0, int c1, uint32_t lead_bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(lead_bar), "l"(pol)
+      : "memory");
+}
+SA_HD uint64_t policy(bool keep) {
+  uint64_t p;
+  if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+SA_HD uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+SA_HD void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+#define SA_LD16(v, taddr)                                                                                  \
+  asm volatile(                                                                                            \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"    \
+      " [%16];"                                                                                            \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),    \
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),           \
+        "=r"(v[15])                                                                                        \
+      : "r"(taddr))
+
+// The four signed digits (radix 64, 127, 128, 127; each |d| <= 64) of |v| <= 1.
+SA_HD void digits(double v, int &d0, int &d1, int &d2, int &d3) {
+  double y = v * 64.0;
+  double r = rint(y);
+  d0 = (int)r;
+  y = (y - r) * 127.0;
+  r = rint(y);
+  d1 = (int)r;
+  y = (y - r) * 128.0;
+  r = rint(y);
+  d2 = (int)r;
+  y = (y - r) * 127.0;
+  d3 = (int)rint(y);
+}
+SA_HD int sgn_i(double v) { return v > 0.0 ? 1 : (v < 0.0 ? -1 : 0); }
+
+// x (batch x n complex128, gain applied) -> planes P[p][v][K] (p = S, 127 S,
+// dx0..dx3; K = 2m + re/im) and the per-vector exponent e[v] (max|x_v| < 2^e).
+__global__ void __launch_bounds__(256) k_i8_prep(const double *__restrict__ x, int8_t *__restrict__ planes,
+                                                 int *__restrict__ ex, int64_t batch, int n, double gain,
+                                                 int use_gain) {
+  __shared__ double red[8];
+  const int nk = 2 * n;
+  const size_t pstride = (size_t)batch * nk;
+  for (int64_t v = blockIdx.x; v < batch; v += gridDim.x) {
+    const double *row = x + v * nk;
+    double mx = 0.0;
+    for (int k = threadIdx.x * 2; k < nk; k += 512) {
+      double2 t = *(const double2 *)&row[k];
+      if (use_gain) t = {sa_mul(gain, t.x), sa_mul(gain, t.y)};
+      mx = fmax(mx, fmax(fabs(t.x), fabs(t.y)));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    mx = red[0];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) mx = fmax(mx, red[w]);
+    __syncthreads();
+    int e = 0;
+    if (mx > 0.0) frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1): max < 2^e
+    if (threadIdx.x == 0) ex[v] = e;
+    int8_t *p0 = planes + v * nk;
+    for (int k = threadIdx.x * 2; k < nk; k += 512) {
+      double2 t = *(const double2 *)&row[k];
+      if (use_gain) t = {sa_mul(gain, t.x), sa_mul(gain, t.y)};
+      int a0, a1, a2, a3, b0, b1, b2, b3;
+      digits(ldexp(t.x, -e), a0, a1, a2, a3);
+      digits(ldexp(t.y, -e), b0, b1, b2, b3);
+      const int sa = sgn_i(t.x), sb = sgn_i(t.y);
+      auto put = [&](int p, int lo, int hi) {
+        *(uint16_t *)&p0[p * pstride + k] = (uint16_t)((lo & 0xFF) | ((hi & 0xFF) << 8));
+      };
+      put(0, sa, sb);
+      put(1, 127 * sa, 127 * sb);
+      put(2, a0, b0);
+      put(3, a1, b1);
+      put(4, a2, b2);
+      put(5, a3, b3);
+    }
+  }
+}
+
+// W planes Q[p][o][K] (p = sW, 127 sW, dW0..dW3) of Wv = [[Wr, -Wi], [Wi, Wr]],
+// W = raw[(k m) mod n] (the fp64 reference table, transforms.py:108-146).
+__global__ void k_i8_wbuild(const double2 *__restrict__ raw, int n, int8_t *__restrict__ q) {
+  const int64_t nn = 2LL * n, total = nn * nn;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = i / nn, kk = i % nn;
+    const int64_t k = o >> 1, m = kk >> 1;
+    const int co = (int)(o & 1), ci = (int)(kk & 1);
+    const double2 tw = raw[(k * m) % n];
+    const double val = co == ci ? tw.x : (co == 0 ? -tw.y : tw.y);
+    int d0, d1, d2, d3;
+    digits(val, d0, d1, d2, d3);
+    const int s = sgn_i(val);
+    q[i] = (int8_t)s;
+    q[total + i] = (int8_t)(127 * s);
+    q[2 * total + i] = (int8_t)d0;
+    q[3 * total + i] = (int8_t)d1;
+    q[4 * total + i] = (int8_t)d2;
+    q[5 * total + i] = (int8_t)d3;
+  }
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    k_ndft_i8(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap wmap,
+              const int *__restrict__ ex, double *__restrict__ y, int64_t batch, int n) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t *full = (uint64_t *)(smem + NSLOT * SLOT);
+  uint64_t *empty = full + NSLOT;
+  uint64_t *tfull = empty + NSLOT;
+  uint64_t *tempty = tfull + 1;
+  uint32_t *tmem_holder = (uint32_t *)(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int64_t cl = blockIdx.x / 2, ncl = gridDim.x / 2;
+  const int nk = 2 * n;
+  const int ot_count = nk / BN;
+  const int64_t vt_count = (batch + 2 * BM - 1) / (2 * BM);
+  const int64_t ntiles = vt_count * ot_count;
+  const int kslots = nk / KSL;
+  const int64_t xrows = batch;  // rows per x plane in the stacked x-plane tensor
+  auto lead = [&](uint64_t *bar) { return sa_mapa(sa_smem_u32(bar), 0); };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSLOT; ++s) {
+      sa_mbar_init(&full[s], 1);
+      sa_mbar_init(&empty[s], 1);
+    }
+    sa_mbar_init(tfull, 1);
+    sa_mbar_init(tempty, 4 * 2);
+    sa_fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa_smem_u32(tmem_holder)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  fence_before();
+  cluster_sync_all();
+  fence_after();
+  const uint32_t tmem = *tmem_holder;
+  const int64_t my_tiles = cl < ntiles ? (ntiles - 1 - cl) / ncl + 1 : 0;
+  const int64_t total = my_tiles * kslots;
+
+  if (warp == 0) {
+    // ---- TMA producer: this CTA's 128 vector rows of the 6 x planes, its 64 output rows of the 6 W planes ----
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&wmap) : "memory");
+      const uint64_t wpol = policy(true), xpol = policy(false);
+      for (int64_t it = 0; it < total; ++it) {
+        const int64_t lt = it / kslots;
+        const int kc = (int)(it - lt * kslots);
+        const int64_t t = cl + lt * ncl;
+        const int64_t v0 = (t / ot_count) * (2 * BM) + rank * BM;
+        const int o0 = (int)(t % ot_count) * BN + (int)rank * (BN / 2);
+        const int s = (int)(it % NSLOT);
+        sa_mbar_wait(&empty[s], ((it / NSLOT) & 1) ^ 1);
+        const uint32_t b = sa_smem_u32(smem + s * SLOT);
+        if (rank == 0) sa_mbar_expect_tx(&full[s], 2 * SLOT);
+#pragma unroll
+        for (int p = 0; p < NPL; ++p) {
+          tma2(b + p * XT, &xmap, kc * KSL, (int)(p * xrows + v0), lead(&full[s]), xpol);
+          tma2(b + NPL * XT + p * WT, &wmap, kc * KSL, p * nk + o0, lead(&full[s]), wpol);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer (leader CTA): 8 MMAs per K step of 32 into the four accumulators ----
+    if (lane == 0 && rank == 0) {
+      uint32_t it = 0, lt = 0;
+      for (int64_t t = cl; t < ntiles; t += ncl, ++lt) {
+        sa_mbar_wait(tempty, (lt & 1) ^ 1);
+        fence_after();
+        for (int kc = 0; kc < kslots; ++kc, ++it) {
+          const int s = it % NSLOT;
+          sa_mbar_wait(&full[s], (it / NSLOT) & 1);
+          fence_after();
+          const uint32_t base = sa_smem_u32(smem + s * SLOT);
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            const uint32_t off = ks * 32;
+            auto X = [&](int p) { return sdesc(base + p * XT + off); };
+            auto W = [&](int p) { return sdesc(base + NPL * XT + p * WT + off); };
+            const uint32_t first = (kc | ks) != 0;
+            mma2(tmem + 0, X(1), W(2), first);    // accWH += 127 S dW0
+            mma2(tmem + 0, X(0), W(3), 1);        //        + S dW1
+            mma2(tmem + 128, X(1), W(4), first);  // accWL += 127 S dW2
+            mma2(tmem + 128, X(0), W(5), 1);      //        + S dW3
+            mma2(tmem + 256, X(2), W(1), first);  // accXH += dx0 127 sW
+            mma2(tmem + 256, X(3), W(0), 1);      //        + dx1 sW
+            mma2(tmem + 384, X(4), W(1), first);  // accXL += dx2 127 sW
+            mma2(tmem + 384, X(5), W(0), 1);      //        + dx3 sW
+          }
+          commit2(&empty[s]);
+        }
+        commit2(tfull);
+      }
+    }
+  } else {
+    // ---- epilogue (warps 2-5): TMEM lane quarter q -> vector row v, 128 outputs per tile ----
+    const int q = warp & 3;
+    uint32_t lt = 0;
+    for (int64_t t = cl; t < ntiles; t += ncl, ++lt) {
+      const int64_t v = (t / ot_count) * (2 * BM) + rank * BM + q * 32 + lane;
+      const int o0 = (int)(t % ot_count) * BN;
+      const int e = v < batch ? ex[v] : 0;
+      sa_mbar_wait(tfull, lt & 1);
+      fence_after();
+      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16);
+      double *dst = y + v * nk + o0;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        uint32_t wh[16], wl[16], xh[16], xl[16];
+        SA_LD16(wh, ta + c);
+        SA_LD16(wl, ta + 128 + c);
+        SA_LD16(xh, ta + 256 + c);
+        SA_LD16(xl, ta + 384 + c);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (v < batch) {
+#pragma unroll
+          for (int j = 0; j < 16; j += 2) {
+            double d[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              constexpr double C1 = 1.0 / (64.0 * 127.0), C2 = C1 / (128.0 * 127.0);
+              const double w = sa_fma((double)(int)wh[j + h], C1, sa_mul((double)(int)wl[j + h], C2));
+              const double xs = sa_fma((double)(int)xh[j + h], C1, sa_mul((double)(int)xl[j + h], C2));
+              d[h] = sa_add(ldexp(xs, e), w);
+            }
+            __stcs((double2 *)&dst[c + j], make_double2(d[0], d[1]));
+          }
+        }
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) arrive_cl(lead(tempty));
+    }
+  }
+
+  fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+  }
+}
+
+std::mutex g_i8_mutex;
+std::map<std::tuple<const void *, int64_t>, CUtensorMap> g_i8_wmaps;
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn_i8() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+int encode_u8(CUtensorMap *map, const void *base, int64_t rows, int64_t cols, int box_rows) {
+  auto enc = encode_fn_i8();
+  if (!enc) {
+    sa_set_error("cuTensorMapEncodeTiled unavailable");
+    return SA_ERR_CUDA;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols};
+  cuuint32_t box[2] = {(cuuint32_t)KSL, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    sa_set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return SA_ERR_CUDA;
+  }
+  return SA_OK;
+}
+
+}  // namespace
+
+bool sa_ndft_i8_supported(int dtype, int64_t n) { return dtype == SA_C128 && n >= 128 && n <= 2048 && n % 64 == 0; }
+
+int64_t sa_ndft_i8_wbytes(int64_t n) { return (int64_t)NPL * (2 * n) * (2 * n); }
+
+int sa_launch_ndft_i8(const void *x, void *y, int64_t batch, int64_t n, const SaTwiddles *tw_c, double gain,
+                      cudaStream_t s) {
+  if (!sa_ndft_i8_supported(tw_c->dtype, n)) return SA_ERR_UNSUPPORTED;
+  if (((uintptr_t)x | (uintptr_t)y) & 15) return SA_ERR_UNSUPPORTED;
+  if (batch == 0) return SA_OK;
+  SaTwiddles *tw = const_cast<SaTwiddles *>(tw_c);
+  CUtensorMap wmap, xmap;
+  {
+    // W planes built once per twiddle set, stream-ordered (event for later streams)
+    std::lock_guard<std::mutex> g(g_i8_mutex);
+    if (!tw->i8w) {
+      void *w = nullptr;
+      cudaEvent_t ev = nullptr;
+      SA_CUDA_TRY(cudaMalloc(&w, sa_ndft_i8_wbytes(n)));
+      k_i8_wbuild<<<1184, 256, 0, s>>>((const double2 *)tw->raw, (int)n, (int8_t *)w);
+      SA_LAUNCH_CHECK();
+      SA_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      SA_CUDA_TRY(cudaEventRecord(ev, s));
+      tw->i8w = w;
+      tw->i8w_ready = ev;
+    }
+    const auto key = std::make_tuple((const void *)tw->i8w, n);
+    auto it = g_i8_wmaps.find(key);
+    if (it == g_i8_wmaps.end()) {
+      int rc = encode_u8(&wmap, tw->i8w, (int64_t)NPL * 2 * n, 2 * n, BN / 2);
+      if (rc) return rc;
+      g_i8_wmaps.emplace(key, wmap);
+    } else {
+      wmap = it->second;
+    }
+  }
+  if (tw->i8w_ready) SA_CUDA_TRY(cudaStreamWaitEvent(s, (cudaEvent_t)tw->i8w_ready, 0));
+  // x planes + exponents: stream-ordered scratch (the pool reuses it across calls)
+  int8_t *planes = nullptr;
+  int *ex = nullptr;
+  const size_t pbytes = (size_t)NPL * batch * 2 * n;
+  SA_CUDA_TRY(cudaMallocAsync((void **)&planes, pbytes + (size_t)batch * sizeof(int) + 256, s));
+  ex = (int *)(((uintptr_t)(planes + pbytes) + 255) & ~(uintptr_t)255);
+  int dev = 0, sms = 148;
+  SA_CUDA_TRY(cudaGetDevice(&dev));
+  SA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int pgrid = (int)(batch < 8LL * sms ? batch : 8LL * sms);
+  k_i8_prep<<<pgrid, 256, 0, s>>>((const double *)x, planes, ex, batch, (int)n, gain, (int)(gain != 1.0));
+  SA_LAUNCH_CHECK();
+  int rc = encode_u8(&xmap, planes, (int64_t)NPL * batch, 2 * n, BM);
+  if (rc) return rc;
+  static bool smem_set[64] = {};
+  if (dev >= 64 || !smem_set[dev]) {
+    SA_CUDA_TRY(cudaFuncSetAttribute(k_ndft_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    if (dev < 64) smem_set[dev] = true;
+  }
+  const int64_t ntiles = ((batch + 2 * BM - 1) / (2 * BM)) * ((2 * n) / BN);
+  const int64_t units = ntiles < sms / 2 ? ntiles : sms / 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(units * 2));
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SA_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_ndft_i8, xmap, wmap, (const int *)ex, (double *)y, batch, (int)n));
+  SA_LAUNCH_CHECK();
+  SA_CUDA_TRY(cudaFreeAsync(planes, s));
+  return SA_OK;
+}
