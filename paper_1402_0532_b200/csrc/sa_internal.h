@@ -24,6 +24,8 @@ struct SaTwiddles {
 };
 
 void sa_set_error(const char *fmt, ...);
+// stream-ordered scratch from a per-device pool that keeps its memory (free with cudaFreeAsync)
+int sa_scratch_alloc(void **p, size_t bytes, cudaStream_t s);
 
 #define SA_CUDA_TRY(expr)                                                       \
   do {                                                                          \

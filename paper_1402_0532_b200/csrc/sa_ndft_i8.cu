@@ -43,13 +43,14 @@ namespace {
 constexpr int BM = 128;               // vectors per CTA (TMEM lanes); M = 256 per pair
 constexpr int BN = 128;               // outputs per tile (each accumulator: 128 TMEM columns)
 constexpr int KSL = 64;               // int8 K elements per slot (64-B rows, SWIZZLE_64B)
-constexpr int NPL = 6;                // planes per operand side
+constexpr int NPL = 6;                // smem tiles per operand side: S, 127 S, four digits
+constexpr int NMEM = 5;               // planes per side in HBM: 127 S is made in smem from S
 constexpr int XT = BM * KSL;          // one x-plane tile per CTA: 8 KB
 constexpr int WT = (BN / 2) * KSL;    // one W-plane tile per CTA (half the outputs): 4 KB
 constexpr int SLOT = NPL * XT + NPL * WT;  // 72 KB
 constexpr int NSLOT = 3;
 constexpr int SMEM = NSLOT * SLOT + 1024 + 256;
-constexpr int THREADS = 6 * 32;
+constexpr int THREADS = 8 * 32;       // producer, MMA, 4 epilogue, 2 scaler warps
 constexpr int TMEM_COLS = 512;
 // kind::i8: D = s32 (2), A = B = s8 (1), K-major, N = 128, M = 256
 constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
@@ -75,11 +76,11 @@ SA_HD void mma2(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
       : "memory");
 }
 SA_HD void arrive_cl(uint32_t cl_addr) { asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory"); }
-SA_HD void tma2(uint32_t dst, const CUtensorMap *map, int c0, int c1, uint32_t lead_bar, uint64_t pol) {
+SA_HD void tma_hint(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar, uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
-      "l"(map), "r"(c0), "r"(c1), "r"(lead_bar), "l"(pol)
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(sa_smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(sa_smem_u32(bar)), "l"(pol)
       : "memory");
 }
 SA_HD uint64_t policy(bool keep) {
@@ -122,7 +123,7 @@ SA_HD void digits(double v, int &d0, int &d1, int &d2, int &d3) {
 }
 SA_HD int sgn_i(double v) { return v > 0.0 ? 1 : (v < 0.0 ? -1 : 0); }
 
-// x (batch x n complex128, gain applied) -> planes P[p][v][K] (p = S, 127 S,
+// x (batch x n complex128, gain applied) -> planes P[p][v][K] (p = S,
 // dx0..dx3; K = 2m + re/im) and the per-vector exponent e[v] (max|x_v| < 2^e).
 __global__ void __launch_bounds__(256) k_i8_prep(const double *__restrict__ x, int8_t *__restrict__ planes,
                                                  int *__restrict__ ex, int64_t batch, int n, double gain,
@@ -161,16 +162,15 @@ __global__ void __launch_bounds__(256) k_i8_prep(const double *__restrict__ x, i
         *(uint16_t *)&p0[p * pstride + k] = (uint16_t)((lo & 0xFF) | ((hi & 0xFF) << 8));
       };
       put(0, sa, sb);
-      put(1, 127 * sa, 127 * sb);
-      put(2, a0, b0);
-      put(3, a1, b1);
-      put(4, a2, b2);
-      put(5, a3, b3);
+      put(1, a0, b0);
+      put(2, a1, b1);
+      put(3, a2, b2);
+      put(4, a3, b3);
     }
   }
 }
 
-// W planes Q[p][o][K] (p = sW, 127 sW, dW0..dW3) of Wv = [[Wr, -Wi], [Wi, Wr]],
+// W planes Q[p][o][K] (p = sW, dW0..dW3) of Wv = [[Wr, -Wi], [Wi, Wr]],
 // W = raw[(k m) mod n] (the fp64 reference table, transforms.py:108-146).
 __global__ void k_i8_wbuild(const double2 *__restrict__ raw, int n, int8_t *__restrict__ q) {
   const int64_t nn = 2LL * n, total = nn * nn;
@@ -184,11 +184,10 @@ __global__ void k_i8_wbuild(const double2 *__restrict__ raw, int n, int8_t *__re
     digits(val, d0, d1, d2, d3);
     const int s = sgn_i(val);
     q[i] = (int8_t)s;
-    q[total + i] = (int8_t)(127 * s);
-    q[2 * total + i] = (int8_t)d0;
-    q[3 * total + i] = (int8_t)d1;
-    q[4 * total + i] = (int8_t)d2;
-    q[5 * total + i] = (int8_t)d3;
+    q[total + i] = (int8_t)d0;
+    q[2 * total + i] = (int8_t)d1;
+    q[3 * total + i] = (int8_t)d2;
+    q[4 * total + i] = (int8_t)d3;
   }
 }
 
@@ -197,9 +196,10 @@ __global__ void __launch_bounds__(THREADS, 1)
               const int *__restrict__ ex, double *__restrict__ y, int64_t batch, int n) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t *full = (uint64_t *)(smem + NSLOT * SLOT);
+  uint64_t *full = (uint64_t *)(smem + NSLOT * SLOT);  // leader: both CTAs' slot s complete
   uint64_t *empty = full + NSLOT;
-  uint64_t *tfull = empty + NSLOT;
+  uint64_t *lfull = empty + NSLOT;                       // this CTA's TMA bytes of slot s landed
+  uint64_t *tfull = lfull + NSLOT;
   uint64_t *tempty = tfull + 1;
   uint32_t *tmem_holder = (uint32_t *)(tempty + 1);
 
@@ -216,8 +216,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSLOT; ++s) {
-      sa_mbar_init(&full[s], 1);
+      sa_mbar_init(&full[s], 2 * 2);  // the two scaler warps of both CTAs
       sa_mbar_init(&empty[s], 1);
+      sa_mbar_init(&lfull[s], 1);
     }
     sa_mbar_init(tfull, 1);
     sa_mbar_init(tempty, 4 * 2);
@@ -250,12 +251,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int o0 = (int)(t % ot_count) * BN + (int)rank * (BN / 2);
         const int s = (int)(it % NSLOT);
         sa_mbar_wait(&empty[s], ((it / NSLOT) & 1) ^ 1);
-        const uint32_t b = sa_smem_u32(smem + s * SLOT);
-        if (rank == 0) sa_mbar_expect_tx(&full[s], 2 * SLOT);
+        unsigned char *b = smem + s * SLOT;
+        sa_mbar_expect_tx(&lfull[s], NMEM * (XT + WT));
 #pragma unroll
-        for (int p = 0; p < NPL; ++p) {
-          tma2(b + p * XT, &xmap, kc * KSL, (int)(p * xrows + v0), lead(&full[s]), xpol);
-          tma2(b + NPL * XT + p * WT, &wmap, kc * KSL, p * nk + o0, lead(&full[s]), wpol);
+        for (int p = 0; p < NMEM; ++p) {  // HBM plane p -> smem tile 0 (S) or p + 1 (digits)
+          const int t = p == 0 ? 0 : p + 1;
+          tma_hint(b + t * XT, &xmap, kc * KSL, (int)(p * xrows + v0), &lfull[s], xpol);
+          tma_hint(b + NPL * XT + t * WT, &wmap, kc * KSL, p * nk + o0, &lfull[s], wpol);
         }
       }
     }
@@ -290,6 +292,33 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         commit2(tfull);
       }
+    }
+  } else if (warp >= 6) {
+    // ---- scalers (warps 6-7): 127 S and 127 sW tiles from the S / sW tiles of each slot ----
+    // bytes are {-1, 0, 1}: 127 x = (x & 1) * 127, negated where the sign bit is set
+    const int st = threadIdx.x - 6 * 32;  // 0..63
+    for (int64_t it = 0; it < total; ++it) {
+      const int s = (int)(it % NSLOT);
+      sa_mbar_wait(&lfull[s], (it / NSLOT) & 1);
+      unsigned char *b = smem + s * SLOT;
+      auto scale_tile = [&](const unsigned char *src, unsigned char *dst, int bytes) {
+        for (int o = st * 16; o < bytes; o += 64 * 16) {
+          uint4 v = *(const uint4 *)(src + o);
+          uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t t = (w[i] & 0x01010101u) * 0x7Fu;  // 0x7F per nonzero byte (no carries)
+            const uint32_t ng = (w[i] >> 7) & 0x01010101u;       // 1 per negative byte
+            w[i] = (t ^ (ng * 0xFFu)) + ng;                        // per-byte two's complement where negative
+          }
+          *(uint4 *)(dst + o) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      };
+      scale_tile(b, b + XT, XT);
+      scale_tile(b + NPL * XT, b + NPL * XT + WT, WT);
+      sa_fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05.mma
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) arrive_cl(lead(&full[s]));
     }
   } else {
     // ---- epilogue (warps 2-5): TMEM lane quarter q -> vector row v, 128 outputs per tile ----
@@ -379,7 +408,7 @@ int encode_u8(CUtensorMap *map, const void *base, int64_t rows, int64_t cols, in
 
 bool sa_ndft_i8_supported(int dtype, int64_t n) { return dtype == SA_C128 && n >= 128 && n <= 2048 && n % 64 == 0; }
 
-int64_t sa_ndft_i8_wbytes(int64_t n) { return (int64_t)NPL * (2 * n) * (2 * n); }
+int64_t sa_ndft_i8_wbytes(int64_t n) { return (int64_t)NMEM * (2 * n) * (2 * n); }
 
 int sa_launch_ndft_i8(const void *x, void *y, int64_t batch, int64_t n, const SaTwiddles *tw_c, double gain,
                       cudaStream_t s) {
@@ -405,7 +434,7 @@ int sa_launch_ndft_i8(const void *x, void *y, int64_t batch, int64_t n, const Sa
     const auto key = std::make_tuple((const void *)tw->i8w, n);
     auto it = g_i8_wmaps.find(key);
     if (it == g_i8_wmaps.end()) {
-      int rc = encode_u8(&wmap, tw->i8w, (int64_t)NPL * 2 * n, 2 * n, BN / 2);
+      int rc = encode_u8(&wmap, tw->i8w, (int64_t)NMEM * 2 * n, 2 * n, BN / 2);
       if (rc) return rc;
       g_i8_wmaps.emplace(key, wmap);
     } else {
@@ -416,8 +445,11 @@ int sa_launch_ndft_i8(const void *x, void *y, int64_t batch, int64_t n, const Sa
   // x planes + exponents: stream-ordered scratch (the pool reuses it across calls)
   int8_t *planes = nullptr;
   int *ex = nullptr;
-  const size_t pbytes = (size_t)NPL * batch * 2 * n;
-  SA_CUDA_TRY(cudaMallocAsync((void **)&planes, pbytes + (size_t)batch * sizeof(int) + 256, s));
+  const size_t pbytes = (size_t)NMEM * batch * 2 * n;
+  {
+    const int rc_ = sa_scratch_alloc((void **)&planes, pbytes + (size_t)batch * sizeof(int) + 256, s);
+    if (rc_) return rc_;
+  }
   ex = (int *)(((uintptr_t)(planes + pbytes) + 255) & ~(uintptr_t)255);
   int dev = 0, sms = 148;
   SA_CUDA_TRY(cudaGetDevice(&dev));
@@ -425,7 +457,7 @@ int sa_launch_ndft_i8(const void *x, void *y, int64_t batch, int64_t n, const Sa
   const int pgrid = (int)(batch < 8LL * sms ? batch : 8LL * sms);
   k_i8_prep<<<pgrid, 256, 0, s>>>((const double *)x, planes, ex, batch, (int)n, gain, (int)(gain != 1.0));
   SA_LAUNCH_CHECK();
-  int rc = encode_u8(&xmap, planes, (int64_t)NPL * batch, 2 * n, BM);
+  int rc = encode_u8(&xmap, planes, (int64_t)NMEM * batch, 2 * n, BM);
   if (rc) return rc;
   static bool smem_set[64] = {};
   if (dev >= 64 || !smem_set[dev]) {

@@ -361,7 +361,10 @@ int launch(int variant, const void *xv, void *yv, int64_t batch, int64_t n, cons
     // pass 2 scatters rows to bit-reversed output columns, so it cannot run in
     // place: pass 1 writes a stream-ordered scratch, pass 2 reads it.
     C2<T> *scratch = nullptr;
-    SA_CUDA_TRY(cudaMallocAsync((void **)&scratch, sizeof(C2<T>) * (size_t)(batch * n), s));
+    {
+      const int rc_ = sa_scratch_alloc((void **)&scratch, sizeof(C2<T>) * (size_t)(batch * n), s);
+      if (rc_) return rc_;
+    }
     k_nlfft_cols<T, 1><<<(unsigned)grid_cols, 256, bytes_cols, s>>>(x, scratch, logn1, logn2, tc, stage,
                                                                     stage2, g, use_gain);
     k_nlfft_rows<T, 1><<<(unsigned)grid_rows, 256, bytes_rows, s>>>(scratch, y, logn1, logn2, tc, stage,

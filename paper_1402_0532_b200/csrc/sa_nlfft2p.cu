@@ -388,7 +388,10 @@ int launch2p(const void *x, void *y, int64_t batch, const SaTwiddles *tw, double
   const size_t ring_bytes = sizeof(typename P::C2) * (size_t)RING * S_CHUNK * NN;
   const size_t ctr_bytes = sizeof(int) * (size_t)(1 + batch + nchunks);
   void *ws = nullptr;
-  SA_CUDA_TRY(cudaMallocAsync(&ws, ring_bytes + ctr_bytes, s));
+  {
+    const int rc_ = sa_scratch_alloc((void **)&ws, ring_bytes + ctr_bytes, s);
+    if (rc_) return rc_;
+  }
   int *ctr = reinterpret_cast<int *>((char *)ws + ring_bytes);
   SA_CUDA_TRY(cudaMemsetAsync(ctr, 0, ctr_bytes, s));
   CUtensorMap mx, mr;

@@ -60,3 +60,35 @@ int sa_twiddles_build(SaTwiddles *tw, const double *host_table, cudaStream_t s) 
   SA_CUDA_TRY(cudaStreamSynchronize(s));
   return SA_OK;
 }
+
+// Stream-ordered scratch from a library-owned pool per device that keeps its
+// memory (release threshold = max): repeated calls reuse it with no driver
+// allocation (the default pool hands memory back at every synchronisation).
+#include <mutex>
+namespace {
+std::mutex g_pool_mutex;
+cudaMemPool_t g_pools[64] = {};
+}  // namespace
+
+int sa_scratch_alloc(void **p, size_t bytes, cudaStream_t s) {
+  int dev = 0;
+  SA_CUDA_TRY(cudaGetDevice(&dev));
+  cudaMemPool_t pool = nullptr;
+  {
+    std::lock_guard<std::mutex> g(g_pool_mutex);
+    if (dev < 64 && g_pools[dev]) {
+      pool = g_pools[dev];
+    } else {
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      SA_CUDA_TRY(cudaMemPoolCreate(&pool, &props));
+      uint64_t keep = ~0ull;
+      SA_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+      if (dev < 64) g_pools[dev] = pool;
+    }
+  }
+  SA_CUDA_TRY(cudaMallocFromPoolAsync(p, bytes, pool, s));
+  return SA_OK;
+}
