@@ -125,19 +125,31 @@ SA_HD int sgn_i(double v) { return v > 0.0 ? 1 : (v < 0.0 ? -1 : 0); }
 
 // x (batch x n complex128, gain applied) -> planes P[p][v][K] (p = S,
 // dx0..dx3; K = 2m + re/im) and the per-vector exponent e[v] (max|x_v| < 2^e).
+template <int IT>
 __global__ void __launch_bounds__(256) k_i8_prep(const double *__restrict__ x, int8_t *__restrict__ planes,
                                                  int *__restrict__ ex, int64_t batch, int n, double gain,
                                                  int use_gain) {
+  // one row per CTA iteration; thread t holds doubles [8 t + 2048 i, +8), i < IT, in
+  // registers (2n <= 2048 IT), so the row is read once and every plane store is 8 bytes
   __shared__ double red[8];
   const int nk = 2 * n;
   const size_t pstride = (size_t)batch * nk;
   for (int64_t v = blockIdx.x; v < batch; v += gridDim.x) {
     const double *row = x + v * nk;
+    double t[IT][8];
     double mx = 0.0;
-    for (int k = threadIdx.x * 2; k < nk; k += 512) {
-      double2 t = *(const double2 *)&row[k];
-      if (use_gain) t = {sa_mul(gain, t.x), sa_mul(gain, t.y)};
-      mx = fmax(mx, fmax(fabs(t.x), fabs(t.y)));
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+      const int k = threadIdx.x * 8 + 2048 * i;
+      if (k < nk) {
+#pragma unroll
+        for (int j = 0; j < 8; j += 2) {
+          double2 u = __ldcs((const double2 *)&row[k + j]);
+          t[i][j] = use_gain ? sa_mul(gain, u.x) : u.x;
+          t[i][j + 1] = use_gain ? sa_mul(gain, u.y) : u.y;
+          mx = fmax(mx, fmax(fabs(t[i][j]), fabs(t[i][j + 1])));
+        }
+      }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -151,21 +163,25 @@ __global__ void __launch_bounds__(256) k_i8_prep(const double *__restrict__ x, i
     if (mx > 0.0) frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1): max < 2^e
     if (threadIdx.x == 0) ex[v] = e;
     int8_t *p0 = planes + v * nk;
-    for (int k = threadIdx.x * 2; k < nk; k += 512) {
-      double2 t = *(const double2 *)&row[k];
-      if (use_gain) t = {sa_mul(gain, t.x), sa_mul(gain, t.y)};
-      int a0, a1, a2, a3, b0, b1, b2, b3;
-      digits(ldexp(t.x, -e), a0, a1, a2, a3);
-      digits(ldexp(t.y, -e), b0, b1, b2, b3);
-      const int sa = sgn_i(t.x), sb = sgn_i(t.y);
-      auto put = [&](int p, int lo, int hi) {
-        *(uint16_t *)&p0[p * pstride + k] = (uint16_t)((lo & 0xFF) | ((hi & 0xFF) << 8));
-      };
-      put(0, sa, sb);
-      put(1, a0, b0);
-      put(2, a1, b1);
-      put(3, a2, b2);
-      put(4, a3, b3);
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+      const int k = threadIdx.x * 8 + 2048 * i;
+      if (k < nk) {
+        uint64_t w[NMEM] = {};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          int d0, d1, d2, d3;
+          digits(ldexp(t[i][j], -e), d0, d1, d2, d3);
+          const int sh = 8 * j;
+          w[0] |= (uint64_t)(uint8_t)sgn_i(t[i][j]) << sh;
+          w[1] |= (uint64_t)(uint8_t)d0 << sh;
+          w[2] |= (uint64_t)(uint8_t)d1 << sh;
+          w[3] |= (uint64_t)(uint8_t)d2 << sh;
+          w[4] |= (uint64_t)(uint8_t)d3 << sh;
+        }
+#pragma unroll
+        for (int p = 0; p < NMEM; ++p) *(uint64_t *)&p0[p * pstride + k] = w[p];
+      }
     }
   }
 }
@@ -406,7 +422,7 @@ int encode_u8(CUtensorMap *map, const void *base, int64_t rows, int64_t cols, in
 
 }  // namespace
 
-bool sa_ndft_i8_supported(int dtype, int64_t n) { return dtype == SA_C128 && n >= 128 && n <= 2048 && n % 64 == 0; }
+bool sa_ndft_i8_supported(int dtype, int64_t n) { return dtype == SA_C128 && n >= 128 && n <= 2048 && n % 64 == 0; }  // 2n <= 2 x 2048 (k_i8_prep)
 
 int64_t sa_ndft_i8_wbytes(int64_t n) { return (int64_t)NMEM * (2 * n) * (2 * n); }
 
@@ -455,7 +471,8 @@ int sa_launch_ndft_i8(const void *x, void *y, int64_t batch, int64_t n, const Sa
   SA_CUDA_TRY(cudaGetDevice(&dev));
   SA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int pgrid = (int)(batch < 8LL * sms ? batch : 8LL * sms);
-  k_i8_prep<<<pgrid, 256, 0, s>>>((const double *)x, planes, ex, batch, (int)n, gain, (int)(gain != 1.0));
+  auto prep = n <= 1024 ? k_i8_prep<1> : k_i8_prep<2>;  // n <= 2048
+  prep<<<pgrid, 256, 0, s>>>((const double *)x, planes, ex, batch, (int)n, gain, (int)(gain != 1.0));
   SA_LAUNCH_CHECK();
   int rc = encode_u8(&xmap, planes, (int64_t)NMEM * batch, 2 * n, BM);
   if (rc) return rc;
