@@ -20,14 +20,18 @@
 // the fp64 bound 1e-9 holds from n = 128 up; measured max|Δ|/‖y‖₁ ~1e-11 on C2
 // (tests/test_gpu_ndft_i8.py).  Smaller n runs the DFMA fast kernel.
 //
-// Pipeline: k_i8_prep (one pass over x: gain, per-vector exponent, six int8
-// planes S, 127 S, dx0..dx3, row-major [v][K]) -> k_ndft_i8 (persistent CTA
-// pairs, cluster 2, tcgen05.mma.cta_group::2.kind::i8, M = 256 vectors, N = 128
-// outputs, K = 32; the four accumulators fill TMEM's 512 columns).  Both operand
-// sets arrive by TMA (SWIZZLE_64B, 64 K per slot, three 72 KB slots per CTA):
-// the six W planes (sW, 127 sW, dW0..dW3: 6 (2n)^2 bytes, built once per twiddle
-// set, L2 evict_last) and the six x planes.  Warp 0 produces, warp 1 issues
-// (leader CTA), warps 2-5 drain TMEM into complex128 rows of y.
+// Pipeline: k_i8_prep (one pass over x: gain, per-vector exponent, the six int8
+// planes S, 127 S, dx0..dx3) -> k_ndft_i8 (persistent CTA pairs, cluster 2,
+// tcgen05.mma.cta_group::2.kind::i8, M = 256 vectors, N = 128 outputs, K = 32;
+// the four accumulators fill TMEM's 512 columns).  Both operand sets are stored
+// in HBM as "smem images": for each 128-vector block (or 64-output block) and
+// 64-K slot the six planes' tiles are contiguous and already SWIZZLE_64B-permuted,
+// so one bulk copy per side (48 KB of x planes, 24 KB of W planes: sW, 127 sW,
+// dW0..dW3, built once per twiddle set) fills a slot -- 128-B requests instead of
+// the 64-B rows a 2-D TMA box would issue (the request rate bounded the first
+// version: 2.48 ms with the MMAs skipped or not).  Three 72 KB slots per CTA.
+// Warp 0 produces, warp 6 relays each CTA's slot completion to the leader, warp
+// 1 issues the MMAs (leader CTA), warps 2-5 drain TMEM into complex128 rows of y.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -43,14 +47,13 @@ namespace {
 constexpr int BM = 128;               // vectors per CTA (TMEM lanes); M = 256 per pair
 constexpr int BN = 128;               // outputs per tile (each accumulator: 128 TMEM columns)
 constexpr int KSL = 64;               // int8 K elements per slot (64-B rows, SWIZZLE_64B)
-constexpr int NPL = 6;                // smem tiles per operand side: S, 127 S, four digits
-constexpr int NMEM = 5;               // planes per side in HBM: 127 S is made in smem from S
+constexpr int NPL = 6;                // planes per operand side: S, 127 S, four digits
 constexpr int XT = BM * KSL;          // one x-plane tile per CTA: 8 KB
 constexpr int WT = (BN / 2) * KSL;    // one W-plane tile per CTA (half the outputs): 4 KB
 constexpr int SLOT = NPL * XT + NPL * WT;  // 72 KB
 constexpr int NSLOT = 3;
 constexpr int SMEM = NSLOT * SLOT + 1024 + 256;
-constexpr int THREADS = 8 * 32;       // producer, MMA, 4 epilogue, 2 scaler warps
+constexpr int THREADS = 7 * 32;       // producer, MMA, 4 epilogue warps, relay
 constexpr int TMEM_COLS = 512;
 // kind::i8: D = s32 (2), A = B = s8 (1), K-major, N = 128, M = 256
 constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
@@ -58,6 +61,15 @@ constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >
 SA_HD uint64_t sdesc(uint32_t saddr) {  // K-major SWIZZLE_64B: 64-B rows, 8-row atoms 512 B apart
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+}
+// byte offset of (row r, K byte b) inside a SWIZZLE_64B tile of 64-B rows
+SA_HD uint32_t sw64(int r, int b) { return (uint32_t)(r * 64 + ((((b >> 4) ^ (r >> 1)) & 3) << 4) + (b & 15)); }
+SA_HD void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          sa_smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(sa_smem_u32(bar)), "l"(pol)
+      : "memory");
 }
 SA_HD void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 SA_HD void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -69,6 +81,9 @@ SA_HD void commit2(uint64_t *bar) {
       : "memory");
 }
 SA_HD void mma2(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+#ifdef SA_I8_PROBE_NOMMA
+  return;
+#endif
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
       " tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
@@ -76,13 +91,6 @@ SA_HD void mma2(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
       : "memory");
 }
 SA_HD void arrive_cl(uint32_t cl_addr) { asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory"); }
-SA_HD void tma_hint(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar, uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(sa_smem_u32(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(sa_smem_u32(bar)), "l"(pol)
-      : "memory");
-}
 SA_HD uint64_t policy(bool keep) {
   uint64_t p;
   if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -123,8 +131,9 @@ SA_HD void digits(double v, int &d0, int &d1, int &d2, int &d3) {
 }
 SA_HD int sgn_i(double v) { return v > 0.0 ? 1 : (v < 0.0 ? -1 : 0); }
 
-// x (batch x n complex128, gain applied) -> planes P[p][v][K] (p = S,
-// dx0..dx3; K = 2m + re/im) and the per-vector exponent e[v] (max|x_v| < 2^e).
+// x (batch x n complex128, gain applied) -> the six planes (S, 127 S, dx0..dx3; K =
+// 2m + re/im) as smem images: block (v / 128, K slot kc) holds the six 8 KB
+// tiles of rows v % 128, SWIZZLE_64B-permuted; e[v] = per-vector exponent (max|x_v| < 2^e).
 template <int IT>
 __global__ void __launch_bounds__(256) k_i8_prep(const double *__restrict__ x, int8_t *__restrict__ planes,
                                                  int *__restrict__ ex, int64_t batch, int n, double gain,
@@ -133,7 +142,7 @@ __global__ void __launch_bounds__(256) k_i8_prep(const double *__restrict__ x, i
   // registers (2n <= 2048 IT), so the row is read once and every plane store is 8 bytes
   __shared__ double red[8];
   const int nk = 2 * n;
-  const size_t pstride = (size_t)batch * nk;
+  const int kslots = nk / KSL;
   for (int64_t v = blockIdx.x; v < batch; v += gridDim.x) {
     const double *row = x + v * nk;
     double t[IT][8];
@@ -162,25 +171,28 @@ __global__ void __launch_bounds__(256) k_i8_prep(const double *__restrict__ x, i
     int e = 0;
     if (mx > 0.0) frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1): max < 2^e
     if (threadIdx.x == 0) ex[v] = e;
-    int8_t *p0 = planes + v * nk;
+    int8_t *blk = planes + (size_t)(v / BM) * kslots * (NPL * XT);
+    const int r = (int)(v % BM);
 #pragma unroll
     for (int i = 0; i < IT; ++i) {
       const int k = threadIdx.x * 8 + 2048 * i;
       if (k < nk) {
-        uint64_t w[NMEM] = {};
+        uint64_t w[6] = {};
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           int d0, d1, d2, d3;
           digits(ldexp(t[i][j], -e), d0, d1, d2, d3);
-          const int sh = 8 * j;
-          w[0] |= (uint64_t)(uint8_t)sgn_i(t[i][j]) << sh;
-          w[1] |= (uint64_t)(uint8_t)d0 << sh;
-          w[2] |= (uint64_t)(uint8_t)d1 << sh;
-          w[3] |= (uint64_t)(uint8_t)d2 << sh;
-          w[4] |= (uint64_t)(uint8_t)d3 << sh;
+          const int sh = 8 * j, sg = sgn_i(t[i][j]);
+          w[0] |= (uint64_t)(uint8_t)sg << sh;
+          w[1] |= (uint64_t)(uint8_t)(127 * sg) << sh;
+          w[2] |= (uint64_t)(uint8_t)d0 << sh;
+          w[3] |= (uint64_t)(uint8_t)d1 << sh;
+          w[4] |= (uint64_t)(uint8_t)d2 << sh;
+          w[5] |= (uint64_t)(uint8_t)d3 << sh;
         }
+        int8_t *tile = blk + (size_t)(k / KSL) * (NPL * XT) + sw64(r, k % KSL);  // 8 bytes, one swizzle chunk
 #pragma unroll
-        for (int p = 0; p < NMEM; ++p) *(uint64_t *)&p0[p * pstride + k] = w[p];
+        for (int p = 0; p < NPL; ++p) *(uint64_t *)(tile + p * XT) = w[p];
       }
     }
   }
@@ -189,7 +201,9 @@ __global__ void __launch_bounds__(256) k_i8_prep(const double *__restrict__ x, i
 // W planes Q[p][o][K] (p = sW, dW0..dW3) of Wv = [[Wr, -Wi], [Wi, Wr]],
 // W = raw[(k m) mod n] (the fp64 reference table, transforms.py:108-146).
 __global__ void k_i8_wbuild(const double2 *__restrict__ raw, int n, int8_t *__restrict__ q) {
+  // smem images: block (o / 64, K slot kc) holds the six 4 KB tiles of rows o % 64
   const int64_t nn = 2LL * n, total = nn * nn;
+  const int kslots = (int)(nn / KSL);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t o = i / nn, kk = i % nn;
     const int64_t k = o >> 1, m = kk >> 1;
@@ -198,18 +212,17 @@ __global__ void k_i8_wbuild(const double2 *__restrict__ raw, int n, int8_t *__re
     const double val = co == ci ? tw.x : (co == 0 ? -tw.y : tw.y);
     int d0, d1, d2, d3;
     digits(val, d0, d1, d2, d3);
-    const int s = sgn_i(val);
-    q[i] = (int8_t)s;
-    q[total + i] = (int8_t)d0;
-    q[2 * total + i] = (int8_t)d1;
-    q[3 * total + i] = (int8_t)d2;
-    q[4 * total + i] = (int8_t)d3;
+    const int sg = sgn_i(val);
+    const int8_t v[NPL] = {(int8_t)sg, (int8_t)(127 * sg), (int8_t)d0, (int8_t)d1, (int8_t)d2, (int8_t)d3};
+    int8_t *tile = q + ((o / (BN / 2)) * kslots + kk / KSL) * (NPL * WT) + sw64((int)(o % (BN / 2)), (int)(kk % KSL));
+#pragma unroll
+    for (int p = 0; p < NPL; ++p) tile[p * WT] = v[p];
   }
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
-    k_ndft_i8(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap wmap,
-              const int *__restrict__ ex, double *__restrict__ y, int64_t batch, int n) {
+    k_ndft_i8(const int8_t *__restrict__ xblk, const int8_t *__restrict__ wblk, const int *__restrict__ ex,
+              double *__restrict__ y, int64_t batch, int n) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t *full = (uint64_t *)(smem + NSLOT * SLOT);  // leader: both CTAs' slot s complete
@@ -227,12 +240,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int64_t vt_count = (batch + 2 * BM - 1) / (2 * BM);
   const int64_t ntiles = vt_count * ot_count;
   const int kslots = nk / KSL;
-  const int64_t xrows = batch;  // rows per x plane in the stacked x-plane tensor
   auto lead = [&](uint64_t *bar) { return sa_mapa(sa_smem_u32(bar), 0); };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSLOT; ++s) {
-      sa_mbar_init(&full[s], 2 * 2);  // the two scaler warps of both CTAs
+      sa_mbar_init(&full[s], 2);  // the relays of both CTAs
       sa_mbar_init(&empty[s], 1);
       sa_mbar_init(&lfull[s], 1);
     }
@@ -254,29 +266,31 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int64_t total = my_tiles * kslots;
 
   if (warp == 0) {
-    // ---- TMA producer: this CTA's 128 vector rows of the 6 x planes, its 64 output rows of the 6 W planes ----
+    // ---- producer: one bulk copy per side per slot (this CTA's 128 vectors / 64 outputs) ----
     if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(&xmap) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(&wmap) : "memory");
       const uint64_t wpol = policy(true), xpol = policy(false);
       for (int64_t it = 0; it < total; ++it) {
         const int64_t lt = it / kslots;
         const int kc = (int)(it - lt * kslots);
         const int64_t t = cl + lt * ncl;
-        const int64_t v0 = (t / ot_count) * (2 * BM) + rank * BM;
-        const int o0 = (int)(t % ot_count) * BN + (int)rank * (BN / 2);
+        const int64_t vb = (t / ot_count) * 2 + rank;            // 128-vector block
+        const int64_t ob = (t % ot_count) * 2 + rank;            // 64-output block
         const int s = (int)(it % NSLOT);
         sa_mbar_wait(&empty[s], ((it / NSLOT) & 1) ^ 1);
         unsigned char *b = smem + s * SLOT;
-        sa_mbar_expect_tx(&lfull[s], NMEM * (XT + WT));
-#pragma unroll
-        for (int p = 0; p < NMEM; ++p) {  // HBM plane p -> smem tile 0 (S) or p + 1 (digits)
-          const int t = p == 0 ? 0 : p + 1;
-          tma_hint(b + t * XT, &xmap, kc * KSL, (int)(p * xrows + v0), &lfull[s], xpol);
-          tma_hint(b + NPL * XT + t * WT, &wmap, kc * KSL, p * nk + o0, &lfull[s], wpol);
-        }
+        sa_mbar_expect_tx(&lfull[s], SLOT);
+        bulk_g2s(b, xblk + (vb * kslots + kc) * (NPL * XT), NPL * XT, &lfull[s], xpol);
+        bulk_g2s(b + NPL * XT, wblk + (ob * kslots + kc) * (NPL * WT), NPL * WT, &lfull[s], wpol);
       }
     }
+  } else if (warp == 6) {
+    // ---- relay: this CTA's slot landed -> arrive on the leader's full barrier ----
+    if (lane == 0)
+      for (int64_t it = 0; it < total; ++it) {
+        const int s = (int)(it % NSLOT);
+        sa_mbar_wait(&lfull[s], (it / NSLOT) & 1);
+        arrive_cl(lead(&full[s]));
+      }
   } else if (warp == 1) {
     // ---- MMA issuer (leader CTA): 8 MMAs per K step of 32 into the four accumulators ----
     if (lane == 0 && rank == 0) {
@@ -309,33 +323,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         commit2(tfull);
       }
     }
-  } else if (warp >= 6) {
-    // ---- scalers (warps 6-7): 127 S and 127 sW tiles from the S / sW tiles of each slot ----
-    // bytes are {-1, 0, 1}: 127 x = (x & 1) * 127, negated where the sign bit is set
-    const int st = threadIdx.x - 6 * 32;  // 0..63
-    for (int64_t it = 0; it < total; ++it) {
-      const int s = (int)(it % NSLOT);
-      sa_mbar_wait(&lfull[s], (it / NSLOT) & 1);
-      unsigned char *b = smem + s * SLOT;
-      auto scale_tile = [&](const unsigned char *src, unsigned char *dst, int bytes) {
-        for (int o = st * 16; o < bytes; o += 64 * 16) {
-          uint4 v = *(const uint4 *)(src + o);
-          uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const uint32_t t = (w[i] & 0x01010101u) * 0x7Fu;  // 0x7F per nonzero byte (no carries)
-            const uint32_t ng = (w[i] >> 7) & 0x01010101u;       // 1 per negative byte
-            w[i] = (t ^ (ng * 0xFFu)) + ng;                        // per-byte two's complement where negative
-          }
-          *(uint4 *)(dst + o) = make_uint4(w[0], w[1], w[2], w[3]);
-        }
-      };
-      scale_tile(b, b + XT, XT);
-      scale_tile(b + NPL * XT, b + NPL * XT + WT, WT);
-      sa_fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05.mma
-      __syncwarp();
-      if ((threadIdx.x & 31) == 0) arrive_cl(lead(&full[s]));
-    }
   } else {
     // ---- epilogue (warps 2-5): TMEM lane quarter q -> vector row v, 128 outputs per tile ----
     const int q = warp & 3;
@@ -348,6 +335,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       fence_after();
       const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16);
       double *dst = y + v * nk + o0;
+#ifdef SA_I8_PROBE_NOEPI
+      if (v < 0)
+#endif
 #pragma unroll 1
       for (int c = 0; c < BN; c += 16) {
         uint32_t wh[16], wl[16], xh[16], xl[16];
@@ -362,10 +352,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             double d[2];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              constexpr double C1 = 1.0 / (64.0 * 127.0), C2 = C1 / (128.0 * 127.0);
-              const double w = sa_fma((double)(int)wh[j + h], C1, sa_mul((double)(int)wl[j + h], C2));
-              const double xs = sa_fma((double)(int)xh[j + h], C1, sa_mul((double)(int)xl[j + h], C2));
-              d[h] = sa_add(ldexp(xs, e), w);
+              // pair digits in int64 (exact), then one conversion and one scaling each
+              constexpr double C2 = 1.0 / (64.0 * 127.0 * 128.0 * 127.0);
+              const long long W = (long long)(int)wh[j + h] * (128 * 127) + (int)wl[j + h];
+              const long long X = (long long)(int)xh[j + h] * (128 * 127) + (int)xl[j + h];
+              d[h] = sa_add(ldexp(sa_mul((double)X, C2), e), sa_mul((double)W, C2));
             }
             __stcs((double2 *)&dst[c + j], make_double2(d[0], d[1]));
           }
@@ -386,45 +377,14 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 std::mutex g_i8_mutex;
-std::map<std::tuple<const void *, int64_t>, CUtensorMap> g_i8_wmaps;
-
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn_i8() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void *p = nullptr;
-    cudaDriverEntryPointQueryResult qr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
-        qr == cudaDriverEntryPointSuccess)
-      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
-  }
-  return fn;
-}
-
-int encode_u8(CUtensorMap *map, const void *base, int64_t rows, int64_t cols, int box_rows) {
-  auto enc = encode_fn_i8();
-  if (!enc) {
-    sa_set_error("cuTensorMapEncodeTiled unavailable");
-    return SA_ERR_CUDA;
-  }
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols};
-  cuuint32_t box[2] = {(cuuint32_t)KSL, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    sa_set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
-    return SA_ERR_CUDA;
-  }
-  return SA_OK;
-}
 
 }  // namespace
 
-bool sa_ndft_i8_supported(int dtype, int64_t n) { return dtype == SA_C128 && n >= 128 && n <= 2048 && n % 64 == 0; }  // 2n <= 2 x 2048 (k_i8_prep)
+bool sa_ndft_i8_supported(int dtype, int64_t n) {
+  return dtype == SA_C128 && n >= 128 && n <= 2048 && n % 64 == 0;  // 2n <= 2 x 2048 (k_i8_prep)
+}
 
-int64_t sa_ndft_i8_wbytes(int64_t n) { return (int64_t)NMEM * (2 * n) * (2 * n); }
+int64_t sa_ndft_i8_wbytes(int64_t n) { return (int64_t)NPL * (2 * n) * (2 * n); }
 
 int sa_launch_ndft_i8(const void *x, void *y, int64_t batch, int64_t n, const SaTwiddles *tw_c, double gain,
                       cudaStream_t s) {
@@ -432,7 +392,6 @@ int sa_launch_ndft_i8(const void *x, void *y, int64_t batch, int64_t n, const Sa
   if (((uintptr_t)x | (uintptr_t)y) & 15) return SA_ERR_UNSUPPORTED;
   if (batch == 0) return SA_OK;
   SaTwiddles *tw = const_cast<SaTwiddles *>(tw_c);
-  CUtensorMap wmap, xmap;
   {
     // W planes built once per twiddle set, stream-ordered (event for later streams)
     std::lock_guard<std::mutex> g(g_i8_mutex);
@@ -447,41 +406,30 @@ int sa_launch_ndft_i8(const void *x, void *y, int64_t batch, int64_t n, const Sa
       tw->i8w = w;
       tw->i8w_ready = ev;
     }
-    const auto key = std::make_tuple((const void *)tw->i8w, n);
-    auto it = g_i8_wmaps.find(key);
-    if (it == g_i8_wmaps.end()) {
-      int rc = encode_u8(&wmap, tw->i8w, (int64_t)NMEM * 2 * n, 2 * n, BN / 2);
-      if (rc) return rc;
-      g_i8_wmaps.emplace(key, wmap);
-    } else {
-      wmap = it->second;
-    }
   }
   if (tw->i8w_ready) SA_CUDA_TRY(cudaStreamWaitEvent(s, (cudaEvent_t)tw->i8w_ready, 0));
-  // x planes + exponents: stream-ordered scratch (the pool reuses it across calls)
+  // x planes (whole 256-vector tiles: rows past the batch are never stored) + exponents
+  const int64_t rows = (batch + 2 * BM - 1) / (2 * BM) * (2 * BM);
+  const size_t pbytes = (size_t)NPL * rows * 2 * n;
   int8_t *planes = nullptr;
-  int *ex = nullptr;
-  const size_t pbytes = (size_t)NMEM * batch * 2 * n;
   {
     const int rc_ = sa_scratch_alloc((void **)&planes, pbytes + (size_t)batch * sizeof(int) + 256, s);
     if (rc_) return rc_;
   }
-  ex = (int *)(((uintptr_t)(planes + pbytes) + 255) & ~(uintptr_t)255);
+  int *ex = (int *)(((uintptr_t)(planes + pbytes) + 255) & ~(uintptr_t)255);
   int dev = 0, sms = 148;
   SA_CUDA_TRY(cudaGetDevice(&dev));
   SA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int pgrid = (int)(batch < 8LL * sms ? batch : 8LL * sms);
-  auto prep = n <= 1024 ? k_i8_prep<1> : k_i8_prep<2>;  // n <= 2048
+  auto prep = n <= 1024 ? k_i8_prep<1> : k_i8_prep<2>;
   prep<<<pgrid, 256, 0, s>>>((const double *)x, planes, ex, batch, (int)n, gain, (int)(gain != 1.0));
   SA_LAUNCH_CHECK();
-  int rc = encode_u8(&xmap, planes, (int64_t)NMEM * batch, 2 * n, BM);
-  if (rc) return rc;
   static bool smem_set[64] = {};
   if (dev >= 64 || !smem_set[dev]) {
     SA_CUDA_TRY(cudaFuncSetAttribute(k_ndft_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
     if (dev < 64) smem_set[dev] = true;
   }
-  const int64_t ntiles = ((batch + 2 * BM - 1) / (2 * BM)) * ((2 * n) / BN);
+  const int64_t ntiles = (rows / (2 * BM)) * ((2 * n) / BN);
   const int64_t units = ntiles < sms / 2 ? ntiles : sms / 2;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(units * 2));
@@ -495,7 +443,8 @@ int sa_launch_ndft_i8(const void *x, void *y, int64_t batch, int64_t n, const Sa
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  SA_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_ndft_i8, xmap, wmap, (const int *)ex, (double *)y, batch, (int)n));
+  SA_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_ndft_i8, (const int8_t *)planes, (const int8_t *)tw->i8w, (const int *)ex,
+                                 (double *)y, batch, (int)n));
   SA_LAUNCH_CHECK();
   SA_CUDA_TRY(cudaFreeAsync(planes, s));
   return SA_OK;
