@@ -53,7 +53,12 @@ constexpr int WT = (BN / 2) * KSL;    // one W-plane tile per CTA (half the outp
 constexpr int SLOT = NPL * XT + NPL * WT;  // 72 KB
 constexpr int NSLOT = 3;
 constexpr int SMEM = NSLOT * SLOT + 1024 + 256;
-constexpr int THREADS = 7 * 32;       // producer, MMA, 4 epilogue warps, relay
+#ifndef SA_I8_EPI_WARPS
+#define SA_I8_EPI_WARPS 8
+#endif
+constexpr int EPI = SA_I8_EPI_WARPS;  // epilogue warps: EPI / 4 per TMEM lane quarter, each a column share
+constexpr int RELAY_WARP = 2 + EPI;
+constexpr int THREADS = (3 + EPI) * 32;  // producer, MMA, epilogue warps, relay
 constexpr int TMEM_COLS = 512;
 // kind::i8: D = s32 (2), A = B = s8 (1), K-major, N = 128, M = 256
 constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
@@ -249,7 +254,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       sa_mbar_init(&lfull[s], 1);
     }
     sa_mbar_init(tfull, 1);
-    sa_mbar_init(tempty, 4 * 2);
+    sa_mbar_init(tempty, EPI * 2);
     sa_fence_mbar_init();
   }
   if (warp == 1) {
@@ -283,7 +288,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         bulk_g2s(b + NPL * XT, wblk + (ob * kslots + kc) * (NPL * WT), NPL * WT, &lfull[s], wpol);
       }
     }
-  } else if (warp == 6) {
+  } else if (warp == RELAY_WARP) {
     // ---- relay: this CTA's slot landed -> arrive on the leader's full barrier ----
     if (lane == 0)
       for (int64_t it = 0; it < total; ++it) {
@@ -324,8 +329,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else {
-    // ---- epilogue (warps 2-5): TMEM lane quarter q -> vector row v, 128 outputs per tile ----
+    // ---- epilogue (warps 2 .. 2 + EPI - 1): TMEM lane quarter q -> vector row v, a share of the 128 outputs ----
     const int q = warp & 3;
+    const int cs = (warp - 2) / 4;  // this warp's column share
+    constexpr int CW = BN / (EPI / 4);
     uint32_t lt = 0;
     for (int64_t t = cl; t < ntiles; t += ncl, ++lt) {
       const int64_t v = (t / ot_count) * (2 * BM) + rank * BM + q * 32 + lane;
@@ -339,7 +346,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (v < 0)
 #endif
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
+      for (int c = cs * CW; c < (cs + 1) * CW; c += 16) {
         uint32_t wh[16], wl[16], xh[16], xl[16];
         SA_LD16(wh, ta + c);
         SA_LD16(wl, ta + 128 + c);
