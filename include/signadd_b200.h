@@ -177,6 +177,19 @@ int sa_ambiguity_integrate_blocks(int dtype, const void *surv, const void *ref, 
 int sa_doppler_nlfft_blocked(int dtype, const void *zb, void *out, int64_t l_count, int64_t m, const void *tw,
                              double gain, void *stream);
 
+/* Host-side writers (§8(f)-4; cli.py:74-116).  sa_format_surface_csv formats
+ * a rows x cols dB map (row-major doubles, the reference's
+ * AmbiguitySurface.magnitude_db) as the reference's surface CSV, byte for
+ * byte: "# manifest=<manifest>\nl,p,magnitude_db\n" and one "l,p,repr(db)"
+ * line per cell (cli.py:184-191 through _write_csv, floats as Python repr()),
+ * in nthreads host threads (<= 0: all).  *out is malloc'ed: free it with
+ * sa_free_host.  sa_format_float_repr writes repr(x) (cap >= 32); returns its
+ * length. */
+int sa_format_surface_csv(const double *db, int64_t rows, int64_t cols, const char *manifest, char **out,
+                          int64_t *out_len, int nthreads);
+int sa_format_float_repr(double x, char *out, int cap);
+void sa_free_host(void *p);
+
 /* Workspace bytes for sa_map_peaks. */
 int sa_peaks_workspace_bytes(int64_t rows, int64_t cols, int k, int64_t *bytes);
 

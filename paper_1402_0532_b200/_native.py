@@ -48,6 +48,10 @@ SIGNATURES = {
     "sa_ambiguity_integrate_v": (_I, [_I, _I, _P, _P, _I64, _I64, _I64, _I64, _I64, _I, _I, _P, _P]),
     "sa_ambiguity_integrate_blocks": (_I, [_I, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I, _P, _I64, _P]),
     "sa_doppler_nlfft_blocked": (_I, [_I, _P, _P, _I64, _I64, _P, ctypes.c_double, _P]),
+    "sa_format_surface_csv": (_I, [_P, _I64, _I64, ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p),
+                                   ctypes.POINTER(ctypes.c_int64), _I]),
+    "sa_format_float_repr": (_I, [ctypes.c_double, ctypes.c_char_p, _I]),
+    "sa_free_host": (None, [_P]),
     "sa_peaks_workspace_bytes": (_I, [_I64, _I64, _I, ctypes.POINTER(_I64)]),
     "sa_map_peaks": (_I, [_I, _P, _I64, _I64, _I, _P, _P, _P, _P, _I64, _P]),
     "sa_map_floor": (_I, [_I, _P, _I64, _I64, _P, _I, _I, _I, _P, _P]),
