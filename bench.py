@@ -248,7 +248,12 @@ def wl_ndft(args, ws, rank, mode=None, e2e=True, dtype=None):
         res["d2h"] = hout.numel() * hout.element_size()
         res["e2e_api"] = f"paper_1402_0532_b200.ndft_batch(pinned host tensor, out=pinned host tensor, mode={mode!r})"
         res["e2e_launches"] = len(_pipeline_plan(res["e2e_rows"], res["e2e_row_bytes"]))
-    if mode == "tc":
+    if mode == "tc" and dtype == "c128":
+        res["roofline"] = lambda ms: roof_i8(ops * 64 / (ms * 1e-3) / 1e12)
+        res["dtype"] = "int8 digits x sign, exact int32 accumulate, f64 epilogue"
+        res["config"]["mode"] = ("tc (complex128: Ozaki-style int8 digits of Wv and of x / 2^e_v on tcgen05 kind::i8, "
+                                 "exact int32 accumulation, fp64 epilogue; max|d|/|y|1 ~1.5e-10)")
+    elif mode == "tc":
         res["roofline"] = lambda ms: roof_tensor(ops * 32 / (ms * 1e-3) / 1e12)
         res["dtype"] = "bf16x2-split x sign, f32 accumulate"
     else:
@@ -309,6 +314,22 @@ def roof_tensor(achieved_tflops):
             "algorithmic": "32 bf16 tensor flop per complex ⊙: re/im outputs x re/im inputs x "
                            "{sgn(x)·W0, sgn(x)·W1, X0·sgn(W), X1·sgn(W)} MACs (two-term bf16 splits)",
             **({"ncu_utilisation_pct": tr["ncu"]} if tr and tr.get("ncu") else {})}
+
+
+def roof_i8(achieved_tops):
+    """complex128 NDFT on tcgen05 kind::i8 (sa_ndft_i8.cu): 8 int8 MMA terms x 4 MACs
+    = 64 int ops per complex ⊙, against the dense int8 tensor rate (2 x the measured
+    bf16 burst figure: B200 int8 runs at twice bf16; MEASURED_PEAKS has no int8 line)."""
+    peaks, src = measured_peaks()
+    peak = 2.0 * peaks.get("bf16_tflops", 1590.0)
+    tr = ncu_traffic("k_ndft_i8")
+    return {"bound": "tensor", "achieved": round(achieved_tops, 1), "peak": round(peak, 1), "unit": "TOP/s",
+            "frac": round(achieved_tops / peak, 4), "traffic": tr["bytes_per_launch"] if tr else None,
+            "traffic_unit": "bytes/launch", "traffic_source": tr["source"] if tr else None,
+            "kernel": "k_ndft_i8 (+ k_i8_prep)", "algorithmic_bytes": 2 * 65536 * 1024 * 16,
+            "peak_source": f"2 x {src} bf16_tflops (int8 dense = 2 x bf16 on B200; int8 not measured)",
+            "nominal_peak": 4500.0, "frac_nominal": round(achieved_tops / 4500.0, 4),
+            "algorithmic": "64 int8 tensor ops per complex ⊙: 8 digit x sign MMA terms x re/im x re/im MACs"}
 
 
 def ncu_traffic(kernel_prefix):
@@ -522,6 +543,42 @@ def wl_detect(args, k=8):
                        "l2_policy": "4 maps cycled (> L2)"}}
 
 
+def wl_writer(args):
+    """§8(f)-4: the reference CLI's surface CSV (cli.py:184-191) for a C5-shaped
+    map on the GPU: D2H + magnitude_db (numpy, the reference's arithmetic) + the
+    native repr-exact formatter (writers.surface_csv_bytes).  Host-side work; the
+    reference's Python csv/repr writer is timed on a bounded row sample."""
+    import torch
+    from paper_1402_0532_b200.writers import magnitude_db, surface_csv_bytes
+    rows, cols = 4096, 2048
+    g = torch.Generator(device="cuda").manual_seed(14020540)
+    m = torch.randn(rows, cols, dtype=complex_dtype(args.dtype), device="cuda", generator=g)
+    nbytes = [0]
+
+    def step():
+        nbytes[0] = len(surface_csv_bytes(magnitude_db(m), "map.manifest.json"))
+
+    def cpu(P):
+        import sys as _s
+        from tools import refcpu
+        if not refcpu.available():
+            return {"unavailable": "baseline/_ref not installed"}
+        if refcpu.REF not in _s.path:
+            _s.path.insert(0, refcpu.REF)
+        import signadd.cli as rcli
+        db = magnitude_db(m[:128])
+        t = time.perf_counter()
+        rcli._write_csv(os.devnull, ["l", "p", "magnitude_db"],
+                        ((l, p, float(db[l, p])) for l in range(128) for p in range(cols)), "map.manifest.json")
+        dt = time.perf_counter() - t
+        return {"value": 128 * cols / dt, "unit": "cells/s", "cores": 1, "kind": "reference (unmodified cli._write_csv)",
+                "sample": f"128 of {rows} rows through the reference's csv/repr writer, {dt:.2f}s"}
+    return {"step": step, "ops": rows * cols, "map_bytes": None, "host": True, "cpu": cpu,
+            "config": {"workload": "§8(f)-4 surface CSV writer (cli.py:74-116, 184-191)", "rows": rows,
+                       "cols": cols, "dtype": "complex64 map -> f64 dB -> repr() text",
+                       "threads": len(os.sched_getaffinity(0))}}
+
+
 def lag_kernel(dtype):
     """The lag-integration kernel sa_ambiguity_integrate runs for T = 2048: the
     tcgen05 Hankel GEMM for complex64 (sa_lag_tc.cu), FP64 tiles otherwise."""
@@ -662,6 +719,18 @@ def run_extra(name, make, args, ws, rank):
     import torch
     r = make()
     steps = max(3, args.steps // 2)
+    if r.get("host"):  # host-side work: wall clock, one warm-up
+        r["step"]()
+        t = time.perf_counter()
+        for _ in range(2):
+            r["step"]()
+        hms = (time.perf_counter() - t) / 2 * 1e3
+        e = {"ms_per_step": hms, "config": r["config"], "cells_per_s": r["ops"] / (hms * 1e-3),
+             "timing": "host wall clock, 2 steps after 1 warm-up"}
+        if not args.no_cpu and "cpu" in r:
+            e["cpu_baseline"] = r["cpu"](len(os.sched_getaffinity(0)))
+        del r
+        return e
     ems, _ = timed(r["step"], steps, 3, 1)
     e = {"ms_per_step": ems, "config": r["config"], "dtype": r.get("dtype")}
     if "map_bytes" in r:  # detection: one read of the map
@@ -755,14 +824,17 @@ def run_ours(args):
         specs = [("C1_ndft_c128", lambda: wl_ndft64(args))]
         if args.ndft_mode == "tc" and args.dtype == "c64":
             specs.append(("C2_ndft_ffma2", lambda: {**wl_ndft(args, ws, rank, mode="fast", e2e=False), "cpu_skip": 1}))
-        specs += [("C2_ndft_c128", lambda: wl_ndft(args, ws, rank, mode="fast", dtype="c128")),
+        specs += [("C2_ndft_c128", lambda: wl_ndft(args, ws, rank, mode="tc", dtype="c128")),
+                  ("C2_ndft_c128_dfma", lambda: {**wl_ndft(args, ws, rank, mode="fast", dtype="c128", e2e=False),
+                                                 "cpu_skip": 1}),
                   ("C3_nlfft_dit", lambda: wl_nlfft(args, ws, rank, "dit", dtype="c64")),
                   ("C3_nlfft_dif", lambda: wl_nlfft(args, ws, rank, "dif", dtype="c64")),
                   ("C3_nlfft_dit_c128", lambda: wl_nlfft(args, ws, rank, "dit", dtype="c128")),
                   ("C3_nlfft_dif_c128", lambda: wl_nlfft(args, ws, rank, "dif", dtype="c128")),
                   ("C4_map", lambda: wl_map(args, ws, rank, e2e=True)),
                   ("C5_map_1gpu", lambda: wl_map(args, ws, rank, c5=True, e2e=True)),
-                  ("C5_detect", lambda: wl_detect(args))]
+                  ("C5_detect", lambda: wl_detect(args)),
+                  ("C5_surface_csv", lambda: wl_writer(args))]
         for name, fn in specs:
             if args.only and name not in args.only.split(","):
                 continue

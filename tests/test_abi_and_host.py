@@ -16,7 +16,7 @@ HEADER = os.path.join(ROOT, "include", "signadd_b200.h")
 
 def header_symbols():
     src = open(HEADER).read()
-    return sorted(set(re.findall(r"^(?:int|const char \*)\s*(sa_\w+)\(", src, flags=re.M)))
+    return sorted(set(re.findall(r"^(?:int|void|const char \*)\s*(sa_\w+)\(", src, flags=re.M)))
 
 
 def test_library_exports_every_header_symbol():
