@@ -83,6 +83,65 @@ __global__ void __launch_bounds__(TILE_THREADS) k_peaks_tile(const C2<T> *__rest
     cd = {(double)m, (long long)(r * cols + c)};
     return strict;
   };
+  if (sizeof(T) == 4 && k <= WARP_K) {
+    // complex64 maps, small k: integer keys (float magnitude bits << 32 | ~tile
+    // index) -- larger key = stronger, ties to the earlier cell -- so each warp
+    // argmax round is two redux.sync max (high word, then low word among the
+    // lanes holding the high maximum) instead of five 128-bit shuffle rounds.
+    using u64 = unsigned long long;
+    constexpr int PER_LANE = TILE * TILE_W / TILE_THREADS;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    u64 mine[PER_LANE];
+#pragma unroll
+    for (int j = 0; j < PER_LANE; ++j) {
+      const int e = warp * 32 * PER_LANE + lane + 32 * j;
+      Cand cd;
+      mine[j] = strict_at(e, cd) ? ((u64)__float_as_uint((float)cd.mag) << 32) | (0xFFFFFFFFu - (unsigned)e) : 0ull;
+    }
+    u64 *keys = reinterpret_cast<u64 *>(cand);  // 8 warps x WARP_K sorted winners
+    u64 *wl = keys + warp * WARP_K;
+    auto warp_max = [&](u64 b) {
+      const unsigned mh = __reduce_max_sync(0xffffffffu, (unsigned)(b >> 32));
+      const unsigned ml = __reduce_max_sync(0xffffffffu, (unsigned)(b >> 32) == mh ? (unsigned)b : 0u);
+      return ((u64)mh << 32) | ml;
+    };
+    int got = 0;
+    for (int rd = 0; rd < k; ++rd) {
+      u64 b = 0;
+#pragma unroll
+      for (int j = 0; j < PER_LANE; ++j) b = mine[j] > b ? mine[j] : b;
+      const u64 w = warp_max(b);
+      if (w == 0) break;  // warp exhausted (uniform)
+      if (lane == 0) wl[rd] = w;
+      ++got;
+#pragma unroll
+      for (int j = 0; j < PER_LANE; ++j)
+        if (mine[j] == w) mine[j] = 0;
+    }
+    for (int rd = got + lane; rd < k; rd += 32) wl[rd] = 0;
+    __syncthreads();
+    if (warp == 0) {  // k-way merge of the 8 sorted warp lists: lane w holds list w's head
+      constexpr int NW = TILE_THREADS / 32;
+      int pos = 0;
+      u64 h = lane < NW ? keys[lane * WARP_K] : 0ull;
+      int rd = 0;
+      for (; rd < k; ++rd) {
+        const u64 w = warp_max(h);
+        if (w == 0) break;
+        if (lane == 0) {
+          const int e = (int)(0xFFFFFFFFu - (unsigned)w);
+          o[rd] = {(double)__uint_as_float((unsigned)(w >> 32)),
+                   (long long)((r0 + e / TILE_W) * cols + c0 + e % TILE_W)};
+        }
+        if (lane < NW && h == w) {
+          ++pos;
+          h = pos < k ? keys[lane * WARP_K + pos] : 0ull;
+        }
+      }
+      for (int e = rd + lane; e < k; e += 32) o[e] = sentinel();
+    }
+    return;
+  }
   if (k <= WARP_K) {
     // Small k: each warp keeps the strict maxima of its 256 cells in registers
     // (8 per lane), extracts its own top k by k rounds of a warp argmax, and the
