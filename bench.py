@@ -108,15 +108,20 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- dist
-def dist_init():
+def dist_init(backend="nccl", share_gpu=False):
     import torch
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if share_gpu:  # test mode: every rank on cuda:0 (NCCL refuses duplicate GPUs: gloo)
+        local = 0
     if ws > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return ws, rank, local
@@ -133,7 +138,7 @@ def max_over_ranks(ws, v: float) -> float:
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -658,7 +663,16 @@ def wl_map(args, ws, rank, c5=False, e2e=False):
             ns, ns, l0, rows, M, 1, _native.SA_NDFT_FAST, _native.ptr(z), _native.stream_ptr()))
 
     ops = sa.map_complex_ops(L, ns, M)
+
+    def result():  # the map as delivered on rank 0 (None elsewhere)
+        step()
+        torch.cuda.synchronize()
+        if ws > 1:
+            return pm.full if pm is not None else full
+        return out
+
     res = {"ops": ops, "cells": L * M, "step": step, "lag_only": lag_only, "launches_per_step": 2,
+           "result": result, "surv": surv, "ref": ref,
            "config": {"workload": ("C5" if c5 else "C4") + " ⊙ range-Doppler map (BASELINE.json configs["
                       + ("4" if c5 else "3") + "])", "ns": ns, "delay_bins": L, "doppler_bins": M,
                       "block_T": ns // M, "doppler": "NL-FFT DIT", "dtype": str(cdt).replace("torch.", ""),
@@ -765,7 +779,7 @@ def run_extra(name, make, args, ws, rank):
 
 def run_ours(args):
     import torch
-    ws, rank, local = dist_init()
+    ws, rank, local = dist_init(args.dist_backend, args.share_gpu)
     import paper_1402_0532_b200 as sa
     sa.require_native()
     w = args.workload
@@ -796,6 +810,12 @@ def run_ours(args):
         line["ops_per_s"] = res["ops"] / (ms * 1e-3)
     if rank == 0 and "roofline" in res:
         line["roofline"] = res["roofline"](ms)
+    if args.check and w in ("map", "map5"):  # the delivered map vs a single-call map on this rank's GPU
+        full = res["result"]()
+        if rank == 0:
+            import paper_1402_0532_b200 as _sa
+            one = _sa.ambiguity_map(res["surv"], res["ref"], res["config"]["delay_bins"], res["config"]["doppler_bins"])
+            line["map_check"] = {"bit_identical": bool(torch.equal(full, one)), "rows": int(full.shape[0])}
     if w in ("map", "map5") and rank == 0:
         lms, _ = timed(res["lag_only"], args.steps, 3, 1)
         line["roofline"] = roof_lag(args.dtype, res["config"]["ns"], res["config"]["delay_bins"] // ws, lms)
@@ -954,6 +974,11 @@ def main():
     ap.add_argument("--no-numpy-ref", action="store_true",
                     help="skip the unmodified-numpy-reference Pool(P) figures (tools/refcpu.py)")
     ap.add_argument("--only", default="", help="comma-separated extra workloads to run (default: all)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo only for the shared-GPU test mode)")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="test mode: all ranks on cuda:0 (NCCL refuses duplicate GPUs; use --dist-backend gloo)")
+    ap.add_argument("--check", action="store_true", help="map workloads: compare the delivered map with a single call")
     ap.add_argument("--map-transport", default="p2p", choices=["p2p", "gather"],
                     help="N>1 map delivery: p2p = rows stored into rank 0's map over peer memory; "
                          "gather = delay-bin shards + NCCL gather (the north star's stated split)")
