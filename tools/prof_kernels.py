@@ -25,6 +25,13 @@ elif what == "map":
     r = torch.from_numpy(sc.ref).to(dt).cuda()
     for _ in range(reps):
         sa.ambiguity_map(s, r, 1024, 512)
+elif what == "map5":
+    from paper_1402_0532_b200.workloads import c5_scene
+    sc = c5_scene()
+    s = torch.from_numpy(sc.surv).to(dt).cuda()
+    r = torch.from_numpy(sc.ref).to(dt).cuda()
+    for _ in range(reps):
+        sa.ambiguity_map(s, r, 4096, 2048)
 elif what == "detect":
     g = torch.Generator(device="cuda").manual_seed(1)
     m = torch.randn(4096, 2048, dtype=dt, device="cuda", generator=g)
