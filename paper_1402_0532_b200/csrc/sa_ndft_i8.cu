@@ -30,8 +30,9 @@
 // dW0..dW3, built once per twiddle set) fills a slot -- 128-B requests instead of
 // the 64-B rows a 2-D TMA box would issue (the request rate bounded the first
 // version: 2.48 ms with the MMAs skipped or not).  Three 72 KB slots per CTA.
-// Warp 0 produces, warp 6 relays each CTA's slot completion to the leader, warp
-// 1 issues the MMAs (leader CTA), warps 2-5 drain TMEM into complex128 rows of y.
+// Warp 0 produces, warp 2 + EPI relays each CTA's slot completion to the leader,
+// warp 1 issues the MMAs (leader CTA), warps 2 .. 1 + EPI drain TMEM into
+// complex128 rows of y (EPI = 8: two warps per TMEM lane quarter, half the columns each).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 

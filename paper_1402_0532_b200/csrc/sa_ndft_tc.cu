@@ -15,7 +15,7 @@
 //   S·W0 + S·W1 + X0·sgn(Wv) + X1·sgn(Wv)
 // accumulate in fp32 in TMEM.  Error vs the fp64 oracle: ≤ 2^-17 relative per
 // term from the splits plus fp32 accumulation (tests: ≤ 1e-4 of ‖y‖₁, the
-// north-star fp32 bound; measured ~3e-8).  Multiplication-free in the ⊙ sense:
+// north-star fp32 bound; measured 8.2e-7 on C2).  Multiplication-free in the ⊙ sense:
 // one factor of every product is a sign.
 //
 // Kernel (persistent, 1 CTA per SM, 448 threads, CTA pairs: cluster of 2):

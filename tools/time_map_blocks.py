@@ -33,8 +33,12 @@ for G in (1, 2, 4, 8):
             _native.stream_ptr()))
     rows = shard_rows(L, G, 0)[1]
     out = torch.empty((rows, M), dtype=torch.complex64, device="cuda")
-    def nlfft():
-        sa.nfft_batch(zs[0], out=out)
+    from paper_1402_0532_b200.twiddle import device_twiddles
+    import ctypes
+    tw = device_twiddles(M, _native.SA_C64, 0)
+    def nlfft():  # the owner's Doppler NL-FFT on its blocked z rows (sa_doppler_nlfft_blocked)
+        _native.check(_native.lib().sa_doppler_nlfft_blocked(_native.SA_C64, _native.ptr(zs[0]), _native.ptr(out),
+                                                              rows, M, ctypes.c_void_p(tw), 1.0, _native.stream_ptr()))
     zl = torch.empty((rows, M), dtype=torch.complex64, device="cuda")
     def lag_rows():
         _native.check(_native.lib().sa_ambiguity_integrate(
