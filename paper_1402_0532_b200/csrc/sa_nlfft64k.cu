@@ -155,6 +155,9 @@ template <typename T> struct Pipe {
   // wait for an mbarrier phase: one warp of the thread group polls, the rest block
   // in the group's named barrier (no issue slots spent spinning)
   SA_HD void group_wait(uint64_t *bar, uint32_t parity) const {
+#ifdef SA_PROBE_NOSYNC  // timing probe only (wrong results): no cross-CTA storage waits
+    if (bar != &tma_bar[gi]) return;
+#endif
 #if SA_WAIT1
     if ((gt >> 5) == 0) sa_mbar_wait(bar, parity);
     group_sync(1 + gi, P::GT);
@@ -228,7 +231,11 @@ template <typename T> struct Pipe {
     for (int64_t sig = cid; sig < batch; sig += ncl, ++i) {
       const int b = (int)(i % P::NS);
       if (threadIdx.x == 0)
+#ifdef SA_PROBE_NOSCATTER
+        sa_mbar_arrive_local(&full_bar[b]);  // probe: no remote bytes expected
+#else
         sa_mbar_expect_tx(&full_bar[b], (uint32_t)(SA_LOCALQ ? P::INTER1 - P::INTER1 / P::CL : P::INTER1));
+#endif
       phaseA(sig, b, (uint32_t)(i / P::NS), sig + ncl);
       if (P::NS == 1) {
         phaseB(sig, 0, (uint32_t)i);
@@ -241,6 +248,9 @@ template <typename T> struct Pipe {
     }
     if (P::NS == 2 && i > 0)
       phaseB(cid + (i - 1) * ncl, (int)((i - 1) % P::NS), (uint32_t)((i - 1) / P::NS));
+#ifdef SA_PROBE_NOSYNC
+    cg::this_cluster().sync();  // the probe skips the storage waits: let peers' stores land first
+#endif
   }
 };
 
@@ -276,6 +286,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
           V x = A::from(wk[(crev4(k) * 16 + rg) * TC + m1_cc]);
           v[k] = use_gain ? A::scale(x, gain) : x;
         }
+#ifndef SA_PROBE_SKIP_A
 #pragma unroll
         for (int k = 0; k < 16; k += 2) r_two_point<T>(v[k], v[k + 1]);  // stage 1
 #pragma unroll
@@ -298,6 +309,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
           else if (k == 4) r_dit_mj<T>(v[k], v[k + 8]);
           else r_dit<T>(v[k], v[k + 8], twA[7 + k]);
         }
+#endif
       }
       group_sync(gbar, GT);
 #pragma unroll
@@ -310,6 +322,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
       group_sync(gbar, GT);  // tile buffer consumed: re-arm it
       if (u + 1 < TPG) pp.tma(&tmx, sig, tt + NG);
       else if (nsig < batch) pp.tma(&tmx, nsig, pp.gi);
+#ifndef SA_PROBE_SKIP_A
 #pragma unroll
       for (int t = 5; t <= 8; ++t) {
         const int hr = 1 << (t - 5), h = 1 << (t - 1);
@@ -317,6 +330,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
         for (int k = 0; k < 16; ++k)
           if (!(k & hr)) r_dit<T>(v[k], v[k + hr], twA[(h - 1) + m2_g + 16 * (k & (hr - 1))]);
       }
+#endif
       // scatter node row R = rev8(c): column q lives in CTA q / COLS
       if (u == 0) pp.group_wait(&pp.empty_bar[b], use & 1);  // peers released storage b
       const int R = rev8(pp.rank * COLS + tt * TC + m2_cc);
@@ -325,7 +339,11 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
       for (int k = 0; k < 16; ++k) {
         const int e = R * COLS + m2_g + 16 * (k % KPC);
         if (SA_LOCALQ && k / KPC == pp.rank) pp.inter(b)[e] = A::to(v[k]);
+#ifndef SA_PROBE_NOSCATTER
         else sa_st_async(pp.peer_inter(b, k / KPC, (uint32_t)(sizeof(C2) * e)), A::to(v[k]), pp.peer_full(b, k / KPC));
+#else
+        else pp.inter(b)[e] = A::to(v[k]);  // probe: local store instead of the DSMEM scatter
+#endif
       }
     }
     pp.local_done(b);
@@ -345,10 +363,13 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
       const int lq = tt * TC + m1_cc;
       const int q = pp.rank * COLS + lq;
       const bool gen = special_column(q);
+#ifndef SA_PROBE_NOTWLD
       if (u > 0) load_wf<T>(wf, stage2, q, m1_g);
+#endif
       V v[16];
 #pragma unroll
       for (int k = 0; k < 16; ++k) v[k] = A::from(inter[(m1_g * 16 + k) * COLS + lq]);
+#ifndef SA_PROBE_SKIP_B
       if (gen) {  // warps with column 0 / 128: general product (twiddles with zero components)
 #pragma unroll
         for (int t = 1; t <= 4; ++t) {  // R bits 0..3
@@ -366,11 +387,13 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
             if (!(k & h)) r_dit_fast<T>(v[k], v[k + h], wf[h - 1 + (k & (h - 1))]);
         }
       }
+#endif
 #pragma unroll
       for (int k = 0; k < 16; ++k) inter[(m1_g * 16 + k) * COLS + lq] = A::to(v[k]);
       group_sync(gbar, GT);
 #pragma unroll
       for (int k = 0; k < 16; ++k) v[k] = A::from(inter[(m1_g + 16 * k) * COLS + lq]);
+#ifndef SA_PROBE_SKIP_B
       if (gen) {
 #pragma unroll
         for (int t = 5; t <= 8; ++t) {  // R bits 4..7
@@ -388,6 +411,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
             if (!(k & hr)) r_dit_fast<T>(v[k], v[k + hr], wf[15 + hr - 1 + (k & (hr - 1))]);
         }
       }
+#endif
 #pragma unroll
       for (int k = 0; k < 16; ++k) __stcs(&ysig[(m1_g + 16 * k) * 256 + q], A::to(v[k]));
     }
