@@ -143,9 +143,10 @@ def max_over_ranks(ws, v: float) -> float:
     return float(t.item())
 
 
-def timed(fn, steps, warmup, ws, sampler=None):
+def timed(fn, steps, warmup, ws, sampler=None, flush=None):
     """W untimed steps, then K steps between barrier+sync; CUDA events on the
-    launching stream; returns (ms_per_step max over ranks, clocks)."""
+    launching stream (``flush`` makes it wait for any side stream the steps use
+    before the end event); returns (ms_per_step max over ranks, clocks)."""
     import torch
     for _ in range(warmup):
         fn()
@@ -161,6 +162,8 @@ def timed(fn, steps, warmup, ws, sampler=None):
     e0.record(s)
     for _ in range(steps):
         fn()
+    if flush:
+        flush()
     e1.record(s)
     torch.cuda.synchronize()
     barrier(ws)
@@ -703,10 +706,44 @@ def wl_map(args, ws, rank, c5=False, e2e=False):
     return res
 
 
+def wl_map_stream(args, ws, rank):
+    """C5 map, streaming: each step submits one CPI to a sharded.MapStream (the
+    lag stage of map i+1 overlaps the delivery of map i into rank 0's memory);
+    timed over K steps including the flush of the last map."""
+    import torch
+    from paper_1402_0532_b200.sharded import MapStream, blocks_shardable
+    from paper_1402_0532_b200.workloads import c5_scene
+    sc = c5_scene()
+    L, M = 4096, 2048
+    cdt = complex_dtype(args.dtype)
+    surv = torch.from_numpy(sc.surv).to(cdt).cuda()
+    ref = torch.from_numpy(sc.ref).to(cdt).cuda()
+    if not blocks_shardable(surv, M, "fast", "mf", "nfft", L, ws):
+        return {"skipped": "not block-shardable"}
+    ms_ = MapStream(L, M, cdt, depth=2)
+    ems, _ = timed(lambda: ms_.submit(surv, ref), max(3, args.steps // 2), 3, ws, flush=ms_.flush)
+    out = {"ms_per_step": ems, "cells_per_s": L * M / (ems * 1e-3), "n_gpus": ws, "scaling": "strong",
+           "config": {"workload": "C5 ⊙ range-Doppler map, streaming CPIs (BASELINE.json configs[4])",
+                      "delay_bins": L, "doppler_bins": M, "maps_in_flight": 2,
+                      "parallelism": f"Doppler-block shards x{ws} (lag) + delay-bin shards (Doppler), map i "
+                                     "delivered into rank 0 on a side stream while map i+1's lag stage runs"}}
+    if args.check:
+        full = ms_.submit(surv, ref)
+        ms_.flush()
+        torch.cuda.synchronize()
+        if rank == 0:
+            import paper_1402_0532_b200 as _sa
+            out["map_check"] = {"bit_identical": bool(torch.equal(full, _sa.ambiguity_map(surv, ref, L, M)))}
+    ms_.close()
+    return out
+
+
 def summarise(name, e):
     """One compact record per workload for the line's trailing ``summary`` key."""
     if "error" in e:
         return {"error": e["error"][:120]}
+    if "ms_per_step" not in e:
+        return {k: v for k, v in e.items() if k in ("skipped", "unavailable")}
     r = {"ms": round(e["ms_per_step"], 4)}
     for k in ("ops_per_s", "cells_per_s"):
         if k in e:
@@ -816,6 +853,10 @@ def run_ours(args):
             import paper_1402_0532_b200 as _sa
             one = _sa.ambiguity_map(res["surv"], res["ref"], res["config"]["delay_bins"], res["config"]["doppler_bins"])
             line["map_check"] = {"bit_identical": bool(torch.equal(full, one)), "rows": int(full.shape[0])}
+    if w == "map5" and ws > 1 and args.check:  # the streaming variant, checked too
+        extras_stream = wl_map_stream(args, ws, rank)
+        if rank == 0:
+            line.setdefault("workloads", {})["C5_map_stream"] = extras_stream
     if w in ("map", "map5") and rank == 0:
         lms, _ = timed(res["lag_only"], args.steps, 3, 1)
         line["roofline"] = roof_lag(args.dtype, res["config"]["ns"], res["config"]["delay_bins"] // ws, lms)
@@ -884,9 +925,15 @@ def run_ours(args):
         except Exception as ex:
             e = {"error": repr(ex)}
         extras["C5_map"] = e
+        if ws > 1:  # CPIs back to back, two maps in flight (sharded.MapStream)
+            try:
+                e2 = wl_map_stream(args, ws, rank)
+                extras["C5_map_stream"] = e2
+            except Exception as ex:
+                extras["C5_map_stream"] = {"error": repr(ex)}
     if rank == 0:
         if extras:
-            line["workloads"] = extras
+            line.setdefault("workloads", {}).update(extras)
         # compact per-workload record LAST, so a truncated stdout tail still shows it
         line["summary"] = {"headline": summarise("headline", {**line, "ops_per_s": line["value"]}),
                            **{k: summarise(k, v) for k, v in extras.items()}}

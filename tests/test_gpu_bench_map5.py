@@ -36,3 +36,5 @@ def test_bench_map5_two_ranks_shared_gpu(sa):
     assert line["n_gpus"] == 2
     assert "Doppler-block shards x2" in line["config"]["parallelism"]
     assert line["map_check"]["bit_identical"] is True, line["map_check"]
+    st = line["workloads"]["C5_map_stream"]  # two CPIs in flight (sharded.MapStream)
+    assert st["map_check"]["bit_identical"] is True and st["config"]["maps_in_flight"] == 2
