@@ -59,7 +59,16 @@ constexpr int SMEM = NSLOT * SLOT + 1024 + 256;
 #endif
 constexpr int EPI = SA_I8_EPI_WARPS;  // epilogue warps: EPI / 4 per TMEM lane quarter, each a column share
 constexpr int RELAY_WARP = 2 + EPI;
-constexpr int THREADS = (3 + EPI) * 32;  // producer, MMA, epilogue warps, relay
+#ifndef SA_I8_NP
+#define SA_I8_NP 1  // CTA pairs per cluster sharing (TMA-multicast) the x planes of one vector tile
+#endif
+constexpr int NP = SA_I8_NP;
+#ifndef SA_I8_SCALE
+#define SA_I8_SCALE 0  // 1: the 127 x sign tiles are made in smem from the sign tiles (5 planes per side in HBM)
+#endif
+constexpr int NMEM = SA_I8_SCALE ? 5 : 6;  // planes per side in HBM (smem images), order S, [127 S,] digits
+constexpr int NSCALE = SA_I8_SCALE ? 2 : 0;  // scaler warps (they also relay); else one relay warp
+constexpr int THREADS = (2 + EPI + (NSCALE ? NSCALE : 1)) * 32;  // producer, MMA, epilogue, scaler/relay
 constexpr int TMEM_COLS = 512;
 // kind::i8: D = s32 (2), A = B = s8 (1), K-major, N = 128, M = 256
 constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
@@ -70,6 +79,13 @@ SA_HD uint64_t sdesc(uint32_t saddr) {  // K-major SWIZZLE_64B: 64-B rows, 8-row
 }
 // byte offset of (row r, K byte b) inside a SWIZZLE_64B tile of 64-B rows
 SA_HD uint32_t sw64(int r, int b) { return (uint32_t)(r * 64 + ((((b >> 4) ^ (r >> 1)) & 3) << 4) + (b & 15)); }
+SA_HD void bulk_g2s_mc(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint16_t mask, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4, %5;" ::"r"(sa_smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(sa_smem_u32(bar)), "h"(mask), "l"(pol)
+      : "memory");
+}
 SA_HD void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
@@ -79,11 +95,11 @@ SA_HD void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar, u
 }
 SA_HD void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 SA_HD void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-SA_HD void commit2(uint64_t *bar) {
+SA_HD void commit2(uint64_t *bar, uint16_t mask) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
           sa_smem_u32(bar)),
-      "h"((uint16_t)3)
+      "h"(mask)
       : "memory");
 }
 SA_HD void mma2(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
@@ -177,7 +193,7 @@ __global__ void __launch_bounds__(256) k_i8_prep(const double *__restrict__ x, i
     int e = 0;
     if (mx > 0.0) frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1): max < 2^e
     if (threadIdx.x == 0) ex[v] = e;
-    int8_t *blk = planes + (size_t)(v / BM) * kslots * (NPL * XT);
+    int8_t *blk = planes + (size_t)(v / BM) * kslots * (NMEM * XT);
     const int r = (int)(v % BM);
 #pragma unroll
     for (int i = 0; i < IT; ++i) {
@@ -196,9 +212,9 @@ __global__ void __launch_bounds__(256) k_i8_prep(const double *__restrict__ x, i
           w[4] |= (uint64_t)(uint8_t)d2 << sh;
           w[5] |= (uint64_t)(uint8_t)d3 << sh;
         }
-        int8_t *tile = blk + (size_t)(k / KSL) * (NPL * XT) + sw64(r, k % KSL);  // 8 bytes, one swizzle chunk
+        int8_t *tile = blk + (size_t)(k / KSL) * (NMEM * XT) + sw64(r, k % KSL);  // 8 bytes, one swizzle chunk
 #pragma unroll
-        for (int p = 0; p < NPL; ++p) *(uint64_t *)(tile + p * XT) = w[p];
+        for (int p = 0; p < NMEM; ++p) *(uint64_t *)(tile + p * XT) = w[p + (NMEM == 5 && p > 0)];
       }
     }
   }
@@ -220,9 +236,9 @@ __global__ void k_i8_wbuild(const double2 *__restrict__ raw, int n, int8_t *__re
     digits(val, d0, d1, d2, d3);
     const int sg = sgn_i(val);
     const int8_t v[NPL] = {(int8_t)sg, (int8_t)(127 * sg), (int8_t)d0, (int8_t)d1, (int8_t)d2, (int8_t)d3};
-    int8_t *tile = q + ((o / (BN / 2)) * kslots + kk / KSL) * (NPL * WT) + sw64((int)(o % (BN / 2)), (int)(kk % KSL));
+    int8_t *tile = q + ((o / (BN / 2)) * kslots + kk / KSL) * (NMEM * WT) + sw64((int)(o % (BN / 2)), (int)(kk % KSL));
 #pragma unroll
-    for (int p = 0; p < NPL; ++p) tile[p * WT] = v[p];
+    for (int p = 0; p < NMEM; ++p) tile[p * WT] = v[p + (NMEM == 5 && p > 0)];
   }
 }
 
@@ -239,19 +255,24 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t *tmem_holder = (uint32_t *)(tempty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_rank();
-  const int64_t cl = blockIdx.x / 2, ncl = gridDim.x / 2;
+  // cluster = NP CTA pairs on the same vector tile, pair pr on output tile NP otp + pr
+  const uint32_t crank = cluster_rank();
+  const uint32_t rank = crank & 1, pr = crank >> 1;
+  const int64_t cl = blockIdx.x / (2 * NP), ncl = gridDim.x / (2 * NP);
   const int nk = 2 * n;
   const int ot_count = nk / BN;
   const int64_t vt_count = (batch + 2 * BM - 1) / (2 * BM);
-  const int64_t ntiles = vt_count * ot_count;
+  const int64_t ntiles = vt_count * (ot_count / NP);  // cluster tiles
   const int kslots = nk / KSL;
-  auto lead = [&](uint64_t *bar) { return sa_mapa(sa_smem_u32(bar), 0); };
+  const uint16_t pair_mask = (uint16_t)(3u << (2 * pr)), all_mask = (uint16_t)((1u << (2 * NP)) - 1);
+  auto lead = [&](uint64_t *bar) { return sa_mapa(sa_smem_u32(bar), crank & ~1u); };
+  auto vt_of = [&](int64_t t) { return t / (ot_count / NP); };
+  auto ot_of = [&](int64_t t) { return (int)(t % (ot_count / NP)) * NP + (int)pr; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSLOT; ++s) {
-      sa_mbar_init(&full[s], 2);  // the relays of both CTAs
-      sa_mbar_init(&empty[s], 1);
+      sa_mbar_init(&full[s], 2 * (NSCALE ? NSCALE : 1));  // the relay / scaler warps of both CTAs
+      sa_mbar_init(&empty[s], NP);  // every pair's MMAs on slot s are done (x tiles are shared)
       sa_mbar_init(&lfull[s], 1);
     }
     sa_mbar_init(tfull, 1);
@@ -279,24 +300,57 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int64_t lt = it / kslots;
         const int kc = (int)(it - lt * kslots);
         const int64_t t = cl + lt * ncl;
-        const int64_t vb = (t / ot_count) * 2 + rank;            // 128-vector block
-        const int64_t ob = (t % ot_count) * 2 + rank;            // 64-output block
+        const int64_t vb = vt_of(t) * 2 + rank;                   // 128-vector block
+        const int64_t ob = (int64_t)ot_of(t) * 2 + rank;          // 64-output block
         const int s = (int)(it % NSLOT);
-        sa_mbar_wait(&empty[s], ((it / NSLOT) & 1) ^ 1);
+        sa_mbar_wait(&empty[s], ((it / NSLOT) & 1) ^ 1);          // every pair is done with slot s
         unsigned char *b = smem + s * SLOT;
-        sa_mbar_expect_tx(&lfull[s], SLOT);
-        bulk_g2s(b, xblk + (vb * kslots + kc) * (NPL * XT), NPL * XT, &lfull[s], xpol);
-        bulk_g2s(b + NPL * XT, wblk + (ob * kslots + kc) * (NPL * WT), NPL * WT, &lfull[s], wpol);
+        sa_mbar_expect_tx(&lfull[s], NMEM * (XT + WT));
+        const int8_t *xs = xblk + (vb * kslots + kc) * (NMEM * XT);
+        const int8_t *ws_ = wblk + (ob * kslots + kc) * (NMEM * WT);
+        if (NMEM == 6) {
+          if (NP == 1) bulk_g2s(b, xs, NPL * XT, &lfull[s], xpol);
+          else if (pr == 0)  // the x tile of rows `rank` goes to the same CTA of every pair
+            bulk_g2s_mc(b, xs, NPL * XT, &lfull[s], (uint16_t)(0x5u << rank), xpol);
+          bulk_g2s(b + NPL * XT, ws_, NPL * WT, &lfull[s], wpol);
+        } else {  // S -> tile 0, digits -> tiles 2..5 (tile 1 = 127 S is made by the scalers)
+          bulk_g2s(b, xs, XT, &lfull[s], xpol);
+          bulk_g2s(b + 2 * XT, xs + XT, 4 * XT, &lfull[s], xpol);
+          bulk_g2s(b + NPL * XT, ws_, WT, &lfull[s], wpol);
+          bulk_g2s(b + NPL * XT + 2 * WT, ws_ + WT, 4 * WT, &lfull[s], wpol);
+        }
       }
     }
-  } else if (warp == RELAY_WARP) {
-    // ---- relay: this CTA's slot landed -> arrive on the leader's full barrier ----
-    if (lane == 0)
-      for (int64_t it = 0; it < total; ++it) {
-        const int s = (int)(it % NSLOT);
-        sa_mbar_wait(&lfull[s], (it / NSLOT) & 1);
-        arrive_cl(lead(&full[s]));
+  } else if (warp >= RELAY_WARP) {
+    // ---- relay (+ scalers): this CTA's slot landed [127 S / 127 sW tiles made from
+    // the sign tiles: bytes {-1,0,1} -> (x & 1) * 127, negated where negative] ->
+    // arrive on the leader's full barrier ----
+    const int st = threadIdx.x - RELAY_WARP * 32, nst = (NSCALE ? NSCALE : 1) * 32;
+    for (int64_t it = 0; it < total; ++it) {
+      const int s = (int)(it % NSLOT);
+      sa_mbar_wait(&lfull[s], (it / NSLOT) & 1);
+      if (NSCALE) {
+        unsigned char *b = smem + s * SLOT;
+        auto scale_tile = [&](const unsigned char *src, unsigned char *dst, int bytes) {
+          for (int o = st * 16; o < bytes; o += nst * 16) {
+            uint4 v = *(const uint4 *)(src + o);
+            uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const uint32_t t = (w[i] & 0x01010101u) * 0x7Fu;
+              const uint32_t ng = (w[i] >> 7) & 0x01010101u;
+              w[i] = (t ^ (ng * 0xFFu)) + ng;
+            }
+            *(uint4 *)(dst + o) = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        };
+        scale_tile(b, b + XT, XT);
+        scale_tile(b + NPL * XT, b + NPL * XT + WT, WT);
+        sa_fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05.mma
       }
+      __syncwarp();
+      if (lane == 0) arrive_cl(lead(&full[s]));
+    }
   } else if (warp == 1) {
     // ---- MMA issuer (leader CTA): 8 MMAs per K step of 32 into the four accumulators ----
     if (lane == 0 && rank == 0) {
@@ -324,9 +378,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             mma2(tmem + 384, X(4), W(1), first);  // accXL += dx2 127 sW
             mma2(tmem + 384, X(5), W(0), 1);      //        + dx3 sW
           }
-          commit2(&empty[s]);
+          commit2(&empty[s], all_mask);
         }
-        commit2(tfull);
+        commit2(tfull, pair_mask);
       }
     }
   } else {
@@ -336,8 +390,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     constexpr int CW = BN / (EPI / 4);
     uint32_t lt = 0;
     for (int64_t t = cl; t < ntiles; t += ncl, ++lt) {
-      const int64_t v = (t / ot_count) * (2 * BM) + rank * BM + q * 32 + lane;
-      const int o0 = (int)(t % ot_count) * BN;
+      const int64_t v = vt_of(t) * (2 * BM) + rank * BM + q * 32 + lane;
+      const int o0 = ot_of(t) * BN;
       const int e = v < batch ? ex[v] : 0;
       sa_mbar_wait(tfull, lt & 1);
       fence_after();
@@ -389,10 +443,10 @@ std::mutex g_i8_mutex;
 }  // namespace
 
 bool sa_ndft_i8_supported(int dtype, int64_t n) {
-  return dtype == SA_C128 && n >= 128 && n <= 2048 && n % 64 == 0;  // 2n <= 2 x 2048 (k_i8_prep)
+  return dtype == SA_C128 && n >= 128 && n <= 2048 && n % (64 * NP) == 0;  // 2n <= 2 x 2048 (k_i8_prep); whole cluster tiles
 }
 
-int64_t sa_ndft_i8_wbytes(int64_t n) { return (int64_t)NPL * (2 * n) * (2 * n); }
+int64_t sa_ndft_i8_wbytes(int64_t n) { return (int64_t)NMEM * (2 * n) * (2 * n); }
 
 int sa_launch_ndft_i8(const void *x, void *y, int64_t batch, int64_t n, const SaTwiddles *tw_c, double gain,
                       cudaStream_t s) {
@@ -418,7 +472,7 @@ int sa_launch_ndft_i8(const void *x, void *y, int64_t batch, int64_t n, const Sa
   if (tw->i8w_ready) SA_CUDA_TRY(cudaStreamWaitEvent(s, (cudaEvent_t)tw->i8w_ready, 0));
   // x planes (whole 256-vector tiles: rows past the batch are never stored) + exponents
   const int64_t rows = (batch + 2 * BM - 1) / (2 * BM) * (2 * BM);
-  const size_t pbytes = (size_t)NPL * rows * 2 * n;
+  const size_t pbytes = (size_t)NMEM * rows * 2 * n;
   int8_t *planes = nullptr;
   {
     const int rc_ = sa_scratch_alloc((void **)&planes, pbytes + (size_t)batch * sizeof(int) + 256, s);
@@ -437,20 +491,24 @@ int sa_launch_ndft_i8(const void *x, void *y, int64_t batch, int64_t n, const Sa
     SA_CUDA_TRY(cudaFuncSetAttribute(k_ndft_i8, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
     if (dev < 64) smem_set[dev] = true;
   }
-  const int64_t ntiles = (rows / (2 * BM)) * ((2 * n) / BN);
-  const int64_t units = ntiles < sms / 2 ? ntiles : sms / 2;
+  const int64_t ntiles = (rows / (2 * BM)) * ((2 * n) / BN / NP);  // cluster tiles
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(units * 2));
   cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = SMEM;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = 2 * NP;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  cfg.gridDim = dim3((unsigned)(2 * NP * (sms / (2 * NP))));
+  int max_clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&max_clusters, k_ndft_i8, &cfg) != cudaSuccess || max_clusters < 1)
+    max_clusters = sms / (2 * NP);
+  const int64_t units = ntiles < max_clusters ? ntiles : max_clusters;
+  cfg.gridDim = dim3((unsigned)(units * 2 * NP));
   SA_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_ndft_i8, (const int8_t *)planes, (const int8_t *)tw->i8w, (const int *)ex,
                                  (double *)y, batch, (int)n));
   SA_LAUNCH_CHECK();
