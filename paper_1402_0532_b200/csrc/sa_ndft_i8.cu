@@ -36,7 +36,9 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <climits>
 #include <map>
+#include <math_constants.h>
 #include <mutex>
 #include <tuple>
 
@@ -178,7 +180,9 @@ __global__ void __launch_bounds__(256) k_i8_prep(const double *__restrict__ x, i
           double2 u = __ldcs((const double2 *)&row[k + j]);
           t[i][j] = use_gain ? sa_mul(gain, u.x) : u.x;
           t[i][j + 1] = use_gain ? sa_mul(gain, u.y) : u.y;
-          mx = fmax(mx, fmax(fabs(t[i][j]), fabs(t[i][j + 1])));
+          // max |x|; a NaN / Inf anywhere makes mx = +Inf (fmax would drop a NaN)
+          const double a0 = fabs(t[i][j]), a1 = fabs(t[i][j + 1]);
+          mx = (a0 == a0 && a1 == a1) ? fmax(mx, fmax(a0, a1)) : INFINITY;
         }
       }
     }
@@ -192,7 +196,9 @@ __global__ void __launch_bounds__(256) k_i8_prep(const double *__restrict__ x, i
     __syncthreads();
     int e = 0;
     if (mx > 0.0) frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1): max < 2^e
+    if (!(mx <= 1.7976931348623157e308)) e = INT_MAX;  // non-finite row: the epilogue writes NaN
     if (threadIdx.x == 0) ex[v] = e;
+    if (e == INT_MAX) e = 0;  // (digits of this row are never used)
     int8_t *blk = planes + (size_t)(v / BM) * kslots * (NMEM * XT);
     const int r = (int)(v % BM);
 #pragma unroll
@@ -418,7 +424,7 @@ __global__ void __launch_bounds__(THREADS, 1)
               constexpr double C2 = 1.0 / (64.0 * 127.0 * 128.0 * 127.0);
               const long long W = (long long)(int)wh[j + h] * (128 * 127) + (int)wl[j + h];
               const long long X = (long long)(int)xh[j + h] * (128 * 127) + (int)xl[j + h];
-              d[h] = sa_add(ldexp(sa_mul((double)X, C2), e), sa_mul((double)W, C2));
+              d[h] = e == INT_MAX ? CUDART_NAN : sa_add(ldexp(sa_mul((double)X, C2), e), sa_mul((double)W, C2));
             }
             __stcs((double2 *)&dst[c + j], make_double2(d[0], d[1]));
           }

@@ -84,3 +84,15 @@ def test_ndft_i8_c2_sampled_rows(sa):
     r = oracle.ndft(x[idx], nthreads=16)
     e = assert_literal(ys, r, TOL_F64)
     print(f"C2 c128 tc: literal max {e.max():.2e}, strict max {strict(ys, r).max():.2e}")
+
+
+def test_ndft_i8_non_finite_rows_are_nan(sa):
+    """A row holding NaN / Inf comes out NaN (as the DFMA kernel's would), other rows unaffected."""
+    g = np.random.default_rng(17)
+    x = g.standard_normal((6, 256)) + 1j * g.standard_normal((6, 256))
+    x[1, 7] = np.nan
+    x[3, 0] = np.inf
+    y = sa.ndft_batch(dev(x), mode="tc").cpu().numpy()
+    assert np.isnan(y[1]).all() and np.isnan(y[3]).all()
+    keep = [0, 2, 4, 5]
+    assert_literal(y[keep], oracle.ndft(x[keep], nthreads=8), TOL_F64)
