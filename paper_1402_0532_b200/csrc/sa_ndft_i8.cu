@@ -226,6 +226,68 @@ __global__ void __launch_bounds__(256) k_i8_prep(const double *__restrict__ x, i
   }
 }
 
+// The same as k_i8_prep with one warp per row (no block barriers, ~8 doubles live
+// per lane): pass 1 takes the row max, pass 2 re-reads the row (L1) and writes
+// the digit planes, 8 bytes per plane per lane.
+__global__ void __launch_bounds__(256) k_i8_prep_w(const double *__restrict__ x, int8_t *__restrict__ planes,
+                                                   int *__restrict__ ex, int64_t batch, int n, double gain,
+                                                   int use_gain) {
+  const int nk = 2 * n;
+  const int kslots = nk / KSL;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  auto ld8 = [&](const double *row, int k, double (&t)[8]) {
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+      double2 u = *(const double2 *)&row[k + j];
+      t[j] = use_gain ? sa_mul(gain, u.x) : u.x;
+      t[j + 1] = use_gain ? sa_mul(gain, u.y) : u.y;
+    }
+  };
+  for (int64_t v = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); v < batch; v += nw) {
+    const double *row = x + v * nk;
+    double mx = 0.0;
+    for (int k = lane * 8; k < nk; k += 256) {
+      double t[8];
+      ld8(row, k, t);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double a = fabs(t[j]);
+        mx = a == a ? fmax(mx, a) : INFINITY;  // a NaN anywhere makes the row non-finite
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    int e = 0;
+    if (mx > 0.0) frexp(mx, &e);
+    if (!(mx <= 1.7976931348623157e308)) e = INT_MAX;  // non-finite row: the epilogue writes NaN
+    if (lane == 0) ex[v] = e;
+    if (e == INT_MAX) e = 0;
+    int8_t *blk = planes + (size_t)(v / BM) * kslots * (NMEM * XT);
+    const int r = (int)(v % BM);
+    for (int k = lane * 8; k < nk; k += 256) {
+      double t[8];
+      ld8(row, k, t);
+      uint64_t w[6] = {};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        int d0, d1, d2, d3;
+        digits(ldexp(t[j], -e), d0, d1, d2, d3);
+        const int sh = 8 * j, sg = sgn_i(t[j]);
+        w[0] |= (uint64_t)(uint8_t)sg << sh;
+        w[1] |= (uint64_t)(uint8_t)(127 * sg) << sh;
+        w[2] |= (uint64_t)(uint8_t)d0 << sh;
+        w[3] |= (uint64_t)(uint8_t)d1 << sh;
+        w[4] |= (uint64_t)(uint8_t)d2 << sh;
+        w[5] |= (uint64_t)(uint8_t)d3 << sh;
+      }
+      int8_t *tile = blk + (size_t)(k / KSL) * (NMEM * XT) + sw64(r, k % KSL);
+#pragma unroll
+      for (int p = 0; p < NMEM; ++p) *(uint64_t *)(tile + p * XT) = w[p + (NMEM == 5 && p > 0)];
+    }
+  }
+}
+
 // W planes Q[p][o][K] (p = sW, dW0..dW3) of Wv = [[Wr, -Wi], [Wi, Wr]],
 // W = raw[(k m) mod n] (the fp64 reference table, transforms.py:108-146).
 __global__ void k_i8_wbuild(const double2 *__restrict__ raw, int n, int8_t *__restrict__ q) {
