@@ -43,9 +43,14 @@ enum sa_ndft_mode {
   SA_NDFT_FAST = 0,  /* sign-split regrouped accumulation (8 FMA per ⊙)        */
   SA_NDFT_EXACT = 1, /* per-⊙ rounding, sequential accumulation: value-identical
                         to transforms.py:223-251                               */
-  SA_NDFT_TC = 2     /* the fast-mode sum as a sign-split bf16 GEMM on tcgen05
-                        tensor cores (complex64, n % 128 == 0, n <= 4096; other
-                        shapes run SA_NDFT_FAST).  Same ≤1e-4 fp32 tolerance. */
+  SA_NDFT_TC = 2,    /* the fast-mode sum on the tcgen05 tensor cores: complex64
+                        as a sign-split bf16 GEMM (n % 128 == 0, n <= 4096;
+                        ≤1e-4), complex128 with exact int8 digits (n % 64 == 0,
+                        128 <= n <= 2048; ≤1e-9); other shapes run SA_NDFT_FAST */
+  SA_NDFT_TC_I8 = 3  /* the fast-mode sum on tcgen05 kind::i8 with exact int8
+                        digits for both dtypes (complex64: one digit pair,
+                        n % 128 == 0, 128 <= n <= 2048, ≤1e-4; complex128 as
+                        SA_NDFT_TC); other shapes run SA_NDFT_FAST */
 };
 
 enum sa_nlfft_variant {

@@ -18,7 +18,7 @@ if os.environ.get("SA_LIB_PATH"):  # development: time an alternative build of t
     LIB_PATH = os.environ["SA_LIB_PATH"]
 
 SA_C64, SA_C128 = 0, 1
-SA_NDFT_FAST, SA_NDFT_EXACT, SA_NDFT_TC = 0, 1, 2
+SA_NDFT_FAST, SA_NDFT_EXACT, SA_NDFT_TC, SA_NDFT_TC_I8 = 0, 1, 2, 3
 SA_DIT, SA_DIF, SA_FFT_EXACT = 0, 1, 2
 SA_LAG_MF, SA_LAG_EXACT = 0, 1
 SA_DOPPLER_NLFFT, SA_DOPPLER_NDFT, SA_DOPPLER_FFT_EXACT = 0, 1, 2

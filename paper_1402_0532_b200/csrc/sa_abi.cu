@@ -116,15 +116,16 @@ int sa_ndft(int dtype, const void *x, void *y, int64_t batch, int64_t n, const v
   SA_REQUIRE(dtype_ok(dtype), SA_ERR_ARG, "bad dtype %d", dtype);
   SA_REQUIRE(n >= 1, SA_ERR_CONTRACT, "transform input must be a 1-d sequence of length >= 1");
   SA_REQUIRE(batch >= 0, SA_ERR_ARG, "negative batch");
-  SA_REQUIRE(mode == SA_NDFT_FAST || mode == SA_NDFT_EXACT || mode == SA_NDFT_TC, SA_ERR_ARG, "bad mode %d",
-             mode);
+  SA_REQUIRE(mode == SA_NDFT_FAST || mode == SA_NDFT_EXACT || mode == SA_NDFT_TC || mode == SA_NDFT_TC_I8,
+             SA_ERR_ARG, "bad mode %d", mode);
   SA_REQUIRE(batch == 0 || (x && y), SA_ERR_ARG, "null pointer");
   SA_REQUIRE(x != y || batch == 0, SA_ERR_ARG, "sa_ndft: x and y must not overlap");
   int rc = check_tw(tw, dtype, n, false);
   if (rc) return rc;
-  if (mode == SA_NDFT_TC) {
-    rc = dtype == SA_C64 ? sa_launch_ndft_tc(x, y, batch, n, (const SaTwiddles *)tw, gain, (cudaStream_t)stream)
-                         : sa_launch_ndft_i8(x, y, batch, n, (const SaTwiddles *)tw, gain, (cudaStream_t)stream);
+  if (mode == SA_NDFT_TC || mode == SA_NDFT_TC_I8) {
+    rc = (dtype == SA_C64 && mode == SA_NDFT_TC)
+             ? sa_launch_ndft_tc(x, y, batch, n, (const SaTwiddles *)tw, gain, (cudaStream_t)stream)
+             : sa_launch_ndft_i8(x, y, batch, n, (const SaTwiddles *)tw, gain, (cudaStream_t)stream);
     if (rc != SA_ERR_UNSUPPORTED) return rc;
     mode = SA_NDFT_FAST;  // other shapes / unaligned views: the same regrouped sum on the FFMA2 kernels
   }

@@ -345,12 +345,15 @@ def ndft_batch(x, *, mode: str = "fast", gain: float = 1.0, out=None, check_fini
     """Batched NDFT over the last axis of a (B, N) complex64/complex128 input.
 
     mode "fast": sign-split regrouped accumulation (8 FMA per ⊙); "exact":
-    value-identical to the reference per vector; "tc": the fast-mode sum as a
-    sign-split bf16 GEMM on the tcgen05 tensor cores (complex64 with n % 128 == 0
-    and n <= 4096; other inputs run "fast"), same fp32 tolerance.  ``gain`` scales the input first
+    value-identical to the reference per vector; "tc": the fast-mode sum on the
+    tcgen05 tensor cores -- complex64 as a sign-split bf16 GEMM (n % 128 == 0,
+    n <= 4096), complex128 with exact int8 digits (n % 64 == 0, 128 <= n <= 2048,
+    within the fp64 bound); "tc8": exact int8 digits for complex64 too (one digit
+    pair, n % 128 == 0, 128 <= n <= 2048).  Other shapes run "fast".  ``gain`` scales the input first
     (as ``transform_gain * y`` in ambiguity.py:176-177).
     """
-    m = {"fast": _native.SA_NDFT_FAST, "exact": _native.SA_NDFT_EXACT, "tc": _native.SA_NDFT_TC}[mode]
+    m = {"fast": _native.SA_NDFT_FAST, "exact": _native.SA_NDFT_EXACT, "tc": _native.SA_NDFT_TC,
+         "tc8": _native.SA_NDFT_TC_I8}[mode]
     if _pinned_host(x) and (out is None or _pinned_host(out)) and not check_finite:
         r = _host_pipelined(x, out, lambda a, b: _launch_ndft(a, b, m, gain), 128, dtype)
         if r is not None:

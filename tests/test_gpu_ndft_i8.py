@@ -96,3 +96,66 @@ def test_ndft_i8_non_finite_rows_are_nan(sa):
     assert np.isnan(y[1]).all() and np.isnan(y[3]).all()
     keep = [0, 2, 4, 5]
     assert_literal(y[keep], oracle.ndft(x[keep], nthreads=8), TOL_F64)
+
+
+# ---- complex64 on the int8 path (mode "tc8", sa_ndft_i8.cu ND=1) -------------
+# One 13-bit-wide digit pair per operand (radix 64 x 127): the same exact int32
+# products, one quarter of the MMAs of complex128.  Error model ~sqrt(2n) 2^-14
+# 2^e / (n sqrt(2n)): ~4e-6 relative to ||y||_1, inside the 1e-4 fp32 bound.
+
+def _ref32(x):
+    return oracle.ndft(np.asarray(x, np.complex64).astype(np.complex128), nthreads=8)
+
+
+@pytest.mark.parametrize("n,rows", [(128, 1), (128, 300), (256, 257), (512, 7), (1024, 129), (2048, 5)])
+def test_ndft_i8_c64_sizes(sa, n, rows):
+    from parity import TOL_F32
+    g = np.random.default_rng(4000 + n + rows)
+    x = ((g.standard_normal((rows, n)) + 1j * g.standard_normal((rows, n))) / np.sqrt(2)).astype(np.complex64)
+    if rows > 4:
+        x[3] = 0
+        x[4, ::3] = 0
+        x[2, 1::2] = -0.0
+    y = sa.ndft_batch(dev(x), mode="tc8").cpu().numpy()
+    assert y.dtype == np.complex64
+    r = _ref32(x)
+    e = assert_literal(y, r, TOL_F32)
+    assert e.max() < 2e-5, e.max()
+    print(f"c64 n={n} rows={rows}: literal max {e.max():.2e}")
+    if rows > 4:
+        assert np.all(y[3] == 0)
+
+
+def test_ndft_i8_c64_range_gain_nonfinite_fallback(sa):
+    from parity import TOL_F32
+    g = np.random.default_rng(21)
+    x = (g.standard_normal((140, 256)) + 1j * g.standard_normal((140, 256))).astype(np.complex64)
+    x[5] *= 1e-30
+    x[6] *= 1e30
+    x[7, ::2] *= 1e-6
+    x[9, ::5] = 1e-45             # fp32 subnormals
+    for gain in (1.0, 16.0, 0.37):
+        y = sa.ndft_batch(dev(x), mode="tc8", gain=gain).cpu().numpy()
+        assert_literal(y, _ref32(gain * x.astype(np.complex128)), TOL_F32)
+    z = x[:6].copy()
+    z[1, 7] = np.nan
+    z[3, 0] = np.inf
+    y = sa.ndft_batch(dev(z), mode="tc8").cpu().numpy()
+    assert np.isnan(y[1]).all() and np.isnan(y[3]).all()
+    assert_literal(y[[0, 2, 4, 5]], _ref32(z[[0, 2, 4, 5]]), TOL_F32)
+    for n in (96, 64, 4096):      # outside the int8 shapes: the fast kernel
+        w = (g.standard_normal((9, n)) + 1j * g.standard_normal((9, n))).astype(np.complex64)
+        assert np.array_equal(sa.ndft_batch(dev(w), mode="tc8").cpu().numpy(),
+                              sa.ndft_batch(dev(w), mode="fast").cpu().numpy())
+
+
+def test_ndft_i8_c64_c2_subset(sa):
+    import torch
+    from parity import TOL_F32
+    from paper_1402_0532_b200.workloads import c2_ndft
+    x = c2_ndft().astype(np.complex64)
+    y = sa.ndft_batch(dev(x), mode="tc8")
+    rows = np.arange(0, x.shape[0], 512)
+    ys = y[torch.from_numpy(rows).cuda()].cpu().numpy()
+    e = assert_literal(ys, _ref32(x[rows]), TOL_F32)
+    print(f"C2 c64 tc8: literal max {e.max():.2e}")

@@ -8,11 +8,11 @@ import paper_1402_0532_b200 as sa
 what = sys.argv[1]
 dt = torch.complex64 if (len(sys.argv) < 3 or sys.argv[2] == "c64") else torch.complex128
 reps = 3
-if what in ("ndft", "ndft_tc"):
+if what in ("ndft", "ndft_tc", "ndft_tc8"):
     x = torch.randn(65536, 1024, dtype=dt, device="cuda")
     y = torch.empty_like(x)
     for _ in range(reps):
-        sa.ndft_batch(x, out=y, mode="tc" if what == "ndft_tc" else "fast")
+        sa.ndft_batch(x, out=y, mode={"ndft": "fast", "ndft_tc": "tc", "ndft_tc8": "tc8"}[what])
 elif what in ("nlfft", "nlfft_dif"):
     x = torch.randn(4096, 65536, dtype=dt, device="cuda")
     y = torch.empty_like(x)
