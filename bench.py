@@ -239,6 +239,8 @@ def wl_ndft(args, ws, rank, mode=None, e2e=True, dtype=None):
     step = lambda: sa.ndft_batch(xd, out=yd, mode=mode)  # noqa: E731
     desc = {"tc": "tc (fast-mode sum as a sign-split GEMM on tcgen05 tensor cores: bf16x2-split operands, "
                   "fp32 accumulate)",
+            "tc8": "tc8 (fast-mode sum as a sign-split GEMM on tcgen05 kind::i8: exact int8 digit pairs of Wv "
+                   "and of x / 2^e_v, exact int32 accumulation, fp32 epilogue)",
             "fast": "fast (sign-split regrouped accumulation, " + ("FFMA2)" if dtype == "c64" else "DFMA)")}[mode]
     res = {"ops": ops, "step": step, "launches_per_step": 1,
            "config": {"workload": "C2 batched NDFT (BASELINE.json configs[1])", "n": n,
@@ -256,7 +258,10 @@ def wl_ndft(args, ws, rank, mode=None, e2e=True, dtype=None):
         res["d2h"] = hout.numel() * hout.element_size()
         res["e2e_api"] = f"paper_1402_0532_b200.ndft_batch(pinned host tensor, out=pinned host tensor, mode={mode!r})"
         res["e2e_launches"] = len(_pipeline_plan(res["e2e_rows"], res["e2e_row_bytes"]))
-    if mode == "tc" and dtype == "c128":
+    if mode == "tc8" and dtype == "c64":
+        res["roofline"] = lambda ms: roof_i8(ops * 32 / (ms * 1e-3) / 1e12, "c64")
+        res["dtype"] = "int8 digits x sign, exact int32 accumulate, f32 epilogue"
+    elif mode == "tc" and dtype == "c128":
         res["roofline"] = lambda ms: roof_i8(ops * 64 / (ms * 1e-3) / 1e12)
         res["dtype"] = "int8 digits x sign, exact int32 accumulate, f64 epilogue"
         res["config"]["mode"] = ("tc (complex128: Ozaki-style int8 digits of Wv and of x / 2^e_v on tcgen05 kind::i8, "
@@ -324,20 +329,23 @@ def roof_tensor(achieved_tflops):
             **({"ncu_utilisation_pct": tr["ncu"]} if tr and tr.get("ncu") else {})}
 
 
-def roof_i8(achieved_tops):
-    """complex128 NDFT on tcgen05 kind::i8 (sa_ndft_i8.cu): 8 int8 MMA terms x 4 MACs
-    = 64 int ops per complex ⊙, against the dense int8 tensor rate (2 x the measured
-    bf16 burst figure: B200 int8 runs at twice bf16; MEASURED_PEAKS has no int8 line)."""
+def roof_i8(achieved_tops, dtype="c128"):
+    """NDFT on tcgen05 kind::i8 (sa_ndft_i8.cu): complex128 8 int8 MMA terms x 4 MACs
+    = 64 int ops per complex ⊙ (complex64: 4 terms, 32 ops), against the dense int8
+    tensor rate (2 x the measured bf16 burst figure: B200 int8 runs at twice bf16;
+    MEASURED_PEAKS has no int8 line).  Achieved is over the whole step (the digit
+    prep kernel included)."""
     peaks, src = measured_peaks()
     peak = 2.0 * peaks.get("bf16_tflops", 1590.0)
-    tr = ncu_traffic("k_ndft_i8")
+    tr = ncu_traffic("k_ndft_i8<2" if dtype == "c128" else "k_ndft_i8<1")
+    terms, per = (8, 64) if dtype == "c128" else (4, 32)
     return {"bound": "tensor", "achieved": round(achieved_tops, 1), "peak": round(peak, 1), "unit": "TOP/s",
             "frac": round(achieved_tops / peak, 4), "traffic": tr["bytes_per_launch"] if tr else None,
             "traffic_unit": "bytes/launch", "traffic_source": tr["source"] if tr else None,
-            "kernel": "k_ndft_i8 (+ k_i8_prep)", "algorithmic_bytes": 2 * 65536 * 1024 * 16,
+            "kernel": "k_ndft_i8 (+ k_i8_prep)", "algorithmic_bytes": 2 * 65536 * 1024 * (16 if dtype == "c128" else 8),
             "peak_source": f"2 x {src} bf16_tflops (int8 dense = 2 x bf16 on B200; int8 not measured)",
             "nominal_peak": 4500.0, "frac_nominal": round(achieved_tops / 4500.0, 4),
-            "algorithmic": "64 int8 tensor ops per complex ⊙: 8 digit x sign MMA terms x re/im x re/im MACs"}
+            "algorithmic": f"{per} int8 tensor ops per complex ⊙: {terms} digit x sign MMA terms x re/im x re/im MACs"}
 
 
 def ncu_traffic(kernel_prefix):
@@ -883,7 +891,9 @@ def run_ours(args):
     extras = {}
     if rank == 0 and ws == 1 and not args.no_extras and w == "ndft":
         specs = [("C1_ndft_c128", lambda: wl_ndft64(args))]
-        if args.ndft_mode == "tc" and args.dtype == "c64":
+        if args.ndft_mode == "tc8" and args.dtype == "c64":
+            specs.append(("C2_ndft_bf16", lambda: {**wl_ndft(args, ws, rank, mode="tc", e2e=False), "cpu_skip": 1}))
+        if args.ndft_mode in ("tc", "tc8") and args.dtype == "c64":
             specs.append(("C2_ndft_ffma2", lambda: {**wl_ndft(args, ws, rank, mode="fast", e2e=False), "cpu_skip": 1}))
         specs += [("C2_ndft_c128", lambda: wl_ndft(args, ws, rank, mode="tc", dtype="c128")),
                   ("C2_ndft_c128_dfma", lambda: {**wl_ndft(args, ws, rank, mode="fast", dtype="c128", e2e=False),
@@ -1013,8 +1023,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="ndft", choices=["ndft", "nlfft", "map", "map5"])
     ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
-    ap.add_argument("--ndft-mode", default="tc", choices=["tc", "fast"],
-                    help="C2 NDFT kernel: tc = tcgen05 sign-split GEMM (complex64), fast = FFMA2 CUDA-core kernel")
+    ap.add_argument("--ndft-mode", default="tc8", choices=["tc8", "tc", "fast"],
+                    help="C2 NDFT kernel (complex64): tc8 = tcgen05 kind::i8 exact-digit GEMM, tc = tcgen05 "
+                         "bf16x2-split GEMM, fast = FFMA2 CUDA-core kernel")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

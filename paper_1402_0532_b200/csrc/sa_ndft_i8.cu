@@ -7,17 +7,18 @@
 // The regrouped sum is one real GEMM per batch (sa_ndft_tc.cu):
 //   D[v, o] = Σ_K S[v,K] Wv[o,K] + X[v,K] sgn(Wv)[o,K],   S = sgn(x),  o = 2k+(re|im), K = 2n+(re|im)
 // One factor of every product is a sign in {-1, 0, +1} -- exact in int8.  The
-// other factor is split into 2 ND signed digits in mixed radix (64, 127, 128, 127):
-//   Wv ~ d0/64 + d1/(64 127) [+ d2/(64 127 128) + d3/(64 127 128 127)]    (|Wv| <= 1, |d| <= 64)
+// other factor is split into 2 ND signed digits in mixed radix (127, 127, 128, 127):
+//   Wv ~ d0/127 + d1/127^2 [+ d2/(127^2 128) + d3/(127^3 128)]    (|Wv| <= 1, |d0| <= 127, |d1..3| <= 64)
 //   x' = x_v / 2^e_v   (per-vector exponent: max|x_v| < 2^e_v), digits alike
-// (round-to-nearest digits; the residual after digit 2 ND is <= 2^-14 / 2^-28).
+// (round-to-nearest digits; the residual after digit 2 ND is <= 2^-15 / 2^-29).
 // Two digits 127 apart share one int32 accumulator by pairing the sign operand
 // with 127 x sign (still int8):
 //   accW_j = Σ (127 S) dW_2j + S dW_2j+1        accX_j = Σ dx_2j (127 sW) + dx_2j+1 sW
-// all exact (|acc| < 2^25 at n <= 2048), and the epilogue forms, in fp64,
-//   D = Σ_j accW_j c_j + 2^e_v Σ_j accX_j c_j,   c_0 = 1/(64 127), c_1 = c_0/(128 127).
-// Error model: per output ~ sqrt(2n) 2^-(14 ND) (1 + 2^e) against ||y||_1 ~ n sqrt(2n):
-//   ND = 2: max|Δ|/‖y‖₁ ~2e-10 at n = 128, 1.5e-10 on C2 (fp64 bound 1e-9);
+// all exact (|acc| < 2^26 at n <= 2048), and the epilogue forms
+//   D = Σ_j accW_j c_j + 2^e_v Σ_j accX_j c_j,   c_0 = 1/127^2, c_1 = c_0/(128 127)
+// (fp64 for complex128, fp32 for complex64).
+// Error model: per output ~ sqrt(2n) 2^-(14 ND + 1) (1 + 2^e) against ||y||_1 ~ n sqrt(2n):
+//   ND = 2: the fp64 bound 1e-9 with a wide margin;
 //   ND = 1: the fp32 bound 1e-4 with a wide margin
 // (tests/test_gpu_ndft_i8.py).  Smaller n runs the FFMA2 / DFMA fast kernels.
 //
@@ -61,6 +62,9 @@ constexpr int TMEM_COLS = 512;
 #endif
 #ifndef SA_I8_EPI_C128
 #define SA_I8_EPI_C128 8
+#endif
+#ifndef SA_I8_T16_C128
+#define SA_I8_T16_C128 1  // complex128 epilogue reads TMEM as 16x256b: 4 lanes per row, 64-B row segments per store
 #endif
 #ifndef SA_I8_STAGE_C64
 #define SA_I8_STAGE_C64 1  // complex64 rows leave through a per-warp smem staging tile
@@ -143,9 +147,17 @@ SA_HD void cluster_sync_all() {
         "=r"(v[15])                                                                                        \
       : "r"(taddr))
 
-// The 2 ND signed digits (radix 64, 127, 128, 127; each |d| <= 64) of |v| <= 1.
+// 16 TMEM lanes x 16 columns: thread t gets lane t/4 (regs 0,1,4,5) and t/4 + 8
+// (regs 2,3,6,7), columns 2 (t%4) + {0, 1} (regs 0-3) and 8 + 2 (t%4) + {0, 1} (regs 4-7)
+#define SA_LD16x256(v, taddr)                                                                              \
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                    \
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),       \
+                 "=r"(v[7])                                                                                \
+               : "r"(taddr))
+
+// The 2 ND signed digits (radix 127, 127, 128, 127) of |v| <= 1.
 template <int ND> SA_HD void digits(double v, int (&d)[2 * ND]) {
-  double y = v * 64.0;
+  double y = v * 127.0;
 #pragma unroll
   for (int i = 0; i < 2 * ND; ++i) {
     const double r = rint(y);
@@ -243,36 +255,41 @@ __global__ void __launch_bounds__(256) k_i8_prep(const T *__restrict__ x, int8_t
     if (!(mx <= T(sizeof(T) == 4 ? 3.4028234663852886e38 : 1.7976931348623157e308))) e = INT_MAX;
     if (threadIdx.x == 0) ex[v] = e;
     if (e == INT_MAX) e = 0;  // (digits of this row are never used)
-    // x 2^-e 64: one exact power-of-two product where the scale is normal
-    const bool fast = sizeof(T) == 4 ? (e > -60 && e < 60) : (e > -900 && e < 900);
-    const T sc = (T)ldexp(1.0, 6 - e);
+    // 127 x 2^-e: an exact power-of-two product where the scale is normal, then 127
+    const bool fast = sizeof(T) == 4 ? (e > -100 && e < 100) : (e > -900 && e < 900);
+    const T sc = (T)ldexp(1.0, -e);
     int8_t *blk = planes + (size_t)(v / BM) * kslots * (NPL * XT);
     const int r = (int)(v % BM);
+    // (uniform per row: one branch, not a per-element select)
+    auto emit = [&](auto scaled) {
 #pragma unroll
-    for (int i = 0; i < IT; ++i) {
-      const int k = threadIdx.x * 8 + 2048 * i;
-      if (k < nk) {
-        uint32_t b[NPL][8];
+      for (int i = 0; i < IT; ++i) {
+        const int k = threadIdx.x * 8 + 2048 * i;
+        if (k < nk) {
+          uint32_t b[NPL][8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const T xv = t[i][j];
-          const uint32_t sg = (uint32_t)((xv > T(0)) - (xv < T(0)));
-          b[0][j] = sg;
-          b[1][j] = sg * 127u;
-          T yv = fast ? sa_mul(xv, sc) : (T)ldexp((double)xv, 6 - e);
+          for (int j = 0; j < 8; ++j) {
+            const T xv = t[i][j];
+            const uint32_t sg = (uint32_t)((xv > T(0)) - (xv < T(0)));
+            b[0][j] = sg;
+            b[1][j] = sg * 127u;
+            T yv = scaled(xv);
 #pragma unroll
-          for (int d = 0; d < 2 * ND; ++d) {
-            const T rr = rint_b(yv, b[2 + d][j]);
-            if (d + 1 < 2 * ND) yv = sa_mul(sa_sub(yv, rr), T((d & 1) ? 128.0 : 127.0));
+            for (int d = 0; d < 2 * ND; ++d) {
+              const T rr = rint_b(yv, b[2 + d][j]);
+              if (d + 1 < 2 * ND) yv = sa_mul(sa_sub(yv, rr), T((d & 1) ? 128.0 : 127.0));
+            }
           }
-        }
-        int8_t *tile = blk + (size_t)(k / KSL) * (NPL * XT) + sw64(r, k % KSL);  // 8 bytes, one swizzle chunk
+          int8_t *tile = blk + (size_t)(k / KSL) * (NPL * XT) + sw64(r, k % KSL);  // 8 bytes, one swizzle chunk
 #pragma unroll
-        for (int p = 0; p < NPL; ++p)
-          *(uint2 *)(tile + p * XT) = make_uint2(pack4(b[p][0], b[p][1], b[p][2], b[p][3]),
-                                                 pack4(b[p][4], b[p][5], b[p][6], b[p][7]));
+          for (int p = 0; p < NPL; ++p)
+            *(uint2 *)(tile + p * XT) = make_uint2(pack4(b[p][0], b[p][1], b[p][2], b[p][3]),
+                                                   pack4(b[p][4], b[p][5], b[p][6], b[p][7]));
+        }
       }
-    }
+    };
+    if (fast) emit([&](T xv) { return sa_mul(sa_mul(xv, sc), T(127)); });
+    else emit([&](T xv) { return (T)sa_mul(ldexp((double)xv, -e), 127.0); });
 #pragma unroll
     for (int i = 0; i < IT; ++i)
 #pragma unroll
@@ -423,7 +440,7 @@ __global__ void __launch_bounds__(Cfg<ND>::THREADS, 1)
     const int q = warp & 3;
     const int cs = (warp - 2) / 4;  // this warp's column share
     constexpr int CW = BN / (EPI / 4);
-    constexpr double CD = ND == 2 ? 1.0 / (64.0 * 127.0 * 128.0 * 127.0) : 1.0 / (64.0 * 127.0);
+    constexpr double CD = ND == 2 ? 1.0 / (127.0 * 127.0 * 128.0 * 127.0) : 1.0 / (127.0 * 127.0);
     uint32_t lt = 0;
     for (int64_t t = cl; t < ntiles; t += ncl, ++lt) {
       const int64_t v = (t / ot_count) * (2 * BM) + rank * BM + q * 32 + lane;
@@ -481,6 +498,53 @@ __global__ void __launch_bounds__(Cfg<ND>::THREADS, 1)
             if (vw + r < batch) __stcs((float4 *)&y[(vw + r) * nk + o0 + c + 4 * ch], val);
           }
           __syncwarp();
+        }
+      } else if constexpr (ND == 2 && SA_I8_T16_C128) {
+        // complex128, 16x256b: thread t holds rows rr(i) = t/4 + 8 (i & 1) + 16 (i >> 1) of the
+        // warp's 32 and columns 2 (t%4) + {0, 1} and 8 + 2 (t%4) + {0, 1} of each 16-column
+        // chunk; four threads store 64 contiguous bytes of a row
+        const int tj = lane & 3;
+        int er[4];
+        double sr[4];
+        bool allfast = true;
+        const int64_t vw = v - lane;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t vi = vw + (lane >> 2) + 8 * (i & 1) + 16 * (i >> 1);
+          er[i] = vi < batch ? ex[vi] : 0;
+          const bool f = er[i] > -960 && er[i] < 1030;
+          sr[i] = f ? ldexp(CD, er[i]) : 0.0;
+          allfast = allfast && f;
+        }
+#pragma unroll 1
+        for (int c = cs * CW; c < (cs + 1) * CW; c += 16) {
+          uint32_t acc[4][2][8];
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) SA_LD16x256(acc[a][h], ta + ((uint32_t)(16 * h) << 16) + a * BN + c);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int64_t vi = vw + (lane >> 2) + 8 * (i & 1) + 16 * (i >> 1);
+            const int h = i >> 1, rb = 2 * (i & 1);
+            double d[4];  // columns 2 tj, 2 tj + 1, 8 + 2 tj, 9 + 2 tj
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int rg = rb + (u & 1) + 4 * (u >> 1);
+              const double w = i51_to_f64((long long)(int)acc[0][h][rg] * (128 * 127) + (int)acc[1][h][rg]);
+              const double xs = i51_to_f64((long long)(int)acc[2][h][rg] * (128 * 127) + (int)acc[3][h][rg]);
+              if (allfast) d[u] = fma(xs, sr[i], sa_mul(w, CD));
+              else d[u] = er[i] == INT_MAX ? CUDART_NAN
+                          : (er[i] > -960 && er[i] < 1030) ? fma(xs, sr[i], sa_mul(w, CD))
+                                                           : sa_add(ldexp(sa_mul(xs, CD), er[i]), sa_mul(w, CD));
+            }
+            if (vi < batch) {
+              double *row = y + vi * nk + o0 + c + 2 * tj;
+              __stcs((double2 *)row, make_double2(d[0], d[1]));
+              __stcs((double2 *)(row + 8), make_double2(d[2], d[3]));
+            }
+          }
         }
       } else {
         // each lane stores its row, 16 B at a time
