@@ -76,6 +76,12 @@ int sa_launch_lag_tc(const void *surv, const void *ref, int64_t ref_len, int64_t
 int sa_launch_lag_tc_blocks(const void *surv, const void *ref, int64_t ref_len, int64_t l0, int64_t l_count, int64_t m,
                             int64_t q0, int64_t q_count, int64_t tb, int conj, void *z, void *const *dst_rows,
                             int64_t rows_base, int64_t rows_extra, int blocked, cudaStream_t s);
+// sa_lag_i8.cu (the same lag stage on tcgen05 kind::i8, exact integer digits; the default,
+// SA_LAG_KIND=bf16 selects sa_lag_tc.cu; SA_ERR_UNSUPPORTED -> the bf16 kernel)
+bool sa_lag_i8_enabled();
+int sa_launch_lag_i8_blocks(const void *surv, const void *ref, int64_t ref_len, int64_t l0, int64_t l_count, int64_t m,
+                            int64_t q0, int64_t q_count, int64_t tb, int conj, void *z, void *const *dst_rows,
+                            int64_t rows_base, int64_t rows_extra, int blocked, cudaStream_t s);
 // blocked z: tiles of 16 lags from the 16-aligned base (sa_lag_tc.cu), rows padded to whole tiles
 inline int64_t sa_zblk_rows(int64_t l0, int64_t l_count) { return (((l0 & 15) + l_count + 15) / 16) * 16; }
 

@@ -1,0 +1,489 @@
+// sa_lag_i8.cu -- the map's fast-mode lag stage (ambiguity.py:146-187 composed
+// with the block sums, as sa_lag_tc.cu) on the tcgen05 tensor cores in EXACT
+// INTEGER arithmetic, complex64: int8 digits x signs, int32 accumulation.
+//
+//   z_l[q] = Σ_{t<T} s[qT+t] ⊙ c[qT+t-l],   c = conj(ref) (ref outside [0, ref_len) = 0)
+//   Re = Σ sgn(sr) cr + sr sgn(cr) − sgn(si) ci − si sgn(ci)
+//   Im = Σ sgn(si) cr + si sgn(cr) + sgn(sr) ci + sr sgn(ci)
+// (the sign-split identity of the fast ⊙, sa_ambiguity.cu).  Every term has a
+// sign in {−1, 0, 1} as one factor (exact in int8); the other factor is split
+// into two signed int8 digits (radix 127, 254) of x / 2^e:
+//   x ≈ 2^e (254 d0 + d1) / (127 · 254),  |d0|, |d1| <= 127,  residual <= 2^e / 64516
+// with e per integration block for s (its T samples) and ONE e for the whole
+// reference c (so a lag's digits never depend on which lags a call covers: any
+// row range or Doppler-block shard of a map is bit-identical to the full call,
+// and integer sums do not depend on the summation order).
+//
+// Formulation ("c-Hankel").  Lag l = lb + 16 j + i (j < MR rows, i < 16 shifts),
+// u = t − i in [−16, T + 16):
+//   Z[j, i] = Σ_u A[j, u] B[i, u],   A[j, u] = c[qT − lb − 16 j + u],  B[i, u] = s[qT + u + i]
+// A is a Hankel matrix in (j, u): stored once per lag group as a linear int8
+// array per plane, rows reversed (r = MR − 1 − j) so that row r + 1 starts 16 B
+// later -- exactly the K-major no-swizzle core-matrix row pitch, so the UMMA
+// descriptor (LBO 16 B, SBO 128 B) reads it in place.  B (16 shifts of the
+// block's s planes) is materialised per K chunk from linear s planes.  The K
+// range is T + 32 whatever the lag count (no zero region).
+//
+// Planes.  A (c): d0 cr, d1 cr, d0 ci, d1 ci, sgn cr, sgn ci.
+//          B (s): sgn sr, sgn si, d0 sr, d0 si, d1 sr, d1 si.
+// Per K step (32 u) and lag group, six MMAs (M = MR, K = 32):
+//   W_p  (32 cols) += A[p] x B[sgn sr; sgn si]                   p = d0cr, d1cr, d0ci, d1ci   (N = 32)
+//   X_p  (64 cols) += A[p] x B[d0 sr; d0 si; d1 sr; d1 si]       p = sgn cr, sgn ci           (N = 64)
+// 256 TMEM columns per group.  Epilogue (per shift i, exact int32):
+//   IWre = 254 (W0r[sr] − W0i[si]) + (W1r[sr] − W1i[si]),  IWim = 254 (W0r[si] + W0i[sr]) + (W1r[si] + W1i[sr])
+//   IXre = 254 (Xr[d0sr] − Xi[d0si]) + (Xr[d1sr] − Xi[d1si]), IXim = 254 (Xr[d0si] + Xi[d0sr]) + (Xr[d1si] + Xi[d1sr])
+//   Re = IWre 2^ec / 32258 + IXre 2^es / 32258 (fp64, rounded once to fp32), Im alike.
+// Each TMEM lane holds the 16 consecutive lags of one blocked-z tile (sa_lag_tc.cu
+// layout): the thread stores one whole 128-B line.
+//
+// One CTA per integration block q: 8 builder warps (A planes per pass, B chunks;
+// warps 0-3 also drain TMEM), one MMA warp.  A non-finite value in the block
+// (s) makes its column NaN; a non-finite reference value makes the whole map NaN
+// (the exponent is global) -- the bf16 kernel (sa_lag_tc.cu) keeps NaN local.
+#include <cuda.h>
+
+#include <cfloat>
+#include <cstdlib>
+#include <math_constants.h>
+
+#include "sa_internal.h"
+#include "sa_regs.cuh"
+
+namespace {
+
+constexpr int NPL = 6;                   // planes per side
+constexpr int KC = 4;                    // K32 steps per B chunk (128 u)
+constexpr int CORE = 128;                // one core matrix: 8 rows x 16 B
+constexpr int B_SBO = 2 * KC * CORE;     // next 8 B rows
+constexpr int B_BYTES = NPL * 2 * B_SBO; // 6 planes x 16 shifts x 128 u = 12 KB
+constexpr int BUILDERS = 256;
+constexpr int THREADS = BUILDERS + 32;   // warp 8 issues the MMAs
+constexpr int NPART = 256;               // |ref| max partials
+constexpr double DSC = 1.0 / (127.0 * 254.0);
+
+struct Geo {
+  int ks, psl, pcl;
+  int off_pc, off_b, off_bar, bytes;
+};
+__host__ __device__ inline Geo geo(int tb, int mr, int g) {
+  Geo o;
+  o.ks = tb / 32 + 1;                           // u in [-16, T + 16)
+  o.psl = (32 * o.ks + 32 + 127) & ~127;        // s planes: x = u + 16 + i
+  o.pcl = (32 * o.ks + 16 * mr + 127) & ~127;   // c planes: x = u + 16 + 16 r
+  o.off_pc = NPL * o.psl;
+  o.off_b = (o.off_pc + g * NPL * o.pcl + 1023) & ~1023;
+  o.off_bar = o.off_b + 2 * B_BYTES;
+  o.bytes = o.off_bar + 256 + 1024;             // barriers, reductions, alignment slack
+  return o;
+}
+
+// kind::i8: D = s32, A = B = s8, K-major, N, M
+constexpr uint32_t idesc(int n, int mr) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(mr >> 4) << 24);
+}
+SA_HD uint64_t sdesc_ns(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(sbo >> 4) << 32) |
+         ((uint64_t)1 << 46);
+}
+SA_HD void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(acc)
+      : "memory");
+}
+SA_HD void commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   sa_smem_u32(bar))
+               : "memory");
+}
+SA_HD void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+SA_HD void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+#define SA_LD16(v, taddr)                                                                                  \
+  asm volatile(                                                                                            \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"    \
+      " [%16];"                                                                                            \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),    \
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),           \
+        "=r"(v[15])                                                                                        \
+      : "r"(taddr))
+SA_HD void tm_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// sign and the two digits of x at scale sc = 127 / 2^e (y = x sc is exact in fp64)
+SA_HD uint32_t digits(float x, double sc, uint32_t &d0, uint32_t &d1) {
+  const double y = (double)x * sc;
+  const double r0 = rint(y);
+  d0 = (uint32_t)(int)r0 & 0xffu;
+  d1 = (uint32_t)(int)rint((y - r0) * 254.0) & 0xffu;
+  return (uint32_t)((x > 0.f) - (x < 0.f)) & 0xffu;
+}
+SA_HD int exponent_of(float mx) {  // mx = f 2^e, f in [0.5, 1): max < 2^e
+  int e = 0;
+  if (mx > 0.f && mx <= FLT_MAX) frexpf(mx, &e);
+  return e;
+}
+SA_HD float amax(float2 v) {  // max |component|; +inf for a non-finite value
+  const float a = fabsf(v.x), b = fabsf(v.y);
+  return (a <= FLT_MAX && b <= FLT_MAX) ? fmaxf(a, b) : INFINITY;
+}
+
+__global__ void __launch_bounds__(256) k_lag_absmax(const float2 *__restrict__ ref, int64_t n, float *__restrict__ part) {
+  __shared__ float red[8];
+  float mx = 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    mx = fmaxf(mx, amax(__ldg(&ref[i])));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) mx = fmaxf(mx, red[w]);
+    part[blockIdx.x] = mx;
+  }
+}
+
+// Where the 16 lags of a tile go: blocked z (one 128-B line) or row-major z, local
+// or the owning rank's z block over peer memory (sa_lag_tc.cu's LagDst).
+struct LagDst {
+  float2 *const *ptr;
+  int64_t base, extra;
+  SA_HD float2 *row(float2 *z, int64_t lag, int64_t m, int64_t q) const {
+    if (!ptr) return z + lag * m + q;
+    const int64_t big = extra * (base + 1);
+    const int64_t o = lag < big ? lag / (base + 1) : extra + (lag - big) / base;
+    const int64_t first = o * base + (o < extra ? o : extra);
+    return ptr[o] + (lag - first) * m + q;
+  }
+  SA_HD float2 *line(float2 *z, int64_t k, int64_t m, int64_t q) const {
+    if (!ptr) return z + (k * m + q) * 16;
+    const int64_t o = (16 * k) / base;
+    return ptr[o] + ((k - o * (base >> 4)) * m + q) * 16;
+  }
+};
+
+template <int MR, int G, bool BLK>
+__global__ void __launch_bounds__(THREADS, 2)
+    k_lag_i8(const float2 *__restrict__ surv, const float2 *__restrict__ ref, int64_t ref_len, int64_t l0g,
+             int64_t l_count, int64_t m, int tb, float csign, const float *__restrict__ cpart, float2 *__restrict__ z,
+             int64_t q0, LagDst dst) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const Geo gm = geo(tb, MR, G);
+  unsigned char *Ps = smem;               // NPL x psl: s planes, x = t + 16
+  unsigned char *Pc = smem + gm.off_pc;   // G x NPL x pcl: c planes of the pass's groups
+  unsigned char *Bb = smem + gm.off_b;    // 2 x B_BYTES
+  uint64_t *empty = (uint64_t *)(smem + gm.off_bar);  // MMAs that read B buffer b are done
+  uint64_t *full = empty + 2;                         // B buffer b built
+  uint32_t *tmem_holder = (uint32_t *)(full + 2);
+  float *red = (float *)(tmem_holder + 2);            // 2 x 9 partial maxima
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t q = q0 + blockIdx.x;
+  const float2 *sb = surv + q * tb;
+  constexpr int LGRP = 16 * MR;  // lags per group
+  constexpr int TMEM_COLS = 256 * G;
+
+  // ---- exponents: |s| over this block, |c| over the whole reference (k_lag_absmax partials) ----
+  {
+    float ms = 0.f, mc = tid < NPART ? cpart[tid] : 0.f;
+    for (int t = tid; t < tb; t += THREADS) ms = fmaxf(ms, amax(__ldg(&sb[t])));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      ms = fmaxf(ms, __shfl_xor_sync(0xffffffffu, ms, o));
+      mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, o));
+    }
+    if (lane == 0) red[warp] = ms, red[9 + warp] = mc;
+  }
+  if (tid == 0) {
+    sa_mbar_init(&empty[0], 1);
+    sa_mbar_init(&empty[1], 1);
+    sa_mbar_init(&full[0], BUILDERS / 32);
+    sa_mbar_init(&full[1], BUILDERS / 32);
+    sa_fence_mbar_init();
+  }
+  __syncthreads();
+  float ms = 0.f, mc = 0.f;
+#pragma unroll
+  for (int w = 0; w < THREADS / 32; ++w) ms = fmaxf(ms, red[w]), mc = fmaxf(mc, red[9 + w]);
+  const bool bad = !(ms <= FLT_MAX) || !(mc <= FLT_MAX);
+  const int es = exponent_of(ms), ec = exponent_of(mc);
+  const double scs = ldexp(127.0, -es), scc = ldexp(127.0, -ec);
+
+  // ---- s planes: x in [0, psl), t = x - 16 (zero outside the block) ----
+  for (int x4 = tid; x4 < gm.psl / 4; x4 += THREADS) {
+    const int t = 4 * x4 - 16;
+    float2 v[4] = {};
+    if (t >= 0 && t < tb) {  // tb % 4 == 0: a group of 4 is all in or all out
+      const float4 a = __ldg((const float4 *)&sb[t]), b = __ldg((const float4 *)&sb[t + 2]);
+      v[0] = make_float2(a.x, a.y), v[1] = make_float2(a.z, a.w), v[2] = make_float2(b.x, b.y), v[3] = make_float2(b.z, b.w);
+    }
+    uint32_t w[NPL] = {};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      uint32_t d0r, d1r, d0i, d1i;
+      const uint32_t sr = digits(v[e].x, scs, d0r, d1r), si = digits(v[e].y, scs, d0i, d1i);
+      w[0] |= sr << (8 * e), w[1] |= si << (8 * e);
+      w[2] |= d0r << (8 * e), w[3] |= d0i << (8 * e);
+      w[4] |= d1r << (8 * e), w[5] |= d1i << (8 * e);
+    }
+#pragma unroll
+    for (int p = 0; p < NPL; ++p) ((uint32_t *)(Ps + p * gm.psl))[x4] = w[p];
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa_smem_u32(tmem_holder)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_holder;
+  const uint32_t pcbase = sa_smem_u32(Pc), bbase = sa_smem_u32(Bb);
+
+  const int64_t lalign = l0g - (l0g & 15);
+  const int ngrp = (int)((l0g - lalign + l_count + LGRP - 1) / LGRP);
+  const int npass = (ngrp + G - 1) / G;
+  const int nch = (gm.ks + KC - 1) / KC;
+  uint32_t cc = 0;  // B chunk counter across passes (buffer cc & 1)
+  for (int pi = 0; pi < npass; ++pi) {
+    const int64_t lpass = lalign + (int64_t)pi * G * LGRP;
+    const int gcount = min(G, ngrp - pi * G);
+    // ---- A: the c planes of this pass's groups (all threads) ----
+    for (int gi = 0; gi < gcount; ++gi) {
+      const int64_t cstart = q * tb - (lpass + (int64_t)gi * LGRP) - 16 * MR;  // c index of x = 0
+      unsigned char *pc = Pc + gi * NPL * gm.pcl;
+      for (int x4 = tid; x4 < gm.pcl / 4; x4 += THREADS) {
+        const int64_t k0 = cstart + 4 * x4;
+        float2 v[4];
+        if (k0 >= 0 && k0 + 4 <= ref_len) {
+          const float4 a = __ldg((const float4 *)&ref[k0]), b = __ldg((const float4 *)&ref[k0 + 2]);
+          v[0] = make_float2(a.x, a.y), v[1] = make_float2(a.z, a.w), v[2] = make_float2(b.x, b.y), v[3] = make_float2(b.z, b.w);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            v[e] = (k0 + e >= 0 && k0 + e < ref_len) ? __ldg(&ref[k0 + e]) : make_float2(0.f, 0.f);
+        }
+        uint32_t w[NPL] = {};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          uint32_t d0r, d1r, d0i, d1i;
+          const uint32_t sr = digits(v[e].x, scc, d0r, d1r), si = digits(csign * v[e].y, scc, d0i, d1i);
+          w[0] |= d0r << (8 * e), w[1] |= d1r << (8 * e);
+          w[2] |= d0i << (8 * e), w[3] |= d1i << (8 * e);
+          w[4] |= sr << (8 * e), w[5] |= si << (8 * e);
+        }
+#pragma unroll
+        for (int p = 0; p < NPL; ++p) ((uint32_t *)(pc + p * gm.pcl))[x4] = w[p];
+      }
+    }
+    sa_fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05.mma
+    fence_before();
+    __syncthreads();
+    fence_after();
+
+    if (warp == BUILDERS / 32) {
+      // ---- MMA issuer: six MMAs per K step and group; commit frees the B buffer ----
+      if (lane == 0) {
+        constexpr uint32_t IDW = idesc(32, MR), IDX = idesc(64, MR);
+        for (int ch = 0; ch < nch; ++ch, ++cc) {
+          const int b = cc & 1;
+          sa_mbar_wait(&full[b], (cc >> 1) & 1);
+          fence_after();
+          const int kn = min(KC, gm.ks - ch * KC);
+          for (int kk = 0; kk < kn; ++kk) {
+            const int kstep = ch * KC + kk;
+            const uint32_t acc = kstep != 0;
+            const uint32_t bo = bbase + b * B_BYTES + kk * 2 * CORE;
+            const uint64_t bw = sdesc_ns(bo, CORE, B_SBO), bx = sdesc_ns(bo + 4 * B_SBO, CORE, B_SBO);
+#pragma unroll
+            for (int gi = 0; gi < G; ++gi) {
+              if (gi < gcount) {
+                const uint32_t pa = pcbase + gi * NPL * gm.pcl + 32 * kstep;
+                const uint32_t tm = tmem + 256 * gi;
+                auto ad = [&](int p) { return sdesc_ns(pa + p * gm.pcl, 16, 128); };
+                mma(tm + 0, ad(0), bw, IDW, acc);
+                mma(tm + 32, ad(1), bw, IDW, acc);
+                mma(tm + 64, ad(2), bw, IDW, acc);
+                mma(tm + 96, ad(3), bw, IDW, acc);
+                mma(tm + 128, ad(4), bx, IDX, acc);
+                mma(tm + 192, ad(5), bx, IDX, acc);
+              }
+            }
+          }
+          commit(&empty[b]);
+        }
+      }
+    } else {
+      // ---- builders: B chunk = 16 shifts of the six s planes, 16-B pieces ----
+      for (int ch = 0; ch < nch; ++ch, ++cc) {
+        const int b = cc & 1;
+        if (cc >= 2) sa_mbar_wait(&empty[b], ((cc >> 1) - 1) & 1);  // MMAs that read this buffer are done
+        unsigned char *B = Bb + b * B_BYTES;
+#pragma unroll
+        for (int it = 0; it < NPL * 16 * 2 * KC / BUILDERS; ++it) {
+          const int e = it * BUILDERS + tid;
+          const int i = e & 15, kc2 = (e >> 4) & (2 * KC - 1), p = e >> 4 >> 3;  // shift, K core, plane
+          if (ch * KC + (kc2 >> 1) < gm.ks) {
+            const int x0 = 32 * ch * KC + 16 * kc2 + i;  // plane byte of B[i][u0]
+            const uint32_t *P32 = (const uint32_t *)(Ps + p * gm.psl) + (x0 >> 2);
+            const uint32_t sh = (uint32_t)(x0 & 3) * 8;
+            const uint32_t a0 = P32[0], a1 = P32[1], a2 = P32[2], a3 = P32[3], a4 = P32[4];
+            const uint4 o = make_uint4(__funnelshift_r(a0, a1, sh), __funnelshift_r(a1, a2, sh),
+                                       __funnelshift_r(a2, a3, sh), __funnelshift_r(a3, a4, sh));
+            *(uint4 *)(B + ((p * 2 + (i >> 3)) * (2 * KC) + kc2) * CORE + (i & 7) * 16) = o;
+          }
+        }
+        sa_fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) sa_mbar_arrive_local(&full[b]);
+      }
+      // ---- epilogue (warps 0-3): the last chunk's commit tracks every MMA of the pass ----
+      if (warp < 4) {
+        const uint32_t last = cc - 1;
+        sa_mbar_wait(&empty[last & 1], (last >> 1) & 1);
+        fence_after();
+        const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
+        const int r = MR == 128 ? warp * 32 + lane : warp * 16 + (lane & 15);
+        const bool live = MR == 128 || lane < 16;  // M = 64: lanes 16-31 hold no rows
+        const double cw = ldexp(DSC, ec), cx = ldexp(DSC, es);
+#pragma unroll 1
+        for (int gi = 0; gi < gcount; ++gi) {
+          const uint32_t gc = ta + 256 * gi;
+          float re[16], im[16];
+          uint32_t u[16], v[16];
+          int iw[16], ix[16];
+          // Re: W (c digits) then X (s digits)
+          SA_LD16(u, gc + 0);
+          SA_LD16(v, gc + 32);
+          tm_wait();    // W0r[sr], W1r[sr]
+#pragma unroll
+          for (int k = 0; k < 16; ++k) iw[k] = 254 * (int)u[k] + (int)v[k];
+          SA_LD16(u, gc + 80);
+          SA_LD16(v, gc + 112);
+          tm_wait();  // W0i[si], W1i[si]
+#pragma unroll
+          for (int k = 0; k < 16; ++k) iw[k] -= 254 * (int)u[k] + (int)v[k];
+          SA_LD16(u, gc + 128);
+          SA_LD16(v, gc + 160);
+          tm_wait(); // Xr[d0sr], Xr[d1sr]
+#pragma unroll
+          for (int k = 0; k < 16; ++k) ix[k] = 254 * (int)u[k] + (int)v[k];
+          SA_LD16(u, gc + 208);
+          SA_LD16(v, gc + 240);
+          tm_wait(); // Xi[d0si], Xi[d1si]
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            ix[k] -= 254 * (int)u[k] + (int)v[k];
+            re[k] = bad ? CUDART_NAN_F : (float)((double)iw[k] * cw + (double)ix[k] * cx);
+          }
+          // Im
+          SA_LD16(u, gc + 16);
+          SA_LD16(v, gc + 48);
+          tm_wait();   // W0r[si], W1r[si]
+#pragma unroll
+          for (int k = 0; k < 16; ++k) iw[k] = 254 * (int)u[k] + (int)v[k];
+          SA_LD16(u, gc + 64);
+          SA_LD16(v, gc + 96);
+          tm_wait();   // W0i[sr], W1i[sr]
+#pragma unroll
+          for (int k = 0; k < 16; ++k) iw[k] += 254 * (int)u[k] + (int)v[k];
+          SA_LD16(u, gc + 144);
+          SA_LD16(v, gc + 176);
+          tm_wait(); // Xr[d0si], Xr[d1si]
+#pragma unroll
+          for (int k = 0; k < 16; ++k) ix[k] = 254 * (int)u[k] + (int)v[k];
+          SA_LD16(u, gc + 192);
+          SA_LD16(v, gc + 224);
+          tm_wait(); // Xi[d0sr], Xi[d1sr]
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            ix[k] += 254 * (int)u[k] + (int)v[k];
+            im[k] = bad ? CUDART_NAN_F : (float)((double)iw[k] * cw + (double)ix[k] * cx);
+          }
+          // this lane: row j = MR - 1 - r, lags lb + 16 j + [0, 16) of block q
+          const int64_t lag0 = lpass + (int64_t)gi * LGRP + 16 * (MR - 1 - r);
+          if (!live) continue;
+          if constexpr (BLK) {
+            if (lag0 + 16 > l0g && lag0 < l0g + l_count) {
+              float4 *ln = reinterpret_cast<float4 *>(dst.line(z, (lag0 - lalign) >> 4, m, q));
+#pragma unroll
+              for (int k = 0; k < 8; ++k) ln[k] = make_float4(re[2 * k], im[2 * k], re[2 * k + 1], im[2 * k + 1]);
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              const int64_t row = lag0 + k - l0g;
+              if (row >= 0 && row < l_count) *dst.row(z, row, m, q) = make_float2(re[k], im[k]);
+            }
+          }
+        }
+      }
+    }
+    fence_before();
+    __syncthreads();  // MMAs of the pass done (epilogue waited), TMEM drained: the next pass may rebuild A
+    fence_after();
+  }
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+}
+
+template <int MR, int G, bool BLK>
+int launch_i8(const void *surv, const void *ref, int64_t ref_len, int64_t l0, int64_t l_count, int64_t m, int64_t q0,
+              int64_t q_count, int64_t tb, int conj, void *z, const LagDst &d, const float *cpart, cudaStream_t s) {
+  const Geo gm = geo((int)tb, MR, G);
+  static int smem_set[64] = {};  // largest smem size set per device
+  int dev = 0;
+  SA_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev >= 64 || smem_set[dev] < gm.bytes) {
+    SA_CUDA_TRY(cudaFuncSetAttribute(k_lag_i8<MR, G, BLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, gm.bytes));
+    if (dev < 64) smem_set[dev] = gm.bytes;
+  }
+  k_lag_i8<MR, G, BLK><<<(unsigned)q_count, THREADS, gm.bytes, s>>>(
+      (const float2 *)surv, (const float2 *)ref, ref_len, l0, l_count, m, (int)tb, conj ? -1.f : 1.f, cpart,
+      (float2 *)z, q0, d);
+  SA_LAUNCH_CHECK();
+  return SA_OK;
+}
+
+}  // namespace
+
+bool sa_lag_i8_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char *e = getenv("SA_LAG_KIND");
+    on = !(e && e[0] == 'b');  // SA_LAG_KIND=bf16: the bf16x2 kernel (sa_lag_tc.cu)
+  }
+  return on != 0;
+}
+
+// Lag-group shape: MR = 128 (2048 lags per group, 24 KB of A per K step) or 64
+// (1024 lags, 12 KB); per K step and group the smem operand reads (A + 8 KB of B)
+// bound the MMAs (N/2 = 128 tensor cycles per group): cost = groups x bytes.
+int sa_launch_lag_i8_blocks(const void *surv, const void *ref, int64_t ref_len, int64_t l0, int64_t l_count, int64_t m,
+                            int64_t q0, int64_t q_count, int64_t tb, int conj, void *z, void *const *dst_rows,
+                            int64_t rows_base, int64_t rows_extra, int blocked, cudaStream_t s) {
+  if (l_count == 0 || q_count == 0) return SA_OK;
+  if (((uintptr_t)ref & 15) != 0) return SA_ERR_UNSUPPORTED;
+  const int64_t span = (l0 & 15) + l_count;
+  const int64_t g128 = (span + 2047) / 2048, g64 = (span + 1023) / 1024;
+  const int mr = g64 * 20 < g128 * 32 ? 64 : 128;
+  const LagDst d{(float2 *const *)dst_rows, rows_base, rows_extra};
+  float *cpart = nullptr;
+  {
+    const int rc_ = sa_scratch_alloc((void **)&cpart, NPART * sizeof(float), s);
+    if (rc_ != SA_OK) return rc_;
+  }
+  k_lag_absmax<<<NPART, 256, 0, s>>>((const float2 *)ref, ref_len, cpart);
+  SA_LAUNCH_CHECK();
+  int rc;
+#define SA_I8_LAUNCH(MR_)                                                                                           \
+  rc = blocked ? launch_i8<MR_, 1, true>(surv, ref, ref_len, l0, l_count, m, q0, q_count, tb, conj, z, d, cpart, s) \
+               : launch_i8<MR_, 1, false>(surv, ref, ref_len, l0, l_count, m, q0, q_count, tb, conj, z, d, cpart, s)
+  if (mr == 64) SA_I8_LAUNCH(64);
+  else SA_I8_LAUNCH(128);
+#undef SA_I8_LAUNCH
+  SA_CUDA_TRY(cudaFreeAsync(cpart, s));
+  return rc;
+}

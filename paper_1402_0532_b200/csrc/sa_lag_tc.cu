@@ -417,6 +417,11 @@ int sa_launch_lag_tc_blocks(const void *surv, const void *ref, int64_t ref_len, 
                             int64_t q0, int64_t q_count, int64_t tb, int conj, void *z, void *const *dst_rows,
                             int64_t rows_base, int64_t rows_extra, int blocked, cudaStream_t s) {
   if (l_count == 0 || q_count == 0) return SA_OK;
+  if (sa_lag_i8_enabled()) {
+    const int rc = sa_launch_lag_i8_blocks(surv, ref, ref_len, l0, l_count, m, q0, q_count, tb, conj, z, dst_rows,
+                                           rows_base, rows_extra, blocked, s);
+    if (rc != SA_ERR_UNSUPPORTED) return rc;
+  }
   const LagShape sh = lag_shape(l0, l_count, tb);
   const LagDst d{(float2 *const *)dst_rows, rows_base, rows_extra};
 #define SA_LAG_LAUNCH(G, MR)                                                                                     \
