@@ -42,6 +42,7 @@
 // (the exponent is global) -- the bf16 kernel (sa_lag_tc.cu) keeps NaN local.
 #include <cuda.h>
 
+#include <algorithm>
 #include <cfloat>
 #include <cstdlib>
 #include <math_constants.h>
@@ -162,73 +163,167 @@ struct LagDst {
   }
 };
 
-template <int MR, int G, bool BLK>
-__global__ void __launch_bounds__(THREADS, 2)
-    k_lag_i8(const float2 *__restrict__ surv, const float2 *__restrict__ ref, int64_t ref_len, int64_t l0g,
-             int64_t l_count, int64_t m, int tb, float csign, const float *__restrict__ cpart, float2 *__restrict__ z,
-             int64_t q0, LagDst dst) {
+// c planes of the whole reference (one exponent ec for all of it): plane p holds
+// byte x = c[x - guard] (zero outside [0, ref_len)), p = d0 cr, d1 cr, d0 ci, d1 ci,
+// sgn cr, sgn ci; the lag kernel bulk-copies its Hankel windows out of them.
+__global__ void __launch_bounds__(256) k_lag_cprep(const float2 *__restrict__ ref, int64_t ref_len, float csign,
+                                                   const float *__restrict__ part, int64_t guard, int64_t cpl,
+                                                   unsigned char *__restrict__ planes) {
+  __shared__ float red[8];
+  float mc = part[threadIdx.x];  // NPART == blockDim.x
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mc;
+  __syncthreads();
+  for (int w = 0; w < 8; ++w) mc = fmaxf(mc, red[w]);
+  const double scc = ldexp(127.0, -exponent_of(mc));
+  for (int64_t x16 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x16 < cpl / 16;
+       x16 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k0 = 16 * x16 - guard;
+    uint32_t w[NPL][4] = {};
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      float2 v[4];
+      const int64_t k = k0 + 4 * h;
+      if (k >= 0 && k + 4 <= ref_len) {
+        const float4 a = __ldg((const float4 *)&ref[k]), b = __ldg((const float4 *)&ref[k + 2]);
+        v[0] = make_float2(a.x, a.y), v[1] = make_float2(a.z, a.w), v[2] = make_float2(b.x, b.y), v[3] = make_float2(b.z, b.w);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = (k + e >= 0 && k + e < ref_len) ? __ldg(&ref[k + e]) : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        uint32_t d0r, d1r, d0i, d1i;
+        const uint32_t sr = digits(v[e].x, scc, d0r, d1r), si = digits(csign * v[e].y, scc, d0i, d1i);
+        w[0][h] |= d0r << (8 * e), w[1][h] |= d1r << (8 * e);
+        w[2][h] |= d0i << (8 * e), w[3][h] |= d1i << (8 * e);
+        w[4][h] |= sr << (8 * e), w[5][h] |= si << (8 * e);
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < NPL; ++p)
+      *(uint4 *)(planes + p * cpl + 16 * x16) = make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
+  }
+}
+
+#ifndef SA_LAGI8_NB
+#define SA_LAGI8_NB 4  // B chunk ring depth
+#endif
+#ifndef SA_LAGI8_NACC
+#define SA_LAGI8_NACC 1  // accumulator sets in TMEM (2: the epilogue of pass p overlaps pass p + 1; 512 columns)
+#endif
+constexpr int NB = SA_LAGI8_NB;
+constexpr int NACC = SA_LAGI8_NACC;
+
+#define SA_LD8(v, taddr)                                                                                \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                  \
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),    \
+                 "=r"(v[7])                                                                             \
+               : "r"(taddr))
+SA_HD void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   sa_smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(sa_smem_u32(bar))
+               : "memory");
+}
+
+// Warp roles: 0-3 epilogue (TMEM lanes 0-127), 4-7 B builders, 8 MMA issuer, 9
+// producer (bulk copies of the A windows, double-buffered per lag-group pass).
+constexpr int NWARPS = 10;
+constexpr int WB0 = 4, WMMA = 8, WPROD = 9;
+
+template <int MR, bool BLK>
+__global__ void __launch_bounds__(NWARPS * 32, 2)
+    k_lag_i8(const float2 *__restrict__ surv, int64_t l0g, int64_t l_count, int64_t m, int tb,
+             const float *__restrict__ cpart, const unsigned char *__restrict__ cplanes, int64_t guard, int64_t cpl,
+             float2 *__restrict__ z, int64_t q0, LagDst dst) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const Geo gm = geo(tb, MR, G);
+  const Geo gm = geo(tb, MR, 2);
+  const int bbytes = B_BYTES;
   unsigned char *Ps = smem;               // NPL x psl: s planes, x = t + 16
-  unsigned char *Pc = smem + gm.off_pc;   // G x NPL x pcl: c planes of the pass's groups
-  unsigned char *Bb = smem + gm.off_b;    // 2 x B_BYTES
-  uint64_t *empty = (uint64_t *)(smem + gm.off_bar);  // MMAs that read B buffer b are done
-  uint64_t *full = empty + 2;                         // B buffer b built
-  uint32_t *tmem_holder = (uint32_t *)(full + 2);
-  float *red = (float *)(tmem_holder + 2);            // 2 x 9 partial maxima
+  unsigned char *Pc = smem + gm.off_pc;   // 2 x NPL x pcl: A windows (double-buffered)
+  unsigned char *Bb = smem + gm.off_b;    // NB x B_BYTES
+  uint64_t *bfull = (uint64_t *)(Bb + NB * bbytes);
+  uint64_t *bempty = bfull + NB;
+  uint64_t *afull = bempty + NB;
+  uint64_t *aempty = afull + 2;
+  uint64_t *tfull = aempty + 2;
+  uint64_t *tempty = tfull + NACC;
+  uint32_t *tmem_holder = (uint32_t *)(tempty + NACC);
+  float *red = (float *)(tmem_holder + 2);  // 2 x NWARPS partial maxima
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t q = q0 + blockIdx.x;
   const float2 *sb = surv + q * tb;
-  constexpr int LGRP = 16 * MR;  // lags per group
-  constexpr int TMEM_COLS = 256 * G;
+  constexpr int LGRP = 16 * MR;  // lags per group (one pass)
+  constexpr int TMEM_COLS = 256 * NACC;
 
   // ---- exponents: |s| over this block, |c| over the whole reference (k_lag_absmax partials) ----
   {
     float ms = 0.f, mc = tid < NPART ? cpart[tid] : 0.f;
-    for (int t = tid; t < tb; t += THREADS) ms = fmaxf(ms, amax(__ldg(&sb[t])));
+    for (int t = tid; t < tb; t += NWARPS * 32) ms = fmaxf(ms, amax(__ldg(&sb[t])));
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       ms = fmaxf(ms, __shfl_xor_sync(0xffffffffu, ms, o));
       mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, o));
     }
-    if (lane == 0) red[warp] = ms, red[9 + warp] = mc;
+    if (lane == 0) red[warp] = ms, red[NWARPS + warp] = mc;
   }
   if (tid == 0) {
-    sa_mbar_init(&empty[0], 1);
-    sa_mbar_init(&empty[1], 1);
-    sa_mbar_init(&full[0], BUILDERS / 32);
-    sa_mbar_init(&full[1], BUILDERS / 32);
+    for (int i = 0; i < NB; ++i) sa_mbar_init(&bfull[i], 4), sa_mbar_init(&bempty[i], 1);
+    for (int i = 0; i < 2; ++i) sa_mbar_init(&afull[i], 1), sa_mbar_init(&aempty[i], 1);
+    for (int i = 0; i < NACC; ++i) sa_mbar_init(&tfull[i], 1), sa_mbar_init(&tempty[i], 4);
     sa_fence_mbar_init();
   }
   __syncthreads();
   float ms = 0.f, mc = 0.f;
 #pragma unroll
-  for (int w = 0; w < THREADS / 32; ++w) ms = fmaxf(ms, red[w]), mc = fmaxf(mc, red[9 + w]);
+  for (int w = 0; w < NWARPS; ++w) ms = fmaxf(ms, red[w]), mc = fmaxf(mc, red[NWARPS + w]);
   const bool bad = !(ms <= FLT_MAX) || !(mc <= FLT_MAX);
   const int es = exponent_of(ms), ec = exponent_of(mc);
-  const double scs = ldexp(127.0, -es), scc = ldexp(127.0, -ec);
 
-  // ---- s planes: x in [0, psl), t = x - 16 (zero outside the block) ----
-  for (int x4 = tid; x4 < gm.psl / 4; x4 += THREADS) {
-    const int t = 4 * x4 - 16;
-    float2 v[4] = {};
-    if (t >= 0 && t < tb) {  // tb % 4 == 0: a group of 4 is all in or all out
-      const float4 a = __ldg((const float4 *)&sb[t]), b = __ldg((const float4 *)&sb[t + 2]);
-      v[0] = make_float2(a.x, a.y), v[1] = make_float2(a.z, a.w), v[2] = make_float2(b.x, b.y), v[3] = make_float2(b.z, b.w);
-    }
-    uint32_t w[NPL] = {};
+  const int64_t lalign = l0g - (l0g & 15);
+  const int npass = (int)((l0g - lalign + l_count + LGRP - 1) / LGRP);
+  const int nch = (gm.ks + KC - 1) / KC;
+  auto cstart = [&](int pi) { return q * tb - (lalign + (int64_t)pi * LGRP) - 16 * MR; };  // c index of x = 0
+
+  // ---- producer: the A windows (six plane segments) of each pass, two buffers; the
+  // first two passes are issued here, the rest (waiting for a buffer) after the role split ----
+  auto produce = [&](int pi) {
+    const int a = pi & 1;
+    if (pi >= 2) sa_mbar_wait(&aempty[a], ((pi >> 1) - 1) & 1);
+    sa_mbar_expect_tx(&afull[a], (uint32_t)(NPL * gm.pcl));
+    const unsigned char *src = cplanes + guard + cstart(pi);
+#pragma unroll 1
+    for (int p = 0; p < NPL; ++p)
+      bulk_g2s(Pc + (a * NPL + p) * gm.pcl, src + (int64_t)p * cpl, (uint32_t)gm.pcl, &afull[a]);
+  };
+  if (warp == WPROD && lane == 0)
+    for (int pi = 0; pi < min(2, npass); ++pi) produce(pi);
+  // ---- s planes: x in [0, psl), t = x - 16 (zero outside the block); all other warps ----
+  if (warp != WPROD) {
+    const double scs = ldexp(127.0, -es);
+    for (int x4 = tid; x4 < gm.psl / 4; x4 += (NWARPS - 1) * 32) {
+      const int t = 4 * x4 - 16;
+      float2 v[4] = {};
+      if (t >= 0 && t < tb) {  // tb % 4 == 0: a group of 4 is all in or all out
+        const float4 a = __ldg((const float4 *)&sb[t]), b = __ldg((const float4 *)&sb[t + 2]);
+        v[0] = make_float2(a.x, a.y), v[1] = make_float2(a.z, a.w), v[2] = make_float2(b.x, b.y), v[3] = make_float2(b.z, b.w);
+      }
+      uint32_t w[NPL] = {};
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      uint32_t d0r, d1r, d0i, d1i;
-      const uint32_t sr = digits(v[e].x, scs, d0r, d1r), si = digits(v[e].y, scs, d0i, d1i);
-      w[0] |= sr << (8 * e), w[1] |= si << (8 * e);
-      w[2] |= d0r << (8 * e), w[3] |= d0i << (8 * e);
-      w[4] |= d1r << (8 * e), w[5] |= d1i << (8 * e);
-    }
+      for (int e = 0; e < 4; ++e) {
+        uint32_t d0r, d1r, d0i, d1i;
+        const uint32_t sr = digits(v[e].x, scs, d0r, d1r), si = digits(v[e].y, scs, d0i, d1i);
+        w[0] |= sr << (8 * e), w[1] |= si << (8 * e);
+        w[2] |= d0r << (8 * e), w[3] |= d0i << (8 * e);
+        w[4] |= d1r << (8 * e), w[5] |= d1i << (8 * e);
+      }
 #pragma unroll
-    for (int p = 0; p < NPL; ++p) ((uint32_t *)(Ps + p * gm.psl))[x4] = w[p];
+      for (int p = 0; p < NPL; ++p) ((uint32_t *)(Ps + p * gm.psl))[x4] = w[p];
+    }
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa_smem_u32(tmem_holder)),
@@ -240,90 +335,60 @@ __global__ void __launch_bounds__(THREADS, 2)
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_holder;
-  const uint32_t pcbase = sa_smem_u32(Pc), bbase = sa_smem_u32(Bb);
 
-  const int64_t lalign = l0g - (l0g & 15);
-  const int ngrp = (int)((l0g - lalign + l_count + LGRP - 1) / LGRP);
-  const int npass = (ngrp + G - 1) / G;
-  const int nch = (gm.ks + KC - 1) / KC;
-  uint32_t cc = 0;  // B chunk counter across passes (buffer cc & 1)
-  for (int pi = 0; pi < npass; ++pi) {
-    const int64_t lpass = lalign + (int64_t)pi * G * LGRP;
-    const int gcount = min(G, ngrp - pi * G);
-    // ---- A: the c planes of this pass's groups (all threads) ----
-    for (int gi = 0; gi < gcount; ++gi) {
-      const int64_t cstart = q * tb - (lpass + (int64_t)gi * LGRP) - 16 * MR;  // c index of x = 0
-      unsigned char *pc = Pc + gi * NPL * gm.pcl;
-      for (int x4 = tid; x4 < gm.pcl / 4; x4 += THREADS) {
-        const int64_t k0 = cstart + 4 * x4;
-        float2 v[4];
-        if (k0 >= 0 && k0 + 4 <= ref_len) {
-          const float4 a = __ldg((const float4 *)&ref[k0]), b = __ldg((const float4 *)&ref[k0 + 2]);
-          v[0] = make_float2(a.x, a.y), v[1] = make_float2(a.z, a.w), v[2] = make_float2(b.x, b.y), v[3] = make_float2(b.z, b.w);
-        } else {
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            v[e] = (k0 + e >= 0 && k0 + e < ref_len) ? __ldg(&ref[k0 + e]) : make_float2(0.f, 0.f);
-        }
-        uint32_t w[NPL] = {};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          uint32_t d0r, d1r, d0i, d1i;
-          const uint32_t sr = digits(v[e].x, scc, d0r, d1r), si = digits(csign * v[e].y, scc, d0i, d1i);
-          w[0] |= d0r << (8 * e), w[1] |= d1r << (8 * e);
-          w[2] |= d0i << (8 * e), w[3] |= d1i << (8 * e);
-          w[4] |= sr << (8 * e), w[5] |= si << (8 * e);
-        }
-#pragma unroll
-        for (int p = 0; p < NPL; ++p) ((uint32_t *)(pc + p * gm.pcl))[x4] = w[p];
-      }
-    }
-    sa_fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05.mma
-    fence_before();
-    __syncthreads();
-    fence_after();
-
-    if (warp == BUILDERS / 32) {
-      // ---- MMA issuer: six MMAs per K step and group; commit frees the B buffer ----
-      if (lane == 0) {
-        constexpr uint32_t IDW = idesc(32, MR), IDX = idesc(64, MR);
+  if (warp == WPROD) {
+    if (lane == 0)
+      for (int pi = 2; pi < npass; ++pi) produce(pi);
+  } else if (warp == WMMA) {
+    // ---- MMA issuer: six MMAs per K step; commits free B slots, A buffers, accumulators ----
+    if (lane == 0) {
+      constexpr uint32_t IDW = idesc(32, MR), IDX = idesc(64, MR);
+      const uint32_t pcbase = sa_smem_u32(Pc), bbase = sa_smem_u32(Bb);
+      uint32_t cc = 0;
+      for (int pi = 0; pi < npass; ++pi) {
+        const int a = pi & 1, ab = pi % NACC;
+        sa_mbar_wait(&afull[a], (pi >> 1) & 1);
+        if (pi >= NACC) sa_mbar_wait(&tempty[ab], ((pi / NACC) - 1) & 1);
+        fence_after();
+        const uint32_t tm = tmem + 256 * ab;
+        const uint32_t pa0 = pcbase + a * NPL * gm.pcl;
         for (int ch = 0; ch < nch; ++ch, ++cc) {
-          const int b = cc & 1;
-          sa_mbar_wait(&full[b], (cc >> 1) & 1);
+          const int b = cc % NB;
+          sa_mbar_wait(&bfull[b], (cc / NB) & 1);
           fence_after();
           const int kn = min(KC, gm.ks - ch * KC);
           for (int kk = 0; kk < kn; ++kk) {
             const int kstep = ch * KC + kk;
             const uint32_t acc = kstep != 0;
-            const uint32_t bo = bbase + b * B_BYTES + kk * 2 * CORE;
+            const uint32_t bo = bbase + b * bbytes + kk * 2 * CORE;
             const uint64_t bw = sdesc_ns(bo, CORE, B_SBO), bx = sdesc_ns(bo + 4 * B_SBO, CORE, B_SBO);
-#pragma unroll
-            for (int gi = 0; gi < G; ++gi) {
-              if (gi < gcount) {
-                const uint32_t pa = pcbase + gi * NPL * gm.pcl + 32 * kstep;
-                const uint32_t tm = tmem + 256 * gi;
-                auto ad = [&](int p) { return sdesc_ns(pa + p * gm.pcl, 16, 128); };
-                mma(tm + 0, ad(0), bw, IDW, acc);
-                mma(tm + 32, ad(1), bw, IDW, acc);
-                mma(tm + 64, ad(2), bw, IDW, acc);
-                mma(tm + 96, ad(3), bw, IDW, acc);
-                mma(tm + 128, ad(4), bx, IDX, acc);
-                mma(tm + 192, ad(5), bx, IDX, acc);
-              }
-            }
+            const uint64_t a0 = sdesc_ns(pa0 + 32 * kstep, 16, 128);
+            const uint64_t ap = (uint64_t)(gm.pcl >> 4);  // descriptor step of one plane
+            mma(tm + 0, a0, bw, IDW, acc);
+            mma(tm + 32, a0 + ap, bw, IDW, acc);
+            mma(tm + 64, a0 + 2 * ap, bw, IDW, acc);
+            mma(tm + 96, a0 + 3 * ap, bw, IDW, acc);
+            mma(tm + 128, a0 + 4 * ap, bx, IDX, acc);
+            mma(tm + 192, a0 + 5 * ap, bx, IDX, acc);
           }
-          commit(&empty[b]);
+          commit(&bempty[b]);
         }
+        commit(&aempty[a]);
+        commit(&tfull[ab]);
       }
-    } else {
-      // ---- builders: B chunk = 16 shifts of the six s planes, 16-B pieces ----
+    }
+  } else if (warp >= WB0 && warp < WB0 + 4) {
+    // ---- builders: B chunk = 16 shifts of the six s planes, 16-B pieces ----
+    const int bt = tid - WB0 * 32;
+    uint32_t cc = 0;
+    for (int pi = 0; pi < npass; ++pi) {
       for (int ch = 0; ch < nch; ++ch, ++cc) {
-        const int b = cc & 1;
-        if (cc >= 2) sa_mbar_wait(&empty[b], ((cc >> 1) - 1) & 1);  // MMAs that read this buffer are done
-        unsigned char *B = Bb + b * B_BYTES;
+        const int b = cc % NB;
+        if (cc >= NB) sa_mbar_wait(&bempty[b], ((cc / NB) - 1) & 1);  // MMAs that read this slot are done
+        unsigned char *B = Bb + b * bbytes;
 #pragma unroll
-        for (int it = 0; it < NPL * 16 * 2 * KC / BUILDERS; ++it) {
-          const int e = it * BUILDERS + tid;
+        for (int it = 0; it < NPL * 16 * 2 * KC / 128; ++it) {
+          const int e = it * 128 + bt;
           const int i = e & 15, kc2 = (e >> 4) & (2 * KC - 1), p = e >> 4 >> 3;  // shift, K core, plane
           if (ch * KC + (kc2 >> 1) < gm.ks) {
             const int x0 = 32 * ch * KC + 16 * kc2 + i;  // plane byte of B[i][u0]
@@ -337,112 +402,101 @@ __global__ void __launch_bounds__(THREADS, 2)
         }
         sa_fence_proxy_async();
         __syncwarp();
-        if (lane == 0) sa_mbar_arrive_local(&full[b]);
+        if (lane == 0) sa_mbar_arrive_local(&bfull[b]);
       }
-      // ---- epilogue (warps 0-3): the last chunk's commit tracks every MMA of the pass ----
-      if (warp < 4) {
-        const uint32_t last = cc - 1;
-        sa_mbar_wait(&empty[last & 1], (last >> 1) & 1);
-        fence_after();
-        const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
-        const int r = MR == 128 ? warp * 32 + lane : warp * 16 + (lane & 15);
-        const bool live = MR == 128 || lane < 16;  // M = 64: lanes 16-31 hold no rows
-        const double cw = ldexp(DSC, ec), cx = ldexp(DSC, es);
+    }
+  } else if (warp < 4) {
+    // ---- epilogue: drain each pass's accumulators; lane = row r, lags of one blocked tile ----
+    const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
+    const int r = MR == 128 ? warp * 32 + lane : warp * 16 + (lane & 15);
+    const bool live = MR == 128 || lane < 16;  // M = 64: lanes 16-31 hold no rows
+    const double cw = ldexp(DSC, ec), cx = ldexp(DSC, es);
+    for (int pi = 0; pi < npass; ++pi) {
+      const int ab = pi % NACC;
+      sa_mbar_wait(&tfull[ab], (pi / NACC) & 1);
+      fence_after();
+      const uint32_t gc = ta + 256 * ab;
+      const int64_t lag0 = lalign + (int64_t)pi * LGRP + 16 * (MR - 1 - r);  // lags lag0 + [0, 16) of block q
+      const bool tile_in = BLK ? (lag0 + 16 > l0g && lag0 < l0g + l_count) : true;
 #pragma unroll 1
-        for (int gi = 0; gi < gcount; ++gi) {
-          const uint32_t gc = ta + 256 * gi;
-          float re[16], im[16];
-          uint32_t u[16], v[16];
-          int iw[16], ix[16];
-          // Re: W (c digits) then X (s digits)
-          SA_LD16(u, gc + 0);
-          SA_LD16(v, gc + 32);
-          tm_wait();    // W0r[sr], W1r[sr]
+      for (int h = 0; h < 2; ++h) {  // shifts 8h .. 8h + 7
+        const uint32_t g8 = gc + 8 * h;
+        uint32_t u[8], v[8];
+        int iw[8], ix[8];
+        float re[8], im[8];
+        SA_LD8(u, g8 + 0);   SA_LD8(v, g8 + 32);  tm_wait();  // W0r[sr], W1r[sr]
 #pragma unroll
-          for (int k = 0; k < 16; ++k) iw[k] = 254 * (int)u[k] + (int)v[k];
-          SA_LD16(u, gc + 80);
-          SA_LD16(v, gc + 112);
-          tm_wait();  // W0i[si], W1i[si]
+        for (int k = 0; k < 8; ++k) iw[k] = 254 * (int)u[k] + (int)v[k];
+        SA_LD8(u, g8 + 80);  SA_LD8(v, g8 + 112); tm_wait();  // W0i[si], W1i[si]
 #pragma unroll
-          for (int k = 0; k < 16; ++k) iw[k] -= 254 * (int)u[k] + (int)v[k];
-          SA_LD16(u, gc + 128);
-          SA_LD16(v, gc + 160);
-          tm_wait(); // Xr[d0sr], Xr[d1sr]
+        for (int k = 0; k < 8; ++k) iw[k] -= 254 * (int)u[k] + (int)v[k];
+        SA_LD8(u, g8 + 128); SA_LD8(v, g8 + 160); tm_wait();  // Xr[d0sr], Xr[d1sr]
 #pragma unroll
-          for (int k = 0; k < 16; ++k) ix[k] = 254 * (int)u[k] + (int)v[k];
-          SA_LD16(u, gc + 208);
-          SA_LD16(v, gc + 240);
-          tm_wait(); // Xi[d0si], Xi[d1si]
+        for (int k = 0; k < 8; ++k) ix[k] = 254 * (int)u[k] + (int)v[k];
+        SA_LD8(u, g8 + 208); SA_LD8(v, g8 + 240); tm_wait();  // Xi[d0si], Xi[d1si]
 #pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            ix[k] -= 254 * (int)u[k] + (int)v[k];
-            re[k] = bad ? CUDART_NAN_F : (float)((double)iw[k] * cw + (double)ix[k] * cx);
-          }
-          // Im
-          SA_LD16(u, gc + 16);
-          SA_LD16(v, gc + 48);
-          tm_wait();   // W0r[si], W1r[si]
+        for (int k = 0; k < 8; ++k) {
+          ix[k] -= 254 * (int)u[k] + (int)v[k];
+          re[k] = bad ? CUDART_NAN_F : (float)((double)iw[k] * cw + (double)ix[k] * cx);
+        }
+        SA_LD8(u, g8 + 16);  SA_LD8(v, g8 + 48);  tm_wait();  // W0r[si], W1r[si]
 #pragma unroll
-          for (int k = 0; k < 16; ++k) iw[k] = 254 * (int)u[k] + (int)v[k];
-          SA_LD16(u, gc + 64);
-          SA_LD16(v, gc + 96);
-          tm_wait();   // W0i[sr], W1i[sr]
+        for (int k = 0; k < 8; ++k) iw[k] = 254 * (int)u[k] + (int)v[k];
+        SA_LD8(u, g8 + 64);  SA_LD8(v, g8 + 96);  tm_wait();  // W0i[sr], W1i[sr]
 #pragma unroll
-          for (int k = 0; k < 16; ++k) iw[k] += 254 * (int)u[k] + (int)v[k];
-          SA_LD16(u, gc + 144);
-          SA_LD16(v, gc + 176);
-          tm_wait(); // Xr[d0si], Xr[d1si]
+        for (int k = 0; k < 8; ++k) iw[k] += 254 * (int)u[k] + (int)v[k];
+        SA_LD8(u, g8 + 144); SA_LD8(v, g8 + 176); tm_wait();  // Xr[d0si], Xr[d1si]
 #pragma unroll
-          for (int k = 0; k < 16; ++k) ix[k] = 254 * (int)u[k] + (int)v[k];
-          SA_LD16(u, gc + 192);
-          SA_LD16(v, gc + 224);
-          tm_wait(); // Xi[d0sr], Xi[d1sr]
+        for (int k = 0; k < 8; ++k) ix[k] = 254 * (int)u[k] + (int)v[k];
+        SA_LD8(u, g8 + 192); SA_LD8(v, g8 + 224); tm_wait();  // Xi[d0sr], Xi[d1sr]
 #pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            ix[k] += 254 * (int)u[k] + (int)v[k];
-            im[k] = bad ? CUDART_NAN_F : (float)((double)iw[k] * cw + (double)ix[k] * cx);
-          }
-          // this lane: row j = MR - 1 - r, lags lb + 16 j + [0, 16) of block q
-          const int64_t lag0 = lpass + (int64_t)gi * LGRP + 16 * (MR - 1 - r);
-          if (!live) continue;
+        for (int k = 0; k < 8; ++k) {
+          ix[k] += 254 * (int)u[k] + (int)v[k];
+          im[k] = bad ? CUDART_NAN_F : (float)((double)iw[k] * cw + (double)ix[k] * cx);
+        }
+        // (no divergent exit from the loop: tcgen05.ld is .sync.aligned)
+        if (live && tile_in) {
           if constexpr (BLK) {
-            if (lag0 + 16 > l0g && lag0 < l0g + l_count) {
-              float4 *ln = reinterpret_cast<float4 *>(dst.line(z, (lag0 - lalign) >> 4, m, q));
+            float4 *ln = reinterpret_cast<float4 *>(dst.line(z, (lag0 - lalign) >> 4, m, q)) + 4 * h;
 #pragma unroll
-              for (int k = 0; k < 8; ++k) ln[k] = make_float4(re[2 * k], im[2 * k], re[2 * k + 1], im[2 * k + 1]);
-            }
+            for (int k = 0; k < 4; ++k) ln[k] = make_float4(re[2 * k], im[2 * k], re[2 * k + 1], im[2 * k + 1]);
           } else {
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              const int64_t row = lag0 + k - l0g;
+            for (int k = 0; k < 8; ++k) {
+              const int64_t row = lag0 + 8 * h + k - l0g;
               if (row >= 0 && row < l_count) *dst.row(z, row, m, q) = make_float2(re[k], im[k]);
             }
           }
         }
+        __syncwarp();
       }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) sa_mbar_arrive_local(&tempty[ab]);
     }
-    fence_before();
-    __syncthreads();  // MMAs of the pass done (epilogue waited), TMEM drained: the next pass may rebuild A
-    fence_after();
   }
+  fence_before();
+  __syncthreads();
+  fence_after();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
 }
 
-template <int MR, int G, bool BLK>
-int launch_i8(const void *surv, const void *ref, int64_t ref_len, int64_t l0, int64_t l_count, int64_t m, int64_t q0,
-              int64_t q_count, int64_t tb, int conj, void *z, const LagDst &d, const float *cpart, cudaStream_t s) {
-  const Geo gm = geo((int)tb, MR, G);
+template <int MR, bool BLK>
+int launch_i8(const void *surv, int64_t l0, int64_t l_count, int64_t m, int64_t q0, int64_t q_count, int64_t tb,
+              void *z, const LagDst &d, const float *cpart, const unsigned char *cplanes, int64_t guard, int64_t cpl,
+              cudaStream_t s) {
+  const Geo gm = geo((int)tb, MR, 2);
+  const int bytes = gm.off_b + NB * B_BYTES + 512 + 1024;
   static int smem_set[64] = {};  // largest smem size set per device
   int dev = 0;
   SA_CUDA_TRY(cudaGetDevice(&dev));
-  if (dev >= 64 || smem_set[dev] < gm.bytes) {
-    SA_CUDA_TRY(cudaFuncSetAttribute(k_lag_i8<MR, G, BLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, gm.bytes));
-    if (dev < 64) smem_set[dev] = gm.bytes;
+  if (dev >= 64 || smem_set[dev] < bytes) {
+    SA_CUDA_TRY(cudaFuncSetAttribute(k_lag_i8<MR, BLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    if (dev < 64) smem_set[dev] = bytes;
   }
-  k_lag_i8<MR, G, BLK><<<(unsigned)q_count, THREADS, gm.bytes, s>>>(
-      (const float2 *)surv, (const float2 *)ref, ref_len, l0, l_count, m, (int)tb, conj ? -1.f : 1.f, cpart,
-      (float2 *)z, q0, d);
+  k_lag_i8<MR, BLK><<<(unsigned)q_count, NWARPS * 32, bytes, s>>>((const float2 *)surv, l0, l_count, m, (int)tb,
+                                                                  cpart, cplanes, guard, cpl, (float2 *)z, q0, d);
   SA_LAUNCH_CHECK();
   return SA_OK;
 }
@@ -465,25 +519,38 @@ int sa_launch_lag_i8_blocks(const void *surv, const void *ref, int64_t ref_len, 
                             int64_t q0, int64_t q_count, int64_t tb, int conj, void *z, void *const *dst_rows,
                             int64_t rows_base, int64_t rows_extra, int blocked, cudaStream_t s) {
   if (l_count == 0 || q_count == 0) return SA_OK;
-  if (((uintptr_t)ref & 15) != 0) return SA_ERR_UNSUPPORTED;
+  if (((uintptr_t)ref & 15) != 0 || tb > 4096) return SA_ERR_UNSUPPORTED;
   const int64_t span = (l0 & 15) + l_count;
   const int64_t g128 = (span + 2047) / 2048, g64 = (span + 1023) / 1024;
   const int mr = g64 * 20 < g128 * 32 ? 64 : 128;
   const LagDst d{(float2 *const *)dst_rows, rows_base, rows_extra};
-  float *cpart = nullptr;
+  // c planes: x = c index + guard over [-guard, (q0 + q_count) T + pcl)
+  const Geo gm = geo((int)tb, mr, 2);
+  const int64_t guard = ((l0 - (l0 & 15)) + span + 16 * mr + 2 * 2048 + 127) / 128 * 128;
+  const int64_t cpl = (guard + (q0 + q_count) * tb + gm.pcl + 255) / 128 * 128;
+  unsigned char *ws = nullptr;
   {
-    const int rc_ = sa_scratch_alloc((void **)&cpart, NPART * sizeof(float), s);
+    const int rc_ = sa_scratch_alloc((void **)&ws, NPART * sizeof(float) + NPL * cpl, s);
     if (rc_ != SA_OK) return rc_;
   }
+  float *cpart = (float *)ws;
+  unsigned char *cplanes = ws + NPART * sizeof(float);
   k_lag_absmax<<<NPART, 256, 0, s>>>((const float2 *)ref, ref_len, cpart);
   SA_LAUNCH_CHECK();
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t nb = std::min<int64_t>((cpl / 16 + 255) / 256, 8 * sms);
+  k_lag_cprep<<<(unsigned)nb, 256, 0, s>>>((const float2 *)ref, ref_len, conj ? -1.f : 1.f, cpart, guard, cpl,
+                                           cplanes);
+  SA_LAUNCH_CHECK();
   int rc;
-#define SA_I8_LAUNCH(MR_)                                                                                           \
-  rc = blocked ? launch_i8<MR_, 1, true>(surv, ref, ref_len, l0, l_count, m, q0, q_count, tb, conj, z, d, cpart, s) \
-               : launch_i8<MR_, 1, false>(surv, ref, ref_len, l0, l_count, m, q0, q_count, tb, conj, z, d, cpart, s)
-  if (mr == 64) SA_I8_LAUNCH(64);
-  else SA_I8_LAUNCH(128);
-#undef SA_I8_LAUNCH
-  SA_CUDA_TRY(cudaFreeAsync(cpart, s));
+  if (mr == 64)
+    rc = blocked ? launch_i8<64, true>(surv, l0, l_count, m, q0, q_count, tb, z, d, cpart, cplanes, guard, cpl, s)
+                 : launch_i8<64, false>(surv, l0, l_count, m, q0, q_count, tb, z, d, cpart, cplanes, guard, cpl, s);
+  else
+    rc = blocked ? launch_i8<128, true>(surv, l0, l_count, m, q0, q_count, tb, z, d, cpart, cplanes, guard, cpl, s)
+                 : launch_i8<128, false>(surv, l0, l_count, m, q0, q_count, tb, z, d, cpart, cplanes, guard, cpl, s);
+  SA_CUDA_TRY(cudaFreeAsync(ws, s));
   return rc;
 }
