@@ -161,6 +161,14 @@ int sa_ambiguity_integrate_v(int dtype, int lag_kind, const void *surv, const vo
                              int64_t ref_len, int64_t l0, int64_t l_count, int64_t m, int conj,
                              int mode, void *z, void *stream);
 
+/* Which tensor-core kernel runs the complex64 fast-mode lag stage (T % 128 == 0):
+ * SA_LAGK_I8 (default; int8 digits x signs on tcgen05 kind::i8, exact int32 sums,
+ * one exponent for the whole reference) or SA_LAGK_BF16 (two-piece bf16 operands,
+ * fp32 sums).  Process-wide; the environment variable SA_LAG_KIND=bf16 sets the
+ * initial value.  kind < 0 only queries.  Returns the previous kind. */
+enum sa_lag_kernel { SA_LAGK_I8 = 0, SA_LAGK_BF16 = 1 };
+int sa_lag_kernel(int kind);
+
 /* Block-sharded lag stage for multi-GPU maps (ambiguity.py:27-28: delay rows and
  * integration blocks are independent): fast-mode ⊙ lag integration of blocks
  * [q0, q0 + q_count) for lags [0, l_count), each lag row stored into the z

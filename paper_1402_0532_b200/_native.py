@@ -58,6 +58,7 @@ SIGNATURES = {
     "sa_ambiguity_map_multi": (_I, [_I, _P, _I, _I, _P, _P, _I64, _I64, _I64, _I64, _I64, ctypes.c_double, _I, _I,
                                     _I, _P, _P, _P, _P, _P]),
     "sa_enable_peer_access": (_I, [_I]),
+    "sa_lag_kernel": (_I, [_I]),
     "sa_ipc_open": (_I, [_P, ctypes.POINTER(_P)]),
     "sa_ipc_close": (_I, [_P]),
     "sa_scene_stereo_fm": (_I, [_I, _P, _I64, _D, _D, _D, _D, _D, _P, _P]),

@@ -47,8 +47,12 @@
 #include <cstdlib>
 #include <math_constants.h>
 
+#include <cooperative_groups.h>
+
 #include "sa_internal.h"
 #include "sa_regs.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -59,7 +63,7 @@ constexpr int B_SBO = 2 * KC * CORE;     // next 8 B rows
 constexpr int B_BYTES = NPL * 2 * B_SBO; // 6 planes x 16 shifts x 128 u = 12 KB
 constexpr int BUILDERS = 256;
 constexpr int THREADS = BUILDERS + 32;   // warp 8 issues the MMAs
-constexpr int NPART = 256;               // |ref| max partials
+constexpr int NPART_MAX = 2048;          // |ref| max partials (k_lag_cprep CTAs)
 constexpr double DSC = 1.0 / (127.0 * 254.0);
 
 struct Geo {
@@ -98,6 +102,11 @@ SA_HD void commit(uint64_t *bar) {
                    sa_smem_u32(bar))
                : "memory");
 }
+SA_HD bool elect_one() {
+  uint32_t p;
+  asm volatile("{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n selp.u32 %0, 1, 0, e;\n}\n" : "=r"(p));
+  return p != 0;
+}
 SA_HD void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 SA_HD void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
@@ -111,14 +120,33 @@ SA_HD void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::
       : "r"(taddr))
 SA_HD void tm_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// sign and the two digits of x at scale sc = 127 / 2^e (y = x sc is exact in fp64)
-SA_HD uint32_t digits(float x, double sc, uint32_t &d0, uint32_t &d1) {
-  const double y = (double)x * sc;
-  const double r0 = rint(y);
-  d0 = (uint32_t)(int)r0 & 0xffu;
-  d1 = (uint32_t)(int)rint((y - r0) * 254.0) & 0xffu;
-  return (uint32_t)((x > 0.f) - (x < 0.f)) & 0xffu;
-}
+// sign and the two digits of x at scale 127 / 2^e.  |e| < 100 (every practical
+// input): fp32 with the 1.5 2^23 shifter (d0 = rint(x sc) of the rounded product, the
+// residual x sc - d0 by one fma, d1 = rint(254 residual)); otherwise fp64 (x sc exact).
+// The path depends only on e, so a sample's digits are the same in every call.
+struct Dig {
+  float sf;
+  double sd;
+  bool fast;
+  SA_HD explicit Dig(int e) : sf(0.f), sd(ldexp(127.0, -e)), fast(e > -100 && e < 100) {
+    if (fast) sf = (float)sd;  // 127 x 2^-e, exact in fp32
+  }
+  SA_HD uint32_t operator()(float x, uint32_t &d0, uint32_t &d1) const {
+    if (fast) {
+      const float t0 = __fadd_rn(__fmul_rn(x, sf), 12582912.0f);
+      const float r0 = __fsub_rn(t0, 12582912.0f);
+      const float t1 = __fmaf_rn(__fmaf_rn(x, sf, -r0), 254.0f, 12582912.0f);
+      d0 = __float_as_uint(t0) & 0xffu;
+      d1 = __float_as_uint(t1) & 0xffu;
+    } else {
+      const double y = (double)x * sd;
+      const double r0 = rint(y);
+      d0 = (uint32_t)(int)r0 & 0xffu;
+      d1 = (uint32_t)(int)rint((y - r0) * 254.0) & 0xffu;
+    }
+    return (uint32_t)((x > 0.f) - (x < 0.f)) & 0xffu;
+  }
+};
 SA_HD int exponent_of(float mx) {  // mx = f 2^e, f in [0.5, 1): max < 2^e
   int e = 0;
   if (mx > 0.f && mx <= FLT_MAX) frexpf(mx, &e);
@@ -127,21 +155,6 @@ SA_HD int exponent_of(float mx) {  // mx = f 2^e, f in [0.5, 1): max < 2^e
 SA_HD float amax(float2 v) {  // max |component|; +inf for a non-finite value
   const float a = fabsf(v.x), b = fabsf(v.y);
   return (a <= FLT_MAX && b <= FLT_MAX) ? fmaxf(a, b) : INFINITY;
-}
-
-__global__ void __launch_bounds__(256) k_lag_absmax(const float2 *__restrict__ ref, int64_t n, float *__restrict__ part) {
-  __shared__ float red[8];
-  float mx = 0.f;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    mx = fmaxf(mx, amax(__ldg(&ref[i])));
-#pragma unroll
-  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < 8; ++w) mx = fmaxf(mx, red[w]);
-    part[blockIdx.x] = mx;
-  }
 }
 
 // Where the 16 lags of a tile go: blocked z (one 128-B line) or row-major z, local
@@ -166,17 +179,42 @@ struct LagDst {
 // c planes of the whole reference (one exponent ec for all of it): plane p holds
 // byte x = c[x - guard] (zero outside [0, ref_len)), p = d0 cr, d1 cr, d0 ci, d1 ci,
 // sgn cr, sgn ci; the lag kernel bulk-copies its Hankel windows out of them.
+// One cooperative launch: |ref| maxima (one partial per CTA), grid barrier, digits
+// (the second read of ref mostly hits L2).
 __global__ void __launch_bounds__(256) k_lag_cprep(const float2 *__restrict__ ref, int64_t ref_len, float csign,
-                                                   const float *__restrict__ part, int64_t guard, int64_t cpl,
+                                                   float *__restrict__ part, int64_t guard, int64_t cpl,
                                                    unsigned char *__restrict__ planes) {
   __shared__ float red[8];
-  float mc = part[threadIdx.x];  // NPART == blockDim.x
+  {
+    float mx = 0.f;
+    const int64_t n4 = (uintptr_t)ref & 15 ? 0 : ref_len / 4;  // 16-B aligned: float4 pairs
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+      const float4 a = __ldg((const float4 *)&ref[4 * i]), b = __ldg((const float4 *)&ref[4 * i + 2]);
+      mx = fmaxf(mx, fmaxf(fmaxf(amax(make_float2(a.x, a.y)), amax(make_float2(a.z, a.w))),
+                           fmaxf(amax(make_float2(b.x, b.y)), amax(make_float2(b.z, b.w)))));
+    }
+    for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ref_len;
+         i += (int64_t)gridDim.x * blockDim.x)
+      mx = fmaxf(mx, amax(__ldg(&ref[i])));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < 8; ++w) mx = fmaxf(mx, red[w]);
+      part[blockIdx.x] = mx;
+    }
+  }
+  cg::this_grid().sync();
+  float mc = 0.f;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) mc = fmaxf(mc, __ldcg(&part[i]));
 #pragma unroll
   for (int o = 16; o; o >>= 1) mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, o));
+  __syncthreads();
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mc;
   __syncthreads();
   for (int w = 0; w < 8; ++w) mc = fmaxf(mc, red[w]);
-  const double scc = ldexp(127.0, -exponent_of(mc));
+  const Dig dig(exponent_of(mc));
   for (int64_t x16 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x16 < cpl / 16;
        x16 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t k0 = 16 * x16 - guard;
@@ -195,7 +233,7 @@ __global__ void __launch_bounds__(256) k_lag_cprep(const float2 *__restrict__ re
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         uint32_t d0r, d1r, d0i, d1i;
-        const uint32_t sr = digits(v[e].x, scc, d0r, d1r), si = digits(csign * v[e].y, scc, d0i, d1i);
+        const uint32_t sr = dig(v[e].x, d0r, d1r), si = dig(csign * v[e].y, d0i, d1i);
         w[0][h] |= d0r << (8 * e), w[1][h] |= d1r << (8 * e);
         w[2][h] |= d0i << (8 * e), w[3][h] |= d1i << (8 * e);
         w[4][h] |= sr << (8 * e), w[5][h] |= si << (8 * e);
@@ -236,7 +274,7 @@ constexpr int WB0 = 4, WMMA = 8, WPROD = 9;
 template <int MR, bool BLK>
 __global__ void __launch_bounds__(NWARPS * 32, 2)
     k_lag_i8(const float2 *__restrict__ surv, int64_t l0g, int64_t l_count, int64_t m, int tb,
-             const float *__restrict__ cpart, const unsigned char *__restrict__ cplanes, int64_t guard, int64_t cpl,
+             const float *__restrict__ cpart, int npart, const unsigned char *__restrict__ cplanes, int64_t guard, int64_t cpl,
              float2 *__restrict__ z, int64_t q0, LagDst dst) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -260,9 +298,10 @@ __global__ void __launch_bounds__(NWARPS * 32, 2)
   constexpr int LGRP = 16 * MR;  // lags per group (one pass)
   constexpr int TMEM_COLS = 256 * NACC;
 
-  // ---- exponents: |s| over this block, |c| over the whole reference (k_lag_absmax partials) ----
+  // ---- exponents: |s| over this block, |c| over the whole reference (k_lag_cprep partials) ----
   {
-    float ms = 0.f, mc = tid < NPART ? cpart[tid] : 0.f;
+    float ms = 0.f, mc = 0.f;
+    for (int i = tid; i < npart; i += NWARPS * 32) mc = fmaxf(mc, cpart[i]);
     for (int t = tid; t < tb; t += NWARPS * 32) ms = fmaxf(ms, amax(__ldg(&sb[t])));
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -304,7 +343,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 2)
     for (int pi = 0; pi < min(2, npass); ++pi) produce(pi);
   // ---- s planes: x in [0, psl), t = x - 16 (zero outside the block); all other warps ----
   if (warp != WPROD) {
-    const double scs = ldexp(127.0, -es);
+    const Dig dig(es);
     for (int x4 = tid; x4 < gm.psl / 4; x4 += (NWARPS - 1) * 32) {
       const int t = 4 * x4 - 16;
       float2 v[4] = {};
@@ -316,7 +355,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 2)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         uint32_t d0r, d1r, d0i, d1i;
-        const uint32_t sr = digits(v[e].x, scs, d0r, d1r), si = digits(v[e].y, scs, d0i, d1i);
+        const uint32_t sr = dig(v[e].x, d0r, d1r), si = dig(v[e].y, d0i, d1i);
         w[0] |= sr << (8 * e), w[1] |= si << (8 * e);
         w[2] |= d0r << (8 * e), w[3] |= d0i << (8 * e);
         w[4] |= d1r << (8 * e), w[5] |= d1i << (8 * e);
@@ -340,42 +379,50 @@ __global__ void __launch_bounds__(NWARPS * 32, 2)
     if (lane == 0)
       for (int pi = 2; pi < npass; ++pi) produce(pi);
   } else if (warp == WMMA) {
-    // ---- MMA issuer: six MMAs per K step; commits free B slots, A buffers, accumulators ----
-    if (lane == 0) {
-      constexpr uint32_t IDW = idesc(32, MR), IDX = idesc(64, MR);
-      const uint32_t pcbase = sa_smem_u32(Pc), bbase = sa_smem_u32(Bb);
-      uint32_t cc = 0;
-      for (int pi = 0; pi < npass; ++pi) {
-        const int a = pi & 1, ab = pi % NACC;
-        sa_mbar_wait(&afull[a], (pi >> 1) & 1);
-        if (pi >= NACC) sa_mbar_wait(&tempty[ab], ((pi / NACC) - 1) & 1);
+    // ---- MMA issuer: the whole warp runs the (uniform) loop, so descriptors live in
+    // uniform registers; one elected lane issues each K step's six MMAs ----
+    constexpr uint32_t IDW = idesc(32, MR), IDX = idesc(64, MR);
+    const uint32_t pcbase = sa_smem_u32(Pc), bbase = sa_smem_u32(Bb);
+    const uint64_t ap = (uint64_t)(gm.pcl >> 4);  // descriptor step of one plane
+    uint32_t cc = 0;
+    for (int pi = 0; pi < npass; ++pi) {
+      const int a = pi & 1, ab = pi % NACC;
+      sa_mbar_wait(&afull[a], (pi >> 1) & 1);
+      if (pi >= NACC) sa_mbar_wait(&tempty[ab], ((pi / NACC) - 1) & 1);
+      fence_after();
+      const uint32_t tm = tmem + 256 * ab;
+      const uint32_t pa0 = pcbase + a * NPL * gm.pcl;
+      for (int ch = 0; ch < nch; ++ch, ++cc) {
+        const int b = cc % NB;
+        sa_mbar_wait(&bfull[b], (cc / NB) & 1);
         fence_after();
-        const uint32_t tm = tmem + 256 * ab;
-        const uint32_t pa0 = pcbase + a * NPL * gm.pcl;
-        for (int ch = 0; ch < nch; ++ch, ++cc) {
-          const int b = cc % NB;
-          sa_mbar_wait(&bfull[b], (cc / NB) & 1);
-          fence_after();
-          const int kn = min(KC, gm.ks - ch * KC);
-          for (int kk = 0; kk < kn; ++kk) {
-            const int kstep = ch * KC + kk;
-            const uint32_t acc = kstep != 0;
-            const uint32_t bo = bbase + b * bbytes + kk * 2 * CORE;
-            const uint64_t bw = sdesc_ns(bo, CORE, B_SBO), bx = sdesc_ns(bo + 4 * B_SBO, CORE, B_SBO);
-            const uint64_t a0 = sdesc_ns(pa0 + 32 * kstep, 16, 128);
-            const uint64_t ap = (uint64_t)(gm.pcl >> 4);  // descriptor step of one plane
-            mma(tm + 0, a0, bw, IDW, acc);
-            mma(tm + 32, a0 + ap, bw, IDW, acc);
-            mma(tm + 64, a0 + 2 * ap, bw, IDW, acc);
-            mma(tm + 96, a0 + 3 * ap, bw, IDW, acc);
-            mma(tm + 128, a0 + 4 * ap, bx, IDX, acc);
-            mma(tm + 192, a0 + 5 * ap, bx, IDX, acc);
-          }
-          commit(&bempty[b]);
+        const int kn = min(KC, gm.ks - ch * KC);
+        for (int kk = 0; kk < kn; ++kk) {
+          const int kstep = ch * KC + kk;
+          const uint32_t bo = bbase + b * B_BYTES + kk * 2 * CORE;
+          const uint64_t bw = sdesc_ns(bo, CORE, B_SBO), bx = sdesc_ns(bo + 4 * B_SBO, CORE, B_SBO);
+          const uint64_t a0 = sdesc_ns(pa0 + 32 * kstep, 16, 128);
+          asm volatile(
+              "{\n .reg .pred e, p;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %12, 0;\n"
+              "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %6, %10, %13, p;\n"
+              "@e tcgen05.mma.cta_group::1.kind::i8 [%1], %7, %10, %13, p;\n"
+              "@e tcgen05.mma.cta_group::1.kind::i8 [%2], %8, %10, %13, p;\n"
+              "@e tcgen05.mma.cta_group::1.kind::i8 [%3], %9, %10, %13, p;\n"
+              "@e tcgen05.mma.cta_group::1.kind::i8 [%4], %14, %11, %15, p;\n"
+              "@e tcgen05.mma.cta_group::1.kind::i8 [%5], %16, %11, %15, p;\n}\n" ::"r"(tm),
+              "r"(tm + 32), "r"(tm + 64), "r"(tm + 96), "r"(tm + 128), "r"(tm + 192), "l"(a0), "l"(a0 + ap),
+              "l"(a0 + 2 * ap), "l"(a0 + 3 * ap), "l"(bw), "l"(bx), "r"((uint32_t)(kstep != 0)), "r"(IDW),
+              "l"(a0 + 4 * ap), "r"(IDX), "l"(a0 + 5 * ap)
+              : "memory");
         }
+        if (elect_one()) commit(&bempty[b]);
+        __syncwarp();
+      }
+      if (elect_one()) {
         commit(&aempty[a]);
         commit(&tfull[ab]);
       }
+      __syncwarp();
     }
   } else if (warp >= WB0 && warp < WB0 + 4) {
     // ---- builders: B chunk = 16 shifts of the six s planes, 16-B pieces ----
@@ -484,7 +531,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 2)
 
 template <int MR, bool BLK>
 int launch_i8(const void *surv, int64_t l0, int64_t l_count, int64_t m, int64_t q0, int64_t q_count, int64_t tb,
-              void *z, const LagDst &d, const float *cpart, const unsigned char *cplanes, int64_t guard, int64_t cpl,
+              void *z, const LagDst &d, const float *cpart, int npart, const unsigned char *cplanes, int64_t guard, int64_t cpl,
               cudaStream_t s) {
   const Geo gm = geo((int)tb, MR, 2);
   const int bytes = gm.off_b + NB * B_BYTES + 512 + 1024;
@@ -496,20 +543,26 @@ int launch_i8(const void *surv, int64_t l0, int64_t l_count, int64_t m, int64_t 
     if (dev < 64) smem_set[dev] = bytes;
   }
   k_lag_i8<MR, BLK><<<(unsigned)q_count, NWARPS * 32, bytes, s>>>((const float2 *)surv, l0, l_count, m, (int)tb,
-                                                                  cpart, cplanes, guard, cpl, (float2 *)z, q0, d);
+                                                                  cpart, npart, cplanes, guard, cpl, (float2 *)z, q0, d);
   SA_LAUNCH_CHECK();
   return SA_OK;
 }
 
 }  // namespace
 
-bool sa_lag_i8_enabled() {
-  static int on = -1;
-  if (on < 0) {
+static int g_lag_kind = -1;  // sa_lag_kernel: SA_LAGK_I8 / SA_LAGK_BF16
+static int lag_kind_now() {
+  if (g_lag_kind < 0) {
     const char *e = getenv("SA_LAG_KIND");
-    on = !(e && e[0] == 'b');  // SA_LAG_KIND=bf16: the bf16x2 kernel (sa_lag_tc.cu)
+    g_lag_kind = (e && e[0] == 'b') ? SA_LAGK_BF16 : SA_LAGK_I8;
   }
-  return on != 0;
+  return g_lag_kind;
+}
+bool sa_lag_i8_enabled() { return lag_kind_now() == SA_LAGK_I8; }
+extern "C" int sa_lag_kernel(int kind) {
+  const int prev = lag_kind_now();
+  if (kind == SA_LAGK_I8 || kind == SA_LAGK_BF16) g_lag_kind = kind;
+  return prev;
 }
 
 // Lag-group shape: MR = 128 (2048 lags per group, 24 KB of A per K step) or 64
@@ -530,27 +583,31 @@ int sa_launch_lag_i8_blocks(const void *surv, const void *ref, int64_t ref_len, 
   const int64_t cpl = (guard + (q0 + q_count) * tb + gm.pcl + 255) / 128 * 128;
   unsigned char *ws = nullptr;
   {
-    const int rc_ = sa_scratch_alloc((void **)&ws, NPART * sizeof(float) + NPL * cpl, s);
+    const int rc_ = sa_scratch_alloc((void **)&ws, NPART_MAX * sizeof(float) + NPL * cpl, s);
     if (rc_ != SA_OK) return rc_;
   }
   float *cpart = (float *)ws;
-  unsigned char *cplanes = ws + NPART * sizeof(float);
-  k_lag_absmax<<<NPART, 256, 0, s>>>((const float2 *)ref, ref_len, cpart);
-  SA_LAUNCH_CHECK();
-  int sms = 148, dev = 0;
-  cudaGetDevice(&dev);
+  unsigned char *cplanes = ws + NPART_MAX * sizeof(float);
+  int sms = 148, dev = 0, per_sm = 1;
+  SA_CUDA_TRY(cudaGetDevice(&dev));
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t nb = std::min<int64_t>((cpl / 16 + 255) / 256, 8 * sms);
-  k_lag_cprep<<<(unsigned)nb, 256, 0, s>>>((const float2 *)ref, ref_len, conj ? -1.f : 1.f, cpart, guard, cpl,
-                                           cplanes);
-  SA_LAUNCH_CHECK();
+  SA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lag_cprep, 256, 0));
+  int npart = (int)std::min<int64_t>(std::min<int64_t>((int64_t)per_sm * sms, NPART_MAX), (cpl / 16 + 255) / 256);
+  npart = std::max(npart, 1);
+  {
+    float cs = conj ? -1.f : 1.f;
+    const float2 *rp = (const float2 *)ref;
+    void *args[] = {(void *)&rp, (void *)&ref_len, (void *)&cs, (void *)&cpart, (void *)&guard, (void *)&cpl,
+                    (void *)&cplanes};
+    SA_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_lag_cprep, dim3(npart), dim3(256), args, 0, s));
+  }
   int rc;
   if (mr == 64)
-    rc = blocked ? launch_i8<64, true>(surv, l0, l_count, m, q0, q_count, tb, z, d, cpart, cplanes, guard, cpl, s)
-                 : launch_i8<64, false>(surv, l0, l_count, m, q0, q_count, tb, z, d, cpart, cplanes, guard, cpl, s);
+    rc = blocked ? launch_i8<64, true>(surv, l0, l_count, m, q0, q_count, tb, z, d, cpart, npart, cplanes, guard, cpl, s)
+                 : launch_i8<64, false>(surv, l0, l_count, m, q0, q_count, tb, z, d, cpart, npart, cplanes, guard, cpl, s);
   else
-    rc = blocked ? launch_i8<128, true>(surv, l0, l_count, m, q0, q_count, tb, z, d, cpart, cplanes, guard, cpl, s)
-                 : launch_i8<128, false>(surv, l0, l_count, m, q0, q_count, tb, z, d, cpart, cplanes, guard, cpl, s);
+    rc = blocked ? launch_i8<128, true>(surv, l0, l_count, m, q0, q_count, tb, z, d, cpart, npart, cplanes, guard, cpl, s)
+                 : launch_i8<128, false>(surv, l0, l_count, m, q0, q_count, tb, z, d, cpart, npart, cplanes, guard, cpl, s);
   SA_CUDA_TRY(cudaFreeAsync(ws, s));
   return rc;
 }

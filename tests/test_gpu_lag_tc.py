@@ -1,5 +1,7 @@
-"""GPU parity of the tensor-core lag integration (sa_lag_tc.cu: fast mode,
-complex64, T % 128 == 0) through the C ABI sa_ambiguity_integrate, against an
+"""GPU parity of the tensor-core lag integration (fast mode, complex64,
+T % 128 == 0; both kernels: sa_lag_i8.cu, int8 digits with exact int32 sums, the
+default, and sa_lag_tc.cu, bf16x2 pieces with fp32 sums, selected by
+sa_lag_kernel) through the C ABI sa_ambiguity_integrate, against an
 fp64 numpy restatement of z_l[q] = Σ_t surv[qT+t] ⊙ conj(ref[qT+t-l])
 (ambiguity.py:116-131,146-155 block-summed), at the fp32 bound
 max_k |Δ_k| / ||z_row||_1 <= 1e-4 (tests/parity.py)."""
@@ -12,6 +14,16 @@ import pytest
 from parity import TOL_F32, assert_literal
 
 pytestmark = pytest.mark.gpu
+SA_LAGK_I8, SA_LAGK_BF16 = 0, 1
+
+
+@pytest.fixture(params=["i8", "bf16"])
+def lagk(request, sa):
+    """Run the test with each lag kernel (process-wide switch, restored after)."""
+    from paper_1402_0532_b200 import _native
+    prev = _native.lib().sa_lag_kernel(SA_LAGK_I8 if request.param == "i8" else SA_LAGK_BF16)
+    yield request.param
+    _native.lib().sa_lag_kernel(prev)
 
 
 def mf(a, b):
@@ -61,7 +73,7 @@ def signals(seed, ns):
 @pytest.mark.parametrize("tb,m,l0,L,conj", [(128, 16, 0, 70, True), (256, 8, 3, 1024, True),
                                              (2048, 8, 0, 1030, True), (2048, 4, 1000, 300, False),
                                              (4096, 4, 17, 2100, True)])
-def test_lag_tc_vs_fp64(sa, tb, m, l0, L, conj):
+def test_lag_tc_vs_fp64(sa, lagk, tb, m, l0, L, conj):
     surv, ref = signals(tb + L, tb * m)
     z = integrate(sa, surv, ref, l0, L, m, conj)
     r = z_ref(surv, ref, l0, L, m, conj)
@@ -70,7 +82,7 @@ def test_lag_tc_vs_fp64(sa, tb, m, l0, L, conj):
     assert e.max() < 1e-5
 
 
-def test_lag_tc_shard_offsets_bit_identical(sa):
+def test_lag_tc_shard_offsets_bit_identical(sa, lagk):
     """Lag shards reproduce the single-call rows bit for bit, whatever lag they
     start at (groups are aligned to lag multiples of 16, so every product keeps
     its u alignment inside the MMA K steps): sharded maps equal the single-GPU map."""
@@ -80,7 +92,7 @@ def test_lag_tc_shard_offsets_bit_identical(sa):
         assert np.array_equal(integrate(sa, surv, ref, a, b - a, 8), full[a:b]), (a, b)
 
 
-def test_lag_tc_map_c4_rows(sa):
+def test_lag_tc_map_c4_rows(sa, lagk):
     """C4 map (lag stage on the tensor cores, Doppler NL-FFT) on target rows vs the oracle."""
     import oracle
     import torch
@@ -115,7 +127,7 @@ def test_map_ndft_doppler_tc_rows(sa):
 
 
 @pytest.mark.parametrize("l0", [3, 13])
-def test_lag_tc_short_ref_never_read_past_end(sa, l0):
+def test_lag_tc_short_ref_never_read_past_end(sa, lagk, l0):
     """lag groups start at multiples of 16, so lags below l0 reach
     ref[ns - lalign - 1] > ref_len - 1 when ref is trimmed to ns - l0 (allowed by
     the lag_product_mf guards, ambiguity.py:121-128).  The words past ref_len are
@@ -137,3 +149,39 @@ def test_lag_tc_short_ref_never_read_past_end(sa, l0):
     got = z.cpu().numpy()
     assert np.isfinite(got).all()
     assert_literal(got, z_ref(surv, ref[:rl], l0, L, m), TOL_F32)
+
+
+@pytest.mark.parametrize("ss,rs", [(1e-35, 1e30), (3e25, 2e-30), (1.0, 1.0)])
+def test_lag_i8_extreme_scales(sa, ss, rs):
+    """int8 digits: the exponents (per block for surv, one for the reference) take
+    the fp64 digit path outside |e| < 100; results stay within the fp32 bound."""
+    from paper_1402_0532_b200 import _native
+    prev = _native.lib().sa_lag_kernel(SA_LAGK_I8)
+    try:
+        surv, ref = signals(99, 2048 * 4)
+        surv = (surv * np.float32(ss)).astype(np.complex64)
+        ref = (ref * np.float32(rs)).astype(np.complex64)
+        z = integrate(sa, surv, ref, 5, 600, 4)
+        assert np.isfinite(z).all()
+        assert_literal(z, z_ref(surv, ref, 5, 600, 4), TOL_F32)
+    finally:
+        _native.lib().sa_lag_kernel(prev)
+
+
+def test_lag_i8_nonfinite(sa):
+    """A NaN in a surveillance block makes that block's column NaN (every lag of
+    the block reads it); a non-finite reference value makes every row NaN (the
+    reference shares one exponent)."""
+    from paper_1402_0532_b200 import _native
+    prev = _native.lib().sa_lag_kernel(SA_LAGK_I8)
+    try:
+        surv, ref = signals(5, 2048 * 4)
+        s2 = surv.copy()
+        s2[2048 + 7] = np.nan
+        z = integrate(sa, s2, ref, 0, 64, 4)
+        assert np.isnan(z[:, 1]).all() and np.isfinite(z[:, [0, 2, 3]]).all()
+        r2 = ref.copy()
+        r2[100] = np.inf
+        assert np.isnan(integrate(sa, surv, r2, 0, 64, 4)).all()
+    finally:
+        _native.lib().sa_lag_kernel(prev)
