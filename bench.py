@@ -595,29 +595,46 @@ def wl_writer(args):
                        "threads": len(os.sched_getaffinity(0))}}
 
 
+def lag_is_i8():
+    from paper_1402_0532_b200 import _native
+    return _native.lib().sa_lag_kernel(-1) == 0
+
+
 def lag_kernel(dtype):
     """The lag-integration kernel sa_ambiguity_integrate runs for T = 2048: the
-    tcgen05 Hankel GEMM for complex64 (sa_lag_tc.cu), FP64 tiles otherwise."""
-    return "k_lag_tc" if dtype == "c64" else "k_lag_integrate_fast<double>"
+    tcgen05 kind::i8 Hankel GEMM for complex64 (sa_lag_i8.cu; sa_lag_tc.cu's bf16
+    kernel with SA_LAG_KIND=bf16), FP64 tiles otherwise."""
+    if dtype != "c64":
+        return "k_lag_integrate_fast<double>"
+    return "k_lag_i8" if lag_is_i8() else "k_lag_tc"
 
 
 def roof_lag(dtype, ns, lags, lms):
-    """Lag stage roofline: complex64 on tcgen05 against the measured bf16 peak
-    (32 tensor flop per ⊙: 8 sign-split terms x 2 bf16 pieces, as the NDFT);
-    complex128 against the live DFMA peak (16 flop per ⊙)."""
+    """Lag stage roofline.  complex64: 32 tensor ops per lag ⊙ on tcgen05 -- int8
+    (sa_lag_i8.cu: 8 sign x digit terms x 2 digits x re/im pairs = 16 int8 MACs)
+    against the int8 rate (2 x the measured bf16 burst figure), or bf16 (sa_lag_tc.cu:
+    8 sign-split terms x 2 pieces) against the bf16 figure.  lms is the whole lag
+    stage (the reference digit prep included).  complex128 against the live DFMA
+    peak (16 flop per ⊙)."""
     if dtype == "c64":
         peaks, src = measured_peaks()
-        peak = peaks.get("bf16_tflops", 1590.0)
+        i8 = lag_is_i8()
+        peak = peaks.get("bf16_tflops", 1590.0) * (2.0 if i8 else 1.0)
         ach = 32 * ns * lags / (lms * 1e-3) / 1e12
         tr = ncu_traffic(lag_kernel(dtype))
-        return {"bound": "tensor", "achieved": round(ach, 1), "peak": peak, "unit": "TFLOP/s",
+        return {"bound": "tensor", "achieved": round(ach, 1), "peak": round(peak, 1),
+                "unit": "TOP/s" if i8 else "TFLOP/s",
                 "frac": round(ach / peak, 4), "traffic": tr["bytes_per_launch"] if tr else None,
                 "traffic_unit": "bytes/launch", "traffic_source": tr["source"] if tr else None,
-                "kernel": lag_kernel(dtype), "kernel_ms": lms,
-                "peak_source": f"{src} bf16_tflops (burst)", "nominal_peak": 2250.0,
-                "frac_nominal": round(ach / 2250.0, 4),
-                "algorithmic": "32 bf16 tensor flop per lag ⊙ (8 sign-split terms x 2 pieces); the Hankel "
-                               "K range (T + 1024 per T samples) is overhead, not counted"}
+                "kernel": lag_kernel(dtype) + (" (+ k_lag_cprep)" if i8 else ""), "kernel_ms": lms,
+                "peak_source": (f"2 x {src} bf16_tflops (int8 dense = 2 x bf16 on B200; int8 not measured)" if i8
+                                else f"{src} bf16_tflops (burst)"),
+                "nominal_peak": 4500.0 if i8 else 2250.0, "frac_nominal": round(ach / (4500.0 if i8 else 2250.0), 4),
+                "algorithmic": ("32 int8 tensor ops per lag ⊙ (sign x 2-digit terms: 16 MACs); K = T + 32 per block "
+                                "(c-Hankel: no zero region)") if i8 else
+                               ("32 bf16 tensor flop per lag ⊙ (8 sign-split terms x 2 pieces); the Hankel "
+                                "K range (T + 1024 per T samples) is overhead, not counted"),
+                **({"ncu_utilisation_pct": tr["ncu"]} if tr and tr.get("ncu") else {})}
     peak = fma_peak_tflops(dtype)
     ach = 16 * ns * lags / (lms * 1e-3) / 1e12
     return {"bound": "fp64_alu", "achieved": round(ach, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
@@ -682,7 +699,7 @@ def wl_map(args, ws, rank, c5=False, e2e=False):
             return pm.full if pm is not None else full
         return out
 
-    res = {"ops": ops, "cells": L * M, "step": step, "lag_only": lag_only, "launches_per_step": 2,
+    res = {"ops": ops, "cells": L * M, "step": step, "lag_only": lag_only, "launches_per_step": 3 if args.dtype == "c64" else 2,
            "result": result, "surv": surv, "ref": ref,
            "config": {"workload": ("C5" if c5 else "C4") + " ⊙ range-Doppler map (BASELINE.json configs["
                       + ("4" if c5 else "3") + "])", "ns": ns, "delay_bins": L, "doppler_bins": M,
@@ -696,7 +713,9 @@ def wl_map(args, ws, rank, c5=False, e2e=False):
                               (", rows stored by the transform kernels into rank 0's IPC-shared map over NVLink, "
                                "one completion all-reduce" if transport == "p2p" else ", NCCL gather to rank 0")
                               if ws > 1 else ""))},
-           "dtype": "bf16x2-split x sign, f32 accumulate (lag); f32 (NL-FFT)" if args.dtype == "c64" else "f64"}
+           "dtype": (("int8 digits x sign, exact int32 accumulate, f64->f32 epilogue (lag)" if lag_is_i8() else
+                      "bf16x2-split x sign, f32 accumulate (lag)") + "; f32 (NL-FFT)") if args.dtype == "c64"
+           else "f64"}
     if e2e and not args.no_e2e:
         hs = torch.from_numpy(sc.surv).to(cdt).pin_memory()
         hr = torch.from_numpy(sc.ref).to(cdt).pin_memory()
