@@ -66,6 +66,9 @@ constexpr int TMEM_COLS = 512;
 #ifndef SA_I8_T16_C128
 #define SA_I8_T16_C128 1  // complex128 epilogue reads TMEM as 16x256b: 4 lanes per row, 64-B row segments per store
 #endif
+#ifndef SA_I8_PREP_WARP
+#define SA_I8_PREP_WARP 1  // complex64 digit prep: one warp per row (0: one CTA per row)
+#endif
 #ifndef SA_I8_STAGE_C64
 #define SA_I8_STAGE_C64 1  // complex64 rows leave through a per-warp smem staging tile
 #endif
@@ -294,6 +297,77 @@ __global__ void __launch_bounds__(256) k_i8_prep(const T *__restrict__ x, int8_t
     for (int i = 0; i < IT; ++i)
 #pragma unroll
       for (int j = 0; j < 8; ++j) t[i][j] = tn[i][j];
+  }
+}
+
+// complex64, n <= 1024: one WARP per row (no block barriers), NV float4 per lane
+// held in registers (k = 4 lane + 128 i: every load instruction is 512 contiguous
+// bytes), warp-shuffle maximum, one 4-byte store per plane per float4 (a warp
+// writes two whole 64-B tile rows).  Digits exactly as k_i8_prep.
+template <int ND, int NV>
+__global__ void __launch_bounds__(256) k_i8_prep_w(const float *__restrict__ x, int8_t *__restrict__ planes,
+                                                   int *__restrict__ ex, int64_t batch, int n, float gain,
+                                                   int use_gain) {
+  constexpr int NPL = Cfg<ND>::NPL;
+  const int lane = threadIdx.x & 31;
+  const int nk = 2 * n;
+  const int kslots = nk / KSL;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = w0; v < batch; v += nw) {
+    const float *row = x + v * nk;
+    float4 t[NV];
+    float mx = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int k = 4 * lane + 128 * i;
+      t[i] = k < nk ? __ldcs((const float4 *)&row[k]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      if (use_gain) t[i] = make_float4(sa_mul(gain, t[i].x), sa_mul(gain, t[i].y), sa_mul(gain, t[i].z), sa_mul(gain, t[i].w));
+      const float a[4] = {fabsf(t[i].x), fabsf(t[i].y), fabsf(t[i].z), fabsf(t[i].w)};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) mx = a[j] == a[j] ? fmaxf(mx, a[j]) : INFINITY;  // a NaN makes the row non-finite
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    int e = 0;
+    if (mx > 0.f) frexp((double)mx, &e);  // mx = f 2^e, f in [0.5, 1): max < 2^e
+    if (!(mx <= 3.4028234663852886e38f)) e = INT_MAX;
+    if (lane == 0) ex[v] = e;
+    if (e == INT_MAX) e = 0;  // (digits of this row are never used)
+    const bool fast = e > -100 && e < 100;
+    const float sc = (float)ldexp(1.0, -e);
+    int8_t *blk = planes + (size_t)(v / BM) * kslots * (NPL * XT);
+    const int r = (int)(v % BM);
+    auto emit = [&](auto scaled) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const int k = 4 * lane + 128 * i;
+        if (k < nk) {
+          const float xs[4] = {t[i].x, t[i].y, t[i].z, t[i].w};
+          uint32_t b[NPL][4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float xv = xs[j];
+            const uint32_t sg = (uint32_t)((xv > 0.f) - (xv < 0.f));
+            b[0][j] = sg;
+            b[1][j] = sg * 127u;
+            float yv = scaled(xv);
+#pragma unroll
+            for (int d = 0; d < 2 * ND; ++d) {
+              const float rr = rint_b(yv, b[2 + d][j]);
+              if (d + 1 < 2 * ND) yv = sa_mul(sa_sub(yv, rr), (d & 1) ? 128.0f : 127.0f);
+            }
+          }
+          int8_t *tile = blk + (size_t)(k / KSL) * (NPL * XT) + sw64(r, k % KSL);  // 4 bytes, inside one chunk
+#pragma unroll
+          for (int p = 0; p < NPL; ++p) *(uint32_t *)(tile + p * XT) = pack4(b[p][0], b[p][1], b[p][2], b[p][3]);
+        }
+      }
+    };
+    if (fast) emit([&](float xv) { return sa_mul(sa_mul(xv, sc), 127.0f); });
+    else emit([&](float xv) { return (float)sa_mul(ldexp((double)xv, -e), 127.0); });
   }
 }
 
@@ -648,14 +722,31 @@ int launch_i8(const void *x, void *y, int64_t batch, int64_t n, SaTwiddles *tw, 
   int dev = 0, sms = 148;
   SA_CUDA_TRY(cudaGetDevice(&dev));
   SA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  // one row per CTA iteration, one wave of resident CTAs
-  auto prep = n <= 1024 ? k_i8_prep<ND, T, 1> : k_i8_prep<ND, T, 2>;
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prep, 256, 0) != cudaSuccess || per_sm < 1) per_sm = 2;
-  const int64_t pmax = (int64_t)per_sm * sms;
-  prep<<<(unsigned)(batch < pmax ? batch : pmax), 256, 0, s>>>((const T *)x, planes, ex, batch, (int)n, (T)gain,
-                                                               (int)(gain != 1.0));
-  SA_LAUNCH_CHECK();
+  if constexpr (ND == 1 && SA_I8_PREP_WARP) {
+    // complex64, n <= 1024: one warp per row, a wave of resident CTAs
+    if (n <= 1024) {
+      auto prepw = n <= 512 ? k_i8_prep_w<1, 8> : k_i8_prep_w<1, 16>;
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prepw, 256, 0) != cudaSuccess || per_sm < 1)
+        per_sm = 2;
+      const int64_t need = (batch + 7) / 8, pmax = (int64_t)per_sm * sms;
+      prepw<<<(unsigned)(need < pmax ? need : pmax), 256, 0, s>>>((const float *)x, planes, ex, batch, (int)n,
+                                                                  (float)gain, (int)(gain != 1.0));
+      SA_LAUNCH_CHECK();
+      goto prepped;
+    }
+  }
+  {
+    // one row per CTA iteration, one wave of resident CTAs
+    auto prep = n <= 1024 ? k_i8_prep<ND, T, 1> : k_i8_prep<ND, T, 2>;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prep, 256, 0) != cudaSuccess || per_sm < 1) per_sm = 2;
+    const int64_t pmax = (int64_t)per_sm * sms;
+    prep<<<(unsigned)(batch < pmax ? batch : pmax), 256, 0, s>>>((const T *)x, planes, ex, batch, (int)n, (T)gain,
+                                                                 (int)(gain != 1.0));
+    SA_LAUNCH_CHECK();
+  }
+prepped:
   static bool smem_set[64] = {};
   if (dev >= 64 || !smem_set[dev]) {
     SA_CUDA_TRY(cudaFuncSetAttribute(k_ndft_i8<ND, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
