@@ -577,10 +577,15 @@ int sa_launch_lag_i8_blocks(const void *surv, const void *ref, int64_t ref_len, 
   const int64_t g128 = (span + 2047) / 2048, g64 = (span + 1023) / 1024;
   const int mr = g64 * 20 < g128 * 32 ? 64 : 128;
   const LagDst d{(float2 *const *)dst_rows, rows_base, rows_extra};
-  // c planes: x = c index + guard over [-guard, (q0 + q_count) T + pcl)
+  // c planes over the windows this call's blocks read: c index = x - guard, x in [0, cpl)
+  // (a block-sharded rank digitises only its own blocks' range; the exponent is
+  // still that of the whole reference)
   const Geo gm = geo((int)tb, mr, 2);
-  const int64_t guard = ((l0 - (l0 & 15)) + span + 16 * mr + 2 * 2048 + 127) / 128 * 128;
-  const int64_t cpl = (guard + (q0 + q_count) * tb + gm.pcl + 255) / 128 * 128;
+  const int64_t lgrp = 16 * mr, npass = (span + lgrp - 1) / lgrp;
+  const int64_t clo = q0 * tb - (l0 - (l0 & 15)) - npass * lgrp - 16 * mr - 128;  // a multiple of 16
+  const int64_t chi = (q0 + q_count) * tb + gm.pcl + 128;
+  const int64_t guard = -clo;
+  const int64_t cpl = (chi - clo + 127) / 128 * 128;
   unsigned char *ws = nullptr;
   {
     const int rc_ = sa_scratch_alloc((void **)&ws, NPART_MAX * sizeof(float) + NPL * cpl, s);
