@@ -185,3 +185,22 @@ def test_lag_i8_nonfinite(sa):
         assert np.isnan(integrate(sa, surv, r2, 0, 64, 4)).all()
     finally:
         _native.lib().sa_lag_kernel(prev)
+
+
+def test_lag_i8_diagonal_bit_identical(sa):
+    """Two T-lag groups (16 MR == T, the C5 shape; with SA_LAGI8_DIAG=1 the
+    diagonal kernel, one reference window for blocks w and w + 1): the rows equal,
+    bit for bit, the same rows computed by single-group calls, and stay within
+    the fp32 bound of the fp64 restatement."""
+    from paper_1402_0532_b200 import _native
+    prev = _native.lib().sa_lag_kernel(SA_LAGK_I8)
+    try:
+        surv, ref = signals(31, 2048 * 6)
+        full = integrate(sa, surv, ref, 0, 4096, 6)
+        for a, b in ((0, 2048), (2048, 4096), (100, 1100), (3000, 4096)):
+            assert np.array_equal(integrate(sa, surv, ref, a, b - a, 6), full[a:b]), (a, b)
+        part = integrate(sa, surv, ref, 7, 4000, 6)  # l0 % 16 != 0: still two groups
+        assert np.array_equal(part, full[7:4007])
+        assert_literal(full[::37], z_ref(surv, ref, 0, 4096, 6)[::37], TOL_F32)
+    finally:
+        _native.lib().sa_lag_kernel(prev)
