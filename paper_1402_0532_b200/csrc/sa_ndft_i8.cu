@@ -69,6 +69,12 @@ constexpr int TMEM_COLS = 512;
 #ifndef SA_I8_PREP_WARP
 #define SA_I8_PREP_WARP 1  // complex64 digit prep: one warp per row (0: one CTA per row)
 #endif
+#ifndef SA_I8_NPREP
+#define SA_I8_NPREP 4  // complex64, n <= 1024: warps (pairs) per CTA that make the x planes inside the kernel (0: separate prep)
+#endif
+#ifndef SA_I8_PREP_LA
+#define SA_I8_PREP_LA 2  // fused prep: rounds of tiles the prep may run ahead (0: unthrottled)
+#endif
 #ifndef SA_I8_STAGE_C64
 #define SA_I8_STAGE_C64 1  // complex64 rows leave through a per-warp smem staging tile
 #endif
@@ -83,7 +89,8 @@ template <int ND> struct Cfg {
   static constexpr int NSLOT = (224 * 1024) / SLOT > 4 ? 4 : (224 * 1024) / SLOT;
   static constexpr int EPI = ND == 1 ? SA_I8_EPI_C64 : SA_I8_EPI_C128;  // epilogue warps
   static constexpr int RELAY_WARP = 2 + EPI;
-  static constexpr int THREADS = (3 + EPI) * 32;  // producer, MMA, epilogue, relay
+  static constexpr int NPREP = ND == 1 ? SA_I8_NPREP : 0;  // digit-prep warps inside the kernel (complex64)
+  static constexpr int THREADS = (3 + EPI + NPREP) * 32;  // producer, MMA, epilogue, relay, prep
   // complex64: per epilogue warp a 32 x 32 fp32 staging tile (rows leave as whole 128-B lines)
   static constexpr bool STAGE = ND == 1 && SA_I8_STAGE_C64;
   static constexpr int STG = STAGE ? EPI * 4096 : 0;
@@ -305,70 +312,77 @@ __global__ void __launch_bounds__(256) k_i8_prep(const T *__restrict__ x, int8_t
 // bytes), warp-shuffle maximum, one 4-byte store per plane per float4 (a warp
 // writes two whole 64-B tile rows).  Digits exactly as k_i8_prep.
 template <int ND, int NV>
-__global__ void __launch_bounds__(256) k_i8_prep_w(const float *__restrict__ x, int8_t *__restrict__ planes,
-                                                   int *__restrict__ ex, int64_t batch, int n, float gain,
-                                                   int use_gain) {
+SA_HD void prep_row_w(const float *__restrict__ x, int8_t *__restrict__ planes, int *__restrict__ ex, int64_t v,
+                      int n, float gain, int use_gain, int lane) {
   constexpr int NPL = Cfg<ND>::NPL;
-  const int lane = threadIdx.x & 31;
   const int nk = 2 * n;
   const int kslots = nk / KSL;
-  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t v = w0; v < batch; v += nw) {
-    const float *row = x + v * nk;
-    float4 t[NV];
-    float mx = 0.f;
+  const float *row = x + v * nk;
+  float4 t[NV];
+  float mx = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int k = 4 * lane + 128 * i;
+    t[i] = k < nk ? __ldcs((const float4 *)&row[k]) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    if (use_gain) t[i] = make_float4(sa_mul(gain, t[i].x), sa_mul(gain, t[i].y), sa_mul(gain, t[i].z), sa_mul(gain, t[i].w));
+    const float a[4] = {fabsf(t[i].x), fabsf(t[i].y), fabsf(t[i].z), fabsf(t[i].w)};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) mx = a[j] == a[j] ? fmaxf(mx, a[j]) : INFINITY;  // a NaN makes the row non-finite
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  int e = 0;
+  if (mx > 0.f) frexp((double)mx, &e);  // mx = f 2^e, f in [0.5, 1): max < 2^e
+  if (!(mx <= 3.4028234663852886e38f)) e = INT_MAX;
+  if (lane == 0) ex[v] = e;
+  if (e == INT_MAX) e = 0;  // (digits of this row are never used)
+  const bool fast = e > -100 && e < 100;
+  const float sc = (float)ldexp(1.0, -e);
+  int8_t *blk = planes + (size_t)(v / BM) * kslots * (NPL * XT);
+  const int r = (int)(v % BM);
+  auto emit = [&](auto scaled) {
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const int k = 4 * lane + 128 * i;
-      t[i] = k < nk ? __ldcs((const float4 *)&row[k]) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+      if (k < nk) {
+        const float xs[4] = {t[i].x, t[i].y, t[i].z, t[i].w};
+        uint32_t b[NPL][4];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      if (use_gain) t[i] = make_float4(sa_mul(gain, t[i].x), sa_mul(gain, t[i].y), sa_mul(gain, t[i].z), sa_mul(gain, t[i].w));
-      const float a[4] = {fabsf(t[i].x), fabsf(t[i].y), fabsf(t[i].z), fabsf(t[i].w)};
+        for (int j = 0; j < 4; ++j) {
+          const float xv = xs[j];
+          const uint32_t sg = (uint32_t)((xv > 0.f) - (xv < 0.f));
+          b[0][j] = sg;
+          b[1][j] = sg * 127u;
+          float yv = scaled(xv);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) mx = a[j] == a[j] ? fmaxf(mx, a[j]) : INFINITY;  // a NaN makes the row non-finite
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    int e = 0;
-    if (mx > 0.f) frexp((double)mx, &e);  // mx = f 2^e, f in [0.5, 1): max < 2^e
-    if (!(mx <= 3.4028234663852886e38f)) e = INT_MAX;
-    if (lane == 0) ex[v] = e;
-    if (e == INT_MAX) e = 0;  // (digits of this row are never used)
-    const bool fast = e > -100 && e < 100;
-    const float sc = (float)ldexp(1.0, -e);
-    int8_t *blk = planes + (size_t)(v / BM) * kslots * (NPL * XT);
-    const int r = (int)(v % BM);
-    auto emit = [&](auto scaled) {
-#pragma unroll
-      for (int i = 0; i < NV; ++i) {
-        const int k = 4 * lane + 128 * i;
-        if (k < nk) {
-          const float xs[4] = {t[i].x, t[i].y, t[i].z, t[i].w};
-          uint32_t b[NPL][4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float xv = xs[j];
-            const uint32_t sg = (uint32_t)((xv > 0.f) - (xv < 0.f));
-            b[0][j] = sg;
-            b[1][j] = sg * 127u;
-            float yv = scaled(xv);
-#pragma unroll
-            for (int d = 0; d < 2 * ND; ++d) {
-              const float rr = rint_b(yv, b[2 + d][j]);
-              if (d + 1 < 2 * ND) yv = sa_mul(sa_sub(yv, rr), (d & 1) ? 128.0f : 127.0f);
-            }
+          for (int d = 0; d < 2 * ND; ++d) {
+            const float rr = rint_b(yv, b[2 + d][j]);
+            if (d + 1 < 2 * ND) yv = sa_mul(sa_sub(yv, rr), (d & 1) ? 128.0f : 127.0f);
           }
-          int8_t *tile = blk + (size_t)(k / KSL) * (NPL * XT) + sw64(r, k % KSL);  // 4 bytes, inside one chunk
-#pragma unroll
-          for (int p = 0; p < NPL; ++p) *(uint32_t *)(tile + p * XT) = pack4(b[p][0], b[p][1], b[p][2], b[p][3]);
         }
+        int8_t *tile = blk + (size_t)(k / KSL) * (NPL * XT) + sw64(r, k % KSL);  // 4 bytes, inside one chunk
+#pragma unroll
+        for (int p = 0; p < NPL; ++p) *(uint32_t *)(tile + p * XT) = pack4(b[p][0], b[p][1], b[p][2], b[p][3]);
       }
-    };
-    if (fast) emit([&](float xv) { return sa_mul(sa_mul(xv, sc), 127.0f); });
-    else emit([&](float xv) { return (float)sa_mul(ldexp((double)xv, -e), 127.0); });
-  }
+    }
+  };
+  if (fast) emit([&](float xv) { return sa_mul(sa_mul(xv, sc), 127.0f); });
+  else emit([&](float xv) { return (float)sa_mul(ldexp((double)xv, -e), 127.0); });
+}
+
+// complex64, n <= 1024: one WARP per row (no block barriers), NV float4 per lane
+// held in registers (k = 4 lane + 128 i: every load instruction is 512 contiguous
+// bytes), warp-shuffle maximum, one 4-byte store per plane per float4 (a warp
+// writes two whole 64-B tile rows).  Digits exactly as k_i8_prep.
+template <int ND, int NV>
+__global__ void __launch_bounds__(256) k_i8_prep_w(const float *__restrict__ x, int8_t *__restrict__ planes,
+                                                   int *__restrict__ ex, int64_t batch, int n, float gain,
+                                                   int use_gain) {
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = w0; v < batch; v += nw) prep_row_w<ND, NV>(x, planes, ex, v, n, gain, use_gain, threadIdx.x & 31);
 }
 
 // W planes (sW, 127 sW, digits) of Wv = [[Wr, -Wi], [Wi, Wr]], W = raw[(k m) mod n]
@@ -400,7 +414,8 @@ __global__ void k_i8_wbuild(const C2T *__restrict__ raw, int n, int8_t *__restri
 template <int ND, typename T>
 __global__ void __launch_bounds__(Cfg<ND>::THREADS, 1)
     k_ndft_i8(const int8_t *__restrict__ xblk, const int8_t *__restrict__ wblk, const int *__restrict__ ex,
-              T *__restrict__ y, int64_t batch, int n) {
+              T *__restrict__ y, int64_t batch, int n, const T *__restrict__ x, unsigned *__restrict__ ready,
+              T gain, int use_gain) {
   using C = Cfg<ND>;
   constexpr int NPL = C::NPL, BN = C::BN, WT = C::WT, SLOT = C::SLOT, NSLOT = C::NSLOT, NB = C::NB;
   constexpr int EPI = C::EPI, RELAY_WARP = C::RELAY_WARP;
@@ -412,6 +427,7 @@ __global__ void __launch_bounds__(Cfg<ND>::THREADS, 1)
   uint64_t *tfull = lfull + NSLOT;                     // accumulator set b holds a finished tile
   uint64_t *tempty = tfull + NB;                       // the epilogue drained set b
   uint32_t *tmem_holder = (uint32_t *)(tempty + NB);
+  int64_t *okt = (int64_t *)(smem + NSLOT * SLOT + 128);  // last tile whose x block the producer verified
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -424,6 +440,7 @@ __global__ void __launch_bounds__(Cfg<ND>::THREADS, 1)
   auto lead = [&](uint64_t *bar) { return sa_mapa(sa_smem_u32(bar), 0); };
 
   if (threadIdx.x == 0) {
+    *okt = -1;
     for (int s = 0; s < NSLOT; ++s) {
       sa_mbar_init(&full[s], 2);  // the relays of both CTAs
       sa_mbar_init(&empty[s], 1);
@@ -459,6 +476,24 @@ __global__ void __launch_bounds__(Cfg<ND>::THREADS, 1)
         const int64_t vb = (t / ot_count) * 2 + rank;  // 128-vector block
         const int64_t ob = (t % ot_count) * 2 + rank;  // N/2-output block
         const int s = (int)(it % NSLOT);
+#ifdef SA_I8_PROBE_NOWAIT
+        if (false) {
+#else
+        if (C::NPREP > 0 && ready && kc == 0) {
+#endif
+          // fused prep: all rows of this 128-vector block have their planes (release-add per
+          // row by the prep warps of every CTA); then the async-proxy reads may see them
+          const int64_t need = std::min<int64_t>(BM, batch - vb * BM);
+          if (need > 0) {
+            unsigned got;
+            do {
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(got) : "l"(ready + vb) : "memory");
+            } while ((int64_t)got < need);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+          }
+        }
+        if (kc == 0)  // this tile's block has its planes and exponents: the epilogue may read ex
+          asm volatile("st.release.cta.shared::cta.b64 [%0], %1;" ::"r"(sa_smem_u32(okt)), "l"(lt) : "memory");
         sa_mbar_wait(&empty[s], ((it / NSLOT) & 1) ^ 1);
         unsigned char *b = smem + s * SLOT;
         sa_mbar_expect_tx(&lfull[s], SLOT);
@@ -506,6 +541,34 @@ __global__ void __launch_bounds__(Cfg<ND>::THREADS, 1)
         commit2(&tfull[ab]);
       }
     }
+  } else if (warp > RELAY_WARP) {
+    // ---- prep warps (complex64, fused): one row at a time, rows in increasing order over
+    // all CTAs' prep warps, each row released to the producers of the CTAs that read it ----
+    if constexpr (C::NPREP > 0) {
+      if (ready) {
+        const int64_t gw = (int64_t)blockIdx.x * C::NPREP + (warp - RELAY_WARP - 1), nw = (int64_t)gridDim.x * C::NPREP;
+        for (int64_t v = gw; v < batch; v += nw) {
+#if SA_I8_PREP_LA > 0
+          // stay at most SA_I8_PREP_LA rounds of tiles ahead of this CTA's producer (every
+          // CTA advances alike), so planes are read back while still in L2
+          const int64_t tfirst = (v / (2 * BM)) * ot_count;
+          for (;;) {
+            int64_t ok;
+            asm volatile("ld.acquire.cta.shared::cta.b64 %0, [%1];" : "=l"(ok) : "r"(sa_smem_u32(okt)) : "memory");
+            if (tfirst <= cl + (ok < 0 ? 0 : ok) * ncl + SA_I8_PREP_LA * ncl) break;
+            __nanosleep(256);
+          }
+#endif
+          prep_row_w<ND, 16>((const float *)x, const_cast<int8_t *>(xblk), const_cast<int *>(ex), v, n, (float)gain,
+                             use_gain, lane);
+#ifndef SA_I8_PROBE_NOFENCE
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // plane stores -> the TMA readers
+#endif
+          __syncwarp();
+          if (lane == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ready + v / BM) : "memory");
+        }
+      }
+    }
   } else {
     // ---- epilogue (warps 2 .. 1 + EPI): TMEM lane quarter q -> vector row v, a column share ----
     // y = c (W + 2^e X) with W, X the digit-pair sums: one conversion each and one
@@ -519,13 +582,19 @@ __global__ void __launch_bounds__(Cfg<ND>::THREADS, 1)
     for (int64_t t = cl; t < ntiles; t += ncl, ++lt) {
       const int64_t v = (t / ot_count) * (2 * BM) + rank * BM + q * 32 + lane;
       const int o0 = (int)(t % ot_count) * BN;
-      const int e = v < batch ? ex[v] : 0;
+      const uint32_t ab = lt % NB;
+      {  // the producer verified this tile's block (fused prep: ex written), then the load
+        int64_t ok;
+        do {
+          asm volatile("ld.acquire.cta.shared::cta.b64 %0, [%1];" : "=l"(ok) : "r"(sa_smem_u32(okt)) : "memory");
+        } while (ok < (int64_t)lt);
+      }
+      const int e = v < batch ? __ldcg(&ex[v]) : 0;  // (its latency overlaps the accumulator wait)
+      sa_mbar_wait(&tfull[ab], (lt / NB) & 1);
+      fence_after();
       const bool fast = ND == 2 ? (e > -960 && e < 1030) : (e > -100 && e < 100);
       const double sxd = fast ? ldexp(CD, e) : 0.0;
       const float sxf = (float)sxd;
-      const uint32_t ab = lt % NB;
-      sa_mbar_wait(&tfull[ab], (lt / NB) & 1);
-      fence_after();
       const uint32_t ta = tmem + ab * (2 * ND * BN) + ((uint32_t)(q * 32) << 16);
 #ifdef SA_I8_PROBE_NOEPI
       if (v >= 0) {
@@ -713,15 +782,25 @@ int launch_i8(const void *x, void *y, int64_t batch, int64_t n, SaTwiddles *tw, 
   // x planes (whole 256-vector tiles: rows past the batch are never stored) + exponents
   const int64_t rows = (batch + 2 * BM - 1) / (2 * BM) * (2 * BM);
   const size_t pbytes = (size_t)C::NPL * rows * 2 * n;
+  // complex64, n <= 1024: the digit prep runs inside the tensor-core kernel (prep warps,
+  // one ready counter per 128-vector block); otherwise a separate prep launch
+  const bool fused = C::NPREP > 0 && n <= 1024;
+  const int64_t nready = rows / BM;
   int8_t *planes = nullptr;
   {
-    const int rc_ = sa_scratch_alloc((void **)&planes, pbytes + (size_t)batch * sizeof(int) + 256, s);
+    const int rc_ = sa_scratch_alloc((void **)&planes, pbytes + (size_t)batch * sizeof(int) + 256 +
+                                                           (size_t)nready * sizeof(unsigned) + 256, s);
     if (rc_) return rc_;
   }
   int *ex = (int *)(((uintptr_t)(planes + pbytes) + 255) & ~(uintptr_t)255);
+  unsigned *ready = (unsigned *)(((uintptr_t)(ex + batch) + 255) & ~(uintptr_t)255);
   int dev = 0, sms = 148;
   SA_CUDA_TRY(cudaGetDevice(&dev));
   SA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (fused) {
+    SA_CUDA_TRY(cudaMemsetAsync(ready, 0, (size_t)nready * sizeof(unsigned), s));
+    goto prepped;
+  }
   if constexpr (ND == 1 && SA_I8_PREP_WARP) {
     // complex64, n <= 1024: one warp per row, a wave of resident CTAs
     if (n <= 1024) {
@@ -767,7 +846,8 @@ prepped:
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   SA_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_ndft_i8<ND, T>, (const int8_t *)planes, (const int8_t *)tw->i8w,
-                                 (const int *)ex, (T *)y, batch, (int)n));
+                                 (const int *)ex, (T *)y, batch, (int)n, (const T *)x, fused ? ready : nullptr,
+                                 (T)gain, (int)(gain != 1.0)));
   SA_LAUNCH_CHECK();
   SA_CUDA_TRY(cudaFreeAsync(planes, s));
   return SA_OK;
