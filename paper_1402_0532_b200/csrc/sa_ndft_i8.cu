@@ -22,8 +22,11 @@
 //   ND = 1: the fp32 bound 1e-4 with a wide margin
 // (tests/test_gpu_ndft_i8.py).  Smaller n runs the FFMA2 / DFMA fast kernels.
 //
-// Pipeline: k_i8_prep (one pass over x, one warp per row: gain, per-vector
-// exponent, the 2 + 2 ND int8 planes S, 127 S, digits) -> k_ndft_i8<ND>
+// Pipeline: the x digit prep (one pass over x: gain, per-vector exponent, the
+// 2 + 2 ND int8 planes S, 127 S, digits) -- for complex64 with n <= 1024 done by
+// prep warps INSIDE k_ndft_i8 (rows released per 128-vector block through a
+// ready counter the producer acquires before its bulk copies), otherwise by
+// k_i8_prep / k_i8_prep_w first -- then k_ndft_i8<ND>
 // (persistent CTA pairs, cluster 2, tcgen05.mma.cta_group::2.kind::i8, M = 256
 // vectors, N = 512 / (2 ND) outputs, K = 32; the 2 ND accumulators fill TMEM's 512
 // columns).  Both operand sets are stored in HBM as "smem images": for each
