@@ -47,12 +47,9 @@
 #include <cstdlib>
 #include <math_constants.h>
 
-#include <cooperative_groups.h>
-
 #include "sa_internal.h"
 #include "sa_regs.cuh"
 
-namespace cg = cooperative_groups;
 
 namespace {
 
@@ -63,7 +60,7 @@ constexpr int B_SBO = 2 * KC * CORE;     // next 8 B rows
 constexpr int B_BYTES = NPL * 2 * B_SBO; // 6 planes x 16 shifts x 128 u = 12 KB
 constexpr int BUILDERS = 256;
 constexpr int THREADS = BUILDERS + 32;   // warp 8 issues the MMAs
-constexpr int NPART_MAX = 2048;          // |ref| max partials (k_lag_cprep CTAs)
+constexpr int NPART_MAX = 2048;          // |ref| max partials (k_lag_absmax CTAs)
 constexpr double DSC = 1.0 / (127.0 * 254.0);
 
 struct Geo {
@@ -176,38 +173,43 @@ struct LagDst {
   }
 };
 
+// |ref| maxima: one partial per CTA (grid-stride, 16-B loads); k_lag_cprep and the
+// lag kernel reduce the partials.
+__global__ void __launch_bounds__(256) k_lag_absmax(const float2 *__restrict__ ref, int64_t ref_len,
+                                                    float *__restrict__ part) {
+  __shared__ float red[8];
+  float mx = 0.f;
+  const int64_t n4 = (uintptr_t)ref & 15 ? 0 : ref_len / 4;  // 16-B aligned: float4 pairs
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 a = __ldg((const float4 *)&ref[4 * i]), b = __ldg((const float4 *)&ref[4 * i + 2]);
+    mx = fmaxf(mx, fmaxf(fmaxf(amax(make_float2(a.x, a.y)), amax(make_float2(a.z, a.w))),
+                         fmaxf(amax(make_float2(b.x, b.y)), amax(make_float2(b.z, b.w)))));
+  }
+  for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ref_len;
+       i += (int64_t)gridDim.x * blockDim.x)
+    mx = fmaxf(mx, amax(__ldg(&ref[i])));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) mx = fmaxf(mx, red[w]);
+    part[blockIdx.x] = mx;
+  }
+}
+
 // c planes of the whole reference (one exponent ec for all of it): plane p holds
 // byte x = c[x - guard] (zero outside [0, ref_len)), p = d0 cr, d1 cr, d0 ci, d1 ci,
 // sgn cr, sgn ci; the lag kernel bulk-copies its Hankel windows out of them.
-// One cooperative launch: |ref| maxima (one partial per CTA), grid barrier, digits
-// (the second read of ref mostly hits L2).
+// (Two ordinary launches, not one cooperative one: a grid barrier would need every
+// CTA resident, which a concurrent kernel -- e.g. an NCCL collective of the
+// streaming multi-GPU map -- can prevent.)
 __global__ void __launch_bounds__(256) k_lag_cprep(const float2 *__restrict__ ref, int64_t ref_len, float csign,
-                                                   float *__restrict__ part, int64_t guard, int64_t cpl,
-                                                   unsigned char *__restrict__ planes) {
+                                                   const float *__restrict__ part, int npart, int64_t guard,
+                                                   int64_t cpl, unsigned char *__restrict__ planes) {
   __shared__ float red[8];
-  {
-    float mx = 0.f;
-    const int64_t n4 = (uintptr_t)ref & 15 ? 0 : ref_len / 4;  // 16-B aligned: float4 pairs
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
-      const float4 a = __ldg((const float4 *)&ref[4 * i]), b = __ldg((const float4 *)&ref[4 * i + 2]);
-      mx = fmaxf(mx, fmaxf(fmaxf(amax(make_float2(a.x, a.y)), amax(make_float2(a.z, a.w))),
-                           fmaxf(amax(make_float2(b.x, b.y)), amax(make_float2(b.z, b.w)))));
-    }
-    for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ref_len;
-         i += (int64_t)gridDim.x * blockDim.x)
-      mx = fmaxf(mx, amax(__ldg(&ref[i])));
-#pragma unroll
-    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int w = 1; w < 8; ++w) mx = fmaxf(mx, red[w]);
-      part[blockIdx.x] = mx;
-    }
-  }
-  cg::this_grid().sync();
   float mc = 0.f;
-  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) mc = fmaxf(mc, __ldcg(&part[i]));
+  for (int i = threadIdx.x; i < npart; i += blockDim.x) mc = fmaxf(mc, __ldcg(&part[i]));
 #pragma unroll
   for (int o = 16; o; o >>= 1) mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, o));
   __syncthreads();
@@ -868,19 +870,16 @@ int sa_launch_lag_i8_blocks(const void *surv, const void *ref, int64_t ref_len, 
   }
   float *cpart = (float *)ws;
   unsigned char *cplanes = ws + NPART_MAX * sizeof(float);
-  int sms = 148, dev = 0, per_sm = 1;
+  int sms = 148, dev = 0;
   SA_CUDA_TRY(cudaGetDevice(&dev));
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  SA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lag_cprep, 256, 0));
-  int npart = (int)std::min<int64_t>(std::min<int64_t>((int64_t)per_sm * sms, NPART_MAX), (cpl / 16 + 255) / 256);
-  npart = std::max(npart, 1);
-  {
-    float cs = conj ? -1.f : 1.f;
-    const float2 *rp = (const float2 *)ref;
-    void *args[] = {(void *)&rp, (void *)&ref_len, (void *)&cs, (void *)&cpart, (void *)&guard, (void *)&cpl,
-                    (void *)&cplanes};
-    SA_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_lag_cprep, dim3(npart), dim3(256), args, 0, s));
-  }
+  const int npart = (int)std::max<int64_t>(1, std::min<int64_t>(4 * sms, (ref_len / 4 + 255) / 256));
+  k_lag_absmax<<<npart, 256, 0, s>>>((const float2 *)ref, ref_len, cpart);
+  SA_LAUNCH_CHECK();
+  const int64_t nb = std::min<int64_t>((cpl / 16 + 255) / 256, 8 * sms);
+  k_lag_cprep<<<(unsigned)nb, 256, 0, s>>>((const float2 *)ref, ref_len, conj ? -1.f : 1.f, cpart, npart, guard, cpl,
+                                           cplanes);
+  SA_LAUNCH_CHECK();
   int rc;
   if (SA_LAGI8_DIAG && npass == 2 && 16 * mr == tb) {  // two T-lag groups: one c window per CTA for two blocks
     if (mr == 64)

@@ -545,12 +545,18 @@ __global__ void __launch_bounds__(Cfg<ND>::THREADS, 1)
       }
     }
   } else if (warp > RELAY_WARP) {
-    // ---- prep warps (complex64, fused): one row at a time, rows in increasing order over
-    // all CTAs' prep warps, each row released to the producers of the CTAs that read it ----
+    // ---- prep warps (complex64, fused): rows taken in increasing order from one ticket
+    // counter (ready[nready]) by whichever prep warps run -- no producer ever waits on a
+    // row owned by a CTA that is not resident -- each row released to the producers of
+    // the CTAs that read it ----
     if constexpr (C::NPREP > 0) {
       if (ready) {
-        const int64_t gw = (int64_t)blockIdx.x * C::NPREP + (warp - RELAY_WARP - 1), nw = (int64_t)gridDim.x * C::NPREP;
-        for (int64_t v = gw; v < batch; v += nw) {
+        unsigned *ticket = ready + (vt_count * 2);
+        for (;;) {
+          unsigned vt = 0;
+          if (lane == 0) vt = atomicAdd(ticket, 1u);
+          const int64_t v = __shfl_sync(0xffffffffu, vt, 0);
+          if (v >= batch) break;
 #if SA_I8_PREP_LA > 0
           // stay at most SA_I8_PREP_LA rounds of tiles ahead of this CTA's producer (every
           // CTA advances alike), so planes are read back while still in L2
@@ -792,7 +798,7 @@ int launch_i8(const void *x, void *y, int64_t batch, int64_t n, SaTwiddles *tw, 
   int8_t *planes = nullptr;
   {
     const int rc_ = sa_scratch_alloc((void **)&planes, pbytes + (size_t)batch * sizeof(int) + 256 +
-                                                           (size_t)nready * sizeof(unsigned) + 256, s);
+                                                           (size_t)(nready + 1) * sizeof(unsigned) + 256, s);
     if (rc_) return rc_;
   }
   int *ex = (int *)(((uintptr_t)(planes + pbytes) + 255) & ~(uintptr_t)255);
@@ -801,7 +807,7 @@ int launch_i8(const void *x, void *y, int64_t batch, int64_t n, SaTwiddles *tw, 
   SA_CUDA_TRY(cudaGetDevice(&dev));
   SA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   if (fused) {
-    SA_CUDA_TRY(cudaMemsetAsync(ready, 0, (size_t)nready * sizeof(unsigned), s));
+    SA_CUDA_TRY(cudaMemsetAsync(ready, 0, (size_t)(nready + 1) * sizeof(unsigned), s));  // + the row ticket
     goto prepped;
   }
   if constexpr (ND == 1 && SA_I8_PREP_WARP) {
