@@ -188,10 +188,9 @@ def test_lag_i8_nonfinite(sa):
 
 
 def test_lag_i8_diagonal_bit_identical(sa):
-    """Two T-lag groups (16 MR == T, the C5 shape; with SA_LAGI8_DIAG=1 the
-    diagonal kernel, one reference window for blocks w and w + 1): the rows equal,
-    bit for bit, the same rows computed by single-group calls, and stay within
-    the fp32 bound of the fp64 restatement."""
+    """Two T-lag groups (16 MR == T, the C5 shape): the rows equal, bit for
+    bit, the same rows computed by single-group calls (exact int32 sums), and
+    stay within the fp32 bound of the fp64 restatement."""
     from paper_1402_0532_b200 import _native
     prev = _native.lib().sa_lag_kernel(SA_LAGK_I8)
     try:
