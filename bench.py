@@ -342,7 +342,8 @@ def roof_i8(achieved_tops, dtype="c128"):
     return {"bound": "tensor", "achieved": round(achieved_tops, 1), "peak": round(peak, 1), "unit": "TOP/s",
             "frac": round(achieved_tops / peak, 4), "traffic": tr["bytes_per_launch"] if tr else None,
             "traffic_unit": "bytes/launch", "traffic_source": tr["source"] if tr else None,
-            "kernel": "k_ndft_i8 (x digit prep inside the kernel)", "algorithmic_bytes": 2 * 65536 * 1024 * (16 if dtype == "c128" else 8),
+            "kernel": "k_ndft_i8 + k_i8_prep" if dtype == "c128" else "k_ndft_i8 (x digit prep inside the kernel)",
+            "algorithmic_bytes": 2 * 65536 * 1024 * (16 if dtype == "c128" else 8),
             "peak_source": f"2 x {src} bf16_tflops (int8 dense = 2 x bf16 on B200; int8 not measured)",
             "nominal_peak": 4500.0, "frac_nominal": round(achieved_tops / 4500.0, 4),
             "algorithmic": f"{per} int8 tensor ops per complex ⊙: {terms} digit x sign MMA terms x re/im x re/im MACs"}
