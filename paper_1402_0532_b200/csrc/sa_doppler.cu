@@ -87,20 +87,47 @@ __global__ void __launch_bounds__(THREADS, 1)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C2 *sm = reinterpret_cast<C2 *>(smem_raw);
   C4 *tws = reinterpret_cast<C4 *>(smem_raw + D::SM_DATA);
-  for (int e = threadIdx.x; e < M - 1; e += THREADS) tws[e] = stage[e];
+  // twiddles and rows: every thread issues a batch of independent loads before its
+  // shared-memory stores (a load-store-load chain would pay the L2 latency per element)
+  constexpr int TB = (M - 1 + THREADS - 1) / THREADS;
+  {
+    C4 t[TB];
+#pragma unroll
+    for (int j = 0; j < TB; ++j) {
+      const int e = threadIdx.x + j * THREADS;
+      if (e < M - 1) t[j] = stage[e];
+    }
+#pragma unroll
+    for (int j = 0; j < TB; ++j) {
+      const int e = threadIdx.x + j * THREADS;
+      if (e < M - 1) tws[e] = t[j];
+    }
+  }
   // rows of this CTA: absolute (16-aligned) rows a0 .. a0 + R - 1; valid rows are
   // row_off .. row_off + l_count - 1 (output row = a - row_off)
   const int64_t a0 = (int64_t)blockIdx.x * R;
-  for (int e = threadIdx.x; e < M * R; e += THREADS) {
-    const int j = e % R, pos = e / R;  // R consecutive threads: one q, R rows
-    const int q = (int)(__brev((unsigned)pos) >> (32 - LOGM));
-    const int64_t a = a0 + j;
-    C2 v = {T(0), T(0)};
-    if (a >= row_off && a < row_off + l_count) {
-      v = blocked ? z[((a >> 4) * M + q) * 16 + (a & 15)] : z[(a - row_off) * M + q];
-      if (use_gain) v = {sa_mul(gain, v.x), sa_mul(gain, v.y)};
+  constexpr int LB = (M * R / THREADS) < 8 ? (M * R / THREADS) : 8;  // loads in flight per thread
+  static_assert((M * R) % (LB * THREADS) == 0, "row staging: whole batches");
+  for (int e0 = threadIdx.x; e0 < M * R; e0 += LB * THREADS) {
+    C2 v[LB];
+#pragma unroll
+    for (int b = 0; b < LB; ++b) {
+      const int e = e0 + b * THREADS;
+      const int j = e % R, pos = e / R;  // R consecutive threads: one q, R rows
+      const int q = (int)(__brev((unsigned)pos) >> (32 - LOGM));
+      const int64_t a = a0 + j;
+      v[b] = {T(0), T(0)};
+      if (a >= row_off && a < row_off + l_count)
+        v[b] = blocked ? z[((a >> 4) * M + q) * 16 + (a & 15)] : z[(a - row_off) * M + q];
     }
-    sm[j * D::STRIDE + pad16(pos)] = v;
+#pragma unroll
+    for (int b = 0; b < LB; ++b) {
+      const int e = e0 + b * THREADS;
+      const int j = e % R, pos = e / R;
+      C2 x = v[b];
+      if (use_gain) x = {sa_mul(gain, x.x), sa_mul(gain, x.y)};
+      sm[j * D::STRIDE + pad16(pos)] = x;
+    }
   }
   __syncthreads();
   constexpr int FULL = LOGM / 4, REM = LOGM % 4;
