@@ -700,7 +700,7 @@ def wl_map(args, ws, rank, c5=False, e2e=False):
             return pm.full if pm is not None else full
         return out
 
-    res = {"ops": ops, "cells": L * M, "step": step, "lag_only": lag_only, "launches_per_step": 3 if args.dtype == "c64" else 2,
+    res = {"ops": ops, "cells": L * M, "step": step, "lag_only": lag_only, "launches_per_step": 4 if args.dtype == "c64" else 2,
            "result": result, "surv": surv, "ref": ref,
            "config": {"workload": ("C5" if c5 else "C4") + " ⊙ range-Doppler map (BASELINE.json configs["
                       + ("4" if c5 else "3") + "])", "ns": ns, "delay_bins": L, "doppler_bins": M,
@@ -726,7 +726,7 @@ def wl_map(args, ws, rank, c5=False, e2e=False):
         res["d2h"] = hout.numel() * hout.element_size()
         res["e2e_api"] = ("paper_1402_0532_b200.ambiguity_map(pinned host surv, pinned host ref, L, M, "
                           "out=pinned host map)")
-        res["e2e_launches"] = 2
+        res["e2e_launches"] = 4 if args.dtype == "c64" else 2
     sv = sc.surv.astype(np.complex64 if args.dtype == "c64" else np.complex128)
     rv = sc.ref.astype(sv.dtype)
     res["cpu"] = lambda P: cpu_map(sv, rv, L, M, P)
