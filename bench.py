@@ -683,10 +683,19 @@ def wl_map(args, ws, rank, c5=False, e2e=False):
         else:
             sa.ambiguity_map(surv, ref, rows, M, l0=l0, out=out, workspace=ws_buf)
 
-    z = torch.empty((rows, M), dtype=cdt, device="cuda")
+    z = torch.empty((rows + 30, M), dtype=cdt, device="cuda")
     from paper_1402_0532_b200 import _native
+    zrows = torch.tensor([z.data_ptr()], dtype=torch.int64, device="cuda")
 
     def lag_only():
+        # the lag stage exactly as the map runs it: complex64 writes the blocked z the
+        # Doppler kernel reads (sa_ambiguity_integrate_blocks, one destination);
+        # otherwise the row-major stage (sa_ambiguity_integrate)
+        if args.dtype == "c64" and l0 == 0 and rows % 16 == 0 and \
+                _native.lib().sa_ambiguity_integrate_blocks(
+                    _native.SA_C64, _native.ptr(surv), _native.ptr(ref), ns, ns, 0, rows, M, 0, M, 1,
+                    _native.ptr(zrows), 1, _native.stream_ptr()) == 0:
+            return
         _native.check(_native.lib().sa_ambiguity_integrate(
             _native.SA_C64 if args.dtype == "c64" else _native.SA_C128, _native.ptr(surv), _native.ptr(ref),
             ns, ns, l0, rows, M, 1, _native.SA_NDFT_FAST, _native.ptr(z), _native.stream_ptr()))
