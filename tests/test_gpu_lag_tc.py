@@ -203,3 +203,28 @@ def test_lag_i8_diagonal_bit_identical(sa):
         assert_literal(full[::37], z_ref(surv, ref, 0, 4096, 6)[::37], TOL_F32)
     finally:
         _native.lib().sa_lag_kernel(prev)
+
+
+def test_lag_i8_concurrent_streams(sa):
+    """Two int8 lag stages on two streams at once (each call owns its reference
+    planes and partials) equal the same calls made one after the other."""
+    import torch
+    from paper_1402_0532_b200 import _native
+    prev = _native.lib().sa_lag_kernel(SA_LAGK_I8)
+    try:
+        cases = [signals(41, 2048 * 8), signals(42, 2048 * 8)]
+        seq = [integrate(sa, s, r, 0, 1500, 8) for s, r in cases]
+        dev_in = [(torch.from_numpy(s).cuda(), torch.from_numpy(r).cuda()) for s, r in cases]
+        zs = [torch.empty((1500, 8), dtype=torch.complex64, device="cuda") for _ in cases]
+        streams = [torch.cuda.Stream() for _ in cases]
+        torch.cuda.synchronize()
+        for (ds, dr), z, st in zip(dev_in, zs, streams):
+            with torch.cuda.stream(st):
+                _native.check(_native.lib().sa_ambiguity_integrate(
+                    _native.SA_C64, _native.ptr(ds), _native.ptr(dr), ds.numel(), dr.numel(), 0, 1500, 8, 1,
+                    _native.SA_NDFT_FAST, _native.ptr(z), _native.stream_ptr()))
+        torch.cuda.synchronize()
+        for z, r in zip(zs, seq):
+            assert np.array_equal(z.cpu().numpy(), r)
+    finally:
+        _native.lib().sa_lag_kernel(prev)
