@@ -197,6 +197,11 @@ def ambiguity_map(s_surv, s_ref, l_bins: int, m: int, *, l0: int = 0, gain: floa
     host_out = out if (out is not None and not is_device_tensor(out)) else None
     if host_out is not None:
         out = None
+    if (out_ptr is None and not device_io and mode == "fast" and lag == "mf" and doppler == "nfft"
+            and dtype == T.complex64):
+        r = _map_host_pipelined(surv, ref, l_bins, m, l0, gain, conjugate_ref, host_out)
+        if r is not None:
+            return r
     ds = _dev(surv, dtype)
     dr = _dev(ref, dtype)
     ns = ds.numel()
@@ -233,6 +238,78 @@ def ambiguity_map(s_surv, s_ref, l_bins: int, m: int, *, l0: int = 0, gain: floa
         T.cuda.current_stream().synchronize()
         return host_out
     return out if device_io else out.cpu().numpy()
+
+
+_MAP_STREAMS: dict = {}
+
+
+def _map_host_pipelined(surv, ref, l_bins, m, l0, gain, conjugate_ref, host_out):
+    """Host (pinned) complex64 inputs -> host map with the uploads overlapped: the
+    reference goes up first (the int8 lag stage needs its global exponent), then the
+    surveillance samples in chunks of Doppler blocks, each chunk's lag stage
+    (sa_ambiguity_integrate_blocks, blocked z) running as soon as its samples
+    landed while the next chunk uploads; then the Doppler NL-FFT and the download.
+    Every block is integrated exactly as in one call, so the map is bit-identical.
+    Returns None when the shape is outside the blocked path (the caller takes the
+    simple path)."""
+    T = torch()
+    if not (isinstance(surv, T.Tensor) and isinstance(ref, T.Tensor)) or surv.dtype != T.complex64 \
+            or ref.dtype != T.complex64 or not (surv.is_pinned() and ref.is_pinned()):
+        return None
+    ns, nr = surv.numel(), ref.numel()
+    if l0 != 0 or l_bins % 16 or m < 64 or m > 2048 or (m & (m - 1)) or ns % m:
+        return None
+    tb = ns // m
+    if tb < 128 or tb % 128 or tb > 4096 or l_bins > m * tb:
+        return None
+    for l in (0, l_bins - 1):
+        _lag_guards(ns, nr, l, ns)
+    dev = T.cuda.current_device()
+    if dev not in _MAP_STREAMS:
+        _MAP_STREAMS[dev] = T.cuda.Stream()
+    up = _MAP_STREAMS[dev]
+    cur = T.cuda.current_stream()
+    ds = T.empty(ns, dtype=T.complex64, device="cuda")
+    dr = T.empty(nr, dtype=T.complex64, device="cuda")
+    z = T.empty(((l_bins + 30) * m,), dtype=T.complex64, device="cuda")
+    out = T.empty((l_bins, m), dtype=T.complex64, device="cuda")
+    zrows = T.tensor([z.data_ptr()], dtype=T.int64, device="cuda")
+    up.wait_stream(cur)
+    # chunks of >= ~4 MiB of samples (each chunk costs three launches), at most 8
+    nchunk = max(1, min(8, m // 16, (ns * 8) >> 22))
+    bounds = [m * k // nchunk for k in range(nchunk + 1)]
+    with T.cuda.stream(up):
+        dr.copy_(ref.reshape(-1), non_blocking=True)
+    evs = []
+    for k in range(nchunk):
+        a, b = bounds[k] * tb, bounds[k + 1] * tb
+        with T.cuda.stream(up):
+            ds[a:b].copy_(surv.reshape(-1)[a:b], non_blocking=True)
+            ev = T.cuda.Event()
+            ev.record(up)
+        evs.append(ev)
+    lib = _native.lib()
+    for k in range(nchunk):
+        cur.wait_event(evs[k])
+        rc = lib.sa_ambiguity_integrate_blocks(
+            _native.SA_C64, _native.ptr(ds), _native.ptr(dr), ns, nr, 0, l_bins, m, bounds[k],
+            bounds[k + 1] - bounds[k], int(conjugate_ref), _native.ptr(zrows), 1, _native.stream_ptr())
+        if rc == _native.SA_ERR_UNSUPPORTED and k == 0:
+            cur.wait_stream(up)
+            return None
+        _native.check(rc)
+    tw = device_twiddles(m, _native.SA_C64, dev)
+    _native.check(lib.sa_doppler_nlfft_blocked(_native.SA_C64, _native.ptr(z), _native.ptr(out), l_bins, m,
+                                                ctypes.c_void_p(tw), float(gain), _native.stream_ptr()))
+    for t in (ds, dr, z, zrows):
+        t.record_stream(cur)
+    ds.record_stream(up)
+    dr.record_stream(up)
+    if host_out is not None:
+        host_out.copy_(out, non_blocking=True)
+        cur.synchronize()
+        return host_out
+    return out.cpu().numpy()
 
 
 def _surface_rate(s_surv, s_ref) -> float:

@@ -228,3 +228,20 @@ def test_lag_i8_concurrent_streams(sa):
             assert np.array_equal(z.cpu().numpy(), r)
     finally:
         _native.lib().sa_lag_kernel(prev)
+
+
+@pytest.mark.parametrize("ns,L,M", [(2048 * 64, 512, 64), (1024 * 128, 1000, 128), (2048 * 64, 64, 64)])
+def test_map_host_pipelined_bit_identical(sa, ns, L, M):
+    """Pinned host complex64 inputs take the upload-overlapped path (reference
+    first, surveillance chunks each followed by its blocks' lag stage); the map
+    equals the device-input map bit for bit (L = 1000: not whole 16-row tiles, the
+    simple path)."""
+    import torch
+    surv, ref = signals(ns + L, ns)
+    hs = torch.from_numpy(surv).pin_memory()
+    hr = torch.from_numpy(ref).pin_memory()
+    hout = torch.empty((L, M), dtype=torch.complex64).pin_memory()
+    got = sa.ambiguity_map(hs, hr, L, M, out=hout, gain=3.0)
+    dev = sa.ambiguity_map(hs.cuda(), hr.cuda(), L, M, gain=3.0).cpu()
+    assert torch.equal(got, dev)
+    assert np.array_equal(sa.ambiguity_map(hs, hr, L, M, gain=3.0), dev.numpy())
