@@ -36,10 +36,15 @@
 // Each TMEM lane holds the 16 consecutive lags of one blocked-z tile (sa_lag_tc.cu
 // layout): the thread stores one whole 128-B line.
 //
-// One CTA per integration block q: 8 builder warps (A planes per pass, B chunks;
-// warps 0-3 also drain TMEM), one MMA warp.  A non-finite value in the block
-// (s) makes its column NaN; a non-finite reference value makes the whole map NaN
-// (the exponent is global) -- the bf16 kernel (sa_lag_tc.cu) keeps NaN local.
+// Launches per call: k_lag_absmax (|ref| partials) -> k_lag_cprep (the six
+// reference digit planes over the range the call's blocks read, in HBM) ->
+// k_lag_i8: one CTA per integration block q, two per SM; warp roles: 0-3
+// epilogue (drain TMEM, store the blocked z tiles), 4-7 B builders (16 shifts of
+// the block's s planes per 128-u chunk, 4-deep ring), 8 MMA issuer (one elected
+// lane per K step's six MMAs), 9 producer (bulk copies of each lag-group pass's
+// A window, double-buffered).  A non-finite value in the block (s) makes its
+// column NaN; a non-finite reference value makes the whole map NaN (the exponent
+// is global) -- the bf16 kernel (sa_lag_tc.cu) keeps NaN local.
 #include <cuda.h>
 
 #include <algorithm>
