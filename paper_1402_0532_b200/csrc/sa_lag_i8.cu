@@ -58,6 +58,23 @@
 
 namespace {
 
+#ifdef SA_LAG_TS  // probe build: per-CTA phase timestamps (globaltimer, ns), tools/probes/lag_ts.py
+__device__ unsigned long long g_lag_ts[4096 * 8];
+SA_HD unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TS(i)                                                                \
+  do {                                                                       \
+    if (blockIdx.x < 4096 && (threadIdx.x & 31) == 0) g_lag_ts[blockIdx.x * 8 + (i)] = gtime(); \
+  } while (0)
+#else
+#define TS(i) \
+  do {        \
+  } while (0)
+#endif
+
 constexpr int NPL = 6;                   // planes per side
 constexpr int KC = 4;                    // K32 steps per B chunk (128 u)
 constexpr int CORE = 128;                // one core matrix: 8 rows x 16 B
@@ -304,6 +321,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 2)
   const float2 *sb = surv + q * tb;
   constexpr int LGRP = 16 * MR;  // lags per group (one pass)
   constexpr int TMEM_COLS = 256 * NACC;
+  if (tid == 0) TS(0);
 
   // ---- exponents: |s| over this block, |c| over the whole reference (k_lag_cprep partials) ----
   {
@@ -381,6 +399,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 2)
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_holder;
+  if (tid == 0) TS(1);
 
   if (warp == WPROD) {
     if (lane == 0)
@@ -395,6 +414,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 2)
     for (int pi = 0; pi < npass; ++pi) {
       const int a = pi & 1, ab = pi % NACC;
       sa_mbar_wait(&afull[a], (pi >> 1) & 1);
+      if (pi == 0 && lane == 0) TS(2);
       if (pi >= NACC) sa_mbar_wait(&tempty[ab], ((pi / NACC) - 1) & 1);
       fence_after();
       const uint32_t tm = tmem + 256 * ab;
@@ -402,6 +422,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 2)
       for (int ch = 0; ch < nch; ++ch, ++cc) {
         const int b = cc % NB;
         sa_mbar_wait(&bfull[b], (cc / NB) & 1);
+        if (cc == 0 && lane == 0) TS(3);
         fence_after();
         const int kn = min(KC, gm.ks - ch * KC);
         for (int kk = 0; kk < kn; ++kk) {
@@ -429,6 +450,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 2)
         commit(&aempty[a]);
         commit(&tfull[ab]);
       }
+      if (lane == 0) TS(4);
       __syncwarp();
     }
   } else if (warp >= WB0 && warp < WB0 + 4) {
@@ -468,6 +490,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 2)
     for (int pi = 0; pi < npass; ++pi) {
       const int ab = pi % NACC;
       sa_mbar_wait(&tfull[ab], (pi / NACC) & 1);
+      if (warp == 0 && lane == 0) TS(5);
       fence_after();
       const uint32_t gc = ta + 256 * ab;
       const int64_t lag0 = lalign + (int64_t)pi * LGRP + 16 * (MR - 1 - r);  // lags lag0 + [0, 16) of block q
@@ -532,6 +555,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 2)
   fence_before();
   __syncthreads();
   fence_after();
+  if (tid == 0) TS(6);
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
 }
@@ -566,6 +590,11 @@ static int lag_kind_now() {
   return g_lag_kind;
 }
 bool sa_lag_i8_enabled() { return lag_kind_now() == SA_LAGK_I8; }
+#ifdef SA_LAG_TS
+extern "C" int sa_lag_ts_read(unsigned long long *host, int n) {
+  return cudaMemcpyFromSymbol(host, g_lag_ts, (size_t)n * sizeof(unsigned long long)) == cudaSuccess ? 0 : -1;
+}
+#endif
 extern "C" int sa_lag_kernel(int kind) {
   const int prev = lag_kind_now();
   if (kind == SA_LAGK_I8 || kind == SA_LAGK_BF16) g_lag_kind = kind;

@@ -1,4 +1,5 @@
-"""Per-CTA phase timestamps of the C4 lag kernel (probe build with -DSA_LAG_TS)."""
+"""Per-CTA phase timestamps of the int8 lag kernel: run with a library built with
+-DSA_LAG_TS (tools/build_variant.sh ts "-DSA_LAG_TS"; SA_LIB_PATH=tools/variants/ts.so)."""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
