@@ -220,6 +220,62 @@ __global__ void __launch_bounds__(256) k_lag_absmax(const float2 *__restrict__ r
   }
 }
 
+// s planes of every block of the call (one CTA per block): the block's exponent
+// (|s| maximum; INT_MAX marks a non-finite block) and its six digit planes
+// [sgn sr, sgn si, d0 sr, d0 si, d1 sr, d1 si] over x in [0, psl), t = x - 16, laid
+// out contiguously per block so the lag kernel fetches them with one bulk copy.
+// Block 0 also stores the reference maximum (from the k_lag_absmax partials).
+// Runs as the trailing blocks of the k_lag_cprep launch.
+__device__ __forceinline__ void sprep_block(int64_t qi, const float2 *__restrict__ surv, int64_t q0, int tb, int psl,
+                                            unsigned char *__restrict__ splanes, int *__restrict__ es_out,
+                                            const float *__restrict__ part, int npart, float *__restrict__ mc_out) {
+  __shared__ float red[8];
+  const float2 *sb = surv + (q0 + qi) * tb;
+  float ms = 0.f;
+  for (int t = threadIdx.x; t < tb; t += blockDim.x) ms = fmaxf(ms, amax(__ldg(&sb[t])));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) ms = fmaxf(ms, __shfl_xor_sync(0xffffffffu, ms, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ms;
+  __syncthreads();
+  for (int w = 0; w < 8; ++w) ms = fmaxf(ms, red[w]);
+  const int es = !(ms <= FLT_MAX) ? INT_MAX : exponent_of(ms);
+  if (threadIdx.x == 0) es_out[qi] = es;
+  if (qi == 0) {  // the reference maximum, reduced once for every lag CTA
+    __syncthreads();
+    float mc = 0.f;
+    for (int i = threadIdx.x; i < npart; i += blockDim.x) mc = fmaxf(mc, __ldcg(&part[i]));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < 8; ++w) mc = fmaxf(mc, red[w]);
+      *mc_out = mc;
+    }
+  }
+  const Dig dig(es == INT_MAX ? 0 : es);
+  unsigned char *ps = splanes + qi * (int64_t)(NPL * psl);
+  for (int x4 = threadIdx.x; x4 < psl / 4; x4 += blockDim.x) {
+    const int t = 4 * x4 - 16;
+    float2 v[4] = {};
+    if (t >= 0 && t < tb) {  // tb % 4 == 0: a group of 4 is all in or all out
+      const float4 a = __ldg((const float4 *)&sb[t]), b = __ldg((const float4 *)&sb[t + 2]);
+      v[0] = make_float2(a.x, a.y), v[1] = make_float2(a.z, a.w), v[2] = make_float2(b.x, b.y), v[3] = make_float2(b.z, b.w);
+    }
+    uint32_t w[NPL] = {};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      uint32_t d0r, d1r, d0i, d1i;
+      const uint32_t sr = dig(v[e].x, d0r, d1r), si = dig(v[e].y, d0i, d1i);
+      w[0] |= sr << (8 * e), w[1] |= si << (8 * e);
+      w[2] |= d0r << (8 * e), w[3] |= d0i << (8 * e);
+      w[4] |= d1r << (8 * e), w[5] |= d1i << (8 * e);
+    }
+#pragma unroll
+    for (int p = 0; p < NPL; ++p) ((uint32_t *)(ps + p * psl))[x4] = w[p];
+  }
+}
+
 // c planes of the whole reference (one exponent ec for all of it): plane p holds
 // byte x = c[x - guard] (zero outside [0, ref_len)), p = d0 cr, d1 cr, d0 ci, d1 ci,
 // sgn cr, sgn ci; the lag kernel bulk-copies its Hankel windows out of them.
@@ -228,7 +284,14 @@ __global__ void __launch_bounds__(256) k_lag_absmax(const float2 *__restrict__ r
 // streaming multi-GPU map -- can prevent.)
 __global__ void __launch_bounds__(256) k_lag_cprep(const float2 *__restrict__ ref, int64_t ref_len, float csign,
                                                    const float *__restrict__ part, int npart, int64_t guard,
-                                                   int64_t cpl, unsigned char *__restrict__ planes) {
+                                                   int64_t cpl, unsigned char *__restrict__ planes, unsigned ncb,
+                                                   const float2 *__restrict__ surv, int64_t q0, int tb, int psl,
+                                                   unsigned char *__restrict__ splanes, int *__restrict__ es_out,
+                                                   float *__restrict__ mc_out) {
+  if (blockIdx.x >= ncb) {  // trailing blocks: one per surveillance block
+    sprep_block(blockIdx.x - ncb, surv, q0, tb, psl, splanes, es_out, part, npart, mc_out);
+    return;
+  }
   __shared__ float red[8];
   float mc = 0.f;
   for (int i = threadIdx.x; i < npart; i += blockDim.x) mc = fmaxf(mc, __ldcg(&part[i]));
@@ -240,7 +303,7 @@ __global__ void __launch_bounds__(256) k_lag_cprep(const float2 *__restrict__ re
   for (int w = 0; w < 8; ++w) mc = fmaxf(mc, red[w]);
   const Dig dig(exponent_of(mc));
   for (int64_t x16 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x16 < cpl / 16;
-       x16 += (int64_t)gridDim.x * blockDim.x) {
+       x16 += (int64_t)ncb * blockDim.x) {
     const int64_t k0 = 16 * x16 - guard;
     uint32_t w[NPL][4] = {};
 #pragma unroll
@@ -297,9 +360,9 @@ constexpr int WB0 = 4, WMMA = 8, WPROD = 9;
 
 template <int MR, bool BLK>
 __global__ void __launch_bounds__(NWARPS * 32, 2)
-    k_lag_i8(const float2 *__restrict__ surv, int64_t l0g, int64_t l_count, int64_t m, int tb,
-             const float *__restrict__ cpart, int npart, const unsigned char *__restrict__ cplanes, int64_t guard, int64_t cpl,
-             float2 *__restrict__ z, int64_t q0, LagDst dst) {
+    k_lag_i8(const unsigned char *__restrict__ splanes, const int *__restrict__ es_in, const float *__restrict__ mc_in,
+             int64_t l0g, int64_t l_count, int64_t m, int tb, const unsigned char *__restrict__ cplanes, int64_t guard,
+             int64_t cpl, float2 *__restrict__ z, int64_t q0, LagDst dst) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const Geo gm = geo(tb, MR, 2);
@@ -313,40 +376,28 @@ __global__ void __launch_bounds__(NWARPS * 32, 2)
   uint64_t *aempty = afull + 2;
   uint64_t *tfull = aempty + 2;
   uint64_t *tempty = tfull + NACC;
-  uint32_t *tmem_holder = (uint32_t *)(tempty + NACC);
-  float *red = (float *)(tmem_holder + 2);  // 2 x NWARPS partial maxima
+  uint64_t *psfull = tempty + NACC;                    // the block's s planes landed
+  uint32_t *tmem_holder = (uint32_t *)(psfull + 1);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t q = q0 + blockIdx.x;
-  const float2 *sb = surv + q * tb;
   constexpr int LGRP = 16 * MR;  // lags per group (one pass)
   constexpr int TMEM_COLS = 256 * NACC;
   if (tid == 0) TS(0);
 
-  // ---- exponents: |s| over this block, |c| over the whole reference (k_lag_cprep partials) ----
-  {
-    float ms = 0.f, mc = 0.f;
-    for (int i = tid; i < npart; i += NWARPS * 32) mc = fmaxf(mc, cpart[i]);
-    for (int t = tid; t < tb; t += NWARPS * 32) ms = fmaxf(ms, amax(__ldg(&sb[t])));
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      ms = fmaxf(ms, __shfl_xor_sync(0xffffffffu, ms, o));
-      mc = fmaxf(mc, __shfl_xor_sync(0xffffffffu, mc, o));
-    }
-    if (lane == 0) red[warp] = ms, red[NWARPS + warp] = mc;
-  }
   if (tid == 0) {
     for (int i = 0; i < NB; ++i) sa_mbar_init(&bfull[i], 4), sa_mbar_init(&bempty[i], 1);
     for (int i = 0; i < 2; ++i) sa_mbar_init(&afull[i], 1), sa_mbar_init(&aempty[i], 1);
     for (int i = 0; i < NACC; ++i) sa_mbar_init(&tfull[i], 1), sa_mbar_init(&tempty[i], 4);
+    sa_mbar_init(psfull, 1);
     sa_fence_mbar_init();
   }
   __syncthreads();
-  float ms = 0.f, mc = 0.f;
-#pragma unroll
-  for (int w = 0; w < NWARPS; ++w) ms = fmaxf(ms, red[w]), mc = fmaxf(mc, red[NWARPS + w]);
-  const bool bad = !(ms <= FLT_MAX) || !(mc <= FLT_MAX);
-  const int es = exponent_of(ms), ec = exponent_of(mc);
+  // exponents from the prep launch (sprep_block): this block's (INT_MAX: non-finite) and the reference maximum
+  const int es_raw = es_in[blockIdx.x];
+  const float mc = *mc_in;
+  const bool bad = es_raw == INT_MAX || !(mc <= FLT_MAX);
+  const int es = es_raw == INT_MAX ? 0 : es_raw, ec = exponent_of(mc);
 
   const int64_t lalign = l0g - (l0g & 15);
   const int npass = (int)((l0g - lalign + l_count + LGRP - 1) / LGRP);
@@ -364,30 +415,10 @@ __global__ void __launch_bounds__(NWARPS * 32, 2)
     for (int p = 0; p < NPL; ++p)
       bulk_g2s(Pc + (a * NPL + p) * gm.pcl, src + (int64_t)p * cpl, (uint32_t)gm.pcl, &afull[a]);
   };
-  if (warp == WPROD && lane == 0)
+  if (warp == WPROD && lane == 0) {
+    sa_mbar_expect_tx(psfull, (uint32_t)(NPL * gm.psl));  // the block's s planes (sprep_block), one bulk copy
+    bulk_g2s(Ps, splanes + (int64_t)blockIdx.x * (NPL * gm.psl), (uint32_t)(NPL * gm.psl), psfull);
     for (int pi = 0; pi < min(2, npass); ++pi) produce(pi);
-  // ---- s planes: x in [0, psl), t = x - 16 (zero outside the block); all other warps ----
-  if (warp != WPROD) {
-    const Dig dig(es);
-    for (int x4 = tid; x4 < gm.psl / 4; x4 += (NWARPS - 1) * 32) {
-      const int t = 4 * x4 - 16;
-      float2 v[4] = {};
-      if (t >= 0 && t < tb) {  // tb % 4 == 0: a group of 4 is all in or all out
-        const float4 a = __ldg((const float4 *)&sb[t]), b = __ldg((const float4 *)&sb[t + 2]);
-        v[0] = make_float2(a.x, a.y), v[1] = make_float2(a.z, a.w), v[2] = make_float2(b.x, b.y), v[3] = make_float2(b.z, b.w);
-      }
-      uint32_t w[NPL] = {};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        uint32_t d0r, d1r, d0i, d1i;
-        const uint32_t sr = dig(v[e].x, d0r, d1r), si = dig(v[e].y, d0i, d1i);
-        w[0] |= sr << (8 * e), w[1] |= si << (8 * e);
-        w[2] |= d0r << (8 * e), w[3] |= d0i << (8 * e);
-        w[4] |= d1r << (8 * e), w[5] |= d1i << (8 * e);
-      }
-#pragma unroll
-      for (int p = 0; p < NPL; ++p) ((uint32_t *)(Ps + p * gm.psl))[x4] = w[p];
-    }
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa_smem_u32(tmem_holder)),
@@ -456,6 +487,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 2)
   } else if (warp >= WB0 && warp < WB0 + 4) {
     // ---- builders: B chunk = 16 shifts of the six s planes, 16-B pieces ----
     const int bt = tid - WB0 * 32;
+    sa_mbar_wait(psfull, 0);  // the block's s planes landed
     uint32_t cc = 0;
     for (int pi = 0; pi < npass; ++pi) {
       for (int ch = 0; ch < nch; ++ch, ++cc) {
@@ -561,9 +593,9 @@ __global__ void __launch_bounds__(NWARPS * 32, 2)
 }
 
 template <int MR, bool BLK>
-int launch_i8(const void *surv, int64_t l0, int64_t l_count, int64_t m, int64_t q0, int64_t q_count, int64_t tb,
-              void *z, const LagDst &d, const float *cpart, int npart, const unsigned char *cplanes, int64_t guard, int64_t cpl,
-              cudaStream_t s) {
+int launch_i8(const unsigned char *splanes, const int *es, const float *mc, int64_t l0, int64_t l_count, int64_t m,
+              int64_t q0, int64_t q_count, int64_t tb, void *z, const LagDst &d, const unsigned char *cplanes,
+              int64_t guard, int64_t cpl, cudaStream_t s) {
   const Geo gm = geo((int)tb, MR, 2);
   const int bytes = gm.off_b + NB * B_BYTES + 512 + 1024;
   static int smem_set[64] = {};  // largest smem size set per device
@@ -573,8 +605,8 @@ int launch_i8(const void *surv, int64_t l0, int64_t l_count, int64_t m, int64_t 
     SA_CUDA_TRY(cudaFuncSetAttribute(k_lag_i8<MR, BLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     if (dev < 64) smem_set[dev] = bytes;
   }
-  k_lag_i8<MR, BLK><<<(unsigned)q_count, NWARPS * 32, bytes, s>>>((const float2 *)surv, l0, l_count, m, (int)tb,
-                                                                  cpart, npart, cplanes, guard, cpl, (float2 *)z, q0, d);
+  k_lag_i8<MR, BLK><<<(unsigned)q_count, NWARPS * 32, bytes, s>>>(splanes, es, mc, l0, l_count, m, (int)tb, cplanes,
+                                                                  guard, cpl, (float2 *)z, q0, d);
   SA_LAUNCH_CHECK();
   return SA_OK;
 }
@@ -624,11 +656,15 @@ int sa_launch_lag_i8_blocks(const void *surv, const void *ref, int64_t ref_len, 
   const int64_t cpl = (chi - clo + 127) / 128 * 128;
   unsigned char *ws = nullptr;
   {
-    const int rc_ = sa_scratch_alloc((void **)&ws, NPART_MAX * sizeof(float) + NPL * cpl, s);
+    const int rc_ = sa_scratch_alloc((void **)&ws, NPART_MAX * sizeof(float) + 16 + 4 * q_count + 15 + NPL * cpl +
+                                                     q_count * NPL * gm.psl, s);
     if (rc_ != SA_OK) return rc_;
   }
   float *cpart = (float *)ws;
-  unsigned char *cplanes = ws + NPART_MAX * sizeof(float);
+  float *mc = cpart + NPART_MAX;
+  int *es = (int *)(mc + 4);
+  unsigned char *cplanes = ws + (NPART_MAX * sizeof(float) + 16 + 4 * q_count + 15) / 16 * 16;
+  unsigned char *splanes = cplanes + NPL * cpl;  // cpl and psl are multiples of 16
   int sms = 148, dev = 0;
   SA_CUDA_TRY(cudaGetDevice(&dev));
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -636,16 +672,17 @@ int sa_launch_lag_i8_blocks(const void *surv, const void *ref, int64_t ref_len, 
   k_lag_absmax<<<npart, 256, 0, s>>>((const float2 *)ref, ref_len, cpart);
   SA_LAUNCH_CHECK();
   const int64_t nb = std::min<int64_t>((cpl / 16 + 255) / 256, 8 * sms);
-  k_lag_cprep<<<(unsigned)nb, 256, 0, s>>>((const float2 *)ref, ref_len, conj ? -1.f : 1.f, cpart, npart, guard, cpl,
-                                           cplanes);
+  k_lag_cprep<<<(unsigned)(nb + q_count), 256, 0, s>>>((const float2 *)ref, ref_len, conj ? -1.f : 1.f, cpart, npart,
+                                                       guard, cpl, cplanes, (unsigned)nb, (const float2 *)surv, q0,
+                                                       (int)tb, gm.psl, splanes, es, mc);
   SA_LAUNCH_CHECK();
   int rc;
   if (mr == 64)
-    rc = blocked ? launch_i8<64, true>(surv, l0, l_count, m, q0, q_count, tb, z, d, cpart, npart, cplanes, guard, cpl, s)
-                 : launch_i8<64, false>(surv, l0, l_count, m, q0, q_count, tb, z, d, cpart, npart, cplanes, guard, cpl, s);
+    rc = blocked ? launch_i8<64, true>(splanes, es, mc, l0, l_count, m, q0, q_count, tb, z, d, cplanes, guard, cpl, s)
+                 : launch_i8<64, false>(splanes, es, mc, l0, l_count, m, q0, q_count, tb, z, d, cplanes, guard, cpl, s);
   else
-    rc = blocked ? launch_i8<128, true>(surv, l0, l_count, m, q0, q_count, tb, z, d, cpart, npart, cplanes, guard, cpl, s)
-                 : launch_i8<128, false>(surv, l0, l_count, m, q0, q_count, tb, z, d, cpart, npart, cplanes, guard, cpl, s);
+    rc = blocked ? launch_i8<128, true>(splanes, es, mc, l0, l_count, m, q0, q_count, tb, z, d, cplanes, guard, cpl, s)
+                 : launch_i8<128, false>(splanes, es, mc, l0, l_count, m, q0, q_count, tb, z, d, cplanes, guard, cpl, s);
   SA_CUDA_TRY(cudaFreeAsync(ws, s));
   return rc;
 }
