@@ -52,6 +52,21 @@ def test_map_peaks_large_vs_oracle(sa, shape):
         assert np.array_equal(as_rows(sa.map_peaks(dev(v), k)), oracle.find_peaks(v, k))
 
 
+@pytest.mark.parametrize("shape", [(4096, 2048), (97, 130), (1, 1), (1, 61), (61, 1), (65, 31), (130, 59)])
+def test_map_peaks_complex64_dense_vs_oracle(sa, shape):
+    """complex64 maps (the integer-key path): quantised magnitudes (ties, plateaus),
+    a checkerboard of strict maxima (64 per 4 x 64 warp strip, the compaction
+    limit) and a continuous map; k up to the per-warp limit and past it."""
+    g = np.random.default_rng(shape[1])
+    q = (g.integers(0, 12, shape) + 1j * g.integers(0, 12, shape)).astype(np.complex64)
+    cb = np.zeros(shape, np.complex64)
+    cb[::2, ::2] = (1 + g.integers(0, 3, cb[::2, ::2].shape)).astype(np.complex64)  # a strict max every 2 x 2
+    c = (g.standard_normal(shape) + 1j * g.standard_normal(shape)).astype(np.complex64)
+    for v in (q, cb, c):
+        for k in (1, 8, 32, 33):
+            assert np.array_equal(as_rows(sa.map_peaks(dev(v), k)), oracle.find_peaks(v, k, "f32"))
+
+
 def test_map_peaks_on_c4_map(sa):
     """The C4 map straight from ambiguity_map (device) -> peaks, vs the oracle on the same map."""
     from paper_1402_0532_b200.workloads import c4_scene
