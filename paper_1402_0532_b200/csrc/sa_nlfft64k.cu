@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cooperative_groups.h>
 #include <cudaTypedefs.h>
+#include <type_traits>
 
 #include "sa_internal.h"
 #include "sa_regs.cuh"
@@ -45,6 +46,9 @@ constexpr int NN = 1 << LOGN;
 #ifndef SA_LOCALQ
 #define SA_LOCALQ 1  // the CTA's own share of the scatter: st.shared + warp arrivals
 #endif
+#ifndef SA_K64_L2S
+#define SA_K64_L2S 0  // c64: second node storage in an L2 scratch (signals alternate smem / L2)
+#endif
 #ifndef SA_K64F_TC
 #define SA_K64F_TC 16
 #define SA_K64F_CL 4
@@ -58,7 +62,8 @@ template <> struct K64<float> {
   static constexpr int TC = SA_K64F_TC;  // columns per tile
   static constexpr int CL = SA_K64F_CL;  // cluster size
   static constexpr int NG = SA_K64F_NG;  // thread groups per CTA
-  static constexpr int NS = SA_K64F_NS;  // node storages (2 = pipelined signals; needs CL >= 8 for c64)
+  static constexpr bool L2S = SA_K64_L2S;  // storage 1 in a global (L2-resident) scratch
+  static constexpr int NS = L2S ? 2 : SA_K64F_NS;  // node storages (2 = pipelined signals)
   static constexpr int MINB = SA_K64F_MINB;  // resident CTAs per SM
 };
 #ifndef SA_K64D_TC  // complex128 shape (-D for sweeps)
@@ -69,12 +74,15 @@ template <> struct K64<double> {
   static constexpr int TC = SA_K64D_TC;
   static constexpr int CL = 8;
   static constexpr int NG = SA_K64D_NG;
+  static constexpr bool L2S = false;
   static constexpr int NS = 1;
   static constexpr int MINB = 1;
 };
 
 template <typename T> struct L64 {
   static constexpr int TC = K64<T>::TC, CL = K64<T>::CL, NG = K64<T>::NG, NS = K64<T>::NS;
+  static constexpr bool L2S = K64<T>::L2S;
+  static constexpr int NSM = L2S ? 1 : NS;  // node storages in smem
   static constexpr int GT = 16 * TC;       // threads per group
   static constexpr int THREADS = NG * GT;
   static constexpr int COLS = 256 / CL;    // node columns owned per CTA
@@ -85,7 +93,7 @@ template <typename T> struct L64 {
   static constexpr size_t INTER1 = sizeof(C2) * 256 * COLS;  // one signal's node share
   static constexpr size_t WORK = sizeof(C2) * 256 * TC;      // one tile
   static constexpr size_t TWA = sizeof(C4) * 255;
-  static constexpr size_t OFF_WORK = NS * INTER1;
+  static constexpr size_t OFF_WORK = NSM * INTER1;
   static constexpr size_t OFF_TWA = OFF_WORK + NG * WORK;
   static constexpr size_t OFF_BAR = OFF_TWA + TWA;
   static constexpr size_t SMEM = OFF_BAR + 8 * (NG + 2 * NS);
@@ -137,10 +145,30 @@ template <typename T> struct Pipe {
   int rank, gi, gt;
   int64_t cid, ncl;
   uint32_t tile_it = 0;
+  C2 *scr = nullptr;  // L2S: this cluster's scratch storage, [owner][INTER1 / sizeof(C2)]
+  static constexpr int SE = (int)(P::INTER1 / sizeof(C2));  // elements of one owner's share
+  SA_HD static bool in_l2(int b) { return P::L2S && b == 1; }
+  template <bool S> SA_HD static C2 ld(const C2 *p) {
+    if constexpr (S) return __ldcg(p);
+    else return *p;
+  }
+  template <bool S> SA_HD static void st(C2 *p, C2 v) {
+    if constexpr (S) __stcg(p, v);
+    else *p = v;
+  }
+  // this CTA's share of storage b (smem, or its owner region of the L2 scratch)
+  SA_HD C2 *share(int b) const { return in_l2(b) ? scr + (size_t)rank * SE : inter(b); }
 
   SA_HD C2 *inter(int b) const { return reinterpret_cast<C2 *>(smem + b * P::INTER1); }
   // after a thread's last local scatter store of a signal: its warp's arrive on full[b]
   SA_HD void local_done(int b) const {
+    if (in_l2(b)) {  // scratch stores of this group -> every owner's full[1] (release at cluster scope)
+      group_sync(1 + gi, P::GT);
+      if (gt == 0)
+#pragma unroll
+        for (int r = 0; r < P::CL; ++r) sa_mbar_arrive_remote_release(peer_full(1, r));
+      return;
+    }
     if (SA_LOCALQ) {
       __syncwarp();
       if ((threadIdx.x & 31) == 0) sa_mbar_arrive_local(&full_bar[b]);
@@ -166,7 +194,7 @@ template <typename T> struct Pipe {
 #endif
   }
 
-  SA_HD void init(unsigned char *smem_raw, const C4 *stage) {
+  SA_HD void init(unsigned char *smem_raw, const C4 *stage, C2 *scratch) {
     cg::cluster_group cluster = cg::this_cluster();
     smem = smem_raw;
     twA = reinterpret_cast<C4 *>(smem + P::OFF_TWA);
@@ -178,6 +206,7 @@ template <typename T> struct Pipe {
     ncl = gridDim.x / P::CL;
     gi = threadIdx.x / P::GT;
     gt = threadIdx.x % P::GT;
+    if (P::L2S) scr = scratch + (size_t)cid * P::CL * SE;
 #pragma unroll
     for (int r = 0; r < P::CL; ++r) {
       pinter[r] = sa_mapa(sa_smem_u32(smem), r);
@@ -188,7 +217,8 @@ template <typename T> struct Pipe {
       for (int g = 0; g < P::NG; ++g) sa_mbar_init(&tma_bar[g], 1);
       for (int b = 0; b < P::NS; ++b) {
         // expect_tx(remote bytes) once per use (+ one arrive per warp for the local share)
-        sa_mbar_init(&full_bar[b], 1 + (SA_LOCALQ ? P::THREADS / 32 : 0));
+        sa_mbar_init(&full_bar[b], in_l2(b) ? P::CL * P::NG  // one arrive per thread group of the cluster
+                                            : 1 + (SA_LOCALQ ? P::THREADS / 32 : 0));
         sa_mbar_init(&empty_bar[b], SA_GREL ? P::CL * P::NG : P::CL);  // remote arrives per use
       }
       sa_fence_mbar_init();
@@ -219,7 +249,20 @@ template <typename T> struct Pipe {
     if (threadIdx.x == 0)
 #endif
 #pragma unroll
-      for (int r = 0; r < P::CL; ++r) sa_mbar_arrive_remote(sa_mapa(sa_smem_u32(&empty_bar[b]), r));
+      for (int r = 0; r < P::CL; ++r) {
+        const uint32_t a = sa_mapa(sa_smem_u32(&empty_bar[b]), r);
+        if (in_l2(b)) sa_mbar_arrive_remote_release(a);  // our scratch write-backs precede the next writer's
+        else sa_mbar_arrive_remote(a);
+      }
+  }
+  // wait until storage b may be written (scratch: cluster-scope acquire)
+  SA_HD void wait_empty(int b, uint32_t parity) const {
+    if (in_l2(b)) sa_mbar_wait_cluster(&empty_bar[b], parity);
+    else group_wait(&empty_bar[b], parity);
+  }
+  SA_HD void wait_full(int b, uint32_t parity) const {
+    if (in_l2(b)) sa_mbar_wait_cluster(&full_bar[b], parity);
+    else group_wait(&full_bar[b], parity);
   }
   // signal loop: phaseA(sig, b, use, next_sig) then (pipelined) phaseB of the
   // previous signal; every storage use waits full/empty with parity use & 1.
@@ -230,7 +273,7 @@ template <typename T> struct Pipe {
     int64_t i = 0;
     for (int64_t sig = cid; sig < batch; sig += ncl, ++i) {
       const int b = (int)(i % P::NS);
-      if (threadIdx.x == 0)
+      if (threadIdx.x == 0 && !in_l2(b))
 #ifdef SA_PROBE_NOSCATTER
         sa_mbar_arrive_local(&full_bar[b]);  // probe: no remote bytes expected
 #else
@@ -258,7 +301,8 @@ template <typename T>
 __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
     k_nlfft64k_dit(const __grid_constant__ CUtensorMap tmx, typename Ar<T>::C2 *__restrict__ y,
                    int64_t batch, const typename Ar<T>::C4 *__restrict__ stage,
-                   const typename Ar<T>::C2 *__restrict__ stage2, T gain, int use_gain) {
+                   const typename Ar<T>::C2 *__restrict__ stage2, T gain, int use_gain,
+                   typename Ar<T>::C2 *__restrict__ scratch) {
   using P = L64<T>;
   using A = Ar<T>;
   using V = typename A::V;
@@ -267,7 +311,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
   constexpr int TC = P::TC, COLS = P::COLS, NG = P::NG, GT = P::GT, TPG = P::TPG;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Pipe<T> pp;
-  pp.init(smem_raw, stage);
+  pp.init(smem_raw, stage, scratch);
   const int gbar = 1 + pp.gi;
   const int m1_cc = pp.gt % TC, m1_g = pp.gt / TC;
   const int m2_g = pp.gt & 15, m2_cc = pp.gt >> 4;
@@ -332,13 +376,14 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
       }
 #endif
       // scatter node row R = rev8(c): column q lives in CTA q / COLS
-      if (u == 0) pp.group_wait(&pp.empty_bar[b], use & 1);  // peers released storage b
+      if (u == 0) pp.wait_empty(b, use & 1);  // peers released storage b
       const int R = rev8(pp.rank * COLS + tt * TC + m2_cc);
       constexpr int KPC = COLS / 16;  // registers per owner CTA
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
         const int e = R * COLS + m2_g + 16 * (k % KPC);
-        if (SA_LOCALQ && k / KPC == pp.rank) pp.inter(b)[e] = A::to(v[k]);
+        if (Pipe<T>::in_l2(b)) __stcg(&pp.scr[(k / KPC) * Pipe<T>::SE + e], A::to(v[k]));
+        else if (SA_LOCALQ && k / KPC == pp.rank) pp.inter(b)[e] = A::to(v[k]);
 #ifndef SA_PROBE_NOSCATTER
         else sa_st_async(pp.peer_inter(b, k / KPC, (uint32_t)(sizeof(C2) * e)), A::to(v[k]), pp.peer_full(b, k / KPC));
 #else
@@ -349,15 +394,16 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
     pp.local_done(b);
   };
 
-  auto phaseB = [&](int64_t sig, int b, uint32_t use) {
-    C2 *inter = pp.inter(b);
+  auto phaseB_s = [&](auto S_, int64_t sig, int b, uint32_t use) {
+    constexpr bool S = decltype(S_)::value;  // storage in the L2 scratch
+    C2 *inter = pp.share(b);
     C2 *ysig = y + sig * NN;
     C2 wf[30];
     {
       const int q0 = pp.rank * COLS + pp.gi * TC + m1_cc;  // independent of the node storage
       load_wf<T>(wf, stage2, q0, m1_g);
     }
-    pp.group_wait(&pp.full_bar[b], use & 1);  // all INTER1 bytes of this signal landed
+    pp.wait_full(b, use & 1);  // all INTER1 bytes of this signal landed
     for (int u = 0; u < TPG; ++u) {
       const int tt = pp.gi + NG * u;
       const int lq = tt * TC + m1_cc;
@@ -368,7 +414,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
 #endif
       V v[16];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = A::from(inter[(m1_g * 16 + k) * COLS + lq]);
+      for (int k = 0; k < 16; ++k) v[k] = A::from(Pipe<T>::template ld<S>(&inter[(m1_g * 16 + k) * COLS + lq]));
 #ifndef SA_PROBE_SKIP_B
       if (gen) {  // warps with column 0 / 128: general product (twiddles with zero components)
 #pragma unroll
@@ -389,10 +435,10 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
       }
 #endif
 #pragma unroll
-      for (int k = 0; k < 16; ++k) inter[(m1_g * 16 + k) * COLS + lq] = A::to(v[k]);
+      for (int k = 0; k < 16; ++k) Pipe<T>::template st<S>(&inter[(m1_g * 16 + k) * COLS + lq], A::to(v[k]));
       group_sync(gbar, GT);
 #pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = A::from(inter[(m1_g + 16 * k) * COLS + lq]);
+      for (int k = 0; k < 16; ++k) v[k] = A::from(Pipe<T>::template ld<S>(&inter[(m1_g + 16 * k) * COLS + lq]));
 #ifndef SA_PROBE_SKIP_B
       if (gen) {
 #pragma unroll
@@ -417,6 +463,16 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
     }
   };
 
+  auto phaseB = [&](int64_t sig, int b, uint32_t use) {
+    if constexpr (P::L2S) {
+      if (Pipe<T>::in_l2(b)) {
+        phaseB_s(std::true_type{}, sig, b, use);
+        return;
+      }
+    }
+    phaseB_s(std::false_type{}, sig, b, use);
+  };
+
   pp.run(&tmx, batch, phaseA, phaseB);
 }
 
@@ -431,7 +487,8 @@ template <typename T>
 __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
     k_nlfft64k_dif(const __grid_constant__ CUtensorMap tmx, typename Ar<T>::C2 *__restrict__ y,
                    int64_t batch, const typename Ar<T>::C4 *__restrict__ stage,
-                   const typename Ar<T>::C2 *__restrict__ stage2, T gain, int use_gain) {
+                   const typename Ar<T>::C2 *__restrict__ stage2, T gain, int use_gain,
+                   typename Ar<T>::C2 *__restrict__ scratch) {
   using P = L64<T>;
   using A = Ar<T>;
   using V = typename A::V;
@@ -440,7 +497,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
   constexpr int TC = P::TC, COLS = P::COLS, NG = P::NG, GT = P::GT, TPG = P::TPG;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Pipe<T> pp;
-  pp.init(smem_raw, stage);
+  pp.init(smem_raw, stage, scratch);
   const int gbar = 1 + pp.gi;
   const int m1_cc = pp.gt % TC, m1_g = pp.gt / TC;
   const int m2_g = pp.gt & 15, m2_cc = pp.gt >> 4;
@@ -504,23 +561,25 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
             if (!(k & h)) r_dif_fast<T>(v[k], v[k + h], wf[h - 1 + (k & (h - 1))]);
         }
       }
-      if (u == 0) pp.group_wait(&pp.empty_bar[b], use & 1);
+      if (u == 0) pp.wait_empty(b, use & 1);
 #pragma unroll
       for (int k = 0; k < 16; ++k) {  // row R = 16g + k -> CTA owning cr = rev8(R), local row cr mod COLS
         const int cr = crev4(k) * 16 + rg1;
         const int lr = cr % COLS;
         const int e = lr * 256 + (q ^ (lr & 15));
-        if (SA_LOCALQ && cr / COLS == pp.rank) pp.inter(b)[e] = A::to(v[k]);  // owner is warp-uniform
+        if (Pipe<T>::in_l2(b)) __stcg(&pp.scr[(cr / COLS) * Pipe<T>::SE + e], A::to(v[k]));
+        else if (SA_LOCALQ && cr / COLS == pp.rank) pp.inter(b)[e] = A::to(v[k]);  // owner is warp-uniform
         else sa_st_async(pp.peer_inter(b, cr / COLS, (uint32_t)(sizeof(C2) * e)), A::to(v[k]), pp.peer_full(b, cr / COLS));
       }
     }
     pp.local_done(b);
   };
 
-  auto phaseB = [&](int64_t sig, int b, uint32_t use) {
-    C2 *inter = pp.inter(b);
+  auto phaseB_s = [&](auto S_, int64_t sig, int b, uint32_t use) {
+    constexpr bool S = decltype(S_)::value;  // storage in the L2 scratch
+    C2 *inter = pp.share(b);
     C2 *ysig = y + sig * NN;
-    pp.group_wait(&pp.full_bar[b], use & 1);
+    pp.wait_full(b, use & 1);
     for (int u = 0; u < TPG; ++u) {
       const int tt = pp.gi + NG * u;
       V v[16];
@@ -529,7 +588,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
         C2 *row = inter + lr * 256;
         const int sw = lr & 15;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) v[k] = A::from(row[(m2_g + 16 * k) ^ sw]);
+        for (int k = 0; k < 16; ++k) v[k] = A::from(Pipe<T>::template ld<S>(&row[(m2_g + 16 * k) ^ sw]));
 #pragma unroll
         for (int s = 8; s >= 5; --s) {
           const int hr = 1 << (s - 5), h = 1 << (s - 1);
@@ -538,7 +597,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
             if (!(k & hr)) r_dif<T>(v[k], v[k + hr], twA[(h - 1) + m2_g + 16 * (k & (hr - 1))]);
         }
 #pragma unroll
-        for (int k = 0; k < 16; ++k) row[(m2_g + 16 * k) ^ sw] = A::to(v[k]);
+        for (int k = 0; k < 16; ++k) Pipe<T>::template st<S>(&row[(m2_g + 16 * k) ^ sw], A::to(v[k]));
       }
       group_sync(gbar, GT);
       {  // round 2 (M1: cc fastest): q = 16g + k ; stages 4..2 + 2-point ; bit-reversed store
@@ -546,7 +605,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
         const C2 *row = inter + lr * 256;
         const int sw = lr & 15;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) v[k] = A::from(row[(m1_g * 16 + k) ^ sw]);
+        for (int k = 0; k < 16; ++k) v[k] = A::from(Pipe<T>::template ld<S>(&row[(m1_g * 16 + k) ^ sw]));
 #pragma unroll
         for (int k = 0; k < 8; ++k) {  // s = 4: j = k
           if (k == 0) r_dif_one<T>(v[k], v[k + 8]);
@@ -575,6 +634,16 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
         for (int k = 0; k < 16; ++k) __stcs(&ysig[(crev4(k) * 16 + rg) * 256 + cr], A::to(v[k]));
       }
     }
+  };
+
+  auto phaseB = [&](int64_t sig, int b, uint32_t use) {
+    if constexpr (P::L2S) {
+      if (Pipe<T>::in_l2(b)) {
+        phaseB_s(std::true_type{}, sig, b, use);
+        return;
+      }
+    }
+    phaseB_s(std::false_type{}, sig, b, use);
   };
 
   pp.run(&tmx, batch, phaseA, phaseB);
@@ -636,9 +705,15 @@ int launch64k(int variant, const void *x, void *y, int64_t batch, const SaTwiddl
     max_clusters = sms / P::CL;
   int64_t ncl = std::min<int64_t>(batch, max_clusters);
   cfg.gridDim = dim3((unsigned)(ncl * P::CL));
+  typename P::C2 *scratch = nullptr;  // L2S: one signal's node storage per cluster (L2-resident)
+  if (P::L2S) {
+    const int rc_ = sa_scratch_alloc((void **)&scratch, (size_t)ncl * NN * sizeof(typename P::C2), s);
+    if (rc_ != SA_OK) return rc_;
+  }
   SA_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, map, (typename P::C2 *)y, batch,
                                  (const typename P::C4 *)tw->stage,
-                                 (const typename P::C2 *)tw->stage2, (T)gain, (int)(gain != 1.0)));
+                                 (const typename P::C2 *)tw->stage2, (T)gain, (int)(gain != 1.0), scratch));
+  if (scratch) SA_CUDA_TRY(cudaFreeAsync(scratch, s));
   return SA_OK;
 }
 

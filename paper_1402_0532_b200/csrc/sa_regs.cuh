@@ -260,6 +260,10 @@ SA_HD void sa_mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
 SA_HD void sa_mbar_arrive_local(uint64_t *bar) {  // release.cta: prior smem writes visible to waiters
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa_smem_u32(bar)) : "memory");
 }
+SA_HD void sa_mbar_arrive_remote_release(uint32_t cluster_addr) {  // publishes prior global writes
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
 SA_HD void sa_mbar_arrive_remote(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
