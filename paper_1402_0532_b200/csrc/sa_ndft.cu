@@ -21,6 +21,7 @@
 //   the transposing stores and the inner-loop loads are conflict-free) with a
 //   register prefetch of the next chunk overlapping the FMA loop.
 #include <algorithm>
+#include <type_traits>
 
 #include "sa_common.cuh"
 #include "sa_internal.h"
@@ -56,11 +57,12 @@ SA_HD int swz(int mm, int vv) { return vv ^ ((mm >> 1) & 7); }
 // (each real ⊗ = one fma of exact sign products, rr/ri = one add each) and the
 // accumulator advanced sequentially over m from +0: value-identical to
 // transforms.py:223-251 (12 FP ops per ⊙ instead of 8).
-template <typename T, bool POW2, bool TW_SMEM, bool EX>
-__global__ void __launch_bounds__(NDFT_THREADS, sizeof(T) == 8 ? SA_D_MINB : 1)
+// TB / TK: vectors per lane / bins per thread (NdftCfg; fp64 also a 1 x 4 tile for
+// batches too small to fill the GPU with the 4 x 4 one).
+template <typename T, bool POW2, bool TW_SMEM, bool EX, int TB = NdftCfg<T>::TB, int TK = NdftCfg<T>::TK>
+__global__ void __launch_bounds__(NDFT_THREADS, sizeof(T) == 8 ? (TB == 1 ? 2 : SA_D_MINB) : 1)
     k_ndft_fast(const C2<T> *__restrict__ x, C2<T> *__restrict__ y, int64_t batch, int n,
                 const C4<T> *__restrict__ quad, T gain, bool use_gain) {
-  constexpr int TB = NdftCfg<T>::TB, TK = NdftCfg<T>::TK;
   constexpr int BV = 32 * TB;               // vectors per CTA
   constexpr int BK = NDFT_WARPS * TK;       // bins per CTA
   constexpr int CHUNK = BV * NC;            // complex samples per chunk
@@ -622,33 +624,44 @@ int launch(const void *xv, void *yv, int64_t batch, int64_t n64, const SaTwiddle
     return launch_f32x2<F2Small, F2SMALL_MINB>((const float2 *)x, (float2 *)y, batch, n, tw, exact, (float)g,
                                                use_gain, s);
   }
-  constexpr int BK = NDFT_WARPS * NdftCfg<T>::TK;
   const bool pow2 = (n & (n - 1)) == 0;
   const bool tw_smem = (size_t)n * sizeof(C4<T>) <= 64 * 1024;
-  size_t bytes = sizeof(C4<T>) * 2 * NC * BV + sizeof(C4<T>) * (tw_smem ? n : 0);
   const C4<T> *quad = (const C4<T> *)tw->quad;
-  int64_t vblocks = (batch + BV - 1) / BV;
-  unsigned kblocks = (unsigned)((n + BK - 1) / BK);
-  for (int64_t vb = 0; vb < vblocks; vb += 65535) {
-    int64_t nvb = std::min<int64_t>(65535, vblocks - vb);
-    dim3 grid(kblocks, (unsigned)nvb);
-    const C2<T> *xs = x + vb * BV * n;
-    C2<T> *ys = y + vb * BV * n;
-    int64_t bleft = batch - vb * BV;
-#define SA_NDFT_GO(P2, TS)                                                                  \
-  do {                                                                                      \
-    auto kern = exact ? k_ndft_fast<T, P2, TS, true> : k_ndft_fast<T, P2, TS, false>;      \
-    SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes)); \
-    kern<<<grid, NDFT_THREADS, bytes, s>>>(xs, ys, bleft, n, quad, g, use_gain);           \
+  auto go = [&](auto tb_, auto tk_) -> int {
+    constexpr int TBv = decltype(tb_)::value, TKv = decltype(tk_)::value;
+    constexpr int BVv = 32 * TBv, BK = NDFT_WARPS * TKv;
+    size_t bytes = sizeof(C4<T>) * 2 * NC * BVv + sizeof(C4<T>) * (tw_smem ? n : 0);
+    int64_t vblocks = (batch + BVv - 1) / BVv;
+    unsigned kblocks = (unsigned)((n + BK - 1) / BK);
+    for (int64_t vb = 0; vb < vblocks; vb += 65535) {
+      int64_t nvb = std::min<int64_t>(65535, vblocks - vb);
+      dim3 grid(kblocks, (unsigned)nvb);
+      const C2<T> *xs = x + vb * BVv * n;
+      C2<T> *ys = y + vb * BVv * n;
+      int64_t bleft = batch - vb * BVv;
+#define SA_NDFT_GO(P2, TS)                                                                              \
+  do {                                                                                                  \
+    auto kern = exact ? k_ndft_fast<T, P2, TS, true, TBv, TKv> : k_ndft_fast<T, P2, TS, false, TBv, TKv>; \
+    SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));   \
+    kern<<<grid, NDFT_THREADS, bytes, s>>>(xs, ys, bleft, n, quad, g, use_gain);                       \
   } while (0)
-    if (pow2 && tw_smem) SA_NDFT_GO(true, true);
-    else if (pow2) SA_NDFT_GO(true, false);
-    else if (tw_smem) SA_NDFT_GO(false, true);
-    else SA_NDFT_GO(false, false);
+      if (pow2 && tw_smem) SA_NDFT_GO(true, true);
+      else if (pow2) SA_NDFT_GO(true, false);
+      else if (tw_smem) SA_NDFT_GO(false, true);
+      else SA_NDFT_GO(false, false);
 #undef SA_NDFT_GO
-  }
-  SA_LAUNCH_CHECK();
-  return SA_OK;
+    }
+    SA_LAUNCH_CHECK();
+    return SA_OK;
+  };
+  // fp64: the 4 x 4 tile when it fills two waves of 148 SMs, else 1 x 4 (C1: 66 -> 258 CTAs)
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  constexpr int BK4 = NDFT_WARPS * NdftCfg<T>::TK;
+  const int64_t ctas = ((batch + BV - 1) / BV) * ((n + BK4 - 1) / BK4);
+  if (ctas < 2 * (int64_t)sms) return go(std::integral_constant<int, 1>{}, std::integral_constant<int, 4>{});
+  return go(std::integral_constant<int, NdftCfg<T>::TB>{}, std::integral_constant<int, NdftCfg<T>::TK>{});
 }
 
 }  // namespace
