@@ -18,6 +18,12 @@
 //   thread group releases on its own (SA_GREL), so a group that finishes phase B
 //   early starts the next signal.  The TMA tile of the next signal is issued at
 //   the end of phase A, so HBM reads overlap phase B.
+// complex64 DIT (SA_K64_PARK): each thread group computes one phase-A tile of the
+// signal after next ahead of time and parks its results in TMEM (tcgen05.st into the
+// thread's own lane, 32 columns per tile; fetched back with tcgen05.ld for the
+// scatter), so that both cluster-wide waits of a signal -- "storage empty" before
+// the scatter and "storage full" before phase B -- have one tile of compute in front
+// of them (Pipe::run_park): C3 1.753 -> 1.676 ms, outputs bit-identical.
 // Each CTA runs NG thread groups (named barriers, own TMA buffer) that split a
 // phase's tiles.  HBM traffic = one read + one write.  Double-buffered node
 // storage (NS = 2, pipelining phase B of signal s behind phase A of s+1) is
@@ -49,6 +55,24 @@ constexpr int NN = 1 << LOGN;
 #ifndef SA_K64_L2S
 #define SA_K64_L2S 0  // c64: second node storage in an L2 scratch (signals alternate smem / L2)
 #endif
+#ifndef SA_K64_PARK
+#define SA_K64_PARK 1  // c64 DIT: one phase-A tile per signal computed ahead and parked in TMEM (run_park)
+#endif
+#ifndef SA_K64_PARK_LOOP
+#define SA_K64_PARK_LOOP 0  // 1: compact one-call-site form of the PARK signal loop (measured slower)
+#endif
+#ifndef SA_K64_PARK_DIF
+#define SA_K64_PARK_DIF 0  // the same for DIF (measured slower: 1.98 vs 1.79 ms)
+#endif
+#ifndef SA_K64_UNROLL_A
+#define SA_K64_UNROLL_A 0
+#endif
+#ifndef SA_K64_SKEW_F
+#define SA_K64_SKEW_F 0  // ns: thread groups > 0 sleep this long after the full wait (de-phases the groups)
+#endif
+#ifndef SA_K64_SKEW_E
+#define SA_K64_SKEW_E 0  // ns: the same after the empty wait
+#endif
 #ifndef SA_K64F_TC
 #define SA_K64F_TC 16
 #define SA_K64F_CL 4
@@ -65,6 +89,8 @@ template <> struct K64<float> {
   static constexpr bool L2S = SA_K64_L2S;  // storage 1 in a global (L2-resident) scratch
   static constexpr int NS = L2S ? 2 : SA_K64F_NS;  // node storages (2 = pipelined signals)
   static constexpr int MINB = SA_K64F_MINB;  // resident CTAs per SM
+  static constexpr bool PARK = SA_K64_PARK && !SA_K64_L2S && SA_K64F_NS == 1 && SA_K64F_NG * SA_K64F_TC == 32;
+  static constexpr bool PARK_DIF = PARK && SA_K64_PARK_DIF;
 };
 #ifndef SA_K64D_TC  // complex128 shape (-D for sweeps)
 #define SA_K64D_TC 8
@@ -77,11 +103,13 @@ template <> struct K64<double> {
   static constexpr bool L2S = false;
   static constexpr int NS = 1;
   static constexpr int MINB = 1;
+  static constexpr bool PARK = false, PARK_DIF = false;
 };
 
 template <typename T> struct L64 {
   static constexpr int TC = K64<T>::TC, CL = K64<T>::CL, NG = K64<T>::NG, NS = K64<T>::NS;
   static constexpr bool L2S = K64<T>::L2S;
+  static constexpr bool PARK = K64<T>::PARK, PARK_DIF = K64<T>::PARK_DIF;
   static constexpr int NSM = L2S ? 1 : NS;  // node storages in smem
   static constexpr int GT = 16 * TC;       // threads per group
   static constexpr int THREADS = NG * GT;
@@ -96,7 +124,13 @@ template <typename T> struct L64 {
   static constexpr size_t OFF_WORK = NSM * INTER1;
   static constexpr size_t OFF_TWA = OFF_WORK + NG * WORK;
   static constexpr size_t OFF_BAR = OFF_TWA + TWA;
-  static constexpr size_t SMEM = OFF_BAR + 8 * (NG + 2 * NS);
+  static constexpr size_t OFF_TMEM = OFF_BAR + 8 * (NG + 2 * NS);  // PARK: the TMEM base address
+  static constexpr size_t SMEM = OFF_TMEM + 8;
+  // PARK: a thread parks one tile's 16 values (32 words) in its own TMEM lane; the 4 warps of a lane
+  // quarter x TPG tiles take 32 columns each
+  static constexpr int PARK_COLS = 32 * TPG * (THREADS / 128);
+  static_assert(!PARK || (TPG == 2 && THREADS % 128 == 0 && PARK_COLS <= 512 && (PARK_COLS & (PARK_COLS - 1)) == 0),
+                "park layout");
   static constexpr int EW = sizeof(C2) / 8;  // 8-byte TMA elements per complex
   static_assert(TILES % NG == 0 && TPG >= 1, "tiles must split evenly over groups");
 };
@@ -134,8 +168,34 @@ template <typename T> SA_HD typename Ar<T>::C4 c4of(const typename Ar<T>::C2 &w)
 }
 SA_HD bool special_column(int q) { return __any_sync(0xffffffffu, q == 0 || q == 128); }
 
+// TMEM parking (SA_K64_PARK): 32 words of the executing thread's own lane, 32x32b shape
+SA_HD void tm_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+SA_HD void tm_ld32(uint32_t (&r)[32], uint32_t taddr) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 // Shared per-CTA state and the signal pipeline orchestration of both kernels.
-template <typename T> struct Pipe {
+// PK: the TMEM-parking schedule (run_park) is in use
+template <typename T, bool PK = false> struct Pipe {
   using P = L64<T>;
   using C2 = typename P::C2;
   using C4 = typename P::C4;
@@ -147,7 +207,28 @@ template <typename T> struct Pipe {
   uint32_t tile_it = 0;
   C2 *scr = nullptr;  // L2S: this cluster's scratch storage, [owner][INTER1 / sizeof(C2)]
   static constexpr int SE = (int)(P::INTER1 / sizeof(C2));  // elements of one owner's share
+  uint32_t tm_park = 0;  // PARK: TMEM address of this thread's first parking slot
   SA_HD static bool in_l2(int b) { return P::L2S && b == 1; }
+  // park / fetch tile u's 16 register values (fp32 pairs) in the thread's TMEM lane
+  template <typename V> SA_HD void park(int u, const V (&v)[16]) const {
+    if constexpr (PK) {
+      uint32_t r[32];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        r[2 * k] = (uint32_t)v[k];
+        r[2 * k + 1] = (uint32_t)(v[k] >> 32);
+      }
+      tm_st32(tm_park + 32u * (uint32_t)u, r);
+    }
+  }
+  template <typename V> SA_HD void unpark(int u, V (&v)[16]) const {
+    if constexpr (PK) {
+      uint32_t r[32];
+      tm_ld32(r, tm_park + 32u * (uint32_t)u);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = (V)r[2 * k] | ((V)r[2 * k + 1] << 32);
+    }
+  }
   template <bool S> SA_HD static C2 ld(const C2 *p) {
     if constexpr (S) return __ldcg(p);
     else return *p;
@@ -223,8 +304,33 @@ template <typename T> struct Pipe {
       }
       sa_fence_mbar_init();
     }
+    if constexpr (PK) {
+      uint32_t *holder = reinterpret_cast<uint32_t *>(smem + P::OFF_TMEM);
+      if (threadIdx.x < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa_smem_u32(holder)),
+                     "r"((uint32_t)P::PARK_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t w = threadIdx.x >> 5;
+      tm_park = *holder + (((w & 3u) * 32u) << 16) + (w >> 2) * (uint32_t)(32 * P::TPG);
+    }
     __syncthreads();
     cluster.sync();
+  }
+  SA_HD void finish() const {
+    if constexpr (PK) {
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        const uint32_t base = *reinterpret_cast<const uint32_t *>(smem + P::OFF_TMEM);
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "r"((uint32_t)P::PARK_COLS)
+                     : "memory");
+      }
+    }
   }
   // group-leader TMA of tile tt (TC columns x 256 rows) of signal sig
   SA_HD void tma(const CUtensorMap *tmx, int64_t sig, int tt) const {
@@ -259,10 +365,12 @@ template <typename T> struct Pipe {
   SA_HD void wait_empty(int b, uint32_t parity) const {
     if (in_l2(b)) sa_mbar_wait_cluster(&empty_bar[b], parity);
     else group_wait(&empty_bar[b], parity);
+    if (SA_K64_SKEW_E > 0 && gi > 0) __nanosleep(SA_K64_SKEW_E * gi);
   }
   SA_HD void wait_full(int b, uint32_t parity) const {
     if (in_l2(b)) sa_mbar_wait_cluster(&full_bar[b], parity);
     else group_wait(&full_bar[b], parity);
+    if (SA_K64_SKEW_F > 0 && gi > 0) __nanosleep(SA_K64_SKEW_F * gi);
   }
   // signal loop: phaseA(sig, b, use, next_sig) then (pipelined) phaseB of the
   // previous signal; every storage use waits full/empty with parity use & 1.
@@ -295,6 +403,78 @@ template <typename T> struct Pipe {
     cg::this_cluster().sync();  // the probe skips the storage waits: let peers' stores land first
 #endif
   }
+  // PARK signal loop (one node storage, TPG = 2).  tileA(M = 3, sig, u, b, use, we, tsig, tu)
+  // computes phase-A tile u of sig (issuing the group's next TMA (tsig, tile index tu) once its
+  // buffer is consumed) and then either parks the 16 results of each thread in TMEM (we = false)
+  // or waits for the storage, scatters them and the parked tile 1, and arrives on full.  Per group:
+  //   B(s) | release | X: A(s+1, tile 0), wait empty, scatter tiles 0 and 1 | Y: A(s+2, tile 1), park |
+  //   wait full | B(s+1) ...
+  // so each of the two cluster-wide waits has one tile of compute in front of it.  One loop, one
+  // call site per lambda (the instruction cache matters: an unrolled phase A costs 5%).
+  template <class FT, class FB>
+  SA_HD void run_park(const CUtensorMap *tmx, int64_t batch, FT tileA, FB phaseB) {
+    static_assert(!PK || P::TPG == 2, "PARK schedule is written for two tiles per group");
+    const uint32_t tx = (uint32_t)(SA_LOCALQ ? P::INTER1 - P::INTER1 / P::CL : P::INTER1);
+#if !SA_K64_PARK_LOOP
+    // straight-line form (default: 1.676 ms C3 DIT against 1.829 for the compact loop below,
+    // although it is twice the code)
+    using M0 = std::integral_constant<int, 0>;
+    using M1 = std::integral_constant<int, 1>;
+    using M2 = std::integral_constant<int, 2>;
+    auto sig_or_none = [&](int64_t sg) { return sg < batch ? sg : (int64_t)-1; };
+    if (cid < batch) tma(tmx, cid, gi);
+    release(0);
+    if (cid < batch) {
+      if (threadIdx.x == 0) sa_mbar_expect_tx(&full_bar[0], tx);
+      tileA(M0{}, cid, 0, 0, 0u, true, cid, 1);
+      tileA(M0{}, cid, 1, 0, 0u, false, sig_or_none(cid + ncl), 1);
+      local_done(0);
+      if (cid + ncl < batch) tileA(M1{}, cid + ncl, 1, 0, 0u, false, cid + ncl, 0);
+    }
+    uint32_t it = 0;
+    for (int64_t sig = cid; sig < batch; sig += ncl, ++it) {
+      const int64_t n1 = sig + ncl, n2 = n1 + ncl;
+      phaseB(sig, 0, it);  // waits full (parity it & 1)
+      if (n1 < batch) {
+        // the next use of the full barrier is armed after this one completed (thread 0 has
+        // passed its wait) and before this group's release lets any peer send
+        if (threadIdx.x == 0) sa_mbar_expect_tx(&full_bar[0], tx);
+        release(0);
+        tileA(M0{}, n1, 0, 0, it + 1, true, sig_or_none(n2), 1);
+        tileA(M2{}, n1, 1, 0, it + 1, false, (int64_t)-1, 0);
+        local_done(0);
+        if (n2 < batch) tileA(M1{}, n2, 1, 0, 0u, false, n2, 0);
+      }
+    }
+    finish();
+    return;
+#endif
+    if (cid < batch) tma(tmx, cid, gi + P::NG);  // tile index 1 of the first signal comes first
+    release(0);
+    for (int64_t i = -2;; ++i) {
+      const int64_t sig = cid + i * ncl;
+      if (i >= 0) {
+        if (sig >= batch) break;
+        phaseB(sig, 0, (uint32_t)i);  // waits full (parity i & 1)
+      }
+#pragma unroll 1
+      for (int j = 0; j < 2; ++j) {
+        const bool isx = j == 0;
+        const int64_t s = sig + (isx ? 1 : 2) * ncl;  // X: signal i + 1, Y: signal i + 2
+        if (s >= batch || (isx && i < -1)) continue;
+        int64_t tsig = s;  // Y: this signal's tile 0 next
+        if (isx) {
+          // the next use of the full barrier is armed after the last one completed (thread 0
+          // has passed its wait) and before this group's release lets any peer send
+          if (threadIdx.x == 0) sa_mbar_expect_tx(&full_bar[0], tx);
+          if (i >= 0) release(0);
+          tsig = s + ncl < batch ? s + ncl : (int64_t)-1;  // X: the next signal's tile 1
+        }
+        tileA(std::integral_constant<int, 3>{}, s, isx ? 0 : 1, 0, (uint32_t)(i + 1), isx, tsig, isx ? 1 : 0);
+      }
+    }
+    finish();
+  }
 };
 
 template <typename T>
@@ -310,19 +490,25 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
   using C4 = typename P::C4;
   constexpr int TC = P::TC, COLS = P::COLS, NG = P::NG, GT = P::GT, TPG = P::TPG;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  Pipe<T> pp;
+  Pipe<T, P::PARK> pp;
   pp.init(smem_raw, stage, scratch);
   const int gbar = 1 + pp.gi;
   const int m1_cc = pp.gt % TC, m1_g = pp.gt / TC;
   const int m2_g = pp.gt & 15, m2_cc = pp.gt >> 4;
   const C4 *twA = pp.twA;
 
-  auto phaseA = [&](int64_t sig, int b, uint32_t use, int64_t nsig) {
-    for (int u = 0; u < TPG; ++u) {
-      const int tt = pp.gi + NG * u;
+  // M = 0: compute and scatter; PARK schedule (run_park): 1 compute and park, 2 fetch the parked
+  // tile and scatter, 3 the runtime-selected form of the compact loop
+  // one phase-A tile; the group's next TMA (signal tsig, tile index tu; none if tsig < 0) is issued
+  // once the tile buffer has been consumed; we: wait for the storage to be free before scattering
+  auto tileA = [&](auto M_, int64_t sig, int u, int b, uint32_t use, bool we, int64_t tsig, int tu) {
+    constexpr int M = decltype(M_)::value;
+    {
+      V v[16];
+      if constexpr (M == 2) pp.unpark(u, v);
+      if constexpr (M != 2) {
       pp.wait_tile();
       C2 *wk = pp.work();
-      V v[16];
       {  // round 1 (M1): v[k] = node 16g+k of sub-transform cc = X[rev8(16g+k)][cc]
         const int rg = rev4(m1_g);
 #pragma unroll
@@ -364,8 +550,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
       for (int k = 0; k < 16; ++k)  // round 2 (M2): node g + 16k of sub-transform cc
         v[k] = A::from(wk[(m2_g + 16 * k) * TC + (m2_cc ^ (m2_g & (TC - 1)))]);
       group_sync(gbar, GT);  // tile buffer consumed: re-arm it
-      if (u + 1 < TPG) pp.tma(&tmx, sig, tt + NG);
-      else if (nsig < batch) pp.tma(&tmx, nsig, pp.gi);
+      if (tsig >= 0) pp.tma(&tmx, tsig, pp.gi + NG * tu);
 #ifndef SA_PROBE_SKIP_A
 #pragma unroll
       for (int t = 5; t <= 8; ++t) {
@@ -375,22 +560,50 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
           if (!(k & hr)) r_dit<T>(v[k], v[k + hr], twA[(h - 1) + m2_g + 16 * (k & (hr - 1))]);
       }
 #endif
-      // scatter node row R = rev8(c): column q lives in CTA q / COLS
-      if (u == 0) pp.wait_empty(b, use & 1);  // peers released storage b
-      const int R = rev8(pp.rank * COLS + tt * TC + m2_cc);
-      constexpr int KPC = COLS / 16;  // registers per owner CTA
+      }
+      // scatter node row R = rev8(c) of tile index uu: column q lives in CTA q / COLS
+      auto scat = [&](int uu) {
+        const int R = rev8(pp.rank * COLS + (pp.gi + NG * uu) * TC + m2_cc);
+        constexpr int KPC = COLS / 16;  // registers per owner CTA
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const int e = R * COLS + m2_g + 16 * (k % KPC);
-        if (Pipe<T>::in_l2(b)) __stcg(&pp.scr[(k / KPC) * Pipe<T>::SE + e], A::to(v[k]));
-        else if (SA_LOCALQ && k / KPC == pp.rank) pp.inter(b)[e] = A::to(v[k]);
+        for (int k = 0; k < 16; ++k) {
+          const int e = R * COLS + m2_g + 16 * (k % KPC);
+          if (Pipe<T>::in_l2(b)) __stcg(&pp.scr[(k / KPC) * Pipe<T>::SE + e], A::to(v[k]));
+          else if (SA_LOCALQ && k / KPC == pp.rank) pp.inter(b)[e] = A::to(v[k]);
 #ifndef SA_PROBE_NOSCATTER
-        else sa_st_async(pp.peer_inter(b, k / KPC, (uint32_t)(sizeof(C2) * e)), A::to(v[k]), pp.peer_full(b, k / KPC));
+          else sa_st_async(pp.peer_inter(b, k / KPC, (uint32_t)(sizeof(C2) * e)), A::to(v[k]), pp.peer_full(b, k / KPC));
 #else
-        else pp.inter(b)[e] = A::to(v[k]);  // probe: local store instead of the DSMEM scatter
+          else pp.inter(b)[e] = A::to(v[k]);  // probe: local store instead of the DSMEM scatter
 #endif
+        }
+      };
+      if constexpr (M == 1) {  // PARK: park this tile
+        pp.park(u, v);
+      } else if constexpr (M == 3) {  // PARK, compact loop: we ? scatter this tile (0) and the parked tile 1 : park
+        if (!we) {
+          pp.park(u, v);
+          return;
+        }
+        pp.wait_empty(b, use & 1);
+#pragma unroll 1
+        for (int w = 0; w < 2; ++w) {
+          if (w) pp.unpark(1, v);
+          scat(w);
+        }
+        pp.local_done(b);
+      } else {
+        if (we) pp.wait_empty(b, use & 1);  // peers released storage b
+        scat(u);
       }
     }
+  };
+  auto phaseA = [&](int64_t sig, int b, uint32_t use, int64_t nsig) {
+#if SA_K64_UNROLL_A
+#pragma unroll
+#endif
+    for (int u = 0; u < TPG; ++u)
+      tileA(std::integral_constant<int, 0>{}, sig, u, b, use, u == 0,
+            u + 1 < TPG ? sig : (nsig < batch ? nsig : (int64_t)-1), u + 1 < TPG ? u + 1 : 0);
     pp.local_done(b);
   };
 
@@ -473,7 +686,11 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
     phaseB_s(std::false_type{}, sig, b, use);
   };
 
-  pp.run(&tmx, batch, phaseA, phaseB);
+  if constexpr (P::PARK) {
+    pp.run_park(&tmx, batch, tileA, phaseB);
+  } else {
+    pp.run(&tmx, batch, phaseA, phaseB);
+  }
 }
 
 // DIF (DESIGN.md convention): stages s = 16..2 with top = a + b, bot = W ⊙ (a − b),
@@ -496,7 +713,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
   using C4 = typename P::C4;
   constexpr int TC = P::TC, COLS = P::COLS, NG = P::NG, GT = P::GT, TPG = P::TPG;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  Pipe<T> pp;
+  Pipe<T, P::PARK_DIF> pp;
   pp.init(smem_raw, stage, scratch);
   const int gbar = 1 + pp.gi;
   const int m1_cc = pp.gt % TC, m1_g = pp.gt / TC;
@@ -504,16 +721,19 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
   const C4 *twA = pp.twA;
   const int rg1 = rev4(m1_g);
 
-  auto phaseA = [&](int64_t sig, int b, uint32_t use, int64_t nsig) {
-    for (int u = 0; u < TPG; ++u) {
+  auto tileA = [&](auto M_, int64_t sig, int u, int b, uint32_t use, bool we, int64_t tsig, int tu) {
+    constexpr int M = decltype(M_)::value;  // as in the DIT kernel
+    {
       const int tt = pp.gi + NG * u;
       const int q = pp.rank * COLS + tt * TC + m1_cc;
+      V v[16];
+      if constexpr (M == 2) pp.unpark(u, v);
+      if constexpr (M != 2) {
       const bool gen = special_column(q);
       C2 wf[30];
       load_wf<T>(wf, stage2, q, m1_g);
       pp.wait_tile();
       C2 *wk = pp.work();
-      V v[16];
 #pragma unroll
       for (int k = 0; k < 16; ++k) {  // R = g + 16k
         V x = A::from(wk[(m1_g + 16 * k) * TC + m1_cc]);
@@ -542,8 +762,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
 #pragma unroll
       for (int k = 0; k < 16; ++k) v[k] = A::from(wk[(m1_g * 16 + k) * TC + m1_cc]);  // R = 16g + k
       group_sync(gbar, GT);  // tile buffer consumed: re-arm it
-      if (u + 1 < TPG) pp.tma(&tmx, sig, tt + NG);
-      else if (nsig < batch) pp.tma(&tmx, nsig, pp.gi);
+      if (tsig >= 0) pp.tma(&tmx, tsig, pp.gi + NG * tu);
       if (gen) {
 #pragma unroll
         for (int t = 4; t >= 1; --t) {  // R bits 3..0
@@ -561,17 +780,46 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
             if (!(k & h)) r_dif_fast<T>(v[k], v[k + h], wf[h - 1 + (k & (h - 1))]);
         }
       }
-      if (u == 0) pp.wait_empty(b, use & 1);
+      }
+      auto scat = [&](int uu) {
+        const int qq = pp.rank * COLS + (pp.gi + NG * uu) * TC + m1_cc;
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {  // row R = 16g + k -> CTA owning cr = rev8(R), local row cr mod COLS
-        const int cr = crev4(k) * 16 + rg1;
-        const int lr = cr % COLS;
-        const int e = lr * 256 + (q ^ (lr & 15));
-        if (Pipe<T>::in_l2(b)) __stcg(&pp.scr[(cr / COLS) * Pipe<T>::SE + e], A::to(v[k]));
-        else if (SA_LOCALQ && cr / COLS == pp.rank) pp.inter(b)[e] = A::to(v[k]);  // owner is warp-uniform
-        else sa_st_async(pp.peer_inter(b, cr / COLS, (uint32_t)(sizeof(C2) * e)), A::to(v[k]), pp.peer_full(b, cr / COLS));
+        for (int k = 0; k < 16; ++k) {  // row R = 16g + k -> CTA owning cr = rev8(R), local row cr mod COLS
+          const int cr = crev4(k) * 16 + rg1;
+          const int lr = cr % COLS;
+          const int e = lr * 256 + (qq ^ (lr & 15));
+          if (Pipe<T>::in_l2(b)) __stcg(&pp.scr[(cr / COLS) * Pipe<T>::SE + e], A::to(v[k]));
+          else if (SA_LOCALQ && cr / COLS == pp.rank) pp.inter(b)[e] = A::to(v[k]);  // owner is warp-uniform
+          else sa_st_async(pp.peer_inter(b, cr / COLS, (uint32_t)(sizeof(C2) * e)), A::to(v[k]), pp.peer_full(b, cr / COLS));
+        }
+      };
+      if constexpr (M == 1) {
+        pp.park(u, v);
+      } else if constexpr (M == 3) {  // PARK: as in the DIT kernel
+        if (!we) {
+          pp.park(u, v);
+          return;
+        }
+        pp.wait_empty(b, use & 1);
+#pragma unroll 1
+        for (int w = 0; w < 2; ++w) {
+          if (w) pp.unpark(1, v);
+          scat(w);
+        }
+        pp.local_done(b);
+      } else {
+        if (we) pp.wait_empty(b, use & 1);
+        scat(u);
       }
     }
+  };
+  auto phaseA = [&](int64_t sig, int b, uint32_t use, int64_t nsig) {
+#if SA_K64_UNROLL_A
+#pragma unroll
+#endif
+    for (int u = 0; u < TPG; ++u)
+      tileA(std::integral_constant<int, 0>{}, sig, u, b, use, u == 0,
+            u + 1 < TPG ? sig : (nsig < batch ? nsig : (int64_t)-1), u + 1 < TPG ? u + 1 : 0);
     pp.local_done(b);
   };
 
@@ -646,7 +894,11 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
     phaseB_s(std::false_type{}, sig, b, use);
   };
 
-  pp.run(&tmx, batch, phaseA, phaseB);
+  if constexpr (P::PARK_DIF) {
+    pp.run_park(&tmx, batch, tileA, phaseB);
+  } else {
+    pp.run(&tmx, batch, phaseA, phaseB);
+  }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {

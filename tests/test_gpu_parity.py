@@ -329,6 +329,23 @@ def test_nfft64k_persistent_loop(sa, dt):
     assert_value_equal(xd.cpu().numpy(), oracle.nfft(xs, "dit", dtype=od, nthreads=8))
 
 
+@pytest.mark.parametrize("variant", ["dit", "dif"])
+def test_nfft64k_batch_edges(sa, variant):
+    """Fused 2^16 kernel, complex64, batch sizes around the number of resident
+    clusters (33 on a B200): 1, 2 and 3+ signals per cluster and clusters with one
+    signal fewer than others -- every prologue / steady / drain case of the signal
+    pipeline (the DIT kernel's TMEM-parking schedule computes one tile of signal
+    s + 2 before phase B of signal s + 1)."""
+    g = np.random.default_rng(165)
+    bmax = 133
+    xs = (g.standard_normal((bmax, 1 << 16)) + 1j * g.standard_normal((bmax, 1 << 16))).astype(np.complex64)
+    ref = oracle.nfft(xs, variant, dtype="f32", nthreads=8)
+    xd = dev(xs)
+    for b in (1, 2, 32, 33, 34, 66, 67, 100, 133):
+        y = sa.nfft_batch(xd[:b], variant=variant).cpu().numpy()
+        assert_value_equal(y, ref[:b])
+
+
 def test_map_c5_sampled_rows(sa):
     """C5 (2^22 samples, 8 targets), 4096 delay bins x 2048 Doppler bins, c64 on
     the GPU; the fp64 oracle of the same complex64 inputs on the target rows and
