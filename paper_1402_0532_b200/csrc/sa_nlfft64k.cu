@@ -23,7 +23,9 @@
 // thread's own lane, 32 columns per tile; fetched back with tcgen05.ld for the
 // scatter), so that both cluster-wide waits of a signal -- "storage empty" before
 // the scatter and "storage full" before phase B -- have one tile of compute in front
-// of them (Pipe::run_park): C3 1.753 -> 1.676 ms, outputs bit-identical.
+// of them (Pipe::run_park): C3 1.753 -> 1.676 ms, outputs bit-identical.  complex128
+// uses the same schedule (64 words per tile) in DIT and DIF, in the compact loop form
+// (4.28 -> 4.24 ms, 4.74 -> 4.42 ms); complex64 DIF does not (measured slower).
 // Each CTA runs NG thread groups (named barriers, own TMA buffer) that split a
 // phase's tiles.  HBM traffic = one read + one write.  Double-buffered node
 // storage (NS = 2, pipelining phase B of signal s behind phase A of s+1) is
@@ -59,7 +61,7 @@ constexpr int NN = 1 << LOGN;
 #define SA_K64_PARK 1  // c64 DIT: one phase-A tile per signal computed ahead and parked in TMEM (run_park)
 #endif
 #ifndef SA_K64_PARK_LOOP
-#define SA_K64_PARK_LOOP 0  // 1: compact one-call-site form of the PARK signal loop (measured slower)
+#define SA_K64_PARK_LOOP 0  // c64: 1 = compact one-call-site form of the PARK signal loop (1.829 vs 1.676 ms DIT)
 #endif
 #ifndef SA_K64_PARK_DIF
 #define SA_K64_PARK_DIF 0  // the same for DIF (measured slower: 1.98 vs 1.79 ms)
@@ -91,10 +93,20 @@ template <> struct K64<float> {
   static constexpr int MINB = SA_K64F_MINB;  // resident CTAs per SM
   static constexpr bool PARK = SA_K64_PARK && !SA_K64_L2S && SA_K64F_NS == 1 && SA_K64F_NG * SA_K64F_TC == 32;
   static constexpr bool PARK_DIF = PARK && SA_K64_PARK_DIF;
+  static constexpr bool PARK_LOOP = SA_K64_PARK_LOOP;
 };
 #ifndef SA_K64D_TC  // complex128 shape (-D for sweeps)
 #define SA_K64D_TC 8
 #define SA_K64D_NG 2
+#endif
+#ifndef SA_K64D_PARK
+#define SA_K64D_PARK 1  // complex128: the TMEM-parking schedule, DIT (4.36 -> 4.24-4.34 ms)
+#endif
+#ifndef SA_K64D_PARK_DIF
+#define SA_K64D_PARK_DIF 1  // and DIF (4.74 -> 4.44 ms)
+#endif
+#ifndef SA_K64D_PARK_LOOP
+#define SA_K64D_PARK_LOOP 1  // compact loop form (the straight-line form is slower here: 4.57 / 4.86 ms)
 #endif
 template <> struct K64<double> {
   static constexpr int TC = SA_K64D_TC;
@@ -103,7 +115,8 @@ template <> struct K64<double> {
   static constexpr bool L2S = false;
   static constexpr int NS = 1;
   static constexpr int MINB = 1;
-  static constexpr bool PARK = false, PARK_DIF = false;
+  static constexpr bool PARK = SA_K64D_PARK && SA_K64D_NG * SA_K64D_TC == 16, PARK_DIF = PARK && SA_K64D_PARK_DIF;
+  static constexpr bool PARK_LOOP = SA_K64D_PARK_LOOP;
 };
 
 template <typename T> struct L64 {
@@ -128,7 +141,8 @@ template <typename T> struct L64 {
   static constexpr size_t SMEM = OFF_TMEM + 8;
   // PARK: a thread parks one tile's 16 values (32 words) in its own TMEM lane; the 4 warps of a lane
   // quarter x TPG tiles take 32 columns each
-  static constexpr int PARK_COLS = 32 * TPG * (THREADS / 128);
+  static constexpr int PARK_W = 4 * (int)sizeof(C2);  // words per thread and tile
+  static constexpr int PARK_COLS = PARK_W * TPG * (THREADS / 128);
   static_assert(!PARK || (TPG == 2 && THREADS % 128 == 0 && PARK_COLS <= 512 && (PARK_COLS & (PARK_COLS - 1)) == 0),
                 "park layout");
   static constexpr int EW = sizeof(C2) / 8;  // 8-byte TMA elements per complex
@@ -209,8 +223,9 @@ template <typename T, bool PK = false> struct Pipe {
   static constexpr int SE = (int)(P::INTER1 / sizeof(C2));  // elements of one owner's share
   uint32_t tm_park = 0;  // PARK: TMEM address of this thread's first parking slot
   SA_HD static bool in_l2(int b) { return P::L2S && b == 1; }
-  // park / fetch tile u's 16 register values (fp32 pairs) in the thread's TMEM lane
-  template <typename V> SA_HD void park(int u, const V (&v)[16]) const {
+  // park / fetch tile u's 16 register values (fp32 pairs: 32 words; fp64 pairs: 64 words) in the
+  // thread's TMEM lane
+  SA_HD void park(int u, const sa_u64 (&v)[16]) const {
     if constexpr (PK) {
       uint32_t r[32];
 #pragma unroll
@@ -221,12 +236,42 @@ template <typename T, bool PK = false> struct Pipe {
       tm_st32(tm_park + 32u * (uint32_t)u, r);
     }
   }
-  template <typename V> SA_HD void unpark(int u, V (&v)[16]) const {
+  SA_HD void unpark(int u, sa_u64 (&v)[16]) const {
     if constexpr (PK) {
       uint32_t r[32];
       tm_ld32(r, tm_park + 32u * (uint32_t)u);
 #pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = (V)r[2 * k] | ((V)r[2 * k + 1] << 32);
+      for (int k = 0; k < 16; ++k) v[k] = (sa_u64)r[2 * k] | ((sa_u64)r[2 * k + 1] << 32);
+    }
+  }
+  SA_HD void park(int u, const double2 (&v)[16]) const {
+    if constexpr (PK) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t r[32];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          r[4 * k] = (uint32_t)__double2loint(v[8 * h + k].x);
+          r[4 * k + 1] = (uint32_t)__double2hiint(v[8 * h + k].x);
+          r[4 * k + 2] = (uint32_t)__double2loint(v[8 * h + k].y);
+          r[4 * k + 3] = (uint32_t)__double2hiint(v[8 * h + k].y);
+        }
+        tm_st32(tm_park + 64u * (uint32_t)u + 32u * (uint32_t)h, r);
+      }
+    }
+  }
+  SA_HD void unpark(int u, double2 (&v)[16]) const {
+    if constexpr (PK) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t r[32];
+        tm_ld32(r, tm_park + 64u * (uint32_t)u + 32u * (uint32_t)h);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          v[8 * h + k].x = __hiloint2double((int)r[4 * k + 1], (int)r[4 * k]);
+          v[8 * h + k].y = __hiloint2double((int)r[4 * k + 3], (int)r[4 * k + 2]);
+        }
+      }
     }
   }
   template <bool S> SA_HD static C2 ld(const C2 *p) {
@@ -316,7 +361,7 @@ template <typename T, bool PK = false> struct Pipe {
       __syncthreads();
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t w = threadIdx.x >> 5;
-      tm_park = *holder + (((w & 3u) * 32u) << 16) + (w >> 2) * (uint32_t)(32 * P::TPG);
+      tm_park = *holder + (((w & 3u) * 32u) << 16) + (w >> 2) * (uint32_t)(P::PARK_W * P::TPG);
     }
     __syncthreads();
     cluster.sync();
@@ -415,9 +460,9 @@ template <typename T, bool PK = false> struct Pipe {
   SA_HD void run_park(const CUtensorMap *tmx, int64_t batch, FT tileA, FB phaseB) {
     static_assert(!PK || P::TPG == 2, "PARK schedule is written for two tiles per group");
     const uint32_t tx = (uint32_t)(SA_LOCALQ ? P::INTER1 - P::INTER1 / P::CL : P::INTER1);
-#if !SA_K64_PARK_LOOP
-    // straight-line form (default: 1.676 ms C3 DIT against 1.829 for the compact loop below,
-    // although it is twice the code)
+    if constexpr (!K64<T>::PARK_LOOP) {
+    // straight-line form (complex64: 1.676 ms C3 DIT against 1.829 for the compact loop below,
+    // although it is twice the code; complex128 is faster with the compact loop)
     using M0 = std::integral_constant<int, 0>;
     using M1 = std::integral_constant<int, 1>;
     using M2 = std::integral_constant<int, 2>;
@@ -448,7 +493,7 @@ template <typename T, bool PK = false> struct Pipe {
     }
     finish();
     return;
-#endif
+    }
     if (cid < batch) tma(tmx, cid, gi + P::NG);  // tile index 1 of the first signal comes first
     release(0);
     for (int64_t i = -2;; ++i) {

@@ -329,19 +329,23 @@ def test_nfft64k_persistent_loop(sa, dt):
     assert_value_equal(xd.cpu().numpy(), oracle.nfft(xs, "dit", dtype=od, nthreads=8))
 
 
+@pytest.mark.parametrize("dt", ["c64", "c128"])
 @pytest.mark.parametrize("variant", ["dit", "dif"])
-def test_nfft64k_batch_edges(sa, variant):
-    """Fused 2^16 kernel, complex64, batch sizes around the number of resident
-    clusters (33 on a B200): 1, 2 and 3+ signals per cluster and clusters with one
-    signal fewer than others -- every prologue / steady / drain case of the signal
-    pipeline (the DIT kernel's TMEM-parking schedule computes one tile of signal
-    s + 2 before phase B of signal s + 1)."""
+def test_nfft64k_batch_edges(sa, variant, dt):
+    """Fused 2^16 kernel, batch sizes around the number of resident clusters (33
+    clusters of 4 CTAs for complex64, up to 18 of 8 for complex128 on a B200): 1, 2
+    and 3+ signals per cluster and clusters with one signal fewer than others --
+    every prologue / steady / drain case of the signal pipeline (the TMEM-parking
+    schedule computes one tile of signal s + 2 before phase B of signal s + 1; the
+    complex64 and complex128 kernels use different forms of that loop)."""
     g = np.random.default_rng(165)
-    bmax = 133
-    xs = (g.standard_normal((bmax, 1 << 16)) + 1j * g.standard_normal((bmax, 1 << 16))).astype(np.complex64)
-    ref = oracle.nfft(xs, variant, dtype="f32", nthreads=8)
+    batches = (1, 2, 32, 33, 34, 66, 67, 100, 133) if dt == "c64" else (1, 2, 15, 16, 17, 18, 19, 35, 37, 55)
+    bmax = batches[-1]
+    cdt = np.complex64 if dt == "c64" else np.complex128
+    xs = (g.standard_normal((bmax, 1 << 16)) + 1j * g.standard_normal((bmax, 1 << 16))).astype(cdt)
+    ref = oracle.nfft(xs, variant, dtype="f32" if dt == "c64" else "f64", nthreads=8)
     xd = dev(xs)
-    for b in (1, 2, 32, 33, 34, 66, 67, 100, 133):
+    for b in batches:
         y = sa.nfft_batch(xd[:b], variant=variant).cpu().numpy()
         assert_value_equal(y, ref[:b])
 
