@@ -69,6 +69,9 @@ constexpr int NN = 1 << LOGN;
 #ifndef SA_K64_UNROLL_A
 #define SA_K64_UNROLL_A 0
 #endif
+#ifndef SA_K64_WX
+#define SA_K64_WX 0  // c64 DIT: phase-A 16 x 16 exchange inside a warp (128B-swizzled TMA tiles, __syncwarp)
+#endif
 #ifndef SA_K64_SKEW_F
 #define SA_K64_SKEW_F 0  // ns: thread groups > 0 sleep this long after the full wait (de-phases the groups)
 #endif
@@ -138,7 +141,8 @@ template <typename T> struct L64 {
   static constexpr size_t OFF_TWA = OFF_WORK + NG * WORK;
   static constexpr size_t OFF_BAR = OFF_TWA + TWA;
   static constexpr size_t OFF_TMEM = OFF_BAR + 8 * (NG + 2 * NS);  // PARK: the TMEM base address
-  static constexpr size_t SMEM = OFF_TMEM + 8;
+  static constexpr size_t OFF_CONS = OFF_TMEM + 8;  // WX = 2: per-group count of warps that consumed the tile
+  static constexpr size_t SMEM = OFF_CONS + 4 * NG;
   // PARK: a thread parks one tile's 16 values (32 words) in its own TMEM lane; the 4 warps of a lane
   // quarter x TPG tiles take 32 columns each
   static constexpr int PARK_W = 4 * (int)sizeof(C2);  // words per thread and tile
@@ -339,6 +343,7 @@ template <typename T, bool PK = false> struct Pipe {
       pfull[r] = sa_mapa(sa_smem_u32(smem + P::OFF_BAR + 8 * P::NG), r);
     }
     for (int e = threadIdx.x; e < 255; e += P::THREADS) twA[e] = stage[e];  // global stages 1..8
+    if (threadIdx.x < P::NG) reinterpret_cast<uint32_t *>(smem + P::OFF_CONS)[threadIdx.x] = 0u;
     if (threadIdx.x == 0) {
       for (int g = 0; g < P::NG; ++g) sa_mbar_init(&tma_bar[g], 1);
       for (int b = 0; b < P::NS; ++b) {
@@ -383,6 +388,21 @@ template <typename T, bool PK = false> struct Pipe {
       sa_fence_proxy_async();
       sa_mbar_expect_tx(&tma_bar[gi], (uint32_t)P::WORK);
       sa_tma_load_2d(work(), tmx, (rank * P::COLS + tt * P::TC) * P::EW, (int)(sig * 256), &tma_bar[gi]);
+    }
+  }
+  // WX = 2: every warp calls this once its lanes have read the tile (after __syncwarp); the last
+  // of the group's warps re-arms the buffer and issues the next TMA -- no group barrier
+  SA_HD void tma_last(const CUtensorMap *tmx, int64_t sig, int tt) const {
+    if ((threadIdx.x & 31) == 0) {
+      uint32_t *cons = reinterpret_cast<uint32_t *>(smem + P::OFF_CONS) + gi;
+      __threadfence_block();
+      const uint32_t old = atomicAdd(cons, 1u);
+      if ((old % (P::GT / 32)) == (P::GT / 32) - 1 && sig >= 0) {
+        __threadfence_block();
+        sa_fence_proxy_async();
+        sa_mbar_expect_tx(&tma_bar[gi], (uint32_t)P::WORK);
+        sa_tma_load_2d(work(), tmx, (rank * P::COLS + tt * P::TC) * P::EW, (int)(sig * 256), &tma_bar[gi]);
+      }
     }
   }
   SA_HD void wait_tile() {
@@ -539,7 +559,12 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
   pp.init(smem_raw, stage, scratch);
   const int gbar = 1 + pp.gi;
   const int m1_cc = pp.gt % TC, m1_g = pp.gt / TC;
-  const int m2_g = pp.gt & 15, m2_cc = pp.gt >> 4;
+  // WX: a warp owns two columns; each half-warp holds eight g values (one parity) of both, so
+  // that its 16 lanes touch 16 distinct 8-byte bank pairs of the 128B-swizzled tile
+  constexpr bool WX = SA_K64_WX && std::is_same<T, float>::value && TC == 16;
+  const int wx_lane = threadIdx.x & 31;
+  const int m2_g = WX ? ((wx_lane >> 1) & 7) * 2 + (wx_lane >> 4) : (pp.gt & 15);
+  const int m2_cc = WX ? 2 * (pp.gt >> 5) + (wx_lane & 1) : (pp.gt >> 4);
   const C4 *twA = pp.twA;
 
   // M = 0: compute and scatter; PARK schedule (run_park): 1 compute and park, 2 fetch the parked
@@ -554,11 +579,13 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
       if constexpr (M != 2) {
       pp.wait_tile();
       C2 *wk = pp.work();
-      {  // round 1 (M1): v[k] = node 16g+k of sub-transform cc = X[rev8(16g+k)][cc]
-        const int rg = rev4(m1_g);
+      // WX: physical position of (row, column m2_cc) in the 128B-swizzled tile
+      auto wx_at = [&](int row) { return row * TC + ((((m2_cc >> 1) ^ (row & 7)) << 1) | (m2_cc & 1)); };
+      {  // round 1 (M1; WX: M2): v[k] = node 16g+k of sub-transform cc = X[rev8(16g+k)][cc]
+        const int rg = rev4(WX ? m2_g : m1_g);
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
-          V x = A::from(wk[(crev4(k) * 16 + rg) * TC + m1_cc]);
+          V x = A::from(WX ? wk[wx_at(crev4(k) * 16 + rg)] : wk[(crev4(k) * 16 + rg) * TC + m1_cc]);
           v[k] = use_gain ? A::scale(x, gain) : x;
         }
 #ifndef SA_PROBE_SKIP_A
@@ -586,6 +613,19 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
         }
 #endif
       }
+      if constexpr (WX) {
+        // the 16 threads of a column are lanes of one warp: exchange through the column's own
+        // 256 slots, entry (g, k) in row rho = ((2g + (k & 1)) << 3) | ((k >> 1) ^ (g >> 1)), so
+        // that writes (fixed k) and reads (fixed k') of a half-warp are bank-conflict free
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          wk[wx_at(((m2_g * 2 + (k & 1)) << 3) | ((k >> 1) ^ (m2_g >> 1)))] = A::to(v[k]);
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 16; ++k)  // node g + 16k = entry (k, g)
+          v[k] = A::from(wk[wx_at(((k * 2 + (m2_g & 1)) << 3) | ((m2_g >> 1) ^ (k >> 1)))]);
+      } else {
       group_sync(gbar, GT);
 #pragma unroll
       for (int k = 0; k < 16; ++k)  // exchange: node q = 16g+k, column swizzled by q & (TC-1)
@@ -594,8 +634,14 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
 #pragma unroll
       for (int k = 0; k < 16; ++k)  // round 2 (M2): node g + 16k of sub-transform cc
         v[k] = A::from(wk[(m2_g + 16 * k) * TC + (m2_cc ^ (m2_g & (TC - 1)))]);
-      group_sync(gbar, GT);  // tile buffer consumed: re-arm it
-      if (tsig >= 0) pp.tma(&tmx, tsig, pp.gi + NG * tu);
+      }
+      if constexpr (WX && SA_K64_WX == 2) {
+        __syncwarp();
+        pp.tma_last(&tmx, tsig, pp.gi + NG * tu);
+      } else {
+        group_sync(gbar, GT);  // tile buffer consumed: re-arm it
+        if (tsig >= 0) pp.tma(&tmx, tsig, pp.gi + NG * tu);
+      }
 #ifndef SA_PROBE_SKIP_A
 #pragma unroll
       for (int t = 5; t <= 8; ++t) {
@@ -972,8 +1018,10 @@ int launch64k(int variant, const void *x, void *y, int64_t batch, const SaTwiddl
   cuuint64_t strides[1] = {(cuuint64_t)(256 * sizeof(typename P::C2))};
   cuuint32_t box[2] = {(cuuint32_t)(P::TC * P::EW), 256};
   cuuint32_t estr[2] = {1, 1};
+  const bool wx = SA_K64_WX && std::is_same<T, float>::value && P::TC == 16 && variant == SA_DIT;
   CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void *>(x), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   wx ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     sa_set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
