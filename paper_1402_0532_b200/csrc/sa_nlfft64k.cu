@@ -141,8 +141,12 @@ template <typename T> struct L64 {
   static constexpr size_t OFF_TWA = OFF_WORK + NG * WORK;
   static constexpr size_t OFF_BAR = OFF_TWA + TWA;
   static constexpr size_t OFF_TMEM = OFF_BAR + 8 * (NG + 2 * NS);  // PARK: the TMEM base address
+#if SA_K64_WX == 2
   static constexpr size_t OFF_CONS = OFF_TMEM + 8;  // WX = 2: per-group count of warps that consumed the tile
   static constexpr size_t SMEM = OFF_CONS + 4 * NG;
+#else
+  static constexpr size_t SMEM = OFF_TMEM + 8;
+#endif
   // PARK: a thread parks one tile's 16 values (32 words) in its own TMEM lane; the 4 warps of a lane
   // quarter x TPG tiles take 32 columns each
   static constexpr int PARK_W = 4 * (int)sizeof(C2);  // words per thread and tile
@@ -343,7 +347,9 @@ template <typename T, bool PK = false> struct Pipe {
       pfull[r] = sa_mapa(sa_smem_u32(smem + P::OFF_BAR + 8 * P::NG), r);
     }
     for (int e = threadIdx.x; e < 255; e += P::THREADS) twA[e] = stage[e];  // global stages 1..8
+#if SA_K64_WX == 2
     if (threadIdx.x < P::NG) reinterpret_cast<uint32_t *>(smem + P::OFF_CONS)[threadIdx.x] = 0u;
+#endif
     if (threadIdx.x == 0) {
       for (int g = 0; g < P::NG; ++g) sa_mbar_init(&tma_bar[g], 1);
       for (int b = 0; b < P::NS; ++b) {
@@ -390,6 +396,7 @@ template <typename T, bool PK = false> struct Pipe {
       sa_tma_load_2d(work(), tmx, (rank * P::COLS + tt * P::TC) * P::EW, (int)(sig * 256), &tma_bar[gi]);
     }
   }
+#if SA_K64_WX == 2
   // WX = 2: every warp calls this once its lanes have read the tile (after __syncwarp); the last
   // of the group's warps re-arms the buffer and issues the next TMA -- no group barrier
   SA_HD void tma_last(const CUtensorMap *tmx, int64_t sig, int tt) const {
@@ -405,6 +412,7 @@ template <typename T, bool PK = false> struct Pipe {
       }
     }
   }
+#endif
   SA_HD void wait_tile() {
     group_wait(&tma_bar[gi], tile_it & 1);
     ++tile_it;
@@ -561,10 +569,14 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
   const int m1_cc = pp.gt % TC, m1_g = pp.gt / TC;
   // WX: a warp owns two columns; each half-warp holds eight g values (one parity) of both, so
   // that its 16 lanes touch 16 distinct 8-byte bank pairs of the 128B-swizzled tile
-  constexpr bool WX = SA_K64_WX && std::is_same<T, float>::value && TC == 16;
+#if SA_K64_WX
+  constexpr bool WX = std::is_same<T, float>::value && TC == 16;
   const int wx_lane = threadIdx.x & 31;
   const int m2_g = WX ? ((wx_lane >> 1) & 7) * 2 + (wx_lane >> 4) : (pp.gt & 15);
   const int m2_cc = WX ? 2 * (pp.gt >> 5) + (wx_lane & 1) : (pp.gt >> 4);
+#else
+  const int m2_g = pp.gt & 15, m2_cc = pp.gt >> 4;
+#endif
   const C4 *twA = pp.twA;
 
   // M = 0: compute and scatter; PARK schedule (run_park): 1 compute and park, 2 fetch the parked
@@ -579,13 +591,23 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
       if constexpr (M != 2) {
       pp.wait_tile();
       C2 *wk = pp.work();
+#if SA_K64_WX
       // WX: physical position of (row, column m2_cc) in the 128B-swizzled tile
       auto wx_at = [&](int row) { return row * TC + ((((m2_cc >> 1) ^ (row & 7)) << 1) | (m2_cc & 1)); };
+#endif
       {  // round 1 (M1; WX: M2): v[k] = node 16g+k of sub-transform cc = X[rev8(16g+k)][cc]
+#if SA_K64_WX
         const int rg = rev4(WX ? m2_g : m1_g);
+#else
+        const int rg = rev4(m1_g);
+#endif
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
+#if SA_K64_WX
           V x = A::from(WX ? wk[wx_at(crev4(k) * 16 + rg)] : wk[(crev4(k) * 16 + rg) * TC + m1_cc]);
+#else
+          V x = A::from(wk[(crev4(k) * 16 + rg) * TC + m1_cc]);
+#endif
           v[k] = use_gain ? A::scale(x, gain) : x;
         }
 #ifndef SA_PROBE_SKIP_A
@@ -613,6 +635,7 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
         }
 #endif
       }
+#if SA_K64_WX
       if constexpr (WX) {
         // the 16 threads of a column are lanes of one warp: exchange through the column's own
         // 256 slots, entry (g, k) in row rho = ((2g + (k & 1)) << 3) | ((k >> 1) ^ (g >> 1)), so
@@ -625,7 +648,9 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
 #pragma unroll
         for (int k = 0; k < 16; ++k)  // node g + 16k = entry (k, g)
           v[k] = A::from(wk[wx_at(((k * 2 + (m2_g & 1)) << 3) | ((m2_g >> 1) ^ (k >> 1)))]);
-      } else {
+      } else
+#endif
+      {
       group_sync(gbar, GT);
 #pragma unroll
       for (int k = 0; k < 16; ++k)  // exchange: node q = 16g+k, column swizzled by q & (TC-1)
@@ -635,10 +660,13 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
       for (int k = 0; k < 16; ++k)  // round 2 (M2): node g + 16k of sub-transform cc
         v[k] = A::from(wk[(m2_g + 16 * k) * TC + (m2_cc ^ (m2_g & (TC - 1)))]);
       }
-      if constexpr (WX && SA_K64_WX == 2) {
+#if SA_K64_WX == 2
+      if constexpr (WX) {
         __syncwarp();
         pp.tma_last(&tmx, tsig, pp.gi + NG * tu);
-      } else {
+      } else
+#endif
+      {
         group_sync(gbar, GT);  // tile buffer consumed: re-arm it
         if (tsig >= 0) pp.tma(&tmx, tsig, pp.gi + NG * tu);
       }
