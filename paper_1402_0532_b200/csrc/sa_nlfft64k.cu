@@ -1056,11 +1056,17 @@ int launch64k(int variant, const void *x, void *y, int64_t batch, const SaTwiddl
     return SA_ERR_CUDA;
   }
   auto kern = variant == SA_DIT ? k_nlfft64k_dit<T> : k_nlfft64k_dif<T>;
-  SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM));
-  if (P::CL > 8) SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  // per device and variant, once: function attributes and the resident cluster count
+  static int cached_clusters[2][64] = {};
   int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  SA_CUDA_TRY(cudaGetDevice(&dev));
+  const int vi = variant == SA_DIT ? 0 : 1;
+  const bool cached = dev < 64 && cached_clusters[vi][dev] > 0;
+  if (!cached) {
+    SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM));
+    if (P::CL > 8) SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1072,10 +1078,15 @@ int launch64k(int variant, const void *x, void *y, int64_t batch, const SaTwiddl
   cfg.stream = s;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  int max_clusters = 0;
-  cfg.gridDim = dim3(P::CL * (sms / P::CL));
-  if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1)
-    max_clusters = sms / P::CL;
+  int max_clusters = cached ? cached_clusters[vi][dev] : 0;
+  if (!cached) {
+    cfg.gridDim = dim3(P::CL * (sms / P::CL));
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1) {
+      cudaGetLastError();
+      max_clusters = sms / P::CL;
+    }
+    if (dev < 64) cached_clusters[vi][dev] = max_clusters;
+  }
   int64_t ncl = std::min<int64_t>(batch, max_clusters);
   cfg.gridDim = dim3((unsigned)(ncl * P::CL));
   typename P::C2 *scratch = nullptr;  // L2S: one signal's node storage per cluster (L2-resident)
