@@ -63,6 +63,9 @@ constexpr int NN = 1 << LOGN;
 #ifndef SA_K64_PARK_LOOP
 #define SA_K64_PARK_LOOP 0  // c64: 1 = compact one-call-site form of the PARK signal loop (1.829 vs 1.676 ms DIT)
 #endif
+#ifndef SA_K64_PARK_S2
+#define SA_K64_PARK_S2 0  // c64 DIT straight-line form: the B-tile / A-tile interleaved order (experiment)
+#endif
 #ifndef SA_K64_PARK_DIF
 #define SA_K64_PARK_DIF 0  // the same for DIF (measured slower: 1.98 vs 1.79 ms)
 #endif
@@ -188,7 +191,13 @@ SA_HD void load_wf(typename Ar<T>::C2 (&wf)[30], const typename Ar<T>::C2 *__res
 template <typename T> SA_HD typename Ar<T>::C4 c4of(const typename Ar<T>::C2 &w) {
   return {fabs(w.x), fabs(w.y), sa_sgn(w.x), sa_sgn(w.y)};
 }
+#if defined(SA_PROBE_NOGEN)  // timing probe only (wrong results in columns 0 and 128): no general-product tiles
+SA_HD bool special_column(int) { return false; }
+#elif defined(SA_PROBE_ALLGEN)  // timing probe: every tile takes the general product
+SA_HD bool special_column(int) { return true; }
+#else
 SA_HD bool special_column(int q) { return __any_sync(0xffffffffu, q == 0 || q == 128); }
+#endif
 
 // TMEM parking (SA_K64_PARK): 32 words of the executing thread's own lane, 32x32b shape
 SA_HD void tm_st32(uint32_t taddr, const uint32_t (&r)[32]) {
@@ -504,6 +513,29 @@ template <typename T, bool PK = false> struct Pipe {
       local_done(0);
       if (cid + ncl < batch) tileA(M1{}, cid + ncl, 1, 0, 0u, false, cid + ncl, 0);
     }
+#if SA_K64_PARK_S2
+    // variant: B tile 0 | A(s+1, tile 0) -> park | B tile 1 | release, wait empty, scatter both parked
+    // tiles | A(s+2, tile 1) -> park | wait full: both TMA loads get a long lead
+    {
+      uint32_t it2 = 0;
+      for (int64_t sig = cid; sig < batch; sig += ncl, ++it2) {
+        const int64_t n1 = sig + ncl, n2 = n1 + ncl;
+        phaseB(sig, 0, it2, 0, 1);
+        if (n1 < batch) tileA(M1{}, n1, 0, 0, 0u, false, sig_or_none(n2), 1);
+        phaseB(sig, 0, it2, 1, 2);
+        if (n1 < batch) {
+          if (threadIdx.x == 0) sa_mbar_expect_tx(&full_bar[0], tx);
+          release(0);
+          tileA(M2{}, n1, 0, 0, it2 + 1, true, (int64_t)-1, 0);
+          tileA(M2{}, n1, 1, 0, it2 + 1, false, (int64_t)-1, 0);
+          local_done(0);
+          if (n2 < batch) tileA(M1{}, n2, 1, 0, 0u, false, n2, 0);
+        }
+      }
+      finish();
+      return;
+    }
+#endif
     uint32_t it = 0;
     for (int64_t sig = cid; sig < batch; sig += ncl, ++it) {
       const int64_t n1 = sig + ncl, n2 = n1 + ncl;
@@ -726,23 +758,24 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
     pp.local_done(b);
   };
 
-  auto phaseB_s = [&](auto S_, int64_t sig, int b, uint32_t use) {
+  // tiles [u0, u1) of the group; the storage wait comes with tile 0
+  auto phaseB_s = [&](auto S_, int64_t sig, int b, uint32_t use, int u0, int u1) {
     constexpr bool S = decltype(S_)::value;  // storage in the L2 scratch
     C2 *inter = pp.share(b);
     C2 *ysig = y + sig * NN;
     C2 wf[30];
     {
-      const int q0 = pp.rank * COLS + pp.gi * TC + m1_cc;  // independent of the node storage
+      const int q0 = pp.rank * COLS + (pp.gi + NG * u0) * TC + m1_cc;  // independent of the node storage
       load_wf<T>(wf, stage2, q0, m1_g);
     }
-    pp.wait_full(b, use & 1);  // all INTER1 bytes of this signal landed
-    for (int u = 0; u < TPG; ++u) {
+    if (u0 == 0) pp.wait_full(b, use & 1);  // all INTER1 bytes of this signal landed
+    for (int u = u0; u < u1; ++u) {
       const int tt = pp.gi + NG * u;
       const int lq = tt * TC + m1_cc;
       const int q = pp.rank * COLS + lq;
       const bool gen = special_column(q);
 #ifndef SA_PROBE_NOTWLD
-      if (u > 0) load_wf<T>(wf, stage2, q, m1_g);
+      if (u > u0) load_wf<T>(wf, stage2, q, m1_g);
 #endif
       V v[16];
 #pragma unroll
@@ -795,14 +828,14 @@ __global__ void __launch_bounds__(L64<T>::THREADS, K64<T>::MINB)
     }
   };
 
-  auto phaseB = [&](int64_t sig, int b, uint32_t use) {
+  auto phaseB = [&](int64_t sig, int b, uint32_t use, int u0 = 0, int u1 = P::TPG) {
     if constexpr (P::L2S) {
       if (Pipe<T>::in_l2(b)) {
-        phaseB_s(std::true_type{}, sig, b, use);
+        phaseB_s(std::true_type{}, sig, b, use, u0, u1);
         return;
       }
     }
-    phaseB_s(std::false_type{}, sig, b, use);
+    phaseB_s(std::false_type{}, sig, b, use, u0, u1);
   };
 
   if constexpr (P::PARK) {
