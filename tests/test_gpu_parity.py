@@ -350,6 +350,40 @@ def test_nfft64k_batch_edges(sa, variant, dt):
         assert_value_equal(y, ref[:b])
 
 
+def test_nfft64k_concurrent_streams_and_tmem(sa):
+    """The fused 2^16 kernels allocate TMEM (parking schedule). Calls on several
+    streams at once -- complex64 DIT, complex128 DIF and an int8 tensor-core NDFT,
+    which takes all 512 TMEM columns of an SM -- must give exactly the results of
+    the same calls made one after the other, repeatedly (allocation and release
+    of TMEM between co-scheduled kernels, no cross-call state)."""
+    import torch
+    g = np.random.default_rng(166)
+    x64 = dev((g.standard_normal((70, 1 << 16)) + 1j * g.standard_normal((70, 1 << 16))).astype(np.complex64))
+    x128 = dev(g.standard_normal((40, 1 << 16)) + 1j * g.standard_normal((40, 1 << 16)))
+    xn = dev((g.standard_normal((3000, 1024)) + 1j * g.standard_normal((3000, 1024))).astype(np.complex64))
+    calls = [lambda o: sa.nfft_batch(x64, out=o, variant="dit"),
+             lambda o: sa.nfft_batch(x128, out=o, variant="dif"),
+             lambda o: sa.ndft_batch(xn, out=o, mode="tc8")]
+    ins = [x64, x128, xn]
+    ref = [torch.empty_like(x) for x in ins]
+    for c, r in zip(calls, ref):
+        c(r)
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in calls]
+    outs = [torch.empty_like(x) for x in ins]
+    for _ in range(5):
+        for o in outs:
+            o.zero_()
+        for c, o, st in zip(calls, outs, streams):
+            st.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(st):
+                c(o)
+                c(o)
+        torch.cuda.synchronize()
+        for o, r in zip(outs, ref):
+            assert torch.equal(o.view(torch.uint8), r.view(torch.uint8))
+
+
 def test_map_c5_sampled_rows(sa):
     """C5 (2^22 samples, 8 targets), 4096 delay bins x 2048 Doppler bins, c64 on
     the GPU; the fp64 oracle of the same complex64 inputs on the target rows and
