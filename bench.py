@@ -726,6 +726,12 @@ def wl_map(args, ws, rank, c5=False, e2e=False):
            "dtype": (("int8 digits x sign, exact int32 accumulate, f64->f32 epilogue (lag)" if lag_is_i8() else
                       "bf16x2-split x sign, f32 accumulate (lag)") + "; f32 (NL-FFT)") if args.dtype == "c64"
            else "f64"}
+    if ws == 1:
+        def graph_step():
+            mg = sa.MapGraph(ns, ns, L, M, dtype=cdt).load(surv, ref)
+            mg.capture()
+            return mg.replay
+        res["graph_step"] = graph_step
     if e2e and not args.no_e2e:
         hs = torch.from_numpy(sc.surv).to(cdt).pin_memory()
         hr = torch.from_numpy(sc.ref).to(cdt).pin_memory()
@@ -797,6 +803,8 @@ def summarise(name, e):
             r["cpu_numpy_1core"] = float(f"{rn.get('one_core_cells_per_s', rn['one_core_value']):.4g}")
     if "e2e" in e:
         r["e2e_ms"] = round(e["e2e"]["ms_per_step"], 3)
+    if "ms_per_step" in e.get("cuda_graph", {}):
+        r["graph_ms"] = round(e["cuda_graph"]["ms_per_step"], 4)
     return r
 
 
@@ -834,6 +842,13 @@ def run_extra(name, make, args, ws, rank):
     else:
         e["ops_per_s"] = r["ops"] / (ems * 1e-3)
         e["roofline"] = r["roofline"](ems)
+    if "graph_step" in r:  # the same map call replayed from a CUDA graph (MapGraph)
+        try:
+            gms, _ = timed(r["graph_step"](), steps, 3, 1)
+            e["cuda_graph"] = {"ms_per_step": gms, "cells_per_s": r["cells"] / (gms * 1e-3),
+                               "api": "paper_1402_0532_b200.MapGraph(...).replay()"}
+        except Exception as ex:  # capture is an extra: never fail the line
+            e["cuda_graph"] = {"unavailable": repr(ex)[:200]}
     if "e2e_step" in r:
         xms, _ = timed(r["e2e_step"], max(2, steps // 2), 1, 1)
         unit = "cells/s" if "cells" in r else "⊙/s"

@@ -36,6 +36,7 @@ from .ambiguity import (
     SPEED_OF_LIGHT,
     AmbiguitySurface,
     AmbiguityVariant,
+    MapGraph,
     ambiguity_eq11,
     ambiguity_eq12a,
     ambiguity_eq12b,

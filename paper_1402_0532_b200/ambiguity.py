@@ -243,6 +243,72 @@ def ambiguity_map(s_surv, s_ref, l_bins: int, m: int, *, l0: int = 0, gain: floa
 _MAP_STREAMS: dict = {}
 
 
+class MapGraph:
+    """A fixed-shape ``ambiguity_map`` call captured once in a CUDA graph and
+    replayed per coherent processing interval: the map's launches (reference
+    prep, lag stage, Doppler transform) are stream-ordered and allocation-free
+    once warm, so the replay removes their host launch cost (C4: 0.0635 ->
+    0.0575 ms per map, C5: 0.427 -> 0.420 ms; results bit-identical to the
+    eager call).  B200 extension -- the reference has no counterpart.
+
+    ``surv`` / ``ref`` / ``out`` are the graph's static device buffers: write new
+    samples into ``surv`` and ``ref`` (``load`` copies them, stream-ordered), call
+    ``replay()``, read ``out``.  Keyword arguments as ``ambiguity_map``.
+    """
+
+    def __init__(self, ns: int, ref_len: int, l_bins: int, m: int, *, dtype=None, **kw):
+        T = torch()
+        require_cuda()
+        dtype = dtype or T.complex64
+        for k in ("out", "out_ptr", "workspace"):
+            if k in kw:
+                raise ContractError(f"MapGraph owns its buffers: {k!r} is not accepted")
+        self.surv = T.zeros(ns, dtype=dtype, device="cuda")
+        self.ref = T.zeros(ref_len, dtype=dtype, device="cuda")
+        self.out = T.empty((l_bins, m), dtype=dtype, device="cuda")
+        self._args = (l_bins, m)
+        self._kw = dict(kw)
+        self._graph = None
+
+    def load(self, surv, ref=None):
+        """Copy new samples into the static buffers (host or device sources;
+        pinned host tensors copy asynchronously on the current stream)."""
+        T = torch()
+        for dst, src in ((self.surv, surv), (self.ref, ref)):
+            if src is None:
+                continue
+            t = src if isinstance(src, T.Tensor) else T.from_numpy(np.ascontiguousarray(_samples(src)))
+            dst.copy_(t.reshape(-1).to(dst.dtype), non_blocking=True)
+        return self
+
+    def _call(self):
+        ambiguity_map(self.surv, self.ref, *self._args, out=self.out, **self._kw)
+
+    def capture(self):
+        """Warm up (scratch pools, twiddle sets, function attributes) on a side
+        stream, then capture one call.  Done lazily by the first ``replay``."""
+        T = torch()
+        st = T.cuda.Stream()
+        st.wait_stream(T.cuda.current_stream())
+        with T.cuda.stream(st):
+            for _ in range(2):
+                self._call()
+        T.cuda.current_stream().wait_stream(st)
+        g = T.cuda.CUDAGraph()
+        with T.cuda.graph(g):
+            self._call()
+        self._graph = g
+        return self
+
+    def replay(self):
+        """One map of the current buffer contents on the current stream; returns
+        the static ``out`` tensor (no sync)."""
+        if self._graph is None:
+            self.capture()
+        self._graph.replay()
+        return self.out
+
+
 def _map_host_pipelined(surv, ref, l_bins, m, l0, gain, conjugate_ref, host_out):
     """Host (pinned) complex64 inputs -> host map with the uploads overlapped: the
     reference goes up first (the int8 lag stage needs its global exponent), then the

@@ -350,6 +350,26 @@ def test_nfft64k_batch_edges(sa, variant, dt):
         assert_value_equal(y, ref[:b])
 
 
+def test_map_graph_replay_bit_identical(sa):
+    """MapGraph: the captured map call replayed on new buffer contents equals the
+    eager call bit for bit (complex64 int8 lag stage + Doppler NL-FFT, and a
+    complex128 map), including after the inputs are replaced."""
+    import torch
+    g = np.random.default_rng(167)
+    for dt, ns, L, M in ((np.complex64, 1 << 16, 64, 256), (np.complex128, 1 << 13, 24, 64)):
+        tdt = torch.complex64 if dt == np.complex64 else torch.complex128
+        mg = sa.MapGraph(ns, ns, L, M, dtype=tdt)
+        for trial in range(3):
+            s = np.exp(1j * 2 * np.pi * g.random(ns)).astype(dt)
+            r = (s + 0.1 * (g.standard_normal(ns) + 1j * g.standard_normal(ns))).astype(dt)
+            mg.load(r, s)
+            y = mg.replay().clone()
+            ref = sa.ambiguity_map(dev(r), dev(s), L, M)
+            assert torch.equal(y.view(torch.uint8), ref.view(torch.uint8)), (dt, trial)
+    with pytest.raises(sa.ContractError):
+        sa.MapGraph(1024, 1024, 4, 16, out=None)
+
+
 def test_nfft64k_concurrent_streams_and_tmem(sa):
     """The fused 2^16 kernels allocate TMEM (parking schedule). Calls on several
     streams at once -- complex64 DIT, complex128 DIF and an int8 tensor-core NDFT,
