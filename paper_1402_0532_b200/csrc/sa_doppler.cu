@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   using C2 = typename D::C2;
   using C4 = typename D::C4;
   constexpr int M = D::M, R = D::R;
+  sa_pdl_wait();  // launched with programmatic serialization: the lag kernel's z is complete from here on
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C2 *sm = reinterpret_cast<C2 *>(smem_raw);
   C4 *tws = reinterpret_cast<C4 *>(smem_raw + D::SM_DATA);
@@ -154,9 +155,9 @@ int launch_dop(const void *z, void *out, int row_off, int64_t l_count, int block
   }
   const int64_t rows = row_off + l_count;
   const int64_t grid = (rows + D::R - 1) / D::R;
-  k_doppler<T, LOGM><<<(unsigned)grid, THREADS, D::SMEM, s>>>(
-      (const typename D::C2 *)z, (typename D::C2 *)out, row_off, l_count, blocked,
-      (const typename D::C4 *)tw->stage, (T)gain, (int)(gain != 1.0));
+  SA_CUDA_TRY(sa_launch_pdl(k_doppler<T, LOGM>, dim3((unsigned)grid), dim3(THREADS), (size_t)D::SMEM, s,
+                            (const typename D::C2 *)z, (typename D::C2 *)out, (int)row_off, (int64_t)l_count,
+                            (int)blocked, (const typename D::C4 *)tw->stage, (T)gain, (int)(gain != 1.0)));
   SA_LAUNCH_CHECK();
   return SA_OK;
 }

@@ -122,3 +122,38 @@ int sa_launch_lag_product(int dtype, int lag_kind, const void *surv, const void 
 int sa_launch_lag_integrate(int dtype, int lag_kind, const void *surv, const void *ref, int64_t ns,
                             int64_t ref_len, int64_t l0, int64_t l_count, int64_t m, int conj,
                             int mode, void *z, cudaStream_t s);
+
+// Launch with programmatic stream serialization (PDL): the kernel's CTAs may become
+// resident while the previous kernel in the stream drains, if that kernel executed
+// griddepcontrol.launch_dependents; the launched kernel must execute
+// griddepcontrol.wait before touching anything its predecessor wrote (sa_pdl_wait()).
+// SA_MAP_PDL=0 in the environment launches normally.
+#ifdef __CUDACC__
+#include <cstdlib>
+#include <utility>
+inline bool sa_pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char *e = getenv("SA_MAP_PDL");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t sa_launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                 Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = sa_pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+__device__ __forceinline__ void sa_pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void sa_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#endif

@@ -199,6 +199,7 @@ struct LagDst {
 // lag kernel reduce the partials.
 __global__ void __launch_bounds__(256) k_lag_absmax(const float2 *__restrict__ ref, int64_t ref_len,
                                                     float *__restrict__ part) {
+  sa_pdl_trigger();  // the prep launch may become resident while this one drains
   __shared__ float red[8];
   float mx = 0.f;
   const int64_t n4 = (uintptr_t)ref & 15 ? 0 : ref_len / 4;  // 16-B aligned: float4 pairs
@@ -288,6 +289,8 @@ __global__ void __launch_bounds__(256) k_lag_cprep(const float2 *__restrict__ re
                                                    const float2 *__restrict__ surv, int64_t q0, int tb, int psl,
                                                    unsigned char *__restrict__ splanes, int *__restrict__ es_out,
                                                    float *__restrict__ mc_out) {
+  sa_pdl_trigger();
+  sa_pdl_wait();  // the |ref| partials of k_lag_absmax
   if (blockIdx.x >= ncb) {  // trailing blocks: one per surveillance block
     sprep_block(blockIdx.x - ncb, surv, q0, tb, psl, splanes, es_out, part, npart, mc_out);
     return;
@@ -363,6 +366,8 @@ __global__ void __launch_bounds__(NWARPS * 32, 2)
     k_lag_i8(const unsigned char *__restrict__ splanes, const int *__restrict__ es_in, const float *__restrict__ mc_in,
              int64_t l0g, int64_t l_count, int64_t m, int tb, const unsigned char *__restrict__ cplanes, int64_t guard,
              int64_t cpl, float2 *__restrict__ z, int64_t q0, LagDst dst) {
+  sa_pdl_trigger();  // the Doppler launch may become resident while the last wave drains
+  sa_pdl_wait();     // the planes, exponents and scales of k_lag_cprep
   extern __shared__ unsigned char smem_raw[];
   unsigned char *smem = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const Geo gm = geo(tb, MR, 2);
@@ -605,8 +610,9 @@ int launch_i8(const unsigned char *splanes, const int *es, const float *mc, int6
     SA_CUDA_TRY(cudaFuncSetAttribute(k_lag_i8<MR, BLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     if (dev < 64) smem_set[dev] = bytes;
   }
-  k_lag_i8<MR, BLK><<<(unsigned)q_count, NWARPS * 32, bytes, s>>>(splanes, es, mc, l0, l_count, m, (int)tb, cplanes,
-                                                                  guard, cpl, (float2 *)z, q0, d);
+  SA_CUDA_TRY(sa_launch_pdl(k_lag_i8<MR, BLK>, dim3((unsigned)q_count), dim3(NWARPS * 32), (size_t)bytes, s,
+                            (const unsigned char *)splanes, (const int *)es, (const float *)mc, l0, l_count, m, (int)tb,
+                            (const unsigned char *)cplanes, guard, cpl, (float2 *)z, q0, d));
   SA_LAUNCH_CHECK();
   return SA_OK;
 }
@@ -672,9 +678,9 @@ int sa_launch_lag_i8_blocks(const void *surv, const void *ref, int64_t ref_len, 
   k_lag_absmax<<<npart, 256, 0, s>>>((const float2 *)ref, ref_len, cpart);
   SA_LAUNCH_CHECK();
   const int64_t nb = std::min<int64_t>((cpl / 16 + 255) / 256, 8 * sms);
-  k_lag_cprep<<<(unsigned)(nb + q_count), 256, 0, s>>>((const float2 *)ref, ref_len, conj ? -1.f : 1.f, cpart, npart,
-                                                       guard, cpl, cplanes, (unsigned)nb, (const float2 *)surv, q0,
-                                                       (int)tb, gm.psl, splanes, es, mc);
+  SA_CUDA_TRY(sa_launch_pdl(k_lag_cprep, dim3((unsigned)(nb + q_count)), dim3(256), (size_t)0, s, (const float2 *)ref,
+                            ref_len, conj ? -1.f : 1.f, (const float *)cpart, npart, guard, cpl, cplanes, (unsigned)nb,
+                            (const float2 *)surv, q0, (int)tb, gm.psl, splanes, es, mc));
   SA_LAUNCH_CHECK();
   int rc;
   if (mr == 64)
