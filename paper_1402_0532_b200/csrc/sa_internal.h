@@ -127,7 +127,11 @@ int sa_launch_lag_integrate(int dtype, int lag_kind, const void *surv, const voi
 // resident while the previous kernel in the stream drains, if that kernel executed
 // griddepcontrol.launch_dependents; the launched kernel must execute
 // griddepcontrol.wait before touching anything its predecessor wrote (sa_pdl_wait()).
-// SA_MAP_PDL=0 in the environment launches normally.
+// Off by default (SA_MAP_PDL=1 in the environment enables it): one full GPU test run with it
+// showed a stale scale read in the lag kernel (test_lag_i8_nonfinite, not reproducible alone) --
+// L1 / read-only-cache lines of a recycled scratch address are not known to be invalidated for a
+// programmatically launched grid, and the kernels of the chain read their predecessors' outputs
+// with cached loads.  The griddepcontrol instructions are no-ops for normal launches.
 #ifdef __CUDACC__
 #include <cstdlib>
 #include <utility>
@@ -135,7 +139,7 @@ inline bool sa_pdl_enabled() {
   static int on = -1;
   if (on < 0) {
     const char *e = getenv("SA_MAP_PDL");
-    on = (e && e[0] == '0') ? 0 : 1;
+    on = (e && e[0] == '1') ? 1 : 0;
   }
   return on == 1;
 }
