@@ -131,7 +131,9 @@ int sa_launch_lag_integrate(int dtype, int lag_kind, const void *surv, const voi
 // showed a stale scale read in the lag kernel (test_lag_i8_nonfinite, not reproducible alone) --
 // L1 / read-only-cache lines of a recycled scratch address are not known to be invalidated for a
 // programmatically launched grid, and the kernels of the chain read their predecessors' outputs
-// with cached loads.  The griddepcontrol instructions are no-ops for normal launches.
+// with cached loads (with ld.global.cg loads four full runs passed, at ~1% cost on the C5 map:
+// DESIGN 5.3e).  Experimental: not safe as built.  The griddepcontrol instructions are no-ops
+// for normal launches.
 #ifdef __CUDACC__
 #include <cstdlib>
 #include <utility>
